@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""bench.py — AttnCache hot-path benchmark (BASELINE.json metric: cached-attention prefill
+tokens/sec and speedup vs full attention; search QPS).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama32_1b] [--impl ours|reference]
+
+A step is one pass of the whole hot path over one query batch of the
+config: search (Alg. 1 l.255-257) -> O = A.V for hits (Alg. 2 l.373-375) -> causal
+softmax attention for misses (Alg. 2 l.376-381).  Default workload: BASELINE.json configs[1]
+(Llama-3.2-1B-shaped, fits one B200).  Inputs are seeded synthetic (synth/) and resident in
+HBM; per-step footprint (~5 GB of maps/V/O) exceeds the 126 MB L2, so no flush is needed.
+Prints ONE JSON line on rank 0.
+
+--impl reference times the CPU oracle (oracle/, the only reference this paper-only tier
+has) on a bounded sample of the same workload and extrapolates to a full step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "cached-attention prefill tokens/sec"
+PAPER_CONTEXT = ("paper (PAPER.md:51, :446, :568; Table 3): 3x attention / 1.6x end-to-end GPU speedup on one "
+                 "A100 80GB, Llama-3-3B fp32, MMLU-STEM; 2x / 1.2x on 2x Xeon Silver 4410Y")
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            m = json.load(f)
+        return {"hbm_gbs": m["hbm_gbs"], "bf16_tflops": m["bf16_tflops"],
+                "bf16_tflops_sustained": m.get("bf16_tflops_sustained", m["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+def tri(S):
+    return S * (S + 1) // 2
+
+
+def apply_bytes_per_hit(cfg):
+    """Algorithmic HBM bytes of O = A.V for one hit (all L layers, H heads): lower-triangle map
+    + V + O."""
+    e_m = torch.tensor([], dtype=synth.torch_dtype(cfg.map_dtype)).element_size()
+    e_v = torch.tensor([], dtype=synth.torch_dtype(cfg.act_dtype)).element_size()
+    return cfg.L * cfg.H * (tri(cfg.S) * e_m + 2 * cfg.S * cfg.d * e_v)
+
+
+def attend_bytes_per_miss(cfg):
+    e_v = torch.tensor([], dtype=synth.torch_dtype(cfg.act_dtype)).element_size()
+    return 4 * cfg.L * cfg.H * cfg.S * cfg.d * e_v
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md clocks line)
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg and --impl reference)
+# ------------------------------------------------------------------------------------------------
+def oracle_step_sample(cfg, n_search=64, n_apply=768, n_attend=192, seed=0):
+    """Times the CPU oracle on a bounded sample of one step of `cfg` and extrapolates.
+
+    Returns (seconds per full step (extrapolated), description, threads)."""
+    import numpy as np
+
+    import oracle
+    from tests._util import storage
+    dev = "cpu"
+    n_hit = cfg.n_hit
+    n_miss = cfg.B - n_hit
+    x = synth.features(cfg, 0, cfg.N, dev)
+    q, _, _ = synth.queries(cfg, dev)
+    rng = np.random.default_rng(seed)
+    xs, qs = storage(x), storage(q)
+    t0 = time.perf_counter()
+    oracle.search(qs[:n_search], xs, cfg.feat_dtype, cfg.tau)
+    t_search = (time.perf_counter() - t0) * cfg.B / n_search
+    # one entry's maps and one query's V/Q/K provide the sampled (layer, head) units
+    maps = storage(synth.maps(cfg, int(rng.integers(cfg.N)), 1, dev))
+    V = storage(synth.activations(cfg, "v", 0, 1, device=dev))
+    Q = storage(synth.activations(cfg, "q", 0, 1, device=dev))
+    K = storage(synth.activations(cfg, "k", 0, 1, device=dev))
+    units = cfg.L * cfg.H
+    ua = rng.integers(0, units, n_apply)
+    t0 = time.perf_counter()
+    oracle.apply(maps, cfg.map_dtype, ua * cfg.S * cfg.S, V, cfg.act_dtype, ua * cfg.S * cfg.d, cfg.S, cfg.d)
+    t_apply = (time.perf_counter() - t0) * (n_hit * units) / n_apply
+    um = rng.integers(0, units, n_attend)
+    t0 = time.perf_counter()
+    oracle.attend(Q, K, V, cfg.act_dtype, um * cfg.S * cfg.d, cfg.S, cfg.d)
+    t_attend = (time.perf_counter() - t0) * (n_miss * units) / n_attend
+    desc = (f"extrapolated from {n_search} of {cfg.B} queries' search, {n_apply} of {n_hit * units} hit "
+            f"(layer,head) A.V units, {n_attend} of {n_miss * units} miss attention units")
+    return t_search + t_apply + t_attend, desc, oracle.get_threads()
+
+
+def run_reference(args, cfg):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.set_threads(os.cpu_count() or 1)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t, desc, cores = oracle_step_sample(cfg, seed=i)
+        if i >= args.warmup:
+            times.append(t)
+    t = statistics.median(times)
+    value = cfg.B * cfg.S / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "bj_config_index": cfg.bj_index, "B": cfg.B, "S": cfg.S},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------------
+def run_ours(args, cfg):
+    rank, world, local = _env_rank()
+    if world > 1:
+        from paper_2510_25979_b200 import dist_bench
+        return dist_bench.run(args, cfg)
+    import paper_2510_25979_b200 as ac
+    from paper_2510_25979_b200.pipeline import PrefillStep
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = ac.Context(local)
+    peaks = _peaks()
+
+    # ---- inputs resident in HBM (untimed) ----
+    x = synth.features(cfg, 0, cfg.N, dev)
+    maps = torch.empty(cfg.N, cfg.L, cfg.H, cfg.S, cfg.S, dtype=synth.torch_dtype(cfg.map_dtype), device=dev)
+    synth.fill_maps(cfg, maps, 0)
+    db = ac.Database(ctx, x, maps)
+    q, _, _ = synth.queries(cfg, dev)
+    Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=dev) for k in "qkv")
+    O = torch.empty_like(V)
+    step = PrefillStep(ctx, db, cfg.tau)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        step(q, Q, K, V, O)
+    ctx.sync()
+    idx, score, hit = step.search(q)
+    n_hit = int(hit.sum().item())
+
+    # ---- timed region: K whole steps, per-stage events on the launch stream ----
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    torch.cuda.synchronize()
+    launches0 = ac.attncache_launch_count()
+    clocks.start()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(args.steps):
+        e = ev[k]
+        e[0].record(stream)
+        idx, score, hit = step.search(q)
+        e[1].record(stream)
+        ac.attncache_apply_cached(db, idx, V, O, hit=hit)
+        e[2].record(stream)
+        ac.attncache_attend_full(ctx, Q, K, V, O, skip=hit)
+        e[3].record(stream)
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = ac.attncache_launch_count() - launches0
+    ctx.sync()
+    total_ms = start.elapsed_time(end)
+    ms = total_ms / args.steps
+    search_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    apply_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    attend_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in ev)
+
+    # ---- comparison: full attention on every row (the paper's "full model" baseline) ----
+    O_full = torch.empty_like(V)
+    hit_rows_only = (1 - hit).contiguous()
+    for _ in range(2):
+        ac.attncache_attend_full(ctx, Q, K, V, O_full)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(args.steps):
+        ac.attncache_attend_full(ctx, Q, K, V, O_full)
+    s1.record(stream)
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record(stream)
+    for _ in range(args.steps):
+        ac.attncache_attend_full(ctx, Q, K, V, O_full, skip=hit_rows_only)
+    h1.record(stream)
+    torch.cuda.synchronize()
+    full_ms = s0.elapsed_time(s1) / args.steps
+    full_hits_ms = h0.elapsed_time(h1) / args.steps
+
+    # ---- e2e: the same step through the public API from pinned host buffers ----
+    e2e = run_e2e(args, cfg, ctx, db, step, q, Q, K, V, dev, stream)
+
+    # ---- roofline of the dominant kernel (apply_cached) ----
+    bytes_alg = n_hit * apply_bytes_per_hit(cfg)
+    achieved = bytes_alg / (apply_ms * 1e-3) / 1e9
+    traffic = _ncu_traffic(cfg.name, "apply")
+    roofline = {"kernel": f"attncache apply_cached ({ac.attncache_variant('apply', V.dtype, cfg.S, cfg.d)})",
+                "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "peak_source": f"{peaks['source']} MEASURED_PEAKS.json hbm_gbs",
+                "algorithmic_bytes_per_launch": bytes_alg, "avg_launch_ms": apply_ms,
+                "note": "launch time measured with CUDA events around the apply_cached call (row-select + A.V "
+                        "kernels) on the launch stream inside the timed region"}
+    attend_alg = (cfg.B - n_hit) * attend_bytes_per_miss(cfg)
+    secondary = {
+        "search": {"ms": search_ms, "qps": cfg.B / (search_ms * 1e-3),
+                   "variant": ac.attncache_variant("search", q.dtype, 0, cfg.D)},
+        "attend_full_misses": {"ms": attend_ms, "hbm_frac": attend_alg / (attend_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                               "variant": ac.attncache_variant("attend", V.dtype, cfg.S, cfg.d)},
+    }
+
+    line = {"metric": METRIC, "value": cfg.B * cfg.S / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg.act_dtype, "data": "synthetic (synth/, seed 0)",
+            "config": {"workload": cfg.name, "bj_config_index": cfg.bj_index, "N": cfg.N, "D": cfg.D, "L": cfg.L,
+                       "H": cfg.H, "S": cfg.S, "d": cfg.d, "B": cfg.B, "hits": n_hit, "tau": cfg.tau,
+                       "parallelism": "single GPU", "l2": "inputs exceed L2 (no flush)"},
+            "speedup_vs_full_attention": {"batch": full_ms / ms, "per_hit_kernel": full_hits_ms / apply_ms,
+                                          "full_attention_ms": full_ms, "paper_context": PAPER_CONTEXT},
+            "search_qps": cfg.B / (search_ms * 1e-3),
+            "stages": secondary, "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+    if not args.no_cpu_baseline:
+        import oracle
+        oracle.set_threads(os.cpu_count() or 1)
+        t, desc, cores = oracle_step_sample(cfg)
+        line["cpu_baseline"] = {"value": cfg.B * cfg.S / t, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                                "sample": desc}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_e2e(args, cfg, ctx, db, step, q, Q, K, V, dev, stream):
+    """Per step: H2D queries -> search -> D2H hit mask -> H2D V (all rows) + Q,K (miss rows only,
+    Alg. 2: q/k projections exist only on a miss) -> apply + attend -> D2H O and idx/score/hit."""
+    import paper_2510_25979_b200 as ac
+    qh = q.cpu().pin_memory()
+    Vh = V.cpu().pin_memory()
+    Qh = Q.cpu().pin_memory()
+    Kh = K.cpu().pin_memory()
+    Oh = torch.empty(V.shape, dtype=V.dtype).pin_memory()
+    resh = [torch.empty(cfg.B, dtype=t).pin_memory() for t in (torch.int64, torch.float32, torch.uint8)]
+    qd, Vd, Qd, Kd, Od = (torch.empty_like(t) for t in (q, V, Q, K, V))
+    row = Vh[0].numel() * Vh.element_size()
+    stats = {"h2d": 0, "d2h": 0}
+
+    def one():
+        qd.copy_(qh, non_blocking=True)
+        idx, score, hit = step.search(qd)
+        hit_h = hit.cpu()  # syncs: the miss set is needed on the host to ship only the miss rows' Q, K
+        Vd.copy_(Vh, non_blocking=True)
+        misses = torch.nonzero(hit_h == 0).flatten().tolist()
+        for b in misses:
+            Qd[b].copy_(Qh[b], non_blocking=True)
+            Kd[b].copy_(Kh[b], non_blocking=True)
+        step.attend(idx, hit, Qd, Kd, Vd, Od)
+        Oh.copy_(Od, non_blocking=True)
+        for t, h in zip((idx, score, hit), resh):
+            h.copy_(t, non_blocking=True)
+        stats["h2d"] = qh.numel() * qh.element_size() + Vh.numel() * Vh.element_size() + 2 * len(misses) * row
+        stats["d2h"] = Oh.numel() * Oh.element_size() + cfg.B * (8 + 4 + 1) + cfg.B
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    n = max(1, min(args.steps, 5))
+    t0.record(stream)
+    for _ in range(n):
+        one()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / n
+    return {"value": cfg.B * cfg.S / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms, "steps": n,
+            "h2d_bytes_per_step": stats["h2d"], "d2h_bytes_per_step": stats["d2h"],
+            "note": "pinned host buffers; includes one mid-step D2H of the hit mask"}
+
+
+def _ncu_traffic(cfg_name, kernel):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        t = json.load(f)
+    return t.get(cfg_name, {}).get(kernel)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="llama32_1b", choices=[k for k in synth.CONFIGS if k != "search_sweep"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        print("bench.py: note: --warmup < 3 does not meet the timing rules (profiling runs only)", file=sys.stderr)
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,195 @@
+/*
+ * attncache.h — C ABI of the B200-native AttnCache hot path (arXiv 2510.25979).
+ *
+ * The library implements the data-parallel hot path of AttnCache: Alg. 1's
+ * "VecDB.search" + threshold gate and Alg. 2's attention
+ * step — on a hit, O = attn_map . V with the cached maps
+ * (Alg. 2 l.373-375); on a miss, the causal softmax(QK^T/sqrt(d_k)) . V of
+ * Eq. 5.  Readings of the paper that the library fixes
+ * are listed in DESIGN.md §Readings (R1..R25).
+ *
+ * Conventions (apply to every call):
+ *  - Every call returns attncache_status; ATTNCACHE_OK == 0.  No exception or
+ *    C++ type crosses the ABI.  attncache_last_error() gives a thread-local
+ *    human-readable detail of the last non-OK status.
+ *  - All data pointers are DEVICE pointers owned by the caller (e.g. torch
+ *    tensors' data_ptr()); host pointers are rejected with
+ *    ATTNCACHE_ERR_INVALID_ARGUMENT when the driver can tell.  Scalars and
+ *    descriptor structs are host memory.
+ *  - Calls are asynchronous on the given stream (a cudaStream_t passed as
+ *    void*; NULL = the legacy default stream); outputs are valid after the
+ *    stream is synchronised.  No steady-state call allocates device memory
+ *    except the first time a larger batch is seen (scratch growth).
+ *  - Errors found by device code (an index outside the database) are
+ *    deferred: the offending rows are skipped and the next
+ *    attncache_ctx_sync() returns the status.
+ *  - All arrays are dense row-major with the innermost dimension contiguous.
+ *  - A ctx is used by one host thread at a time.  A db is immutable after
+ *    load and may be read concurrently.
+ */
+#ifndef ATTNCACHE_H_
+#define ATTNCACHE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ATTNCACHE_OK = 0,
+    ATTNCACHE_ERR_INVALID_ARGUMENT = 1, /* null pointer, NaN tau, bad range, host pointer     */
+    ATTNCACHE_ERR_SHAPE = 2,            /* S/L/H/d/D disagree with the database  */
+    ATTNCACHE_ERR_DTYPE = 3,            /* unsupported dtype or dtype combination             */
+    ATTNCACHE_ERR_ALIGNMENT = 4,        /* base pointer or row pitch not 16-byte aligned      */
+    ATTNCACHE_ERR_NOT_FOUND = 5,        /* an index outside the database (deferred)           */
+    ATTNCACHE_ERR_EMPTY = 6,            /* search against a database with no entries          */
+    ATTNCACHE_ERR_OUT_OF_MEMORY = 7,
+    ATTNCACHE_ERR_CUDA = 8,             /* a CUDA runtime/driver error (sticky errors too)    */
+    ATTNCACHE_ERR_STATE = 9,            /* wrong device / destroyed handle                    */
+    ATTNCACHE_ERR_UNSUPPORTED = 10      /* e.g. no sm_100 device                              */
+} attncache_status;
+
+typedef enum { ATTNCACHE_F32 = 0, ATTNCACHE_F16 = 1, ATTNCACHE_BF16 = 2 } attncache_dtype;
+
+typedef struct attncache_ctx attncache_ctx; /* per process and device: scratch + deferred errors */
+typedef struct attncache_db attncache_db;   /* this rank's shard view of the memoization database */
+
+const char *attncache_status_string(attncache_status s);
+const char *attncache_last_error(void);
+/* Library version, e.g. 100 for 0.1.0. */
+int32_t attncache_version(void);
+/* Number of device kernels this library has launched in this process (all devices, all
+ * streams; a monotone counter used to report gpu_launches).  Library-internal memsets are
+ * not counted. */
+uint64_t attncache_launch_count(void);
+
+/* ---- lifecycle --------------------------------------------------------- */
+
+/* Creates a context bound to CUDA device `device` (the caller's current device is not changed
+ * permanently).  Requires compute capability 10.0 (sm_100a); else ATTNCACHE_ERR_UNSUPPORTED. */
+attncache_status attncache_ctx_create(int32_t device, attncache_ctx **out);
+attncache_status attncache_ctx_destroy(attncache_ctx *ctx);
+/* Synchronises the device and returns (then clears) any deferred error: ERR_NOT_FOUND when an
+ * apply call met an index outside its shard, ERR_CUDA on an asynchronous CUDA fault. */
+attncache_status attncache_ctx_sync(attncache_ctx *ctx);
+
+/* ---- database (Fig. 4: "Both databases share the same index") ----
+ *
+ * The feature-vector DB (key = vector, value = index) and the attention-map DB (key = index,
+ * value = maps) share one index space [0, n_global).  This rank holds the contiguous slice
+ * [shard_begin, shard_begin + shard_count).  db_load BORROWS `feats` and `maps`: the caller
+ * keeps them alive and unmodified until attncache_db_free.
+ *   feats: [shard_count][feat_dim] in feat_dtype (F32 or BF16), rows L2-normalised by the
+ *          producer (reading R2: the library never renormalises).
+ *   maps : [shard_count][n_layers][n_heads][seq_len][seq_len] in map_dtype (F16 or BF16):
+ *          post-softmax causal maps, exact +0.0 above the diagonal (reading R11) — layer-
+ *          contiguous per entry and head-major inside a layer.  May be NULL
+ *          for a search-only database (n_layers = n_heads = seq_len = 0).
+ * Errors: INVALID_ARGUMENT (ranges, null feats with shard_count > 0, n_global >= 2^32),
+ * DTYPE, ALIGNMENT (feats/maps base or row pitch not a multiple of 16 bytes). */
+typedef struct {
+    int64_t n_global;
+    int64_t shard_begin;
+    int64_t shard_count;
+    int32_t feat_dim;
+    int32_t feat_dtype; /* attncache_dtype */
+    const void *feats;
+    int32_t n_layers;
+    int32_t n_heads;
+    int32_t seq_len;
+    int32_t map_dtype; /* attncache_dtype */
+    const void *maps;
+} attncache_db_desc;
+
+attncache_status attncache_db_load(attncache_ctx *ctx, const attncache_db_desc *desc, attncache_db **out);
+attncache_status attncache_db_free(attncache_db *db);
+
+/* ---- Alg. 1: VecDB.search + theta gate -----------
+ *
+ * attncache_search — single-rank search over this shard (which must cover the whole DB,
+ * shard_count == n_global; otherwise use search_keys + keys_decode across ranks).
+ *   queries: [n_queries][feat_dim] in the DB's feat_dtype (no silent casts; reading R10).
+ *   idx[b]  : global index of the top-1 entry by inner product s = q . x (fp32 accumulation),
+ *             the LOWEST index among equal scores (reading R3); always set, also on a miss.
+ *   score[b]: that fp32 inner product.   hit[b]: 1 iff score[b] >= tau (inclusive).
+ * tau may be any non-NaN float (tau > 1: every query misses).  n_queries may be 0.
+ * Errors: EMPTY (n_global == 0), INVALID_ARGUMENT (NaN tau, null pointers with n > 0). */
+attncache_status attncache_search(attncache_db *db, const void *queries, int64_t n_queries, float tau,
+                                  int64_t *idx, float *score, uint8_t *hit, void *stream);
+
+/* Sharded halves of the same search (C1/C2 of SURVEY.md §2.4).  search_keys writes, per query,
+ * the packed key of this shard's top-1:  key = ord(score) << 32 | (0xFFFFFFFF - global_index),
+ * an unsigned 64-bit value where ord() maps fp32 bits to an order-preserving u32 (-0.0
+ * canonicalised to +0.0).  The maximum key over shards is the global top-1 with the
+ * lowest-index tie-break, in any reduction order (reading R3).  An empty shard writes 0 (the
+ * neutral element).  keys: [n_queries] uint64 on the device (callers may move them as int64 bit
+ * patterns, e.g. with an all-gather).
+ * keys_decode reduces keys [n_shards][n_queries] by unsigned max over shards (the cross-shard
+ * top-1 of north_star) and decodes idx/score/hit exactly as attncache_search does; a query whose
+ * keys are all 0 gets idx = -1, score = -inf, hit = 0. */
+attncache_status attncache_search_keys(attncache_db *db, const void *queries, int64_t n_queries,
+                                       uint64_t *keys, void *stream);
+attncache_status attncache_keys_decode(const uint64_t *keys, int32_t n_shards, int64_t n_queries, float tau,
+                                       int64_t *idx, float *score, uint8_t *hit, void *stream);
+
+/* ---- Alg. 2 hit branch: O = attn_map . V ---------------
+ *
+ * For every row b in [0, n_rows) that is selected — hit[b] != 0 when `hit` is non-NULL, else
+ * idx[b] >= 0 — and for every layer l in [layer_begin, layer_end) and head h:
+ *     O[b][l-layer_begin][h] (S x d) = maps[idx[b] - shard_begin][l][h] (S x S) . V[b][l-layer_begin][h] (S x d)
+ * accumulated in fp32 and rounded once to act_dtype.  Unselected rows of O are left untouched.
+ * V, O: [n_rows][layer_end-layer_begin][n_heads][seq_len][head_dim] in act_dtype.
+ * The maps are read in place from the DB (no "attention cache" copy; reading R18); tiles above
+ * the diagonal are never read.  A selected idx outside this shard is skipped and reported by the
+ * next attncache_ctx_sync() as ERR_NOT_FOUND.  Supported: act_dtype == map_dtype (tensor cores),
+ * or act_dtype F32 with any map dtype (CUDA cores).
+ * Errors: SHAPE (layer range outside [0, n_layers), head_dim <= 0), DTYPE, ALIGNMENT, STATE
+ * (db has no maps). */
+attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                        int32_t layer_begin, int32_t layer_end, int32_t head_dim,
+                                        int32_t act_dtype, const void *V, void *O, void *stream);
+
+/* ---- Alg. 2 miss branch core (Eq. 5) -------
+ *
+ * O = softmax(Q K^T * scale with keys j > i masked) . V for every selected row b (skip == NULL
+ * or skip[b] == 0), layer and head.  Q and K arrive post-RoPE (RoPE is outside the path;
+ * reading R16).  scale <= 0 means 1/sqrt(head_dim).  Q, K, V, O:
+ * [batch][n_layers][n_heads][seq_len][head_dim] in act_dtype; fp32 softmax statistics.
+ * Local to the calling device. */
+attncache_status attncache_attend_full(attncache_ctx *ctx, int64_t batch, int32_t n_layers, int32_t n_heads,
+                                       int32_t seq_len, int32_t head_dim, int32_t act_dtype, const void *Q,
+                                       const void *K, const void *V, float scale, const uint8_t *skip, void *O,
+                                       void *stream);
+
+/* ---- routing helpers for the multi-GPU path (north_star: hits go to the owning GPU) ----
+ *
+ * route_plan: for rows b in [0, n_rows) with hit[b] != 0, owner[b] = the rank r with
+ * shard_begins[r] <= idx[b] < shard_begins[r+1] (shard_begins: device int64[world+1]);
+ * owner[b] = -1 for misses.  counts[r] = number of rows owned by r; order = the selected rows
+ * grouped by owner (ascending rank, ascending b inside a rank), n = sum(counts) entries used.
+ * Deterministic.  gather_rows: dst[k] = src[rows[k]]; scatter_rows: dst[rows[k]] = src[k];
+ * rows are int64 row numbers and rows are row_bytes long (multiple of 16). */
+attncache_status attncache_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                      const int64_t *shard_begins, int32_t world, int32_t *owner, int32_t *counts,
+                                      int64_t *order, void *stream);
+attncache_status attncache_gather_rows(const void *src, const int64_t *rows, int64_t n_rows, int64_t row_bytes,
+                                       void *dst, void *stream);
+attncache_status attncache_scatter_rows(const void *src, const int64_t *rows, int64_t n_rows, int64_t row_bytes,
+                                        void *dst, void *stream);
+
+/* ---- test/debug: literal AttnMapsDB.get(idx, n) (Alg. 1 l.259) ------------
+ * Copies maps[idx - shard_begin][layer_begin:layer_end] of a LOCAL entry to `out` (device).
+ * Errors: NOT_FOUND (idx outside this shard), SHAPE. */
+attncache_status attncache_fetch_maps(attncache_db *db, int64_t idx, int32_t layer_begin, int32_t layer_end,
+                                      void *out, void *stream);
+
+/* ---- introspection: kernel variant chosen for a call (for tests/bench) ----
+ * kind: 0 = search, 1 = apply, 2 = attend.  Returns a static string such as "tc" (tcgen05) or
+ * "ffma" for the arguments given (no launch). */
+const char *attncache_variant(int32_t kind, int32_t dtype, int32_t seq_len, int32_t head_dim);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATTNCACHE_H_ */

@@ -1,0 +1,333 @@
+"""B200-native AttnCache hot path (arXiv 2510.25979) — thin Python binding over libattncache.so.
+
+The binding only marshals arguments: torch supplies device memory (``data_ptr``)
+and streams (``cuda_stream``); every step of the path runs in the library's
+CUDA kernels (include/attncache.h).  There is no CPU fallback: if the
+extension is missing or the device is not sm_100a, calls raise.
+
+Function names follow the C ABI (``attncache_search`` ...).  Paper mapping:
+Alg. 1 VecDB.search + theta gate -> ``attncache_search``; Alg. 2 hit branch
+``mat_mul(attn_map, v)`` -> ``attncache_apply_cached``; Alg. 2 miss branch
+(softmax(QK^T/sqrt(d_k)) . V, Eq. 5) -> ``attncache_attend_full``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+__all__ = [
+    "AttnCacheError", "Context", "Database", "lib_path", "load_library",
+    "attncache_ctx_create", "attncache_ctx_destroy", "attncache_ctx_sync", "attncache_db_load",
+    "attncache_db_free", "attncache_search", "attncache_search_keys", "attncache_keys_decode",
+    "attncache_apply_cached", "attncache_attend_full", "attncache_route_plan", "attncache_gather_rows",
+    "attncache_scatter_rows", "attncache_fetch_maps", "attncache_variant", "attncache_version", "attncache_launch_count",
+    "ABI_FUNCTIONS",
+]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_PKG, "lib", "libattncache.so")
+
+# every symbol include/attncache.h declares
+ABI_FUNCTIONS = [
+    "attncache_status_string", "attncache_last_error", "attncache_version", "attncache_ctx_create",
+    "attncache_ctx_destroy", "attncache_ctx_sync", "attncache_db_load", "attncache_db_free", "attncache_search",
+    "attncache_search_keys", "attncache_keys_decode", "attncache_apply_cached", "attncache_attend_full",
+    "attncache_route_plan", "attncache_gather_rows", "attncache_scatter_rows", "attncache_fetch_maps",
+    "attncache_variant", "attncache_launch_count",
+]
+
+_DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
+
+
+class _DbDesc(ctypes.Structure):
+    _fields_ = [("n_global", ctypes.c_int64), ("shard_begin", ctypes.c_int64), ("shard_count", ctypes.c_int64),
+                ("feat_dim", ctypes.c_int32), ("feat_dtype", ctypes.c_int32), ("feats", ctypes.c_void_p),
+                ("n_layers", ctypes.c_int32), ("n_heads", ctypes.c_int32), ("seq_len", ctypes.c_int32),
+                ("map_dtype", ctypes.c_int32), ("maps", ctypes.c_void_p)]
+
+
+class AttnCacheError(RuntimeError):
+    def __init__(self, status: int, name: str, detail: str):
+        super().__init__(f"{name}: {detail}")
+        self.status = status
+        self.name = name
+
+
+_lib = None
+
+
+def load_library():
+    """Loads libattncache.so (built in-tree by paper_2510_25979_b200.build). Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(lib_path):
+        raise ImportError(f"libattncache.so not built at {lib_path}; run `python -m paper_2510_25979_b200.build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(lib_path)
+    P, I64, I32, F32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
+    sig = {
+        "attncache_status_string": ([I32], ctypes.c_char_p),
+        "attncache_last_error": ([], ctypes.c_char_p),
+        "attncache_version": ([], I32),
+        "attncache_launch_count": ([], ctypes.c_uint64),
+        "attncache_variant": ([I32, I32, I32, I32], ctypes.c_char_p),
+        "attncache_ctx_create": ([I32, ctypes.POINTER(P)], I32),
+        "attncache_ctx_destroy": ([P], I32),
+        "attncache_ctx_sync": ([P], I32),
+        "attncache_db_load": ([P, ctypes.POINTER(_DbDesc), ctypes.POINTER(P)], I32),
+        "attncache_db_free": ([P], I32),
+        "attncache_search": ([P, P, I64, F32, P, P, P, P], I32),
+        "attncache_search_keys": ([P, P, I64, P, P], I32),
+        "attncache_keys_decode": ([P, I32, I64, F32, P, P, P, P], I32),
+        "attncache_apply_cached": ([P, P, P, I64, I32, I32, I32, I32, P, P, P], I32),
+        "attncache_attend_full": ([P, I64, I32, I32, I32, I32, I32, P, P, P, F32, P, P, P], I32),
+        "attncache_route_plan": ([P, P, I64, P, I32, P, P, P, P], I32),
+        "attncache_gather_rows": ([P, P, I64, I64, P, P], I32),
+        "attncache_scatter_rows": ([P, P, I64, I64, P, P], I32),
+        "attncache_fetch_maps": ([P, I64, I32, I32, P, P], I32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        L = load_library()
+        raise AttnCacheError(status, L.attncache_status_string(status).decode(), L.attncache_last_error().decode())
+
+
+def _p(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream, device) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev(t: torch.Tensor, what: str):
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+
+
+class Context:
+    """attncache_ctx: one per process and device."""
+
+    def __init__(self, device: int = 0):
+        L = load_library()
+        h = ctypes.c_void_p()
+        _check(L.attncache_ctx_create(int(device), ctypes.byref(h)))
+        self.handle = h
+        self.device = int(device)
+
+    def sync(self):
+        _check(load_library().attncache_ctx_sync(self.handle))
+
+    def close(self):
+        if self.handle:
+            load_library().attncache_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Database:
+    """attncache_db: this rank's shard of the feature-vector DB and the attention-map DB
+    ("Both databases share the same index").  Keeps the borrowed tensors alive."""
+
+    def __init__(self, ctx: Context, feats: torch.Tensor, maps: Optional[torch.Tensor] = None,
+                 n_global: Optional[int] = None, shard_begin: int = 0):
+        L = load_library()
+        _dev(feats, "feats")
+        if maps is not None:
+            _dev(maps, "maps")
+            if maps.dim() != 5 or maps.shape[0] != feats.shape[0] or maps.shape[3] != maps.shape[4]:
+                raise ValueError("maps must be [n][L][H][S][S] with n == len(feats)")
+        n = feats.shape[0]
+        desc = _DbDesc(n_global=n if n_global is None else int(n_global), shard_begin=int(shard_begin),
+                       shard_count=n, feat_dim=feats.shape[1], feat_dtype=_DT[feats.dtype],
+                       feats=feats.data_ptr() if n else None,
+                       n_layers=maps.shape[1] if maps is not None else 0,
+                       n_heads=maps.shape[2] if maps is not None else 0,
+                       seq_len=maps.shape[3] if maps is not None else 0,
+                       map_dtype=_DT[maps.dtype] if maps is not None else 0,
+                       maps=maps.data_ptr() if (maps is not None and n) else None)
+        h = ctypes.c_void_p()
+        _check(L.attncache_db_load(ctx.handle, ctypes.byref(desc), ctypes.byref(h)))
+        self.handle = h
+        self.ctx = ctx
+        self.feats, self.maps = feats, maps
+        self.n_global, self.shard_begin, self.shard_count = desc.n_global, desc.shard_begin, n
+        self.device = feats.device
+
+    def close(self):
+        if self.handle:
+            load_library().attncache_db_free(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---- function-style API mirroring the C names ---------------------------------------------------
+
+def attncache_version() -> int:
+    return int(load_library().attncache_version())
+
+
+def attncache_launch_count() -> int:
+    """Kernels launched by the library so far in this process (for gpu_launches)."""
+    return int(load_library().attncache_launch_count())
+
+
+def attncache_variant(kind: str, dtype: torch.dtype, seq_len: int, head_dim: int) -> str:
+    k = {"search": 0, "apply": 1, "attend": 2}[kind]
+    return load_library().attncache_variant(k, _DT[dtype], int(seq_len), int(head_dim)).decode()
+
+
+def attncache_ctx_create(device: int = 0) -> Context:
+    return Context(device)
+
+
+def attncache_ctx_destroy(ctx: Context) -> None:
+    ctx.close()
+
+
+def attncache_ctx_sync(ctx: Context) -> None:
+    ctx.sync()
+
+
+def attncache_db_load(ctx: Context, feats, maps=None, n_global=None, shard_begin=0) -> Database:
+    return Database(ctx, feats, maps, n_global, shard_begin)
+
+
+def attncache_db_free(db: Database) -> None:
+    db.close()
+
+
+def attncache_search(db: Database, queries: torch.Tensor, tau: float, idx=None, score=None, hit=None, stream=None):
+    """Alg. 1 l.255-257 on a single rank: returns (idx int64[B], score f32[B], hit u8[B])."""
+    _dev(queries, "queries")
+    B = queries.shape[0]
+    dev = queries.device
+    idx = torch.empty(B, dtype=torch.int64, device=dev) if idx is None else idx
+    score = torch.empty(B, dtype=torch.float32, device=dev) if score is None else score
+    hit = torch.empty(B, dtype=torch.uint8, device=dev) if hit is None else hit
+    _check(load_library().attncache_search(db.handle, _p(queries), B, float(tau), _p(idx), _p(score), _p(hit),
+                                           _stream(stream, dev)))
+    return idx, score, hit
+
+
+def attncache_search_keys(db: Database, queries: torch.Tensor, keys=None, stream=None) -> torch.Tensor:
+    """This shard's packed top-1 keys (int64 view of the u64 keys)."""
+    _dev(queries, "queries")
+    B = queries.shape[0]
+    keys = torch.empty(B, dtype=torch.int64, device=queries.device) if keys is None else keys
+    _check(load_library().attncache_search_keys(db.handle, _p(queries), B, _p(keys), _stream(stream, queries.device)))
+    return keys
+
+
+def attncache_keys_decode(keys: torch.Tensor, tau: float, idx=None, score=None, hit=None, stream=None):
+    """keys: [n_shards][B] (or [B]) packed keys -> cross-shard top-1 idx/score/hit."""
+    keys = keys.reshape(-1, keys.shape[-1])
+    n_shards, B = keys.shape
+    dev = keys.device
+    idx = torch.empty(B, dtype=torch.int64, device=dev) if idx is None else idx
+    score = torch.empty(B, dtype=torch.float32, device=dev) if score is None else score
+    hit = torch.empty(B, dtype=torch.uint8, device=dev) if hit is None else hit
+    _check(load_library().attncache_keys_decode(_p(keys), n_shards, B, float(tau), _p(idx), _p(score), _p(hit),
+                                                _stream(stream, dev)))
+    return idx, score, hit
+
+
+def attncache_apply_cached(db: Database, idx: torch.Tensor, V: torch.Tensor, O: Optional[torch.Tensor] = None,
+                           hit: Optional[torch.Tensor] = None, layer_begin: int = 0, layer_end: Optional[int] = None,
+                           stream=None) -> torch.Tensor:
+    """Alg. 2 l.373-375: O[b] = maps[idx[b]] . V[b] for selected rows; V, O [B][L'][H][S][d]."""
+    _dev(V, "V")
+    _dev(idx, "idx")
+    layer_end = (db.maps.shape[1] if db.maps is not None else 0) if layer_end is None else layer_end
+    O = torch.empty_like(V) if O is None else O
+    _dev(O, "O")
+    if V.dim() != 5 or O.shape != V.shape or V.shape[0] != idx.shape[0]:
+        raise ValueError("V/O must be [B][L'][H][S][d] matching idx")
+    if db.maps is not None and (V.shape[1] != layer_end - layer_begin or V.shape[2] != db.maps.shape[2]
+                                or V.shape[3] != db.maps.shape[3]):
+        raise AttnCacheError(2, "ATTNCACHE_ERR_SHAPE", "V shape disagrees with the database (L', H, S)")
+    _check(load_library().attncache_apply_cached(db.handle, _p(idx), _p(hit), V.shape[0], int(layer_begin),
+                                                 int(layer_end), V.shape[4], _DT[V.dtype], _p(V), _p(O),
+                                                 _stream(stream, V.device)))
+    return O
+
+
+def attncache_attend_full(ctx: Context, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor,
+                          O: Optional[torch.Tensor] = None, scale: float = 0.0, skip: Optional[torch.Tensor] = None,
+                          stream=None) -> torch.Tensor:
+    """Alg. 2 l.376-381 / Eq. 5: O = softmax(QK^T*scale, causal) . V; Q, K, V, O [B][L][H][S][d]."""
+    for t, n in ((Q, "Q"), (K, "K"), (V, "V")):
+        _dev(t, n)
+    if not (Q.shape == K.shape == V.shape) or Q.dim() != 5 or not (Q.dtype == K.dtype == V.dtype):
+        raise ValueError("Q, K, V must share one [B][L][H][S][d] shape and dtype")
+    O = torch.empty_like(V) if O is None else O
+    _dev(O, "O")
+    B, Lq, H, S, d = Q.shape
+    _check(load_library().attncache_attend_full(ctx.handle, B, Lq, H, S, d, _DT[Q.dtype], _p(Q), _p(K), _p(V),
+                                                float(scale), _p(skip), _p(O), _stream(stream, Q.device)))
+    return O
+
+
+def attncache_route_plan(idx, hit, shard_begins: torch.Tensor, owner=None, counts=None, order=None, stream=None):
+    n = idx.shape[0]
+    world = shard_begins.shape[0] - 1
+    dev = idx.device
+    owner = torch.empty(n, dtype=torch.int32, device=dev) if owner is None else owner
+    counts = torch.empty(world, dtype=torch.int32, device=dev) if counts is None else counts
+    order = torch.empty(max(n, 1), dtype=torch.int64, device=dev) if order is None else order
+    _check(load_library().attncache_route_plan(_p(idx), _p(hit), n, _p(shard_begins), world, _p(owner), _p(counts),
+                                               _p(order), _stream(stream, dev)))
+    return owner, counts, order
+
+
+def attncache_gather_rows(src: torch.Tensor, rows: torch.Tensor, dst: Optional[torch.Tensor] = None, stream=None):
+    row_bytes = src[0].numel() * src.element_size() if src.shape[0] else 0
+    dst = torch.empty((rows.shape[0], *src.shape[1:]), dtype=src.dtype, device=src.device) if dst is None else dst
+    if rows.shape[0]:
+        _check(load_library().attncache_gather_rows(_p(src), _p(rows), rows.shape[0], row_bytes, _p(dst),
+                                                    _stream(stream, src.device)))
+    return dst
+
+
+def attncache_scatter_rows(src: torch.Tensor, rows: torch.Tensor, dst: torch.Tensor, stream=None):
+    if rows.shape[0]:
+        row_bytes = src[0].numel() * src.element_size()
+        _check(load_library().attncache_scatter_rows(_p(src), _p(rows), rows.shape[0], row_bytes, _p(dst),
+                                                     _stream(stream, src.device)))
+    return dst
+
+
+def attncache_fetch_maps(db: Database, idx: int, layer_begin: int = 0, layer_end: Optional[int] = None,
+                         out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    m = db.maps
+    layer_end = m.shape[1] if layer_end is None else layer_end
+    out = torch.empty((layer_end - layer_begin, *m.shape[2:]), dtype=m.dtype, device=m.device) if out is None else out
+    _check(load_library().attncache_fetch_maps(db.handle, int(idx), int(layer_begin), int(layer_end), _p(out),
+                                               _stream(stream, m.device)))
+    return out

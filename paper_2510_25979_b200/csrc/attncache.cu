@@ -1,0 +1,424 @@
+// attncache.cu — the C ABI (include/attncache.h): validation, scratch management, dispatch.
+// Every step of the hot path runs in the kernels launched from here; nothing computes on the host.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <cmath>
+
+#include "kernels.cuh"
+
+namespace ac {
+
+static thread_local char g_err[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+attncache_status fail(attncache_status s, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+attncache_status cuda_status(cudaError_t e, const char *what) {
+    if (e == cudaErrorMemoryAllocation) return fail(ATTNCACHE_ERR_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+    return fail(ATTNCACHE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+attncache_status ensure_scratch(Scratch &s, size_t bytes) {
+    if (s.bytes >= bytes) return ATTNCACHE_OK;
+    if (s.ptr) {
+        AC_CUDA(cudaDeviceSynchronize());  // the old buffer may still be in use by queued work
+        AC_CUDA(cudaFree(s.ptr));
+        s.ptr = nullptr;
+        s.bytes = 0;
+    }
+    size_t cap = bytes < 4096 ? 4096 : bytes + bytes / 2;
+    AC_CUDA(cudaMalloc(&s.ptr, cap));
+    s.bytes = cap;
+    return ATTNCACHE_OK;
+}
+
+// A device pointer check: rejects host (unregistered or pinned) memory when the runtime can tell.
+static bool is_device_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace ac
+
+using namespace ac;
+
+extern "C" {
+
+const char *attncache_status_string(attncache_status s) {
+    switch (s) {
+    case ATTNCACHE_OK: return "ATTNCACHE_OK";
+    case ATTNCACHE_ERR_INVALID_ARGUMENT: return "ATTNCACHE_ERR_INVALID_ARGUMENT";
+    case ATTNCACHE_ERR_SHAPE: return "ATTNCACHE_ERR_SHAPE";
+    case ATTNCACHE_ERR_DTYPE: return "ATTNCACHE_ERR_DTYPE";
+    case ATTNCACHE_ERR_ALIGNMENT: return "ATTNCACHE_ERR_ALIGNMENT";
+    case ATTNCACHE_ERR_NOT_FOUND: return "ATTNCACHE_ERR_NOT_FOUND";
+    case ATTNCACHE_ERR_EMPTY: return "ATTNCACHE_ERR_EMPTY";
+    case ATTNCACHE_ERR_OUT_OF_MEMORY: return "ATTNCACHE_ERR_OUT_OF_MEMORY";
+    case ATTNCACHE_ERR_CUDA: return "ATTNCACHE_ERR_CUDA";
+    case ATTNCACHE_ERR_STATE: return "ATTNCACHE_ERR_STATE";
+    case ATTNCACHE_ERR_UNSUPPORTED: return "ATTNCACHE_ERR_UNSUPPORTED";
+    }
+    return "ATTNCACHE_ERR_UNKNOWN";
+}
+
+const char *attncache_last_error(void) { return g_err; }
+
+int32_t attncache_version(void) { return 100; }
+
+uint64_t attncache_launch_count(void) { return ac::launch_count(); }
+
+const char *attncache_variant(int32_t kind, int32_t dtype, int32_t seq_len, int32_t head_dim) {
+    switch (kind) {
+    case 0: return search_tc_supported(dtype, head_dim) ? "tc" : "ffma";  // head_dim = feat_dim here
+    case 1: return apply_tc_supported(dtype, dtype, seq_len, head_dim) ? "tc" : "ffma";
+    case 2: return attend_tc_supported(dtype, seq_len, head_dim) ? "tc" : "ffma";
+    }
+    return "none";
+}
+
+// ---- lifecycle ------------------------------------------------------------------------------
+
+attncache_status attncache_ctx_create(int32_t device, attncache_ctx **out) {
+    if (!out) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_create: out is NULL");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(ATTNCACHE_ERR_UNSUPPORTED, "ctx_create: no CUDA device (%s)", cudaGetErrorString(e));
+    }
+    if (device < 0 || device >= n) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_create: device %d of %d", device, n);
+    cudaDeviceProp prop;
+    AC_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(ATTNCACHE_ERR_UNSUPPORTED, "ctx_create: device %d is sm_%d%d; this library is built for sm_100a",
+                    device, prop.major, prop.minor);
+    DeviceGuard g(device);
+    attncache_ctx *c = new attncache_ctx();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    e = cudaMalloc(&c->d_error, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(c->d_error, 0, sizeof(int));
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_status(e, "ctx_create: scratch");
+    }
+    *out = c;
+    return ATTNCACHE_OK;
+}
+
+attncache_status attncache_ctx_destroy(attncache_ctx *ctx) {
+    if (!ctx) return ATTNCACHE_OK;
+    DeviceGuard g(ctx->device);
+    cudaDeviceSynchronize();
+    cudaFree(ctx->d_error);
+    cudaFree(ctx->apply_list.ptr);
+    cudaFree(ctx->attend_list.ptr);
+    cudaFree(ctx->search_keys.ptr);
+    delete ctx;
+    return ATTNCACHE_OK;
+}
+
+attncache_status attncache_ctx_sync(attncache_ctx *ctx) {
+    if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_sync: ctx is NULL");
+    DeviceGuard g(ctx->device);
+    AC_CUDA(cudaDeviceSynchronize());
+    int flags = 0;
+    AC_CUDA(cudaMemcpy(&flags, ctx->d_error, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flags) {
+        AC_CUDA(cudaMemset(ctx->d_error, 0, sizeof(int)));
+        if (flags & 1) return fail(ATTNCACHE_ERR_NOT_FOUND, "apply_cached: an index outside this shard was skipped");
+    }
+    return ATTNCACHE_OK;
+}
+
+// ---- database -------------------------------------------------------------------------------
+
+attncache_status attncache_db_load(attncache_ctx *ctx, const attncache_db_desc *d, attncache_db **out) {
+    if (!ctx || !d || !out) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: NULL argument");
+    *out = nullptr;
+    if (d->n_global < 0 || d->shard_begin < 0 || d->shard_count < 0 || d->shard_begin + d->shard_count > d->n_global)
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: shard [%lld, +%lld) outside [0, %lld)",
+                    (long long)d->shard_begin, (long long)d->shard_count, (long long)d->n_global);
+    if (d->n_global >= (int64_t)0xFFFFFFFFll)
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: n_global must be < 2^32 - 1 (packed keys)");
+    if (d->feat_dim <= 0) return fail(ATTNCACHE_ERR_SHAPE, "db_load: feat_dim %d", d->feat_dim);
+    if (d->feat_dtype != ATTNCACHE_F32 && d->feat_dtype != ATTNCACHE_BF16)
+        return fail(ATTNCACHE_ERR_DTYPE, "db_load: feat_dtype must be F32 or BF16");
+    DeviceGuard g(ctx->device);
+    if (d->shard_count > 0) {
+        if (!d->feats) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: feats is NULL");
+        if (!is_device_ptr(d->feats)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: feats is not device memory");
+        if (!aligned16(d->feats) || ((int64_t)d->feat_dim * dtype_size(d->feat_dtype)) % 16)
+            return fail(ATTNCACHE_ERR_ALIGNMENT, "db_load: feats base / row pitch not 16-byte aligned");
+    }
+    const bool has_maps = d->n_layers > 0 || d->n_heads > 0 || d->seq_len > 0 || d->maps;
+    if (has_maps) {
+        if (d->n_layers <= 0 || d->n_heads <= 0 || d->seq_len <= 0)
+            return fail(ATTNCACHE_ERR_SHAPE, "db_load: L=%d H=%d S=%d", d->n_layers, d->n_heads, d->seq_len);
+        if (d->map_dtype != ATTNCACHE_F16 && d->map_dtype != ATTNCACHE_BF16)
+            return fail(ATTNCACHE_ERR_DTYPE, "db_load: map_dtype must be F16 or BF16");
+        if (d->shard_count > 0) {
+            if (!d->maps) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: maps is NULL");
+            if (!is_device_ptr(d->maps)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: maps is not device memory");
+            if (!aligned16(d->maps) || ((int64_t)d->seq_len * 2) % 16)
+                return fail(ATTNCACHE_ERR_ALIGNMENT, "db_load: maps base / row pitch (S*2 bytes) not 16-byte aligned");
+        }
+    }
+    attncache_db *db = new attncache_db();
+    db->ctx = ctx;
+    db->d = *d;
+    if (!has_maps) db->d.maps = nullptr;
+    *out = db;
+    return ATTNCACHE_OK;
+}
+
+attncache_status attncache_db_free(attncache_db *db) {
+    delete db;
+    return ATTNCACHE_OK;
+}
+
+// ---- search ---------------------------------------------------------------------------------
+
+static attncache_status search_keys_impl(attncache_db *db, const void *queries, int64_t n, uint64_t *keys,
+                                         cudaStream_t st) {
+    const attncache_db_desc &d = db->d;
+    AC_CUDA(cudaMemsetAsync(keys, 0, sizeof(uint64_t) * (size_t)n, st));
+    if (d.shard_count == 0 || n == 0) return ATTNCACHE_OK;
+    if (search_tc_supported(d.feat_dtype, d.feat_dim)) {
+        AC_CUDA(launch_search_tc(queries, d.feats, n, d.shard_count, d.feat_dim, d.shard_begin, keys,
+                                 db->ctx->sm_count, st));
+    } else {
+        AC_CUDA(launch_search_ffma(d.feat_dtype, queries, d.feats, n, d.shard_count, d.feat_dim, d.shard_begin, keys, st));
+    }
+    return ATTNCACHE_OK;
+}
+
+static attncache_status check_queries(attncache_db *db, const void *queries, int64_t n) {
+    if (!db) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: db is NULL");
+    if (n < 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: n_queries < 0");
+    if (n > 0) {
+        if (!queries) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: queries is NULL");
+        if (!is_device_ptr(queries)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: queries is not device memory");
+        if (!aligned16(queries)) return fail(ATTNCACHE_ERR_ALIGNMENT, "search: queries not 16-byte aligned");
+    }
+    return ATTNCACHE_OK;
+}
+
+attncache_status attncache_search_keys(attncache_db *db, const void *queries, int64_t n, uint64_t *keys, void *stream) {
+    attncache_status s = check_queries(db, queries, n);
+    if (s) return s;
+    if (n > 0 && !keys) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search_keys: keys is NULL");
+    DeviceGuard g(db->ctx->device);
+    return search_keys_impl(db, queries, n, keys, (cudaStream_t)stream);
+}
+
+attncache_status attncache_keys_decode(const uint64_t *keys, int32_t n_shards, int64_t n, float tau, int64_t *idx,
+                                       float *score, uint8_t *hit, void *stream) {
+    if (std::isnan(tau)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "keys_decode: tau is NaN");
+    if (n < 0 || n_shards <= 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "keys_decode: n=%lld n_shards=%d", (long long)n, n_shards);
+    if (n > 0 && (!keys || !idx || !score || !hit)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "keys_decode: NULL output");
+    AC_CUDA(launch_keys_decode(keys, n_shards, n, tau, idx, score, hit, (cudaStream_t)stream));
+    return ATTNCACHE_OK;
+}
+
+attncache_status attncache_search(attncache_db *db, const void *queries, int64_t n, float tau, int64_t *idx,
+                                  float *score, uint8_t *hit, void *stream) {
+    attncache_status s = check_queries(db, queries, n);
+    if (s) return s;
+    if (std::isnan(tau)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: tau is NaN");
+    if (db->d.n_global == 0) return fail(ATTNCACHE_ERR_EMPTY, "search: the database has no entries");
+    if (db->d.shard_count != db->d.n_global)
+        return fail(ATTNCACHE_ERR_STATE, "search: this db is one shard of %lld; use search_keys + keys_decode",
+                    (long long)db->d.n_global);
+    if (n == 0) return ATTNCACHE_OK;
+    if (!idx || !score || !hit) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: NULL output");
+    DeviceGuard g(db->ctx->device);
+    s = ensure_scratch(db->ctx->search_keys, sizeof(uint64_t) * (size_t)n);
+    if (s) return s;
+    uint64_t *keys = (uint64_t *)db->ctx->search_keys.ptr;
+    s = search_keys_impl(db, queries, n, keys, (cudaStream_t)stream);
+    if (s) return s;
+    AC_CUDA(launch_keys_decode(keys, 1, n, tau, idx, score, hit, (cudaStream_t)stream));
+    return ATTNCACHE_OK;
+}
+
+// ---- apply ----------------------------------------------------------------------------------
+
+attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                        int32_t layer_begin, int32_t layer_end, int32_t head_dim, int32_t act_dtype,
+                                        const void *V, void *O, void *stream) {
+    if (!db) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: db is NULL");
+    const attncache_db_desc &d = db->d;
+    if (d.n_layers <= 0) return fail(ATTNCACHE_ERR_STATE, "apply_cached: this database holds no maps");
+    if (n_rows < 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: n_rows < 0");
+    if (layer_begin < 0 || layer_end > d.n_layers || layer_begin >= layer_end)
+        return fail(ATTNCACHE_ERR_SHAPE, "apply_cached: layers [%d, %d) outside [0, %d)", layer_begin, layer_end, d.n_layers);
+    if (head_dim <= 0) return fail(ATTNCACHE_ERR_SHAPE, "apply_cached: head_dim %d", head_dim);
+    if (!dtype_valid(act_dtype)) return fail(ATTNCACHE_ERR_DTYPE, "apply_cached: act_dtype %d", act_dtype);
+    if (!(act_dtype == ATTNCACHE_F32 || act_dtype == d.map_dtype))
+        return fail(ATTNCACHE_ERR_DTYPE, "apply_cached: act_dtype must equal the map dtype or be F32");
+    if (n_rows == 0) return ATTNCACHE_OK;
+    if (!idx || !V || !O) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: NULL idx/V/O");
+    if (!is_device_ptr(idx) || !is_device_ptr(V) || !is_device_ptr(O) || (hit && !is_device_ptr(hit)))
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: idx/hit/V/O must be device memory");
+    if (!aligned16(V) || !aligned16(O) || ((int64_t)head_dim * dtype_size(act_dtype)) % 16)
+        return fail(ATTNCACHE_ERR_ALIGNMENT, "apply_cached: V/O base or row pitch (head_dim*elem) not 16-byte aligned");
+    DeviceGuard g(db->ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    attncache_status s = ensure_scratch(db->ctx->apply_list, rowlist_bytes(n_rows));
+    if (s) return s;
+    ApplyArgs a;
+    a.maps = d.maps;
+    a.L = d.n_layers;
+    a.H = d.n_heads;
+    a.S = d.seq_len;
+    a.d = head_dim;
+    a.layer_begin = layer_begin;
+    a.n_lay = layer_end - layer_begin;
+    a.map_dt = d.map_dtype;
+    a.act_dt = act_dtype;
+    a.V = V;
+    a.O = O;
+    a.list = rowlist_view(db->ctx->apply_list.ptr, n_rows);
+    a.max_rows = n_rows;
+    AC_CUDA(launch_select_apply(idx, hit, n_rows, d.shard_begin, d.shard_count, a.list, db->ctx->d_error, st));
+    if (apply_tc_supported(d.map_dtype, act_dtype, d.seq_len, head_dim)) {
+        AC_CUDA(launch_apply_tc(a, db->ctx->sm_count, st));
+    } else {
+        AC_CUDA(launch_apply_ffma(a, db->ctx->sm_count, st));
+    }
+    return ATTNCACHE_OK;
+}
+
+// ---- attend ---------------------------------------------------------------------------------
+
+attncache_status attncache_attend_full(attncache_ctx *ctx, int64_t batch, int32_t L, int32_t H, int32_t S, int32_t dd,
+                                       int32_t act_dtype, const void *Q, const void *K, const void *V, float scale,
+                                       const uint8_t *skip, void *O, void *stream) {
+    if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "attend_full: ctx is NULL");
+    if (batch < 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "attend_full: batch < 0");
+    if (L <= 0 || H <= 0 || S <= 0 || dd <= 0) return fail(ATTNCACHE_ERR_SHAPE, "attend_full: L=%d H=%d S=%d d=%d", L, H, S, dd);
+    if (S > 8192) return fail(ATTNCACHE_ERR_SHAPE, "attend_full: seq_len %d > 8192", S);
+    if (!dtype_valid(act_dtype)) return fail(ATTNCACHE_ERR_DTYPE, "attend_full: act_dtype %d", act_dtype);
+    if (std::isnan(scale)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "attend_full: scale is NaN");
+    if (batch == 0) return ATTNCACHE_OK;
+    if (!Q || !K || !V || !O) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "attend_full: NULL Q/K/V/O");
+    if (!is_device_ptr(Q) || !is_device_ptr(K) || !is_device_ptr(V) || !is_device_ptr(O) || (skip && !is_device_ptr(skip)))
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "attend_full: Q/K/V/O/skip must be device memory");
+    if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || ((int64_t)dd * dtype_size(act_dtype)) % 16)
+        return fail(ATTNCACHE_ERR_ALIGNMENT, "attend_full: base or row pitch (head_dim*elem) not 16-byte aligned");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    attncache_status s = ensure_scratch(ctx->attend_list, rowlist_bytes(batch));
+    if (s) return s;
+    AttendArgs a;
+    a.L = L;
+    a.H = H;
+    a.S = S;
+    a.d = dd;
+    a.dt = act_dtype;
+    a.scale = scale > 0.f ? scale : 1.0f / sqrtf((float)dd);
+    a.Q = Q;
+    a.K = K;
+    a.V = V;
+    a.O = O;
+    a.list = rowlist_view(ctx->attend_list.ptr, batch);
+    a.max_rows = batch;
+    AC_CUDA(launch_select_attend(skip, batch, a.list, st));
+    if (attend_tc_supported(act_dtype, S, dd)) {
+        AC_CUDA(launch_attend_tc(a, ctx->sm_count, st));
+    } else {
+        AC_CUDA(launch_attend_ffma(a, ctx->sm_count, st));
+    }
+    return ATTNCACHE_OK;
+}
+
+// ---- routing --------------------------------------------------------------------------------
+
+attncache_status attncache_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n, const int64_t *shard_begins,
+                                      int32_t world, int32_t *owner, int32_t *counts, int64_t *order, void *stream) {
+    if (n < 0 || world <= 0 || world > 1024) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "route_plan: n=%lld world=%d", (long long)n, world);
+    if (!shard_begins || !counts || (n > 0 && (!idx || !hit || !owner || !order)))
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "route_plan: NULL argument");
+    AC_CUDA(launch_route_plan(idx, hit, n, shard_begins, world, owner, counts, order, (cudaStream_t)stream));
+    return ATTNCACHE_OK;
+}
+
+static attncache_status copy_rows(const void *src, const int64_t *rows, int64_t n, int64_t row_bytes, void *dst,
+                                  bool gather, void *stream) {
+    if (n < 0 || row_bytes <= 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "copy_rows: n=%lld row_bytes=%lld", (long long)n, (long long)row_bytes);
+    if (n == 0) return ATTNCACHE_OK;
+    if (!src || !rows || !dst) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "copy_rows: NULL argument");
+    if (row_bytes % 16 || !aligned16(src) || !aligned16(dst)) return fail(ATTNCACHE_ERR_ALIGNMENT, "copy_rows: 16-byte alignment");
+    AC_CUDA(launch_copy_rows(src, rows, n, row_bytes, dst, gather, (cudaStream_t)stream));
+    return ATTNCACHE_OK;
+}
+
+attncache_status attncache_gather_rows(const void *src, const int64_t *rows, int64_t n, int64_t row_bytes, void *dst,
+                                       void *stream) {
+    return copy_rows(src, rows, n, row_bytes, dst, true, stream);
+}
+
+attncache_status attncache_scatter_rows(const void *src, const int64_t *rows, int64_t n, int64_t row_bytes, void *dst,
+                                        void *stream) {
+    return copy_rows(src, rows, n, row_bytes, dst, false, stream);
+}
+
+// ---- fetch (debug: literal AttnMapsDB.get) ---------------------------------------------------
+
+attncache_status attncache_fetch_maps(attncache_db *db, int64_t idx, int32_t layer_begin, int32_t layer_end, void *out,
+                                      void *stream) {
+    if (!db || !out) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "fetch_maps: NULL argument");
+    const attncache_db_desc &d = db->d;
+    if (d.n_layers <= 0) return fail(ATTNCACHE_ERR_STATE, "fetch_maps: this database holds no maps");
+    if (idx < d.shard_begin || idx >= d.shard_begin + d.shard_count)
+        return fail(ATTNCACHE_ERR_NOT_FOUND, "fetch_maps: index %lld not in this shard", (long long)idx);
+    if (layer_begin < 0 || layer_end > d.n_layers || layer_begin >= layer_end)
+        return fail(ATTNCACHE_ERR_SHAPE, "fetch_maps: layers [%d, %d)", layer_begin, layer_end);
+    const size_t per_layer = (size_t)d.n_heads * d.seq_len * d.seq_len * 2;
+    const char *src = (const char *)d.maps + ((size_t)(idx - d.shard_begin) * d.n_layers + layer_begin) * per_layer;
+    DeviceGuard g(db->ctx->device);
+    AC_CUDA(cudaMemcpyAsync(out, src, per_layer * (layer_end - layer_begin), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return ATTNCACHE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// kernels.cuh — host-side launchers of the device kernels (internal to libattncache).
+#pragma once
+#include "common.cuh"
+
+namespace ac {
+
+// Compacted selection list living in ctx scratch:
+//   int32 count | pad to 16 B | int32 rows[cap] | int64 ents[cap] (apply only)
+struct RowList {
+    int32_t *count;
+    int32_t *rows;
+    int64_t *ents;
+    int64_t cap;
+};
+RowList rowlist_view(void *base, int64_t cap);
+size_t rowlist_bytes(int64_t cap);
+
+// Rows with (hit ? hit[b] : idx[b] >= 0); entry = idx[b] - shard_begin must lie in
+// [0, shard_count) else *err |= 1 and the row is dropped.
+cudaError_t launch_select_apply(const int64_t *idx, const uint8_t *hit, int64_t n, int64_t shard_begin,
+                                int64_t shard_count, RowList out, int *err, cudaStream_t st);
+// Rows with skip == NULL || skip[b] == 0.
+cudaError_t launch_select_attend(const uint8_t *skip, int64_t n, RowList out, cudaStream_t st);
+
+// ---- search ----
+cudaError_t launch_search_ffma(int32_t dt, const void *q, const void *x, int64_t B, int64_t n, int32_t D,
+                               int64_t gbase, uint64_t *keys, cudaStream_t st);
+bool search_tc_supported(int32_t dt, int32_t D);
+cudaError_t launch_search_tc(const void *q, const void *x, int64_t B, int64_t n, int32_t D, int64_t gbase,
+                             uint64_t *keys, int sm_count, cudaStream_t st);
+cudaError_t launch_keys_decode(const uint64_t *keys, int32_t n_shards, int64_t n, float tau, int64_t *idx, float *score, uint8_t *hit,
+                               cudaStream_t st);
+
+// ---- apply (O = A . V) ----
+struct ApplyArgs {
+    const void *maps;  // shard maps [n_loc][L][H][S][S]
+    int32_t L, H, S, d;
+    int32_t layer_begin, n_lay;  // layer slice of V/O
+    int32_t map_dt, act_dt;
+    const void *V;
+    void *O;
+    RowList list;
+    int64_t max_rows;  // host upper bound on list count (n_rows)
+};
+cudaError_t launch_apply_ffma(const ApplyArgs &a, int sm_count, cudaStream_t st);
+bool apply_tc_supported(int32_t map_dt, int32_t act_dt, int32_t S, int32_t d);
+cudaError_t launch_apply_tc(const ApplyArgs &a, int sm_count, cudaStream_t st);
+
+// ---- attend (causal softmax attention) ----
+struct AttendArgs {
+    int32_t L, H, S, d, dt;
+    float scale;
+    const void *Q, *K, *V;
+    void *O;
+    RowList list;
+    int64_t max_rows;
+};
+cudaError_t launch_attend_ffma(const AttendArgs &a, int sm_count, cudaStream_t st);
+bool attend_tc_supported(int32_t dt, int32_t S, int32_t d);
+cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st);
+
+// ---- routing ----
+cudaError_t launch_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n, const int64_t *shard_begins,
+                              int32_t world, int32_t *owner, int32_t *counts, int64_t *order, cudaStream_t st);
+cudaError_t launch_copy_rows(const void *src, const int64_t *rows, int64_t n_rows, int64_t row_bytes, void *dst,
+                             bool gather, cudaStream_t st);
+
+}  // namespace ac

@@ -1,0 +1,392 @@
+// kernels_simt.cu — CUDA-core (FFMA) kernels: the fp32 / mixed-dtype paths of search, A.V and
+// causal attention, plus selection (compaction), key decoding and routing helpers.
+//
+// These are the generic-dtype paths (BASELINE.json configs[0] keeps fp32 features and fp32 V,
+// which the bf16/fp16 tensor-core kernels do not cover).  Tensor-core kernels live in
+// kernels_tc_*.cu.
+#include "kernels.cuh"
+
+namespace ac {
+
+// ============================================================================================
+// selection lists
+// ============================================================================================
+size_t rowlist_bytes(int64_t cap) { return 16 + (size_t)cap * 4 + 8 + (size_t)cap * 8; }
+
+RowList rowlist_view(void *base, int64_t cap) {
+    RowList r;
+    char *p = (char *)base;
+    r.count = (int32_t *)p;
+    r.rows = (int32_t *)(p + 16);
+    size_t off = 16 + (size_t)cap * 4;
+    off = (off + 7) & ~(size_t)7;
+    r.ents = (int64_t *)(p + off);
+    r.cap = cap;
+    return r;
+}
+
+// Order-preserving block compaction (one CTA of 1024 threads; n is at most a few 10^5 rows).
+template <typename Pred>
+__device__ void compact_rows(int64_t n, Pred pred, RowList out) {
+    __shared__ int warp_tot[32];
+    __shared__ int base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) base = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < n; b0 += blockDim.x) {
+        int64_t b = b0 + tid;
+        int64_t ent = -1;
+        bool sel = (b < n) && pred(b, ent);
+        unsigned m = __ballot_sync(0xffffffffu, sel);
+        if (lane == 0) warp_tot[warp] = __popc(m);
+        __syncthreads();
+        if (tid == 0) {
+            int run = base;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                int t = warp_tot[w];
+                warp_tot[w] = run;
+                run += t;
+            }
+            base = run;
+        }
+        __syncthreads();
+        if (sel) {
+            int pos = warp_tot[warp] + __popc(m & ((1u << lane) - 1u));
+            out.rows[pos] = (int32_t)b;
+            out.ents[pos] = ent;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *out.count = base;
+}
+
+__global__ void select_apply_kernel(const int64_t *idx, const uint8_t *hit, int64_t n, int64_t shard_begin,
+                                    int64_t shard_count, RowList out, int *err) {
+    compact_rows(n,
+                 [&](int64_t b, int64_t &ent) {
+                     bool want = hit ? (hit[b] != 0) : (idx[b] >= 0);
+                     if (!want) return false;
+                     int64_t e = idx[b] - shard_begin;
+                     if (e < 0 || e >= shard_count) {
+                         atomicOr(err, 1);
+                         return false;
+                     }
+                     ent = e;
+                     return true;
+                 },
+                 out);
+}
+
+__global__ void select_attend_kernel(const uint8_t *skip, int64_t n, RowList out) {
+    compact_rows(n, [&](int64_t b, int64_t &ent) { ent = b; return skip == nullptr || skip[b] == 0; }, out);
+}
+
+cudaError_t launch_select_apply(const int64_t *idx, const uint8_t *hit, int64_t n, int64_t shard_begin,
+                                int64_t shard_count, RowList out, int *err, cudaStream_t st) {
+    select_apply_kernel<<<1, 1024, 0, st>>>(idx, hit, n, shard_begin, shard_count, out, err);
+    return count_launches(1), cudaGetLastError();
+}
+
+cudaError_t launch_select_attend(const uint8_t *skip, int64_t n, RowList out, cudaStream_t st) {
+    select_attend_kernel<<<1, 1024, 0, st>>>(skip, n, out);
+    return count_launches(1), cudaGetLastError();
+}
+
+// ============================================================================================
+// search: s[b][i] = q_b . x_i (fp32 accumulation), running top-1 per query, packed-key max
+// (Alg. 1 l.255; reading R3)
+// ============================================================================================
+constexpr int kSearchQPB = 8;       // queries per CTA
+constexpr int kSearchThreads = 256;
+
+template <int DT>
+__global__ void __launch_bounds__(kSearchThreads) search_simt_kernel(const typename Elem<DT>::T *__restrict__ q,
+                                                                     const typename Elem<DT>::T *__restrict__ x,
+                                                                     int64_t B, int64_t n, int D, int64_t gbase,
+                                                                     int64_t per_block, uint64_t *keys) {
+    extern __shared__ float sq[];  // [kSearchQPB][D]
+    __shared__ unsigned long long skey[kSearchQPB];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int64_t b0 = (int64_t)blockIdx.y * kSearchQPB;
+    const int nq = (int)min64(kSearchQPB, B - b0);
+    for (int i = tid; i < kSearchQPB * D; i += blockDim.x) {
+        int qq = i / D;
+        sq[i] = qq < nq ? Elem<DT>::ld(q, (b0 + qq) * D + (i % D)) : 0.f;
+    }
+    if (tid < kSearchQPB) skey[tid] = 0ull;
+    __syncthreads();
+    const int64_t e0 = (int64_t)blockIdx.x * per_block, e1 = min64(n, e0 + per_block);
+    float best[kSearchQPB];
+    uint32_t barg[kSearchQPB];
+#pragma unroll
+    for (int qq = 0; qq < kSearchQPB; ++qq) best[qq] = -INFINITY, barg[qq] = 0xFFFFFFFFu;
+    for (int64_t e = e0 + warp; e < e1; e += nwarps) {
+        float acc[kSearchQPB];
+#pragma unroll
+        for (int qq = 0; qq < kSearchQPB; ++qq) acc[qq] = 0.f;
+        for (int k = lane; k < D; k += 32) {
+            float xv = Elem<DT>::ld(x, e * D + k);
+#pragma unroll
+            for (int qq = 0; qq < kSearchQPB; ++qq) acc[qq] = fmaf(sq[qq * D + k], xv, acc[qq]);
+        }
+#pragma unroll
+        for (int qq = 0; qq < kSearchQPB; ++qq) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) acc[qq] += __shfl_xor_sync(0xffffffffu, acc[qq], o);
+            if (acc[qq] > best[qq]) best[qq] = acc[qq], barg[qq] = (uint32_t)(gbase + e);
+        }
+    }
+    if (lane == 0) {
+        for (int qq = 0; qq < nq; ++qq)
+            if (barg[qq] != 0xFFFFFFFFu) atomicMax(&skey[qq], (unsigned long long)pack_key(best[qq], barg[qq]));
+    }
+    __syncthreads();
+    if (tid < nq && skey[tid]) atomicMax((unsigned long long *)&keys[b0 + tid], skey[tid]);
+}
+
+cudaError_t launch_search_ffma(int32_t dt, const void *q, const void *x, int64_t B, int64_t n, int32_t D,
+                               int64_t gbase, uint64_t *keys, cudaStream_t st) {
+    if (B == 0 || n == 0) return cudaSuccess;
+    const int64_t per_block = 256;
+    dim3 grid((unsigned)((n + per_block - 1) / per_block), (unsigned)((B + kSearchQPB - 1) / kSearchQPB));
+    size_t smem = sizeof(float) * kSearchQPB * D;
+    switch (dt) {
+    case ATTNCACHE_F32:
+        cudaFuncSetAttribute(search_simt_kernel<ATTNCACHE_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        search_simt_kernel<ATTNCACHE_F32><<<grid, kSearchThreads, smem, st>>>(
+            (const float *)q, (const float *)x, B, n, D, gbase, per_block, keys);
+        break;
+    case ATTNCACHE_BF16:
+        cudaFuncSetAttribute(search_simt_kernel<ATTNCACHE_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        search_simt_kernel<ATTNCACHE_BF16><<<grid, kSearchThreads, smem, st>>>(
+            (const __nv_bfloat16 *)q, (const __nv_bfloat16 *)x, B, n, D, gbase, per_block, keys);
+        break;
+    default:
+        return cudaErrorInvalidValue;
+    }
+    return count_launches(1), cudaGetLastError();
+}
+
+__global__ void keys_decode_kernel(const uint64_t *keys, int n_shards, int64_t n, float tau, int64_t *idx,
+                                   float *score, uint8_t *hit) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = 0;
+        for (int r = 0; r < n_shards; ++r) {  // cross-shard top-1: max of packed keys (reading R3)
+            uint64_t kr = keys[(int64_t)r * n + b];
+            k = kr > k ? kr : k;
+        }
+        if (k == 0) {  // no entry anywhere (empty shards)
+            idx[b] = -1;
+            score[b] = -INFINITY;
+            hit[b] = 0;
+        } else {
+            float s = ord_score((uint32_t)(k >> 32));
+            idx[b] = (int64_t)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFu));
+            score[b] = s;
+            hit[b] = s >= tau ? 1 : 0;  // inclusive gate
+        }
+    }
+}
+
+cudaError_t launch_keys_decode(const uint64_t *keys, int32_t n_shards, int64_t n, float tau, int64_t *idx, float *score,
+                               uint8_t *hit, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    int blocks = (int)min64((n + 255) / 256, 1024);
+    keys_decode_kernel<<<blocks, 256, 0, st>>>(keys, n_shards, n, tau, idx, score, hit);
+    return count_launches(1), cudaGetLastError();
+}
+
+// ============================================================================================
+// apply (CUDA cores): one warp per output row i of a unit; lanes over columns.
+//   O[i][c] = sum_{j <= i} A[i][j] V[j][c]   (entries j > i are exact zeros; reading R11)
+// ============================================================================================
+template <int MDT, int VDT>
+__global__ void __launch_bounds__(256) apply_simt_kernel(ApplyArgs a) {
+    using MT = typename Elem<MDT>::T;
+    using VT = typename Elem<VDT>::T;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t count = *a.list.count;
+    const int64_t units_per_row = (int64_t)a.n_lay * a.H;
+    const int64_t total = count * units_per_row * a.S;
+    const MT *maps = (const MT *)a.maps;
+    const VT *V = (const VT *)a.V;
+    VT *O = (VT *)a.O;
+    for (int64_t w = gw; w < total; w += nw) {
+        const int i = (int)(w % a.S);
+        const int64_t u = w / a.S;              // unit within the selected rows
+        const int64_t slot = u / units_per_row;
+        const int64_t lh = u % units_per_row;   // (layer - layer_begin) * H + h
+        const int l = (int)(lh / a.H), h = (int)(lh % a.H);
+        const int64_t row = a.list.rows[slot], ent = a.list.ents[slot];
+        const MT *A = maps + (((ent * a.L + a.layer_begin + l) * a.H + h) * a.S + i) * (int64_t)a.S;
+        const int64_t vbase = ((row * a.n_lay + l) * a.H + h) * (int64_t)a.S * a.d;
+        for (int c0 = 0; c0 < a.d; c0 += 32) {
+            const int c = c0 + lane;
+            float acc = 0.f;
+            if (c < a.d)
+                for (int j = 0; j <= i; ++j) acc = fmaf(Elem<MDT>::ld(A, j), Elem<VDT>::ld(V, vbase + (int64_t)j * a.d + c), acc);
+            if (c < a.d) Elem<VDT>::st(O, vbase + (int64_t)i * a.d + c, acc);
+        }
+    }
+}
+
+cudaError_t launch_apply_ffma(const ApplyArgs &a, int sm_count, cudaStream_t st) {
+    int blocks = sm_count * 8;
+#define AC_APPLY(MDT, VDT)                                                      \
+    if (a.map_dt == MDT && a.act_dt == VDT) {                                  \
+        apply_simt_kernel<MDT, VDT><<<blocks, 256, 0, st>>>(a);                \
+        return count_launches(1), cudaGetLastError();                                             \
+    }
+    AC_APPLY(ATTNCACHE_F16, ATTNCACHE_F32)
+    AC_APPLY(ATTNCACHE_BF16, ATTNCACHE_F32)
+    AC_APPLY(ATTNCACHE_F16, ATTNCACHE_F16)
+    AC_APPLY(ATTNCACHE_BF16, ATTNCACHE_BF16)
+#undef AC_APPLY
+    return cudaErrorInvalidValue;
+}
+
+// ============================================================================================
+// attend (CUDA cores): one warp per query row i of a unit.
+//   z_j = scale * Q_i . K_j (j <= i); p_j = exp(z_j - max); O_i = sum_j p_j V_j / sum_j p_j
+// ============================================================================================
+template <int DT>
+__global__ void __launch_bounds__(256) attend_simt_kernel(AttendArgs a) {
+    using T = typename Elem<DT>::T;
+    extern __shared__ float sp[];  // [warps][S]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float *p = sp + (int64_t)warp * a.S;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t count = *a.list.count;
+    const int64_t units_per_row = (int64_t)a.L * a.H;
+    const int64_t total = count * units_per_row * a.S;
+    const T *Q = (const T *)a.Q, *K = (const T *)a.K, *V = (const T *)a.V;
+    T *O = (T *)a.O;
+    for (int64_t w = gw; w < total; w += nw) {
+        const int i = (int)(w % a.S);
+        const int64_t u = w / a.S;
+        const int64_t slot = u / units_per_row, lh = u % units_per_row;
+        const int64_t row = a.list.rows[slot];
+        const int64_t base = (row * units_per_row + lh) * (int64_t)a.S * a.d;
+        float m = -INFINITY;
+        for (int j = lane; j <= i; j += 32) {
+            float z = 0.f;
+            for (int c = 0; c < a.d; ++c)
+                z = fmaf(Elem<DT>::ld(Q, base + (int64_t)i * a.d + c), Elem<DT>::ld(K, base + (int64_t)j * a.d + c), z);
+            z *= a.scale;
+            p[j] = z;
+            m = fmaxf(m, z);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        float sum = 0.f;
+        for (int j = lane; j <= i; j += 32) {
+            float e = expf(p[j] - m);
+            p[j] = e;
+            sum += e;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        __syncwarp();
+        const float inv = 1.f / sum;
+        for (int c = lane; c < a.d; c += 32) {
+            float acc = 0.f;
+            for (int j = 0; j <= i; ++j) acc = fmaf(p[j], Elem<DT>::ld(V, base + (int64_t)j * a.d + c), acc);
+            Elem<DT>::st(O, base + (int64_t)i * a.d + c, acc * inv);
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_attend_ffma(const AttendArgs &a, int sm_count, cudaStream_t st) {
+    int blocks = sm_count * 4;
+    size_t smem = sizeof(float) * 8 * a.S;
+#define AC_ATTEND(DT)                                                                                   \
+    if (a.dt == DT) {                                                                                  \
+        cudaFuncSetAttribute(attend_simt_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        attend_simt_kernel<DT><<<blocks, 256, smem, st>>>(a);                                         \
+        return count_launches(1), cudaGetLastError();                                                                     \
+    }
+    AC_ATTEND(ATTNCACHE_F32)
+    AC_ATTEND(ATTNCACHE_F16)
+    AC_ATTEND(ATTNCACHE_BF16)
+#undef AC_ATTEND
+    return cudaErrorInvalidValue;
+}
+
+// ============================================================================================
+// routing helpers
+// ============================================================================================
+__global__ void route_plan_kernel(const int64_t *idx, const uint8_t *hit, int64_t n, const int64_t *sb, int world,
+                                  int32_t *owner, int32_t *counts, int64_t *order) {
+    __shared__ int warp_tot[32];
+    __shared__ int base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int64_t b = tid; b < n; b += blockDim.x) {
+        int o = -1;
+        if (hit[b]) {
+            int64_t e = idx[b];
+            for (int r = 0; r < world; ++r)
+                if (e >= sb[r] && e < sb[r + 1]) o = r;
+        }
+        owner[b] = o;
+    }
+    if (tid == 0) base = 0;
+    __syncthreads();
+    for (int r = 0; r < world; ++r) {
+        int start = base;
+        for (int64_t b0 = 0; b0 < n; b0 += blockDim.x) {
+            int64_t b = b0 + tid;
+            bool sel = b < n && owner[b] == r;
+            unsigned m = __ballot_sync(0xffffffffu, sel);
+            if (lane == 0) warp_tot[warp] = __popc(m);
+            __syncthreads();
+            if (tid == 0) {
+                int run = base;
+                for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                    int t = warp_tot[w];
+                    warp_tot[w] = run;
+                    run += t;
+                }
+                base = run;
+            }
+            __syncthreads();
+            if (sel) order[warp_tot[warp] + __popc(m & ((1u << lane) - 1u))] = b;
+            __syncthreads();
+        }
+        if (tid == 0) counts[r] = base - start;
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n, const int64_t *shard_begins,
+                              int32_t world, int32_t *owner, int32_t *counts, int64_t *order, cudaStream_t st) {
+    route_plan_kernel<<<1, 1024, 0, st>>>(idx, hit, n, shard_begins, world, owner, counts, order);
+    return count_launches(1), cudaGetLastError();
+}
+
+__global__ void copy_rows_kernel(const int4 *src, const int64_t *rows, int64_t n_rows, int64_t row_words, int4 *dst,
+                                 bool gather) {
+    const int64_t total = n_rows * row_words;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t k = t / row_words, w = t % row_words;
+        int64_t r = rows[k];
+        if (gather)
+            dst[k * row_words + w] = src[r * row_words + w];
+        else
+            dst[r * row_words + w] = src[k * row_words + w];
+    }
+}
+
+cudaError_t launch_copy_rows(const void *src, const int64_t *rows, int64_t n_rows, int64_t row_bytes, void *dst,
+                             bool gather, cudaStream_t st) {
+    if (n_rows == 0) return cudaSuccess;
+    int64_t words = row_bytes / 16;
+    int blocks = (int)min64((n_rows * words + 255) / 256, 148 * 16);
+    copy_rows_kernel<<<blocks, 256, 0, st>>>((const int4 *)src, rows, n_rows, words, (int4 *)dst, gather);
+    return count_launches(1), cudaGetLastError();
+}
+
+}  // namespace ac

@@ -1,0 +1,359 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded bytes.
+
+Tolerances and the search exactness rule are in tests/_util.py (BASELINE.json north_star).
+Sizes: every config's per-entry shape (L, H, S, d, D) is exercised; small-N databases keep the
+oracle fast, and test_full_step_llama32 runs BASELINE.json configs[1] at full size in the launch
+configuration bench.py times, checking every search decision and sampled output units.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests._util import DT_NAME, check_close, check_search, storage
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def ac():
+    from paper_2510_25979_b200 import build
+    build.build()
+    import paper_2510_25979_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(ac):
+    return ac.Context(0)
+
+
+def _normed(n, D, dtype, seed):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    x = torch.randn(n, D, device=DEV, generator=g)
+    return (x / x.norm(dim=1, keepdim=True)).to(dtype)
+
+
+def _units(rows, n_lay, H):
+    """All (row, layer, head) units of the given batch rows."""
+    return [(b, l, h) for b in rows for l in range(n_lay) for h in range(H)]
+
+
+def _apply_ref(maps_np, map_dt, ents, V_np, v_dt, units, L, H, S, d, layer_begin=0, n_lay=None):
+    n_lay = L if n_lay is None else n_lay
+    a_off = [(((ents[b] * L + layer_begin + l) * H + h) * S * S) for b, l, h in units]
+    v_off = [(((b * n_lay + l) * H + h) * S * d) for b, l, h in units]
+    return oracle.apply(maps_np, map_dt, a_off, V_np, v_dt, v_off, S, d)
+
+
+def _gather_units(O, units):
+    return torch.stack([O[b, l, h] for b, l, h in units])
+
+
+# ------------------------------------------------------------------------------------------------
+# search (Alg. 1 l.255-257)
+# ------------------------------------------------------------------------------------------------
+
+def test_search_tiny_config(ac, ctx):
+    cfg = synth.CONFIGS["tiny"]
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    db = ac.Database(ctx, x)
+    q, pos, tgt = synth.queries(cfg, DEV)
+    idx, score, hit = ac.attncache_search(db, q, cfg.tau)
+    torch.cuda.synchronize()
+    check_search(q, x, idx, score, hit, cfg.tau)
+    assert hit.sum().item() == cfg.n_hit
+    assert idx[pos].cpu().tolist() == tgt.tolist()
+
+
+@pytest.mark.parametrize("cfg_name", ["llama32_1b", "llama3_8b"])
+def test_search_full_feature_db(ac, ctx, cfg_name):
+    cfg = synth.CONFIGS[cfg_name]
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    db = ac.Database(ctx, x)
+    q, pos, tgt = synth.queries(cfg, DEV)
+    idx, score, hit = ac.attncache_search(db, q, cfg.tau)
+    check_search(q, x, idx, score, hit, cfg.tau)
+    assert idx[pos].cpu().tolist() == tgt.tolist() and hit.sum().item() == cfg.n_hit
+    idx2, score2, hit2 = ac.attncache_search(db, q, cfg.tau)  # deterministic
+    assert torch.equal(idx, idx2) and torch.equal(score, score2) and torch.equal(hit, hit2)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("N,B,D", [(1000, 130, 1024), (1, 3, 384), (4097, 257, 4096)])
+def test_search_ragged_with_planted_ties(ac, ctx, dtype, N, B, D):
+    x = _normed(N, D, dtype, 11)
+    q = _normed(B, D, dtype, 12)
+    if N > 700:
+        x[700] = x[3]           # exact duplicates inside and across tiles: the lowest index wins
+        x[N - 1] = x[3]
+        q[0] = x[3]
+        q[1] = x[N - 1]
+    db = ac.Database(ctx, x)
+    idx, score, hit = ac.attncache_search(db, q, 0.9)
+    check_search(q, x, idx, score, hit, 0.9)
+    if N > 700:
+        assert idx[0].item() == 3 and idx[1].item() == 3
+
+
+def test_search_basis_ties_and_exact_threshold(ac, ctx):
+    D = 1024
+    for dtype in (torch.float32, torch.bfloat16):
+        x = torch.eye(D, device=DEV, dtype=dtype)
+        pairs = [(3, 11), (900, 2), (1023, 0), (500, 501)]
+        q = torch.zeros(len(pairs) + 1, D, device=DEV)
+        for r, (i, j) in enumerate(pairs):
+            q[r, i] = q[r, j] = 1 / math.sqrt(2)
+        q[-1, 77] = 1.0
+        db = ac.Database(ctx, x)
+        idx, score, hit = ac.attncache_search(db, q.to(dtype), 0.5)
+        assert idx.cpu().tolist() == [min(p) for p in pairs] + [77]
+        assert score[-1].item() == 1.0 and hit.all()
+        # inclusive gate at an exactly representable score (tests/golden/search_threshold.json)
+        xt = torch.zeros(2, D, device=DEV)
+        xt[1, 0], xt[1, 1] = 0.90625, math.sqrt(1 - 0.90625 ** 2)
+        xt[0, 5] = 1.0
+        db = ac.Database(ctx, xt.to(dtype))
+        e0 = torch.zeros(1, D, device=DEV, dtype=dtype)
+        e0[0, 0] = 1
+        idx, score, hit = ac.attncache_search(db, e0, 0.90625)
+        assert idx.item() == 1 and score.item() == 0.90625 and hit.item() == 1
+        _, _, hit = ac.attncache_search(db, e0, float(np.nextafter(np.float32(0.90625), np.float32(1))))
+        assert hit.item() == 0
+
+
+def test_search_errors_and_degenerate(ac, ctx):
+    x = _normed(64, 384, torch.float32, 1)
+    db = ac.Database(ctx, x)
+    q = _normed(4, 384, torch.float32, 2)
+    with pytest.raises(ac.AttnCacheError) as e:
+        ac.attncache_search(db, q, float("nan"))
+    assert e.value.name == "ATTNCACHE_ERR_INVALID_ARGUMENT"
+    _, _, hit = ac.attncache_search(db, q, 2.0)
+    assert hit.sum().item() == 0                          # tau > 1: every query misses
+    empty = ac.Database(ctx, torch.zeros(0, 384, device=DEV))
+    with pytest.raises(ac.AttnCacheError) as e:
+        ac.attncache_search(empty, q, 0.5)
+    assert e.value.name == "ATTNCACHE_ERR_EMPTY"
+    ac.attncache_search(db, q[:0], 0.5)                   # B = 0 is a no-op
+    with pytest.raises(ac.AttnCacheError) as e:
+        ac.Database(ctx, x.to(torch.float16))
+    assert e.value.name == "ATTNCACHE_ERR_DTYPE"
+
+
+def test_search_sharded_keys_equal_single_rank(ac, ctx):
+    cfg = synth.CONFIGS["llama32_1b"]
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    x[3000] = x[17]                                       # a cross-shard duplicate
+    q, _, _ = synth.queries(cfg, DEV)
+    q[5] = x[3000]
+    ref = ac.attncache_search(ac.Database(ctx, x), q, cfg.tau)
+    bounds = [0, 1000, 1001, 2500, cfg.N]                 # includes a 1-entry shard
+    keys = torch.stack([ac.attncache_search_keys(ac.Database(ctx, x[a:b], n_global=cfg.N, shard_begin=a), q)
+                        for a, b in zip(bounds, bounds[1:])])
+    got = ac.attncache_keys_decode(keys, cfg.tau)
+    for r, g in zip(ref, got):
+        assert torch.equal(r, g)
+    assert got[0][5].item() == 17
+
+
+def test_search_sweep_1m_sampled(ac, ctx):
+    cfg = synth.CONFIGS["search_sweep"]
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    db = ac.Database(ctx, x)
+    q, pos, tgt = synth.queries(cfg, DEV, B=1024)
+    idx, score, hit = ac.attncache_search(db, q, cfg.tau)
+    assert idx[pos].cpu().tolist() == tgt.tolist()        # planted hits find their entry
+    assert hit[pos].all() and hit.sum().item() == len(pos)
+    sample = torch.cat([pos[:12], torch.nonzero(hit == 0).flatten()[:12].cpu()])
+    check_search(q[sample.to(DEV)], x, idx[sample.to(DEV)], score[sample.to(DEV)], hit[sample.to(DEV)], cfg.tau)
+
+
+# ------------------------------------------------------------------------------------------------
+# apply (Alg. 2 l.373-375)
+# ------------------------------------------------------------------------------------------------
+
+def test_apply_tiny_config_all_units(ac, ctx):
+    cfg = synth.CONFIGS["tiny"]
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    maps = synth.maps(cfg, 0, cfg.N, DEV)
+    db = ac.Database(ctx, x, maps)
+    q, pos, tgt = synth.queries(cfg, DEV)
+    idx, score, hit = ac.attncache_search(db, q, cfg.tau)
+    V = synth.activations(cfg, "v", 0, cfg.B, device=DEV)
+    O = torch.full_like(V, 7.0)
+    ac.attncache_apply_cached(db, idx, V, O, hit=hit)
+    ctx.sync()
+    rows = torch.nonzero(hit).flatten().tolist()
+    miss = [b for b in range(cfg.B) if b not in rows]
+    assert torch.all(O[miss] == 7.0)                      # rows that missed are untouched
+    units = _units(rows, cfg.L, cfg.H)
+    ref = _apply_ref(storage(maps), "f16", idx.cpu().numpy(), storage(V), "f32", units, cfg.L, cfg.H, cfg.S, cfg.d)
+    check_close(_gather_units(O, units), ref, V.dtype, "apply tiny")
+
+
+@pytest.mark.parametrize("cfg_name,N,B,n_sample", [("llama32_1b", 48, 8, None), ("llama3_8b", 8, 4, 48),
+                                                    ("long_prefill", 4, 3, 12)])
+def test_apply_config_shapes(ac, ctx, cfg_name, N, B, n_sample):
+    cfg = synth.CONFIGS[cfg_name].with_(N=N)
+    x = synth.features(cfg, 0, N, DEV)
+    maps = synth.maps(cfg, 0, N, DEV)
+    db = ac.Database(ctx, x, maps)
+    idx = torch.tensor([(5 * b + 1) % N for b in range(B)], device=DEV)
+    hit = torch.tensor([1 if b % 4 != 2 else 0 for b in range(B)], device=DEV, dtype=torch.uint8)
+    V = synth.activations(cfg, "v", 0, B, device=DEV)
+    O = torch.full_like(V, 3.0)
+    ac.attncache_apply_cached(db, idx, V, O, hit=hit)
+    ctx.sync()
+    rows = torch.nonzero(hit).flatten().tolist()
+    assert torch.all(O[hit == 0] == 3.0)
+    units = _units(rows, cfg.L, cfg.H)
+    if n_sample:
+        rng = np.random.default_rng(0)
+        units = [units[i] for i in sorted(rng.choice(len(units), n_sample, replace=False))]
+        units += [(rows[-1], cfg.L - 1, cfg.H - 1)]
+    ref = _apply_ref(storage(maps), "bf16", idx.cpu().numpy(), storage(V), "bf16", units, cfg.L, cfg.H, cfg.S, cfg.d)
+    check_close(_gather_units(O, units), ref, V.dtype, f"apply {cfg_name}")
+    O2 = torch.full_like(V, 3.0)
+    ac.attncache_apply_cached(db, idx, V, O2, hit=hit)
+    assert torch.equal(O, O2)                             # bitwise deterministic
+
+
+@pytest.mark.parametrize("S,d", [(128, 64), (256, 128), (32, 64)])
+def test_apply_identity_and_one_hot_are_exact(ac, ctx, S, d):
+    L, H, N = 2, 3, 2
+    maps = torch.zeros(N, L, H, S, S, device=DEV, dtype=torch.bfloat16)
+    maps[0] = torch.eye(S, device=DEV, dtype=torch.bfloat16)
+    maps[1, ..., 0] = 1.0
+    db = ac.Database(ctx, _normed(N, 1024, torch.bfloat16, 3), maps)
+    V = torch.randn(2, L, H, S, d, device=DEV).to(torch.bfloat16)
+    O = ac.attncache_apply_cached(db, torch.tensor([0, 1], device=DEV), V)
+    torch.cuda.synchronize()
+    assert torch.equal(O[0], V[0])                        # A = I gives O = V bitwise
+    assert torch.equal(O[1], V[1, :, :, :1, :].expand(L, H, S, d))
+
+
+def test_apply_layer_slices_equal_all_layers(ac, ctx):
+    # Alg. 2 runs layer by layer; a per-layer call must equal the all-layer call bitwise (reading R13)
+    cfg = synth.CONFIGS["llama32_1b"].with_(N=6, L=4)
+    db = ac.Database(ctx, synth.features(cfg, 0, 6, DEV), synth.maps(cfg, 0, 6, DEV))
+    idx = torch.tensor([5, 0, 3], device=DEV)
+    V = synth.activations(cfg, "v", 0, 3, device=DEV)
+    O_all = ac.attncache_apply_cached(db, idx, V)
+    for l in range(cfg.L):
+        Vl = V[:, l:l + 1].contiguous()
+        Ol = ac.attncache_apply_cached(db, idx, Vl, layer_begin=l, layer_end=l + 1)
+        assert torch.equal(Ol[:, 0], O_all[:, l])
+
+
+def test_apply_out_of_shard_index_is_deferred_not_found(ac, ctx):
+    cfg = synth.CONFIGS["llama32_1b"].with_(N=4, L=1)
+    db = ac.Database(ctx, synth.features(cfg, 0, 4, DEV), synth.maps(cfg, 0, 4, DEV))
+    V = synth.activations(cfg, "v", 0, 2, device=DEV)
+    O = torch.zeros_like(V)
+    ac.attncache_apply_cached(db, torch.tensor([1, 4], device=DEV), V, O)
+    with pytest.raises(ac.AttnCacheError) as e:
+        ctx.sync()
+    assert e.value.name == "ATTNCACHE_ERR_NOT_FOUND"
+    assert torch.all(O[1] == 0) and not torch.all(O[0] == 0)
+    ctx.sync()  # cleared
+    with pytest.raises(ac.AttnCacheError) as e:
+        ac.attncache_apply_cached(db, torch.tensor([1, 2], device=DEV), V[:, :, :, :64].contiguous())
+    assert e.value.name == "ATTNCACHE_ERR_SHAPE"
+
+
+# ------------------------------------------------------------------------------------------------
+# attend (Alg. 2 l.376-381, Eq. 5)
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg_name,B,n_sample", [("tiny", 3, None), ("llama32_1b", 3, 24), ("llama3_8b", 2, 12),
+                                                 ("long_prefill", 2, 6)])
+def test_attend_config_shapes(ac, ctx, cfg_name, B, n_sample):
+    cfg = synth.CONFIGS[cfg_name]
+    Q, K, V = (synth.activations(cfg, k, 0, B, device=DEV) for k in "qkv")
+    skip = torch.zeros(B, dtype=torch.uint8, device=DEV)
+    skip[1] = 1
+    O = torch.full_like(V, 5.0)
+    ac.attncache_attend_full(ctx, Q, K, V, O, skip=skip)
+    torch.cuda.synchronize()
+    assert torch.all(O[1] == 5.0)
+    rows = [b for b in range(B) if b != 1]
+    units = _units(rows, cfg.L, cfg.H)
+    if n_sample:
+        rng = np.random.default_rng(1)
+        units = [units[i] for i in sorted(rng.choice(len(units), n_sample, replace=False))]
+    off = [(((b * cfg.L + l) * cfg.H + h) * cfg.S * cfg.d) for b, l, h in units]
+    ref = oracle.attend(storage(Q), storage(K), storage(V), DT_NAME[Q.dtype], off, cfg.S, cfg.d)
+    check_close(_gather_units(O, units), ref, V.dtype, f"attend {cfg_name}")
+
+
+@pytest.mark.parametrize("S,d", [(1, 64), (5, 64), (128, 64), (200, 128)])
+def test_attend_odd_lengths(ac, ctx, S, d):
+    Q, K, V = (torch.randn(2, 2, 2, S, d, device=DEV).to(torch.bfloat16) for _ in range(3))
+    O = ac.attncache_attend_full(ctx, Q, K, V)
+    torch.cuda.synchronize()
+    units = _units([0, 1], 2, 2)
+    off = [(((b * 2 + l) * 2 + h) * S * d) for b, l, h in units]
+    ref = oracle.attend(storage(Q), storage(K), storage(V), "bf16", off, S, d)
+    check_close(_gather_units(O, units), ref, torch.bfloat16, "attend odd")
+    if S == 1:
+        assert torch.equal(O, V)
+
+
+def test_capture_then_reuse_matches_full_attention(ac, ctx):
+    """maps captured from an input, stored as a DB entry, reproduce full attention."""
+    cfg = synth.CONFIGS["llama32_1b"].with_(N=2, L=2, H=4)
+    Q, K, V = (synth.activations(cfg, k, 0, 1, device=DEV) for k in "qkv")
+    units = _units([0], cfg.L, cfg.H)
+    off = [((l * cfg.H + h) * cfg.S * cfg.d) for _, l, h in units]
+    P = oracle.attention_map(storage(Q), storage(K), "bf16", off, cfg.S, cfg.d)  # fp64 capture
+    maps = torch.zeros(2, cfg.L, cfg.H, cfg.S, cfg.S, dtype=torch.bfloat16)
+    maps[1] = torch.from_numpy(P.reshape(cfg.L, cfg.H, cfg.S, cfg.S)).to(torch.bfloat16)
+    db = ac.Database(ctx, synth.features(cfg, 0, 2, DEV), maps.to(DEV))
+    O_reuse = ac.attncache_apply_cached(db, torch.tensor([1], device=DEV), V)
+    O_full = ac.attncache_attend_full(ctx, Q, K, V)
+    torch.cuda.synchronize()
+    ref = oracle.attend(storage(Q), storage(K), storage(V), "bf16", off, cfg.S, cfg.d)
+    check_close(O_reuse[0].reshape(-1, cfg.S, cfg.d), ref, torch.bfloat16, "reuse")
+    check_close(O_full[0].reshape(-1, cfg.S, cfg.d), ref, torch.bfloat16, "full")
+
+
+# ------------------------------------------------------------------------------------------------
+# the whole step at BASELINE.json configs[1] full size, as bench.py runs it
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.slow
+def test_full_step_llama32(ac, ctx):
+    from paper_2510_25979_b200.pipeline import PrefillStep
+    cfg = synth.CONFIGS["llama32_1b"]
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    maps = torch.empty(cfg.N, cfg.L, cfg.H, cfg.S, cfg.S, dtype=torch.bfloat16, device=DEV)
+    synth.fill_maps(cfg, maps, 0)
+    db = ac.Database(ctx, x, maps)
+    q, pos, tgt = synth.queries(cfg, DEV)
+    Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qkv")
+    O = torch.empty_like(V)
+    step = PrefillStep(ctx, db, cfg.tau)
+    idx, score, hit = step(q, Q, K, V, O)
+    ctx.sync()
+    check_search(q, x, idx, score, hit, cfg.tau)
+    assert hit.sum().item() == cfg.n_hit and idx[pos].cpu().tolist() == tgt.tolist()
+    rng = np.random.default_rng(2)
+    hits = torch.nonzero(hit).flatten().tolist()
+    misses = torch.nonzero(hit == 0).flatten().tolist()
+    hu = [(hits[i], int(rng.integers(cfg.L)), int(rng.integers(cfg.H))) for i in rng.choice(len(hits), 24)]
+    hu.append((hits[-1], cfg.L - 1, cfg.H - 1))
+    ents = idx.cpu().numpy()
+    A_np = np.stack([storage(maps[ents[b], l, h]) for b, l, h in hu]).reshape(-1)
+    v_off = [(((b * cfg.L + l) * cfg.H + h) * cfg.S * cfg.d) for b, l, h in hu]
+    Vs = storage(V)
+    ref = oracle.apply(A_np, "bf16", [u * cfg.S * cfg.S for u in range(len(hu))], Vs, "bf16", v_off, cfg.S, cfg.d)
+    check_close(_gather_units(O, hu), ref, torch.bfloat16, "step apply")
+    mu = [(misses[i], int(rng.integers(cfg.L)), int(rng.integers(cfg.H))) for i in rng.choice(len(misses), 12)]
+    off = [(((b * cfg.L + l) * cfg.H + h) * cfg.S * cfg.d) for b, l, h in mu]
+    ref = oracle.attend(storage(Q), storage(K), Vs, "bf16", off, cfg.S, cfg.d)
+    check_close(_gather_units(O, mu), ref, torch.bfloat16, "step attend")
