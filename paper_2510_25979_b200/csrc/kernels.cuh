@@ -1,5 +1,7 @@
 // kernels.cuh — host-side launchers of the device kernels (internal to libattncache).
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace ac {
@@ -58,6 +60,10 @@ struct AttendArgs {
 cudaError_t launch_attend_ffma(const AttendArgs &a, int sm_count, cudaStream_t st);
 bool attend_tc_supported(int32_t dt, int32_t S, int32_t d);
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st);
+
+// ---- TMA descriptors (tma_host.cu) ----
+cudaError_t make_tmap_2d_16(CUtensorMap *out, const void *base, bool bf16, uint64_t inner, uint64_t outer,
+                            uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
 
 // ---- routing ----
 cudaError_t launch_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n, const int64_t *shard_begins,

@@ -1,6 +1,246 @@
-// kernels_tc_apply.cu — tcgen05 A.V (placeholder until the tensor-core kernel lands).
+// kernels_tc_apply.cu — O = A . V on 5th-gen tensor cores (Alg. 2 l.373-375).
+//
+// One persistent CTA per SM walks the (hit, layer, head) units of the compacted hit list.  A unit
+// is split into 128-row blocks; row block rb needs map columns [0, 128(rb+1)) only (the maps are
+// causal: exact zeros above the diagonal, reading R11), processed as 64-column chunks.
+//
+// Roles (320 threads):
+//   warps 0-3  map loader: cp.async 16-byte pieces of the lower triangle straight from the DB
+//              (no "attention cache" copy, reading R18); pieces entirely above the diagonal are
+//              zero-filled in shared memory without touching HBM.  Writes the 128B-swizzled
+//              K-major layout tcgen05 reads.
+//   warp 4     V loader: TMA 2-D loads of V rows [64kc, 64kc+64) (128B swizzle, MN-major B).
+//   warp 5     MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128, N=d, K=16, fp32 in TMEM;
+//              owns TMEM allocation (2 accumulators: the epilogue of one row block overlaps the
+//              MMAs of the next).
+//   warps 6-9  epilogue: tcgen05.ld -> fp32 -> act dtype (RN) -> 16-byte global stores of O.
 #include "kernels.cuh"
+#include "sm100.cuh"
+
 namespace ac {
-bool apply_tc_supported(int32_t, int32_t, int32_t, int32_t) { return false; }
-cudaError_t launch_apply_tc(const ApplyArgs &, int, cudaStream_t) { return cudaErrorNotSupported; }
+using namespace sm100;
+
+namespace {
+
+constexpr int kThreads = 320;
+constexpr int kRows = 128;     // MMA M
+constexpr int kChunk = 64;     // map columns (= V rows) per pipeline stage
+constexpr int kABytes = kRows * kChunk * 2;
+
+template <int kD>
+struct Cfg {
+    static constexpr int kVBytes = kChunk * kD * 2;
+    static constexpr int kStageBytes = kABytes + kVBytes;
+    static constexpr int kStages = kD == 64 ? 8 : 6;
+    static constexpr int kLag = kStages - 2;  // cp.async groups a loader thread keeps in flight
+    static constexpr uint32_t kTmemCols = 2 * kD;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int kD>
+__global__ void __launch_bounds__(kThreads, 1)
+    apply_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ApplyArgs a, const uint32_t idesc) {
+    using C = Cfg<kD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = (uint64_t *)(smem + C::kStages * C::kStageBytes);
+    uint64_t *empty = full + C::kStages;
+    uint64_t *tfull = empty + C::kStages;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full[s], 128 + 1);  // 128 map-loader threads + the V loader's expect_tx arrival
+            mbar_init(&empty[s], 1);       // tcgen05.commit
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 4 && lane == 0) tma_prefetch_desc(&tmV);
+    if (warp == 5) tmem_alloc<C::kTmemCols>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int S = a.S;
+    const int n_rb = S / kRows;
+    const int64_t per_row = (int64_t)a.n_lay * a.H;
+    const int64_t units = (int64_t)(*a.list.count) * per_row;
+
+    if (warp < 4) {
+        // ------------------------------ map loader ------------------------------------------
+        const int tid = threadIdx.x;
+        const uint64_t policy = policy_evict_first();  // maps are read exactly once
+        const __nv_bfloat16 *maps = (const __nv_bfloat16 *)a.maps;  // 16-bit payload (bf16 or f16)
+        uint32_t cnt = 0, pending = 0;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+            const int64_t slot = u / per_row, lh = u % per_row;
+            const int l = (int)(lh / a.H), h = (int)(lh % a.H);
+            const int64_t ent = a.list.ents[slot];
+            const __nv_bfloat16 *A = maps + (((ent * a.L + a.layer_begin + l) * a.H + h) * (int64_t)S) * S;
+            for (int rb = 0; rb < n_rb; ++rb) {
+                const int n_kc = 2 * (rb + 1);
+                for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
+                    const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    const uint32_t dst = smem_u32(smem + s * C::kStageBytes);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int p = tid + 128 * j;
+                        const int r = p >> 3, c = p & 7;
+                        const int R = rb * kRows + r, col = kc * kChunk + c * 8;
+                        const bool need = col <= R;  // the piece holds at least one entry on/below the diagonal
+                        const __nv_bfloat16 *src = A + (int64_t)R * S + (need ? col : 0);
+                        cp_async_16_hint(dst + sw128_offset(r, c), src, need ? 16u : 0u, policy);
+                    }
+                    cp_async_commit();
+                    if (++pending > (uint32_t)C::kLag) {
+                        cp_async_wait<C::kLag>();
+                        fence_proxy_async_smem();
+                        mbar_arrive(&full[(cnt - C::kLag) % C::kStages]);
+                        --pending;
+                    }
+                }
+            }
+        }
+        cp_async_wait<0>();
+        fence_proxy_async_smem();
+        for (uint32_t i = cnt - pending; i < cnt; ++i) mbar_arrive(&full[i % C::kStages]);
+    } else if (warp == 4) {
+        // ------------------------------ V loader (TMA) ---------------------------------------
+        if (lane == 0) {
+            uint32_t cnt = 0;
+            for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+                const int64_t slot = u / per_row, lh = u % per_row;
+                const int64_t row = a.list.rows[slot];
+                const int32_t vrow0 = (int32_t)((row * per_row + lh) * S);
+                for (int rb = 0; rb < n_rb; ++rb) {
+                    const int n_kc = 2 * (rb + 1);
+                    for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
+                        const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
+                        mbar_wait(&empty[s], ph ^ 1u);
+                        mbar_arrive_expect_tx(&full[s], C::kVBytes);
+                        const uint32_t dst = smem_u32(smem + s * C::kStageBytes + kABytes);
+#pragma unroll
+                        for (int half = 0; half < kD / 64; ++half)
+                            tma_load_2d(dst + half * (kChunk * 128), &tmV, &full[s], half * 64, vrow0 + kc * kChunk);
+                    }
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ------------------------------ MMA issuer -------------------------------------------
+        if (lane == 0) {
+            uint32_t cnt = 0, item = 0;
+            for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+                for (int rb = 0; rb < n_rb; ++rb, ++item) {
+                    const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;
+                    mbar_wait(&tempty[acc], aph ^ 1u);
+                    tc_fence_after();
+                    const uint32_t d_tmem = tmem + acc * kD;
+                    const int n_kc = 2 * (rb + 1);
+                    for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
+                        const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
+                        mbar_wait(&full[s], ph);
+                        tc_fence_after();
+                        const uint32_t a_base = smem_u32(smem + s * C::kStageBytes);
+                        const uint32_t v_base = a_base + kABytes;
+#pragma unroll
+                        for (int k = 0; k < kChunk / 16; ++k) {
+                            // A: K-major SW128, +32 B per K=16 step inside the 128-byte row.
+                            const uint64_t ad = smem_desc(a_base + k * 32, 16, 1024, kSwizzle128B);
+                            // B (V): MN-major SW128, 16 K-rows = 2048 B per step; LBO = next 64 columns.
+                            const uint64_t bd = smem_desc(v_base + k * 2048, kChunk * 128, 1024, kSwizzle128B);
+                            umma_f16(d_tmem, ad, bd, idesc, (kc | k) != 0);
+                        }
+                        umma_commit(&empty[s]);
+                    }
+                    umma_commit(&tfull[acc]);
+                }
+            }
+        }
+    } else {
+        // ------------------------------ epilogue ---------------------------------------------
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int row_in_tile = q * 32 + lane;
+        uint32_t item = 0;
+        uint16_t *O = (uint16_t *)a.O;
+        const bool bf16 = a.act_dt == ATTNCACHE_BF16;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+            const int64_t slot = u / per_row, lh = u % per_row;
+            const int64_t row = a.list.rows[slot];
+            uint16_t *Ou = O + ((row * per_row + lh) * S) * (int64_t)kD;
+            for (int rb = 0; rb < n_rb; ++rb, ++item) {
+                const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;
+                mbar_wait(&tfull[acc], aph);
+                tc_fence_after();
+                uint32_t v[kD];
+                const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * kD;
+#pragma unroll
+                for (int cb = 0; cb < kD / 32; ++cb)
+                    tmem_ld_32x32b_x32(taddr + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[cb * 32]));
+                tmem_ld_wait();
+                tc_fence_before();
+                mbar_arrive(&tempty[acc]);
+                uint4 *dst = (uint4 *)(Ou + (int64_t)(rb * kRows + row_in_tile) * kD);
+#pragma unroll
+                for (int c8 = 0; c8 < kD / 8; ++c8) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float lo = __uint_as_float(v[c8 * 8 + 2 * e]), hi = __uint_as_float(v[c8 * 8 + 2 * e + 1]);
+                        if (bf16) {
+                            __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+                            w[e] = *reinterpret_cast<uint32_t *>(&p);
+                        } else {
+                            __half2 p = __floats2half2_rn(lo, hi);
+                            w[e] = *reinterpret_cast<uint32_t *>(&p);
+                        }
+                    }
+                    dst[c8] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc<C::kTmemCols>(tmem);
+    }
+}
+
+template <int kD>
+cudaError_t launch(const ApplyArgs &a, int sm_count, cudaStream_t st) {
+    using C = Cfg<kD>;
+    const bool bf16 = a.act_dt == ATTNCACHE_BF16;
+    const uint64_t rows = (uint64_t)a.max_rows * a.n_lay * a.H * a.S;
+    CUtensorMap tmV;
+    cudaError_t e = make_tmap_2d_16(&tmV, a.V, bf16, kD, rows, (uint64_t)kD * 2, 64, kChunk, 128);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(apply_tc_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return e;
+    const uint32_t idesc = idesc_f16(kRows, kD, bf16 ? 1u : 0u, /*a_mn=*/0u, /*b_mn=*/1u);
+    apply_tc_kernel<kD><<<sm_count, kThreads, C::kSmem, st>>>(tmV, a, idesc);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool apply_tc_supported(int32_t map_dt, int32_t act_dt, int32_t S, int32_t d) {
+    return map_dt == act_dt && (map_dt == ATTNCACHE_BF16 || map_dt == ATTNCACHE_F16) && S >= kRows && S % kRows == 0 &&
+           (d == 64 || d == 128);
+}
+
+cudaError_t launch_apply_tc(const ApplyArgs &a, int sm_count, cudaStream_t st) {
+    if ((uint64_t)a.max_rows * a.n_lay * a.H * a.S >= (1ull << 31)) return cudaErrorInvalidValue;  // TMA coordinate range
+    return a.d == 64 ? launch<64>(a, sm_count, st) : launch<128>(a, sm_count, st);
+}
+
 }  // namespace ac
