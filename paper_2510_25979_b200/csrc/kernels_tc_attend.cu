@@ -168,40 +168,95 @@ __global__ void __launch_bounds__(kThreads, 1)
                         umma_f16(d_tmem, ad, bd, idesc_s, k != 0);
                     }
                     umma_commit(&s_full[buf]);
-                    if (j > 0) issue_pv(cnt - 1);  // PV of the previous block overlaps softmax of this one
+                    // PV of the previous key block (possibly of the previous item) overlaps the
+                    // softmax of this one: the pipeline runs across item boundaries.
+                    if (cnt > 0) issue_pv(cnt - 1);
                 }
-                issue_pv(cnt - 1);
             }
+            if (cnt > 0) issue_pv(cnt - 1);
         }
     } else {
         // ------------------------------ softmax + epilogue -----------------------------------
+        // Software-pipelined over key blocks across items: P of block cnt is produced before PV of
+        // block cnt-1 is folded in, so the tensor core computes PV(cnt-1) while this warp group
+        // runs the exponentials of block cnt; an item's epilogue runs once its last PV is folded.
         const int q = warp & 3;
         const int r = q * 32 + lane;  // query row inside the block == TMEM lane
         const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
         const float sl2 = a.scale * 1.4426950408889634f;  // scale * log2(e)
         uint16_t *O = (uint16_t *)a.O;
         const bool bf16 = a.dt == ATTNCACHE_BF16;
+        float o[kD];
+#pragma unroll
+        for (int c = 0; c < kD; ++c) o[c] = 0.f;
+        float m = -INFINITY, l = 0.f;        // running stats of the item being processed
+        float alpha_pend = 1.f;              // rescale to apply when folding the pending PV
+        int64_t prev_row0 = -1;              // pending item (its last PV not yet folded)
+        int prev_qb = 0;
+        float prev_l = 0.f;
+        bool pend = false;                   // a PV (block cnt-1) is outstanding
+        bool pend_last = false;              // ... and it is the last block of its item
         uint32_t cnt = 0;
+
+        auto fold_pending = [&]() {
+            const uint32_t pbuf_idx = (cnt - 1) & 1u, pvph = ((cnt - 1) >> 1) & 1u;
+            mbar_wait(&pv_full[pbuf_idx], pvph);
+            tc_fence_after();
+            const float al = pend_last ? 1.f : alpha_pend;
+#pragma unroll
+            for (int c = 0; c < kD / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(tmem + lane_addr + 256 + pbuf_idx * kD + c * 32, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) o[c * 32 + e] = (o[c * 32 + e] + __uint_as_float(v[e])) * al;
+            }
+            tc_fence_before();
+            mbar_arrive(&pv_empty[pbuf_idx]);
+            if (pend_last) {  // epilogue of the finished item: normalise, round, store
+                const float inv = 1.f / prev_l;
+                uint4 *dst = (uint4 *)(O + (prev_row0 + prev_qb * kBlk + r) * (int64_t)kD);
+#pragma unroll
+                for (int c8 = 0; c8 < kD / 8; ++c8) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float lo = o[c8 * 8 + 2 * e] * inv, hi = o[c8 * 8 + 2 * e + 1] * inv;
+                        if (bf16) {
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
+                            w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        } else {
+                            __half2 h2 = __floats2half2_rn(lo, hi);
+                            w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        }
+                    }
+                    dst[c8] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+#pragma unroll
+                for (int c = 0; c < kD; ++c) o[c] = 0.f;
+            }
+        };
+
         for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
             int64_t row0;
             int qb;
             decode(t, row0, qb);
-            float o[kD];
-#pragma unroll
-            for (int c = 0; c < kD; ++c) o[c] = 0.f;
-            float m = -INFINITY, l = 0.f;
             for (int j = 0; j <= qb; ++j, ++cnt) {
                 const uint32_t buf = cnt & 1u, bph = (cnt >> 1) & 1u;
                 const uint32_t pb = cnt % C::kPBufs, pph = (cnt / C::kPBufs) & 1u;
                 const bool diag = j == qb;
-                const int lim = diag ? r : kBlk - 1;  // keys k <= lim are visible (causal mask)
+                const int lim = diag ? r : kBlk - 1;           // keys k <= lim are visible (causal mask)
+                const int n_chunks = diag ? q + 1 : kBlk / 32; // warp-uniform: 32-key chunks with visible keys
+                if (j == 0) {
+                    m = -INFINITY;
+                    l = 0.f;
+                }
                 mbar_wait(&s_full[buf], bph);
                 tc_fence_after();
                 const uint32_t s_addr = tmem + lane_addr + buf * kBlk;
                 // pass 1: row max of the visible scores
                 float mx = -INFINITY;
-#pragma unroll
-                for (int c = 0; c < kBlk / 32; ++c) {
+                for (int c = 0; c < n_chunks; ++c) {
                     uint32_t v[32];
                     tmem_ld_32x32b_x32(s_addr + c * 32, v);
                     tmem_ld_wait();
@@ -210,30 +265,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (c * 32 + e <= lim) mx = fmaxf(mx, __uint_as_float(v[e]));
                 }
                 const float m_new = fmaxf(m, mx * sl2);
-                // pass 2: p = exp2(s*scale*log2e - m_new), rounded to bf16, written to P (K-major SW128)
+                // pass 2: p = exp2(s*scale*log2e - m_new), rounded, written to P (K-major SW128)
                 mbar_wait(&p_empty[pb], pph ^ 1u);
                 uint8_t *prow = pbuf + pb * C::kPBytes;
                 float rs = 0.f;
 #pragma unroll
                 for (int c = 0; c < kBlk / 32; ++c) {
-                    uint32_t v[32];
-                    tmem_ld_32x32b_x32(s_addr + c * 32, v);
-                    tmem_ld_wait();
                     uint32_t w[16];
+                    if (c < n_chunks) {
+                        uint32_t v[32];
+                        tmem_ld_32x32b_x32(s_addr + c * 32, v);
+                        tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int k0 = c * 32 + 2 * e;
-                        float p0 = k0 <= lim ? ex2(fmaf(__uint_as_float(v[2 * e]), sl2, -m_new)) : 0.f;
-                        float p1 = k0 + 1 <= lim ? ex2(fmaf(__uint_as_float(v[2 * e + 1]), sl2, -m_new)) : 0.f;
-                        if (bf16) {
-                            __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                            rs += __low2float(h2) + __high2float(h2);
-                            w[e] = *reinterpret_cast<uint32_t *>(&h2);
-                        } else {
-                            __half2 h2 = __floats2half2_rn(p0, p1);
-                            rs += __low2float(h2) + __high2float(h2);
-                            w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        for (int e = 0; e < 16; ++e) {
+                            const int k0 = c * 32 + 2 * e;
+                            const float p0 = k0 <= lim ? ex2(fmaf(__uint_as_float(v[2 * e]), sl2, -m_new)) : 0.f;
+                            const float p1 = k0 + 1 <= lim ? ex2(fmaf(__uint_as_float(v[2 * e + 1]), sl2, -m_new)) : 0.f;
+                            if (bf16) {
+                                __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                                rs += __low2float(h2) + __high2float(h2);
+                                w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                            } else {
+                                __half2 h2 = __floats2half2_rn(p0, p1);
+                                rs += __low2float(h2) + __high2float(h2);
+                                w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                            }
                         }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) w[e] = 0u;
                     }
                     // columns [32c, 32c+32): chunk (32c)/64, 16-byte pieces 4*(c&1) .. +3
                     uint8_t *chunk = prow + (c >> 1) * (kBlk * 128);
@@ -246,61 +306,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_arrive(&s_empty[buf]);
                 fence_proxy_async_smem();
                 mbar_arrive(&p_full[pb]);
-                const float alpha = ex2(m - m_new);  // 0 on the first block (m = -inf)
+                const float alpha = ex2(m - m_new);  // 0 on the first block of an item (m = -inf)
                 l = l * alpha + rs;
-                if (j > 0) {
-                    // fold in PV of the previous block (relative to m), then rescale to m_new
-                    const uint32_t pbuf_idx = (cnt - 1) & 1u, pvph = ((cnt - 1) >> 1) & 1u;
-                    mbar_wait(&pv_full[pbuf_idx], pvph);
-                    tc_fence_after();
-#pragma unroll
-                    for (int c = 0; c < kD / 32; ++c) {
-                        uint32_t v[32];
-                        tmem_ld_32x32b_x32(tmem + lane_addr + 256 + pbuf_idx * kD + c * 32, v);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) o[c * 32 + e] = (o[c * 32 + e] + __uint_as_float(v[e])) * alpha;
-                    }
-                    tc_fence_before();
-                    mbar_arrive(&pv_empty[pbuf_idx]);
-                }
                 m = m_new;
-            }
-            // last block's PV, normalise, store
-            {
-                const uint32_t pbuf_idx = (cnt - 1) & 1u, pvph = ((cnt - 1) >> 1) & 1u;
-                mbar_wait(&pv_full[pbuf_idx], pvph);
-                tc_fence_after();
-#pragma unroll
-                for (int c = 0; c < kD / 32; ++c) {
-                    uint32_t v[32];
-                    tmem_ld_32x32b_x32(tmem + lane_addr + 256 + pbuf_idx * kD + c * 32, v);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) o[c * 32 + e] += __uint_as_float(v[e]);
+                // Fold the previous block's PV (the tensor core computed it while we made P): within
+                // an item it is relative to the previous max and is rescaled by this block's alpha;
+                // if it closed the previous item, that item's epilogue runs now.
+                alpha_pend = alpha;
+                if (pend) fold_pending();
+                pend = true;
+                pend_last = diag;
+                if (diag) {
+                    prev_row0 = row0;
+                    prev_qb = qb;
+                    prev_l = l;
                 }
-                tc_fence_before();
-                mbar_arrive(&pv_empty[pbuf_idx]);
-            }
-            const float inv = 1.f / l;
-            uint4 *dst = (uint4 *)(O + (row0 + qb * kBlk + r) * (int64_t)kD);
-#pragma unroll
-            for (int c8 = 0; c8 < kD / 8; ++c8) {
-                uint32_t w[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float lo = o[c8 * 8 + 2 * e] * inv, hi = o[c8 * 8 + 2 * e + 1] * inv;
-                    if (bf16) {
-                        __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
-                        w[e] = *reinterpret_cast<uint32_t *>(&h2);
-                    } else {
-                        __half2 h2 = __floats2half2_rn(lo, hi);
-                        w[e] = *reinterpret_cast<uint32_t *>(&h2);
-                    }
-                }
-                dst[c8] = make_uint4(w[0], w[1], w[2], w[3]);
             }
         }
+        if (pend) fold_pending();
     }
     __syncthreads();
     if (warp == 1) {
