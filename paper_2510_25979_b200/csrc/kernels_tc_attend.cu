@@ -2,12 +2,16 @@
 // PAPER.md:376-381; Eq. 5): O = softmax(Q K^T * scale, keys j > i masked) . V.
 //
 // Work item = (unit, 128-query block qb); it visits key blocks j = 0..qb (causal block skipping).
-// Per key block:  S_j = Q K_j^T   (tcgen05, M=128 queries, N=128 keys, K=d, fp32 in TMEM)
-//                 P_j = exp2(S_j*scale*log2e - m_j)  (online softmax, one query row per thread)
-//                 PV_j = P_j V_j   (tcgen05, M=128, N=d, K=128 keys; P staged bf16 in smem)
-//                 O   = (O + PV_{j-1}) * exp2(m_{j-1} - m_j)   (fp32 registers), O /= l at the end.
-// Roles (192 threads): warp 0 TMA loader (Q, K_j, V_j per stage), warp 1 MMA issuer + TMEM owner,
-// warps 2-5 softmax + epilogue (TMEM lane quarter = warp % 4).
+// Per key block (global block counter blk, double-buffered in TMEM):
+//   S   = Q K_j^T            tcgen05 SS, M=128 queries, N=128 keys, K=d; fp32 in TMEM cols [128b, 128b+128)
+//   P   = exp2(S*scale*log2e - m)  one query row per thread; bf16 P written back over the first 64
+//                            columns of the same S buffer (two keys per 32-bit column)
+//   PV  = P V_j              tcgen05 TS (A = P from TMEM), M=128, N=d, K=128 keys; fp32 in TMEM
+//   O   = (O + PV_prev) * exp2(m_prev - m)  in fp32 registers; O / l at the item's end.
+// The softmax of block blk overlaps the tensor core's PV of block blk-1 (software pipeline that
+// runs across item boundaries).  Q, K and V stream through separate TMA rings so Q and K slots are
+// released as soon as their S MMA retires.
+// Roles (192 threads): warp 0 TMA loader, warp 1 MMA issuer + TMEM owner, warps 2-5 softmax/epilogue.
 #include "kernels.cuh"
 #include "sm100.cuh"
 
@@ -21,13 +25,10 @@ constexpr int kBlk = 128;  // queries per item = keys per block
 
 template <int kD>
 struct Cfg {
-    static constexpr int kTile = kBlk * kD * 2;      // one [128][d] bf16 tile
-    static constexpr int kStageBytes = 3 * kTile;    // Q, K_j, V_j
-    static constexpr int kStages = kD == 64 ? 3 : 2;
-    static constexpr int kPBufs = kD == 64 ? 2 : 1;
-    static constexpr int kPBytes = kBlk * kBlk * 2;  // P tile, two 64-key chunks
-    static constexpr int kSmem = kStages * kStageBytes + kPBufs * kPBytes + 1024 + 512;
-    static constexpr uint32_t kTmemCols = 512;       // S: 2 x 128 cols, PV: 2 x d cols
+    static constexpr int kTile = kBlk * kD * 2;     // one [128][d] 16-bit tile
+    static constexpr int kRing = kD == 64 ? 4 : 2;  // slots per Q / K / V ring
+    static constexpr int kSmem = 3 * kRing * kTile + 1024 + 512;
+    static constexpr uint32_t kTmemCols = 512;      // S/P: 2 x 128 cols at 0, PV: 2 x d cols at 256
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -36,41 +37,51 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+struct Ring {
+    uint32_t slot, phase;
+};
+template <int N>
+__device__ __forceinline__ Ring ring(uint32_t i) {
+    return {i % N, (i / N) & 1u};
+}
+
 template <int kD>
 __global__ void __launch_bounds__(kThreads, 1)
     attend_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const AttendArgs a, const uint32_t idesc_s,
                      const uint32_t idesc_pv) {
     using C = Cfg<kD>;
+    constexpr int R = C::kRing;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t *pbuf = smem + C::kStages * C::kStageBytes;
-    uint64_t *bars = (uint64_t *)(pbuf + C::kPBufs * C::kPBytes);
-    uint64_t *kv_full = bars;                    // [kStages]
-    uint64_t *kv_empty = kv_full + C::kStages;   // [kStages]
-    uint64_t *s_full = kv_empty + C::kStages;    // [2]
-    uint64_t *s_empty = s_full + 2;              // [2]
-    uint64_t *p_full = s_empty + 2;              // [kPBufs]
-    uint64_t *p_empty = p_full + C::kPBufs;      // [kPBufs]
-    uint64_t *pv_full = p_empty + C::kPBufs;     // [2]
-    uint64_t *pv_empty = pv_full + 2;            // [2]
+    uint8_t *sQ = smem, *sK = smem + R * C::kTile, *sV = smem + 2 * R * C::kTile;
+    uint64_t *bars = (uint64_t *)(smem + 3 * R * C::kTile);
+    uint64_t *q_full = bars, *q_empty = q_full + R;
+    uint64_t *k_full = q_empty + R, *k_empty = k_full + R;
+    uint64_t *v_full = k_empty + R, *v_empty = v_full + R;
+    uint64_t *s_full = v_empty + R;    // [2] S computed
+    uint64_t *p_full = s_full + 2;     // [2] P written (128 threads)
+    uint64_t *s_free = p_full + 2;     // [2] the PV that read P retired: S/P buffer reusable
+    uint64_t *pv_full = s_free + 2;    // [2]
+    uint64_t *pv_empty = pv_full + 2;  // [2] (128 threads)
     uint32_t *tmem_slot = (uint32_t *)(pv_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < C::kStages; ++s) {
-            mbar_init(&kv_full[s], 1);
-            mbar_init(&kv_empty[s], 1);
+        for (int s = 0; s < R; ++s) {
+            mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], 1);
+            mbar_init(&k_full[s], 1);
+            mbar_init(&k_empty[s], 1);
+            mbar_init(&v_full[s], 1);
+            mbar_init(&v_empty[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], 128);
+            mbar_init(&p_full[i], 128);
+            mbar_init(&s_free[i], 1);
             mbar_init(&pv_full[i], 1);
             mbar_init(&pv_empty[i], 128);
-        }
-        for (int i = 0; i < C::kPBufs; ++i) {
-            mbar_init(&p_full[i], 128);
-            mbar_init(&p_empty[i], 1);
         }
         fence_barrier_init();
     }
@@ -85,101 +96,100 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    const int S = a.S;
-    const int n_qb = S / kBlk;
-    const int64_t per_row = (int64_t)a.L * a.H;
-    const int64_t units = (int64_t)(*a.list.count) * per_row;
-    const int64_t items = units * n_qb;
-    // item t -> (unit, qb): heaviest query blocks first so the persistent CTAs finish together
-    auto decode = [&](int64_t t, int64_t &unit_row0, int &qb) {
-        qb = n_qb - 1 - (int)(t / units);
-        const int64_t u = t % units;
-        const int64_t slot = u / per_row, lh = u % per_row;
-        unit_row0 = ((int64_t)a.list.rows[slot] * per_row + lh) * S;  // first [S][d] row of the unit
+    const uint32_t S = (uint32_t)a.S;
+    const uint32_t n_qb = S / kBlk;
+    const uint32_t per_row = (uint32_t)(a.L * a.H);
+    const uint32_t units = (uint32_t)(*a.list.count) * per_row;
+    const uint32_t items = units * n_qb;
+    // item t -> (unit, qb), heaviest query blocks first so the persistent CTAs finish together.
+    auto decode = [&](uint32_t t, int64_t &unit_row0, int &qb) {
+        qb = (int)(n_qb - 1 - t / units);
+        const uint32_t u = t % units;
+        unit_row0 = ((int64_t)a.list.rows[u / per_row] * per_row + u % per_row) * S;
     };
 
     if (warp == 0) {
         // ------------------------------ TMA loader -------------------------------------------
         if (lane == 0) {
-            uint32_t cnt = 0;
-            for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
+            uint32_t it = 0, blk = 0;
+            for (uint32_t t = blockIdx.x; t < items; t += gridDim.x, ++it) {
                 int64_t row0;
                 int qb;
                 decode(t, row0, qb);
-                for (int j = 0; j <= qb; ++j, ++cnt) {
-                    const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
-                    mbar_wait(&kv_empty[s], ph ^ 1u);
-                    mbar_arrive_expect_tx(&kv_full[s], C::kStageBytes);
-                    const uint32_t base = smem_u32(smem + s * C::kStageBytes);
-#pragma unroll
-                    for (int h = 0; h < kD / 64; ++h) {
-                        tma_load_2d(base + h * (kBlk * 128), &tmQ, &kv_full[s], h * 64, (int32_t)(row0 + qb * kBlk));
-                        tma_load_2d(base + C::kTile + h * (kBlk * 128), &tmK, &kv_full[s], h * 64,
-                                    (int32_t)(row0 + j * kBlk));
-                        tma_load_2d(base + 2 * C::kTile + h * (kBlk * 128), &tmV, &kv_full[s], h * 64,
-                                    (int32_t)(row0 + j * kBlk));
-                    }
+                const Ring rq = ring<R>(it);
+                mbar_wait(&q_empty[rq.slot], rq.phase ^ 1u);
+                mbar_arrive_expect_tx(&q_full[rq.slot], C::kTile);
+                for (int h = 0; h < kD / 64; ++h)
+                    tma_load_2d(smem_u32(sQ + rq.slot * C::kTile + h * (kBlk * 128)), &tmQ, &q_full[rq.slot], h * 64,
+                                (int32_t)(row0 + qb * kBlk));
+                for (int j = 0; j <= qb; ++j, ++blk) {
+                    const Ring rk = ring<R>(blk);
+                    mbar_wait(&k_empty[rk.slot], rk.phase ^ 1u);
+                    mbar_arrive_expect_tx(&k_full[rk.slot], C::kTile);
+                    for (int h = 0; h < kD / 64; ++h)
+                        tma_load_2d(smem_u32(sK + rk.slot * C::kTile + h * (kBlk * 128)), &tmK, &k_full[rk.slot],
+                                    h * 64, (int32_t)(row0 + j * kBlk));
+                    mbar_wait(&v_empty[rk.slot], rk.phase ^ 1u);
+                    mbar_arrive_expect_tx(&v_full[rk.slot], C::kTile);
+                    for (int h = 0; h < kD / 64; ++h)
+                        tma_load_2d(smem_u32(sV + rk.slot * C::kTile + h * (kBlk * 128)), &tmV, &v_full[rk.slot],
+                                    h * 64, (int32_t)(row0 + j * kBlk));
                 }
             }
         }
     } else if (warp == 1) {
         // ------------------------------ MMA issuer -------------------------------------------
         if (lane == 0) {
-            uint32_t cnt = 0;   // key blocks over all items (stage ring, S/PV double buffers)
             auto issue_pv = [&](uint32_t c) {
-                const uint32_t s = c % C::kStages;
-                const uint32_t pb = c % C::kPBufs, pph = (c / C::kPBufs) & 1u;
+                const Ring rv = ring<R>(c);
                 const uint32_t buf = c & 1u, bph = (c >> 1) & 1u;
-                mbar_wait(&p_full[pb], pph);
+                mbar_wait(&p_full[buf], bph);
+                mbar_wait(&v_full[rv.slot], rv.phase);
                 mbar_wait(&pv_empty[buf], bph ^ 1u);
                 tc_fence_after();
-                const uint32_t p_base = smem_u32(pbuf + pb * C::kPBytes);
-                const uint32_t v_base = smem_u32(smem + s * C::kStageBytes + 2 * C::kTile);
+                const uint32_t v_base = smem_u32(sV + rv.slot * C::kTile);
                 const uint32_t d_tmem = tmem + 256 + buf * kD;
 #pragma unroll
                 for (int k = 0; k < kBlk / 16; ++k) {
-                    // P: K-major SW128, two 64-key chunks of 16 KB; V: MN-major SW128, 16 rows per step.
-                    const uint64_t ad = smem_desc(p_base + (k >> 2) * (kBlk * 128) + (k & 3) * 32, 16, 1024, kSwizzle128B);
+                    // A = P in TMEM (8 columns = 16 keys per step); B = V, MN-major SW128, 16 rows per step
                     const uint64_t bd = smem_desc(v_base + k * 2048, kBlk * 128, 1024, kSwizzle128B);
-                    umma_f16(d_tmem, ad, bd, idesc_pv, k != 0);
+                    umma_f16_ts(d_tmem, tmem + buf * kBlk + k * 8, bd, idesc_pv, k != 0);
                 }
                 umma_commit(&pv_full[buf]);
-                umma_commit(&p_empty[pb]);
-                umma_commit(&kv_empty[s]);
+                umma_commit(&v_empty[rv.slot]);
+                umma_commit(&s_free[buf]);
             };
-            for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
+            uint32_t it = 0, blk = 0;
+            for (uint32_t t = blockIdx.x; t < items; t += gridDim.x, ++it) {
                 int64_t row0;
                 int qb;
                 decode(t, row0, qb);
-                for (int j = 0; j <= qb; ++j, ++cnt) {
-                    const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
-                    const uint32_t buf = cnt & 1u, bph = (cnt >> 1) & 1u;
-                    mbar_wait(&kv_full[s], ph);
-                    mbar_wait(&s_empty[buf], bph ^ 1u);
+                const Ring rq = ring<R>(it);
+                mbar_wait(&q_full[rq.slot], rq.phase);
+                const uint32_t q_base = smem_u32(sQ + rq.slot * C::kTile);
+                for (int j = 0; j <= qb; ++j, ++blk) {
+                    const Ring rk = ring<R>(blk);
+                    const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
+                    mbar_wait(&k_full[rk.slot], rk.phase);
+                    mbar_wait(&s_free[buf], bph ^ 1u);
                     tc_fence_after();
-                    const uint32_t q_base = smem_u32(smem + s * C::kStageBytes);
-                    const uint32_t k_base = q_base + C::kTile;
-                    const uint32_t d_tmem = tmem + buf * kBlk;
+                    const uint32_t k_base = smem_u32(sK + rk.slot * C::kTile);
 #pragma unroll
                     for (int k = 0; k < kD / 16; ++k) {
                         const uint32_t off = (k >> 2) * (kBlk * 128) + (k & 3) * 32;
-                        const uint64_t ad = smem_desc(q_base + off, 16, 1024, kSwizzle128B);
-                        const uint64_t bd = smem_desc(k_base + off, 16, 1024, kSwizzle128B);
-                        umma_f16(d_tmem, ad, bd, idesc_s, k != 0);
+                        umma_f16(tmem + buf * kBlk, smem_desc(q_base + off, 16, 1024, kSwizzle128B),
+                                 smem_desc(k_base + off, 16, 1024, kSwizzle128B), idesc_s, k != 0);
                     }
                     umma_commit(&s_full[buf]);
-                    // PV of the previous key block (possibly of the previous item) overlaps the
-                    // softmax of this one: the pipeline runs across item boundaries.
-                    if (cnt > 0) issue_pv(cnt - 1);
+                    umma_commit(&k_empty[rk.slot]);
+                    if (j == qb) umma_commit(&q_empty[rq.slot]);
+                    if (blk > 0) issue_pv(blk - 1);
                 }
             }
-            if (cnt > 0) issue_pv(cnt - 1);
+            if (blk > 0) issue_pv(blk - 1);
         }
     } else {
         // ------------------------------ softmax + epilogue -----------------------------------
-        // Software-pipelined over key blocks across items: P of block cnt is produced before PV of
-        // block cnt-1 is folded in, so the tensor core computes PV(cnt-1) while this warp group
-        // runs the exponentials of block cnt; an item's epilogue runs once its last PV is folded.
         const int q = warp & 3;
         const int r = q * 32 + lane;  // query row inside the block == TMEM lane
         const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
@@ -189,31 +199,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         float o[kD];
 #pragma unroll
         for (int c = 0; c < kD; ++c) o[c] = 0.f;
-        float m = -INFINITY, l = 0.f;        // running stats of the item being processed
-        float alpha_pend = 1.f;              // rescale to apply when folding the pending PV
-        int64_t prev_row0 = -1;              // pending item (its last PV not yet folded)
+        float m = -INFINITY, l = 0.f;  // running statistics of the current item
+        int64_t prev_row0 = 0;         // item whose last PV is pending
         int prev_qb = 0;
-        float prev_l = 0.f;
-        bool pend = false;                   // a PV (block cnt-1) is outstanding
-        bool pend_last = false;              // ... and it is the last block of its item
-        uint32_t cnt = 0;
+        float prev_l = 1.f;
+        float alpha = 1.f;
+        bool pend = false, pend_last = false;
+        uint32_t blk = 0;
 
+        // Folds PV of block blk-1 into o (rescaled by `alpha` unless it closed its item; then the
+        // item's epilogue normalises, rounds and stores O and o restarts from zero).
         auto fold_pending = [&]() {
-            const uint32_t pbuf_idx = (cnt - 1) & 1u, pvph = ((cnt - 1) >> 1) & 1u;
-            mbar_wait(&pv_full[pbuf_idx], pvph);
+            const uint32_t pb = (blk - 1) & 1u, pph = ((blk - 1) >> 1) & 1u;
+            mbar_wait(&pv_full[pb], pph);
             tc_fence_after();
-            const float al = pend_last ? 1.f : alpha_pend;
+            const float al = pend_last ? 1.f : alpha;
 #pragma unroll
             for (int c = 0; c < kD / 32; ++c) {
                 uint32_t v[32];
-                tmem_ld_32x32b_x32(tmem + lane_addr + 256 + pbuf_idx * kD + c * 32, v);
+                tmem_ld_32x32b_x32(tmem + lane_addr + 256 + pb * kD + c * 32, v);
                 tmem_ld_wait();
 #pragma unroll
                 for (int e = 0; e < 32; ++e) o[c * 32 + e] = (o[c * 32 + e] + __uint_as_float(v[e])) * al;
             }
             tc_fence_before();
-            mbar_arrive(&pv_empty[pbuf_idx]);
-            if (pend_last) {  // epilogue of the finished item: normalise, round, store
+            mbar_arrive(&pv_empty[pb]);
+            if (pend_last) {
                 const float inv = 1.f / prev_l;
                 uint4 *dst = (uint4 *)(O + (prev_row0 + prev_qb * kBlk + r) * (int64_t)kD);
 #pragma unroll
@@ -237,24 +248,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         };
 
-        for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
+        for (uint32_t t = blockIdx.x; t < items; t += gridDim.x) {
             int64_t row0;
             int qb;
             decode(t, row0, qb);
-            for (int j = 0; j <= qb; ++j, ++cnt) {
-                const uint32_t buf = cnt & 1u, bph = (cnt >> 1) & 1u;
-                const uint32_t pb = cnt % C::kPBufs, pph = (cnt / C::kPBufs) & 1u;
+            m = -INFINITY;
+            l = 0.f;
+            for (int j = 0; j <= qb; ++j, ++blk) {
+                const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
                 const bool diag = j == qb;
-                const int lim = diag ? r : kBlk - 1;           // keys k <= lim are visible (causal mask)
-                const int n_chunks = diag ? q + 1 : kBlk / 32; // warp-uniform: 32-key chunks with visible keys
-                if (j == 0) {
-                    m = -INFINITY;
-                    l = 0.f;
-                }
+                const int lim = diag ? r : kBlk - 1;            // keys k <= lim are visible (causal mask)
+                const int n_chunks = diag ? q + 1 : kBlk / 32;  // warp-uniform: 32-key chunks with visible keys
                 mbar_wait(&s_full[buf], bph);
                 tc_fence_after();
                 const uint32_t s_addr = tmem + lane_addr + buf * kBlk;
-                // pass 1: row max of the visible scores
                 float mx = -INFINITY;
                 for (int c = 0; c < n_chunks; ++c) {
                     uint32_t v[32];
@@ -265,9 +272,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (c * 32 + e <= lim) mx = fmaxf(mx, __uint_as_float(v[e]));
                 }
                 const float m_new = fmaxf(m, mx * sl2);
-                // pass 2: p = exp2(s*scale*log2e - m_new), rounded, written to P (K-major SW128)
-                mbar_wait(&p_empty[pb], pph ^ 1u);
-                uint8_t *prow = pbuf + pb * C::kPBytes;
                 float rs = 0.f;
 #pragma unroll
                 for (int c = 0; c < kBlk / 32; ++c) {
@@ -295,24 +299,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int e = 0; e < 16; ++e) w[e] = 0u;
                     }
-                    // columns [32c, 32c+32): chunk (32c)/64, 16-byte pieces 4*(c&1) .. +3
-                    uint8_t *chunk = prow + (c >> 1) * (kBlk * 128);
-#pragma unroll
-                    for (int pc = 0; pc < 4; ++pc)
-                        *reinterpret_cast<uint4 *>(chunk + sw128_offset(r, (c & 1) * 4 + pc)) =
-                            make_uint4(w[4 * pc], w[4 * pc + 1], w[4 * pc + 2], w[4 * pc + 3]);
+                    // keys [32c, 32c+32) -> P columns [16c, 16c+16) (already read as S chunk c/2 <= c)
+                    tmem_st_32x32b_x16(s_addr + c * 16, w);
                 }
+                tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(&s_empty[buf]);
-                fence_proxy_async_smem();
-                mbar_arrive(&p_full[pb]);
-                const float alpha = ex2(m - m_new);  // 0 on the first block of an item (m = -inf)
+                mbar_arrive(&p_full[buf]);
+                alpha = ex2(m - m_new);  // 0 on an item's first block (m = -inf)
                 l = l * alpha + rs;
                 m = m_new;
-                // Fold the previous block's PV (the tensor core computed it while we made P): within
-                // an item it is relative to the previous max and is rescaled by this block's alpha;
-                // if it closed the previous item, that item's epilogue runs now.
-                alpha_pend = alpha;
                 if (pend) fold_pending();
                 pend = true;
                 pend_last = diag;
@@ -345,8 +340,8 @@ cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
     e = cudaFuncSetAttribute(attend_tc_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     const uint32_t fmt = bf16 ? 1u : 0u;
-    const uint32_t idesc_s = idesc_f16(kBlk, kBlk, fmt, 0u, 0u);   // Q K-major x K K-major
-    const uint32_t idesc_pv = idesc_f16(kBlk, kD, fmt, 0u, 1u);    // P K-major x V MN-major
+    const uint32_t idesc_s = idesc_f16(kBlk, kBlk, fmt, 0u, 0u);  // Q K-major x K K-major
+    const uint32_t idesc_pv = idesc_f16(kBlk, kD, fmt, 0u, 1u);   // P (TMEM) x V MN-major
     attend_tc_kernel<kD><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, tv, a, idesc_s, idesc_pv);
     count_launches(1);
     return cudaGetLastError();
@@ -359,7 +354,9 @@ bool attend_tc_supported(int32_t dt, int32_t S, int32_t d) {
 }
 
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st) {
-    if ((uint64_t)a.max_rows * a.L * a.H * a.S >= (1ull << 31)) return cudaErrorInvalidValue;
+    const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
+    if (rows >= (1ull << 31) || (uint64_t)a.max_rows * a.L * a.H * (a.S / kBlk) >= (1ull << 32))
+        return cudaErrorInvalidValue;
     return a.d == 64 ? launch<64>(a, sm_count, st) : launch<128>(a, sm_count, st);
 }
 
