@@ -37,6 +37,38 @@ struct Cfg {
     static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// Walks this CTA's units u = blockIdx.x, +gridDim.x, ... of the compacted hit list.  The hit-list
+// entry (batch row and/or DB entry) of the next unit is loaded one unit ahead so its latency hides
+// behind the current unit instead of stalling the pipeline once per unit.
+template <bool kRow, bool kEnt>
+struct UnitIter {
+    uint32_t u, stride, units, per_row;
+    const int32_t *rows;
+    const int64_t *ents;
+    int32_t next_row = 0;
+    int64_t next_ent = 0;
+    __device__ UnitIter(uint32_t first, uint32_t stride_, uint32_t units_, uint32_t per_row_, const RowList &l)
+        : u(first), stride(stride_), units(units_), per_row(per_row_), rows(l.rows), ents(l.ents) {
+        fetch();
+    }
+    __device__ __forceinline__ void fetch() {
+        if (u < units) {
+            if (kRow) next_row = rows[u / per_row];
+            if (kEnt) next_ent = ents[u / per_row];
+        }
+    }
+    // lh = (layer - layer_begin) * H + head of the unit
+    __device__ __forceinline__ bool next(uint32_t &lh, int64_t &row, int64_t &ent) {
+        if (u >= units) return false;
+        lh = u % per_row;
+        row = next_row;
+        ent = next_ent;
+        u += stride;
+        fetch();
+        return true;
+    }
+};
+
 template <int kD>
 __global__ void __launch_bounds__(kThreads, 1)
     apply_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ApplyArgs a, const uint32_t idesc) {
@@ -70,8 +102,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int S = a.S;
     const int n_rb = S / kRows;
-    const int64_t per_row = (int64_t)a.n_lay * a.H;
-    const int64_t units = (int64_t)(*a.list.count) * per_row;
+    const uint32_t per_row = (uint32_t)(a.n_lay * a.H);
+    const uint32_t units = (uint32_t)(*a.list.count) * per_row;
 
     if (warp < 4) {
         // ------------------------------ map loader ------------------------------------------
@@ -79,10 +111,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t policy = policy_evict_first();  // maps are read exactly once
         const __nv_bfloat16 *maps = (const __nv_bfloat16 *)a.maps;  // 16-bit payload (bf16 or f16)
         uint32_t cnt = 0, pending = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-            const int64_t slot = u / per_row, lh = u % per_row;
+        UnitIter<false, true> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
+        uint32_t lh;
+        int64_t row, ent;
+        while (iter.next(lh, row, ent)) {
             const int l = (int)(lh / a.H), h = (int)(lh % a.H);
-            const int64_t ent = a.list.ents[slot];
             const __nv_bfloat16 *A = maps + (((ent * a.L + a.layer_begin + l) * a.H + h) * (int64_t)S) * S;
             for (int rb = 0; rb < n_rb; ++rb) {
                 const int n_kc = 2 * (rb + 1);
@@ -116,9 +149,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------ V loader (TMA) ---------------------------------------
         if (lane == 0) {
             uint32_t cnt = 0;
-            for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-                const int64_t slot = u / per_row, lh = u % per_row;
-                const int64_t row = a.list.rows[slot];
+            UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
+            uint32_t lh;
+            int64_t row, ent;
+            while (iter.next(lh, row, ent)) {
                 const int32_t vrow0 = (int32_t)((row * per_row + lh) * S);
                 for (int rb = 0; rb < n_rb; ++rb) {
                     const int n_kc = 2 * (rb + 1);
@@ -138,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------ MMA issuer -------------------------------------------
         if (lane == 0) {
             uint32_t cnt = 0, item = 0;
-            for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+            for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
                 for (int rb = 0; rb < n_rb; ++rb, ++item) {
                     const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;
                     mbar_wait(&tempty[acc], aph ^ 1u);
@@ -172,9 +206,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t item = 0;
         uint16_t *O = (uint16_t *)a.O;
         const bool bf16 = a.act_dt == ATTNCACHE_BF16;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-            const int64_t slot = u / per_row, lh = u % per_row;
-            const int64_t row = a.list.rows[slot];
+        UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
+        uint32_t lh;
+        int64_t row, ent;
+        while (iter.next(lh, row, ent)) {
             uint16_t *Ou = O + ((row * per_row + lh) * S) * (int64_t)kD;
             for (int rb = 0; rb < n_rb; ++rb, ++item) {
                 const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;

@@ -23,12 +23,19 @@ namespace {
 constexpr int kThreads = 192;
 constexpr int kBlk = 128;  // queries per item = keys per block
 
-template <int kD>
+// kTwoCTA: two co-resident CTAs per SM (d = 64), each with one S/P buffer, 2-slot rings and 256 TMEM
+// columns, so one CTA's softmax latency hides behind the other's; else one CTA per SM with
+// double-buffered S/P.
+template <int kD, bool kTwoCTA>
 struct Cfg {
-    static constexpr int kTile = kBlk * kD * 2;     // one [128][d] 16-bit tile
-    static constexpr int kRing = kD == 64 ? 4 : 2;  // slots per Q / K / V ring
+    static constexpr int kTile = kBlk * kD * 2;                          // one [128][d] 16-bit tile
+    static constexpr int kRing = kTwoCTA ? 2 : (kD == 64 ? 4 : 2);      // slots per Q / K / V ring
+    static constexpr int kSBufs = kTwoCTA ? 1 : 2;                       // S/P buffers (128 cols each)
+    static constexpr uint32_t kPVBase = 128 * kSBufs;                    // PV: 2 x d columns
+    static constexpr uint32_t kTmemCols = kTwoCTA ? 256 : 512;
+    static constexpr int kMinBlocks = kTwoCTA ? 2 : 1;
     static constexpr int kSmem = 3 * kRing * kTile + 1024 + 512;
-    static constexpr uint32_t kTmemCols = 512;      // S/P: 2 x 128 cols at 0, PV: 2 x d cols at 256
+    static_assert(kPVBase + 2 * kD <= kTmemCols, "TMEM budget");
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -45,13 +52,14 @@ __device__ __forceinline__ Ring ring(uint32_t i) {
     return {i % N, (i / N) & 1u};
 }
 
-template <int kD>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int kD, bool kTwoCTA>
+__global__ void __launch_bounds__(kThreads, Cfg<kD, kTwoCTA>::kMinBlocks)
     attend_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const AttendArgs a, const uint32_t idesc_s,
                      const uint32_t idesc_pv) {
-    using C = Cfg<kD>;
+    using C = Cfg<kD, kTwoCTA>;
     constexpr int R = C::kRing;
+    constexpr int NS = C::kSBufs;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sQ = smem, *sK = smem + R * C::kTile, *sV = smem + 2 * R * C::kTile;
@@ -142,22 +150,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             auto issue_pv = [&](uint32_t c) {
                 const Ring rv = ring<R>(c);
-                const uint32_t buf = c & 1u, bph = (c >> 1) & 1u;
-                mbar_wait(&p_full[buf], bph);
+                const Ring rs = ring<NS>(c);                        // S/P buffer
+                const uint32_t buf = c & 1u, bph = (c >> 1) & 1u;   // PV buffer
+                mbar_wait(&p_full[rs.slot], rs.phase);
                 mbar_wait(&v_full[rv.slot], rv.phase);
                 mbar_wait(&pv_empty[buf], bph ^ 1u);
                 tc_fence_after();
                 const uint32_t v_base = smem_u32(sV + rv.slot * C::kTile);
-                const uint32_t d_tmem = tmem + 256 + buf * kD;
+                const uint32_t d_tmem = tmem + C::kPVBase + buf * kD;
 #pragma unroll
                 for (int k = 0; k < kBlk / 16; ++k) {
                     // A = P in TMEM (8 columns = 16 keys per step); B = V, MN-major SW128, 16 rows per step
                     const uint64_t bd = smem_desc(v_base + k * 2048, kBlk * 128, 1024, kSwizzle128B);
-                    umma_f16_ts(d_tmem, tmem + buf * kBlk + k * 8, bd, idesc_pv, k != 0);
+                    umma_f16_ts(d_tmem, tmem + rs.slot * kBlk + k * 8, bd, idesc_pv, k != 0);
                 }
                 umma_commit(&pv_full[buf]);
                 umma_commit(&v_empty[rv.slot]);
-                umma_commit(&s_free[buf]);
+                umma_commit(&s_free[rs.slot]);
             };
             uint32_t it = 0, blk = 0;
             for (uint32_t t = blockIdx.x; t < items; t += gridDim.x, ++it) {
@@ -169,9 +178,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t q_base = smem_u32(sQ + rq.slot * C::kTile);
                 for (int j = 0; j <= qb; ++j, ++blk) {
                     const Ring rk = ring<R>(blk);
-                    const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
+                    const Ring rs = ring<NS>(blk);
+                    const uint32_t buf = rs.slot;
+                    // With one S/P buffer, S(blk) reuses the buffer PV(blk-1) reads: issue PV first.
+                    if (NS == 1 && blk > 0) issue_pv(blk - 1);
                     mbar_wait(&k_full[rk.slot], rk.phase);
-                    mbar_wait(&s_free[buf], bph ^ 1u);
+                    mbar_wait(&s_free[buf], rs.phase ^ 1u);
                     tc_fence_after();
                     const uint32_t k_base = smem_u32(sK + rk.slot * C::kTile);
 #pragma unroll
@@ -183,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     umma_commit(&s_full[buf]);
                     umma_commit(&k_empty[rk.slot]);
                     if (j == qb) umma_commit(&q_empty[rq.slot]);
-                    if (blk > 0) issue_pv(blk - 1);
+                    if (NS > 1 && blk > 0) issue_pv(blk - 1);
                 }
             }
             if (blk > 0) issue_pv(blk - 1);
@@ -217,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < kD / 32; ++c) {
                 uint32_t v[32];
-                tmem_ld_32x32b_x32(tmem + lane_addr + 256 + pb * kD + c * 32, v);
+                tmem_ld_32x32b_x32(tmem + lane_addr + C::kPVBase + pb * kD + c * 32, v);
                 tmem_ld_wait();
 #pragma unroll
                 for (int e = 0; e < 32; ++e) o[c * 32 + e] = (o[c * 32 + e] + __uint_as_float(v[e])) * al;
@@ -255,7 +267,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             m = -INFINITY;
             l = 0.f;
             for (int j = 0; j <= qb; ++j, ++blk) {
-                const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
+                const Ring rsb = ring<NS>(blk);
+                const uint32_t buf = rsb.slot, bph = rsb.phase;
                 const bool diag = j == qb;
                 const int lim = diag ? r : kBlk - 1;            // keys k <= lim are visible (causal mask)
                 const int n_chunks = diag ? q + 1 : kBlk / 32;  // warp-uniform: 32-key chunks with visible keys
@@ -327,9 +340,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int kD>
+template <int kD, bool kTwoCTA>
 cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
-    using C = Cfg<kD>;
+    using C = Cfg<kD, kTwoCTA>;
     const bool bf16 = a.dt == ATTNCACHE_BF16;
     const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
     CUtensorMap tq, tk, tv;
@@ -337,12 +350,12 @@ cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
     if (e == cudaSuccess) e = make_tmap_2d_16(&tk, a.K, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e == cudaSuccess) e = make_tmap_2d_16(&tv, a.V, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(attend_tc_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    e = cudaFuncSetAttribute(attend_tc_kernel<kD, kTwoCTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     const uint32_t fmt = bf16 ? 1u : 0u;
     const uint32_t idesc_s = idesc_f16(kBlk, kBlk, fmt, 0u, 0u);  // Q K-major x K K-major
     const uint32_t idesc_pv = idesc_f16(kBlk, kD, fmt, 0u, 1u);   // P (TMEM) x V MN-major
-    attend_tc_kernel<kD><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, tv, a, idesc_s, idesc_pv);
+    attend_tc_kernel<kD, kTwoCTA><<<sm_count * C::kMinBlocks, kThreads, C::kSmem, st>>>(tq, tk, tv, a, idesc_s, idesc_pv);
     count_launches(1);
     return cudaGetLastError();
 }
@@ -357,7 +370,7 @@ cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st)
     const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
     if (rows >= (1ull << 31) || (uint64_t)a.max_rows * a.L * a.H * (a.S / kBlk) >= (1ull << 32))
         return cudaErrorInvalidValue;
-    return a.d == 64 ? launch<64>(a, sm_count, st) : launch<128>(a, sm_count, st);
+    return a.d == 64 ? launch<64, true>(a, sm_count, st) : launch<128, false>(a, sm_count, st);
 }
 
 }  // namespace ac
