@@ -203,9 +203,10 @@ def run_ours(args, cfg):
 
     # ---- inputs resident in HBM (untimed) ----
     x = synth.features(cfg, 0, cfg.N, dev)
-    maps = torch.empty(cfg.N, cfg.L, cfg.H, cfg.S, cfg.S, dtype=synth.torch_dtype(cfg.map_dtype), device=dev)
-    synth.fill_maps(cfg, maps, 0)
-    db = ac.Database(ctx, x, maps)
+    # DB building (Fig. 4 step 3): the generator's dense maps are stored in the PACKED layout
+    maps = ac.pack_db_maps(lambda b, out: synth.fill_maps(cfg, out, b), cfg.N, cfg.L, cfg.H, cfg.S,
+                           synth.torch_dtype(cfg.map_dtype), dev, chunk=max(1, (1 << 30) // cfg.map_bytes_per_entry))
+    db = ac.Database(ctx, x, maps, packed=True, seq_len=cfg.S)
     q, _, _ = synth.queries(cfg, dev)
     Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=dev) for k in "qkv")
     O = torch.empty_like(V)

@@ -52,6 +52,17 @@ typedef enum {
 
 typedef enum { ATTNCACHE_F32 = 0, ATTNCACHE_F16 = 1, ATTNCACHE_BF16 = 2 } attncache_dtype;
 
+/* Storage layout of one S x S causal map (see attncache_db_desc):
+ *  DENSE  — the full square, row-major, exact +0.0 above the diagonal (S*S elements).
+ *  PACKED — the lower triangle only, row-major, row i holding its first 8*(i/8 + 1) elements
+ *           (whole 16-byte pieces; entries j > i inside the last piece are the dense map's
+ *           +0.0), rows back to back:  row i starts at element 8*(4q(q+1) + r(q+1)) with
+ *           q = i / 8, r = i % 8, and a map occupies attncache_packed_map_elems(S) elements.
+ *           Requires S % 8 == 0.  It holds exactly the bytes A.V reads (about half of DENSE), so
+ *           HBM traffic and DB capacity both halve; attncache_pack_maps builds it (DB building,
+ *           Fig. 4 step 3 "store"). */
+typedef enum { ATTNCACHE_MAPS_DENSE = 0, ATTNCACHE_MAPS_PACKED = 1 } attncache_map_layout;
+
 typedef struct attncache_ctx attncache_ctx; /* per process and device: scratch + deferred errors */
 typedef struct attncache_db attncache_db;   /* this rank's shard view of the memoization database */
 
@@ -82,8 +93,9 @@ attncache_status attncache_ctx_sync(attncache_ctx *ctx);
  * keeps them alive and unmodified until attncache_db_free.
  *   feats: [shard_count][feat_dim] in feat_dtype (F32 or BF16), rows L2-normalised by the
  *          producer (reading R2: the library never renormalises).
- *   maps : [shard_count][n_layers][n_heads][seq_len][seq_len] in map_dtype (F16 or BF16):
- *          post-softmax causal maps, exact +0.0 above the diagonal (reading R11) — layer-
+ *   maps : [shard_count][n_layers][n_heads][map] in map_dtype (F16 or BF16) where each map is
+ *          one post-softmax causal S x S map in `map_layout` (DENSE: S*S elements, exact +0.0
+ *          above the diagonal, reading R11; PACKED: see attncache_map_layout) — layer-
  *          contiguous per entry and head-major inside a layer.  May be NULL
  *          for a search-only database (n_layers = n_heads = seq_len = 0).
  * Errors: INVALID_ARGUMENT (ranges, null feats with shard_count > 0, n_global >= 2^32),
@@ -100,6 +112,7 @@ typedef struct {
     int32_t seq_len;
     int32_t map_dtype; /* attncache_dtype */
     const void *maps;
+    int32_t map_layout; /* attncache_map_layout */
 } attncache_db_desc;
 
 attncache_status attncache_db_load(attncache_ctx *ctx, const attncache_db_desc *desc, attncache_db **out);
@@ -178,9 +191,18 @@ attncache_status attncache_gather_rows(const void *src, const int64_t *rows, int
 attncache_status attncache_scatter_rows(const void *src, const int64_t *rows, int64_t n_rows, int64_t row_bytes,
                                         void *dst, void *stream);
 
+/* ---- DB building: packed map layout (Fig. 4 step 3) -----------
+ * Number of elements one PACKED S x S map occupies (0 if S % 8 != 0). */
+int64_t attncache_packed_map_elems(int32_t seq_len);
+/* Converts n_maps DENSE S x S maps (16-bit elements, device) into the PACKED layout (device,
+ * n_maps * attncache_packed_map_elems(S) elements).  Pure data movement: the packed map holds the
+ * dense map's bytes for every j <= i.  Errors: SHAPE (S % 8 != 0), ALIGNMENT. */
+attncache_status attncache_pack_maps(const void *dense, int64_t n_maps, int32_t seq_len, void *packed, void *stream);
+
 /* ---- test/debug: literal AttnMapsDB.get(idx, n) (Alg. 1 l.259) ------------
- * Copies maps[idx - shard_begin][layer_begin:layer_end] of a LOCAL entry to `out` (device).
- * Errors: NOT_FOUND (idx outside this shard), SHAPE. */
+ * Writes maps[idx - shard_begin][layer_begin:layer_end] of a LOCAL entry to `out` (device) as
+ * DENSE [layers][H][S][S] maps whatever the DB layout (a PACKED DB is expanded, +0.0 above the
+ * diagonal).  Errors: NOT_FOUND (idx outside this shard), SHAPE. */
 attncache_status attncache_fetch_maps(attncache_db *db, int64_t idx, int32_t layer_begin, int32_t layer_end,
                                       void *out, void *stream);
 

@@ -24,6 +24,7 @@ __all__ = [
     "attncache_db_free", "attncache_search", "attncache_search_keys", "attncache_keys_decode",
     "attncache_apply_cached", "attncache_attend_full", "attncache_route_plan", "attncache_gather_rows",
     "attncache_scatter_rows", "attncache_fetch_maps", "attncache_variant", "attncache_version", "attncache_launch_count",
+    "attncache_packed_map_elems", "attncache_pack_maps", "pack_db_maps",
     "ABI_FUNCTIONS",
 ]
 
@@ -36,7 +37,7 @@ ABI_FUNCTIONS = [
     "attncache_ctx_destroy", "attncache_ctx_sync", "attncache_db_load", "attncache_db_free", "attncache_search",
     "attncache_search_keys", "attncache_keys_decode", "attncache_apply_cached", "attncache_attend_full",
     "attncache_route_plan", "attncache_gather_rows", "attncache_scatter_rows", "attncache_fetch_maps",
-    "attncache_variant", "attncache_launch_count",
+    "attncache_variant", "attncache_launch_count", "attncache_packed_map_elems", "attncache_pack_maps",
 ]
 
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -46,7 +47,7 @@ class _DbDesc(ctypes.Structure):
     _fields_ = [("n_global", ctypes.c_int64), ("shard_begin", ctypes.c_int64), ("shard_count", ctypes.c_int64),
                 ("feat_dim", ctypes.c_int32), ("feat_dtype", ctypes.c_int32), ("feats", ctypes.c_void_p),
                 ("n_layers", ctypes.c_int32), ("n_heads", ctypes.c_int32), ("seq_len", ctypes.c_int32),
-                ("map_dtype", ctypes.c_int32), ("maps", ctypes.c_void_p)]
+                ("map_dtype", ctypes.c_int32), ("maps", ctypes.c_void_p), ("map_layout", ctypes.c_int32)]
 
 
 class AttnCacheError(RuntimeError):
@@ -89,6 +90,8 @@ def load_library():
         "attncache_gather_rows": ([P, P, I64, I64, P, P], I32),
         "attncache_scatter_rows": ([P, P, I64, I64, P, P], I32),
         "attncache_fetch_maps": ([P, I64, I32, I32, P, P], I32),
+        "attncache_packed_map_elems": ([I32], I64),
+        "attncache_pack_maps": ([P, I64, I32, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -148,30 +151,47 @@ class Context:
 
 class Database:
     """attncache_db: this rank's shard of the feature-vector DB and the attention-map DB
-    ("Both databases share the same index").  Keeps the borrowed tensors alive."""
+    ("Both databases share the same index").  Keeps the borrowed tensors alive.
+
+    maps: DENSE [n][L][H][S][S] (packed=False) or PACKED [n][L][H][attncache_packed_map_elems(S)]
+    (packed=True, seq_len required); see include/attncache.h attncache_map_layout."""
 
     def __init__(self, ctx: Context, feats: torch.Tensor, maps: Optional[torch.Tensor] = None,
-                 n_global: Optional[int] = None, shard_begin: int = 0):
+                 n_global: Optional[int] = None, shard_begin: int = 0, packed: bool = False,
+                 seq_len: Optional[int] = None):
         L = load_library()
         _dev(feats, "feats")
+        S = 0
         if maps is not None:
             _dev(maps, "maps")
-            if maps.dim() != 5 or maps.shape[0] != feats.shape[0] or maps.shape[3] != maps.shape[4]:
-                raise ValueError("maps must be [n][L][H][S][S] with n == len(feats)")
+            if maps.shape[0] != feats.shape[0]:
+                raise ValueError("maps and feats must hold the same entries")
+            if packed:
+                S = int(seq_len)
+                if maps.dim() != 4 or maps.shape[3] != attncache_packed_map_elems(S):
+                    raise ValueError("packed maps must be [n][L][H][attncache_packed_map_elems(S)]")
+            else:
+                if maps.dim() != 5 or maps.shape[3] != maps.shape[4]:
+                    raise ValueError("dense maps must be [n][L][H][S][S]")
+                S = maps.shape[3]
         n = feats.shape[0]
         desc = _DbDesc(n_global=n if n_global is None else int(n_global), shard_begin=int(shard_begin),
                        shard_count=n, feat_dim=feats.shape[1], feat_dtype=_DT[feats.dtype],
                        feats=feats.data_ptr() if n else None,
                        n_layers=maps.shape[1] if maps is not None else 0,
                        n_heads=maps.shape[2] if maps is not None else 0,
-                       seq_len=maps.shape[3] if maps is not None else 0,
+                       seq_len=S,
                        map_dtype=_DT[maps.dtype] if maps is not None else 0,
-                       maps=maps.data_ptr() if (maps is not None and n) else None)
+                       maps=maps.data_ptr() if (maps is not None and n) else None,
+                       map_layout=1 if packed else 0)
         h = ctypes.c_void_p()
         _check(L.attncache_db_load(ctx.handle, ctypes.byref(desc), ctypes.byref(h)))
         self.handle = h
         self.ctx = ctx
         self.feats, self.maps = feats, maps
+        self.packed, self.seq_len = packed, S
+        self.n_layers = maps.shape[1] if maps is not None else 0
+        self.n_heads = maps.shape[2] if maps is not None else 0
         self.n_global, self.shard_begin, self.shard_count = desc.n_global, desc.shard_begin, n
         self.device = feats.device
 
@@ -264,13 +284,13 @@ def attncache_apply_cached(db: Database, idx: torch.Tensor, V: torch.Tensor, O: 
     """Alg. 2 l.373-375: O[b] = maps[idx[b]] . V[b] for selected rows; V, O [B][L'][H][S][d]."""
     _dev(V, "V")
     _dev(idx, "idx")
-    layer_end = (db.maps.shape[1] if db.maps is not None else 0) if layer_end is None else layer_end
+    layer_end = db.n_layers if layer_end is None else layer_end
     O = torch.empty_like(V) if O is None else O
     _dev(O, "O")
     if V.dim() != 5 or O.shape != V.shape or V.shape[0] != idx.shape[0]:
         raise ValueError("V/O must be [B][L'][H][S][d] matching idx")
-    if db.maps is not None and (V.shape[1] != layer_end - layer_begin or V.shape[2] != db.maps.shape[2]
-                                or V.shape[3] != db.maps.shape[3]):
+    if db.maps is not None and (V.shape[1] != layer_end - layer_begin or V.shape[2] != db.n_heads
+                                or V.shape[3] != db.seq_len):
         raise AttnCacheError(2, "ATTNCACHE_ERR_SHAPE", "V shape disagrees with the database (L', H, S)")
     _check(load_library().attncache_apply_cached(db.handle, _p(idx), _p(hit), V.shape[0], int(layer_begin),
                                                  int(layer_end), V.shape[4], _DT[V.dtype], _p(V), _p(O),
@@ -325,9 +345,42 @@ def attncache_scatter_rows(src: torch.Tensor, rows: torch.Tensor, dst: torch.Ten
 
 def attncache_fetch_maps(db: Database, idx: int, layer_begin: int = 0, layer_end: Optional[int] = None,
                          out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    m = db.maps
-    layer_end = m.shape[1] if layer_end is None else layer_end
-    out = torch.empty((layer_end - layer_begin, *m.shape[2:]), dtype=m.dtype, device=m.device) if out is None else out
+    """Literal AttnMapsDB.get(idx, n) (Alg. 1 l.259): DENSE [layers][H][S][S] maps of a local entry."""
+    layer_end = db.n_layers if layer_end is None else layer_end
+    S = db.seq_len
+    out = torch.empty((layer_end - layer_begin, db.n_heads, S, S), dtype=db.maps.dtype,
+                      device=db.maps.device) if out is None else out
     _check(load_library().attncache_fetch_maps(db.handle, int(idx), int(layer_begin), int(layer_end), _p(out),
-                                               _stream(stream, m.device)))
+                                               _stream(stream, db.maps.device)))
     return out
+
+
+def attncache_packed_map_elems(seq_len: int) -> int:
+    return int(load_library().attncache_packed_map_elems(int(seq_len)))
+
+
+def attncache_pack_maps(dense: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """DENSE [..., S, S] maps -> PACKED [..., attncache_packed_map_elems(S)] (DB building, Fig. 4 step 3)."""
+    _dev(dense, "dense")
+    S = dense.shape[-1]
+    if dense.shape[-2] != S or dense.element_size() != 2:
+        raise ValueError("dense maps must be [..., S, S] 16-bit")
+    P = attncache_packed_map_elems(S)
+    out = torch.empty((*dense.shape[:-2], P), dtype=dense.dtype, device=dense.device) if out is None else out
+    _dev(out, "out")
+    n_maps = dense.numel() // (S * S)
+    _check(load_library().attncache_pack_maps(_p(dense), n_maps, S, _p(out), _stream(stream, dense.device)))
+    return out
+
+
+def pack_db_maps(cfg_maps_fn, n_entries: int, L: int, H: int, S: int, dtype, device, chunk: int = 16) -> torch.Tensor:
+    """Builds a PACKED map DB [n][L][H][P] by packing dense maps chunk by chunk; cfg_maps_fn(begin, out)
+    fills a DENSE [count][L][H][S][S] staging buffer for entries [begin, begin + count)."""
+    P = attncache_packed_map_elems(S)
+    db = torch.empty((n_entries, L, H, P), dtype=dtype, device=device)
+    stage = torch.empty((min(chunk, n_entries), L, H, S, S), dtype=dtype, device=device)
+    for b in range(0, n_entries, chunk):
+        cnt = min(chunk, n_entries - b)
+        cfg_maps_fn(b, stage[:cnt])
+        attncache_pack_maps(stage[:cnt], db[b:b + cnt])
+    return db

@@ -196,11 +196,15 @@ attncache_status attncache_db_load(attncache_ctx *ctx, const attncache_db_desc *
             return fail(ATTNCACHE_ERR_SHAPE, "db_load: L=%d H=%d S=%d", d->n_layers, d->n_heads, d->seq_len);
         if (d->map_dtype != ATTNCACHE_F16 && d->map_dtype != ATTNCACHE_BF16)
             return fail(ATTNCACHE_ERR_DTYPE, "db_load: map_dtype must be F16 or BF16");
+        if (d->map_layout != ATTNCACHE_MAPS_DENSE && d->map_layout != ATTNCACHE_MAPS_PACKED)
+            return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: map_layout %d", d->map_layout);
+        if (d->seq_len % 8)
+            return fail(ATTNCACHE_ERR_ALIGNMENT, "db_load: seq_len %d: map rows (S*2 bytes) must be 16-byte aligned",
+                        d->seq_len);
         if (d->shard_count > 0) {
             if (!d->maps) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: maps is NULL");
             if (!is_device_ptr(d->maps)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: maps is not device memory");
-            if (!aligned16(d->maps) || ((int64_t)d->seq_len * 2) % 16)
-                return fail(ATTNCACHE_ERR_ALIGNMENT, "db_load: maps base / row pitch (S*2 bytes) not 16-byte aligned");
+            if (!aligned16(d->maps)) return fail(ATTNCACHE_ERR_ALIGNMENT, "db_load: maps base not 16-byte aligned");
         }
     }
     attncache_db *db = new attncache_db();
@@ -316,6 +320,8 @@ attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, co
     a.n_lay = layer_end - layer_begin;
     a.map_dt = d.map_dtype;
     a.act_dt = act_dtype;
+    a.map_layout = d.map_layout;
+    a.map_stride = map_elems(d.seq_len, d.map_layout);
     a.V = V;
     a.O = O;
     a.list = rowlist_view(db->ctx->apply_list.ptr, n_rows);
@@ -414,10 +420,34 @@ attncache_status attncache_fetch_maps(attncache_db *db, int64_t idx, int32_t lay
         return fail(ATTNCACHE_ERR_NOT_FOUND, "fetch_maps: index %lld not in this shard", (long long)idx);
     if (layer_begin < 0 || layer_end > d.n_layers || layer_begin >= layer_end)
         return fail(ATTNCACHE_ERR_SHAPE, "fetch_maps: layers [%d, %d)", layer_begin, layer_end);
-    const size_t per_layer = (size_t)d.n_heads * d.seq_len * d.seq_len * 2;
-    const char *src = (const char *)d.maps + ((size_t)(idx - d.shard_begin) * d.n_layers + layer_begin) * per_layer;
+    const int64_t maps_per_layer = d.n_heads;
+    const int64_t stride = map_elems(d.seq_len, d.map_layout);
+    const uint16_t *src = (const uint16_t *)d.maps +
+                          ((idx - d.shard_begin) * d.n_layers + layer_begin) * maps_per_layer * stride;
+    const int64_t n_maps = maps_per_layer * (layer_end - layer_begin);
     DeviceGuard g(db->ctx->device);
-    AC_CUDA(cudaMemcpyAsync(out, src, per_layer * (layer_end - layer_begin), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    if (d.map_layout == ATTNCACHE_MAPS_DENSE) {
+        AC_CUDA(cudaMemcpyAsync(out, src, (size_t)n_maps * stride * 2, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    } else {
+        AC_CUDA(launch_pack_maps(out, n_maps, d.seq_len, const_cast<uint16_t *>(src), /*unpack=*/true,
+                                 (cudaStream_t)stream));
+    }
+    return ATTNCACHE_OK;
+}
+
+// ---- DB building: packed layout --------------------------------------------------------------
+
+int64_t attncache_packed_map_elems(int32_t seq_len) {
+    return (seq_len > 0 && seq_len % 8 == 0) ? packed_row_off(seq_len) : 0;
+}
+
+attncache_status attncache_pack_maps(const void *dense, int64_t n_maps, int32_t S, void *packed, void *stream) {
+    if (n_maps < 0 || S <= 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "pack_maps: n_maps=%lld S=%d", (long long)n_maps, S);
+    if (S % 8) return fail(ATTNCACHE_ERR_SHAPE, "pack_maps: seq_len %d is not a multiple of 8", S);
+    if (n_maps == 0) return ATTNCACHE_OK;
+    if (!dense || !packed) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "pack_maps: NULL argument");
+    if (!aligned16(dense) || !aligned16(packed)) return fail(ATTNCACHE_ERR_ALIGNMENT, "pack_maps: 16-byte alignment");
+    AC_CUDA(launch_pack_maps(dense, n_maps, S, packed, /*unpack=*/false, (cudaStream_t)stream));
     return ATTNCACHE_OK;
 }
 

@@ -33,6 +33,20 @@ uint64_t launch_count();
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
+// PACKED map layout (include/attncache.h): row i starts at element 8*(4q(q+1) + r(q+1)), q = i/8,
+// r = i%8, and holds 8*(q+1) elements; a map holds packed_row_off(S) elements (S % 8 == 0).
+__host__ __device__ __forceinline__ int64_t packed_row_off(int64_t i) {
+    const int64_t q = i >> 3, r = i & 7;
+    return 8 * (4 * q * (q + 1) + r * (q + 1));
+}
+__host__ __device__ __forceinline__ int64_t map_elems(int32_t S, int32_t layout) {
+    return layout == ATTNCACHE_MAPS_PACKED ? packed_row_off(S) : (int64_t)S * S;
+}
+// Element offset of map row i in either layout.
+__host__ __device__ __forceinline__ int64_t map_row_off(int64_t i, int32_t S, int32_t layout) {
+    return layout == ATTNCACHE_MAPS_PACKED ? packed_row_off(i) : i * S;
+}
+
 inline int dtype_size(int32_t dt) { return dt == ATTNCACHE_F32 ? 4 : 2; }
 inline bool dtype_valid(int32_t dt) { return dt == ATTNCACHE_F32 || dt == ATTNCACHE_F16 || dt == ATTNCACHE_BF16; }
 

@@ -39,6 +39,8 @@ struct ApplyArgs {
     int32_t L, H, S, d;
     int32_t layer_begin, n_lay;  // layer slice of V/O
     int32_t map_dt, act_dt;
+    int32_t map_layout;  // ATTNCACHE_MAPS_DENSE / _PACKED
+    int64_t map_stride;  // elements per S x S map
     const void *V;
     void *O;
     RowList list;
@@ -64,6 +66,9 @@ cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st)
 // ---- TMA descriptors (tma_host.cu) ----
 cudaError_t make_tmap_2d_16(CUtensorMap *out, const void *base, bool bf16, uint64_t inner, uint64_t outer,
                             uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
+
+// ---- packed map layout ----
+cudaError_t launch_pack_maps(const void *dense, int64_t n_maps, int32_t S, void *packed, bool unpack, cudaStream_t st);
 
 // ---- routing ----
 cudaError_t launch_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n, const int64_t *shard_begins,

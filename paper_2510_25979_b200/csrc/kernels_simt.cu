@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(256) apply_simt_kernel(ApplyArgs a) {
         const int64_t lh = u % units_per_row;   // (layer - layer_begin) * H + h
         const int l = (int)(lh / a.H), h = (int)(lh % a.H);
         const int64_t row = a.list.rows[slot], ent = a.list.ents[slot];
-        const MT *A = maps + (((ent * a.L + a.layer_begin + l) * a.H + h) * a.S + i) * (int64_t)a.S;
+        const MT *A = maps + ((ent * a.L + a.layer_begin + l) * a.H + h) * a.map_stride + map_row_off(i, a.S, a.map_layout);
         const int64_t vbase = ((row * a.n_lay + l) * a.H + h) * (int64_t)a.S * a.d;
         for (int c0 = 0; c0 < a.d; c0 += 32) {
             const int c = c0 + lane;
@@ -314,6 +314,40 @@ cudaError_t launch_attend_ffma(const AttendArgs &a, int sm_count, cudaStream_t s
     AC_ATTEND(ATTNCACHE_BF16)
 #undef AC_ATTEND
     return cudaErrorInvalidValue;
+}
+
+// ============================================================================================
+// packed map layout: one warp per map row, lanes over 16-byte pieces
+// ============================================================================================
+__global__ void pack_maps_kernel(const uint4 *dense, int64_t n_maps, int S, uint4 *packed, bool unpack) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t rows = n_maps * S;
+    const int64_t dense_pieces = (int64_t)S * S / 8, packed_pieces = packed_row_off(S) / 8;
+    const int per_row = S / 8;
+    for (int64_t w = gw; w < rows; w += nw) {
+        const int64_t m = w / S;
+        const int i = (int)(w % S);
+        const uint4 *drow = dense + m * dense_pieces + (int64_t)i * per_row;
+        const uint4 *prow = packed + m * packed_pieces + packed_row_off(i) / 8;
+        const int stored = i / 8 + 1;  // pieces kept for row i
+        for (int c = lane; c < per_row; c += 32) {
+            if (!unpack) {
+                if (c < stored) ((uint4 *)prow)[c] = drow[c];
+            } else {
+                ((uint4 *)drow)[c] = c < stored ? prow[c] : make_uint4(0, 0, 0, 0);
+            }
+        }
+    }
+}
+
+cudaError_t launch_pack_maps(const void *dense, int64_t n_maps, int32_t S, void *packed, bool unpack, cudaStream_t st) {
+    if (n_maps == 0) return cudaSuccess;
+    const int64_t warps = n_maps * S;
+    const int blocks = (int)min64((warps * 32 + 255) / 256, 148 * 64);
+    pack_maps_kernel<<<blocks, 256, 0, st>>>((const uint4 *)dense, n_maps, S, (uint4 *)packed, unpack);
+    return count_launches(1), cudaGetLastError();
 }
 
 // ============================================================================================

@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         int64_t row, ent;
         while (iter.next(lh, row, ent)) {
             const int l = (int)(lh / a.H), h = (int)(lh % a.H);
-            const __nv_bfloat16 *A = maps + (((ent * a.L + a.layer_begin + l) * a.H + h) * (int64_t)S) * S;
+            const __nv_bfloat16 *A = maps + ((ent * a.L + a.layer_begin + l) * a.H + h) * a.map_stride;
+            const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
             for (int rb = 0; rb < n_rb; ++rb) {
                 const int n_kc = 2 * (rb + 1);
                 for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
@@ -129,7 +130,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int r = p >> 3, c = p & 7;
                         const int R = rb * kRows + r, col = kc * kChunk + c * 8;
                         const bool need = col <= R;  // the piece holds at least one entry on/below the diagonal
-                        const __nv_bfloat16 *src = A + (int64_t)R * S + (need ? col : 0);
+                        const __nv_bfloat16 *src =
+                            A + (packed ? packed_row_off(R) : (int64_t)R * S) + (need ? col : 0);
                         cp_async_16_hint(dst + sw128_offset(r, c), src, need ? 16u : 0u, policy);
                     }
                     cp_async_commit();

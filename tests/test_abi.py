@@ -90,3 +90,12 @@ def test_keys_are_order_preserving():
     assert order == ranked
     assert key(-0.0, 4) == key(0.0, 4)
     assert all(k > 0 for k in keys)
+
+
+def test_packed_layout_size_formula(lib):
+    """PACKED layout (include/attncache.h): row i keeps 8*(i//8 + 1) elements, rows back to back."""
+    import paper_2510_25979_b200 as ac
+    for S in (8, 32, 128, 256, 1024):
+        assert ac.attncache_packed_map_elems(S) == sum(8 * (i // 8 + 1) for i in range(S))
+        assert ac.attncache_packed_map_elems(S) >= S * (S + 1) // 2      # holds the whole triangle
+    assert ac.attncache_packed_map_elems(30) == 0

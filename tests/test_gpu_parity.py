@@ -266,6 +266,27 @@ def test_apply_out_of_shard_index_is_deferred_not_found(ac, ctx):
     assert e.value.name == "ATTNCACHE_ERR_SHAPE"
 
 
+@pytest.mark.parametrize("cfg_name,N,B", [("tiny", 6, 4), ("llama32_1b", 6, 3), ("llama3_8b", 3, 2),
+                                          ("long_prefill", 2, 2)])
+def test_apply_packed_layout_equals_dense(ac, ctx, cfg_name, N, B):
+    """The PACKED DB layout holds exactly the bytes A.V reads: results are bitwise identical."""
+    cfg = synth.CONFIGS[cfg_name].with_(N=N)
+    x = synth.features(cfg, 0, N, DEV)
+    dense = synth.maps(cfg, 0, N, DEV)
+    packed = ac.attncache_pack_maps(dense)
+    assert packed.shape[-1] == ac.attncache_packed_map_elems(cfg.S)
+    db_d = ac.Database(ctx, x, dense)
+    db_p = ac.Database(ctx, x, packed, packed=True, seq_len=cfg.S)
+    idx = torch.tensor([(3 * b + 1) % N for b in range(B)], device=DEV)
+    V = synth.activations(cfg, "v", 0, B, device=DEV)
+    O_d = ac.attncache_apply_cached(db_d, idx, V)
+    O_p = ac.attncache_apply_cached(db_p, idx, V)
+    assert torch.equal(O_d, O_p)
+    for e in (0, N - 1):                                   # fetch expands PACKED back to DENSE
+        assert torch.equal(ac.attncache_fetch_maps(db_p, e), dense[e])
+        assert torch.equal(ac.attncache_fetch_maps(db_d, e, 1, 2), dense[e, 1:2])
+
+
 # ------------------------------------------------------------------------------------------------
 # attend (Alg. 2 l.376-381, Eq. 5)
 # ------------------------------------------------------------------------------------------------
@@ -331,9 +352,10 @@ def test_full_step_llama32(ac, ctx):
     from paper_2510_25979_b200.pipeline import PrefillStep
     cfg = synth.CONFIGS["llama32_1b"]
     x = synth.features(cfg, 0, cfg.N, DEV)
-    maps = torch.empty(cfg.N, cfg.L, cfg.H, cfg.S, cfg.S, dtype=torch.bfloat16, device=DEV)
-    synth.fill_maps(cfg, maps, 0)
-    db = ac.Database(ctx, x, maps)
+    # the bench's DB: PACKED maps built by the library from the generator's dense maps
+    maps = ac.pack_db_maps(lambda b, out: synth.fill_maps(cfg, out, b), cfg.N, cfg.L, cfg.H, cfg.S,
+                           torch.bfloat16, DEV, chunk=64)
+    db = ac.Database(ctx, x, maps, packed=True, seq_len=cfg.S)
     q, pos, tgt = synth.queries(cfg, DEV)
     Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qkv")
     O = torch.empty_like(V)
@@ -348,7 +370,8 @@ def test_full_step_llama32(ac, ctx):
     hu = [(hits[i], int(rng.integers(cfg.L)), int(rng.integers(cfg.H))) for i in rng.choice(len(hits), 24)]
     hu.append((hits[-1], cfg.L - 1, cfg.H - 1))
     ents = idx.cpu().numpy()
-    A_np = np.stack([storage(maps[ents[b], l, h]) for b, l, h in hu]).reshape(-1)
+    dense = {e: synth.maps(cfg, int(e), 1, DEV)[0] for e in set(int(ents[b]) for b, _, _ in hu)}
+    A_np = np.stack([storage(dense[int(ents[b])][l, h]) for b, l, h in hu]).reshape(-1)
     v_off = [(((b * cfg.L + l) * cfg.H + h) * cfg.S * cfg.d) for b, l, h in hu]
     Vs = storage(V)
     ref = oracle.apply(A_np, "bf16", [u * cfg.S * cfg.S for u in range(len(hu))], Vs, "bf16", v_off, cfg.S, cfg.d)
