@@ -34,7 +34,8 @@ struct Cfg {
     static constexpr int kStages = kD == 64 ? 8 : 6;
     static constexpr int kLag = kStages - 2;  // cp.async groups a loader thread keeps in flight
     static constexpr uint32_t kTmemCols = 2 * kD;
-    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kOutWarpBytes = 32 * kD * 2;  // epilogue staging: one warp's 32 rows of O
+    static constexpr int kSmem = kStages * kStageBytes + 4 * kOutWarpBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 // Walks this CTA's units u = blockIdx.x, +gridDim.x, ... of the compacted hit list.  The hit-list
@@ -71,11 +72,13 @@ struct UnitIter {
 
 template <int kD>
 __global__ void __launch_bounds__(kThreads, 1)
-    apply_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ApplyArgs a, const uint32_t idesc) {
+    apply_tc_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const ApplyArgs a,
+                    const uint32_t idesc) {
     using C = Cfg<kD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t *full = (uint64_t *)(smem + C::kStages * C::kStageBytes);
+    uint8_t *sOut = smem + C::kStages * C::kStageBytes;  // [4 warps][kD/64 halves][32 rows][128 B]
+    uint64_t *full = (uint64_t *)(sOut + 4 * C::kOutWarpBytes);
     uint64_t *empty = full + C::kStages;
     uint64_t *tfull = empty + C::kStages;
     uint64_t *tempty = tfull + 2;
@@ -93,7 +96,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_barrier_init();
     }
-    if (warp == 4 && lane == 0) tma_prefetch_desc(&tmV);
+    if (warp == 4 && lane == 0) {
+        tma_prefetch_desc(&tmV);
+        tma_prefetch_desc(&tmO);
+    }
     if (warp == 5) tmem_alloc<C::kTmemCols>(tmem_slot);
     tc_fence_before();
     __syncthreads();
@@ -107,32 +113,40 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp < 4) {
         // ------------------------------ map loader ------------------------------------------
+        // Thread tid owns 16-byte piece c = tid % 8 of tile rows r0 + 16j (j = 0..7), r0 = tid / 8.
+        // Rows r0 + 16j share r0 % 8, so their 128B-swizzle XOR is the same and the shared-memory
+        // offsets are soff + 2048 j; only the row pointers change per row block.
         const int tid = threadIdx.x;
+        const int c = tid & 7, r0 = tid >> 3;
+        const uint32_t soff = (uint32_t)((r0 >> 3) * 1024 + (r0 & 7) * 128 + ((c ^ (r0 & 7)) << 4));
         const uint64_t policy = policy_evict_first();  // maps are read exactly once
         const __nv_bfloat16 *maps = (const __nv_bfloat16 *)a.maps;  // 16-bit payload (bf16 or f16)
+        const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
         uint32_t cnt = 0, pending = 0;
         UnitIter<false, true> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
         uint32_t lh;
         int64_t row, ent;
         while (iter.next(lh, row, ent)) {
             const int l = (int)(lh / a.H), h = (int)(lh % a.H);
-            const __nv_bfloat16 *A = maps + ((ent * a.L + a.layer_begin + l) * a.H + h) * a.map_stride;
-            const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
+            const __nv_bfloat16 *A = maps + ((ent * a.L + a.layer_begin + l) * a.H + h) * a.map_stride + c * 8;
             for (int rb = 0; rb < n_rb; ++rb) {
+                const __nv_bfloat16 *rowp[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int R = rb * kRows + r0 + 16 * j;
+                    rowp[j] = A + (packed ? packed_row_off(R) : (int64_t)R * S);
+                }
                 const int n_kc = 2 * (rb + 1);
                 for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
                     const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
-                    const uint32_t dst = smem_u32(smem + s * C::kStageBytes);
+                    const uint32_t dst = smem_u32(smem + s * C::kStageBytes) + soff;
+                    const int col = kc * kChunk + c * 8;  // first column of this thread's piece
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const int p = tid + 128 * j;
-                        const int r = p >> 3, c = p & 7;
-                        const int R = rb * kRows + r, col = kc * kChunk + c * 8;
-                        const bool need = col <= R;  // the piece holds at least one entry on/below the diagonal
-                        const __nv_bfloat16 *src =
-                            A + (packed ? packed_row_off(R) : (int64_t)R * S) + (need ? col : 0);
-                        cp_async_16_hint(dst + sw128_offset(r, c), src, need ? 16u : 0u, policy);
+                        // the piece holds at least one entry on/below the diagonal, else zero-fill
+                        const bool need = col <= rb * kRows + r0 + 16 * j;
+                        cp_async_16_hint(dst + 2048 * j, rowp[j] + (need ? kc * kChunk : 0), need ? 16u : 0u, policy);
                     }
                     cp_async_commit();
                     if (++pending > (uint32_t)C::kLag) {
@@ -152,9 +166,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             uint32_t cnt = 0;
             UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
+            // L2 prefetch kAhead units ahead: the unit's PACKED map and its V are contiguous, so one
+            // bulk prefetch each pulls them toward the SM long before the cp.async / TMA loads ask,
+            // which keeps enough bytes in flight without spending shared memory on them.
+            constexpr uint32_t kAhead = 2;
+            UnitIter<true, true> ahead(blockIdx.x + kAhead * gridDim.x, gridDim.x, units, per_row, a.list);
+            const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
+            const uint16_t *maps16 = (const uint16_t *)a.maps;
+            const uint16_t *V16 = (const uint16_t *)a.V;
             uint32_t lh;
             int64_t row, ent;
             while (iter.next(lh, row, ent)) {
+                uint32_t lh2;
+                int64_t row2, ent2;
+                if (ahead.next(lh2, row2, ent2)) {
+                    if (packed) {
+                        const int l2 = (int)(lh2 / a.H), h2 = (int)(lh2 % a.H);
+                        prefetch_l2_bulk(maps16 + ((ent2 * a.L + a.layer_begin + l2) * a.H + h2) * a.map_stride,
+                                         (uint32_t)(a.map_stride * 2));
+                    }
+                    prefetch_l2_bulk(V16 + (row2 * per_row + lh2) * (int64_t)S * kD, (uint32_t)(S * kD * 2));
+                }
                 const int32_t vrow0 = (int32_t)((row * per_row + lh) * S);
                 for (int rb = 0; rb < n_rb; ++rb) {
                     const int n_kc = 2 * (rb + 1);
@@ -203,47 +235,64 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ------------------------------ epilogue ---------------------------------------------
+        // TMEM -> registers -> act dtype -> this warp's 128B-swizzled staging tile -> TMA store of
+        // the warp's 32 rows (full-line writes instead of per-thread 16-byte stores).
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const int row_in_tile = q * 32 + lane;
         uint32_t item = 0;
-        uint16_t *O = (uint16_t *)a.O;
         const bool bf16 = a.act_dt == ATTNCACHE_BF16;
+        uint8_t *stage_o = sOut + (warp - 6) * C::kOutWarpBytes;
+        const uint32_t stage_o_u32 = smem_u32(stage_o);
         UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
         uint32_t lh;
         int64_t row, ent;
         while (iter.next(lh, row, ent)) {
-            uint16_t *Ou = O + ((row * per_row + lh) * S) * (int64_t)kD;
+            const int64_t orow_unit = (row * per_row + lh) * S;  // first O row of the unit
             for (int rb = 0; rb < n_rb; ++rb, ++item) {
                 const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;
                 mbar_wait(&tfull[acc], aph);
                 tc_fence_after();
-                uint32_t v[kD];
                 const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + acc * kD;
+                if (lane == 0) bulk_wait_read<0>();  // the previous TMA store has read the staging tile
+                __syncwarp();
 #pragma unroll
-                for (int cb = 0; cb < kD / 32; ++cb)
-                    tmem_ld_32x32b_x32(taddr + cb * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[cb * 32]));
-                tmem_ld_wait();
-                tc_fence_before();
-                mbar_arrive(&tempty[acc]);
-                uint4 *dst = (uint4 *)(Ou + (int64_t)(rb * kRows + row_in_tile) * kD);
-#pragma unroll
-                for (int c8 = 0; c8 < kD / 8; ++c8) {
-                    uint32_t w[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float lo = __uint_as_float(v[c8 * 8 + 2 * e]), hi = __uint_as_float(v[c8 * 8 + 2 * e + 1]);
-                        if (bf16) {
-                            __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
-                            w[e] = *reinterpret_cast<uint32_t *>(&p);
-                        } else {
-                            __half2 p = __floats2half2_rn(lo, hi);
-                            w[e] = *reinterpret_cast<uint32_t *>(&p);
-                        }
+                for (int half = 0; half < kD / 64; ++half) {  // 64 columns at a time (register budget)
+                    uint32_t v[64];
+                    tmem_ld_32x32b_x32(taddr + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                    tmem_ld_32x32b_x32(taddr + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+                    tmem_ld_wait();
+                    if (half == kD / 64 - 1) {
+                        tc_fence_before();
+                        mbar_arrive(&tempty[acc]);  // accumulator drained: the next row block may start
                     }
-                    dst[c8] = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+                    for (int c8 = 0; c8 < 8; ++c8) {
+                        uint32_t w[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float lo = __uint_as_float(v[c8 * 8 + 2 * e]), hi = __uint_as_float(v[c8 * 8 + 2 * e + 1]);
+                            if (bf16) {
+                                __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+                                w[e] = *reinterpret_cast<uint32_t *>(&p);
+                            } else {
+                                __half2 p = __floats2half2_rn(lo, hi);
+                                w[e] = *reinterpret_cast<uint32_t *>(&p);
+                            }
+                        }
+                        *reinterpret_cast<uint4 *>(stage_o + half * 4096 + sw128_offset(lane, c8)) =
+                            make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    const int32_t orow = (int32_t)(orow_unit + rb * kRows + q * 32);
+#pragma unroll
+                    for (int half = 0; half < kD / 64; ++half) tma_store_2d(&tmO, stage_o_u32 + half * 4096, half * 64, orow);
+                    bulk_commit();
                 }
             }
         }
+        if (lane == 0) bulk_wait<0>();
     }
     __syncthreads();
     if (warp == 5) {
@@ -257,13 +306,14 @@ cudaError_t launch(const ApplyArgs &a, int sm_count, cudaStream_t st) {
     using C = Cfg<kD>;
     const bool bf16 = a.act_dt == ATTNCACHE_BF16;
     const uint64_t rows = (uint64_t)a.max_rows * a.n_lay * a.H * a.S;
-    CUtensorMap tmV;
+    CUtensorMap tmV, tmO;
     cudaError_t e = make_tmap_2d_16(&tmV, a.V, bf16, kD, rows, (uint64_t)kD * 2, 64, kChunk, 128);
+    if (e == cudaSuccess) e = make_tmap_2d_16(&tmO, a.O, bf16, kD, rows, (uint64_t)kD * 2, 64, 32, 128);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(apply_tc_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     const uint32_t idesc = idesc_f16(kRows, kD, bf16 ? 1u : 0u, /*a_mn=*/0u, /*b_mn=*/1u);
-    apply_tc_kernel<kD><<<sm_count, kThreads, C::kSmem, st>>>(tmV, a, idesc);
+    apply_tc_kernel<kD><<<sm_count, kThreads, C::kSmem, st>>>(tmV, tmO, a, idesc);
     count_launches(1);
     return cudaGetLastError();
 }
