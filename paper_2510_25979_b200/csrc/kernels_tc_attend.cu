@@ -238,13 +238,13 @@ __global__ void __launch_bounds__(kThreads, Cfg<kD, kTwoCTA>::kMinBlocks)
             mbar_arrive(&pv_empty[pb]);
             if (pend_last) {
                 const float inv = 1.f / prev_l;
-                uint4 *dst = (uint4 *)(O + (prev_row0 + prev_qb * kBlk + r) * (int64_t)kD);
+                uint16_t *dst = O + (prev_row0 + prev_qb * kBlk + r) * (int64_t)kD;
 #pragma unroll
-                for (int c8 = 0; c8 < kD / 8; ++c8) {
-                    uint32_t w[4];
+                for (int c16 = 0; c16 < kD / 16; ++c16) {  // 32-byte stores: whole sectors, no partial writes
+                    uint32_t w[8];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float lo = o[c8 * 8 + 2 * e] * inv, hi = o[c8 * 8 + 2 * e + 1] * inv;
+                    for (int e = 0; e < 8; ++e) {
+                        const float lo = o[c16 * 16 + 2 * e] * inv, hi = o[c16 * 16 + 2 * e + 1] * inv;
                         if (bf16) {
                             __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
                             w[e] = *reinterpret_cast<uint32_t *>(&h2);
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<kD, kTwoCTA>::kMinBlocks)
                             w[e] = *reinterpret_cast<uint32_t *>(&h2);
                         }
                     }
-                    dst[c8] = make_uint4(w[0], w[1], w[2], w[3]);
+                    st_global_v8(dst + c16 * 16, w);
                 }
 #pragma unroll
                 for (int c = 0; c < kD; ++c) o[c] = 0.f;
