@@ -182,7 +182,7 @@ attncache_status attncache_attend_full(attncache_ctx *ctx, int64_t batch, int32_
  * owner[b] = -1 for misses.  counts[r] = number of rows owned by r; order = the selected rows
  * grouped by owner (ascending rank, ascending b inside a rank), n = sum(counts) entries used.
  * Deterministic.  gather_rows: dst[k] = src[rows[k]]; scatter_rows: dst[rows[k]] = src[k];
- * rows are int64 row numbers and rows are row_bytes long (multiple of 16). */
+ * rows are int64 row numbers and rows are row_bytes long (a multiple of 8; 16 is faster). */
 attncache_status attncache_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n_rows,
                                       const int64_t *shard_begins, int32_t world, int32_t *owner, int32_t *counts,
                                       int64_t *order, void *stream);

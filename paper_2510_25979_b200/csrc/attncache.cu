@@ -394,7 +394,9 @@ static attncache_status copy_rows(const void *src, const int64_t *rows, int64_t 
     if (n < 0 || row_bytes <= 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "copy_rows: n=%lld row_bytes=%lld", (long long)n, (long long)row_bytes);
     if (n == 0) return ATTNCACHE_OK;
     if (!src || !rows || !dst) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "copy_rows: NULL argument");
-    if (row_bytes % 16 || !aligned16(src) || !aligned16(dst)) return fail(ATTNCACHE_ERR_ALIGNMENT, "copy_rows: 16-byte alignment");
+    const bool ok16 = row_bytes % 16 == 0 && aligned16(src) && aligned16(dst);
+    const bool ok8 = row_bytes % 8 == 0 && ((uintptr_t)src & 7) == 0 && ((uintptr_t)dst & 7) == 0;
+    if (!ok16 && !ok8) return fail(ATTNCACHE_ERR_ALIGNMENT, "copy_rows: rows and bases must be 8-byte multiples/aligned");
     AC_CUDA(launch_copy_rows(src, rows, n, row_bytes, dst, gather, (cudaStream_t)stream));
     return ATTNCACHE_OK;
 }

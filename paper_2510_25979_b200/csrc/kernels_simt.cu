@@ -401,7 +401,8 @@ cudaError_t launch_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n,
     return count_launches(1), cudaGetLastError();
 }
 
-__global__ void copy_rows_kernel(const int4 *src, const int64_t *rows, int64_t n_rows, int64_t row_words, int4 *dst,
+template <typename W>
+__global__ void copy_rows_kernel(const W *src, const int64_t *rows, int64_t n_rows, int64_t row_words, W *dst,
                                  bool gather) {
     const int64_t total = n_rows * row_words;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -417,9 +418,15 @@ __global__ void copy_rows_kernel(const int4 *src, const int64_t *rows, int64_t n
 cudaError_t launch_copy_rows(const void *src, const int64_t *rows, int64_t n_rows, int64_t row_bytes, void *dst,
                              bool gather, cudaStream_t st) {
     if (n_rows == 0) return cudaSuccess;
-    int64_t words = row_bytes / 16;
-    int blocks = (int)min64((n_rows * words + 255) / 256, 148 * 16);
-    copy_rows_kernel<<<blocks, 256, 0, st>>>((const int4 *)src, rows, n_rows, words, (int4 *)dst, gather);
+    if (row_bytes % 16 == 0) {
+        const int64_t words = row_bytes / 16;
+        int blocks = (int)min64((n_rows * words + 255) / 256, 148 * 16);
+        copy_rows_kernel<int4><<<blocks, 256, 0, st>>>((const int4 *)src, rows, n_rows, words, (int4 *)dst, gather);
+    } else {
+        const int64_t words = row_bytes / 8;
+        int blocks = (int)min64((n_rows * words + 255) / 256, 148 * 16);
+        copy_rows_kernel<int2><<<blocks, 256, 0, st>>>((const int2 *)src, rows, n_rows, words, (int2 *)dst, gather);
+    }
     return count_launches(1), cudaGetLastError();
 }
 

@@ -1,0 +1,136 @@
+"""Multi-GPU data-parallel AttnCache step (BASELINE.json north_star).
+
+The memoization database shards by contiguous entry ranges across ranks (one process per GPU).
+Each query has a home rank.  One step:
+
+  a2  C1  all-gather the query batch                               (torch.distributed, NCCL)
+  a3  K1  local exact top-1 over this shard -> packed keys          (attncache_search_keys)
+  a4  C2  all-gather the keys; K2 max over shards + tau gate        (attncache_keys_decode)
+  a5  K3  bucket the home hits by owner rank                        (attncache_route_plan)
+      C3  exchange per-peer row counts (host sync: sizes the buffers)
+  a6  C4  V rows -> owner (all_to_all);  K4  O = A.V on the owner  (attncache_apply_cached)
+  a7  C5  O rows -> home  (all_to_all);  K3  scatter into O          (attncache_scatter_rows)
+  a8  K5  misses: local causal attention                            (attncache_attend_full)
+
+Collectives are torch.distributed (NCCL over NVLink/NVSwitch on the GPU box, gloo in the CPU
+tests); every per-rank computation goes through `ops`, which in the product is `CudaOps` (the C
+ABI).  The CPU tests inject their own reference ops to check this host logic with world size 2-3.
+"""
+from __future__ import annotations
+
+from typing import List, Optional
+
+import torch
+import torch.distributed as dist
+
+from . import (Context, Database, attncache_apply_cached, attncache_attend_full, attncache_gather_rows,
+               attncache_keys_decode, attncache_route_plan, attncache_scatter_rows, attncache_search_keys)
+
+
+def shard_range(n: int, world: int, rank: int):
+    """Contiguous entry range [begin, begin + count) of `rank` (the first n % world ranks get one more)."""
+    base, extra = divmod(n, world)
+    begin = rank * base + min(rank, extra)
+    return begin, base + (1 if rank < extra else 0)
+
+
+class CudaOps:
+    """The product's per-rank kernels (C ABI) for one shard."""
+
+    def __init__(self, ctx: Context, db: Database):
+        self.ctx, self.db = ctx, db
+
+    def search_keys(self, q):
+        return attncache_search_keys(self.db, q)
+
+    def keys_decode(self, keys_all, tau):
+        return attncache_keys_decode(keys_all, tau)
+
+    def route_plan(self, idx, hit, shard_begins):
+        return attncache_route_plan(idx, hit, shard_begins)
+
+    def gather_rows(self, src, rows):
+        return attncache_gather_rows(src, rows)
+
+    def scatter_rows(self, src, rows, dst):
+        return attncache_scatter_rows(src, rows, dst)
+
+    def apply_cached(self, idx, V, layer_begin=0, layer_end=None):
+        return attncache_apply_cached(self.db, idx, V, layer_begin=layer_begin, layer_end=layer_end)
+
+    def attend_full(self, Q, K, V, O, skip):
+        return attncache_attend_full(self.ctx, Q, K, V, O, skip=skip)
+
+
+class ShardedPrefill:
+    """One rank's view of the sharded step.  All ranks must call the same methods in the same order
+    (NCCL semantics); home batch sizes may differ per rank and may be 0."""
+
+    def __init__(self, ops, n_global: int, tau: float, group=None, device="cuda"):
+        self.ops, self.n_global, self.tau, self.group = ops, int(n_global), float(tau), group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = torch.device(device)
+        begins = [shard_range(self.n_global, self.world, r)[0] for r in range(self.world)] + [self.n_global]
+        self.shard_begins = torch.tensor(begins, dtype=torch.int64, device=self.device)
+
+    # ---- a2-a4: sharded search -------------------------------------------------------------------
+    def _home_sizes(self, b_home: int) -> List[int]:
+        t = torch.tensor([b_home], dtype=torch.int64, device=self.device)
+        out = torch.empty(self.world, dtype=torch.int64, device=self.device)
+        dist.all_gather_into_tensor(out, t, group=self.group)
+        return out.cpu().tolist()
+
+    def search(self, q_home: torch.Tensor):
+        """Returns this rank's (idx, score, hit) for its home queries: the global top-1 over all shards."""
+        sizes = self._home_sizes(q_home.shape[0])
+        bmax = max(max(sizes), 1)
+        D = q_home.shape[1]
+        pad = torch.zeros(bmax, D, dtype=q_home.dtype, device=self.device)
+        pad[:q_home.shape[0]] = q_home
+        q_all = torch.empty(self.world * bmax, D, dtype=q_home.dtype, device=self.device)
+        dist.all_gather_into_tensor(q_all, pad, group=self.group)                              # C1
+        q_all = q_all.view(self.world, bmax, D)
+        q_all = torch.cat([q_all[r, :sizes[r]] for r in range(self.world)]) if sum(sizes) else q_all[0, :0]
+        keys = self.ops.search_keys(q_all.contiguous())                                         # K1
+        keys_all = torch.empty(self.world * keys.shape[0], dtype=keys.dtype, device=self.device)
+        dist.all_gather_into_tensor(keys_all, keys, group=self.group)                           # C2
+        idx, score, hit = self.ops.keys_decode(keys_all.view(self.world, -1), self.tau)         # K2
+        lo = sum(sizes[:self.rank])
+        hi = lo + sizes[self.rank]
+        return idx[lo:hi].contiguous(), score[lo:hi].contiguous(), hit[lo:hi].contiguous()
+
+    # ---- a5-a7: route hits to the owner, compute A.V there, return O ---------------------------------
+    def apply_routed(self, idx_home, hit_home, V_home, O_home, layer_begin=0, layer_end=None):
+        b_home = idx_home.shape[0]
+        owner, counts, order = self.ops.route_plan(idx_home, hit_home, self.shard_begins)       # K3
+        send_counts = counts.to(torch.int64)
+        recv_counts = torch.empty_like(send_counts)
+        dist.all_to_all_single(recv_counts, send_counts, group=self.group)                       # C3
+        send_n = send_counts.cpu().tolist()
+        recv_n = recv_counts.cpu().tolist()
+        rows = order[:sum(send_n)].contiguous()
+        row_shape = V_home.shape[1:]
+        V_send = self.ops.gather_rows(V_home, rows) if sum(send_n) else V_home[:0]
+        idx_send = self.ops.gather_rows(idx_home, rows) if sum(send_n) else idx_home[:0]
+        V_recv = torch.empty((sum(recv_n), *row_shape), dtype=V_home.dtype, device=self.device)
+        idx_recv = torch.empty(sum(recv_n), dtype=idx_home.dtype, device=self.device)
+        dist.all_to_all_single(V_recv, V_send, recv_n, send_n, group=self.group)                 # C4
+        dist.all_to_all_single(idx_recv, idx_send, recv_n, send_n, group=self.group)
+        if sum(recv_n):
+            O_recv = self.ops.apply_cached(idx_recv, V_recv, layer_begin, layer_end)            # K4
+        else:
+            O_recv = V_recv
+        O_back = torch.empty((sum(send_n), *row_shape), dtype=V_home.dtype, device=self.device)
+        dist.all_to_all_single(O_back, O_recv, send_n, recv_n, group=self.group)                 # C5
+        if sum(send_n):
+            self.ops.scatter_rows(O_back, rows, O_home)                                          # K3
+        return O_home
+
+    # ---- the whole step ----------------------------------------------------------------------------
+    def __call__(self, q_home, Q_home, K_home, V_home, O_home):
+        idx, score, hit = self.search(q_home)
+        self.apply_routed(idx, hit, V_home, O_home)
+        if q_home.shape[0]:
+            self.ops.attend_full(Q_home, K_home, V_home, O_home, hit)                           # K5
+        return idx, score, hit

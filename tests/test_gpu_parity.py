@@ -380,3 +380,35 @@ def test_full_step_llama32(ac, ctx):
     off = [(((b * cfg.L + l) * cfg.H + h) * cfg.S * cfg.d) for b, l, h in mu]
     ref = oracle.attend(storage(Q), storage(K), Vs, "bf16", off, cfg.S, cfg.d)
     check_close(_gather_units(O, mu), ref, torch.bfloat16, "step attend")
+
+
+def test_sharded_prefill_world1_matches_single_gpu_step(ac, ctx):
+    """The multi-GPU orchestration (dist.ShardedPrefill over NCCL) at world size 1 reproduces the
+    single-GPU step bitwise (the multi-rank host logic is covered by tests/test_dist_gloo.py)."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2510_25979_b200.dist import CudaOps, ShardedPrefill
+    from paper_2510_25979_b200.pipeline import PrefillStep
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        cfg = synth.CONFIGS["llama32_1b"].with_(N=64, B=16, L=2)
+        x = synth.features(cfg, 0, cfg.N, DEV)
+        maps = ac.attncache_pack_maps(synth.maps(cfg, 0, cfg.N, DEV))
+        db = ac.Database(ctx, x, maps, packed=True, seq_len=cfg.S)
+        q, pos, tgt = synth.queries(cfg, DEV)
+        Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qkv")
+        O1, O2 = torch.empty_like(V), torch.empty_like(V)
+        r1 = PrefillStep(ctx, db, cfg.tau)(q, Q, K, V, O1)
+        r2 = ShardedPrefill(CudaOps(ctx, db), cfg.N, cfg.tau, device=DEV)(q, Q, K, V, O2)
+        torch.cuda.synchronize()
+        for a, b in zip(r1, r2):
+            assert torch.equal(a, b)
+        assert torch.equal(O1, O2)
+    finally:
+        dist.destroy_process_group()
