@@ -126,11 +126,15 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline leg and --impl reference)
 # ------------------------------------------------------------------------------------------------
-def oracle_step_sample(cfg, n_search=64, n_apply=768, n_attend=192, seed=0):
+def oracle_step_sample(cfg, budget=6e8, seed=0):
     """Times the CPU oracle on a bounded sample of one step of `cfg` and extrapolates.
 
-    Returns (seconds per full step (extrapolated), description, threads)."""
+    Each stage gets about `budget` multiply-adds of work (a few seconds of fp64 CPU time on a
+    16-core host).  Returns (seconds per full step (extrapolated), description, threads)."""
     import numpy as np
+    n_search = int(min(cfg.B, max(4, budget // (cfg.N * cfg.D))))
+    n_apply = int(max(4, budget // (cfg.S * cfg.S * cfg.d)))
+    n_attend = int(max(4, budget // (cfg.S * cfg.S * cfg.d)))
 
     import oracle
     from tests._util import storage
