@@ -166,27 +166,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             uint32_t cnt = 0;
             UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
-            // L2 prefetch kAhead units ahead: the unit's PACKED map and its V are contiguous, so one
-            // bulk prefetch each pulls them toward the SM long before the cp.async / TMA loads ask,
-            // which keeps enough bytes in flight without spending shared memory on them.
-            constexpr uint32_t kAhead = 2;
-            UnitIter<true, true> ahead(blockIdx.x + kAhead * gridDim.x, gridDim.x, units, per_row, a.list);
-            const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
-            const uint16_t *maps16 = (const uint16_t *)a.maps;
-            const uint16_t *V16 = (const uint16_t *)a.V;
+            // V is re-read by every row block of the unit (S > 128): keep it in L2 (evict_last) while
+            // the maps stream through with evict_first.
+            const uint64_t v_policy = policy_evict_last();
             uint32_t lh;
             int64_t row, ent;
             while (iter.next(lh, row, ent)) {
-                uint32_t lh2;
-                int64_t row2, ent2;
-                if (ahead.next(lh2, row2, ent2)) {
-                    if (packed) {
-                        const int l2 = (int)(lh2 / a.H), h2 = (int)(lh2 % a.H);
-                        prefetch_l2_bulk(maps16 + ((ent2 * a.L + a.layer_begin + l2) * a.H + h2) * a.map_stride,
-                                         (uint32_t)(a.map_stride * 2));
-                    }
-                    prefetch_l2_bulk(V16 + (row2 * per_row + lh2) * (int64_t)S * kD, (uint32_t)(S * kD * 2));
-                }
                 const int32_t vrow0 = (int32_t)((row * per_row + lh) * S);
                 for (int rb = 0; rb < n_rb; ++rb) {
                     const int n_kc = 2 * (rb + 1);
@@ -197,7 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t dst = smem_u32(smem + s * C::kStageBytes + kABytes);
 #pragma unroll
                         for (int half = 0; half < kD / 64; ++half)
-                            tma_load_2d(dst + half * (kChunk * 128), &tmV, &full[s], half * 64, vrow0 + kc * kChunk);
+                            tma_load_2d_hint(dst + half * (kChunk * 128), &tmV, &full[s], half * 64, vrow0 + kc * kChunk,
+                                             v_policy);
                     }
                 }
             }
