@@ -2,16 +2,18 @@
 // PAPER.md:376-381; Eq. 5): O = softmax(Q K^T * scale, keys j > i masked) . V.
 //
 // Work item = (unit, 128-query block qb); it visits key blocks j = 0..qb (causal block skipping).
-// Per key block (global block counter blk, double-buffered in TMEM):
-//   S   = Q K_j^T            tcgen05 SS, M=128 queries, N=128 keys, K=d; fp32 in TMEM cols [128b, 128b+128)
-//   P   = exp2(S*scale*log2e - m)  one query row per thread; bf16 P written back over the first 64
-//                            columns of the same S buffer (two keys per 32-bit column)
-//   PV  = P V_j              tcgen05 TS (A = P from TMEM), M=128, N=d, K=128 keys; fp32 in TMEM
-//   O   = (O + PV_prev) * exp2(m_prev - m)  in fp32 registers; O / l at the item's end.
-// The softmax of block blk overlaps the tensor core's PV of block blk-1 (software pipeline that
-// runs across item boundaries).  Q, K and V stream through separate TMA rings so Q and K slots are
-// released as soon as their S MMA retires.
-// Roles (192 threads): warp 0 TMA loader, warp 1 MMA issuer + TMEM owner, warps 2-5 softmax/epilogue.
+// Two softmax warp groups (WG0 = warps 2-5, WG1 = warps 6-9) own two independent item streams of
+// the CTA (items blockIdx.x + (2k + g) * gridDim.x) and ping-pong on the tensor core: while WG g
+// turns S into P, the MMA warp computes the other group's S or PV.  Per WG, in TMEM:
+//   S/P  (128 columns)  S = Q K_j^T (SS MMA, M=128 queries, N=128 keys, K=d, fp32); the softmax
+//                       writes bf16 P back over the first 64 columns (two keys per column).
+//   O    (d columns)    O += P V_j (TS MMA: A = P from TMEM, B = V MN-major from smem).
+// Online softmax with lazy rescaling: P is taken relative to a reference max m_ref that only
+// moves (rescaling O in TMEM and l) when the running max exceeds it by more than 8 (log2 units),
+// so P <= 2^8 and the correction is rare.  At the item's end O / l is rounded and stored with
+// 32-byte (full-sector) stores.
+// Roles (320 threads): warp 0 TMA loader (Q per item, K_j/V_j per block), warp 1 MMA issuer +
+// TMEM owner, warps 2-9 the two softmax/epilogue groups (TMEM lane quarter = warp % 4).
 #include "kernels.cuh"
 #include "sm100.cuh"
 
@@ -20,22 +22,17 @@ using namespace sm100;
 
 namespace {
 
-constexpr int kThreads = 192;
-constexpr int kBlk = 128;  // queries per item = keys per block
+constexpr int kThreads = 320;
+constexpr int kBlk = 128;                 // queries per item = keys per block
+constexpr float kRescaleThreshold = 8.f;  // log2 units: P <= 2^8 between rescales
 
-// kTwoCTA: two co-resident CTAs per SM (d = 64), each with one S/P buffer, 2-slot rings and 256 TMEM
-// columns, so one CTA's softmax latency hides behind the other's; else one CTA per SM with
-// double-buffered S/P.
-template <int kD, bool kTwoCTA>
+template <int kD>
 struct Cfg {
-    static constexpr int kTile = kBlk * kD * 2;                          // one [128][d] 16-bit tile
-    static constexpr int kRing = kTwoCTA ? 2 : (kD == 64 ? 4 : 2);      // slots per Q / K / V ring
-    static constexpr int kSBufs = kTwoCTA ? 1 : 2;                       // S/P buffers (128 cols each)
-    static constexpr uint32_t kPVBase = 128 * kSBufs;                    // PV: 2 x d columns
-    static constexpr uint32_t kTmemCols = kTwoCTA ? 256 : 512;
-    static constexpr int kMinBlocks = kTwoCTA ? 2 : 1;
-    static constexpr int kSmem = 3 * kRing * kTile + 1024 + 512;
-    static_assert(kPVBase + 2 * kD <= kTmemCols, "TMEM budget");
+    static constexpr int kTile = kBlk * kD * 2;       // one [128][d] 16-bit tile
+    static constexpr int kQSlots = kD == 64 ? 2 : 1;  // per stream
+    static constexpr int kKV = kD == 64 ? 4 : 2;      // K ring and V ring slots
+    static constexpr int kSmem = (2 * kQSlots + 2 * kKV) * kTile + 1024 + 512;
+    static constexpr uint32_t kTmemCols = 512;        // S/P: 2 x 128 at 0; O: 2 x d at 256
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -52,44 +49,76 @@ __device__ __forceinline__ Ring ring(uint32_t i) {
     return {i % N, (i / N) & 1u};
 }
 
-template <int kD, bool kTwoCTA>
-__global__ void __launch_bounds__(kThreads, Cfg<kD, kTwoCTA>::kMinBlocks)
+// One CTA-local item stream: items t = first, first + stride, ...; item -> (unit's first row,
+// query block qb), heaviest query blocks first.  j walks the item's key blocks.
+struct Stream {
+    uint32_t t, stride, items, units, per_row, n_qb, S;
+    const int32_t *rows;
+    bool active = false;
+    int64_t row0 = 0;
+    int qb = 0, j = 0;
+    __device__ void init(uint32_t first, uint32_t stride_, uint32_t items_, uint32_t units_, uint32_t per_row_,
+                         uint32_t n_qb_, uint32_t S_, const int32_t *rows_) {
+        t = first, stride = stride_, items = items_, units = units_, per_row = per_row_, n_qb = n_qb_, S = S_;
+        rows = rows_;
+        start_item();
+    }
+    __device__ void start_item() {
+        active = t < items;
+        if (!active) return;
+        const uint32_t u = t % units;
+        qb = (int)(n_qb - 1 - t / units);
+        row0 = ((int64_t)rows[u / per_row] * per_row + u % per_row) * S;
+        j = 0;
+    }
+    // Moves past the current key block; returns true when that block ended the item.
+    __device__ bool advance() {
+        if (++j > qb) {
+            t += stride;
+            start_item();
+            return true;
+        }
+        return false;
+    }
+};
+
+template <int kD>
+__global__ void __launch_bounds__(kThreads, 1)
     attend_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const AttendArgs a, const uint32_t idesc_s,
                      const uint32_t idesc_pv) {
-    using C = Cfg<kD, kTwoCTA>;
-    constexpr int R = C::kRing;
-    constexpr int NS = C::kSBufs;
+    using C = Cfg<kD>;
+    constexpr int NQ = C::kQSlots, NKV = C::kKV;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t *sQ = smem, *sK = smem + R * C::kTile, *sV = smem + 2 * R * C::kTile;
-    uint64_t *bars = (uint64_t *)(smem + 3 * R * C::kTile);
-    uint64_t *q_full = bars, *q_empty = q_full + R;
-    uint64_t *k_full = q_empty + R, *k_empty = k_full + R;
-    uint64_t *v_full = k_empty + R, *v_empty = v_full + R;
-    uint64_t *s_full = v_empty + R;    // [2] S computed
-    uint64_t *p_full = s_full + 2;     // [2] P written (128 threads)
-    uint64_t *s_free = p_full + 2;     // [2] the PV that read P retired: S/P buffer reusable
-    uint64_t *pv_full = s_free + 2;    // [2]
-    uint64_t *pv_empty = pv_full + 2;  // [2] (128 threads)
-    uint32_t *tmem_slot = (uint32_t *)(pv_empty + 2);
+    uint8_t *sQ = smem;                    // [2 streams][NQ][tile]
+    uint8_t *sK = sQ + 2 * NQ * C::kTile;  // [NKV][tile]
+    uint8_t *sV = sK + NKV * C::kTile;     // [NKV][tile]
+    uint64_t *bars = (uint64_t *)(sV + NKV * C::kTile);
+    uint64_t *q_full = bars, *q_empty = q_full + 2 * NQ;
+    uint64_t *k_full = q_empty + 2 * NQ, *k_empty = k_full + NKV;
+    uint64_t *v_full = k_empty + NKV, *v_empty = v_full + NKV;
+    uint64_t *s_full = v_empty + NKV;  // [2] S of WG g computed
+    uint64_t *p_full = s_full + 2;     // [2] P of WG g written (128 arrivals)
+    uint64_t *pv_done = p_full + 2;    // [2] PV of WG g retired (S/P buffer reusable, O complete)
+    uint32_t *tmem_slot = (uint32_t *)(pv_done + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < R; ++s) {
+        for (int s = 0; s < 2 * NQ; ++s) {
             mbar_init(&q_full[s], 1);
             mbar_init(&q_empty[s], 1);
+        }
+        for (int s = 0; s < NKV; ++s) {
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
             mbar_init(&v_full[s], 1);
             mbar_init(&v_empty[s], 1);
         }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 128);
-            mbar_init(&s_free[i], 1);
-            mbar_init(&pv_full[i], 1);
-            mbar_init(&pv_empty[i], 128);
+        for (int g = 0; g < 2; ++g) {
+            mbar_init(&s_full[g], 1);
+            mbar_init(&p_full[g], 128);
+            mbar_init(&pv_done[g], 1);
         }
         fence_barrier_init();
     }
@@ -109,229 +138,222 @@ __global__ void __launch_bounds__(kThreads, Cfg<kD, kTwoCTA>::kMinBlocks)
     const uint32_t per_row = (uint32_t)(a.L * a.H);
     const uint32_t units = (uint32_t)(*a.list.count) * per_row;
     const uint32_t items = units * n_qb;
-    // item t -> (unit, qb), heaviest query blocks first so the persistent CTAs finish together.
-    auto decode = [&](uint32_t t, int64_t &unit_row0, int &qb) {
-        qb = (int)(n_qb - 1 - t / units);
-        const uint32_t u = t % units;
-        unit_row0 = ((int64_t)a.list.rows[u / per_row] * per_row + u % per_row) * S;
-    };
+    const uint32_t stride = 2 * gridDim.x;
 
-    if (warp == 0) {
-        // ------------------------------ TMA loader -------------------------------------------
+    if (warp < 2) {
+        // The loader (warp 0) and the MMA issuer (warp 1) walk the same merged order of events:
+        // one key block of stream 0, one of stream 1, ... (a finished stream is skipped).
         if (lane == 0) {
-            uint32_t it = 0, blk = 0;
-            for (uint32_t t = blockIdx.x; t < items; t += gridDim.x, ++it) {
-                int64_t row0;
-                int qb;
-                decode(t, row0, qb);
-                const Ring rq = ring<R>(it);
-                mbar_wait(&q_empty[rq.slot], rq.phase ^ 1u);
-                mbar_arrive_expect_tx(&q_full[rq.slot], C::kTile);
-                for (int h = 0; h < kD / 64; ++h)
-                    tma_load_2d(smem_u32(sQ + rq.slot * C::kTile + h * (kBlk * 128)), &tmQ, &q_full[rq.slot], h * 64,
-                                (int32_t)(row0 + qb * kBlk));
-                for (int j = 0; j <= qb; ++j, ++blk) {
-                    const Ring rk = ring<R>(blk);
-                    mbar_wait(&k_empty[rk.slot], rk.phase ^ 1u);
-                    mbar_arrive_expect_tx(&k_full[rk.slot], C::kTile);
-                    for (int h = 0; h < kD / 64; ++h)
-                        tma_load_2d(smem_u32(sK + rk.slot * C::kTile + h * (kBlk * 128)), &tmK, &k_full[rk.slot],
-                                    h * 64, (int32_t)(row0 + j * kBlk));
-                    mbar_wait(&v_empty[rk.slot], rk.phase ^ 1u);
-                    mbar_arrive_expect_tx(&v_full[rk.slot], C::kTile);
-                    for (int h = 0; h < kD / 64; ++h)
-                        tma_load_2d(smem_u32(sV + rk.slot * C::kTile + h * (kBlk * 128)), &tmV, &v_full[rk.slot],
-                                    h * 64, (int32_t)(row0 + j * kBlk));
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ------------------------------ MMA issuer -------------------------------------------
-        if (lane == 0) {
-            auto issue_pv = [&](uint32_t c) {
-                const Ring rv = ring<R>(c);
-                const Ring rs = ring<NS>(c);                        // S/P buffer
-                const uint32_t buf = c & 1u, bph = (c >> 1) & 1u;   // PV buffer
-                mbar_wait(&p_full[rs.slot], rs.phase);
+            Stream st[2];
+            st[0].init(blockIdx.x, stride, items, units, per_row, n_qb, S, a.list.rows);
+            st[1].init(blockIdx.x + gridDim.x, stride, items, units, per_row, n_qb, S, a.list.rows);
+            uint32_t qcnt[2] = {0, 0};  // items started per stream (Q ring position)
+            uint32_t bcnt[2] = {0, 0};  // key blocks per stream (S/P/PV barrier phases)
+            uint32_t kv = 0;            // key blocks overall (K/V ring position)
+            int g = 0;
+            // MMA: PV of an event is issued after the S of the next event (ping-pong) unless the
+            // next event belongs to the same group (its S needs the S/P buffer that PV reads).
+            int pend_g = -1;
+            uint32_t pend_kv = 0, pend_b = 0;
+            bool pend_first = false;
+            auto issue_pv = [&]() {
+                const Ring rv = ring<NKV>(pend_kv);
+                mbar_wait(&p_full[pend_g], pend_b & 1u);
                 mbar_wait(&v_full[rv.slot], rv.phase);
-                mbar_wait(&pv_empty[buf], bph ^ 1u);
                 tc_fence_after();
                 const uint32_t v_base = smem_u32(sV + rv.slot * C::kTile);
-                const uint32_t d_tmem = tmem + C::kPVBase + buf * kD;
 #pragma unroll
-                for (int k = 0; k < kBlk / 16; ++k) {
-                    // A = P in TMEM (8 columns = 16 keys per step); B = V, MN-major SW128, 16 rows per step
-                    const uint64_t bd = smem_desc(v_base + k * 2048, kBlk * 128, 1024, kSwizzle128B);
-                    umma_f16_ts(d_tmem, tmem + rs.slot * kBlk + k * 8, bd, idesc_pv, k != 0);
-                }
-                umma_commit(&pv_full[buf]);
+                for (int k = 0; k < kBlk / 16; ++k)  // A = P (8 TMEM columns = 16 keys per step)
+                    umma_f16_ts(tmem + 256 + pend_g * kD, tmem + pend_g * kBlk + k * 8,
+                                smem_desc(v_base + k * 2048, kBlk * 128, 1024, kSwizzle128B), idesc_pv,
+                                (!pend_first || k != 0) ? 1u : 0u);
                 umma_commit(&v_empty[rv.slot]);
-                umma_commit(&s_free[rs.slot]);
+                umma_commit(&pv_done[pend_g]);
+                pend_g = -1;
             };
-            uint32_t it = 0, blk = 0;
-            for (uint32_t t = blockIdx.x; t < items; t += gridDim.x, ++it) {
-                int64_t row0;
-                int qb;
-                decode(t, row0, qb);
-                const Ring rq = ring<R>(it);
-                mbar_wait(&q_full[rq.slot], rq.phase);
-                const uint32_t q_base = smem_u32(sQ + rq.slot * C::kTile);
-                for (int j = 0; j <= qb; ++j, ++blk) {
-                    const Ring rk = ring<R>(blk);
-                    const Ring rs = ring<NS>(blk);
-                    const uint32_t buf = rs.slot;
-                    // With one S/P buffer, S(blk) reuses the buffer PV(blk-1) reads: issue PV first.
-                    if (NS == 1 && blk > 0) issue_pv(blk - 1);
-                    mbar_wait(&k_full[rk.slot], rk.phase);
-                    mbar_wait(&s_free[buf], rs.phase ^ 1u);
+            while (st[0].active || st[1].active) {
+                if (!st[g].active) g ^= 1;
+                Stream &s = st[g];
+                const int j = s.j;
+                const Ring rq = ring<NQ>(qcnt[g]);
+                const uint32_t qslot = g * NQ + rq.slot;
+                const Ring rkv = ring<NKV>(kv);
+                if (warp == 0) {
+                    // ------------------------------ TMA loader ---------------------------------
+                    if (j == 0) {
+                        mbar_wait(&q_empty[qslot], rq.phase ^ 1u);
+                        mbar_arrive_expect_tx(&q_full[qslot], C::kTile);
+                        for (int h = 0; h < kD / 64; ++h)
+                            tma_load_2d(smem_u32(sQ + qslot * C::kTile + h * (kBlk * 128)), &tmQ, &q_full[qslot],
+                                        h * 64, (int32_t)(s.row0 + s.qb * kBlk));
+                    }
+                    mbar_wait(&k_empty[rkv.slot], rkv.phase ^ 1u);
+                    mbar_arrive_expect_tx(&k_full[rkv.slot], C::kTile);
+                    for (int h = 0; h < kD / 64; ++h)
+                        tma_load_2d(smem_u32(sK + rkv.slot * C::kTile + h * (kBlk * 128)), &tmK, &k_full[rkv.slot],
+                                    h * 64, (int32_t)(s.row0 + j * kBlk));
+                    mbar_wait(&v_empty[rkv.slot], rkv.phase ^ 1u);
+                    mbar_arrive_expect_tx(&v_full[rkv.slot], C::kTile);
+                    for (int h = 0; h < kD / 64; ++h)
+                        tma_load_2d(smem_u32(sV + rkv.slot * C::kTile + h * (kBlk * 128)), &tmV, &v_full[rkv.slot],
+                                    h * 64, (int32_t)(s.row0 + j * kBlk));
+                } else {
+                    // ------------------------------ MMA issuer ---------------------------------
+                    if (pend_g == g) issue_pv();
+                    if (j == 0) mbar_wait(&q_full[qslot], rq.phase);
+                    mbar_wait(&k_full[rkv.slot], rkv.phase);
+                    if (bcnt[g] > 0) mbar_wait(&pv_done[g], (bcnt[g] - 1) & 1u);  // S/P buffer free
                     tc_fence_after();
-                    const uint32_t k_base = smem_u32(sK + rk.slot * C::kTile);
+                    const uint32_t q_base = smem_u32(sQ + qslot * C::kTile);
+                    const uint32_t k_base = smem_u32(sK + rkv.slot * C::kTile);
 #pragma unroll
                     for (int k = 0; k < kD / 16; ++k) {
                         const uint32_t off = (k >> 2) * (kBlk * 128) + (k & 3) * 32;
-                        umma_f16(tmem + buf * kBlk, smem_desc(q_base + off, 16, 1024, kSwizzle128B),
+                        umma_f16(tmem + g * kBlk, smem_desc(q_base + off, 16, 1024, kSwizzle128B),
                                  smem_desc(k_base + off, 16, 1024, kSwizzle128B), idesc_s, k != 0);
                     }
-                    umma_commit(&s_full[buf]);
-                    umma_commit(&k_empty[rk.slot]);
-                    if (j == qb) umma_commit(&q_empty[rq.slot]);
-                    if (NS > 1 && blk > 0) issue_pv(blk - 1);
+                    umma_commit(&s_full[g]);
+                    umma_commit(&k_empty[rkv.slot]);
+                    if (j == s.qb) umma_commit(&q_empty[qslot]);
+                    if (pend_g >= 0) issue_pv();  // the other group's PV overlaps this group's softmax
+                    pend_g = g;
+                    pend_kv = kv;
+                    pend_b = bcnt[g];
+                    pend_first = j == 0;
                 }
+                ++bcnt[g];
+                ++kv;
+                if (s.advance()) ++qcnt[g];
+                g ^= 1;
             }
-            if (blk > 0) issue_pv(blk - 1);
+            if (warp == 1 && pend_g >= 0) issue_pv();
         }
     } else {
-        // ------------------------------ softmax + epilogue -----------------------------------
-        const int q = warp & 3;
+        // ------------------------------ softmax + epilogue (one WG per stream) -------------------
+        const int g = (warp - 2) >> 2;
+        const int q = warp & 3;       // TMEM lane quarter
         const int r = q * 32 + lane;  // query row inside the block == TMEM lane
         const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+        const uint32_t s_addr = tmem + lane_addr + g * kBlk;
+        const uint32_t o_addr = tmem + lane_addr + 256 + g * kD;
         const float sl2 = a.scale * 1.4426950408889634f;  // scale * log2(e)
         uint16_t *O = (uint16_t *)a.O;
         const bool bf16 = a.dt == ATTNCACHE_BF16;
-        float o[kD];
-#pragma unroll
-        for (int c = 0; c < kD; ++c) o[c] = 0.f;
-        float m = -INFINITY, l = 0.f;  // running statistics of the current item
-        int64_t prev_row0 = 0;         // item whose last PV is pending
-        int prev_qb = 0;
-        float prev_l = 1.f;
-        float alpha = 1.f;
-        bool pend = false, pend_last = false;
-        uint32_t blk = 0;
-
-        // Folds PV of block blk-1 into o (rescaled by `alpha` unless it closed its item; then the
-        // item's epilogue normalises, rounds and stores O and o restarts from zero).
-        auto fold_pending = [&]() {
-            const uint32_t pb = (blk - 1) & 1u, pph = ((blk - 1) >> 1) & 1u;
-            mbar_wait(&pv_full[pb], pph);
+        Stream s;
+        s.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, a.list.rows);
+        uint32_t b = 0;  // key blocks of this stream
+        float m_ref = 0.f, l = 0.f;
+        while (s.active) {
+            const int j = s.j;
+            const bool diag = j == s.qb;
+            const int lim = diag ? r : kBlk - 1;            // keys k <= lim are visible (causal mask)
+            const int n_chunks = diag ? q + 1 : kBlk / 32;  // warp-uniform: 32-key chunks with visible keys
+            mbar_wait(&s_full[g], b & 1u);
             tc_fence_after();
-            const float al = pend_last ? 1.f : alpha;
-#pragma unroll
-            for (int c = 0; c < kD / 32; ++c) {
+            float mx = -INFINITY;
+            for (int c = 0; c < n_chunks; ++c) {
                 uint32_t v[32];
-                tmem_ld_32x32b_x32(tmem + lane_addr + C::kPVBase + pb * kD + c * 32, v);
+                tmem_ld_32x32b_x32(s_addr + c * 32, v);
                 tmem_ld_wait();
+                float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int e = 0; e < 32; ++e) o[c * 32 + e] = (o[c * 32 + e] + __uint_as_float(v[e])) * al;
+                for (int e = 0; e < 32; ++e)
+                    if (c * 32 + e <= lim) m4[e & 3] = fmaxf(m4[e & 3], __uint_as_float(v[e]));
+                mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
             }
-            tc_fence_before();
-            mbar_arrive(&pv_empty[pb]);
-            if (pend_last) {
-                const float inv = 1.f / prev_l;
-                uint16_t *dst = O + (prev_row0 + prev_qb * kBlk + r) * (int64_t)kD;
-#pragma unroll
-                for (int c16 = 0; c16 < kD / 16; ++c16) {  // 32-byte stores: whole sectors, no partial writes
-                    uint32_t w[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const float lo = o[c16 * 16 + 2 * e] * inv, hi = o[c16 * 16 + 2 * e + 1] * inv;
-                        if (bf16) {
-                            __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
-                            w[e] = *reinterpret_cast<uint32_t *>(&h2);
-                        } else {
-                            __half2 h2 = __floats2half2_rn(lo, hi);
-                            w[e] = *reinterpret_cast<uint32_t *>(&h2);
-                        }
-                    }
-                    st_global_v8(dst + c16 * 16, w);
-                }
-#pragma unroll
-                for (int c = 0; c < kD; ++c) o[c] = 0.f;
-            }
-        };
-
-        for (uint32_t t = blockIdx.x; t < items; t += gridDim.x) {
-            int64_t row0;
-            int qb;
-            decode(t, row0, qb);
-            m = -INFINITY;
-            l = 0.f;
-            for (int j = 0; j <= qb; ++j, ++blk) {
-                const Ring rsb = ring<NS>(blk);
-                const uint32_t buf = rsb.slot, bph = rsb.phase;
-                const bool diag = j == qb;
-                const int lim = diag ? r : kBlk - 1;            // keys k <= lim are visible (causal mask)
-                const int n_chunks = diag ? q + 1 : kBlk / 32;  // warp-uniform: 32-key chunks with visible keys
-                mbar_wait(&s_full[buf], bph);
+            const float m_blk = mx * sl2;
+            if (j == 0) {
+                m_ref = m_blk;
+                l = 0.f;
+            } else if (m_blk > m_ref + kRescaleThreshold) {
+                // lazy rescale of O (every PV so far; complete once the previous PV retired) and l
+                const float alpha = ex2(m_ref - m_blk);
+                mbar_wait(&pv_done[g], (b - 1) & 1u);
                 tc_fence_after();
-                const uint32_t s_addr = tmem + lane_addr + buf * kBlk;
-                float mx = -INFINITY;
-                for (int c = 0; c < n_chunks; ++c) {
+#pragma unroll
+                for (int c = 0; c < kD / 32; ++c) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(o_addr + c * 32, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t w[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) w[e] = __float_as_uint(__uint_as_float(v[h * 16 + e]) * alpha);
+                        tmem_st_32x32b_x16(o_addr + c * 32 + h * 16, w);
+                    }
+                }
+                l *= alpha;
+                m_ref = m_blk;
+            }
+            float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int c = 0; c < kBlk / 32; ++c) {
+                uint32_t w[16];
+                if (c < n_chunks) {
                     uint32_t v[32];
                     tmem_ld_32x32b_x32(s_addr + c * 32, v);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (c * 32 + e <= lim) mx = fmaxf(mx, __uint_as_float(v[e]));
+                    for (int e = 0; e < 16; ++e) {
+                        const int k0 = c * 32 + 2 * e;
+                        const float p0 = k0 <= lim ? ex2(fmaf(__uint_as_float(v[2 * e]), sl2, -m_ref)) : 0.f;
+                        const float p1 = k0 + 1 <= lim ? ex2(fmaf(__uint_as_float(v[2 * e + 1]), sl2, -m_ref)) : 0.f;
+                        if (bf16) {
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                            rs4[e & 3] += __low2float(h2) + __high2float(h2);
+                            w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        } else {
+                            __half2 h2 = __floats2half2_rn(p0, p1);
+                            rs4[e & 3] += __low2float(h2) + __high2float(h2);
+                            w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) w[e] = 0u;
                 }
-                const float m_new = fmaxf(m, mx * sl2);
-                float rs = 0.f;
+                // keys [32c, 32c+32) -> P columns [16c, 16c+16) (those S columns are consumed)
+                tmem_st_32x32b_x16(s_addr + c * 16, w);
+            }
+            l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&p_full[g]);
+            if (diag) {
+                // epilogue: the item's last PV retired -> O / l -> act dtype -> 32-byte stores
+                mbar_wait(&pv_done[g], b & 1u);
+                tc_fence_after();
+                const float inv = 1.f / l;
+                uint16_t *dst = O + (s.row0 + s.qb * kBlk + r) * (int64_t)kD;
 #pragma unroll
-                for (int c = 0; c < kBlk / 32; ++c) {
-                    uint32_t w[16];
-                    if (c < n_chunks) {
-                        uint32_t v[32];
-                        tmem_ld_32x32b_x32(s_addr + c * 32, v);
-                        tmem_ld_wait();
+                for (int c = 0; c < kD / 32; ++c) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(o_addr + c * 32, v);
+                    tmem_ld_wait();
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) {
-                            const int k0 = c * 32 + 2 * e;
-                            const float p0 = k0 <= lim ? ex2(fmaf(__uint_as_float(v[2 * e]), sl2, -m_new)) : 0.f;
-                            const float p1 = k0 + 1 <= lim ? ex2(fmaf(__uint_as_float(v[2 * e + 1]), sl2, -m_new)) : 0.f;
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t w[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const float lo = __uint_as_float(v[h * 16 + 2 * e]) * inv;
+                            const float hi = __uint_as_float(v[h * 16 + 2 * e + 1]) * inv;
                             if (bf16) {
-                                __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                                rs += __low2float(h2) + __high2float(h2);
+                                __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
                                 w[e] = *reinterpret_cast<uint32_t *>(&h2);
                             } else {
-                                __half2 h2 = __floats2half2_rn(p0, p1);
-                                rs += __low2float(h2) + __high2float(h2);
+                                __half2 h2 = __floats2half2_rn(lo, hi);
                                 w[e] = *reinterpret_cast<uint32_t *>(&h2);
                             }
                         }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) w[e] = 0u;
+                        st_global_v8(dst + c * 32 + h * 16, w);
                     }
-                    // keys [32c, 32c+32) -> P columns [16c, 16c+16) (already read as S chunk c/2 <= c)
-                    tmem_st_32x32b_x16(s_addr + c * 16, w);
                 }
-                tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(&p_full[buf]);
-                alpha = ex2(m - m_new);  // 0 on an item's first block (m = -inf)
-                l = l * alpha + rs;
-                m = m_new;
-                if (pend) fold_pending();
-                pend = true;
-                pend_last = diag;
-                if (diag) {
-                    prev_row0 = row0;
-                    prev_qb = qb;
-                    prev_l = l;
-                }
             }
+            ++b;
+            s.advance();
         }
-        if (pend) fold_pending();
     }
     __syncthreads();
     if (warp == 1) {
@@ -340,9 +362,9 @@ __global__ void __launch_bounds__(kThreads, Cfg<kD, kTwoCTA>::kMinBlocks)
     }
 }
 
-template <int kD, bool kTwoCTA>
+template <int kD>
 cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
-    using C = Cfg<kD, kTwoCTA>;
+    using C = Cfg<kD>;
     const bool bf16 = a.dt == ATTNCACHE_BF16;
     const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
     CUtensorMap tq, tk, tv;
@@ -350,12 +372,12 @@ cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
     if (e == cudaSuccess) e = make_tmap_2d_16(&tk, a.K, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e == cudaSuccess) e = make_tmap_2d_16(&tv, a.V, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(attend_tc_kernel<kD, kTwoCTA>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    e = cudaFuncSetAttribute(attend_tc_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     const uint32_t fmt = bf16 ? 1u : 0u;
     const uint32_t idesc_s = idesc_f16(kBlk, kBlk, fmt, 0u, 0u);  // Q K-major x K K-major
     const uint32_t idesc_pv = idesc_f16(kBlk, kD, fmt, 0u, 1u);   // P (TMEM) x V MN-major
-    attend_tc_kernel<kD, kTwoCTA><<<sm_count * C::kMinBlocks, kThreads, C::kSmem, st>>>(tq, tk, tv, a, idesc_s, idesc_pv);
+    attend_tc_kernel<kD><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, tv, a, idesc_s, idesc_pv);
     count_launches(1);
     return cudaGetLastError();
 }
@@ -368,9 +390,9 @@ bool attend_tc_supported(int32_t dt, int32_t S, int32_t d) {
 
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st) {
     const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
-    if (rows >= (1ull << 31) || (uint64_t)a.max_rows * a.L * a.H * (a.S / kBlk) >= (1ull << 32))
+    if (rows >= (1ull << 31) || (uint64_t)a.max_rows * a.L * a.H * (a.S / kBlk) >= (1ull << 31))
         return cudaErrorInvalidValue;
-    return a.d == 64 ? launch<64, true>(a, sm_count, st) : launch<128, false>(a, sm_count, st);
+    return a.d == 64 ? launch<64>(a, sm_count, st) : launch<128>(a, sm_count, st);
 }
 
 }  // namespace ac
