@@ -17,6 +17,8 @@
 #include "kernels.cuh"
 #include "sm100.cuh"
 
+#include <type_traits>
+
 namespace ac {
 using namespace sm100;
 
@@ -82,7 +84,7 @@ struct Stream {
     }
 };
 
-template <int kD>
+template <int kD, bool kBF16>
 __global__ void __launch_bounds__(kThreads, 1)
     attend_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const AttendArgs a, const uint32_t idesc_s,
@@ -144,13 +146,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // The loader (warp 0) and the MMA issuer (warp 1) walk the same merged order of events:
         // one key block of stream 0, one of stream 1, ... (a finished stream is skipped).
         if (lane == 0) {
-            Stream st[2];
-            st[0].init(blockIdx.x, stride, items, units, per_row, n_qb, S, a.list.rows);
-            st[1].init(blockIdx.x + gridDim.x, stride, items, units, per_row, n_qb, S, a.list.rows);
-            uint32_t qcnt[2] = {0, 0};  // items started per stream (Q ring position)
-            uint32_t bcnt[2] = {0, 0};  // key blocks per stream (S/P/PV barrier phases)
-            uint32_t kv = 0;            // key blocks overall (K/V ring position)
-            int g = 0;
+            Stream st0, st1;
+            st0.init(blockIdx.x, stride, items, units, per_row, n_qb, S, a.list.rows);
+            st1.init(blockIdx.x + gridDim.x, stride, items, units, per_row, n_qb, S, a.list.rows);
+            uint32_t qcnt0 = 0, qcnt1 = 0;  // items started per stream (Q ring position)
+            uint32_t bcnt0 = 0, bcnt1 = 0;  // key blocks per stream (S/P/PV barrier phases)
+            uint32_t kv = 0;                // key blocks overall (K/V ring position)
             // MMA: PV of an event is issued after the S of the next event (ping-pong) unless the
             // next event belongs to the same group (its S needs the S/P buffer that PV reads).
             int pend_g = -1;
@@ -171,11 +172,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma_commit(&pv_done[pend_g]);
                 pend_g = -1;
             };
-            while (st[0].active || st[1].active) {
-                if (!st[g].active) g ^= 1;
-                Stream &s = st[g];
+            // one key block of stream g (g is a compile-time constant at each call site)
+            auto event = [&](Stream &s, const int g, uint32_t &qcnt, uint32_t &bcnt) {
                 const int j = s.j;
-                const Ring rq = ring<NQ>(qcnt[g]);
+                const Ring rq = ring<NQ>(qcnt);
                 const uint32_t qslot = g * NQ + rq.slot;
                 const Ring rkv = ring<NKV>(kv);
                 if (warp == 0) {
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (pend_g == g) issue_pv();
                     if (j == 0) mbar_wait(&q_full[qslot], rq.phase);
                     mbar_wait(&k_full[rkv.slot], rkv.phase);
-                    if (bcnt[g] > 0) mbar_wait(&pv_done[g], (bcnt[g] - 1) & 1u);  // S/P buffer free
+                    if (bcnt > 0) mbar_wait(&pv_done[g], (bcnt - 1) & 1u);  // S/P buffer free
                     tc_fence_after();
                     const uint32_t q_base = smem_u32(sQ + qslot * C::kTile);
                     const uint32_t k_base = smem_u32(sK + rkv.slot * C::kTile);
@@ -218,13 +218,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (pend_g >= 0) issue_pv();  // the other group's PV overlaps this group's softmax
                     pend_g = g;
                     pend_kv = kv;
-                    pend_b = bcnt[g];
+                    pend_b = bcnt;
                     pend_first = j == 0;
                 }
-                ++bcnt[g];
+                ++bcnt;
                 ++kv;
-                if (s.advance()) ++qcnt[g];
-                g ^= 1;
+                if (s.advance()) ++qcnt;
+            };
+            while (st0.active || st1.active) {
+                if (st0.active) event(st0, 0, qcnt0, bcnt0);
+                if (st1.active) event(st1, 1, qcnt1, bcnt1);
             }
             if (warp == 1 && pend_g >= 0) issue_pv();
         }
@@ -238,7 +241,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t o_addr = tmem + lane_addr + 256 + g * kD;
         const float sl2 = a.scale * 1.4426950408889634f;  // scale * log2(e)
         uint16_t *O = (uint16_t *)a.O;
-        const bool bf16 = a.dt == ATTNCACHE_BF16;
         Stream s;
         s.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, a.list.rows);
         uint32_t b = 0;  // key blocks of this stream
@@ -250,17 +252,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int n_chunks = diag ? q + 1 : kBlk / 32;  // warp-uniform: 32-key chunks with visible keys
             mbar_wait(&s_full[g], b & 1u);
             tc_fence_after();
+            // Diagonal blocks mask keys k > r per lane; the others take the unpredicated path.
             float mx = -INFINITY;
-            for (int c = 0; c < n_chunks; ++c) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(s_addr + c * 32, v);
-                tmem_ld_wait();
-                float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            auto max_pass = [&](auto masked) {
+                for (int c = 0; c < n_chunks; ++c) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(s_addr + c * 32, v);
+                    tmem_ld_wait();
+                    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int e = 0; e < 32; ++e)
-                    if (c * 32 + e <= lim) m4[e & 3] = fmaxf(m4[e & 3], __uint_as_float(v[e]));
-                mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
-            }
+                    for (int e = 0; e < 32; ++e)
+                        if (!decltype(masked)::value || c * 32 + e <= lim)
+                            m4[e & 3] = fmaxf(m4[e & 3], __uint_as_float(v[e]));
+                    mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
+                }
+            };
+            if (diag)
+                max_pass(std::true_type{});
+            else
+                max_pass(std::false_type{});
             const float m_blk = mx * sl2;
             if (j == 0) {
                 m_ref = m_blk;
@@ -286,36 +296,48 @@ __global__ void __launch_bounds__(kThreads, 1)
                 l *= alpha;
                 m_ref = m_blk;
             }
+            // p = exp2(s * scale * log2e - m_ref), rounded to the MMA dtype and written over the
+            // consumed S columns; l sums the unrounded p (an unbiased estimate of the rounded sum,
+            // within 2^-9 relative; keeps the row sum off the critical path).
             float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+            auto exp_pass = [&](auto masked) {
 #pragma unroll
-            for (int c = 0; c < kBlk / 32; ++c) {
-                uint32_t w[16];
-                if (c < n_chunks) {
-                    uint32_t v[32];
-                    tmem_ld_32x32b_x32(s_addr + c * 32, v);
-                    tmem_ld_wait();
+                for (int c = 0; c < kBlk / 32; ++c) {
+                    uint32_t w[16];
+                    if (c < n_chunks) {
+                        uint32_t v[32];
+                        tmem_ld_32x32b_x32(s_addr + c * 32, v);
+                        tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int k0 = c * 32 + 2 * e;
-                        const float p0 = k0 <= lim ? ex2(fmaf(__uint_as_float(v[2 * e]), sl2, -m_ref)) : 0.f;
-                        const float p1 = k0 + 1 <= lim ? ex2(fmaf(__uint_as_float(v[2 * e + 1]), sl2, -m_ref)) : 0.f;
-                        if (bf16) {
-                            __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                            rs4[e & 3] += __low2float(h2) + __high2float(h2);
-                            w[e] = *reinterpret_cast<uint32_t *>(&h2);
-                        } else {
-                            __half2 h2 = __floats2half2_rn(p0, p1);
-                            rs4[e & 3] += __low2float(h2) + __high2float(h2);
-                            w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        for (int e = 0; e < 16; ++e) {
+                            const int k0 = c * 32 + 2 * e;
+                            float p0 = ex2(fmaf(__uint_as_float(v[2 * e]), sl2, -m_ref));
+                            float p1 = ex2(fmaf(__uint_as_float(v[2 * e + 1]), sl2, -m_ref));
+                            if (decltype(masked)::value) {
+                                p0 = k0 <= lim ? p0 : 0.f;
+                                p1 = k0 + 1 <= lim ? p1 : 0.f;
+                            }
+                            rs4[e & 3] += p0 + p1;
+                            if constexpr (kBF16) {
+                                __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                                w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                            } else {
+                                __half2 h2 = __floats2half2_rn(p0, p1);
+                                w[e] = *reinterpret_cast<uint32_t *>(&h2);
+                            }
                         }
-                    }
-                } else {
+                    } else {
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) w[e] = 0u;
+                        for (int e = 0; e < 16; ++e) w[e] = 0u;
+                    }
+                    // keys [32c, 32c+32) -> P columns [16c, 16c+16) (those S columns are consumed)
+                    tmem_st_32x32b_x16(s_addr + c * 16, w);
                 }
-                // keys [32c, 32c+32) -> P columns [16c, 16c+16) (those S columns are consumed)
-                tmem_st_32x32b_x16(s_addr + c * 16, w);
-            }
+            };
+            if (diag)
+                exp_pass(std::true_type{});
+            else
+                exp_pass(std::false_type{});
             l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
             tmem_st_wait();
             tc_fence_before();
@@ -338,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int e = 0; e < 8; ++e) {
                             const float lo = __uint_as_float(v[h * 16 + 2 * e]) * inv;
                             const float hi = __uint_as_float(v[h * 16 + 2 * e + 1]) * inv;
-                            if (bf16) {
+                            if constexpr (kBF16) {
                                 __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
                                 w[e] = *reinterpret_cast<uint32_t *>(&h2);
                             } else {
@@ -362,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int kD>
+template <int kD, bool kBF16>
 cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
     using C = Cfg<kD>;
     const bool bf16 = a.dt == ATTNCACHE_BF16;
@@ -372,12 +394,12 @@ cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
     if (e == cudaSuccess) e = make_tmap_2d_16(&tk, a.K, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e == cudaSuccess) e = make_tmap_2d_16(&tv, a.V, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(attend_tc_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    e = cudaFuncSetAttribute(attend_tc_kernel<kD, kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     const uint32_t fmt = bf16 ? 1u : 0u;
     const uint32_t idesc_s = idesc_f16(kBlk, kBlk, fmt, 0u, 0u);  // Q K-major x K K-major
     const uint32_t idesc_pv = idesc_f16(kBlk, kD, fmt, 0u, 1u);   // P (TMEM) x V MN-major
-    attend_tc_kernel<kD><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, tv, a, idesc_s, idesc_pv);
+    attend_tc_kernel<kD, kBF16><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, tv, a, idesc_s, idesc_pv);
     count_launches(1);
     return cudaGetLastError();
 }
@@ -392,7 +414,8 @@ cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st)
     const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
     if (rows >= (1ull << 31) || (uint64_t)a.max_rows * a.L * a.H * (a.S / kBlk) >= (1ull << 31))
         return cudaErrorInvalidValue;
-    return a.d == 64 ? launch<64>(a, sm_count, st) : launch<128>(a, sm_count, st);
+    if (a.d == 64) return launch_attend_tc64(a, sm_count, st);
+    return a.dt == ATTNCACHE_BF16 ? launch<128, true>(a, sm_count, st) : launch<128, false>(a, sm_count, st);
 }
 
 }  // namespace ac
