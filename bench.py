@@ -301,6 +301,14 @@ def run_ours(args, cfg):
                                           "full_attention_ms": full_ms, "paper_context": PAPER_CONTEXT},
             "search_qps": cfg.B / (search_ms * 1e-3),
             "stages": secondary, "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+    # paper-comparable baseline: eager torch attention (matmul -> masked softmax -> matmul, the
+    # unfused attention of PAPER.md Table 4's "AM" + "AM.V" rows) on every row of the batch
+    eager_ms = eager_attention_ms(Q, K, V, stream, max(2, args.steps // 2))
+    line["speedup_vs_full_attention"]["eager_torch_attention_ms"] = eager_ms
+    line["speedup_vs_full_attention"]["batch_vs_eager_torch"] = eager_ms / ms
+    del O_full
+    if not args.no_search_sweep:
+        line["search_sweep"] = search_sweep(ac, ctx, dev, stream, max(3, args.steps), peaks)
     if not args.no_cpu_baseline:
         import oracle
         oracle.set_threads(os.cpu_count() or 1)
@@ -309,6 +317,57 @@ def run_ours(args, cfg):
                                 "sample": desc}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def eager_attention_ms(Q, K, V, stream, steps):
+    """Unfused torch attention (a comparison point, not this library's path)."""
+    S = Q.shape[-2]
+    mask = torch.triu(torch.ones(S, S, dtype=torch.bool, device=Q.device), diagonal=1)
+    scale = 1.0 / math.sqrt(Q.shape[-1])
+
+    def run():
+        s = torch.matmul(Q, K.transpose(-1, -2)) * scale
+        s.masked_fill_(mask, float("-inf"))
+        return torch.matmul(torch.softmax(s, dim=-1, dtype=torch.float32).to(V.dtype), V)
+
+    run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def search_sweep(ac, ctx, dev, stream, steps, peaks):
+    """BASELINE.json configs[4]: exact top-1 over 1M x 1024 bf16 features at B = 1/64/1024/8192
+    (half planted hits); search QPS and roofline fractions (K1 + K2)."""
+    cfg = synth.CONFIGS["search_sweep"]
+    x = synth.features(cfg, 0, cfg.N, dev)
+    db = ac.Database(ctx, x)
+    out = {"workload": "search_sweep (BASELINE.json configs[4])", "N": cfg.N, "D": cfg.D, "points": []}
+    for B in (1, 64, 1024, 8192):
+        q, pos, _ = synth.queries(cfg, dev, B=B)
+        idx, score, hit = ac.attncache_search(db, q, cfg.tau)
+        for _ in range(2):
+            ac.attncache_search(db, q, cfg.tau, idx, score, hit)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            ac.attncache_search(db, q, cfg.tau, idx, score, hit)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        nbytes = (cfg.N + B) * cfg.D * 2 + 8 * B
+        flops = 2.0 * B * cfg.N * cfg.D
+        out["points"].append({"B": B, "ms": ms, "qps": B / (ms * 1e-3), "hits": int(hit.sum().item()),
+                              "planted_hits": len(pos),
+                              "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                              "tensor_frac": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                              "variant": ac.attncache_variant("search", q.dtype, 0, cfg.D)})
+    del db, x
+    return out
 
 
 def run_dist(args, cfg):
@@ -442,6 +501,7 @@ def main(argv=None):
     ap.add_argument("--config", default="llama32_1b", choices=[k for k in synth.CONFIGS if k != "search_sweep"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-search-sweep", action="store_true", help="skip the configs[4] search-QPS sweep")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("bench.py: note: --warmup < 3 does not meet the timing rules (profiling runs only)", file=sys.stderr)

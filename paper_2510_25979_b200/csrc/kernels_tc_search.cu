@@ -2,10 +2,10 @@
 //
 // s[b][i] = sum_k q[b][k] x[i][k] (bf16 inputs, fp32 accumulation in TMEM) over this shard,
 // reduced on the fly to one packed (score, index) key per query (reading R3): the score matrix is
-// never written to memory.  Work item = (128-query tile, 128-entry tile), ordered entry-tile-major
-// so concurrently running CTAs share the same DB rows through L2 (the DB streams from HBM once).
-// Roles (192 threads): warp 0 TMA loader, warp 1 MMA issuer (M=128 queries, N=128 entries, K=16),
-// warps 2-5 epilogue: each thread owns one query (= TMEM lane), scans its 128 scores in ascending
+// never written to memory.  Work item = (128-query tile, 64/128/256-entry tile), ordered
+// entry-tile-major so concurrently running CTAs share the same DB rows through L2 (the DB streams
+// from HBM once).  Roles (192 threads): warp 0 TMA loader, warp 1 MMA issuer (M=128 queries,
+// N=entry tile, K=16), warps 2-5 epilogue: each thread owns one query (= TMEM lane), scans its scores in ascending
 // entry order keeping the first maximum, and merges with atomicMax on the packed key.
 #include "kernels.cuh"
 #include "sm100.cuh"
@@ -17,18 +17,27 @@ namespace {
 
 constexpr int kThreads = 192;
 constexpr int kTileQ = 128;
-constexpr int kTileE = 128;
 constexpr int kChunk = 64;                       // K elements per stage (one 128-byte swizzle row)
 constexpr int kQBytes = kTileQ * kChunk * 2;
-constexpr int kXBytes = kTileE * kChunk * 2;
-constexpr int kStageBytes = kQBytes + kXBytes;
-constexpr int kStages = 6;
-constexpr uint32_t kTmemCols = 2 * kTileE;
-constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
 
+// Entry-tile width kTileE in {64, 128, 256}: wide tiles cut the L2 re-reads of the query tile for
+// large batches (tensor-bound); narrow tiles give small searches enough CTAs.
+template <int kTileE>
+struct Cfg {
+    static constexpr int kXBytes = kTileE * kChunk * 2;
+    static constexpr int kStageBytes = kQBytes + kXBytes;
+    static constexpr int kStages = kTileE == 256 ? 4 : kTileE == 128 ? 6 : 8;
+    static constexpr uint32_t kTmemCols = 2 * kTileE;  // double-buffered fp32 accumulator
+    static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+};
+
+template <int kTileE>
 __global__ void __launch_bounds__(kThreads, 1)
     search_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX, int64_t B,
                      int64_t n, int D, int64_t gbase, unsigned long long *keys, uint32_t idesc) {
+    using C = Cfg<kTileE>;
+    constexpr int kStages = C::kStages, kStageBytes = C::kStageBytes;
+    constexpr uint32_t kTmemCols = C::kTmemCols;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *full = (uint64_t *)(smem + kStages * kStageBytes);
@@ -145,21 +154,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 bool search_tc_supported(int32_t dt, int32_t D) { return dt == ATTNCACHE_BF16 && D >= kChunk && D % kChunk == 0; }
 
-cudaError_t launch_search_tc(const void *q, const void *x, int64_t B, int64_t n, int32_t D, int64_t gbase,
-                             uint64_t *keys, int sm_count, cudaStream_t st) {
-    if (B == 0 || n == 0) return cudaSuccess;
+template <int kTileE>
+static cudaError_t launch_t(const void *q, const void *x, int64_t B, int64_t n, int32_t D, int64_t gbase,
+                           uint64_t *keys, int sm_count, cudaStream_t st) {
+    using C = Cfg<kTileE>;
     CUtensorMap tq, tx;
     cudaError_t e = make_tmap_2d_16(&tq, q, true, D, B, (uint64_t)D * 2, kChunk, kTileQ, 128);
     if (e == cudaSuccess) e = make_tmap_2d_16(&tx, x, true, D, n, (uint64_t)D * 2, kChunk, kTileE, 128);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(search_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    e = cudaFuncSetAttribute(search_tc_kernel<kTileE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     const int64_t items = ((B + kTileQ - 1) / kTileQ) * ((n + kTileE - 1) / kTileE);
     const int grid = (int)min64(items, sm_count);
     const uint32_t idesc = idesc_f16(kTileQ, kTileE, 1u, 0u, 0u);
-    search_tc_kernel<<<grid, kThreads, kSmem, st>>>(tq, tx, B, n, D, gbase, (unsigned long long *)keys, idesc);
+    search_tc_kernel<kTileE><<<grid, kThreads, C::kSmem, st>>>(tq, tx, B, n, D, gbase, (unsigned long long *)keys, idesc);
     count_launches(1);
     return cudaGetLastError();
+}
+
+cudaError_t launch_search_tc(const void *q, const void *x, int64_t B, int64_t n, int32_t D, int64_t gbase,
+                             uint64_t *keys, int sm_count, cudaStream_t st) {
+    if (B == 0 || n == 0) return cudaSuccess;
+    // the widest entry tile that still gives every SM at least two work items
+    const int64_t n_qt = (B + kTileQ - 1) / kTileQ;
+    if (n_qt * ((n + 255) / 256) >= 2 * sm_count) return launch_t<256>(q, x, B, n, D, gbase, keys, sm_count, st);
+    if (n_qt * ((n + 127) / 128) >= 2 * sm_count) return launch_t<128>(q, x, B, n, D, gbase, keys, sm_count, st);
+    return launch_t<64>(q, x, B, n, D, gbase, keys, sm_count, st);
 }
 
 }  // namespace ac
