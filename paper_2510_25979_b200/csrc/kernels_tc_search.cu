@@ -34,7 +34,7 @@ struct Cfg {
 template <int kTileE>
 __global__ void __launch_bounds__(kThreads, 1)
     search_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX, int64_t B,
-                     int64_t n, int D, int64_t gbase, unsigned long long *keys, uint32_t idesc) {
+                     int64_t n, int D, int64_t gbase, unsigned long long *keys, uint32_t idesc, uint32_t q_rows) {
     using C = Cfg<kTileE>;
     constexpr int kStages = C::kStages, kStageBytes = C::kStageBytes;
     constexpr uint32_t kTmemCols = C::kTmemCols;
@@ -81,7 +81,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
                     const uint32_t s = cnt % kStages, ph = (cnt / kStages) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
-                    mbar_arrive_expect_tx(&full[s], kStageBytes);
+                    // small batches load only q_rows query rows; the MMA's other rows read stale shared
+                    // memory, which only reaches TMEM lanes the epilogue never reads (b >= B)
+                    mbar_arrive_expect_tx(&full[s], (q_rows + kTileE) * (kChunk * 2));
                     const uint32_t base = smem_u32(smem + s * kStageBytes);
                     tma_load_2d(base, &tmQ, &full[s], kc * kChunk, qt * kTileQ);
                     tma_load_2d(base + kQBytes, &tmX, &full[s], kc * kChunk, et * kTileE);
@@ -159,7 +161,8 @@ static cudaError_t launch_t(const void *q, const void *x, int64_t B, int64_t n, 
                            uint64_t *keys, int sm_count, cudaStream_t st) {
     using C = Cfg<kTileE>;
     CUtensorMap tq, tx;
-    cudaError_t e = make_tmap_2d_16(&tq, q, true, D, B, (uint64_t)D * 2, kChunk, kTileQ, 128);
+    const uint32_t q_rows = B >= kTileQ ? kTileQ : (uint32_t)((B + 7) / 8 * 8);
+    cudaError_t e = make_tmap_2d_16(&tq, q, true, D, B, (uint64_t)D * 2, kChunk, q_rows, 128);
     if (e == cudaSuccess) e = make_tmap_2d_16(&tx, x, true, D, n, (uint64_t)D * 2, kChunk, kTileE, 128);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(search_tc_kernel<kTileE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
@@ -167,7 +170,8 @@ static cudaError_t launch_t(const void *q, const void *x, int64_t B, int64_t n, 
     const int64_t items = ((B + kTileQ - 1) / kTileQ) * ((n + kTileE - 1) / kTileE);
     const int grid = (int)min64(items, sm_count);
     const uint32_t idesc = idesc_f16(kTileQ, kTileE, 1u, 0u, 0u);
-    search_tc_kernel<kTileE><<<grid, kThreads, C::kSmem, st>>>(tq, tx, B, n, D, gbase, (unsigned long long *)keys, idesc);
+    search_tc_kernel<kTileE><<<grid, kThreads, C::kSmem, st>>>(tq, tx, B, n, D, gbase, (unsigned long long *)keys, idesc,
+                                                             q_rows);
     count_launches(1);
     return cudaGetLastError();
 }
