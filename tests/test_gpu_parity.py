@@ -412,3 +412,25 @@ def test_sharded_prefill_world1_matches_single_gpu_step(ac, ctx):
         assert torch.equal(O1, O2)
     finally:
         dist.destroy_process_group()
+
+
+def test_host_prefill_pipeline_matches_device_step(ac, ctx):
+    """pipeline.HostPrefill (pinned host buffers, chunked copies overlapping the kernels, ragged last
+    chunk) returns exactly what the device-resident step computes."""
+    from paper_2510_25979_b200.pipeline import HostPrefill, PrefillStep
+    cfg = synth.CONFIGS["llama32_1b"].with_(N=48, B=37, L=2)
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    maps = ac.attncache_pack_maps(synth.maps(cfg, 0, cfg.N, DEV))
+    db = ac.Database(ctx, x, maps, packed=True, seq_len=cfg.S)
+    q, _, _ = synth.queries(cfg, DEV)
+    Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qkv")
+    step = PrefillStep(ctx, db, cfg.tau)
+    O_dev = torch.empty_like(V)
+    ref = step(q, Q, K, V, O_dev)
+    Oh = torch.empty(V.shape, dtype=V.dtype).pin_memory()
+    got = HostPrefill(step, chunk=8, depth=2)(q.cpu().pin_memory(), Q.cpu().pin_memory(), K.cpu().pin_memory(),
+                                               V.cpu().pin_memory(), Oh)
+    torch.cuda.synchronize()
+    for r, g in zip(ref, got):
+        assert torch.equal(r.cpu(), g)
+    assert torch.equal(O_dev.cpu(), Oh)
