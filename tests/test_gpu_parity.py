@@ -434,3 +434,26 @@ def test_host_prefill_pipeline_matches_device_step(ac, ctx):
     for r, g in zip(ref, got):
         assert torch.equal(r.cpu(), g)
     assert torch.equal(O_dev.cpu(), Oh)
+
+
+def test_repeat_runs_are_bitwise_identical(ac, ctx):
+    """racecheck does not see the async proxy (TMA/tcgen05), so every tensor-core
+    kernel is re-run on identical inputs and must reproduce its output bit for bit."""
+    for name in ("llama32_1b", "llama3_8b"):
+        cfg = synth.CONFIGS[name].with_(N=24, B=10, L=2)
+        x = synth.features(cfg, 0, cfg.N, DEV)
+        maps = ac.attncache_pack_maps(synth.maps(cfg, 0, cfg.N, DEV))
+        db = ac.Database(ctx, x, maps, packed=True, seq_len=cfg.S)
+        q, _, _ = synth.queries(cfg, DEV)
+        Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qkv")
+        idx0 = torch.arange(cfg.B, device=DEV) % cfg.N
+        ref = None
+        for _ in range(20):
+            s = ac.attncache_search(db, q, cfg.tau)
+            Oa = ac.attncache_apply_cached(db, idx0, V)
+            Of = ac.attncache_attend_full(ctx, Q, K, V)
+            cur = (*s, Oa, Of)
+            if ref is None:
+                ref = tuple(t.clone() for t in cur)
+            else:
+                assert all(torch.equal(a, b) for a, b in zip(ref, cur)), name
