@@ -301,6 +301,8 @@ def run_ours(args, cfg):
                                           "full_attention_ms": full_ms, "paper_context": PAPER_CONTEXT},
             "search_qps": cfg.B / (search_ms * 1e-3),
             "stages": secondary, "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+    # §8(f) f1, DB building: capture the misses' maps (Q, K -> packed bf16 DB entries)
+    secondary["capture_misses"] = capture_stage(ac, ctx, cfg, Q, K, hit, stream, max(3, args.steps), peaks)
     # paper-comparable baseline: eager torch attention (matmul -> masked softmax -> matmul, the
     # unfused attention of PAPER.md Table 4's "AM" + "AM.V" rows) on every row of the batch
     eager_ms = eager_attention_ms(Q, K, V, stream, max(2, args.steps // 2))
@@ -317,6 +319,26 @@ def run_ours(args, cfg):
                                 "sample": desc}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def capture_stage(ac, ctx, cfg, Q, K, hit, stream, steps, peaks):
+    """DB building (f1): maps of the batch's misses written as PACKED DB entries; HBM roofline on
+    Q + K read and the packed maps written."""
+    P = ac.attncache_packed_map_elems(cfg.S)
+    out = torch.empty(cfg.B, cfg.L, cfg.H, P, dtype=synth.torch_dtype(cfg.map_dtype), device=Q.device)
+    ac.attncache_capture_maps(ctx, Q, K, map_dtype=out.dtype, packed=True, out=out, skip=hit)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        ac.attncache_capture_maps(ctx, Q, K, map_dtype=out.dtype, packed=True, out=out, skip=hit)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    n_miss = int((hit == 0).sum().item())
+    nbytes = n_miss * cfg.L * cfg.H * (2 * cfg.S * cfg.d * Q.element_size() + P * out.element_size())
+    del out
+    return {"ms": ms, "bytes": nbytes, "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+            "variant": ac.attncache_variant("capture", Q.dtype, cfg.S, cfg.d)}
 
 
 def eager_attention_ms(Q, K, V, stream, steps):

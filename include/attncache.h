@@ -175,6 +175,19 @@ attncache_status attncache_attend_full(attncache_ctx *ctx, int64_t batch, int32_
                                        const void *K, const void *V, float scale, const uint8_t *skip, void *O,
                                        void *stream);
 
+/* ---- DB building, capture (Fig. 4 step 1; "collect
+ * the input hidden states and their corresponding attention maps at each layer") --------------
+ * maps_out[b][l][h] = softmax(Q K^T * scale with keys j > i masked), rounded once to map_dtype (the
+ * post-softmax probabilities of the miss branch; reading R12), for every selected row b (skip == NULL
+ * or skip[b] == 0), stored in `map_layout` exactly as a DB entry [n_layers][n_heads][map] (DENSE:
+ * +0.0 above the diagonal); unselected rows untouched.  Q, K: [batch][L][H][S][d] in act_dtype;
+ * scale <= 0 means 1/sqrt(head_dim).  maps_out rows can be handed to attncache_db_load as entries.
+ * Errors: SHAPE (S % 8 != 0 for 16-byte map rows), DTYPE (map_dtype not F16/BF16), ALIGNMENT. */
+attncache_status attncache_capture_maps(attncache_ctx *ctx, int64_t batch, int32_t n_layers, int32_t n_heads,
+                                        int32_t seq_len, int32_t head_dim, int32_t act_dtype, const void *Q,
+                                        const void *K, float scale, const uint8_t *skip, int32_t map_dtype,
+                                        int32_t map_layout, void *maps_out, void *stream);
+
 /* ---- routing helpers for the multi-GPU path (north_star: hits go to the owning GPU) ----
  *
  * route_plan: for rows b in [0, n_rows) with hit[b] != 0, owner[b] = the rank r with
@@ -207,7 +220,7 @@ attncache_status attncache_fetch_maps(attncache_db *db, int64_t idx, int32_t lay
                                       void *out, void *stream);
 
 /* ---- introspection: kernel variant chosen for a call (for tests/bench) ----
- * kind: 0 = search, 1 = apply, 2 = attend.  Returns a static string such as "tc" (tcgen05) or
+ * kind: 0 = search, 1 = apply, 2 = attend, 3 = capture.  Returns a static string such as "tc" (tcgen05) or
  * "ffma" for the arguments given (no launch). */
 const char *attncache_variant(int32_t kind, int32_t dtype, int32_t seq_len, int32_t head_dim);
 

@@ -24,7 +24,7 @@ __all__ = [
     "attncache_db_free", "attncache_search", "attncache_search_keys", "attncache_keys_decode",
     "attncache_apply_cached", "attncache_attend_full", "attncache_route_plan", "attncache_gather_rows",
     "attncache_scatter_rows", "attncache_fetch_maps", "attncache_variant", "attncache_version", "attncache_launch_count",
-    "attncache_packed_map_elems", "attncache_pack_maps", "pack_db_maps",
+    "attncache_packed_map_elems", "attncache_pack_maps", "pack_db_maps", "attncache_capture_maps",
     "ABI_FUNCTIONS",
 ]
 
@@ -38,6 +38,7 @@ ABI_FUNCTIONS = [
     "attncache_search_keys", "attncache_keys_decode", "attncache_apply_cached", "attncache_attend_full",
     "attncache_route_plan", "attncache_gather_rows", "attncache_scatter_rows", "attncache_fetch_maps",
     "attncache_variant", "attncache_launch_count", "attncache_packed_map_elems", "attncache_pack_maps",
+    "attncache_capture_maps",
 ]
 
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -92,6 +93,7 @@ def load_library():
         "attncache_fetch_maps": ([P, I64, I32, I32, P, P], I32),
         "attncache_packed_map_elems": ([I32], I64),
         "attncache_pack_maps": ([P, I64, I32, P, P], I32),
+        "attncache_capture_maps": ([P, I64, I32, I32, I32, I32, I32, P, P, F32, P, I32, I32, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -219,7 +221,7 @@ def attncache_launch_count() -> int:
 
 
 def attncache_variant(kind: str, dtype: torch.dtype, seq_len: int, head_dim: int) -> str:
-    k = {"search": 0, "apply": 1, "attend": 2}[kind]
+    k = {"search": 0, "apply": 1, "attend": 2, "capture": 3}[kind]
     return load_library().attncache_variant(k, _DT[dtype], int(seq_len), int(head_dim)).decode()
 
 
@@ -384,3 +386,23 @@ def pack_db_maps(cfg_maps_fn, n_entries: int, L: int, H: int, S: int, dtype, dev
         cfg_maps_fn(b, stage[:cnt])
         attncache_pack_maps(stage[:cnt], db[b:b + cnt])
     return db
+
+
+def attncache_capture_maps(ctx: Context, Q: torch.Tensor, K: torch.Tensor, map_dtype=torch.bfloat16,
+                           packed: bool = True, out: Optional[torch.Tensor] = None, scale: float = 0.0,
+                           skip: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """DB building (Fig. 4 step 1): the causal softmax maps of Q, K as DB entries
+    [B][L][H][map] (PACKED or DENSE [..][S][S]) in map_dtype."""
+    for t, n in ((Q, "Q"), (K, "K")):
+        _dev(t, n)
+    if Q.shape != K.shape or Q.dim() != 5 or Q.dtype != K.dtype:
+        raise ValueError("Q, K must share one [B][L][H][S][d] shape and dtype")
+    B, Lq, H, S, d = Q.shape
+    if out is None:
+        tail = (attncache_packed_map_elems(S),) if packed else (S, S)
+        out = torch.empty((B, Lq, H, *tail), dtype=map_dtype, device=Q.device)
+    _dev(out, "out")
+    _check(load_library().attncache_capture_maps(ctx.handle, B, Lq, H, S, d, _DT[Q.dtype], _p(Q), _p(K), float(scale),
+                                                 _p(skip), _DT[out.dtype], 1 if packed else 0, _p(out),
+                                                 _stream(stream, Q.device)))
+    return out

@@ -110,6 +110,7 @@ const char *attncache_variant(int32_t kind, int32_t dtype, int32_t seq_len, int3
     case 0: return search_tc_supported(dtype, head_dim) ? "tc" : "ffma";  // head_dim = feat_dim here
     case 1: return apply_tc_supported(dtype, dtype, seq_len, head_dim) ? "tc" : "ffma";
     case 2: return attend_tc_supported(dtype, seq_len, head_dim) ? "tc" : "ffma";
+    case 3: return capture_tc_supported(dtype, seq_len, head_dim) ? "tc" : "ffma";
     }
     return "none";
 }
@@ -374,6 +375,56 @@ attncache_status attncache_attend_full(attncache_ctx *ctx, int64_t batch, int32_
         AC_CUDA(launch_attend_tc(a, ctx->sm_count, st));
     } else {
         AC_CUDA(launch_attend_ffma(a, ctx->sm_count, st));
+    }
+    return ATTNCACHE_OK;
+}
+
+// ---- capture (DB building) ------------------------------------------------------------------
+
+attncache_status attncache_capture_maps(attncache_ctx *ctx, int64_t batch, int32_t L, int32_t H, int32_t S, int32_t dd,
+                                        int32_t act_dtype, const void *Q, const void *K, float scale,
+                                        const uint8_t *skip, int32_t map_dtype, int32_t map_layout, void *maps_out,
+                                        void *stream) {
+    if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "capture_maps: ctx is NULL");
+    if (batch < 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "capture_maps: batch < 0");
+    if (L <= 0 || H <= 0 || S <= 0 || dd <= 0) return fail(ATTNCACHE_ERR_SHAPE, "capture_maps: L=%d H=%d S=%d d=%d", L, H, S, dd);
+    if (S % 8 || S > 8192) return fail(ATTNCACHE_ERR_SHAPE, "capture_maps: seq_len %d (needs S %% 8 == 0, <= 8192)", S);
+    if (!dtype_valid(act_dtype)) return fail(ATTNCACHE_ERR_DTYPE, "capture_maps: act_dtype %d", act_dtype);
+    if (map_dtype != ATTNCACHE_F16 && map_dtype != ATTNCACHE_BF16)
+        return fail(ATTNCACHE_ERR_DTYPE, "capture_maps: map_dtype must be F16 or BF16");
+    if (map_layout != ATTNCACHE_MAPS_DENSE && map_layout != ATTNCACHE_MAPS_PACKED)
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "capture_maps: map_layout %d", map_layout);
+    if (std::isnan(scale)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "capture_maps: scale is NaN");
+    if (batch == 0) return ATTNCACHE_OK;
+    if (!Q || !K || !maps_out) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "capture_maps: NULL Q/K/maps_out");
+    if (!is_device_ptr(Q) || !is_device_ptr(K) || !is_device_ptr(maps_out) || (skip && !is_device_ptr(skip)))
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "capture_maps: Q/K/maps_out/skip must be device memory");
+    if (!aligned16(Q) || !aligned16(K) || !aligned16(maps_out) || ((int64_t)dd * dtype_size(act_dtype)) % 16)
+        return fail(ATTNCACHE_ERR_ALIGNMENT, "capture_maps: base or row pitch not 16-byte aligned");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    attncache_status s = ensure_scratch(ctx->attend_list, rowlist_bytes(batch));
+    if (s) return s;
+    CaptureArgs a;
+    a.L = L;
+    a.H = H;
+    a.S = S;
+    a.d = dd;
+    a.dt = act_dtype;
+    a.map_dt = map_dtype;
+    a.map_layout = map_layout;
+    a.map_stride = map_elems(S, map_layout);
+    a.scale = scale > 0.f ? scale : 1.0f / sqrtf((float)dd);
+    a.Q = Q;
+    a.K = K;
+    a.maps = maps_out;
+    a.list = rowlist_view(ctx->attend_list.ptr, batch);
+    a.max_rows = batch;
+    AC_CUDA(launch_select_attend(skip, batch, a.list, st));
+    if (capture_tc_supported(act_dtype, S, dd)) {
+        AC_CUDA(launch_capture_tc(a, ctx->sm_count, st));
+    } else {
+        AC_CUDA(launch_capture_simt(a, ctx->sm_count, st));
     }
     return ATTNCACHE_OK;
 }

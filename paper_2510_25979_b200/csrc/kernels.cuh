@@ -64,6 +64,21 @@ bool attend_tc_supported(int32_t dt, int32_t S, int32_t d);
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st);
 cudaError_t launch_attend_tc64(const AttendArgs &a, int sm_count, cudaStream_t st);  // d = 64 variant
 
+// ---- capture (DB building: the causal maps of a prefill) ----
+struct CaptureArgs {
+    int32_t L, H, S, d, dt;  // dt: Q/K dtype
+    int32_t map_dt, map_layout;
+    int64_t map_stride;      // elements per S x S map in map_layout
+    float scale;
+    const void *Q, *K;
+    void *maps;              // [rows][L][H][map]
+    RowList list;
+    int64_t max_rows;
+};
+cudaError_t launch_capture_simt(const CaptureArgs &a, int sm_count, cudaStream_t st);
+bool capture_tc_supported(int32_t dt, int32_t S, int32_t d);
+cudaError_t launch_capture_tc(const CaptureArgs &a, int sm_count, cudaStream_t st);
+
 // ---- TMA descriptors (tma_host.cu) ----
 cudaError_t make_tmap_2d_16(CUtensorMap *out, const void *base, bool bf16, uint64_t inner, uint64_t outer,
                             uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);

@@ -317,6 +317,78 @@ cudaError_t launch_attend_ffma(const AttendArgs &a, int sm_count, cudaStream_t s
 }
 
 // ============================================================================================
+// capture (CUDA cores): one warp per query row i of a unit; P_ij = exp(z_ij - m) / sum, j <= i,
+// rounded to the map dtype; entries j > i that the layout stores are written as +0.0.
+// ============================================================================================
+template <int DT, int MDT>
+__global__ void __launch_bounds__(256) capture_simt_kernel(CaptureArgs a) {
+    using T = typename Elem<DT>::T;
+    using MT = typename Elem<MDT>::T;
+    extern __shared__ float sp[];  // [warps][S]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float *p = sp + (int64_t)warp * a.S;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t count = *a.list.count;
+    const int64_t units_per_row = (int64_t)a.L * a.H;
+    const int64_t total = count * units_per_row * a.S;
+    const T *Q = (const T *)a.Q, *K = (const T *)a.K;
+    MT *maps = (MT *)a.maps;
+    const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
+    for (int64_t w = gw; w < total; w += nw) {
+        const int i = (int)(w % a.S);
+        const int64_t u = w / a.S;
+        const int64_t slot = u / units_per_row, lh = u % units_per_row;
+        const int64_t row = a.list.rows[slot];
+        const int64_t base = (row * units_per_row + lh) * (int64_t)a.S * a.d;
+        MT *mrow = maps + (row * units_per_row + lh) * a.map_stride + map_row_off(i, a.S, a.map_layout);
+        const int stored = packed ? 8 * (i / 8 + 1) : a.S;
+        float m = -INFINITY;
+        for (int j = lane; j <= i; j += 32) {
+            float z = 0.f;
+            for (int c = 0; c < a.d; ++c)
+                z = fmaf(Elem<DT>::ld(Q, base + (int64_t)i * a.d + c), Elem<DT>::ld(K, base + (int64_t)j * a.d + c), z);
+            z *= a.scale;
+            p[j] = z;
+            m = fmaxf(m, z);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        float sum = 0.f;
+        for (int j = lane; j <= i; j += 32) {
+            float e = expf(p[j] - m);
+            p[j] = e;
+            sum += e;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        __syncwarp();
+        const float inv = 1.f / sum;
+        for (int j = lane; j < stored; j += 32) Elem<MDT>::st(mrow, j, j <= i ? p[j] * inv : 0.f);
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_capture_simt(const CaptureArgs &a, int sm_count, cudaStream_t st) {
+    int blocks = sm_count * 4;
+    size_t smem = sizeof(float) * 8 * a.S;
+#define AC_CAPTURE(DT, MDT)                                                                                  \
+    if (a.dt == DT && a.map_dt == MDT) {                                                                    \
+        cudaFuncSetAttribute(capture_simt_kernel<DT, MDT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        capture_simt_kernel<DT, MDT><<<blocks, 256, smem, st>>>(a);                                         \
+        return count_launches(1), cudaGetLastError();                                                       \
+    }
+    AC_CAPTURE(ATTNCACHE_F32, ATTNCACHE_F16)
+    AC_CAPTURE(ATTNCACHE_F32, ATTNCACHE_BF16)
+    AC_CAPTURE(ATTNCACHE_F16, ATTNCACHE_F16)
+    AC_CAPTURE(ATTNCACHE_BF16, ATTNCACHE_BF16)
+    AC_CAPTURE(ATTNCACHE_F16, ATTNCACHE_BF16)
+    AC_CAPTURE(ATTNCACHE_BF16, ATTNCACHE_F16)
+#undef AC_CAPTURE
+    return cudaErrorInvalidValue;
+}
+
+// ============================================================================================
 // packed map layout: one warp per map row, lanes over 16-byte pieces
 // ============================================================================================
 __global__ void pack_maps_kernel(const uint4 *dense, int64_t n_maps, int S, uint4 *packed, bool unpack) {

@@ -11,6 +11,9 @@ print("tok/s %.4g ms %.4f | search %.4f apply %.4f (frac %.3f) attend %.4f (hbm 
          d["roofline"]["frac"], st.get("attend_full_misses", {}).get("ms", 0),
          st.get("attend_full_misses", {}).get("hbm_frac", 0), sp.get("full_attention_ms", 0), sp.get("batch", 0),
          sp.get("eager_torch_attention_ms"), sp.get("batch_vs_eager_torch"), d.get("e2e", {}).get("value")))
+if "capture_misses" in st:
+    c = st["capture_misses"]
+    print("  capture (f1) %.4f ms hbm %.3f %s" % (c["ms"], c["hbm_frac"], c["variant"]))
 for p in d.get("search_sweep", {}).get("points", []):
     print("  search B=%5d  %.4f ms  qps %.4g  hbm %.3f tensor %.3f hits %d/%d" % (
         p["B"], p["ms"], p["qps"], p["hbm_frac"], p["tensor_frac"], p["hits"], p["planted_hits"]))

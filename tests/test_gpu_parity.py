@@ -457,3 +457,48 @@ def test_repeat_runs_are_bitwise_identical(ac, ctx):
                 ref = tuple(t.clone() for t in cur)
             else:
                 assert all(torch.equal(a, b) for a, b in zip(ref, cur)), name
+
+
+@pytest.mark.parametrize("cfg_name,B,n_sample", [("tiny", 2, None), ("llama32_1b", 2, 24), ("llama3_8b", 1, 12),
+                                                 ("long_prefill", 1, 4)])
+@pytest.mark.parametrize("packed", [False, True])
+def test_capture_maps_match_oracle_attention_map(ac, ctx, cfg_name, B, n_sample, packed):
+    """§8(f) f1: captured maps = the oracle's fp64 causal softmax (Eq. 5) rounded to the map dtype;
+    exact zeros above the diagonal, rows sum to 1 within the map dtype's rounding."""
+    cfg = synth.CONFIGS[cfg_name].with_(L=min(2, synth.CONFIGS[cfg_name].L))
+    Q, K = (synth.activations(cfg, k, 0, B, device=DEV) for k in "qk")
+    mdt = synth.torch_dtype(cfg.map_dtype)
+    maps = ac.attncache_capture_maps(ctx, Q, K, map_dtype=mdt, packed=packed)
+    dense = maps
+    torch.cuda.synchronize()
+    if packed:  # expand through a DB for comparison (fetch returns DENSE maps)
+        db = ac.Database(ctx, synth.features(cfg.with_(N=B), 0, B, DEV), maps, packed=True, seq_len=cfg.S)
+        dense = torch.stack([ac.attncache_fetch_maps(db, b) for b in range(B)])
+    units = _units(list(range(B)), cfg.L, cfg.H)
+    if n_sample:
+        rng = np.random.default_rng(3)
+        units = [units[i] for i in sorted(rng.choice(len(units), n_sample, replace=False))]
+    off = [(((b * cfg.L + l) * cfg.H + h) * cfg.S * cfg.d) for b, l, h in units]
+    P = oracle.attention_map(storage(Q), storage(K), DT_NAME[Q.dtype], off, cfg.S, cfg.d)
+    got = torch.stack([dense[b, l, h] for b, l, h in units]).double().cpu().numpy()
+    iu = np.triu_indices(cfg.S, 1)
+    assert np.all(got[:, iu[0], iu[1]] == 0.0)
+    assert np.max(np.abs(got - P)) <= 3e-3
+    assert np.max(np.abs(got.sum(-1) - 1.0)) <= 2.5e-3
+
+
+def test_capture_then_reuse_through_the_gpu_path(ac, ctx):
+    """Capture maps with the GPU (DB building), store them as PACKED DB entries, then the hit branch
+    A.V reproduces the miss branch's attention (at configs[1] shapes)."""
+    cfg = synth.CONFIGS["llama32_1b"].with_(L=2, N=3)
+    Q, K, V = (synth.activations(cfg, k, 0, 3, device=DEV) for k in "qkv")
+    maps = ac.attncache_capture_maps(ctx, Q, K, map_dtype=torch.bfloat16, packed=True)
+    db = ac.Database(ctx, synth.features(cfg, 0, 3, DEV), maps, packed=True, seq_len=cfg.S)
+    O_reuse = ac.attncache_apply_cached(db, torch.tensor([0, 1, 2], device=DEV), V)
+    O_full = ac.attncache_attend_full(ctx, Q, K, V)
+    torch.cuda.synchronize()
+    units = _units([0, 1, 2], cfg.L, cfg.H)
+    off = [(((b * cfg.L + l) * cfg.H + h) * cfg.S * cfg.d) for b, l, h in units]
+    ref = oracle.attend(storage(Q), storage(K), storage(V), "bf16", off, cfg.S, cfg.d)
+    check_close(_gather_units(O_reuse, units), ref, torch.bfloat16, "captured reuse")
+    check_close(_gather_units(O_full, units), ref, torch.bfloat16, "full")
