@@ -347,10 +347,16 @@ def eager_attention_ms(Q, K, V, stream, steps):
     mask = torch.triu(torch.ones(S, S, dtype=torch.bool, device=Q.device), diagonal=1)
     scale = 1.0 / math.sqrt(Q.shape[-1])
 
+    B = Q.shape[0]
+    per_row = Q[0].numel() // Q.shape[-1] * S * 4  # fp32 score bytes of one batch row
+    rows = max(1, min(B, (8 << 30) // per_row))    # bound the materialised scores to ~8 GB
+
     def run():
-        s = torch.matmul(Q, K.transpose(-1, -2)) * scale
-        s.masked_fill_(mask, float("-inf"))
-        return torch.matmul(torch.softmax(s, dim=-1, dtype=torch.float32).to(V.dtype), V)
+        for b0 in range(0, B, rows):
+            q, k, v = Q[b0:b0 + rows], K[b0:b0 + rows], V[b0:b0 + rows]
+            s = torch.matmul(q, k.transpose(-1, -2)) * scale
+            s.masked_fill_(mask, float("-inf"))
+            torch.matmul(torch.softmax(s, dim=-1, dtype=torch.float32).to(v.dtype), v)
 
     run()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
