@@ -52,6 +52,7 @@ def _load():
             lib.oracle_apply.argtypes = [P, I32, P, P, I32, P, I64, I32, I32, P]
             lib.oracle_attend.argtypes = [P, P, P, I32, P, I64, I32, I32, D, P]
             lib.oracle_attention_map.argtypes = [P, P, I32, P, I64, I32, I32, D, P]
+            lib.oracle_rope.argtypes = [P, I32, I64, I32, I32, D, P]
             lib.oracle_decode.argtypes = [P, I64, I32]
             lib.oracle_decode.restype = D
             lib.oracle_set_threads.argtypes = [I32]
@@ -165,3 +166,13 @@ def attention_map(Q: np.ndarray, K: np.ndarray, dtype: str, off, S: int, d: int,
     P = np.empty((off.size, S, S), np.float64)
     _load().oracle_attention_map(_ptr(Q), _ptr(K), _DT[dtype], _ptr(off), off.size, S, d, scale, _ptr(P))
     return P
+
+
+def rope(X: np.ndarray, dtype: str, S: int, d: int, base: float = 10000.0) -> np.ndarray:
+    """Alg. 2 l.379 rotary_pos_emb (rotate-half convention, R29) of [units][S][d] -> f64."""
+    X = _raw(X, dtype).reshape(-1)
+    if X.size % (S * d) or d % 2:
+        raise ValueError("X must hold whole [S][d] units with d even")
+    Y = np.empty(X.size, np.float64)
+    _load().oracle_rope(_ptr(X), _DT[dtype], X.size // (S * d), S, d, float(base), _ptr(Y))
+    return Y.reshape(-1, S, d)

@@ -21,6 +21,8 @@
  *   apply   — Alg. 2 l.373-375: "h <- mat_mul(attn_map, v)"
  *             i.e. O = A . V, written as the plain matrix product over every
  *             column of A (the stored upper triangle is exact zeros).
+ *   rope    — Alg. 2 l.379 rotary_pos_emb (rotate-half convention; reading R29), used
+ *             only by the Eq. 5 block-level comparison (f4).
  *   attend  — Alg. 2 l.376-381 and Eq. 5:
  *             AttnMaps = softmax(Q K^T / sqrt(d_k)) with the causal mask of a
  *             decoder LLM (keys j <= i), then mat_mul(attn_map, v).
@@ -223,4 +225,22 @@ void oracle_attend(const void *Q, const void *K, const void *V, int32_t dtype, c
         }
         free(P);
     }
+}
+
+/* ---- RoPE (Alg. 2 l.379 "rotary_pos_emb(q, k)"; used by the Eq. 5 block-level
+ * comparison).  Reading R29: the rotate-half convention of Llama-family
+ * models: for i < d/2 the pair (x_i, x_{i+d/2}) at position p is rotated by the angle
+ * p * base^(-2i/d).  Y = RoPE(X) for n_units units of [S][d], position p = row index. */
+void oracle_rope(const void *X, int32_t dtype, int64_t n_units, int32_t S, int32_t d, double base, double *Y) {
+#pragma omp parallel for schedule(static)
+    for (int64_t u = 0; u < n_units; ++u)
+        for (int32_t p = 0; p < S; ++p)
+            for (int32_t i = 0; i < d / 2; ++i) {
+                const int64_t row = (u * S + p) * (int64_t)d;
+                const double theta = pow(base, -2.0 * i / d);
+                const double c = cos(p * theta), s = sin(p * theta);
+                const double x1 = load(X, row + i, dtype), x2 = load(X, row + i + d / 2, dtype);
+                Y[row + i] = x1 * c - x2 * s;
+                Y[row + i + d / 2] = x2 * c + x1 * s;
+            }
 }

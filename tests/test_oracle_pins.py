@@ -345,3 +345,28 @@ def test_generated_tiny_inputs_invariants():
     # the generator is deterministic and shard-independent
     assert torch.equal(synth.features(cfg, 100, 50), x[100:150])
     assert torch.equal(synth.maps(cfg, 2, 1)[0], M[2])
+
+
+# ----------------------------------------------------------------------------------------------
+# RoPE — Alg. 2 l.379 (rotate-half convention, reading R29); SPEC.md:55-58 examples
+# ----------------------------------------------------------------------------------------------
+
+def test_rope_pins():
+    rng = np.random.default_rng(14)
+    S, d = 40, 16
+    X = rng.standard_normal((2, S, d)).astype(np.float32)
+    Y = oracle.rope(X, "f32", S, d)
+    assert np.array_equal(Y[:, 0], X[:, 0].astype(np.float64))                 # position 0: identity
+    n_x = X.astype(np.float64)[..., : d // 2] ** 2 + X.astype(np.float64)[..., d // 2:] ** 2
+    n_y = Y[..., : d // 2] ** 2 + Y[..., d // 2:] ** 2
+    assert np.allclose(n_x, n_y, atol=1e-12)                                   # pairwise isometry
+    # d = 2: pair (x0, x1) at position p rotated by exactly p radians (theta_0 = base^0 = 1)
+    X2 = np.tile(np.array([[1.0, 0.0]], np.float32), (5, 1))[None]
+    Y2 = oracle.rope(X2, "f32", 5, 2)[0]
+    assert np.allclose(Y2, np.stack([np.cos(np.arange(5)), np.sin(np.arange(5))], 1), atol=1e-15)
+    # relative-position property: <R_p q, R_p' k> depends only on p - p'
+    q = rng.standard_normal(d).astype(np.float32)
+    k = rng.standard_normal(d).astype(np.float32)
+    Q = oracle.rope(np.tile(q, (S, 1))[None], "f32", S, d)[0]
+    K = oracle.rope(np.tile(k, (S, 1))[None], "f32", S, d)[0]
+    assert abs(Q[10] @ K[7] - Q[30] @ K[27]) < 1e-9 and abs(Q[5] @ K[5] - q.astype(np.float64) @ k) < 1e-9
