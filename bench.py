@@ -309,6 +309,8 @@ def run_ours(args, cfg):
     line["speedup_vs_full_attention"]["eager_torch_attention_ms"] = eager_ms
     line["speedup_vs_full_attention"]["batch_vs_eager_torch"] = eager_ms / ms
     del O_full
+    # §8(f) f4: Eq. 5 block level (Q/K/V projections + RoPE + attention vs V projection + A.V)
+    line["eq5_block"] = eq5_block(ac, ctx, db, cfg, idx, hit, stream, max(3, args.steps // 2))
     if not args.no_search_sweep:
         line["search_sweep"] = search_sweep(ac, ctx, dev, stream, max(3, args.steps), peaks)
     if not args.no_cpu_baseline:
@@ -339,6 +341,37 @@ def capture_stage(ac, ctx, cfg, Q, K, hit, stream, steps, peaks):
     del out
     return {"ms": ms, "bytes": nbytes, "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
             "variant": ac.attncache_variant("capture", Q.dtype, cfg.S, cfg.d)}
+
+
+def eq5_block(ac, ctx, db, cfg, idx, hit, stream, steps):
+    """One layer's attention block for the whole batch: the full path on every row vs the cached
+    path (hits: V projection + A.V; misses: the full path), and the all-hit per-row ratio.  The paper's
+    3x attention speedup is this block-level quantity (Table 4)."""
+    from paper_2510_25979_b200.block import AttentionBlock
+    X, (Wq, Wk, Wv) = synth.block_inputs(cfg, idx.device)
+    blk = AttentionBlock(ctx, db, Wq, Wk, Wv, cfg.H, cfg.d, layer=0)
+    miss_rows = torch.nonzero(hit == 0).flatten()
+    none = miss_rows[:0]
+    all_hit = torch.ones_like(hit)
+
+    def timed(fn):
+        fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    full_ms = timed(lambda: blk.full(X))
+    cached_ms = timed(lambda: blk.cached(X, idx, hit, miss_rows))
+    hits_ms = timed(lambda: blk.cached(X, idx, all_hit, none))
+    del X, Wq, Wk, Wv, blk
+    return {"layer_full_ms": full_ms, "layer_cached_ms": cached_ms, "layer_all_hits_ms": hits_ms,
+            "speedup_batch": full_ms / cached_ms, "speedup_per_hit": full_ms / hits_ms,
+            "note": "one layer, whole batch; projections via cuBLAS (torch.matmul), RoPE/A.V/attention via "
+                    "this library; synthetic weights; paper: 3x attention on A100 (PAPER.md:446)"}
 
 
 def eager_attention_ms(Q, K, V, stream, steps):

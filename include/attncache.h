@@ -188,6 +188,13 @@ attncache_status attncache_capture_maps(attncache_ctx *ctx, int64_t batch, int32
                                         const void *K, float scale, const uint8_t *skip, int32_t map_dtype,
                                         int32_t map_layout, void *maps_out, void *stream);
 
+/* ---- RoPE for the Eq. 5 block-level comparison (Alg. 2 l.379) ----------
+ * In place on X [n_units][S][d] (act_dtype): for i < d/2 the pair (x_i, x_{i+d/2}) at position p
+ * (= row index) is rotated by the angle p * base^(-2i/d) (rotate-half convention; reading R29),
+ * computed in fp32 and rounded once.  Errors: SHAPE (d odd), DTYPE, ALIGNMENT. */
+attncache_status attncache_rope(void *X, int64_t n_units, int32_t seq_len, int32_t head_dim, int32_t act_dtype,
+                                float base, void *stream);
+
 /* ---- routing helpers for the multi-GPU path (north_star: hits go to the owning GPU) ----
  *
  * route_plan: for rows b in [0, n_rows) with hit[b] != 0, owner[b] = the rank r with

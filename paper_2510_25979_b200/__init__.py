@@ -24,7 +24,7 @@ __all__ = [
     "attncache_db_free", "attncache_search", "attncache_search_keys", "attncache_keys_decode",
     "attncache_apply_cached", "attncache_attend_full", "attncache_route_plan", "attncache_gather_rows",
     "attncache_scatter_rows", "attncache_fetch_maps", "attncache_variant", "attncache_version", "attncache_launch_count",
-    "attncache_packed_map_elems", "attncache_pack_maps", "pack_db_maps", "attncache_capture_maps",
+    "attncache_packed_map_elems", "attncache_pack_maps", "pack_db_maps", "attncache_capture_maps", "attncache_rope",
     "ABI_FUNCTIONS",
 ]
 
@@ -38,7 +38,7 @@ ABI_FUNCTIONS = [
     "attncache_search_keys", "attncache_keys_decode", "attncache_apply_cached", "attncache_attend_full",
     "attncache_route_plan", "attncache_gather_rows", "attncache_scatter_rows", "attncache_fetch_maps",
     "attncache_variant", "attncache_launch_count", "attncache_packed_map_elems", "attncache_pack_maps",
-    "attncache_capture_maps",
+    "attncache_capture_maps", "attncache_rope",
 ]
 
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -93,6 +93,7 @@ def load_library():
         "attncache_fetch_maps": ([P, I64, I32, I32, P, P], I32),
         "attncache_packed_map_elems": ([I32], I64),
         "attncache_pack_maps": ([P, I64, I32, P, P], I32),
+        "attncache_rope": ([P, I64, I32, I32, I32, F32, P], I32),
         "attncache_capture_maps": ([P, I64, I32, I32, I32, I32, I32, P, P, F32, P, I32, I32, P, P], I32),
     }
     for name, (args, res) in sig.items():
@@ -406,3 +407,12 @@ def attncache_capture_maps(ctx: Context, Q: torch.Tensor, K: torch.Tensor, map_d
                                                  _p(skip), _DT[out.dtype], 1 if packed else 0, _p(out),
                                                  _stream(stream, Q.device)))
     return out
+
+
+def attncache_rope(X: torch.Tensor, base: float = 10000.0, stream=None) -> torch.Tensor:
+    """In-place RoPE (rotate-half) on X [..., S, d]; position = index along S (f4 block comparison)."""
+    _dev(X, "X")
+    S, d = X.shape[-2], X.shape[-1]
+    _check(load_library().attncache_rope(_p(X), X.numel() // (S * d), S, d, _DT[X.dtype], float(base),
+                                         _stream(stream, X.device)))
+    return X

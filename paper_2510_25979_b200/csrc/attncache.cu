@@ -379,6 +379,19 @@ attncache_status attncache_attend_full(attncache_ctx *ctx, int64_t batch, int32_
     return ATTNCACHE_OK;
 }
 
+// ---- RoPE (f4) ----------------------------------------------------------------------------------
+
+attncache_status attncache_rope(void *X, int64_t n_units, int32_t S, int32_t d, int32_t dt, float base, void *stream) {
+    if (n_units < 0 || S <= 0 || d <= 0) return fail(ATTNCACHE_ERR_SHAPE, "rope: n_units=%lld S=%d d=%d", (long long)n_units, S, d);
+    if (d % 2) return fail(ATTNCACHE_ERR_SHAPE, "rope: head_dim %d is odd", d);
+    if (!dtype_valid(dt)) return fail(ATTNCACHE_ERR_DTYPE, "rope: dtype %d", dt);
+    if (!(base > 1.f)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "rope: base must be > 1");
+    if (n_units == 0) return ATTNCACHE_OK;
+    if (!X || !is_device_ptr(X)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "rope: X must be device memory");
+    AC_CUDA(launch_rope(X, n_units, S, d, dt, base, (cudaStream_t)stream));
+    return ATTNCACHE_OK;
+}
+
 // ---- capture (DB building) ------------------------------------------------------------------
 
 attncache_status attncache_capture_maps(attncache_ctx *ctx, int64_t batch, int32_t L, int32_t H, int32_t S, int32_t dd,

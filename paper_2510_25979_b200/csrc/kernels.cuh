@@ -79,6 +79,9 @@ cudaError_t launch_capture_simt(const CaptureArgs &a, int sm_count, cudaStream_t
 bool capture_tc_supported(int32_t dt, int32_t S, int32_t d);
 cudaError_t launch_capture_tc(const CaptureArgs &a, int sm_count, cudaStream_t st);
 
+// ---- RoPE (f4 block-level comparison) ----
+cudaError_t launch_rope(void *X, int64_t n_units, int32_t S, int32_t d, int32_t dt, float base, cudaStream_t st);
+
 // ---- TMA descriptors (tma_host.cu) ----
 cudaError_t make_tmap_2d_16(CUtensorMap *out, const void *base, bool bf16, uint64_t inner, uint64_t outer,
                             uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);

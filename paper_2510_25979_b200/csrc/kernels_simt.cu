@@ -389,6 +389,40 @@ cudaError_t launch_capture_simt(const CaptureArgs &a, int sm_count, cudaStream_t
 }
 
 // ============================================================================================
+// RoPE (rotate-half): one thread per (unit, position, pair i < d/2); fp32 angle and rotation
+// ============================================================================================
+template <int DT>
+__global__ void rope_kernel(typename Elem<DT>::T *X, int64_t n_units, int S, int d, float log2_base) {
+    const int half = d / 2;
+    const int64_t total = n_units * S * half;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t % half);
+        const int64_t rs = t / half;  // (unit, position) row
+        const int p = (int)(rs % S);
+        const float theta = exp2f(-2.f * i / d * log2_base);
+        float sn, cs;
+        sincosf((float)p * theta, &sn, &cs);
+        const int64_t row = rs * d;
+        const float x1 = Elem<DT>::ld(X, row + i), x2 = Elem<DT>::ld(X, row + i + half);
+        Elem<DT>::st(X, row + i, x1 * cs - x2 * sn);
+        Elem<DT>::st(X, row + i + half, x2 * cs + x1 * sn);
+    }
+}
+
+cudaError_t launch_rope(void *X, int64_t n_units, int32_t S, int32_t d, int32_t dt, float base, cudaStream_t st) {
+    const int64_t total = n_units * S * (d / 2);
+    if (total == 0) return cudaSuccess;
+    const int blocks = (int)min64((total + 255) / 256, 148 * 32);
+    const float lb = log2f(base);
+    switch (dt) {
+    case ATTNCACHE_F32: rope_kernel<ATTNCACHE_F32><<<blocks, 256, 0, st>>>((float *)X, n_units, S, d, lb); break;
+    case ATTNCACHE_F16: rope_kernel<ATTNCACHE_F16><<<blocks, 256, 0, st>>>((__half *)X, n_units, S, d, lb); break;
+    default: rope_kernel<ATTNCACHE_BF16><<<blocks, 256, 0, st>>>((__nv_bfloat16 *)X, n_units, S, d, lb); break;
+    }
+    return count_launches(1), cudaGetLastError();
+}
+
+// ============================================================================================
 // packed map layout: one warp per map row, lanes over 16-byte pieces
 // ============================================================================================
 __global__ void pack_maps_kernel(const uint4 *dense, int64_t n_maps, int S, uint4 *packed, bool unpack) {

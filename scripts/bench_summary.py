@@ -14,6 +14,10 @@ print("tok/s %.4g ms %.4f | search %.4f apply %.4f (frac %.3f) attend %.4f (hbm 
 if "capture_misses" in st:
     c = st["capture_misses"]
     print("  capture (f1) %.4f ms hbm %.3f %s" % (c["ms"], c["hbm_frac"], c["variant"]))
+if "eq5_block" in d:
+    e = d["eq5_block"]
+    print("  eq5 block (one layer): full %.4f ms cached %.4f ms (x%.2f)  all-hit %.4f ms (x%.2f)" % (
+        e["layer_full_ms"], e["layer_cached_ms"], e["speedup_batch"], e["layer_all_hits_ms"], e["speedup_per_hit"]))
 for p in d.get("search_sweep", {}).get("points", []):
     print("  search B=%5d  %.4f ms  qps %.4g  hbm %.3f tensor %.3f hits %d/%d" % (
         p["B"], p["ms"], p["qps"], p["hbm_frac"], p["tensor_frac"], p["hits"], p["planted_hits"]))

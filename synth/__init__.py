@@ -22,7 +22,7 @@ __all__ = ["Config", "CONFIGS", "seed_for", "features", "fill_maps", "maps", "qu
 
 _TD = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
 _KINDS = {"feat": 1, "map": 2, "qnoise": 3, "qmiss": 4, "targets": 5, "positions": 6,
-          "q": 7, "k": 8, "v": 9, "misc": 10}
+          "q": 7, "k": 8, "v": 9, "misc": 10, "x": 11, "wq": 12, "wk": 13, "wv": 14}
 FEAT_CHUNK = 4096  # feature rows are drawn in fixed chunks of this many entries
 
 
@@ -198,3 +198,16 @@ def activations(cfg: Config, kind: str, b_begin: int, count: int, layer_begin: i
             g = _gen(dev, cfg.seed, kind, (b_begin + i) * 65536 + layer_begin + l)
             out[i, l].copy_(torch.randn(cfg.H, cfg.S, cfg.d, generator=g, device=dev))
     return out
+
+
+def block_inputs(cfg: Config, device="cpu", B: int | None = None):
+    """Eq. 5 block-level comparison inputs (f4): hidden states X [B][S][E] ~ N(0,1) and projection
+    weights W_Q, W_K, W_V [E][E] ~ N(0, 1/E), E = H * d, in the activation dtype (synthetic: no
+    trained weights are available)."""
+    B = cfg.B if B is None else B
+    E = cfg.H * cfg.d
+    dt = _TD[cfg.act_dtype]
+    X = torch.randn(B, cfg.S, E, generator=_gen(device, cfg.seed, "x", 0), device=device).to(dt)
+    W = [(torch.randn(E, E, generator=_gen(device, cfg.seed, k, 0), device=device) / math.sqrt(E)).to(dt)
+         for k in ("wq", "wk", "wv")]
+    return X, W

@@ -502,3 +502,40 @@ def test_capture_then_reuse_through_the_gpu_path(ac, ctx):
     ref = oracle.attend(storage(Q), storage(K), storage(V), "bf16", off, cfg.S, cfg.d)
     check_close(_gather_units(O_reuse, units), ref, torch.bfloat16, "captured reuse")
     check_close(_gather_units(O_full, units), ref, torch.bfloat16, "full")
+
+
+def test_rope_kernel_matches_oracle(ac, ctx):
+    """f4 support kernel: RoPE (rotate-half, reading R29) against the oracle.  fp32 angles p*theta
+    carry ~3 ulp relative error, i.e. up to S*3*2^-24 ~ 5e-5 rad at S = 256, times |x| <~ 5."""
+    for dtype, tol in ((torch.float32, 3e-4), (torch.bfloat16, 2e-2)):
+        X = torch.randn(3, 2, 256, 128, device=DEV).to(dtype)
+        ref = oracle.rope(storage(X), DT_NAME[dtype], 256, 128, base=500000.0)
+        Y = ac.attncache_rope(X.clone(), 500000.0)
+        torch.cuda.synchronize()
+        err = np.abs(Y.double().cpu().numpy().reshape(ref.shape) - ref).max()
+        assert err <= tol, (dtype, err)
+
+
+def test_eq5_block_cached_equals_full_with_captured_maps(ac, ctx):
+    """f4: with maps captured from the block's own Q, K (RoPE applied) the cached block (V projection
+    + A.V) reproduces the full block (projections + RoPE + attention) — Alg. 2's two branches agree."""
+    from paper_2510_25979_b200.block import AttentionBlock
+    cfg = synth.CONFIGS["llama32_1b"].with_(B=3, N=3, L=1, H=4)
+    X, (Wq, Wk, Wv) = synth.block_inputs(cfg, DEV)
+    db0 = ac.Database(ctx, synth.features(cfg, 0, 3, DEV),
+                      torch.zeros(3, 1, cfg.H, ac.attncache_packed_map_elems(cfg.S), dtype=torch.bfloat16, device=DEV),
+                      packed=True, seq_len=cfg.S)
+    blk = AttentionBlock(ctx, db0, Wq, Wk, Wv, cfg.H, cfg.d)
+    Q, K = blk._proj(X, blk.Wq), blk._proj(X, blk.Wk)
+    ac.attncache_rope(Q, blk.rope_base)
+    ac.attncache_rope(K, blk.rope_base)
+    maps = ac.attncache_capture_maps(ctx, Q, K, packed=True)
+    blk.db = ac.Database(ctx, synth.features(cfg, 0, 3, DEV), maps, packed=True, seq_len=cfg.S)
+    idx = torch.arange(3, device=DEV)
+    O_full = blk.full(X)
+    O_cached = blk.cached(X, idx, torch.ones(3, dtype=torch.uint8, device=DEV), idx[:0])
+    O_mixed = blk.cached(X, idx, torch.tensor([1, 0, 1], dtype=torch.uint8, device=DEV), idx[1:2])
+    torch.cuda.synchronize()
+    d = (O_full.double() - O_cached.double()).abs().max().item()
+    assert d < 3e-2, d
+    assert torch.equal(O_mixed[1], O_full[1])
