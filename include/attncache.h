@@ -98,8 +98,8 @@ attncache_status attncache_ctx_sync(attncache_ctx *ctx);
  *          above the diagonal, reading R11; PACKED: see attncache_map_layout) — layer-
  *          contiguous per entry and head-major inside a layer.  May be NULL
  *          for a search-only database (n_layers = n_heads = seq_len = 0).
- * Errors: INVALID_ARGUMENT (ranges, null feats with shard_count > 0, n_global >= 2^32),
- * DTYPE, ALIGNMENT (feats/maps base or row pitch not a multiple of 16 bytes). */
+ * Errors: INVALID_ARGUMENT (ranges, null feats with shard_count > 0, n_global >= 2^32, PACKED
+ * non-causal maps), DTYPE, ALIGNMENT (feats/maps base or row pitch not a multiple of 16 bytes). */
 typedef struct {
     int64_t n_global;
     int64_t shard_begin;
@@ -112,7 +112,9 @@ typedef struct {
     int32_t seq_len;
     int32_t map_dtype; /* attncache_dtype */
     const void *maps;
-    int32_t map_layout; /* attncache_map_layout */
+    int32_t map_layout;     /* attncache_map_layout */
+    int32_t maps_noncausal; /* 0: causal decoder maps (R11); 1: full encoder maps (bidirectional
+                               models; f3) — A.V reads every column; DENSE only */
 } attncache_db_desc;
 
 attncache_status attncache_db_load(attncache_ctx *ctx, const attncache_db_desc *desc, attncache_db **out);

@@ -48,7 +48,8 @@ class _DbDesc(ctypes.Structure):
     _fields_ = [("n_global", ctypes.c_int64), ("shard_begin", ctypes.c_int64), ("shard_count", ctypes.c_int64),
                 ("feat_dim", ctypes.c_int32), ("feat_dtype", ctypes.c_int32), ("feats", ctypes.c_void_p),
                 ("n_layers", ctypes.c_int32), ("n_heads", ctypes.c_int32), ("seq_len", ctypes.c_int32),
-                ("map_dtype", ctypes.c_int32), ("maps", ctypes.c_void_p), ("map_layout", ctypes.c_int32)]
+                ("map_dtype", ctypes.c_int32), ("maps", ctypes.c_void_p), ("map_layout", ctypes.c_int32),
+                ("maps_noncausal", ctypes.c_int32)]
 
 
 class AttnCacheError(RuntimeError):
@@ -161,7 +162,7 @@ class Database:
 
     def __init__(self, ctx: Context, feats: torch.Tensor, maps: Optional[torch.Tensor] = None,
                  n_global: Optional[int] = None, shard_begin: int = 0, packed: bool = False,
-                 seq_len: Optional[int] = None):
+                 seq_len: Optional[int] = None, causal: bool = True):
         L = load_library()
         _dev(feats, "feats")
         S = 0
@@ -186,7 +187,7 @@ class Database:
                        seq_len=S,
                        map_dtype=_DT[maps.dtype] if maps is not None else 0,
                        maps=maps.data_ptr() if (maps is not None and n) else None,
-                       map_layout=1 if packed else 0)
+                       map_layout=1 if packed else 0, maps_noncausal=0 if causal else 1)
         h = ctypes.c_void_p()
         _check(L.attncache_db_load(ctx.handle, ctypes.byref(desc), ctypes.byref(h)))
         self.handle = h

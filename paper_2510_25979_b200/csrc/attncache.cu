@@ -199,6 +199,8 @@ attncache_status attncache_db_load(attncache_ctx *ctx, const attncache_db_desc *
             return fail(ATTNCACHE_ERR_DTYPE, "db_load: map_dtype must be F16 or BF16");
         if (d->map_layout != ATTNCACHE_MAPS_DENSE && d->map_layout != ATTNCACHE_MAPS_PACKED)
             return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: map_layout %d", d->map_layout);
+        if (d->maps_noncausal && d->map_layout == ATTNCACHE_MAPS_PACKED)
+            return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "db_load: non-causal maps need the DENSE layout");
         if (d->seq_len % 8)
             return fail(ATTNCACHE_ERR_ALIGNMENT, "db_load: seq_len %d: map rows (S*2 bytes) must be 16-byte aligned",
                         d->seq_len);
@@ -323,6 +325,7 @@ attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, co
     a.act_dt = act_dtype;
     a.map_layout = d.map_layout;
     a.map_stride = map_elems(d.seq_len, d.map_layout);
+    a.causal = d.maps_noncausal ? 0 : 1;
     a.V = V;
     a.O = O;
     a.list = rowlist_view(db->ctx->apply_list.ptr, n_rows);

@@ -41,6 +41,7 @@ struct ApplyArgs {
     int32_t map_dt, act_dt;
     int32_t map_layout;  // ATTNCACHE_MAPS_DENSE / _PACKED
     int64_t map_stride;  // elements per S x S map
+    int32_t causal;      // 1: lower-triangular maps (decoder); 0: full maps (encoder, f3)
     const void *V;
     void *O;
     RowList list;

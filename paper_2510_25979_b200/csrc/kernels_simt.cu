@@ -198,7 +198,8 @@ cudaError_t launch_keys_decode(const uint64_t *keys, int32_t n_shards, int64_t n
 
 // ============================================================================================
 // apply (CUDA cores): one warp per output row i of a unit; lanes over columns.
-//   O[i][c] = sum_{j <= i} A[i][j] V[j][c]   (entries j > i are exact zeros; reading R11)
+//   O[i][c] = sum_{j <= i} A[i][j] V[j][c]   (causal maps: entries j > i are exact zeros; R11)
+//   O[i][c] = sum_j A[i][j] V[j][c]          (non-causal encoder maps, f3)
 // ============================================================================================
 template <int MDT, int VDT>
 __global__ void __launch_bounds__(256) apply_simt_kernel(ApplyArgs a) {
@@ -226,7 +227,8 @@ __global__ void __launch_bounds__(256) apply_simt_kernel(ApplyArgs a) {
             const int c = c0 + lane;
             float acc = 0.f;
             if (c < a.d)
-                for (int j = 0; j <= i; ++j) acc = fmaf(Elem<MDT>::ld(A, j), Elem<VDT>::ld(V, vbase + (int64_t)j * a.d + c), acc);
+                for (int j = 0, jn = a.causal ? i : a.S - 1; j <= jn; ++j)
+                    acc = fmaf(Elem<MDT>::ld(A, j), Elem<VDT>::ld(V, vbase + (int64_t)j * a.d + c), acc);
             if (c < a.d) Elem<VDT>::st(O, vbase + (int64_t)i * a.d + c, acc);
         }
     }

@@ -2,7 +2,8 @@
 //
 // One persistent CTA per SM walks the (hit, layer, head) units of the compacted hit list.  A unit
 // is split into 128-row blocks; row block rb needs map columns [0, 128(rb+1)) only (the maps are
-// causal: exact zeros above the diagonal, reading R11), processed as 64-column chunks.
+// causal: exact zeros above the diagonal, reading R11), processed as 64-column chunks.  A
+// non-causal (encoder, f3) DB visits every column.
 //
 // Roles (320 threads):
 //   warps 0-3  map loader: cp.async 16-byte pieces of the lower triangle straight from the DB
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int R = rb * kRows + r0 + 16 * j;
                     rowp[j] = A + (packed ? packed_row_off(R) : (int64_t)R * S);
                 }
-                const int n_kc = 2 * (rb + 1);
+                const int n_kc = a.causal ? 2 * (rb + 1) : S / kChunk;
                 for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
                     const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         // the piece holds at least one entry on/below the diagonal, else zero-fill
-                        const bool need = col <= rb * kRows + r0 + 16 * j;
+                        const bool need = !a.causal || col <= rb * kRows + r0 + 16 * j;
                         cp_async_16_hint(dst + 2048 * j, rowp[j] + (need ? kc * kChunk : 0), need ? 16u : 0u, policy);
                     }
                     cp_async_commit();
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             while (iter.next(lh, row, ent)) {
                 const int32_t vrow0 = (int32_t)((row * per_row + lh) * S);
                 for (int rb = 0; rb < n_rb; ++rb) {
-                    const int n_kc = 2 * (rb + 1);
+                    const int n_kc = a.causal ? 2 * (rb + 1) : S / kChunk;
                     for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
                         const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
                         mbar_wait(&empty[s], ph ^ 1u);
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&tempty[acc], aph ^ 1u);
                     tc_fence_after();
                     const uint32_t d_tmem = tmem + acc * kD;
-                    const int n_kc = 2 * (rb + 1);
+                    const int n_kc = a.causal ? 2 * (rb + 1) : S / kChunk;
                     for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
                         const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
                         mbar_wait(&full[s], ph);

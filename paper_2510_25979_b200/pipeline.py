@@ -50,6 +50,25 @@ class PrefillStep:
         return idx, score, hit
 
 
+class PerLayerPrefill:
+    """AttnCache-f (Table 4): a search per layer.
+
+    Each layer l has its own feature DB (embeddings of that layer's hidden states) sharing the index
+    space of one map DB; layer l's hits apply that layer's maps of their own top-1 entry, its misses
+    run full attention.  Tensors are per layer (as a model produces them): q_l [B][D], Q_l/K_l/V_l/O_l
+    [B][1][H][S][d].
+    """
+
+    def __init__(self, ctx: Context, map_db: Database, feature_dbs, tau: float):
+        self.ctx, self.map_db, self.feature_dbs, self.tau = ctx, map_db, list(feature_dbs), float(tau)
+
+    def layer(self, l: int, q_l, Q_l, K_l, V_l, O_l, stream=None):
+        idx, score, hit = attncache_search(self.feature_dbs[l], q_l, self.tau, stream=stream)
+        attncache_apply_cached(self.map_db, idx, V_l, O_l, hit=hit, layer_begin=l, layer_end=l + 1, stream=stream)
+        attncache_attend_full(self.ctx, Q_l, K_l, V_l, O_l, skip=hit, stream=stream)
+        return idx, score, hit
+
+
 class HostPrefill:
     """The same step end to end from (pinned) host buffers, pipelined over chunks of the batch.
 

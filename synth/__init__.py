@@ -128,11 +128,12 @@ def _feature_rows(cfg: Config, rows: torch.Tensor, device) -> torch.Tensor:
     return out
 
 
-def fill_maps(cfg: Config, out: torch.Tensor, begin: int) -> torch.Tensor:
+def fill_maps(cfg: Config, out: torch.Tensor, begin: int, causal: bool = True) -> torch.Tensor:
     """Write the maps of entries [begin, begin+len(out)) into out [n][L][H][S][S].
 
     Per (entry, layer, head): logits ~ N(0,1), causal mask (j > i -> -inf), softmax over j in
     fp32, cast round-to-nearest to the map dtype (BASELINE.json configs; readings R11, R12).
+    causal=False draws the bidirectional maps of an encoder (f3: PAPER.md:774-775), no mask.
     This is the DB producer's capture recipe, not part of the hot path.
     """
     n, S = out.shape[0], cfg.S
@@ -140,14 +141,15 @@ def fill_maps(cfg: Config, out: torch.Tensor, begin: int) -> torch.Tensor:
     upper = torch.triu(torch.ones(S, S, dtype=torch.bool, device=dev), diagonal=1)
     for e in range(n):
         z = torch.randn(cfg.L * cfg.H, S, S, generator=_gen(dev, cfg.seed, "map", begin + e), device=dev)
-        z.masked_fill_(upper, float("-inf"))
+        if causal:
+            z.masked_fill_(upper, float("-inf"))
         out[e].view(cfg.L * cfg.H, S, S).copy_(torch.softmax(z, dim=-1))
     return out
 
 
-def maps(cfg: Config, begin: int, count: int, device="cpu") -> torch.Tensor:
+def maps(cfg: Config, begin: int, count: int, device="cpu", causal: bool = True) -> torch.Tensor:
     out = torch.empty(count, cfg.L, cfg.H, cfg.S, cfg.S, dtype=_TD[cfg.map_dtype], device=device)
-    return fill_maps(cfg, out, begin)
+    return fill_maps(cfg, out, begin, causal)
 
 
 def query_plan(cfg: Config, B: int | None = None):

@@ -539,3 +539,50 @@ def test_eq5_block_cached_equals_full_with_captured_maps(ac, ctx):
     d = (O_full.double() - O_cached.double()).abs().max().item()
     assert d < 3e-2, d
     assert torch.equal(O_mixed[1], O_full[1])
+
+
+@pytest.mark.parametrize("cfg_name,N,B", [("tiny", 5, 3), ("llama32_1b", 4, 3), ("llama3_8b", 2, 2)])
+def test_apply_noncausal_encoder_maps(ac, ctx, cfg_name, N, B):
+    """f3: bidirectional (encoder) maps — A.V over every column."""
+    cfg = synth.CONFIGS[cfg_name].with_(N=N, L=min(2, synth.CONFIGS[cfg_name].L))
+    maps = synth.maps(cfg, 0, N, DEV, causal=False)
+    db = ac.Database(ctx, synth.features(cfg, 0, N, DEV), maps, causal=False)
+    idx = torch.tensor([(2 * b + 1) % N for b in range(B)], device=DEV)
+    V = synth.activations(cfg, "v", 0, B, device=DEV)
+    O = ac.attncache_apply_cached(db, idx, V)
+    torch.cuda.synchronize()
+    units = _units(list(range(B)), cfg.L, cfg.H)
+    ref = _apply_ref(storage(maps), cfg.map_dtype, idx.cpu().numpy(), storage(V), cfg.act_dtype, units, cfg.L, cfg.H,
+                     cfg.S, cfg.d)
+    check_close(_gather_units(O, units), ref, V.dtype, f"non-causal {cfg_name}")
+    with pytest.raises(ac.AttnCacheError):
+        ac.Database(ctx, synth.features(cfg, 0, N, DEV), ac.attncache_pack_maps(maps), packed=True, seq_len=cfg.S,
+                    causal=False)
+
+
+def test_per_layer_search_attncache_f(ac, ctx):
+    """f3 AttnCache-f: one feature DB per layer sharing the map DB's index; each layer applies the
+    maps of its own top-1 entry (or runs full attention on its misses)."""
+    from paper_2510_25979_b200.pipeline import PerLayerPrefill
+    base = synth.CONFIGS["llama32_1b"].with_(N=32, B=6, L=2)
+    maps = synth.maps(base, 0, base.N, DEV)
+    map_db = ac.Database(ctx, synth.features(base, 0, base.N, DEV), maps)
+    cfgs = [base.with_(seed=100 + l) for l in range(base.L)]  # each layer: its own embeddings
+    fdbs = [ac.Database(ctx, synth.features(c, 0, c.N, DEV)) for c in cfgs]
+    step = PerLayerPrefill(ctx, map_db, fdbs, base.tau)
+    for l, c in enumerate(cfgs):
+        q, pos, tgt = synth.queries(c, DEV)
+        Q, K, V = (synth.activations(base, k, 0, base.B, layer_begin=l, layer_end=l + 1, device=DEV) for k in "qkv")
+        O = torch.empty_like(V)
+        idx, score, hit = step.layer(l, q, Q, K, V, O)
+        torch.cuda.synchronize()
+        assert idx[pos].cpu().tolist() == tgt.tolist()
+        for b in range(base.B):
+            units = [(b, 0, h) for h in range(base.H)]
+            v_off = [(((b * 1 + 0) * base.H + h) * base.S * base.d) for _, _, h in units]
+            if hit[b]:
+                a_off = [((int(idx[b]) * base.L + l) * base.H + h) * base.S * base.S for _, _, h in units]
+                ref = oracle.apply(storage(maps), "bf16", a_off, storage(V), "bf16", v_off, base.S, base.d)
+            else:
+                ref = oracle.attend(storage(Q), storage(K), storage(V), "bf16", v_off, base.S, base.d)
+            check_close(_gather_units(O, units), ref, torch.bfloat16, f"layer {l} row {b}")
