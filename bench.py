@@ -126,7 +126,7 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline leg and --impl reference)
 # ------------------------------------------------------------------------------------------------
-def oracle_step_sample(cfg, budget=6e8, seed=0):
+def oracle_step_sample(cfg, budget=2.5e9, seed=0):
     """Times the CPU oracle on a bounded sample of one step of `cfg` and extrapolates.
 
     Each stage gets about `budget` multiply-adds of work (a few seconds of fp64 CPU time on a
