@@ -195,7 +195,7 @@ def run_reference(args, cfg):
 # ------------------------------------------------------------------------------------------------
 def run_ours(args, cfg):
     rank, world, local = _env_rank()
-    if world > 1:
+    if world > 1 or args.force_dist:
         return run_dist(args, cfg)
     import paper_2510_25979_b200 as ac
     from paper_2510_25979_b200.pipeline import PrefillStep
@@ -293,7 +293,7 @@ def run_ours(args, cfg):
 
     line = {"metric": METRIC, "value": cfg.B * cfg.S / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": cfg.act_dtype, "data": "synthetic (synth/, seed 0)",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": cfg.act_dtype, "data": "synthetic (synth/, seed 0)",
             "config": {"workload": cfg.name, "bj_config_index": cfg.bj_index, "N": cfg.N, "D": cfg.D, "L": cfg.L,
                        "H": cfg.H, "S": cfg.S, "d": cfg.d, "B": cfg.B, "hits": n_hit, "tau": cfg.tau,
                        "parallelism": "single GPU", "l2": "inputs exceed L2 (no flush)"},
@@ -431,21 +431,37 @@ def search_sweep(ac, ctx, dev, stream, steps, peaks):
     return out
 
 
+def _rows_activations(cfg, kind, rows, dev):
+    """Q/K/V of the given global query positions (the same seeds as synth.activations)."""
+    out = torch.empty(len(rows), cfg.L, cfg.H, cfg.S, cfg.d, dtype=synth.torch_dtype(cfg.act_dtype), device=dev)
+    for k, b in enumerate(rows):
+        synth.activations(cfg, kind, b, 1, out=out[k:k + 1])
+    return out
+
+
 def run_dist(args, cfg):
     """N > 1 (torchrun, one process per GPU, NCCL): the DB is sharded by contiguous entry ranges,
-    each rank is home to a contiguous block of the query batch; one step = sharded search (query
-    all-gather, local top-1, key all-gather + max) -> hits routed to the owning GPU (V out, O back by
-    all_to_all) -> local attention for misses.  Same global data at every N (strong scaling)."""
+    each rank is home to a contiguous block of the query batch; same global data at every N (strong
+    scaling).  One step = sharded search (query all-gather, local top-1, key all-gather + max), then
+
+      --placement affinity (default; SURVEY.md §8(e) owner-affinity): every query is placed once on the
+        rank that processes all its layers (hits on the owner of their entry, misses greedily on the
+        least-loaded ranks), its request state (hidden states [S][E]) moves there by one all_to_all, and
+        A.V / attention run locally;
+      --placement routed (the north_star's literal routing): hits' V rows go to the owner and O rows
+        come back by all_to_all, misses stay home."""
     import torch.distributed as dist
 
     import paper_2510_25979_b200 as ac
-    from paper_2510_25979_b200.dist import CudaOps, ShardedPrefill, shard_range
+    from paper_2510_25979_b200.dist import AffinityPrefill, CudaOps, ShardedPrefill, shard_range
     rank, world, local = _env_rank()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     ctx = ac.Context(local)
     peaks = _peaks()
+    if args.scaling == "weak":  # the config's batch on EVERY GPU: global batch B * world, same sharded DB
+        cfg = cfg.with_(B=cfg.B * world)
     begin, count = shard_range(cfg.N, world, rank)
     x = synth.features(cfg, begin, count, dev)
     maps = ac.pack_db_maps(lambda b, out: synth.fill_maps(cfg, out, begin + b), count, cfg.L, cfg.H, cfg.S,
@@ -454,11 +470,31 @@ def run_dist(args, cfg):
     q_all, _, _ = synth.queries(cfg, dev)
     hb, hc = shard_range(cfg.B, world, rank)
     q = q_all[hb:hb + hc].contiguous()
-    Q, K, V = (synth.activations(cfg, k, hb, hc, device=dev) for k in "qkv")
-    O = torch.empty_like(V)
-    step = ShardedPrefill(CudaOps(ctx, db), cfg.N, cfg.tau, device=dev)
+    sizes = [shard_range(cfg.B, world, r)[1] for r in range(world)]
+    if args.placement == "affinity":
+        step = AffinityPrefill(CudaOps(ctx, db), cfg.N, cfg.tau, hit_cost=apply_bytes_per_hit(cfg),
+                               miss_cost=attend_bytes_per_miss(cfg), device=dev)
+        plan0 = step.plan(q, sizes)
+        loc = step.local_queries(plan0)
+        # the synthetic activations of the queries this rank processes, generated here from their seeds
+        # (in a model they come from the relocated hidden states)
+        Q, K, V = (_rows_activations(cfg, k, loc.tolist(), dev) for k in "qkv")
+        O = torch.empty_like(V)
+        E = cfg.H * cfg.d
+        X_home = torch.randn(hc, cfg.S, E, device=dev).to(synth.torch_dtype(cfg.act_dtype))
+
+        def one_step():
+            plan = step.plan(q, sizes)
+            step.relocate(X_home, plan)
+            step.apply_local(plan, loc, V, O, Q, K)
+            return plan
+    else:
+        Q, K, V = (synth.activations(cfg, k, hb, hc, device=dev) for k in "qkv")
+        O = torch.empty_like(V)
+        step = ShardedPrefill(CudaOps(ctx, db), cfg.N, cfg.tau, device=dev)
+        one_step = lambda: step(q, Q, K, V, O)  # noqa: E731
     for _ in range(args.warmup):
-        step(q, Q, K, V, O)
+        res = one_step()
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = ac.attncache_launch_count()
@@ -467,26 +503,42 @@ def run_dist(args, cfg):
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
     for _ in range(args.steps):
-        idx, score, hit = step(q, Q, K, V, O)
+        res = one_step()
     end.record()
     torch.cuda.synchronize()
     dist.barrier()
     clk = clocks.stop()
     ms = torch.tensor([start.elapsed_time(end) / args.steps], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)  # the step time is the slowest rank's
-    n_hit = torch.tensor([int(hit.sum().item())], device=dev)
+    if args.placement == "affinity":
+        assert torch.equal(step.local_queries(res), loc), "placement changed between steps"
+        n_hit = torch.tensor([int(res["hit"].sum().item()) if rank == 0 else 0], device=dev)
+        extra = {"local_queries": int(loc.numel()), "relocated_bytes_per_query": cfg.S * cfg.H * cfg.d * 2}
+        per_rank = torch.tensor([loc.numel()], device=dev)
+        gathered = [torch.empty_like(per_rank) for _ in range(world)]
+        dist.all_gather(gathered, per_rank)
+        extra["queries_per_rank"] = [int(t.item()) for t in gathered]
+        extra["plan_load_bytes_per_rank"] = [float(v) for v in res["load"].tolist()]
+    else:
+        n_hit = torch.tensor([int(res[2].sum().item())], device=dev)
+        extra = {}
     dist.all_reduce(n_hit)
     launches = torch.tensor([ac.attncache_launch_count() - launches0], device=dev)
     dist.all_reduce(launches)
     ctx.sync()
     ms = float(ms.item())
     if rank == 0:
+        par = (f"DB sharded by entry over {world} GPUs; " +
+               ("owner-affinity placement: hits on the owner, misses on the least-loaded GPUs, request state "
+                "moved once (NCCL all_to_all), all layers local" if args.placement == "affinity" else
+                "hits routed to the owner (V out, O back by NCCL all_to_all)"))
         line = {"metric": METRIC, "value": cfg.B * cfg.S / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": cfg.act_dtype, "data": "synthetic (synth/, seed 0)",
+                "scaling": args.scaling, "vs_baseline": None, "dtype": cfg.act_dtype,
+                "data": "synthetic (synth/, seed 0)",
                 "config": {"workload": cfg.name, "bj_config_index": cfg.bj_index, "N": cfg.N, "B": cfg.B, "S": cfg.S,
-                           "hits": int(n_hit.item()), "parallelism": f"DB sharded by entry over {world} GPUs; "
-                           "hits routed to the owner (NCCL all_to_all)", "l2": "inputs exceed L2 (no flush)"},
+                           "hits": int(n_hit.item()), "placement": args.placement, "parallelism": par,
+                           "l2": "inputs exceed L2 (no flush)", **extra},
                 "gpu_launches": int(launches.item()), "clocks": clk,
                 "roofline": {"bound": "hbm", "achieved": None, "peak": peaks["hbm_gbs"] * world, "unit": "GB/s",
                              "frac": None, "traffic": None,
@@ -551,6 +603,12 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-search-sweep", action="store_true", help="skip the configs[4] search-QPS sweep")
+    ap.add_argument("--placement", default="affinity", choices=["affinity", "routed"],
+                    help="N > 1: owner-affinity placement (default) or the literal V->owner / O->home routing")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: the config's global batch split over the GPUs (strong, default) or the config's batch "
+                         "on every GPU (weak)")
+    ap.add_argument("--force-dist", action="store_true", help="run the multi-GPU path even at world size 1 (testing)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("bench.py: note: --warmup < 3 does not meet the timing rules (profiling runs only)", file=sys.stderr)

@@ -213,6 +213,25 @@ attncache_status attncache_gather_rows(const void *src, const int64_t *rows, int
 attncache_status attncache_scatter_rows(const void *src, const int64_t *rows, int64_t n_rows, int64_t row_bytes,
                                         void *dst, void *stream);
 
+/* ---- owner-affinity placement (the scalable multi-GPU variant) ----
+ * HOST function: plain host pointers, no device work, callable without a GPU.  Decides once per batch,
+ * before the layer loop, which rank processes each query, so that no per-layer V or O crosses NVLink
+ * (the prescribed V -> owner / O -> home routing moves both for every layer):
+ *   - a hit row b goes to the rank r owning its entry, shard_begins[r] <= idx[b] < shard_begins[r+1],
+ *     where the maps are local (north_star: "routed to the owning GPU");
+ *   - then every miss row, in ascending b, goes to the rank with the smallest accumulated cost (the
+ *     lowest rank on ties); a hit adds hit_cost to its rank and a miss miss_cost (callers pass the
+ *     per-query algorithmic HBM bytes of one A.V / one attention, which set the kernel times).
+ * Placing equal-cost misses one at a time on the least-loaded rank, on top of the fixed hit loads,
+ * minimises the maximum load (tested against brute force).  idx, hit: [n_rows] for the whole batch
+ * (every rank computes the same plan from the same inputs).  Outputs: assign[b] = the processing rank;
+ * load[r] (optional, may be NULL; [world]) = the accumulated cost on rank r.  Deterministic.
+ * Errors: INVALID_ARGUMENT (n_rows < 0, world outside [1, 1024], NULL arrays, shard_begins not
+ * non-decreasing, NaN or negative costs, a hit idx outside [shard_begins[0], shard_begins[world])). */
+attncache_status attncache_affinity_plan(const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                         const int64_t *shard_begins, int32_t world, double hit_cost,
+                                         double miss_cost, int32_t *assign, double *load);
+
 /* ---- DB building: packed map layout (Fig. 4 step 3) -----------
  * Number of elements one PACKED S x S map occupies (0 if S % 8 != 0). */
 int64_t attncache_packed_map_elems(int32_t seq_len);

@@ -25,7 +25,7 @@ __all__ = [
     "attncache_apply_cached", "attncache_attend_full", "attncache_route_plan", "attncache_gather_rows",
     "attncache_scatter_rows", "attncache_fetch_maps", "attncache_variant", "attncache_version", "attncache_launch_count",
     "attncache_packed_map_elems", "attncache_pack_maps", "pack_db_maps", "attncache_capture_maps", "attncache_rope",
-    "ABI_FUNCTIONS",
+    "attncache_affinity_plan", "ABI_FUNCTIONS",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -38,7 +38,7 @@ ABI_FUNCTIONS = [
     "attncache_search_keys", "attncache_keys_decode", "attncache_apply_cached", "attncache_attend_full",
     "attncache_route_plan", "attncache_gather_rows", "attncache_scatter_rows", "attncache_fetch_maps",
     "attncache_variant", "attncache_launch_count", "attncache_packed_map_elems", "attncache_pack_maps",
-    "attncache_capture_maps", "attncache_rope",
+    "attncache_capture_maps", "attncache_rope", "attncache_affinity_plan",
 ]
 
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -96,6 +96,7 @@ def load_library():
         "attncache_pack_maps": ([P, I64, I32, P, P], I32),
         "attncache_rope": ([P, I64, I32, I32, I32, F32, P], I32),
         "attncache_capture_maps": ([P, I64, I32, I32, I32, I32, I32, P, P, F32, P, I32, I32, P, P], I32),
+        "attncache_affinity_plan": ([P, P, I64, P, I32, ctypes.c_double, ctypes.c_double, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -417,3 +418,29 @@ def attncache_rope(X: torch.Tensor, base: float = 10000.0, stream=None) -> torch
     _check(load_library().attncache_rope(_p(X), X.numel() // (S * d), S, d, _DT[X.dtype], float(base),
                                          _stream(stream, X.device)))
     return X
+
+
+def attncache_affinity_plan(idx, hit, shard_begins, hit_cost: float = 1.0, miss_cost: float = 1.0):
+    """Owner-affinity placement (host function): returns (assign int32[n], load float64[world]).
+    idx/hit are torch tensors (any device; read on the host) or numpy arrays; the outputs follow the input
+    kind (CPU torch tensors or numpy arrays)."""
+    import numpy as np
+    as_torch = isinstance(idx, torch.Tensor)
+    if as_torch:
+        idx = idx.detach().to("cpu", torch.int64).numpy()
+        hit = hit.detach().to("cpu", torch.uint8).numpy()
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    hit = np.ascontiguousarray(hit, dtype=np.uint8)
+    if isinstance(shard_begins, torch.Tensor):
+        shard_begins = shard_begins.detach().cpu().numpy()
+    sb = np.ascontiguousarray(shard_begins, dtype=np.int64)
+    world = sb.shape[0] - 1
+    n = idx.shape[0]
+    assign = np.empty(n, dtype=np.int32)
+    load = np.empty(max(world, 0), dtype=np.float64)
+    ptr = lambda a: ctypes.c_void_p(a.ctypes.data) if a.size else None  # noqa: E731
+    _check(load_library().attncache_affinity_plan(ptr(idx), ptr(hit), n, ptr(sb), world, float(hit_cost),
+                                                  float(miss_cost), ptr(assign), ptr(load)))
+    if as_torch:
+        return torch.from_numpy(assign), torch.from_numpy(load)
+    return assign, load

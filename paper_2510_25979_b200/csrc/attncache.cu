@@ -456,6 +456,47 @@ attncache_status attncache_route_plan(const int64_t *idx, const uint8_t *hit, in
     return ATTNCACHE_OK;
 }
 
+attncache_status attncache_affinity_plan(const int64_t *idx, const uint8_t *hit, int64_t n, const int64_t *sb,
+                                         int32_t world, double hit_cost, double miss_cost, int32_t *assign,
+                                         double *load) {
+    if (n < 0 || world <= 0 || world > 1024)
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan: n=%lld world=%d", (long long)n, world);
+    if (!sb || (n > 0 && (!idx || !hit || !assign))) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan: NULL argument");
+    if (!(hit_cost >= 0.0) || !(miss_cost >= 0.0))  // also rejects NaN
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan: costs must be non-negative numbers");
+    for (int r = 0; r < world; ++r)
+        if (sb[r + 1] < sb[r]) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan: shard_begins decreasing at %d", r);
+    double acc[1024];
+    for (int r = 0; r < world; ++r) acc[r] = 0.0;
+    // hits: the owner of the entry (its maps are local there)
+    for (int64_t b = 0; b < n; ++b) {
+        if (!hit[b]) continue;
+        const int64_t e = idx[b];
+        if (e < sb[0] || e >= sb[world])
+            return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan: hit row %lld has idx %lld outside [%lld, %lld)",
+                        (long long)b, (long long)e, (long long)sb[0], (long long)sb[world]);
+        int lo = 0, hi = world - 1;  // the last r with sb[r] <= e (binary search; empty shards skipped)
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) / 2;
+            if (sb[mid] <= e) lo = mid; else hi = mid - 1;
+        }
+        assign[b] = lo;
+        acc[lo] += hit_cost;
+    }
+    // misses: ascending b, each on the least-loaded rank (lowest rank on ties)
+    for (int64_t b = 0; b < n; ++b) {
+        if (hit[b]) continue;
+        int best = 0;
+        for (int r = 1; r < world; ++r)
+            if (acc[r] < acc[best]) best = r;
+        assign[b] = best;
+        acc[best] += miss_cost;
+    }
+    if (load)
+        for (int r = 0; r < world; ++r) load[r] = acc[r];
+    return ATTNCACHE_OK;
+}
+
 static attncache_status copy_rows(const void *src, const int64_t *rows, int64_t n, int64_t row_bytes, void *dst,
                                   bool gather, void *stream) {
     if (n < 0 || row_bytes <= 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "copy_rows: n=%lld row_bytes=%lld", (long long)n, (long long)row_bytes);

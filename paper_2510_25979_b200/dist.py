@@ -12,6 +12,13 @@ Each query has a home rank.  One step:
   a7  C5  O rows -> home  (all_to_all);  K3  scatter into O          (attncache_scatter_rows)
   a8  K5  misses: local causal attention                            (attncache_attend_full)
 
+Owner-affinity variant (`AffinityPrefill`): after the search, which every rank
+runs for the whole batch, each query is placed ONCE, before the layer loop, on the rank that will
+process all its layers: a hit on the owner of its entry, misses on the least-loaded ranks
+(attncache_affinity_plan, a host function of the C ABI).  The request's hidden state moves once
+(one all_to_all of [S][E] rows) instead of V and O for every layer, so NVLink carries
+B*S*E*2 bytes per batch rather than 2*B*L*H*S*d*2, and every A.V reads local maps.
+
 Collectives are torch.distributed (NCCL over NVLink/NVSwitch on the GPU box, gloo in the CPU
 tests); every per-rank computation goes through `ops`, which in the product is `CudaOps` (the C
 ABI).  The CPU tests inject their own reference ops to check this host logic with world size 2-3.
@@ -20,11 +27,13 @@ from __future__ import annotations
 
 from typing import List, Optional
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import (Context, Database, attncache_apply_cached, attncache_attend_full, attncache_gather_rows,
-               attncache_keys_decode, attncache_route_plan, attncache_scatter_rows, attncache_search_keys)
+from . import (Context, Database, attncache_affinity_plan, attncache_apply_cached, attncache_attend_full,
+               attncache_gather_rows, attncache_keys_decode, attncache_route_plan, attncache_scatter_rows,
+               attncache_search_keys)
 
 
 def shard_range(n: int, world: int, rank: int):
@@ -58,6 +67,9 @@ class CudaOps:
     def apply_cached(self, idx, V, layer_begin=0, layer_end=None):
         return attncache_apply_cached(self.db, idx, V, layer_begin=layer_begin, layer_end=layer_end)
 
+    def apply_cached_masked(self, idx, hit, V, O, layer_begin=0, layer_end=None):
+        return attncache_apply_cached(self.db, idx, V, O, hit=hit, layer_begin=layer_begin, layer_end=layer_end)
+
     def attend_full(self, Q, K, V, O, skip):
         return attncache_attend_full(self.ctx, Q, K, V, O, skip=skip)
 
@@ -83,22 +95,33 @@ class ShardedPrefill:
 
     def search(self, q_home: torch.Tensor):
         """Returns this rank's (idx, score, hit) for its home queries: the global top-1 over all shards."""
-        sizes = self._home_sizes(q_home.shape[0])
+        idx, score, hit, sizes = self.search_all(q_home)
+        lo = sum(sizes[:self.rank])
+        hi = lo + sizes[self.rank]
+        return idx[lo:hi].contiguous(), score[lo:hi].contiguous(), hit[lo:hi].contiguous()
+
+    def search_all(self, q_home: torch.Tensor, sizes: Optional[List[int]] = None):
+        """The global top-1 of EVERY query of the batch (each rank decodes all keys after C2), in the
+        order of the home blocks (rank 0's queries first); returns (idx, score, hit, home sizes).
+        `sizes` (the home batch size of every rank) may be passed when known, saving one exchange."""
+        sizes = self._home_sizes(q_home.shape[0]) if sizes is None else list(sizes)
         bmax = max(max(sizes), 1)
         D = q_home.shape[1]
-        pad = torch.zeros(bmax, D, dtype=q_home.dtype, device=self.device)
-        pad[:q_home.shape[0]] = q_home
-        q_all = torch.empty(self.world * bmax, D, dtype=q_home.dtype, device=self.device)
-        dist.all_gather_into_tensor(q_all, pad, group=self.group)                              # C1
-        q_all = q_all.view(self.world, bmax, D)
-        q_all = torch.cat([q_all[r, :sizes[r]] for r in range(self.world)]) if sum(sizes) else q_all[0, :0]
+        if min(sizes) == bmax:  # equal home blocks: gather in place, no padding
+            q_all = torch.empty(self.world * bmax, D, dtype=q_home.dtype, device=self.device)
+            dist.all_gather_into_tensor(q_all, q_home.contiguous(), group=self.group)          # C1
+        else:
+            pad = torch.zeros(bmax, D, dtype=q_home.dtype, device=self.device)
+            pad[:q_home.shape[0]] = q_home
+            q_all = torch.empty(self.world * bmax, D, dtype=q_home.dtype, device=self.device)
+            dist.all_gather_into_tensor(q_all, pad, group=self.group)                          # C1
+            q_all = q_all.view(self.world, bmax, D)
+            q_all = torch.cat([q_all[r, :sizes[r]] for r in range(self.world)]) if sum(sizes) else q_all[0, :0]
         keys = self.ops.search_keys(q_all.contiguous())                                         # K1
         keys_all = torch.empty(self.world * keys.shape[0], dtype=keys.dtype, device=self.device)
         dist.all_gather_into_tensor(keys_all, keys, group=self.group)                           # C2
         idx, score, hit = self.ops.keys_decode(keys_all.view(self.world, -1), self.tau)         # K2
-        lo = sum(sizes[:self.rank])
-        hi = lo + sizes[self.rank]
-        return idx[lo:hi].contiguous(), score[lo:hi].contiguous(), hit[lo:hi].contiguous()
+        return idx, score, hit, sizes
 
     # ---- a5-a7: route hits to the owner, compute A.V there, return O ---------------------------------
     def apply_routed(self, idx_home, hit_home, V_home, O_home, layer_begin=0, layer_end=None):
@@ -134,3 +157,73 @@ class ShardedPrefill:
         if q_home.shape[0]:
             self.ops.attend_full(Q_home, K_home, V_home, O_home, hit)                           # K5
         return idx, score, hit
+
+
+class AffinityPrefill(ShardedPrefill):
+    """Owner-affinity placement: the sharded search, then one placement of every
+    query on the rank that processes all of its layers locally.
+
+    hit_cost / miss_cost weight the greedy miss placement (attncache_affinity_plan); callers pass the
+    algorithmic HBM bytes of one query's A.V and of one query's attention.
+
+    Host work per batch is one small D2H (the decoded top-1 of every query, misses as -1), the C
+    placement, and one small H2D (this rank's relocation order and its local idx/hit), so the GPU idles
+    only for the host's planning between the search and the local layer work."""
+
+    def __init__(self, ops, n_global: int, tau: float, hit_cost: float = 1.0, miss_cost: float = 1.0,
+                 group=None, device="cuda"):
+        super().__init__(ops, n_global, tau, group=group, device=device)
+        self.hit_cost, self.miss_cost = float(hit_cost), float(miss_cost)
+        self._sb_host = np.asarray([shard_range(self.n_global, self.world, r)[0] for r in range(self.world)]
+                                   + [self.n_global], dtype=np.int64)
+
+    def plan(self, q_home: torch.Tensor, sizes: Optional[List[int]] = None):
+        """Search + placement.  Returns a dict with the whole batch's idx/score/hit (device), `assign`
+        (numpy int32[B], the processing rank of every query), the home sizes, the per-rank loads, and
+        this rank's local queries with their idx/hit on the device."""
+        idx, score, hit, sizes = self.search_all(q_home, sizes)
+        code = torch.where(hit.bool(), idx, torch.full_like(idx, -1)).cpu().numpy()            # one D2H
+        hit_h = (code >= 0).astype(np.uint8)
+        assign, load = attncache_affinity_plan(np.maximum(code, 0), hit_h, self._sb_host, self.hit_cost,
+                                               self.miss_cost)
+        loc = np.nonzero(assign == self.rank)[0]
+        lo = sum(sizes[:self.rank])
+        mine = assign[lo:lo + sizes[self.rank]].astype(np.int64)
+        send_order = np.argsort(mine, kind="stable")                                            # by destination, then b
+        send_n = np.bincount(mine, minlength=self.world).tolist()
+        bounds = np.cumsum([0] + list(sizes))
+        recv_n = [int((assign[bounds[r]:bounds[r + 1]] == self.rank).sum()) for r in range(self.world)]
+        # one H2D: [send_order | idx_loc | hit_loc] as int64
+        n_loc = loc.shape[0]
+        host = np.concatenate([send_order, code[loc].clip(min=0), hit_h[loc].astype(np.int64)])
+        dev = torch.from_numpy(host).to(self.device, non_blocking=False)
+        return {"idx": idx, "score": score, "hit": hit, "assign": assign, "sizes": sizes, "load": load,
+                "loc": torch.from_numpy(loc), "send_order": dev[:send_order.shape[0]], "send_n": send_n,
+                "recv_n": recv_n, "idx_loc": dev[send_order.shape[0]:send_order.shape[0] + n_loc],
+                "hit_loc": dev[send_order.shape[0] + n_loc:].to(torch.uint8)}
+
+    def local_queries(self, plan) -> torch.Tensor:
+        """Global batch positions this rank processes, ascending (int64, CPU)."""
+        return plan["loc"]
+
+    def relocate(self, rows_home: torch.Tensor, plan) -> torch.Tensor:
+        """Moves each home row (one query's request state, e.g. its hidden states [S][E]) to the rank
+        the plan assigns it to: one all_to_all.  Returns the rows of `local_queries(plan)` in that order
+        (home blocks are contiguous and ascending in rank, so sources arrive in global order)."""
+        send_n, recv_n = plan["send_n"], plan["recv_n"]
+        row_shape = rows_home.shape[1:]
+        send = self.ops.gather_rows(rows_home, plan["send_order"]) if rows_home.shape[0] else rows_home[:0]
+        recv = torch.empty((sum(recv_n), *row_shape), dtype=rows_home.dtype, device=self.device)
+        dist.all_to_all_single(recv, send.contiguous(), recv_n, send_n, group=self.group)
+        return recv
+
+    def apply_local(self, plan, loc, V_loc, O_loc, Q_loc=None, K_loc=None, layer_begin=0, layer_end=None):
+        """All the layers of this rank's queries, locally: O = A.V for hits (the maps are in this shard),
+        causal attention for misses.  V_loc/O_loc (and Q_loc/K_loc) are [len(loc)][L'][H][S][d]."""
+        if not loc.numel():
+            return O_loc
+        idx_loc, hit_loc = plan["idx_loc"], plan["hit_loc"]
+        self.ops.apply_cached_masked(idx_loc, hit_loc, V_loc, O_loc, layer_begin, layer_end)     # K4
+        if Q_loc is not None:
+            self.ops.attend_full(Q_loc, K_loc, V_loc, O_loc, hit_loc)                           # K5
+        return O_loc

@@ -410,6 +410,18 @@ def test_sharded_prefill_world1_matches_single_gpu_step(ac, ctx):
         for a, b in zip(r1, r2):
             assert torch.equal(a, b)
         assert torch.equal(O1, O2)
+        # owner-affinity placement: at world size 1 every query is local and the result is the same
+        from paper_2510_25979_b200.dist import AffinityPrefill
+        aff = AffinityPrefill(CudaOps(ctx, db), cfg.N, cfg.tau, hit_cost=1.0, miss_cost=1.3, device=DEV)
+        plan = aff.plan(q)
+        loc = aff.local_queries(plan)
+        assert loc.tolist() == list(range(cfg.B))
+        X = torch.randn(cfg.B, cfg.S, 64, device=DEV, dtype=torch.bfloat16)
+        assert torch.equal(aff.relocate(X, plan), X)
+        O3 = torch.empty_like(V)
+        aff.apply_local(plan, loc, V, O3, Q, K)
+        torch.cuda.synchronize()
+        assert torch.equal(O1, O3)
     finally:
         dist.destroy_process_group()
 
