@@ -53,6 +53,7 @@ def _load():
             lib.oracle_attend.argtypes = [P, P, P, I32, P, I64, I32, I32, D, P]
             lib.oracle_attention_map.argtypes = [P, P, I32, P, I64, I32, I32, D, P]
             lib.oracle_rope.argtypes = [P, I32, I64, I32, I32, D, P]
+            lib.oracle_project.argtypes = [P, I64, I32, I32, P, P, I32, P, P, I32, P]
             lib.oracle_decode.argtypes = [P, I64, I32]
             lib.oracle_decode.restype = D
             lib.oracle_set_threads.argtypes = [I32]
@@ -176,3 +177,21 @@ def rope(X: np.ndarray, dtype: str, S: int, d: int, base: float = 10000.0) -> np
     Y = np.empty(X.size, np.float64)
     _load().oracle_rope(_ptr(X), _DT[dtype], X.size // (S * d), S, d, float(base), _ptr(Y))
     return Y.reshape(-1, S, d)
+
+
+def project(h: np.ndarray, dtype: str, W1: np.ndarray, b1: np.ndarray, W2: np.ndarray, b2: np.ndarray) -> np.ndarray:
+    """Alg. 1 l.254 feature_projector (readings R30-R32): f = normalize(W2 relu(W1 h + b1) + b2).
+
+    h: [B][E], W1: [Hd][E], W2: [D][Hd] in storage dtype; b1, b2 float32.  Returns f64 [B][D]."""
+    h = _raw(h, dtype)
+    W1 = _raw(W1, dtype)
+    W2 = _raw(W2, dtype)
+    b1 = np.ascontiguousarray(b1, dtype=np.float32)
+    b2 = np.ascontiguousarray(b2, dtype=np.float32)
+    B, E = h.shape
+    Hd, D = W1.shape[0], W2.shape[0]
+    if W1.shape != (Hd, E) or W2.shape != (D, Hd) or b1.shape != (Hd,) or b2.shape != (D,):
+        raise ValueError("oracle.project: shapes disagree")
+    f = np.empty((B, D), np.float64)
+    _load().oracle_project(_ptr(h), B, E, _DT[dtype], _ptr(W1), _ptr(b1), Hd, _ptr(W2), _ptr(b2), D, _ptr(f))
+    return f

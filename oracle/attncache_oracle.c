@@ -26,6 +26,10 @@
  *   attend  — Alg. 2 l.376-381 and Eq. 5:
  *             AttnMaps = softmax(Q K^T / sqrt(d_k)) with the causal mask of a
  *             decoder LLM (keys j <= i), then mat_mul(attn_map, v).
+ *   project — Alg. 1 l.254 "f <- feature_projector(h)" with the
+ *             projector of PAPER.md:278 ("two layers of Multi-Layer Perceptron
+ *             ... maps the input embedding to a feature vector"): z = relu(W1 h
+ *             + b1), y = W2 z + b2, f = y / ||y||_2 (readings R30-R32).
  *
  * Parity pins for each function live in tests/test_oracle_pins.py.
  */
@@ -243,4 +247,37 @@ void oracle_rope(const void *X, int32_t dtype, int64_t n_units, int32_t S, int32
                 Y[row + i] = x1 * c - x2 * s;
                 Y[row + i + d / 2] = x2 * c + x1 * s;
             }
+}
+
+/* ---- feature projector: Alg. 1 l.254, PAPER.md:278 ------------------------
+ * Readings: R30 h is the sentence's input embedding vector [E]; R31 the two MLP layers
+ * are affine maps with a ReLU between them (the paper names no activation); R32 the feature vector
+ * is L2-normalised (the DB holds unit vectors, north_star; reading R2), and y = 0 gives f = 0.
+ *   z[j] = max(0, sum_k W1[j][k] h[k] + b1[j])     j < Hd
+ *   y[c] = sum_j W2[c][j] z[j] + b2[c]             c < D
+ *   f[c] = y[c] / sqrt(sum_c y[c]^2)
+ * h: [B][E], W1: [Hd][E], W2: [D][Hd] in `dtype`; b1: [Hd], b2: [D] fp32; f: [B][D] fp64. */
+void oracle_project(const void *h, int64_t B, int32_t E, int32_t dtype, const void *W1, const float *b1,
+                    int32_t Hd, const void *W2, const float *b2, int32_t D, double *f) {
+#pragma omp parallel for schedule(static)
+    for (int64_t b = 0; b < B; ++b) {
+        double *z = (double *)malloc(sizeof(double) * (size_t)(Hd > 0 ? Hd : 1));
+        double *y = f + b * (int64_t)D;
+        for (int32_t j = 0; j < Hd; ++j) {
+            double s = 0.0;
+            for (int32_t k = 0; k < E; ++k) s += load(W1, (int64_t)j * E + k, dtype) * load(h, b * (int64_t)E + k, dtype);
+            s += (double)b1[j];
+            z[j] = s > 0.0 ? s : 0.0;
+        }
+        double nn = 0.0;
+        for (int32_t c = 0; c < D; ++c) {
+            double s = 0.0;
+            for (int32_t j = 0; j < Hd; ++j) s += load(W2, (int64_t)c * Hd + j, dtype) * z[j];
+            y[c] = s + (double)b2[c];
+            nn += y[c] * y[c];
+        }
+        const double norm = sqrt(nn);
+        for (int32_t c = 0; c < D; ++c) y[c] = norm > 0.0 ? y[c] / norm : 0.0;
+        free(z);
+    }
 }

@@ -370,3 +370,92 @@ def test_rope_pins():
     Q = oracle.rope(np.tile(q, (S, 1))[None], "f32", S, d)[0]
     K = oracle.rope(np.tile(k, (S, 1))[None], "f32", S, d)[0]
     assert abs(Q[10] @ K[7] - Q[30] @ K[27]) < 1e-9 and abs(Q[5] @ K[5] - q.astype(np.float64) @ k) < 1e-9
+
+
+# ----------------------------------------------------------------------------------------------
+# feature projector — Alg. 1 l.254, PAPER.md:278 two-layer MLP; readings R30-R32
+# ----------------------------------------------------------------------------------------------
+
+def _proj_inputs(rng, B, E, Hd, D, dtype):
+    h = rng.standard_normal((B, E)).astype(np.float32)
+    W1 = (rng.standard_normal((Hd, E)) / math.sqrt(E)).astype(np.float32)
+    W2 = (rng.standard_normal((D, Hd)) / math.sqrt(Hd)).astype(np.float32)
+    b1 = (0.1 * rng.standard_normal(Hd)).astype(np.float32)
+    b2 = (0.1 * rng.standard_normal(D)).astype(np.float32)
+    if dtype == "bf16":
+        h, W1, W2 = _bf16_bits(h), _bf16_bits(W1), _bf16_bits(W2)
+    return h, W1, b1, W2, b2
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_project_golden_hand_computed(dtype):
+    g = _gold("project_mlp.json")
+    conv = _bf16_bits if dtype == "bf16" else (lambda a: np.asarray(a, np.float32))
+    f = oracle.project(conv(g["h"]), dtype, conv(g["W1"]), np.float32(g["b1"]), conv(g["W2"]), np.float32(g["b2"]))
+    assert np.allclose(f, np.array(g["f"]), rtol=0, atol=1e-15)
+
+
+def test_project_identity_weights_is_normalisation():
+    """W1 = I, b1 = 0, W2 = I, b2 = 0: f = relu(h) / ||relu(h)|| (closed form; ReLU zeroes negatives)."""
+    rng = np.random.default_rng(5)
+    E = 16
+    h = rng.standard_normal((6, E)).astype(np.float32)
+    h[0] = np.abs(h[0])                                     # all positive: f = h / ||h||
+    I = np.eye(E, dtype=np.float32)
+    z = np.zeros(E, np.float32)
+    f = oracle.project(h, "f32", I, z, I, z)
+    r = np.maximum(h.astype(np.float64), 0.0)
+    for b in range(6):
+        n = math.sqrt(sum(float(v) ** 2 for v in r[b]))
+        assert np.allclose(f[b], r[b] / n, rtol=0, atol=1e-15)
+    assert np.allclose(f[0], h[0] / np.linalg.norm(h[0].astype(np.float64)), rtol=0, atol=1e-15)
+
+
+def test_project_exact_rational_brute_force():
+    """Tiny bf16 instance: hidden layer and pre-normalisation output in exact rationals; f^2 * ||y||^2 = y^2
+    and the signs agree (the oracle's sqrt is the only inexact step)."""
+    rng = np.random.default_rng(9)
+    B, E, Hd, D = 3, 5, 4, 3
+    h, W1, b1, W2, b2 = _proj_inputs(rng, B, E, Hd, D, "bf16")
+    f = oracle.project(h, "bf16", W1, b1, W2, b2)
+    hq, W1q, W2q = _exact(h, "bf16"), _exact(W1, "bf16"), _exact(W2, "bf16")
+    for b in range(B):
+        z = [max(Fraction(0), sum(W1q[j * E + k] * hq[b * E + k] for k in range(E)) + Fraction(float(b1[j])))
+             for j in range(Hd)]
+        y = [sum(W2q[c * Hd + j] * z[j] for j in range(Hd)) + Fraction(float(b2[c])) for c in range(D)]
+        nn = sum(v * v for v in y)
+        for c in range(D):
+            assert abs(float(f[b, c]) ** 2 * float(nn) - float(y[c] * y[c])) <= 1e-12 * float(nn)
+            assert (f[b, c] > 0) == (y[c] > 0)
+
+
+def test_project_invariants():
+    """Unit norm; positive scaling of (W2, b2) leaves f unchanged (bitwise: x4 is exact); permuting the
+    output units permutes f; permuting the hidden units (rows of W1/b1, columns of W2) leaves f unchanged."""
+    rng = np.random.default_rng(11)
+    B, E, Hd, D = 7, 24, 16, 12
+    h, W1, b1, W2, b2 = _proj_inputs(rng, B, E, Hd, D, "f32")
+    f = oracle.project(h, "f32", W1, b1, W2, b2)
+    assert np.allclose(np.linalg.norm(f, axis=1), 1.0, rtol=0, atol=1e-14)
+    f4 = oracle.project(h, "f32", W1, b1, (4 * W2).astype(np.float32), (4 * b2).astype(np.float32))
+    assert np.array_equal(f4, f)
+    perm = rng.permutation(D)
+    fp = oracle.project(h, "f32", W1, b1, np.ascontiguousarray(W2[perm]), np.ascontiguousarray(b2[perm]))
+    assert np.allclose(fp, f[:, perm], rtol=0, atol=1e-14)
+    hp = rng.permutation(Hd)
+    fh = oracle.project(h, "f32", np.ascontiguousarray(W1[hp]), np.ascontiguousarray(b1[hp]),
+                        np.ascontiguousarray(W2[:, hp]), b2)
+    assert np.allclose(fh, f, rtol=0, atol=1e-14)
+
+
+def test_project_matches_library_mlp():
+    """Independent library special case: torch.nn.functional.linear + relu + normalize in fp64."""
+    rng = np.random.default_rng(13)
+    B, E, Hd, D = 9, 64, 32, 48
+    h, W1, b1, W2, b2 = _proj_inputs(rng, B, E, Hd, D, "bf16")
+    f = oracle.project(h, "bf16", W1, b1, W2, b2)
+    t = lambda a: torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).double()  # noqa: E731
+    z = torch.relu(torch.nn.functional.linear(t(h), t(W1), torch.from_numpy(b1).double()))
+    y = torch.nn.functional.linear(z, t(W2), torch.from_numpy(b2).double())
+    ref = torch.nn.functional.normalize(y, dim=1).numpy()
+    assert np.allclose(f, ref, rtol=0, atol=1e-13)
