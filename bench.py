@@ -303,6 +303,8 @@ def run_ours(args, cfg):
             "stages": secondary, "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
     # §8(f) f1, DB building: capture the misses' maps (Q, K -> packed bf16 DB entries)
     secondary["capture_misses"] = capture_stage(ac, ctx, cfg, Q, K, hit, stream, max(3, args.steps), peaks)
+    # §8(f) f2: the feature projector (Alg. 1 l.254) on this batch and at a tensor-bound batch
+    secondary["project"] = project_stage(ac, ctx, cfg, dev, stream, max(3, args.steps), peaks)
     # paper-comparable baseline: eager torch attention (matmul -> masked softmax -> matmul, the
     # unfused attention of PAPER.md Table 4's "AM" + "AM.V" rows) on every row of the batch
     eager_ms = eager_attention_ms(Q, K, V, stream, max(2, args.steps // 2))
@@ -341,6 +343,32 @@ def capture_stage(ac, ctx, cfg, Q, K, hit, stream, steps, peaks):
     del out
     return {"ms": ms, "bytes": nbytes, "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
             "variant": ac.attncache_variant("capture", Q.dtype, cfg.S, cfg.d)}
+
+
+def project_stage(ac, ctx, cfg, dev, stream, steps, peaks):
+    """f2, Alg. 1 l.254: f = normalize(W2 relu(W1 h + b1) + b2) (synthetic weights, reading R31) at the config's
+    batch and at B = 8192 (tensor-bound); roofline on flops 2B(E*Hd + Hd*D) vs bytes (weights + h + f)."""
+    out = []
+    for B in (cfg.B, 8192):
+        h, W1, b1, W2, b2 = synth.projector_inputs(cfg, B=B, device=dev)
+        f = torch.empty(B, cfg.D, dtype=synth.torch_dtype(cfg.feat_dtype), device=dev)
+        ac.attncache_project_features(ctx, h, W1, b1, W2, b2, out=f)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            ac.attncache_project_features(ctx, h, W1, b1, W2, b2, out=f)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        E, Hd, D = h.shape[1], W1.shape[0], cfg.D
+        flops = 2.0 * B * (E * Hd + Hd * D)
+        nbytes = (Hd * E + D * Hd) * h.element_size() + B * E * h.element_size() + B * D * f.element_size()
+        out.append({"B": B, "E": E, "hidden": Hd, "D": D, "ms": ms, "tflops": flops / (ms * 1e-3) / 1e12,
+                    "tensor_frac": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                    "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                    "variant": ac.attncache_variant("project", h.dtype, E, Hd)})
+        del h, W1, W2, f
+    return out
 
 
 def eq5_block(ac, ctx, db, cfg, idx, hit, stream, steps):

@@ -190,6 +190,23 @@ attncache_status attncache_capture_maps(attncache_ctx *ctx, int64_t batch, int32
                                         const void *K, float scale, const uint8_t *skip, int32_t map_dtype,
                                         int32_t map_layout, void *maps_out, void *stream);
 
+/* ---- feature projector (Alg. 1 l.254 "f <- feature_projector(h)", PAPER.md:254;
+ * PAPER.md:278 "two layers of Multi-Layer Perceptron ... maps the input embedding to a feature vector") ----
+ * For every row b of h (readings R30-R32):
+ *     z = relu(W1 h[b] + b1)        W1: [hidden_dim][in_dim]  (nn.Linear layout), b1: [hidden_dim] fp32
+ *     y = W2 z + b2                 W2: [feat_dim][hidden_dim],                   b2: [feat_dim] fp32
+ *     features[b] = y / ||y||_2     (0 if y = 0), rounded once to feat_dtype
+ * h: [n][in_dim], W1, W2 in act_dtype (BF16/F16: tensor cores when in_dim, hidden_dim and feat_dim are
+ * multiples of 64; F32 or other shapes: CUDA cores); fp32 accumulation; z is rounded once to act_dtype
+ * (the second layer's operand) and y kept in fp32.  features: [n][feat_dim] in feat_dtype, ready to be
+ * searched (attncache_search) or stored as DB rows (Fig. 4 step 2).  Device pointers;
+ * scratch (z, y) is owned by ctx.  Errors: SHAPE (non-positive dims), DTYPE, ALIGNMENT (bases, or rows
+ * of in_dim / hidden_dim elements, not 16-byte aligned), INVALID_ARGUMENT (NULL or host pointers). */
+attncache_status attncache_project_features(attncache_ctx *ctx, const void *h, int64_t n, int32_t in_dim,
+                                            int32_t act_dtype, const void *W1, const float *b1, int32_t hidden_dim,
+                                            const void *W2, const float *b2, int32_t feat_dim, int32_t feat_dtype,
+                                            void *features, void *stream);
+
 /* ---- RoPE for the Eq. 5 block-level comparison (Alg. 2 l.379) ----------
  * In place on X [n_units][S][d] (act_dtype): for i < d/2 the pair (x_i, x_{i+d/2}) at position p
  * (= row index) is rotated by the angle p * base^(-2i/d) (rotate-half convention; reading R29),
@@ -248,8 +265,9 @@ attncache_status attncache_fetch_maps(attncache_db *db, int64_t idx, int32_t lay
                                       void *out, void *stream);
 
 /* ---- introspection: kernel variant chosen for a call (for tests/bench) ----
- * kind: 0 = search, 1 = apply, 2 = attend, 3 = capture.  Returns a static string such as "tc" (tcgen05) or
- * "ffma" for the arguments given (no launch). */
+ * kind: 0 = search, 1 = apply, 2 = attend, 3 = capture, 4 = one projector layer (seq_len = its K, head_dim =
+ * its output width).  Returns a static string such as "tc" (tcgen05) or "ffma" for the arguments given
+ * (no launch). */
 const char *attncache_variant(int32_t kind, int32_t dtype, int32_t seq_len, int32_t head_dim);
 
 #ifdef __cplusplus

@@ -25,7 +25,7 @@ __all__ = [
     "attncache_apply_cached", "attncache_attend_full", "attncache_route_plan", "attncache_gather_rows",
     "attncache_scatter_rows", "attncache_fetch_maps", "attncache_variant", "attncache_version", "attncache_launch_count",
     "attncache_packed_map_elems", "attncache_pack_maps", "pack_db_maps", "attncache_capture_maps", "attncache_rope",
-    "attncache_affinity_plan", "ABI_FUNCTIONS",
+    "attncache_affinity_plan", "attncache_project_features", "ABI_FUNCTIONS",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -38,7 +38,7 @@ ABI_FUNCTIONS = [
     "attncache_search_keys", "attncache_keys_decode", "attncache_apply_cached", "attncache_attend_full",
     "attncache_route_plan", "attncache_gather_rows", "attncache_scatter_rows", "attncache_fetch_maps",
     "attncache_variant", "attncache_launch_count", "attncache_packed_map_elems", "attncache_pack_maps",
-    "attncache_capture_maps", "attncache_rope", "attncache_affinity_plan",
+    "attncache_capture_maps", "attncache_rope", "attncache_affinity_plan", "attncache_project_features",
 ]
 
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -97,6 +97,7 @@ def load_library():
         "attncache_rope": ([P, I64, I32, I32, I32, F32, P], I32),
         "attncache_capture_maps": ([P, I64, I32, I32, I32, I32, I32, P, P, F32, P, I32, I32, P, P], I32),
         "attncache_affinity_plan": ([P, P, I64, P, I32, ctypes.c_double, ctypes.c_double, P, P], I32),
+        "attncache_project_features": ([P, P, I64, I32, I32, P, P, I32, P, P, I32, I32, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -224,7 +225,7 @@ def attncache_launch_count() -> int:
 
 
 def attncache_variant(kind: str, dtype: torch.dtype, seq_len: int, head_dim: int) -> str:
-    k = {"search": 0, "apply": 1, "attend": 2, "capture": 3}[kind]
+    k = {"search": 0, "apply": 1, "attend": 2, "capture": 3, "project": 4}[kind]
     return load_library().attncache_variant(k, _DT[dtype], int(seq_len), int(head_dim)).decode()
 
 
@@ -444,3 +445,26 @@ def attncache_affinity_plan(idx, hit, shard_begins, hit_cost: float = 1.0, miss_
     if as_torch:
         return torch.from_numpy(assign), torch.from_numpy(load)
     return assign, load
+
+
+def attncache_project_features(ctx: Context, h: torch.Tensor, W1: torch.Tensor, b1: torch.Tensor, W2: torch.Tensor,
+                               b2: torch.Tensor, feat_dtype=None, out: Optional[torch.Tensor] = None,
+                               stream=None) -> torch.Tensor:
+    """Alg. 1 l.254 feature_projector (f2): features = normalize(W2 relu(W1 h + b1) + b2) as [n][D] in feat_dtype
+    (default: h's dtype).  h [n][E], W1 [Hd][E], W2 [D][Hd] (one dtype), b1 [Hd], b2 [D] fp32."""
+    for t, nme in ((h, "h"), (W1, "W1"), (b1, "b1"), (W2, "W2"), (b2, "b2")):
+        _dev(t, nme)
+    if h.dim() != 2 or W1.dim() != 2 or W2.dim() != 2 or W1.shape[1] != h.shape[1] or W2.shape[1] != W1.shape[0]:
+        raise ValueError("project_features: h [n][E], W1 [Hd][E], W2 [D][Hd]")
+    if not (h.dtype == W1.dtype == W2.dtype) or b1.dtype != torch.float32 or b2.dtype != torch.float32:
+        raise ValueError("project_features: h/W1/W2 share one dtype; b1/b2 are float32")
+    if b1.shape != (W1.shape[0],) or b2.shape != (W2.shape[0],):
+        raise ValueError("project_features: bias shapes")
+    n, E = h.shape
+    Hd, D = W1.shape[0], W2.shape[0]
+    feat_dtype = h.dtype if feat_dtype is None else feat_dtype
+    out = torch.empty((n, D), dtype=feat_dtype, device=h.device) if out is None else out
+    _dev(out, "out")
+    _check(load_library().attncache_project_features(ctx.handle, _p(h), n, E, _DT[h.dtype], _p(W1), _p(b1), Hd, _p(W2),
+                                                     _p(b2), D, _DT[out.dtype], _p(out), _stream(stream, h.device)))
+    return out

@@ -106,6 +106,7 @@ int32_t attncache_version(void) { return 100; }
 uint64_t attncache_launch_count(void) { return ac::launch_count(); }
 
 const char *attncache_variant(int32_t kind, int32_t dtype, int32_t seq_len, int32_t head_dim) {
+    if (kind == 4) return linear_tc_supported(dtype, seq_len, head_dim) ? "tc" : "ffma";
     switch (kind) {
     case 0: return search_tc_supported(dtype, head_dim) ? "tc" : "ffma";  // head_dim = feat_dim here
     case 1: return apply_tc_supported(dtype, dtype, seq_len, head_dim) ? "tc" : "ffma";
@@ -154,6 +155,7 @@ attncache_status attncache_ctx_destroy(attncache_ctx *ctx) {
     cudaFree(ctx->apply_list.ptr);
     cudaFree(ctx->attend_list.ptr);
     cudaFree(ctx->search_keys.ptr);
+    cudaFree(ctx->project_buf.ptr);
     delete ctx;
     return ATTNCACHE_OK;
 }
@@ -379,6 +381,54 @@ attncache_status attncache_attend_full(attncache_ctx *ctx, int64_t batch, int32_
     } else {
         AC_CUDA(launch_attend_ffma(a, ctx->sm_count, st));
     }
+    return ATTNCACHE_OK;
+}
+
+// ---- feature projector (f2) ---------------------------------------------------------------------
+
+attncache_status attncache_project_features(attncache_ctx *ctx, const void *h, int64_t n, int32_t in_dim,
+                                            int32_t act_dtype, const void *W1, const float *b1, int32_t hidden_dim,
+                                            const void *W2, const float *b2, int32_t feat_dim, int32_t feat_dtype,
+                                            void *features, void *stream) {
+    if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "project_features: ctx is NULL");
+    if (n < 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "project_features: n < 0");
+    if (in_dim <= 0 || hidden_dim <= 0 || feat_dim <= 0)
+        return fail(ATTNCACHE_ERR_SHAPE, "project_features: in_dim=%d hidden_dim=%d feat_dim=%d", in_dim, hidden_dim, feat_dim);
+    if (!dtype_valid(act_dtype) || !dtype_valid(feat_dtype))
+        return fail(ATTNCACHE_ERR_DTYPE, "project_features: act_dtype %d feat_dtype %d", act_dtype, feat_dtype);
+    if (!W1 || !b1 || !W2 || !b2) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "project_features: NULL weights");
+    if (!is_device_ptr(W1) || !is_device_ptr(b1) || !is_device_ptr(W2) || !is_device_ptr(b2))
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "project_features: weights must be device memory");
+    if (n == 0) return ATTNCACHE_OK;
+    if (!h || !features) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "project_features: NULL h/features");
+    if (!is_device_ptr(h) || !is_device_ptr(features))
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "project_features: h/features must be device memory");
+    const int es = dtype_size(act_dtype);
+    if (!aligned16(h) || !aligned16(W1) || !aligned16(W2) || !aligned16(b1) || !aligned16(b2) || !aligned16(features) ||
+        ((int64_t)in_dim * es) % 16 || ((int64_t)hidden_dim * es) % 16)
+        return fail(ATTNCACHE_ERR_ALIGNMENT, "project_features: bases or row pitches (in_dim, hidden_dim) not 16-byte aligned");
+    DeviceGuard g(ctx->device);
+    // scratch: z [n][Hd] (act dtype) then y [n][D] fp32, 256-byte aligned
+    const size_t zb = ((size_t)n * hidden_dim * es + 255) & ~(size_t)255;
+    const size_t yb = (size_t)n * feat_dim * 4;
+    attncache_status s = ensure_scratch(ctx->project_buf, zb + yb);
+    if (s) return s;
+    ProjectArgs a;
+    a.M = n;
+    a.E = in_dim;
+    a.Hd = hidden_dim;
+    a.D = feat_dim;
+    a.dt = act_dtype;
+    a.feat_dt = feat_dtype;
+    a.h = h;
+    a.W1 = W1;
+    a.W2 = W2;
+    a.b1 = b1;
+    a.b2 = b2;
+    a.z = ctx->project_buf.ptr;
+    a.y = (float *)((uint8_t *)ctx->project_buf.ptr + zb);
+    a.f = features;
+    AC_CUDA(launch_project(a, ctx->sm_count, (cudaStream_t)stream));
     return ATTNCACHE_OK;
 }
 

@@ -97,6 +97,7 @@ struct attncache_ctx {
     ac::Scratch apply_list;  // compacted (row, entry) list for apply
     ac::Scratch attend_list; // compacted row list for attend
     ac::Scratch search_keys; // per-query keys for single-rank search
+    ac::Scratch project_buf; // feature projector intermediates (z, y)
 };
 
 struct attncache_db {

@@ -80,6 +80,20 @@ cudaError_t launch_capture_simt(const CaptureArgs &a, int sm_count, cudaStream_t
 bool capture_tc_supported(int32_t dt, int32_t S, int32_t d);
 cudaError_t launch_capture_tc(const CaptureArgs &a, int sm_count, cudaStream_t st);
 
+// ---- feature projector (f2): z = relu(W1 h + b1), y = W2 z + b2, f = y / ||y|| ----
+struct ProjectArgs {
+    int64_t M;            // rows (sentences)
+    int32_t E, Hd, D;     // input, hidden, feature dims
+    int32_t dt, feat_dt;  // dtype of h/W1/W2/z; dtype of f
+    const void *h, *W1, *W2;
+    const float *b1, *b2;
+    void *z;              // scratch [M][Hd] in dt
+    float *y;             // scratch [M][D] fp32
+    void *f;              // [M][D] in feat_dt
+};
+bool linear_tc_supported(int32_t dt, int32_t K, int32_t Nout);
+cudaError_t launch_project(const ProjectArgs &a, int sm_count, cudaStream_t st);
+
 // ---- RoPE (f4 block-level comparison) ----
 cudaError_t launch_rope(void *X, int64_t n_units, int32_t S, int32_t d, int32_t dt, float base, cudaStream_t st);
 

@@ -12,7 +12,8 @@ from typing import Optional
 
 import torch
 
-from . import (Context, Database, attncache_apply_cached, attncache_attend_full, attncache_search)
+from . import (Context, Database, attncache_apply_cached, attncache_attend_full, attncache_project_features,
+               attncache_search)
 
 
 class PrefillStep:
@@ -48,6 +49,24 @@ class PrefillStep:
         idx, score, hit = self.search(queries, stream=stream)
         self.attend(idx, hit, Q, K, V, O, stream=stream)
         return idx, score, hit
+
+
+class FeatureProjector:
+    """Alg. 1 l.254 `f <- feature_projector(h)`: the two-layer MLP that maps
+    sentence embeddings h [B][E] to L2-normalised feature vectors [B][D] in the DB's feature dtype, which
+    `PrefillStep.search` then takes (Alg. 1 l.255).  Weights in the nn.Linear layout (readings R30-R32)."""
+
+    def __init__(self, ctx: Context, W1, b1, W2, b2, feat_dtype=None):
+        self.ctx, self.W1, self.b1, self.W2, self.b2 = ctx, W1, b1, W2, b2
+        self.feat_dtype = W1.dtype if feat_dtype is None else feat_dtype
+        self._out = {}
+
+    def __call__(self, h, stream=None):
+        B = h.shape[0]
+        if B not in self._out:
+            self._out[B] = torch.empty(B, self.W2.shape[0], dtype=self.feat_dtype, device=h.device)
+        return attncache_project_features(self.ctx, h, self.W1, self.b1, self.W2, self.b2, out=self._out[B],
+                                          stream=stream)
 
 
 class PerLayerPrefill:

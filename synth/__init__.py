@@ -18,11 +18,11 @@ import math
 import torch
 
 __all__ = ["Config", "CONFIGS", "seed_for", "features", "fill_maps", "maps", "query_plan", "queries",
-           "activations", "torch_dtype", "FEAT_CHUNK"]
+           "activations", "torch_dtype", "FEAT_CHUNK", "EMBED_DIM", "projector_inputs"]
 
 _TD = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
 _KINDS = {"feat": 1, "map": 2, "qnoise": 3, "qmiss": 4, "targets": 5, "positions": 6,
-          "q": 7, "k": 8, "v": 9, "misc": 10, "x": 11, "wq": 12, "wk": 13, "wv": 14}
+          "q": 7, "k": 8, "v": 9, "misc": 10, "x": 11, "wq": 12, "wk": 13, "wv": 14, "proj": 15}
 FEAT_CHUNK = 4096  # feature rows are drawn in fixed chunks of this many entries
 
 
@@ -213,3 +213,25 @@ def block_inputs(cfg: Config, device="cpu", B: int | None = None):
     W = [(torch.randn(E, E, generator=_gen(device, cfg.seed, k, 0), device=device) / math.sqrt(E)).to(dt)
          for k in ("wq", "wk", "wv")]
     return X, W
+
+
+# Model hidden size E of the sentence embedding that the feature projector maps to the D-dim feature
+# (reading R30: Llama-3.2-1B 2048, Llama-3-8B 4096; tiny / sweep configs use small stand-ins).
+EMBED_DIM = {"tiny": 256, "llama32_1b": 2048, "llama3_8b": 4096, "long_prefill": 4096, "search_sweep": 1024}
+
+
+def projector_inputs(cfg: Config, B: int | None = None, device="cpu", E: int | None = None,
+                     hidden: int | None = None):
+    """Feature-projector inputs (f2; readings R30-R31): sentence embeddings h [B][E] ~ N(0,1) and synthetic
+    weights W1 [Hd][E] ~ N(0, 1/E), W2 [D][Hd] ~ N(0, 1/Hd) in the activation dtype (fp32 for fp32 features),
+    biases b1 [Hd], b2 [D] ~ N(0, 0.01) fp32.  Hd = D unless given.  No trained projector is available."""
+    B = cfg.B if B is None else B
+    E = EMBED_DIM[cfg.name] if E is None else E
+    Hd = cfg.D if hidden is None else hidden
+    dt = _TD[cfg.act_dtype] if cfg.feat_dtype != "f32" else torch.float32
+    h = torch.randn(B, E, generator=_gen(device, cfg.seed, "proj", 0), device=device).to(dt)
+    W1 = (torch.randn(Hd, E, generator=_gen(device, cfg.seed, "proj", 1), device=device) / math.sqrt(E)).to(dt)
+    W2 = (torch.randn(cfg.D, Hd, generator=_gen(device, cfg.seed, "proj", 2), device=device) / math.sqrt(Hd)).to(dt)
+    b1 = 0.1 * torch.randn(Hd, generator=_gen(device, cfg.seed, "proj", 3), device=device)
+    b2 = 0.1 * torch.randn(cfg.D, generator=_gen(device, cfg.seed, "proj", 4), device=device)
+    return h, W1, b1, W2, b2

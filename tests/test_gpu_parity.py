@@ -598,3 +598,78 @@ def test_per_layer_search_attncache_f(ac, ctx):
             else:
                 ref = oracle.attend(storage(Q), storage(K), storage(V), "bf16", v_off, base.S, base.d)
             check_close(_gather_units(O, units), ref, torch.bfloat16, f"layer {l} row {b}")
+
+
+# ------------------------------------------------------------------------------------------------
+# feature projector (f2; Alg. 1 l.254; readings R30-R32)
+# ------------------------------------------------------------------------------------------------
+
+def _project_check(ac, ctx, cfg, B, E, Hd, feat_dtype=None, tc=True):
+    h, W1, b1, W2, b2 = synth.projector_inputs(cfg, B=B, device=DEV, E=E, hidden=Hd)
+    f = ac.attncache_project_features(ctx, h, W1, b1, W2, b2, feat_dtype=feat_dtype)
+    torch.cuda.synchronize()
+    assert ac.attncache_variant("project", h.dtype, E, Hd) == ("tc" if tc else "ffma")
+    dt = DT_NAME[h.dtype]
+    ref = oracle.project(storage(h), dt, storage(W1), b1.cpu().numpy(), storage(W2), b2.cpu().numpy())
+    # one "unit" per row: max-abs over all elements, rel-L2 per row (north_star bf16 bounds; fp32: _util)
+    check_close(f.unsqueeze(1), ref[:, None, :], f.dtype, f"project {cfg.name} B={B} E={E} Hd={Hd}")
+    return f, (h, W1, b1, W2, b2)
+
+
+@pytest.mark.parametrize("name,B", [("llama32_1b", 256), ("llama32_1b", 1), ("llama32_1b", 130),
+                                    ("llama3_8b", 37), ("search_sweep", 257)])
+def test_project_parity_tc(ac, ctx, name, B):
+    cfg = synth.CONFIGS[name]
+    f, _ = _project_check(ac, ctx, cfg, B, synth.EMBED_DIM[name], cfg.D)
+    n = f.double().norm(dim=1)
+    assert torch.all((n - 1).abs() < 1e-2)                 # unit rows (bf16 rounding of each element)
+
+
+def test_project_parity_ffma_paths(ac, ctx):
+    """fp32 (configs[0], FFMA) and a bf16 shape the tensor-core path does not take (dims not multiples of 64)."""
+    _project_check(ac, ctx, synth.CONFIGS["tiny"], 8, 256, 384, tc=False)
+    cfg = synth.CONFIGS["llama32_1b"].with_(D=40)
+    _project_check(ac, ctx, cfg, 19, 200, 72, tc=False)
+
+
+def test_project_deterministic_and_zero_output(ac, ctx):
+    cfg = synth.CONFIGS["llama32_1b"]
+    h, W1, b1, W2, b2 = synth.projector_inputs(cfg, B=300, device=DEV)
+    f1 = ac.attncache_project_features(ctx, h, W1, b1, W2, b2)
+    f2 = ac.attncache_project_features(ctx, h, W1, b1, W2, b2)
+    assert torch.equal(f1, f2)
+    z = ac.attncache_project_features(ctx, h, W1, b1, torch.zeros_like(W2), torch.zeros_like(b2))
+    assert torch.equal(z, torch.zeros_like(z))             # y = 0 gives f = 0 (reading R32)
+
+
+def test_project_then_search(ac, ctx):
+    """Alg. 1 l.254-257 end to end: DB rows and queries both embedded by the projector (Fig. 4 step 2),
+    queries are noisy copies of DB embeddings; the search decisions on the projected features follow the
+    exactness rule and the planted rows are found."""
+    cfg = synth.CONFIGS["llama32_1b"]
+    E = synth.EMBED_DIM[cfg.name]
+    h_db, W1, b1, W2, b2 = synth.projector_inputs(cfg, B=500, device=DEV)
+    feats = ac.attncache_project_features(ctx, h_db, W1, b1, W2, b2)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    rows = torch.tensor([3, 77, 499, 250], device=DEV)
+    hq = h_db[rows].float() + 0.01 * torch.randn(len(rows), E, device=DEV, generator=g)
+    hq = torch.cat([hq, torch.randn(4, E, device=DEV, generator=g)]).to(h_db.dtype)
+    q = ac.attncache_project_features(ctx, hq, W1, b1, W2, b2)
+    db = ac.Database(ctx, feats)
+    idx, score, hit = ac.attncache_search(db, q, 0.9)
+    torch.cuda.synchronize()
+    check_search(q, feats, idx, score, hit, 0.9)
+    assert idx[:4].tolist() == rows.tolist() and hit[:4].tolist() == [1] * 4
+
+
+def test_project_errors(ac, ctx):
+    cfg = synth.CONFIGS["llama32_1b"]
+    h, W1, b1, W2, b2 = synth.projector_inputs(cfg, B=4, device=DEV)
+    L = ac.load_library()
+    args = (W1.data_ptr(), b1.data_ptr(), W1.shape[0], W2.data_ptr(), b2.data_ptr(), W2.shape[0], 2)
+    assert L.attncache_project_features(ctx.handle, None, 4, h.shape[1], 2, *args, None, None) == 1  # NULL h
+    f = torch.empty(4, cfg.D, dtype=torch.bfloat16, device=DEV)
+    assert L.attncache_project_features(ctx.handle, h.data_ptr(), 4, 0, 2, *args, f.data_ptr(), None) == 2  # SHAPE
+    assert L.attncache_project_features(ctx.handle, h.data_ptr(), 4, 196, 2, *args, f.data_ptr(), None) == 4  # pitch
+    out = ac.attncache_project_features(ctx, h[:0], W1, b1, W2, b2)
+    assert out.shape == (0, cfg.D)
