@@ -18,13 +18,14 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "build")
-LIB_DIR = os.path.join(PKG, "lib")
+# ATTNCACHE_BUILD_ROOT / ATTNCACHE_EXTRA_FLAGS: out-of-tree experiment builds (scripts/); the product uses neither
+OBJ = os.path.join(os.environ.get("ATTNCACHE_BUILD_ROOT", PKG), "build")
+LIB_DIR = os.path.join(os.environ.get("ATTNCACHE_BUILD_ROOT", PKG), "lib")
 LIB = os.path.join(LIB_DIR, "libattncache.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+         "-I", os.path.join(ROOT, "include"), "-I", CSRC] + os.environ.get("ATTNCACHE_EXTRA_FLAGS", "").split()
 
 
 def _deps():

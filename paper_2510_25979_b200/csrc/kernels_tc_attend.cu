@@ -12,8 +12,10 @@
 // moves (rescaling O in TMEM and l) when the running max exceeds it by more than 8 (log2 units),
 // so P <= 2^8 and the correction is rare.  At the item's end O / l is rounded and stored with
 // 32-byte (full-sector) stores.
-// Roles (320 threads): warp 0 TMA loader (Q per item, K_j/V_j per block), warp 1 MMA issuer +
-// TMEM owner, warps 2-9 the two softmax/epilogue groups (TMEM lane quarter = warp % 4).
+// Roles (384 threads): warp 0 TMA loader (Q per item, K_j/V_j per block), warp 1 MMA issuer +
+// TMEM owner (warps 2-3 idle; the producer warpgroup drops to 56 registers), warps 4-11 the two
+// softmax/epilogue groups with 224 registers each (TMEM lane quarter = warp % 4), which keep the
+// whole S row in registers: one TMEM load per key block, packed f32x2 FMA/add.
 #include "kernels.cuh"
 #include "sm100.cuh"
 
@@ -24,7 +26,7 @@ using namespace sm100;
 
 namespace {
 
-constexpr int kThreads = 320;
+constexpr int kThreads = 384;  // 3 warpgroups: producers (warps 0-3), softmax group 0 (4-7), group 1 (8-11)
 constexpr int kBlk = 128;                 // queries per item = keys per block
 constexpr float kRescaleThreshold = 8.f;  // log2 units: P <= 2^8 between rescales
 
@@ -32,8 +34,9 @@ template <int kD>
 struct Cfg {
     static constexpr int kTile = kBlk * kD * 2;       // one [128][d] 16-bit tile
     static constexpr int kQSlots = kD == 64 ? 2 : 1;  // per stream
-    static constexpr int kKV = kD == 64 ? 4 : 2;      // K ring and V ring slots
-    static constexpr int kSmem = (2 * kQSlots + 2 * kKV) * kTile + 1024 + 512;
+    static constexpr int kK = kD == 64 ? 4 : 2;       // K ring slots
+    static constexpr int kV = kD == 64 ? 4 : 3;       // V ring slots (V of a block is consumed last: deeper)
+    static constexpr int kSmem = (2 * kQSlots + kK + kV) * kTile + 1024 + 512;
     static constexpr uint32_t kTmemCols = 512;        // S/P: 2 x 128 at 0; O: 2 x d at 256
 };
 
@@ -41,6 +44,30 @@ __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2): low word = first element.
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+    return ((uint64_t)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
 }
 
 struct Ring {
@@ -90,17 +117,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tmV, const AttendArgs a, const uint32_t idesc_s,
                      const uint32_t idesc_pv) {
     using C = Cfg<kD>;
-    constexpr int NQ = C::kQSlots, NKV = C::kKV;
+    constexpr int NQ = C::kQSlots, NK = C::kK, NV = C::kV;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sQ = smem;                    // [2 streams][NQ][tile]
-    uint8_t *sK = sQ + 2 * NQ * C::kTile;  // [NKV][tile]
-    uint8_t *sV = sK + NKV * C::kTile;     // [NKV][tile]
-    uint64_t *bars = (uint64_t *)(sV + NKV * C::kTile);
+    uint8_t *sK = sQ + 2 * NQ * C::kTile;  // [NK][tile]
+    uint8_t *sV = sK + NK * C::kTile;      // [NV][tile]
+    uint64_t *bars = (uint64_t *)(sV + NV * C::kTile);
     uint64_t *q_full = bars, *q_empty = q_full + 2 * NQ;
-    uint64_t *k_full = q_empty + 2 * NQ, *k_empty = k_full + NKV;
-    uint64_t *v_full = k_empty + NKV, *v_empty = v_full + NKV;
-    uint64_t *s_full = v_empty + NKV;  // [2] S of WG g computed
+    uint64_t *k_full = q_empty + 2 * NQ, *k_empty = k_full + NK;
+    uint64_t *v_full = k_empty + NK, *v_empty = v_full + NV;
+    uint64_t *s_full = v_empty + NV;   // [2] S of WG g computed
     uint64_t *p_full = s_full + 2;     // [2] P of WG g written (128 arrivals)
     uint64_t *pv_done = p_full + 2;    // [2] PV of WG g retired (S/P buffer reusable, O complete)
     uint32_t *tmem_slot = (uint32_t *)(pv_done + 2);
@@ -111,9 +138,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&q_full[s], 1);
             mbar_init(&q_empty[s], 1);
         }
-        for (int s = 0; s < NKV; ++s) {
+        for (int s = 0; s < NK; ++s) {
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
+        }
+        for (int s = 0; s < NV; ++s) {
             mbar_init(&v_full[s], 1);
             mbar_init(&v_empty[s], 1);
         }
@@ -142,10 +171,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t items = units * n_qb;
     const uint32_t stride = 2 * gridDim.x;
 
-    if (warp < 2) {
-        // The loader (warp 0) and the MMA issuer (warp 1) walk the same merged order of events:
-        // one key block of stream 0, one of stream 1, ... (a finished stream is skipped).
-        if (lane == 0) {
+    if (warp < 4) {
+        // Producer warpgroup: gives registers to the softmax groups (setmaxnreg; the register file is
+        // split per SM sub-partition, and each holds one warp of every warpgroup: 56 + 2 x 224 regs).
+        setmaxnreg_dec<56>();
+        // The loader (warp 0) and the MMA issuer (warp 1), one lane each, walk the same merged order of
+        // events: one key block of stream 0, one of stream 1, ... (a finished stream is skipped).
+        // Warps 2-3 idle.  (A whole-warp MMA issuer polling the barriers was measured slower.)
+        if (warp < 2 && lane == 0) {
             Stream st0, st1;
             st0.init(blockIdx.x, stride, items, units, per_row, n_qb, S, a.list.rows);
             st1.init(blockIdx.x + gridDim.x, stride, items, units, per_row, n_qb, S, a.list.rows);
@@ -158,9 +191,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t pend_kv = 0, pend_b = 0;
             bool pend_first = false;
             auto issue_pv = [&]() {
-                const Ring rv = ring<NKV>(pend_kv);
+                const Ring rv = ring<NV>(pend_kv);
                 mbar_wait(&p_full[pend_g], pend_b & 1u);
+#if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
                 mbar_wait(&v_full[rv.slot], rv.phase);
+#endif
                 tc_fence_after();
                 const uint32_t v_base = smem_u32(sV + rv.slot * C::kTile);
 #pragma unroll
@@ -177,7 +212,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int j = s.j;
                 const Ring rq = ring<NQ>(qcnt);
                 const uint32_t qslot = g * NQ + rq.slot;
-                const Ring rkv = ring<NKV>(kv);
+                const Ring rk = ring<NK>(kv), rv = ring<NV>(kv);
+#if defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5)  // experiment: no loads
+                if (warp == 0) {
+                } else
+#endif
                 if (warp == 0) {
                     // ------------------------------ TMA loader ---------------------------------
                     if (j == 0) {
@@ -187,25 +226,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tma_load_2d(smem_u32(sQ + qslot * C::kTile + h * (kBlk * 128)), &tmQ, &q_full[qslot],
                                         h * 64, (int32_t)(s.row0 + s.qb * kBlk));
                     }
-                    mbar_wait(&k_empty[rkv.slot], rkv.phase ^ 1u);
-                    mbar_arrive_expect_tx(&k_full[rkv.slot], C::kTile);
+                    mbar_wait(&k_empty[rk.slot], rk.phase ^ 1u);
+                    mbar_arrive_expect_tx(&k_full[rk.slot], C::kTile);
                     for (int h = 0; h < kD / 64; ++h)
-                        tma_load_2d(smem_u32(sK + rkv.slot * C::kTile + h * (kBlk * 128)), &tmK, &k_full[rkv.slot],
+                        tma_load_2d(smem_u32(sK + rk.slot * C::kTile + h * (kBlk * 128)), &tmK, &k_full[rk.slot],
                                     h * 64, (int32_t)(s.row0 + j * kBlk));
-                    mbar_wait(&v_empty[rkv.slot], rkv.phase ^ 1u);
-                    mbar_arrive_expect_tx(&v_full[rkv.slot], C::kTile);
+                    mbar_wait(&v_empty[rv.slot], rv.phase ^ 1u);
+                    mbar_arrive_expect_tx(&v_full[rv.slot], C::kTile);
                     for (int h = 0; h < kD / 64; ++h)
-                        tma_load_2d(smem_u32(sV + rkv.slot * C::kTile + h * (kBlk * 128)), &tmV, &v_full[rkv.slot],
+                        tma_load_2d(smem_u32(sV + rv.slot * C::kTile + h * (kBlk * 128)), &tmV, &v_full[rv.slot],
                                     h * 64, (int32_t)(s.row0 + j * kBlk));
                 } else {
                     // ------------------------------ MMA issuer ---------------------------------
                     if (pend_g == g) issue_pv();
+#if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
                     if (j == 0) mbar_wait(&q_full[qslot], rq.phase);
-                    mbar_wait(&k_full[rkv.slot], rkv.phase);
-                    if (bcnt > 0) mbar_wait(&pv_done[g], (bcnt - 1) & 1u);  // S/P buffer free
+                    mbar_wait(&k_full[rk.slot], rk.phase);
+#endif
+                    // S overwrites the S/P columns the group's previous PV reads: tcgen05.mma ops issued by
+                    // this thread execute in issue order (the tcgen05 pipeline), so S is queued right behind
+                    // that PV without waiting for it to retire and the tensor pipe never drains here.
                     tc_fence_after();
                     const uint32_t q_base = smem_u32(sQ + qslot * C::kTile);
-                    const uint32_t k_base = smem_u32(sK + rkv.slot * C::kTile);
+                    const uint32_t k_base = smem_u32(sK + rk.slot * C::kTile);
 #pragma unroll
                     for (int k = 0; k < kD / 16; ++k) {
                         const uint32_t off = (k >> 2) * (kBlk * 128) + (k & 3) * 32;
@@ -213,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  smem_desc(k_base + off, 16, 1024, kSwizzle128B), idesc_s, k != 0);
                     }
                     umma_commit(&s_full[g]);
-                    umma_commit(&k_empty[rkv.slot]);
+                    umma_commit(&k_empty[rk.slot]);
                     if (j == s.qb) umma_commit(&q_empty[qslot]);
                     if (pend_g >= 0) issue_pv();  // the other group's PV overlaps this group's softmax
                     pend_g = g;
@@ -233,7 +276,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ------------------------------ softmax + epilogue (one WG per stream) -------------------
-        const int g = (warp - 2) >> 2;
+        setmaxnreg_inc<224>();  // the whole S row (128 fp32) stays in registers
+        const int g = (warp - 4) >> 2;
         const int q = warp & 3;       // TMEM lane quarter
         const int r = q * 32 + lane;  // query row inside the block == TMEM lane
         const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
@@ -249,28 +293,43 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int j = s.j;
             const bool diag = j == s.qb;
             const int lim = diag ? r : kBlk - 1;            // keys k <= lim are visible (causal mask)
-            const int n_chunks = diag ? q + 1 : kBlk / 32;  // warp-uniform: 32-key chunks with visible keys
             mbar_wait(&s_full[g], b & 1u);
             tc_fence_after();
-            // Diagonal blocks mask keys k > r per lane; the others take the unpredicated path.
-            float mx = -INFINITY;
-            auto max_pass = [&](auto masked) {
-                for (int c = 0; c < n_chunks; ++c) {
-                    uint32_t v[32];
-                    tmem_ld_32x32b_x32(s_addr + c * 32, v);
-                    tmem_ld_wait();
-                    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            // The whole S row (128 keys) is loaded from TMEM once (two back-to-back loads, one wait) and
+            // kept in registers for the max and the exponentials.  Diagonal blocks set keys k > r to -inf,
+            // which the exponential turns into an exact 0.
+#if defined(ATT_EXP) && (ATT_EXP == 1 || ATT_EXP == 4 || ATT_EXP == 5)  // experiment: no softmax math
+            {
+                uint32_t w[16];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (!decltype(masked)::value || c * 32 + e <= lim)
-                            m4[e & 3] = fmaxf(m4[e & 3], __uint_as_float(v[e]));
-                    mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
-                }
-            };
-            if (diag)
-                max_pass(std::true_type{});
-            else
-                max_pass(std::false_type{});
+                for (int e = 0; e < 16; ++e) w[e] = 0u;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_st_32x32b_x16(s_addr + c * 16, w);
+                l = 1.f;
+            }
+            if (false) {
+#else
+            {
+#endif
+            uint32_t sv[kBlk];
+            tmem_ld_32x32b_x64(s_addr, sv);
+            tmem_ld_32x32b_x64(s_addr + 64, sv + 64);
+            tmem_ld_wait();
+            if (diag) {
+#pragma unroll
+                for (int e = 0; e < kBlk; ++e)
+                    if (e > lim) sv[e] = 0xff800000u;  // -inf
+            }
+            float m8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m8[i] = fmaxf(__uint_as_float(sv[i]), __uint_as_float(sv[8 + i]));
+#pragma unroll
+            for (int e = 16; e < kBlk; e += 16)
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    m8[i] = fmaxf(m8[i], fmaxf(__uint_as_float(sv[e + i]), __uint_as_float(sv[e + 8 + i])));
+            const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                   fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
             const float m_blk = mx * sl2;
             if (j == 0) {
                 m_ref = m_blk;
@@ -296,53 +355,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                 l *= alpha;
                 m_ref = m_blk;
             }
-            // p = exp2(s * scale * log2e - m_ref), rounded to the MMA dtype and written over the
-            // consumed S columns; l sums the unrounded p (an unbiased estimate of the rounded sum,
-            // within 2^-9 relative; keeps the row sum off the critical path).
-            float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-            auto exp_pass = [&](auto masked) {
+            // p = exp2(s * scale * log2e - m_ref) for key pairs (packed f32x2 FMA / add), rounded to the MMA
+            // dtype two keys per 32-bit word, written in place (sv[e] <- keys 2e, 2e+1) and then over the
+            // consumed S columns; l sums the unrounded p (an unbiased estimate of the rounded sum, within
+            // 2^-9 relative; keeps the row sum off the critical path).
+            {
+                const uint64_t scale2 = pack2(sl2, sl2), neg_m2 = pack2(-m_ref, -m_ref);
+                uint64_t rs2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-                for (int c = 0; c < kBlk / 32; ++c) {
-                    uint32_t w[16];
-                    if (c < n_chunks) {
-                        uint32_t v[32];
-                        tmem_ld_32x32b_x32(s_addr + c * 32, v);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) {
-                            const int k0 = c * 32 + 2 * e;
-                            float p0 = ex2(fmaf(__uint_as_float(v[2 * e]), sl2, -m_ref));
-                            float p1 = ex2(fmaf(__uint_as_float(v[2 * e + 1]), sl2, -m_ref));
-                            if (decltype(masked)::value) {
-                                p0 = k0 <= lim ? p0 : 0.f;
-                                p1 = k0 + 1 <= lim ? p1 : 0.f;
-                            }
-                            rs4[e & 3] += p0 + p1;
-                            if constexpr (kBF16) {
-                                __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                                w[e] = *reinterpret_cast<uint32_t *>(&h2);
-                            } else {
-                                __half2 h2 = __floats2half2_rn(p0, p1);
-                                w[e] = *reinterpret_cast<uint32_t *>(&h2);
-                            }
-                        }
+                for (int e = 0; e < kBlk / 2; ++e) {
+                    const uint64_t x2 = ffma2(((uint64_t)sv[2 * e + 1] << 32) | sv[2 * e], scale2, neg_m2);
+#if defined(ATT_EXP) && ATT_EXP == 2  // experiment: no MUFU
+                    const float p0 = __uint_as_float((uint32_t)x2) * 0.001f, p1 = __uint_as_float((uint32_t)(x2 >> 32)) * 0.001f;
+#else
+                    const float p0 = ex2(__uint_as_float((uint32_t)x2)), p1 = ex2(__uint_as_float((uint32_t)(x2 >> 32)));
+#endif
+                    rs2[e & 3] = fadd2(rs2[e & 3], pack2(p0, p1));
+                    if constexpr (kBF16) {
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                        sv[e] = *reinterpret_cast<uint32_t *>(&h2);
                     } else {
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) w[e] = 0u;
+                        __half2 h2 = __floats2half2_rn(p0, p1);
+                        sv[e] = *reinterpret_cast<uint32_t *>(&h2);
                     }
-                    // keys [32c, 32c+32) -> P columns [16c, 16c+16) (those S columns are consumed)
-                    tmem_st_32x32b_x16(s_addr + c * 16, w);
                 }
-            };
-            if (diag)
-                exp_pass(std::true_type{});
-            else
-                exp_pass(std::false_type{});
-            l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t w[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) w[e] = sv[c * 16 + e];
+                    tmem_st_32x32b_x16(s_addr + c * 16, w);  // keys [32c, 32c+32) -> P columns [16c, 16c+16)
+                }
+                const uint64_t t2 = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
+                l += __uint_as_float((uint32_t)t2) + __uint_as_float((uint32_t)(t2 >> 32));
+            }
+            }
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&p_full[g]);
+#if defined(ATT_EXP) && ATT_EXP == 5  // experiment: skeleton without the epilogue
+            if (false) {
+#else
             if (diag) {
+#endif
                 // epilogue: the item's last PV retired -> O / l -> act dtype -> 32-byte stores
                 mbar_wait(&pv_done[g], b & 1u);
                 tc_fence_after();
