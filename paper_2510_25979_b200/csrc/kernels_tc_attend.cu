@@ -10,8 +10,8 @@
 //   O    (d columns)    O += P V_j (TS MMA: A = P from TMEM, B = V MN-major from smem).
 // Online softmax with lazy rescaling: P is taken relative to a reference max m_ref that only
 // moves (rescaling O in TMEM and l) when the running max exceeds it by more than 8 (log2 units),
-// so P <= 2^8 and the correction is rare.  At the item's end O / l is rounded and stored with
-// 32-byte (full-sector) stores.
+// so P <= 2^8 and the correction is rare.  At the item's end O / l is rounded, staged per warp in a
+// 128B-swizzled shared tile and written with TMA stores.
 // Roles (384 threads): warp 0 TMA loader (Q per item, K_j/V_j per block), warp 1 MMA issuer +
 // TMEM owner (warps 2-3 idle; the producer warpgroup drops to 56 registers), warps 4-11 the two
 // softmax/epilogue groups with 224 registers each (TMEM lane quarter = warp % 4), which keep the
@@ -35,8 +35,9 @@ struct Cfg {
     static constexpr int kTile = kBlk * kD * 2;       // one [128][d] 16-bit tile
     static constexpr int kQSlots = kD == 64 ? 2 : 1;  // per stream
     static constexpr int kK = kD == 64 ? 4 : 2;       // K ring slots
-    static constexpr int kV = kD == 64 ? 4 : 3;       // V ring slots (V of a block is consumed last: deeper)
-    static constexpr int kSmem = (2 * kQSlots + kK + kV) * kTile + 1024 + 512;
+    static constexpr int kV = kD == 64 ? 4 : 2;       // V ring slots
+    static constexpr int kOutWarp = 32 * 64 * 2;     // per softmax warp: O staging [32 rows][64 cols] (128B swizzle)
+    static constexpr int kSmem = (2 * kQSlots + kK + kV) * kTile + 8 * kOutWarp + 1024 + 512;
     static constexpr uint32_t kTmemCols = 512;        // S/P: 2 x 128 at 0; O: 2 x d at 256
 };
 
@@ -114,8 +115,8 @@ struct Stream {
 template <int kD, bool kBF16>
 __global__ void __launch_bounds__(kThreads, 1)
     attend_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                     const __grid_constant__ CUtensorMap tmV, const AttendArgs a, const uint32_t idesc_s,
-                     const uint32_t idesc_pv) {
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                     const AttendArgs a, const uint32_t idesc_s, const uint32_t idesc_pv) {
     using C = Cfg<kD>;
     constexpr int NQ = C::kQSlots, NK = C::kK, NV = C::kV;
     extern __shared__ uint8_t smem_raw[];
@@ -123,7 +124,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t *sQ = smem;                    // [2 streams][NQ][tile]
     uint8_t *sK = sQ + 2 * NQ * C::kTile;  // [NK][tile]
     uint8_t *sV = sK + NK * C::kTile;      // [NV][tile]
-    uint64_t *bars = (uint64_t *)(sV + NV * C::kTile);
+    uint8_t *sOut = sV + NV * C::kTile;    // [8 softmax warps][kOutWarp]
+    uint64_t *bars = (uint64_t *)(sOut + 8 * C::kOutWarp);
     uint64_t *q_full = bars, *q_empty = q_full + 2 * NQ;
     uint64_t *k_full = q_empty + 2 * NQ, *k_empty = k_full + NK;
     uint64_t *v_full = k_empty + NK, *v_empty = v_full + NV;
@@ -157,6 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmQ);
         tma_prefetch_desc(&tmK);
         tma_prefetch_desc(&tmV);
+        tma_prefetch_desc(&tmO);
     }
     if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
     tc_fence_before();
@@ -283,8 +286,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
         const uint32_t s_addr = tmem + lane_addr + g * kBlk;
         const uint32_t o_addr = tmem + lane_addr + 256 + g * kD;
+        uint8_t *stage_o = sOut + (warp - 4) * C::kOutWarp;
+        const uint32_t stage_o_u32 = smem_u32(stage_o);
         const float sl2 = a.scale * 1.4426950408889634f;  // scale * log2(e)
-        uint16_t *O = (uint16_t *)a.O;
         Stream s;
         s.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, a.list.rows);
         uint32_t b = 0;  // key blocks of this stream
@@ -402,19 +406,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&pv_done[g], b & 1u);
                 tc_fence_after();
                 const float inv = 1.f / l;
-                uint16_t *dst = O + (s.row0 + s.qb * kBlk + r) * (int64_t)kD;
+                // TMEM -> registers -> act dtype -> this warp's 128B-swizzled staging tile -> TMA store of the
+                // warp's 32 rows, 64 columns at a time (full-line writes; per-thread row stores stalled the
+                // group on the LSU and delayed its next P)
+                const int32_t orow = (int32_t)(s.row0 + s.qb * kBlk + q * 32);
 #pragma unroll
-                for (int c = 0; c < kD / 32; ++c) {
-                    uint32_t v[32];
-                    tmem_ld_32x32b_x32(o_addr + c * 32, v);
+                for (int half = 0; half < kD / 64; ++half) {
+                    uint32_t v[64];
+                    tmem_ld_32x32b_x32(o_addr + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                    tmem_ld_32x32b_x32(o_addr + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
                     tmem_ld_wait();
+                    if (lane == 0) bulk_wait_read<0>();  // the previous TMA store has read the staging tile
+                    __syncwarp();
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        uint32_t w[8];
+                    for (int c8 = 0; c8 < 8; ++c8) {
+                        uint32_t w[4];
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            const float lo = __uint_as_float(v[h * 16 + 2 * e]) * inv;
-                            const float hi = __uint_as_float(v[h * 16 + 2 * e + 1]) * inv;
+                        for (int e = 0; e < 4; ++e) {
+                            const float lo = __uint_as_float(v[c8 * 8 + 2 * e]) * inv;
+                            const float hi = __uint_as_float(v[c8 * 8 + 2 * e + 1]) * inv;
                             if constexpr (kBF16) {
                                 __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
                                 w[e] = *reinterpret_cast<uint32_t *>(&h2);
@@ -423,7 +433,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 w[e] = *reinterpret_cast<uint32_t *>(&h2);
                             }
                         }
-                        st_global_v8(dst + c * 32 + h * 16, w);
+                        *reinterpret_cast<uint4 *>(stage_o + sw128_offset(lane, c8)) = make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tmO, stage_o_u32, half * 64, orow);
+                        bulk_commit();
                     }
                 }
                 tc_fence_before();
@@ -431,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++b;
             s.advance();
         }
+        if (lane == 0) bulk_wait<0>();  // O stores complete before the CTA (and its smem) retires
     }
     __syncthreads();
     if (warp == 1) {
@@ -444,8 +461,9 @@ cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
     using C = Cfg<kD>;
     const bool bf16 = a.dt == ATTNCACHE_BF16;
     const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
-    CUtensorMap tq, tk, tv;
+    CUtensorMap tq, tk, tv, to;
     cudaError_t e = make_tmap_2d_16(&tq, a.Q, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
+    if (e == cudaSuccess) e = make_tmap_2d_16(&to, a.O, bf16, kD, rows, (uint64_t)kD * 2, 64, 32, 128);
     if (e == cudaSuccess) e = make_tmap_2d_16(&tk, a.K, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e == cudaSuccess) e = make_tmap_2d_16(&tv, a.V, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e != cudaSuccess) return e;
@@ -454,7 +472,7 @@ cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
     const uint32_t fmt = bf16 ? 1u : 0u;
     const uint32_t idesc_s = idesc_f16(kBlk, kBlk, fmt, 0u, 0u);  // Q K-major x K K-major
     const uint32_t idesc_pv = idesc_f16(kBlk, kD, fmt, 0u, 1u);   // P (TMEM) x V MN-major
-    attend_tc_kernel<kD, kBF16><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, tv, a, idesc_s, idesc_pv);
+    attend_tc_kernel<kD, kBF16><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, tv, to, a, idesc_s, idesc_pv);
     count_launches(1);
     return cudaGetLastError();
 }
