@@ -12,8 +12,8 @@
 // moves (rescaling O in TMEM and l) when the running max exceeds it by more than 8 (log2 units),
 // so P <= 2^8 and the correction is rare.  At the item's end O / l is rounded, staged per warp in a
 // 128B-swizzled shared tile and written with TMA stores.
-// Roles (384 threads): warp 0 TMA loader (Q per item, K_j/V_j per block), warp 1 MMA issuer +
-// TMEM owner (warps 2-3 idle; the producer warpgroup drops to 56 registers), warps 4-11 the two
+// Roles (384 threads): warp 0 TMA loader of Q (per item) and K_j, warp 2 TMA loader of V_j, warp 1 MMA
+// issuer + TMEM owner (warp 3 idle; the producer warpgroup drops to 56 registers), warps 4-11 the two
 // softmax/epilogue groups with 224 registers each (TMEM lane quarter = warp % 4), which keep the
 // whole S row in registers: one TMEM load per key block, packed f32x2 FMA/add.
 #include "kernels.cuh"
@@ -71,6 +71,27 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
     return d;
 }
 
+#if defined(ATT_TRACE)  // timeline experiment (scripts/attend_trace.py): clock64 stamps of CTA 0
+__device__ unsigned long long g_att_trace[2][256][6];     // softmax warps 4 / 8, lane 0, first 256 blocks
+__device__ unsigned long long g_att_trace_mma[512][8];    // MMA warp, first 512 events
+#define ATT_TRACE_REC(slot)                                                                       \
+    do {                                                                                          \
+        if (blockIdx.x == 0 && lane == 0 && (warp == 4 || warp == 8) && b < 256)                   \
+            g_att_trace[warp == 8][b][slot] = clock64();                                           \
+    } while (0)
+#define ATT_TRACE_MMA(ev, slot)                                                                   \
+    do {                                                                                          \
+        if (blockIdx.x == 0 && warp == 1 && (ev) < 512) g_att_trace_mma[(ev)][slot] = clock64();   \
+    } while (0)
+#else
+#define ATT_TRACE_REC(slot) \
+    do {                    \
+    } while (0)
+#define ATT_TRACE_MMA(ev, slot) \
+    do {                        \
+    } while (0)
+#endif
+
 struct Ring {
     uint32_t slot, phase;
 };
@@ -80,24 +101,32 @@ __device__ __forceinline__ Ring ring(uint32_t i) {
 }
 
 // One CTA-local item stream: items t = first, first + stride, ...; item -> (unit's first row,
-// query block qb), heaviest query blocks first.  j walks the item's key blocks.
+// query block qb).  Units are taken in L2-sized groups of `group` units (K/V of a group fit in about
+// 48 MB of L2) and inside a group the heaviest query blocks come first: every query block of a unit
+// re-reads the unit's K/V blocks, and ordering all units' qb = n_qb-1 blocks first (the previous
+// order) made those re-reads come from HBM (3.3x the algorithmic bytes at configs[3]).  The last
+// group is the batch's tail, still heaviest first, so the persistent CTAs finish together.
+// j walks the item's key blocks.
 struct Stream {
-    uint32_t t, stride, items, units, per_row, n_qb, S;
+    uint32_t t, stride, items, units, per_row, n_qb, S, group;
     const int32_t *rows;
     bool active = false;
     int64_t row0 = 0;
     int qb = 0, j = 0;
     __device__ void init(uint32_t first, uint32_t stride_, uint32_t items_, uint32_t units_, uint32_t per_row_,
-                         uint32_t n_qb_, uint32_t S_, const int32_t *rows_) {
+                         uint32_t n_qb_, uint32_t S_, uint32_t group_, const int32_t *rows_) {
         t = first, stride = stride_, items = items_, units = units_, per_row = per_row_, n_qb = n_qb_, S = S_;
+        group = group_;
         rows = rows_;
         start_item();
     }
     __device__ void start_item() {
         active = t < items;
         if (!active) return;
-        const uint32_t u = t % units;
-        qb = (int)(n_qb - 1 - t / units);
+        const uint32_t gi = t / (group * n_qb), w = t - gi * (group * n_qb);
+        const uint32_t gbase = gi * group, gsize = min(group, units - gbase);
+        const uint32_t u = gbase + w % gsize;
+        qb = (int)(n_qb - 1 - w / gsize);
         row0 = ((int64_t)rows[u / per_row] * per_row + u % per_row) * S;
         j = 0;
     }
@@ -173,18 +202,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t units = (uint32_t)(*a.list.count) * per_row;
     const uint32_t items = units * n_qb;
     const uint32_t stride = 2 * gridDim.x;
+    const uint32_t l2_group = max(1u, (48u << 20) / (2u * S * kD * 2u));  // units whose K and V fit in ~48 MB
 
     if (warp < 4) {
         // Producer warpgroup: gives registers to the softmax groups (setmaxnreg; the register file is
         // split per SM sub-partition, and each holds one warp of every warpgroup: 56 + 2 x 224 regs).
         setmaxnreg_dec<56>();
-        // The loader (warp 0) and the MMA issuer (warp 1), one lane each, walk the same merged order of
+        // The Q/K loader (warp 0) and the MMA issuer (warp 1), one lane each, walk the same merged order of
         // events: one key block of stream 0, one of stream 1, ... (a finished stream is skipped).
-        // Warps 2-3 idle.  (A whole-warp MMA issuer polling the barriers was measured slower.)
-        if (warp < 2 && lane == 0) {
+        // Warp 2 loads V on its own (same event order); warp 3 idles.  (A whole-warp MMA issuer polling the
+        // barriers was measured slower.)
+        if (warp < 3 && lane == 0) {
             Stream st0, st1;
-            st0.init(blockIdx.x, stride, items, units, per_row, n_qb, S, a.list.rows);
-            st1.init(blockIdx.x + gridDim.x, stride, items, units, per_row, n_qb, S, a.list.rows);
+            st0.init(blockIdx.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows);
+            st1.init(blockIdx.x + gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows);
             uint32_t qcnt0 = 0, qcnt1 = 0;  // items started per stream (Q ring position)
             uint32_t bcnt0 = 0, bcnt1 = 0;  // key blocks per stream (S/P/PV barrier phases)
             uint32_t kv = 0;                // key blocks overall (K/V ring position)
@@ -195,19 +226,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             bool pend_first = false;
             auto issue_pv = [&]() {
                 const Ring rv = ring<NV>(pend_kv);
+                ATT_TRACE_MMA(pend_kv, 3);
                 mbar_wait(&p_full[pend_g], pend_b & 1u);
+                ATT_TRACE_MMA(pend_kv, 4);
 #if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
                 mbar_wait(&v_full[rv.slot], rv.phase);
 #endif
+                ATT_TRACE_MMA(pend_kv, 5);
                 tc_fence_after();
                 const uint32_t v_base = smem_u32(sV + rv.slot * C::kTile);
-#pragma unroll
-                for (int k = 0; k < kBlk / 16; ++k)  // A = P (8 TMEM columns = 16 keys per step)
-                    umma_f16_ts(tmem + 256 + pend_g * kD, tmem + pend_g * kBlk + k * 8,
-                                smem_desc(v_base + k * 2048, kBlk * 128, 1024, kSwizzle128B), idesc_pv,
-                                (!pend_first || k != 0) ? 1u : 0u);
+                // A = P (8 TMEM columns = 16 keys per step), B = V MN-major: 8 steps in one statement
+                umma_f16_ts_k8(tmem + 256 + pend_g * kD, tmem + pend_g * kBlk,
+                               smem_desc(v_base, kBlk * 128, 1024, kSwizzle128B), idesc_pv, pend_first ? 0u : 1u);
                 umma_commit(&v_empty[rv.slot]);
                 umma_commit(&pv_done[pend_g]);
+                ATT_TRACE_MMA(pend_kv, 6);
                 pend_g = -1;
             };
             // one key block of stream g (g is a compile-time constant at each call site)
@@ -217,11 +250,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t qslot = g * NQ + rq.slot;
                 const Ring rk = ring<NK>(kv), rv = ring<NV>(kv);
 #if defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5)  // experiment: no loads
-                if (warp == 0) {
+                if (warp != 1) {
                 } else
 #endif
-                if (warp == 0) {
-                    // ------------------------------ TMA loader ---------------------------------
+                if (warp == 2) {
+                    // ------------------------------ TMA loader: V -------------------------------
+                    // its own thread, so a V slot still held by an in-flight PV never delays the next K
+                    mbar_wait(&v_empty[rv.slot], rv.phase ^ 1u);
+                    mbar_arrive_expect_tx(&v_full[rv.slot], C::kTile);
+                    for (int h = 0; h < kD / 64; ++h)
+                        tma_load_2d(smem_u32(sV + rv.slot * C::kTile + h * (kBlk * 128)), &tmV, &v_full[rv.slot],
+                                    h * 64, (int32_t)(s.row0 + j * kBlk));
+                } else if (warp == 0) {
+                    // ------------------------------ TMA loader: Q, K ----------------------------
                     if (j == 0) {
                         mbar_wait(&q_empty[qslot], rq.phase ^ 1u);
                         mbar_arrive_expect_tx(&q_full[qslot], C::kTile);
@@ -234,31 +275,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int h = 0; h < kD / 64; ++h)
                         tma_load_2d(smem_u32(sK + rk.slot * C::kTile + h * (kBlk * 128)), &tmK, &k_full[rk.slot],
                                     h * 64, (int32_t)(s.row0 + j * kBlk));
-                    mbar_wait(&v_empty[rv.slot], rv.phase ^ 1u);
-                    mbar_arrive_expect_tx(&v_full[rv.slot], C::kTile);
-                    for (int h = 0; h < kD / 64; ++h)
-                        tma_load_2d(smem_u32(sV + rv.slot * C::kTile + h * (kBlk * 128)), &tmV, &v_full[rv.slot],
-                                    h * 64, (int32_t)(s.row0 + j * kBlk));
                 } else {
                     // ------------------------------ MMA issuer ---------------------------------
                     if (pend_g == g) issue_pv();
+                    ATT_TRACE_MMA(kv, 0);
 #if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
                     if (j == 0) mbar_wait(&q_full[qslot], rq.phase);
                     mbar_wait(&k_full[rk.slot], rk.phase);
 #endif
+                    ATT_TRACE_MMA(kv, 1);
                     // S overwrites the S/P columns the group's previous PV reads: tcgen05.mma ops issued by
                     // this thread execute in issue order (the tcgen05 pipeline), so S is queued right behind
                     // that PV without waiting for it to retire and the tensor pipe never drains here.
                     tc_fence_after();
                     const uint32_t q_base = smem_u32(sQ + qslot * C::kTile);
                     const uint32_t k_base = smem_u32(sK + rk.slot * C::kTile);
-#pragma unroll
-                    for (int k = 0; k < kD / 16; ++k) {
-                        const uint32_t off = (k >> 2) * (kBlk * 128) + (k & 3) * 32;
-                        umma_f16(tmem + g * kBlk, smem_desc(q_base + off, 16, 1024, kSwizzle128B),
-                                 smem_desc(k_base + off, 16, 1024, kSwizzle128B), idesc_s, k != 0);
-                    }
+                    static_assert(kD == 128, "8 K-steps of 16 over two 64-column swizzle halves");
+                    umma_f16_ss_k8<kBlk * 128 / 16>(tmem + g * kBlk, smem_desc(q_base, 16, 1024, kSwizzle128B),
+                                                   smem_desc(k_base, 16, 1024, kSwizzle128B), idesc_s, 0u);
                     umma_commit(&s_full[g]);
+                    ATT_TRACE_MMA(kv, 2);
                     umma_commit(&k_empty[rk.slot]);
                     if (j == s.qb) umma_commit(&q_empty[qslot]);
                     if (pend_g >= 0) issue_pv();  // the other group's PV overlaps this group's softmax
@@ -290,14 +326,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t stage_o_u32 = smem_u32(stage_o);
         const float sl2 = a.scale * 1.4426950408889634f;  // scale * log2(e)
         Stream s;
-        s.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, a.list.rows);
+        s.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows);
         uint32_t b = 0;  // key blocks of this stream
         float m_ref = 0.f, l = 0.f;
         while (s.active) {
             const int j = s.j;
             const bool diag = j == s.qb;
             const int lim = diag ? r : kBlk - 1;            // keys k <= lim are visible (causal mask)
+            ATT_TRACE_REC(0);
             mbar_wait(&s_full[g], b & 1u);
+            ATT_TRACE_REC(1);
             tc_fence_after();
             // The whole S row (128 keys) is loaded from TMEM once (two back-to-back loads, one wait) and
             // kept in registers for the max and the exponentials.  Diagonal blocks set keys k > r to -inf,
@@ -319,6 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld_32x32b_x64(s_addr, sv);
             tmem_ld_32x32b_x64(s_addr + 64, sv + 64);
             tmem_ld_wait();
+            ATT_TRACE_REC(2);
             if (diag) {
 #pragma unroll
                 for (int e = 0; e < kBlk; ++e)
@@ -334,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     m8[i] = fmaxf(m8[i], fmaxf(__uint_as_float(sv[e + i]), __uint_as_float(sv[e + 8 + i])));
             const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                                    fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+            ATT_TRACE_REC(3);
             const float m_blk = mx * sl2;
             if (j == 0) {
                 m_ref = m_blk;
@@ -395,8 +435,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             }
             tmem_st_wait();
+            ATT_TRACE_REC(4);
             tc_fence_before();
             mbar_arrive(&p_full[g]);
+            ATT_TRACE_REC(5);
 #if defined(ATT_EXP) && ATT_EXP == 5  // experiment: skeleton without the epilogue
             if (false) {
 #else
@@ -492,3 +534,11 @@ cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st)
 }
 
 }  // namespace ac
+#if defined(ATT_TRACE)
+extern "C" int attncache_debug_att_trace(void *out) {
+    return (int)cudaMemcpyFromSymbol(out, ac::g_att_trace, sizeof(ac::g_att_trace));
+}
+extern "C" int attncache_debug_att_trace_mma(void *out) {
+    return (int)cudaMemcpyFromSymbol(out, ac::g_att_trace_mma, sizeof(ac::g_att_trace_mma));
+}
+#endif

@@ -110,10 +110,15 @@ __global__ void __launch_bounds__(kThreads, Cfg<kD, kTwoCTA>::kMinBlocks)
     const uint32_t per_row = (uint32_t)(a.L * a.H);
     const uint32_t units = (uint32_t)(*a.list.count) * per_row;
     const uint32_t items = units * n_qb;
-    // item t -> (unit, qb), heaviest query blocks first so the persistent CTAs finish together.
+    // item t -> (unit, qb): units in L2-sized groups (their K and V fit in ~48 MB, so a unit's query
+    // blocks re-read K/V from L2), heaviest query blocks first inside a group so the persistent CTAs
+    // finish together (kernels_tc_attend.cu, Stream).
+    const uint32_t l2_group = max(1u, (48u << 20) / (2u * S * kD * 2u));
     auto decode = [&](uint32_t t, int64_t &unit_row0, int &qb) {
-        qb = (int)(n_qb - 1 - t / units);
-        const uint32_t u = t % units;
+        const uint32_t gi = t / (l2_group * n_qb), w = t - gi * (l2_group * n_qb);
+        const uint32_t gbase = gi * l2_group, gsize = min(l2_group, units - gbase);
+        qb = (int)(n_qb - 1 - w / gsize);
+        const uint32_t u = gbase + w % gsize;
         unit_row0 = ((int64_t)a.list.rows[u / per_row] * per_row + u % per_row) * S;
     };
 

@@ -87,10 +87,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t per_row = (uint32_t)(a.L * a.H);
     const uint32_t units = (uint32_t)(*a.list.count) * per_row;
     const uint32_t items = units * n_qb;
-    // item t -> (selected row, (layer, head), qb), heaviest query blocks first
+    // item t -> (selected row, (layer, head), qb): units in L2-sized groups (K of a group fits in ~48 MB;
+    // both passes re-read it), heaviest query blocks first inside a group
+    const uint32_t l2_group = max(1u, (48u << 20) / (S * (uint32_t)a.d * 2u));
     auto decode = [&](uint32_t t, int64_t &row, uint32_t &lh, int &qb) {
-        qb = (int)(n_qb - 1 - t / units);
-        const uint32_t u = t % units;
+        const uint32_t gi = t / (l2_group * n_qb), w = t - gi * (l2_group * n_qb);
+        const uint32_t gbase = gi * l2_group, gsize = min(l2_group, units - gbase);
+        qb = (int)(n_qb - 1 - w / gsize);
+        const uint32_t u = gbase + w % gsize;
         row = a.list.rows[u / per_row];
         lh = u % per_row;
     };

@@ -1,0 +1,51 @@
+"""Timeline of the d=128 attention softmax (CTA 0, group 0 = warp 4 and group 1 = warp 8, lane 0): builds
+the library with -DATT_TRACE out of tree, runs configs[3]'s misses once and prints per-block phase
+durations in cycles: wait for S, TMEM load of S, row max, exp + P store, arrive, and the gap to the next."""
+import ctypes
+import os
+import subprocess
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+env = dict(os.environ, ATTNCACHE_BUILD_ROOT="/tmp/atttrace", ATTNCACHE_EXTRA_FLAGS="-DATT_TRACE")
+subprocess.check_call([sys.executable, "-m", "paper_2510_25979_b200.build"], env=env, cwd=ROOT, stdout=subprocess.DEVNULL)
+import synth  # noqa: E402
+import paper_2510_25979_b200 as ac  # noqa: E402
+ac.lib_path = "/tmp/atttrace/lib/libattncache.so"
+name = sys.argv[1] if len(sys.argv) > 1 else "long_prefill"
+cfg = synth.CONFIGS[name]
+rows = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.B - cfg.n_hit
+ctx = ac.Context(0)
+g = torch.Generator(device="cuda").manual_seed(0)
+shape = (rows, cfg.L, cfg.H, cfg.S, cfg.d)
+Q, K, V = (torch.randn(shape, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+O = ac.attncache_attend_full(ctx, Q, K, V)
+torch.cuda.synchronize()
+ac.attncache_attend_full(ctx, Q, K, V, O)
+torch.cuda.synchronize()
+buf = np.zeros((2, 256, 6), dtype=np.uint64)
+lib = ac.load_library()
+assert lib.attncache_debug_att_trace(ctypes.c_void_p(buf.ctypes.data)) == 0
+t = buf.astype(np.int64)
+for grp in range(2):
+    d = np.diff(t[grp], axis=1)
+    gap = t[grp, 1:, 0] - t[grp, :-1, 5]
+    per = t[grp, 1:, 0] - t[grp, :-1, 0]
+    sel = slice(20, 200)
+    print(f"group {grp}: median cycles  wait_S {np.median(d[sel, 0]):.0f}  load_S {np.median(d[sel, 1]):.0f}  "
+          f"max {np.median(d[sel, 2]):.0f}  exp+store {np.median(d[sel, 3]):.0f}  arrive {np.median(d[sel, 4]):.0f}  "
+          f"gap {np.median(gap[sel]):.0f}  period {np.median(per[sel]):.0f}")
+print("first blocks of group 0 (wait, load, max, exp, arrive, gap):")
+for i in range(20, 30):
+    print(list(np.diff(t[0, i])), t[0, i + 1, 0] - t[0, i, 5])
+mm = np.zeros((512, 8), dtype=np.uint64)
+assert lib.attncache_debug_att_trace_mma(ctypes.c_void_p(mm.ctypes.data)) == 0
+m = mm.astype(np.int64)
+print("MMA warp, events 40..60 (cycles rel. to event 40 start): start, k_ready, S_issued | pv: start, p_full, v_full, issued")
+base = m[40, 0]
+for e in range(40, 60):
+    print(e, [int(x - base) if x else None for x in m[e, :7]])
