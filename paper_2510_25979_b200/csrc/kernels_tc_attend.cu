@@ -2,9 +2,10 @@
 // PAPER.md:376-381; Eq. 5): O = softmax(Q K^T * scale, keys j > i masked) . V.
 //
 // Work item = (unit, 128-query block qb); it visits key blocks j = 0..qb (causal block skipping).
-// Two softmax warp groups (WG0 = warps 2-5, WG1 = warps 6-9) own two independent item streams of
-// the CTA (items blockIdx.x + (2k + g) * gridDim.x) and ping-pong on the tensor core: while WG g
-// turns S into P, the MMA warp computes the other group's S or PV.  Per WG, in TMEM:
+// Two softmax warp groups (WG0 = warps 4-7, WG1 = warps 8-11) own two independent item streams of
+// the CTA (items blockIdx.x + (2k + g) * gridDim.x), each with its own loader and MMA thread, and
+// share the tensor core: while WG g turns S into P, the pipe runs the other group's S or PV.  Per WG,
+// in TMEM:
 //   S/P  (128 columns)  S = Q K_j^T (SS MMA, M=128 queries, N=128 keys, K=d, fp32); the softmax
 //                       writes bf16 P back over the first 64 columns (two keys per column).
 //   O    (d columns)    O += P V_j (TS MMA: A = P from TMEM, B = V MN-major from smem).
@@ -12,8 +13,8 @@
 // moves (rescaling O in TMEM and l) when the running max exceeds it by more than 8 (log2 units),
 // so P <= 2^8 and the correction is rare.  At the item's end O / l is rounded, staged per warp in a
 // 128B-swizzled shared tile and written with TMA stores.
-// Roles (384 threads): warp 0 TMA loader of Q (per item) and K_j, warp 2 TMA loader of V_j, warp 1 MMA
-// issuer + TMEM owner (warp 3 idle; the producer warpgroup drops to 56 registers), warps 4-11 the two
+// Roles (384 threads): per group g, warp 2g loads its Q (per item), K_j and V_j by TMA and warp 2g+1
+// issues its MMAs (warp 1 also owns TMEM); the producer warpgroup drops to 56 registers, warps 4-11 the two
 // softmax/epilogue groups with 224 registers each (TMEM lane quarter = warp % 4), which keep the
 // whole S row in registers: one TMEM load per key block, packed f32x2 FMA/add.
 #include "kernels.cuh"
@@ -34,8 +35,8 @@ template <int kD>
 struct Cfg {
     static constexpr int kTile = kBlk * kD * 2;       // one [128][d] 16-bit tile
     static constexpr int kQSlots = kD == 64 ? 2 : 1;  // per stream
-    static constexpr int kK = kD == 64 ? 4 : 2;       // K ring slots
-    static constexpr int kV = kD == 64 ? 4 : 2;       // V ring slots
+    static constexpr int kK = 2;                      // K: one slot per group
+    static constexpr int kV = 2;                      // V: one slot per group
     static constexpr int kOutWarp = 32 * 64 * 2;     // per softmax warp: O staging [32 rows][64 cols] (128B swizzle)
     static constexpr int kSmem = (2 * kQSlots + kK + kV) * kTile + 8 * kOutWarp + 1024 + 512;
     static constexpr uint32_t kTmemCols = 512;        // S/P: 2 x 128 at 0; O: 2 x d at 256
@@ -205,113 +206,82 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t l2_group = max(1u, (48u << 20) / (2u * S * kD * 2u));  // units whose K and V fit in ~48 MB
 
     if (warp < 4) {
-        // Producer warpgroup: gives registers to the softmax groups (setmaxnreg; the register file is
-        // split per SM sub-partition, and each holds one warp of every warpgroup: 56 + 2 x 224 regs).
+        // Producer warpgroup: two independent per-group pipelines.  Group g (= item stream g) has its own
+        // loader thread (warp 2g: Q per item, K_j and V_j per key block, one smem slot each) and its own
+        // MMA-issuing thread (warp 2g+1: S_j, then PV_j once the group's softmax has written P_j).  Both
+        // MMA threads feed the one tensor pipe, so while one thread waits for its softmax or pays the
+        // per-event bookkeeping the other keeps the pipe busy (a single issuing thread left it idle for
+        // ~45% of each key block, measured with scripts/attend_trace.py).  The registers go to the
+        // softmax groups (setmaxnreg; the register file is split per SM sub-partition, each holding one
+        // warp of every warpgroup: 56 + 2 x 224).
         setmaxnreg_dec<56>();
-        // The Q/K loader (warp 0) and the MMA issuer (warp 1), one lane each, walk the same merged order of
-        // events: one key block of stream 0, one of stream 1, ... (a finished stream is skipped).
-        // Warp 2 loads V on its own (same event order); warp 3 idles.  (A whole-warp MMA issuer polling the
-        // barriers was measured slower.)
-        if (warp < 3 && lane == 0) {
-            Stream st0, st1;
-            st0.init(blockIdx.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows);
-            st1.init(blockIdx.x + gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows);
-            uint32_t qcnt0 = 0, qcnt1 = 0;  // items started per stream (Q ring position)
-            uint32_t bcnt0 = 0, bcnt1 = 0;  // key blocks per stream (S/P/PV barrier phases)
-            uint32_t kv = 0;                // key blocks overall (K/V ring position)
-            // MMA: PV of an event is issued after the S of the next event (ping-pong) unless the
-            // next event belongs to the same group (its S needs the S/P buffer that PV reads).
-            int pend_g = -1;
-            uint32_t pend_kv = 0, pend_b = 0;
-            bool pend_first = false;
-            auto issue_pv = [&]() {
-                const Ring rv = ring<NV>(pend_kv);
-                ATT_TRACE_MMA(pend_kv, 3);
-                mbar_wait(&p_full[pend_g], pend_b & 1u);
-                ATT_TRACE_MMA(pend_kv, 4);
+        const int g = warp >> 1;
+        if (lane == 0) {
+            Stream st;
+            st.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows);
+            uint32_t b = 0, it = 0;  // key blocks and items of this stream
+            if ((warp & 1) == 0) {
+                // ------------------------------ TMA loader of group g ----------------------------
+                const uint32_t q_s = smem_u32(sQ + g * C::kTile), k_s = smem_u32(sK + g * C::kTile);
+                const uint32_t v_s = smem_u32(sV + g * C::kTile);
+                while (st.active) {
 #if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
-                mbar_wait(&v_full[rv.slot], rv.phase);
-#endif
-                ATT_TRACE_MMA(pend_kv, 5);
-                tc_fence_after();
-                const uint32_t v_base = smem_u32(sV + rv.slot * C::kTile);
-                // A = P (8 TMEM columns = 16 keys per step), B = V MN-major: 8 steps in one statement
-                umma_f16_ts_k8(tmem + 256 + pend_g * kD, tmem + pend_g * kBlk,
-                               smem_desc(v_base, kBlk * 128, 1024, kSwizzle128B), idesc_pv, pend_first ? 0u : 1u);
-                umma_commit(&v_empty[rv.slot]);
-                umma_commit(&pv_done[pend_g]);
-                ATT_TRACE_MMA(pend_kv, 6);
-                pend_g = -1;
-            };
-            // one key block of stream g (g is a compile-time constant at each call site)
-            auto event = [&](Stream &s, const int g, uint32_t &qcnt, uint32_t &bcnt) {
-                const int j = s.j;
-                const Ring rq = ring<NQ>(qcnt);
-                const uint32_t qslot = g * NQ + rq.slot;
-                const Ring rk = ring<NK>(kv), rv = ring<NV>(kv);
-#if defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5)  // experiment: no loads
-                if (warp != 1) {
-                } else
-#endif
-                if (warp == 2) {
-                    // ------------------------------ TMA loader: V -------------------------------
-                    // its own thread, so a V slot still held by an in-flight PV never delays the next K
-                    mbar_wait(&v_empty[rv.slot], rv.phase ^ 1u);
-                    mbar_arrive_expect_tx(&v_full[rv.slot], C::kTile);
-                    for (int h = 0; h < kD / 64; ++h)
-                        tma_load_2d(smem_u32(sV + rv.slot * C::kTile + h * (kBlk * 128)), &tmV, &v_full[rv.slot],
-                                    h * 64, (int32_t)(s.row0 + j * kBlk));
-                } else if (warp == 0) {
-                    // ------------------------------ TMA loader: Q, K ----------------------------
-                    if (j == 0) {
-                        mbar_wait(&q_empty[qslot], rq.phase ^ 1u);
-                        mbar_arrive_expect_tx(&q_full[qslot], C::kTile);
+                    const int32_t r_j = (int32_t)(st.row0 + st.j * kBlk);
+                    if (st.j == 0) {
+                        mbar_wait(&q_empty[g], (it & 1u) ^ 1u);
+                        mbar_arrive_expect_tx(&q_full[g], C::kTile);
                         for (int h = 0; h < kD / 64; ++h)
-                            tma_load_2d(smem_u32(sQ + qslot * C::kTile + h * (kBlk * 128)), &tmQ, &q_full[qslot],
-                                        h * 64, (int32_t)(s.row0 + s.qb * kBlk));
+                            tma_load_2d(q_s + h * (kBlk * 128), &tmQ, &q_full[g], h * 64, (int32_t)(st.row0 + st.qb * kBlk));
                     }
-                    mbar_wait(&k_empty[rk.slot], rk.phase ^ 1u);
-                    mbar_arrive_expect_tx(&k_full[rk.slot], C::kTile);
-                    for (int h = 0; h < kD / 64; ++h)
-                        tma_load_2d(smem_u32(sK + rk.slot * C::kTile + h * (kBlk * 128)), &tmK, &k_full[rk.slot],
-                                    h * 64, (int32_t)(s.row0 + j * kBlk));
-                } else {
-                    // ------------------------------ MMA issuer ---------------------------------
-                    if (pend_g == g) issue_pv();
-                    ATT_TRACE_MMA(kv, 0);
-#if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
-                    if (j == 0) mbar_wait(&q_full[qslot], rq.phase);
-                    mbar_wait(&k_full[rk.slot], rk.phase);
+                    mbar_wait(&k_empty[g], (b & 1u) ^ 1u);
+                    mbar_arrive_expect_tx(&k_full[g], C::kTile);
+                    for (int h = 0; h < kD / 64; ++h) tma_load_2d(k_s + h * (kBlk * 128), &tmK, &k_full[g], h * 64, r_j);
+                    mbar_wait(&v_empty[g], (b & 1u) ^ 1u);
+                    mbar_arrive_expect_tx(&v_full[g], C::kTile);
+                    for (int h = 0; h < kD / 64; ++h) tma_load_2d(v_s + h * (kBlk * 128), &tmV, &v_full[g], h * 64, r_j);
 #endif
-                    ATT_TRACE_MMA(kv, 1);
-                    // S overwrites the S/P columns the group's previous PV reads: tcgen05.mma ops issued by
-                    // this thread execute in issue order (the tcgen05 pipeline), so S is queued right behind
-                    // that PV without waiting for it to retire and the tensor pipe never drains here.
-                    tc_fence_after();
-                    const uint32_t q_base = smem_u32(sQ + qslot * C::kTile);
-                    const uint32_t k_base = smem_u32(sK + rk.slot * C::kTile);
-                    static_assert(kD == 128, "8 K-steps of 16 over two 64-column swizzle halves");
-                    umma_f16_ss_k8<kBlk * 128 / 16>(tmem + g * kBlk, smem_desc(q_base, 16, 1024, kSwizzle128B),
-                                                   smem_desc(k_base, 16, 1024, kSwizzle128B), idesc_s, 0u);
-                    umma_commit(&s_full[g]);
-                    ATT_TRACE_MMA(kv, 2);
-                    umma_commit(&k_empty[rk.slot]);
-                    if (j == s.qb) umma_commit(&q_empty[qslot]);
-                    if (pend_g >= 0) issue_pv();  // the other group's PV overlaps this group's softmax
-                    pend_g = g;
-                    pend_kv = kv;
-                    pend_b = bcnt;
-                    pend_first = j == 0;
+                    ++b;
+                    if (st.advance()) ++it;
                 }
-                ++bcnt;
-                ++kv;
-                if (s.advance()) ++qcnt;
-            };
-            while (st0.active || st1.active) {
-                if (st0.active) event(st0, 0, qcnt0, bcnt0);
-                if (st1.active) event(st1, 1, qcnt1, bcnt1);
+            } else {
+                // ------------------------------ MMA issuer of group g ----------------------------
+                // S_j overwrites the S/P columns PV_{j-1} reads: tcgen05.mma ops of one thread execute in
+                // issue order (the tcgen05 pipeline), so S_j is issued right behind PV_{j-1}.
+                const uint32_t q_b = smem_u32(sQ + g * C::kTile), k_b = smem_u32(sK + g * C::kTile);
+                const uint32_t v_b = smem_u32(sV + g * C::kTile);
+                const uint32_t s_t = tmem + g * kBlk, o_t = tmem + 256 + g * kD;
+                while (st.active) {
+                    const int j = st.j;
+                    ATT_TRACE_MMA(b * 2 + g, 0);
+#if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
+                    if (j == 0) mbar_wait(&q_full[g], it & 1u);
+                    mbar_wait(&k_full[g], b & 1u);
+#endif
+                    ATT_TRACE_MMA(b * 2 + g, 1);
+                    tc_fence_after();
+                    static_assert(kD == 128, "8 K-steps of 16 over two 64-column swizzle halves");
+                    umma_f16_ss_k8<kBlk * 128 / 16>(s_t, smem_desc(q_b, 16, 1024, kSwizzle128B),
+                                                   smem_desc(k_b, 16, 1024, kSwizzle128B), idesc_s, 0u);
+                    umma_commit(&s_full[g]);
+                    umma_commit(&k_empty[g]);
+                    if (j == st.qb) umma_commit(&q_empty[g]);
+                    ATT_TRACE_MMA(b * 2 + g, 2);
+                    mbar_wait(&p_full[g], b & 1u);
+                    ATT_TRACE_MMA(b * 2 + g, 4);
+#if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
+                    mbar_wait(&v_full[g], b & 1u);
+#endif
+                    ATT_TRACE_MMA(b * 2 + g, 5);
+                    tc_fence_after();
+                    // A = P (8 TMEM columns = 16 keys per step), B = V MN-major: 8 steps in one statement
+                    umma_f16_ts_k8(o_t, s_t, smem_desc(v_b, kBlk * 128, 1024, kSwizzle128B), idesc_pv, j == 0 ? 0u : 1u);
+                    umma_commit(&v_empty[g]);
+                    umma_commit(&pv_done[g]);
+                    ATT_TRACE_MMA(b * 2 + g, 6);
+                    ++b;
+                    if (st.advance()) ++it;
+                }
             }
-            if (warp == 1 && pend_g >= 0) issue_pv();
         }
     } else {
         // ------------------------------ softmax + epilogue (one WG per stream) -------------------
