@@ -93,6 +93,32 @@ __device__ unsigned long long g_att_trace_mma[512][8];    // MMA warp, first 512
     } while (0)
 #endif
 
+// Key pairs (of every 8) whose exp2 runs as a polynomial on the FMA pipe on off-diagonal blocks.  0: the
+// sweep (scripts/attend_poly.sh; configs[3]: 0 -> 1.52 ms, 2 -> 1.54, 3 -> 1.56, 4 -> 1.63) shows the
+// softmax is bound by its instruction stream and latency, not by MUFU throughput, on this kernel.
+#ifndef ATT_POLY_PAIRS
+#define ATT_POLY_PAIRS 0
+#endif
+constexpr int kPolyPairs = ATT_POLY_PAIRS;
+
+// 2^x for a pair of fp32 values on the FMA/ALU pipes (no MUFU): x = j + f with j = round(x) (the
+// 1.5*2^23 shift trick leaves j in the low mantissa bits of t) and f in [-0.5, 0.5]; 2^f by a degree-3
+// minimax polynomial (max relative error 7.5e-5, far below the 2^-9 of the bf16 P it feeds); 2^j is
+// added to the exponent field.  x is clamped to >= -125 so the exponent cannot wrap (2^-125 is 0 at
+// bf16 resolution against the row's largest term, 1).  Inputs are finite (off-diagonal blocks).
+__device__ __forceinline__ void exp2_poly2(uint64_t x2, float &p0, float &p1) {
+    const float x0 = fmaxf(__uint_as_float((uint32_t)x2), -125.f), x1 = fmaxf(__uint_as_float((uint32_t)(x2 >> 32)), -125.f);
+    const uint64_t xc = pack2(x0, x1);
+    const uint64_t t2 = fadd2(xc, pack2(12582912.f, 12582912.f));       // 1.5 * 2^23 + round(x)
+    const uint64_t j2 = fadd2(t2, pack2(-12582912.f, -12582912.f));     // round(x) as fp32
+    const uint64_t f2 = ffma2(j2, pack2(-1.f, -1.f), xc);              // f = x - round(x)
+    uint64_t q2 = ffma2(pack2(0.05517154f, 0.05517154f), f2, pack2(0.24261118f, 0.24261118f));
+    q2 = ffma2(q2, f2, pack2(0.69326102f, 0.69326102f));
+    q2 = ffma2(q2, f2, pack2(0.99992807f, 0.99992807f));
+    p0 = __uint_as_float((uint32_t)q2 + ((uint32_t)t2 << 23));
+    p1 = __uint_as_float((uint32_t)(q2 >> 32) + ((uint32_t)(t2 >> 32) << 23));
+}
+
 struct Ring {
     uint32_t slot, phase;
 };
@@ -376,23 +402,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             {
                 const uint64_t scale2 = pack2(sl2, sl2), neg_m2 = pack2(-m_ref, -m_ref);
                 uint64_t rs2[4] = {0ull, 0ull, 0ull, 0ull};
+                // Off-diagonal blocks may compute kPolyPairs of every 8 key pairs with a polynomial exp2 on
+                // the FMA pipe (exp2_poly2), the rest on MUFU.EX2; diagonal blocks (masked keys at -inf)
+                // use MUFU only.
+                auto exp_pass = [&](auto poly) {
 #pragma unroll
-                for (int e = 0; e < kBlk / 2; ++e) {
-                    const uint64_t x2 = ffma2(((uint64_t)sv[2 * e + 1] << 32) | sv[2 * e], scale2, neg_m2);
+                    for (int e = 0; e < kBlk / 2; ++e) {
+                        const uint64_t x2 = ffma2(((uint64_t)sv[2 * e + 1] << 32) | sv[2 * e], scale2, neg_m2);
+                        float p0, p1;
 #if defined(ATT_EXP) && ATT_EXP == 2  // experiment: no MUFU
-                    const float p0 = __uint_as_float((uint32_t)x2) * 0.001f, p1 = __uint_as_float((uint32_t)(x2 >> 32)) * 0.001f;
+                        p0 = __uint_as_float((uint32_t)x2) * 0.001f, p1 = __uint_as_float((uint32_t)(x2 >> 32)) * 0.001f;
 #else
-                    const float p0 = ex2(__uint_as_float((uint32_t)x2)), p1 = ex2(__uint_as_float((uint32_t)(x2 >> 32)));
+                        if (decltype(poly)::value && (e & 7) < kPolyPairs) {
+                            exp2_poly2(x2, p0, p1);
+                        } else {
+                            p0 = ex2(__uint_as_float((uint32_t)x2));
+                            p1 = ex2(__uint_as_float((uint32_t)(x2 >> 32)));
+                        }
 #endif
-                    rs2[e & 3] = fadd2(rs2[e & 3], pack2(p0, p1));
-                    if constexpr (kBF16) {
-                        __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                        sv[e] = *reinterpret_cast<uint32_t *>(&h2);
-                    } else {
-                        __half2 h2 = __floats2half2_rn(p0, p1);
-                        sv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        rs2[e & 3] = fadd2(rs2[e & 3], pack2(p0, p1));
+                        if constexpr (kBF16) {
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                            sv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        } else {
+                            __half2 h2 = __floats2half2_rn(p0, p1);
+                            sv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        }
                     }
-                }
+                };
+                if (diag)
+                    exp_pass(std::false_type{});
+                else
+                    exp_pass(std::true_type{});
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     uint32_t w[16];
