@@ -34,7 +34,7 @@ constexpr float kRescaleThreshold = 8.f;  // log2 units: P <= 2^8 between rescal
 template <int kD>
 struct Cfg {
     static constexpr int kTile = kBlk * kD * 2;       // one [128][d] 16-bit tile
-    static constexpr int kQSlots = kD == 64 ? 2 : 1;  // per stream
+    static constexpr int kQSlots = 1;                 // per stream
     static constexpr int kK = 2;                      // K: one slot per group
     static constexpr int kV = 2;                      // V: one slot per group
     static constexpr int kOutWarp = 32 * 64 * 2;     // per softmax warp: O staging [32 rows][64 cols] (128B swizzle)
@@ -285,9 +285,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
                     ATT_TRACE_MMA(b * 2 + g, 1);
                     tc_fence_after();
-                    static_assert(kD == 128, "8 K-steps of 16 over two 64-column swizzle halves");
-                    umma_f16_ss_k8<kBlk * 128 / 16>(s_t, smem_desc(q_b, 16, 1024, kSwizzle128B),
-                                                   smem_desc(k_b, 16, 1024, kSwizzle128B), idesc_s, 0u);
+                    if constexpr (kD == 128) {  // 8 K-steps of 16 over two 64-column swizzle halves
+                        umma_f16_ss_k8<kBlk * 128 / 16>(s_t, smem_desc(q_b, 16, 1024, kSwizzle128B),
+                                                       smem_desc(k_b, 16, 1024, kSwizzle128B), idesc_s, 0u);
+                    } else {  // d = 64: 4 K-steps inside one swizzle atom column
+#pragma unroll
+                        for (int k = 0; k < kD / 16; ++k)
+                            umma_f16(s_t, smem_desc(q_b + k * 32, 16, 1024, kSwizzle128B),
+                                     smem_desc(k_b + k * 32, 16, 1024, kSwizzle128B), idesc_s, k != 0);
+                    }
                     umma_commit(&s_full[g]);
                     umma_commit(&k_empty[g]);
                     if (j == st.qb) umma_commit(&q_empty[g]);
@@ -540,7 +546,9 @@ cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st)
     const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
     if (rows >= (1ull << 31) || (uint64_t)a.max_rows * a.L * a.H * (a.S / kBlk) >= (1ull << 31))
         return cudaErrorInvalidValue;
-    if (a.d == 64) return launch_attend_tc64(a, sm_count, st);
+    // d = 64 uses the same two-group kernel (the earlier two-CTA-per-SM d = 64 kernel with O in registers
+    // reached 78 % of the HBM roofline at configs[1]; this one 94 %)
+    if (a.d == 64) return a.dt == ATTNCACHE_BF16 ? launch<64, true>(a, sm_count, st) : launch<64, false>(a, sm_count, st);
     return a.dt == ATTNCACHE_BF16 ? launch<128, true>(a, sm_count, st) : launch<128, false>(a, sm_count, st);
 }
 
