@@ -8,8 +8,11 @@
 //   pass 1: S again; P = exp2(s*scale*log2e - m - log2 l), masked, rounded, stored.
 // Recomputing S (2x the Q K^T flops) keeps the kernel one launch with no score round trip through
 // HBM; the kernel is bound by writing the maps.
-// Roles (192 threads): warp 0 TMA loader, warp 1 MMA issuer + TMEM owner (2 S buffers), warps 2-5
-// epilogue (TMEM lane quarter = warp % 4, one query row per thread).
+// Roles (384 threads): two independent groups (two item streams per CTA), each with a TMA loader thread
+// (warp 2g), an MMA thread (warp 2g+1; two 128-column S buffers per group) and a 4-warp epilogue group
+// (warps 4-7 / 8-11; TMEM lane quarter = warp % 4, one query row per thread, the S row held in
+// registers: one TMEM load per block).  A single epilogue group left the kernel at 0.29 of its HBM
+// roofline (bench stages.capture_misses, configs[1]).
 #include "kernels.cuh"
 #include "sm100.cuh"
 
@@ -18,16 +21,15 @@ using namespace sm100;
 
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 384;  // 3 warpgroups: producers (warps 0-3), epilogue group 0 (4-7), group 1 (8-11)
 constexpr int kBlk = 128;
 
 template <int kD>
 struct Cfg {
     static constexpr int kTile = kBlk * kD * 2;
-    static constexpr int kQSlots = 2;
-    static constexpr int kKSlots = kD == 64 ? 6 : 4;
-    static constexpr int kSmem = (kQSlots + kKSlots) * kTile + 1024 + 512;
-    static constexpr uint32_t kTmemCols = 256;  // two 128-column S buffers
+    static constexpr int kKSlots = 2;  // per group
+    static constexpr int kSmem = (2 + 2 * kKSlots) * kTile + 1024 + 512;
+    static constexpr uint32_t kTmemCols = 512;  // per group two 128-column S buffers
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -40,33 +42,41 @@ __device__ __forceinline__ float lg2(float x) {
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
 
 template <int kD>
 __global__ void __launch_bounds__(kThreads, 1)
     capture_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                       const CaptureArgs a, const uint32_t idesc) {
     using C = Cfg<kD>;
-    constexpr int NQ = C::kQSlots, NK = C::kKSlots;
+    constexpr int NK = C::kKSlots;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t *sQ = smem, *sK = smem + NQ * C::kTile;
-    uint64_t *bars = (uint64_t *)(sK + NK * C::kTile);
-    uint64_t *q_full = bars, *q_empty = q_full + NQ;
-    uint64_t *k_full = q_empty + NQ, *k_empty = k_full + NK;
-    uint64_t *s_full = k_empty + NK, *s_free = s_full + 2;
-    uint32_t *tmem_slot = (uint32_t *)(s_free + 2);
+    uint8_t *sQ = smem, *sK = smem + 2 * C::kTile;  // Q: [group]; K: [group][NK]
+    uint64_t *bars = (uint64_t *)(sK + 2 * NK * C::kTile);
+    uint64_t *q_full = bars, *q_empty = q_full + 2;        // [group]
+    uint64_t *k_full = q_empty + 2, *k_empty = k_full + 2 * NK;  // [group][NK]
+    uint64_t *s_full = k_empty + 2 * NK, *s_free = s_full + 4;   // [group][2 S buffers]
+    uint32_t *tmem_slot = (uint32_t *)(s_free + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NQ; ++s) {
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&q_full[s], 1);
             mbar_init(&q_empty[s], 1);
         }
-        for (int s = 0; s < NK; ++s) {
+        for (int s = 0; s < 2 * NK; ++s) {
             mbar_init(&k_full[s], 1);
             mbar_init(&k_empty[s], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 4; ++i) {
             mbar_init(&s_full[i], 1);
             mbar_init(&s_free[i], 128);
         }
@@ -87,6 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t per_row = (uint32_t)(a.L * a.H);
     const uint32_t units = (uint32_t)(*a.list.count) * per_row;
     const uint32_t items = units * n_qb;
+    const uint32_t stride = 2 * gridDim.x;  // two item streams per CTA (one per group)
     // item t -> (selected row, (layer, head), qb): units in L2-sized groups (K of a group fits in ~48 MB;
     // both passes re-read it), heaviest query blocks first inside a group
     const uint32_t l2_group = max(1u, (48u << 20) / (S * (uint32_t)a.d * 2u));
@@ -99,29 +110,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         lh = u % per_row;
     };
 
-    if (warp < 2) {
+    if (warp < 4) {
+        // Producers: per group g, warp 2g loads Q (per item) and K_j (per block and pass), warp 2g+1
+        // issues S_j = Q K_j^T into one of the group's two S buffers.  The two groups are independent
+        // pipelines sharing the tensor pipe (as in kernels_tc_attend.cu).
+        setmaxnreg_dec<56>();
+        const int g = warp >> 1;
         if (lane == 0) {
             uint32_t it = 0, blk = 0;
-            for (uint32_t t = blockIdx.x; t < items; t += gridDim.x, ++it) {
+            for (uint32_t t = blockIdx.x + g * gridDim.x; t < items; t += stride, ++it) {
                 int64_t row;
                 uint32_t lh;
                 int qb;
                 decode(t, row, lh, qb);
                 const int64_t row0 = (row * per_row + lh) * (int64_t)S;  // first Q/K row of the unit
-                const uint32_t qs = it % NQ, qph = (it / NQ) & 1u;
-                if (warp == 0) {
-                    mbar_wait(&q_empty[qs], qph ^ 1u);
-                    mbar_arrive_expect_tx(&q_full[qs], C::kTile);
+                const uint32_t qph = it & 1u;
+                if ((warp & 1) == 0) {
+                    mbar_wait(&q_empty[g], qph ^ 1u);
+                    mbar_arrive_expect_tx(&q_full[g], C::kTile);
                     for (int h = 0; h < kD / 64; ++h)
-                        tma_load_2d(smem_u32(sQ + qs * C::kTile + h * (kBlk * 128)), &tmQ, &q_full[qs], h * 64,
+                        tma_load_2d(smem_u32(sQ + g * C::kTile + h * (kBlk * 128)), &tmQ, &q_full[g], h * 64,
                                     (int32_t)(row0 + qb * kBlk));
                 } else {
-                    mbar_wait(&q_full[qs], qph);
+                    mbar_wait(&q_full[g], qph);
                 }
                 for (int pass = 0; pass < 2; ++pass) {
                     for (int j = 0; j <= qb; ++j, ++blk) {
-                        const uint32_t ks = blk % NK, kph = (blk / NK) & 1u;
-                        if (warp == 0) {
+                        const uint32_t ks = g * NK + blk % NK, kph = (blk / NK) & 1u;
+                        if ((warp & 1) == 0) {
                             mbar_wait(&k_empty[ks], kph ^ 1u);
                             mbar_arrive_expect_tx(&k_full[ks], C::kTile);
                             for (int h = 0; h < kD / 64; ++h)
@@ -130,24 +146,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                         } else {
                             const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
                             mbar_wait(&k_full[ks], kph);
-                            mbar_wait(&s_free[buf], bph ^ 1u);
+                            mbar_wait(&s_free[g * 2 + buf], bph ^ 1u);
                             tc_fence_after();
-                            const uint32_t q_base = smem_u32(sQ + qs * C::kTile), k_base = smem_u32(sK + ks * C::kTile);
+                            const uint32_t q_base = smem_u32(sQ + g * C::kTile), k_base = smem_u32(sK + ks * C::kTile);
 #pragma unroll
                             for (int k = 0; k < kD / 16; ++k) {
                                 const uint32_t off = (k >> 2) * (kBlk * 128) + (k & 3) * 32;
-                                umma_f16(tmem + buf * kBlk, smem_desc(q_base + off, 16, 1024, kSwizzle128B),
+                                umma_f16(tmem + g * 256 + buf * kBlk, smem_desc(q_base + off, 16, 1024, kSwizzle128B),
                                          smem_desc(k_base + off, 16, 1024, kSwizzle128B), idesc, k != 0);
                             }
-                            umma_commit(&s_full[buf]);
+                            umma_commit(&s_full[g * 2 + buf]);
                             umma_commit(&k_empty[ks]);
-                            if (pass == 1 && j == qb) umma_commit(&q_empty[qs]);
+                            if (pass == 1 && j == qb) umma_commit(&q_empty[g]);
                         }
                     }
                 }
             }
         }
     } else {
+        // ------------------------------ epilogue group g (one query row per thread) -----------------
+        setmaxnreg_inc<224>();
+        const int g = (warp - 4) >> 2;
         const int q = warp & 3;
         const int r = q * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
@@ -156,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool bf16 = a.map_dt == ATTNCACHE_BF16;
         const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
         uint32_t blk = 0;
-        for (uint32_t t = blockIdx.x; t < items; t += gridDim.x) {
+        for (uint32_t t = blockIdx.x + g * gridDim.x; t < items; t += stride) {
             int64_t row;
             uint32_t lh;
             int qb;
@@ -171,49 +190,50 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
                     const bool diag = j == qb;
                     const int lim = diag ? r : kBlk - 1;
-                    const int n_chunks = diag ? q + 1 : kBlk / 32;
-                    mbar_wait(&s_full[buf], bph);
+                    mbar_wait(&s_full[g * 2 + buf], bph);
                     tc_fence_after();
-                    const uint32_t s_addr = tmem + lane_addr + buf * kBlk;
+                    const uint32_t s_addr = tmem + lane_addr + g * 256 + buf * kBlk;
+                    // the whole S row of the block in registers (one TMEM round trip); masked keys -inf
+                    uint32_t sv[kBlk];
+                    tmem_ld_32x32b_x64(s_addr, sv);
+                    tmem_ld_32x32b_x64(s_addr + 64, sv + 64);
+                    tmem_ld_wait();
+                    tc_fence_before();
+                    mbar_arrive(&s_free[g * 2 + buf]);  // S is in registers: the buffer may be refilled
+                    if (diag) {
+#pragma unroll
+                        for (int e = 0; e < kBlk; ++e)
+                            if (e > lim) sv[e] = 0xff800000u;
+                    }
                     if (pass == 0) {
-                        for (int c = 0; c < n_chunks; ++c) {
-                            uint32_t v[32];
-                            tmem_ld_32x32b_x32(s_addr + c * 32, v);
-                            tmem_ld_wait();
-                            float mx = -INFINITY;
+                        float m8[8];
 #pragma unroll
-                            for (int e = 0; e < 32; ++e)
-                                if (c * 32 + e <= lim) mx = fmaxf(mx, __uint_as_float(v[e]) * sl2);
-                            const float m_new = fmaxf(m, mx);
-                            float sum = 0.f;
+                        for (int i = 0; i < 8; ++i) m8[i] = fmaxf(__uint_as_float(sv[i]), __uint_as_float(sv[8 + i]));
 #pragma unroll
-                            for (int e = 0; e < 32; ++e)
-                                if (c * 32 + e <= lim) sum += ex2(fmaf(__uint_as_float(v[e]), sl2, -m_new));
-                            l = l * ex2(m - m_new) + sum;
-                            m = m_new;
-                        }
-                        tc_fence_before();
-                        mbar_arrive(&s_free[buf]);
+                        for (int e = 16; e < kBlk; e += 16)
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                m8[i] = fmaxf(m8[i], fmaxf(__uint_as_float(sv[e + i]), __uint_as_float(sv[e + 8 + i])));
+                        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * sl2;
+                        const float m_new = fmaxf(m, mx);
+                        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                        for (int e = 0; e < kBlk; ++e) s4[e & 3] += ex2(fmaf(__uint_as_float(sv[e]), sl2, -m_new));
+                        l = l * ex2(m - m_new) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
+                        m = m_new;
                         if (diag) off = m + lg2(l);  // P = exp2(s*sl2 - off)
                     } else {
-                        // this block's columns [128j, 128j + 128) that the row stores (the TMEM loads
-                        // are warp-uniform; only the stores depend on the lane's row length)
+                        // this block's columns [128j, 128j + 128) that the row stores
                         const int c0 = j * kBlk;
                         const int ncols = min(kBlk, stored - c0);
 #pragma unroll
                         for (int c = 0; c < kBlk / 32; ++c) {
-                            uint32_t v[32];
-                            if (c < n_chunks) {
-                                tmem_ld_32x32b_x32(s_addr + c * 32, v);
-                                tmem_ld_wait();
-                            }
                             uint32_t w[16];
 #pragma unroll
                             for (int e = 0; e < 16; ++e) {
-                                const int k0 = c * 32 + 2 * e;
-                                const float p0 = (c < n_chunks && k0 <= lim) ? ex2(fmaf(__uint_as_float(v[2 * e]), sl2, -off)) : 0.f;
-                                const float p1 =
-                                    (c < n_chunks && k0 + 1 <= lim) ? ex2(fmaf(__uint_as_float(v[2 * e + 1]), sl2, -off)) : 0.f;
+                                const float p0 = ex2(fmaf(__uint_as_float(sv[c * 32 + 2 * e]), sl2, -off));
+                                const float p1 = ex2(fmaf(__uint_as_float(sv[c * 32 + 2 * e + 1]), sl2, -off));
                                 if (bf16) {
                                     __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                                     w[e] = *reinterpret_cast<uint32_t *>(&h2);
@@ -223,12 +243,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             }
                             uint4 *dst = (uint4 *)(mrow + c0 + c * 32);
+#if defined(CAP_EXP) && CAP_EXP == 1  // experiment: no map stores
+                            if (w[0] == 0x12345678u && w[15] == 0x9abcdef0u) dst[0] = make_uint4(w[1], w[2], w[3], w[4]);
+#else
 #pragma unroll
                             for (int pc = 0; pc < 4; ++pc)
                                 if (c * 32 + pc * 8 < ncols) dst[pc] = make_uint4(w[4 * pc], w[4 * pc + 1], w[4 * pc + 2], w[4 * pc + 3]);
+#endif
                         }
-                        tc_fence_before();
-                        mbar_arrive(&s_free[buf]);
                     }
                 }
             }
