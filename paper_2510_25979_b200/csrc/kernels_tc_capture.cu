@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                                                fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * sl2;
                         const float m_new = fmaxf(m, mx);
+                        // row sum on MUFU.EX2 (an FMA-pipe polynomial for 2-8 of every 8 pairs was measured
+                        // slower: scripts/capture_poly.sh at configs 1/2)
                         float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                         for (int e = 0; e < kBlk; ++e) s4[e & 3] += ex2(fmaf(__uint_as_float(sv[e]), sl2, -m_new));

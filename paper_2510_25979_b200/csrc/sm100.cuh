@@ -263,6 +263,40 @@ __device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         : "memory");
 }
 
+// ---- packed fp32 pairs and an FMA-pipe exp2 ----------------------------------------------------------
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2): low word = first element.
+__device__ __forceinline__ uint64_t pack2(float lo, float hi) {
+    return ((uint64_t)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// 2^x for a pair of fp32 values on the FMA/ALU pipes (no MUFU): x = j + f with j = round(x) (the
+// 1.5*2^23 shift trick leaves j in the low mantissa bits of t) and f in [-0.5, 0.5]; 2^f by a degree-3
+// minimax polynomial (max relative error 7.5e-5, far below the 2^-9 of the bf16 P it feeds); 2^j is
+// added to the exponent field.  x is clamped to >= -125 so the exponent cannot wrap (2^-125 is 0 at
+// bf16 resolution against the row's largest term, 1).  Inputs are finite (off-diagonal blocks).
+__device__ __forceinline__ void exp2_poly2(uint64_t x2, float &p0, float &p1) {
+    const float x0 = fmaxf(__uint_as_float((uint32_t)x2), -125.f), x1 = fmaxf(__uint_as_float((uint32_t)(x2 >> 32)), -125.f);
+    const uint64_t xc = pack2(x0, x1);
+    const uint64_t t2 = fadd2(xc, pack2(12582912.f, 12582912.f));       // 1.5 * 2^23 + round(x)
+    const uint64_t j2 = fadd2(t2, pack2(-12582912.f, -12582912.f));     // round(x) as fp32
+    const uint64_t f2 = ffma2(j2, pack2(-1.f, -1.f), xc);              // f = x - round(x)
+    uint64_t q2 = ffma2(pack2(0.05517154f, 0.05517154f), f2, pack2(0.24261118f, 0.24261118f));
+    q2 = ffma2(q2, f2, pack2(0.69326102f, 0.69326102f));
+    q2 = ffma2(q2, f2, pack2(0.99992807f, 0.99992807f));
+    p0 = __uint_as_float((uint32_t)q2 + ((uint32_t)t2 << 23));
+    p1 = __uint_as_float((uint32_t)(q2 >> 32) + ((uint32_t)(t2 >> 32) << 23));
+}
+
 // ---- descriptors ----------------------------------------------------------------------------------
 // Shared-memory matrix descriptor (tcgen05): start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
 // version 1 [46,48), base offset 0 [49,52), LBO mode 0 [52], layout type [61,64).

@@ -9,6 +9,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 import paper_2510_25979_b200 as ac  # noqa: E402
 
+if os.environ.get("ATTNCACHE_LIB"):  # an out-of-tree experiment build
+    ac.lib_path = os.environ["ATTNCACHE_LIB"]
+
 name = sys.argv[1] if len(sys.argv) > 1 else "llama32_1b"
 cfg = synth.CONFIGS[name]
 rows = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.B - cfg.n_hit
