@@ -165,6 +165,16 @@ attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, co
                                         int32_t layer_begin, int32_t layer_end, int32_t head_dim,
                                         int32_t act_dtype, const void *V, void *O, void *stream);
 
+/* Grouped-query attention (GQA; SURVEY.md §8(f) f3 "optional GQA n_kv_heads"; Llama-3 models keep fewer
+ * K/V heads than query heads): the same as attncache_apply_cached with V: [n_rows][layer_end-layer_begin]
+ * [n_kv_heads][seq_len][head_dim] and O: [n_rows][layer_end-layer_begin][n_heads][seq_len][head_dim]; the map
+ * of query head h multiplies V head h / (n_heads / n_kv_heads).  n_kv_heads == n_heads is exactly
+ * attncache_apply_cached.  Errors as apply_cached, plus SHAPE when n_kv_heads does not divide n_heads. */
+attncache_status attncache_apply_cached_gqa(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                            int32_t layer_begin, int32_t layer_end, int32_t head_dim,
+                                            int32_t n_kv_heads, int32_t act_dtype, const void *V, void *O,
+                                            void *stream);
+
 /* ---- Alg. 2 miss branch core (Eq. 5) -------
  *
  * O = softmax(Q K^T * scale with keys j > i masked) . V for every selected row b (skip == NULL
@@ -176,6 +186,14 @@ attncache_status attncache_attend_full(attncache_ctx *ctx, int64_t batch, int32_
                                        int32_t seq_len, int32_t head_dim, int32_t act_dtype, const void *Q,
                                        const void *K, const void *V, float scale, const uint8_t *skip, void *O,
                                        void *stream);
+
+/* GQA variant: Q, O: [batch][n_layers][n_heads][seq_len][head_dim]; K, V: [batch][n_layers][n_kv_heads]
+ * [seq_len][head_dim]; query head h attends with K/V head h / (n_heads / n_kv_heads).  n_kv_heads == n_heads is
+ * exactly attncache_attend_full.  Errors as attend_full, plus SHAPE when n_kv_heads does not divide n_heads. */
+attncache_status attncache_attend_full_gqa(attncache_ctx *ctx, int64_t batch, int32_t n_layers, int32_t n_heads,
+                                           int32_t n_kv_heads, int32_t seq_len, int32_t head_dim, int32_t act_dtype,
+                                           const void *Q, const void *K, const void *V, float scale,
+                                           const uint8_t *skip, void *O, void *stream);
 
 /* ---- DB building, capture (Fig. 4 step 1; "collect
  * the input hidden states and their corresponding attention maps at each layer") --------------
@@ -206,6 +224,13 @@ attncache_status attncache_project_features(attncache_ctx *ctx, const void *h, i
                                             int32_t act_dtype, const void *W1, const float *b1, int32_t hidden_dim,
                                             const void *W2, const float *b2, int32_t feat_dim, int32_t feat_dtype,
                                             void *features, void *stream);
+
+/* GQA variant of attncache_capture_maps: K: [batch][L][n_kv_heads][S][d], one map per query head (query head h
+ * uses K head h / (n_heads / n_kv_heads)).  Errors as capture_maps, plus SHAPE (n_kv_heads not dividing n_heads). */
+attncache_status attncache_capture_maps_gqa(attncache_ctx *ctx, int64_t batch, int32_t n_layers, int32_t n_heads,
+                                            int32_t n_kv_heads, int32_t seq_len, int32_t head_dim, int32_t act_dtype,
+                                            const void *Q, const void *K, float scale, const uint8_t *skip,
+                                            int32_t map_dtype, int32_t map_layout, void *maps_out, void *stream);
 
 /* ---- RoPE for the Eq. 5 block-level comparison (Alg. 2 l.379) ----------
  * In place on X [n_units][S][d] (act_dtype): for i < d/2 the pair (x_i, x_{i+d/2}) at position p

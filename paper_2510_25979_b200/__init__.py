@@ -25,7 +25,8 @@ __all__ = [
     "attncache_apply_cached", "attncache_attend_full", "attncache_route_plan", "attncache_gather_rows",
     "attncache_scatter_rows", "attncache_fetch_maps", "attncache_variant", "attncache_version", "attncache_launch_count",
     "attncache_packed_map_elems", "attncache_pack_maps", "pack_db_maps", "attncache_capture_maps", "attncache_rope",
-    "attncache_affinity_plan", "attncache_project_features", "ABI_FUNCTIONS",
+    "attncache_affinity_plan", "attncache_project_features", "attncache_apply_cached_gqa", "attncache_attend_full_gqa",
+    "attncache_capture_maps_gqa", "ABI_FUNCTIONS",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -39,6 +40,7 @@ ABI_FUNCTIONS = [
     "attncache_route_plan", "attncache_gather_rows", "attncache_scatter_rows", "attncache_fetch_maps",
     "attncache_variant", "attncache_launch_count", "attncache_packed_map_elems", "attncache_pack_maps",
     "attncache_capture_maps", "attncache_rope", "attncache_affinity_plan", "attncache_project_features",
+    "attncache_apply_cached_gqa", "attncache_attend_full_gqa", "attncache_capture_maps_gqa",
 ]
 
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -98,6 +100,9 @@ def load_library():
         "attncache_capture_maps": ([P, I64, I32, I32, I32, I32, I32, P, P, F32, P, I32, I32, P, P], I32),
         "attncache_affinity_plan": ([P, P, I64, P, I32, ctypes.c_double, ctypes.c_double, P, P], I32),
         "attncache_project_features": ([P, P, I64, I32, I32, P, P, I32, P, P, I32, I32, P, P], I32),
+        "attncache_apply_cached_gqa": ([P, P, P, I64, I32, I32, I32, I32, I32, P, P, P], I32),
+        "attncache_attend_full_gqa": ([P, I64, I32, I32, I32, I32, I32, I32, P, P, P, F32, P, P, P], I32),
+        "attncache_capture_maps_gqa": ([P, I64, I32, I32, I32, I32, I32, I32, P, P, F32, P, I32, I32, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -287,21 +292,32 @@ def attncache_keys_decode(keys: torch.Tensor, tau: float, idx=None, score=None, 
 def attncache_apply_cached(db: Database, idx: torch.Tensor, V: torch.Tensor, O: Optional[torch.Tensor] = None,
                            hit: Optional[torch.Tensor] = None, layer_begin: int = 0, layer_end: Optional[int] = None,
                            stream=None) -> torch.Tensor:
-    """Alg. 2 l.373-375: O[b] = maps[idx[b]] . V[b] for selected rows; V, O [B][L'][H][S][d]."""
+    """Alg. 2 l.373-375: O[b] = maps[idx[b]] . V[b] for selected rows; V [B][L'][Hkv][S][d], O [B][L'][H][S][d]
+    (Hkv = H: multi-head; Hkv < H dividing H: grouped-query attention, map head h reads V head h // (H // Hkv))."""
     _dev(V, "V")
     _dev(idx, "idx")
     layer_end = db.n_layers if layer_end is None else layer_end
-    O = torch.empty_like(V) if O is None else O
+    if V.dim() != 5 or V.shape[0] != idx.shape[0]:
+        raise ValueError("V must be [B][L'][Hkv][S][d] matching idx")
+    H = db.n_heads if db.maps is not None else V.shape[2]
+    if O is None:
+        O = torch.empty((V.shape[0], V.shape[1], H, V.shape[3], V.shape[4]), dtype=V.dtype, device=V.device)
     _dev(O, "O")
-    if V.dim() != 5 or O.shape != V.shape or V.shape[0] != idx.shape[0]:
-        raise ValueError("V/O must be [B][L'][H][S][d] matching idx")
-    if db.maps is not None and (V.shape[1] != layer_end - layer_begin or V.shape[2] != db.n_heads
-                                or V.shape[3] != db.seq_len):
-        raise AttnCacheError(2, "ATTNCACHE_ERR_SHAPE", "V shape disagrees with the database (L', H, S)")
-    _check(load_library().attncache_apply_cached(db.handle, _p(idx), _p(hit), V.shape[0], int(layer_begin),
-                                                 int(layer_end), V.shape[4], _DT[V.dtype], _p(V), _p(O),
-                                                 _stream(stream, V.device)))
+    if O.shape != (V.shape[0], V.shape[1], H, V.shape[3], V.shape[4]):
+        raise ValueError("O must be [B][L'][H][S][d] with V's B, L', S, d")
+    if db.maps is not None and (V.shape[1] != layer_end - layer_begin or V.shape[3] != db.seq_len):
+        raise AttnCacheError(2, "ATTNCACHE_ERR_SHAPE", "V shape disagrees with the database (L', S)")
+    _check(load_library().attncache_apply_cached_gqa(db.handle, _p(idx), _p(hit), V.shape[0], int(layer_begin),
+                                                     int(layer_end), V.shape[4], V.shape[2], _DT[V.dtype], _p(V), _p(O),
+                                                     _stream(stream, V.device)))
     return O
+
+
+def attncache_apply_cached_gqa(db: Database, idx: torch.Tensor, V: torch.Tensor, O: Optional[torch.Tensor] = None,
+                               hit: Optional[torch.Tensor] = None, layer_begin: int = 0,
+                               layer_end: Optional[int] = None, stream=None) -> torch.Tensor:
+    """Grouped-query A.V (the C call of the same name); the head counts come from V and the database."""
+    return attncache_apply_cached(db, idx, V, O, hit, layer_begin, layer_end, stream)
 
 
 def attncache_attend_full(ctx: Context, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor,
@@ -310,14 +326,20 @@ def attncache_attend_full(ctx: Context, Q: torch.Tensor, K: torch.Tensor, V: tor
     """Alg. 2 l.376-381 / Eq. 5: O = softmax(QK^T*scale, causal) . V; Q, K, V, O [B][L][H][S][d]."""
     for t, n in ((Q, "Q"), (K, "K"), (V, "V")):
         _dev(t, n)
-    if not (Q.shape == K.shape == V.shape) or Q.dim() != 5 or not (Q.dtype == K.dtype == V.dtype):
-        raise ValueError("Q, K, V must share one [B][L][H][S][d] shape and dtype")
-    O = torch.empty_like(V) if O is None else O
+    if Q.dim() != 5 or K.shape != V.shape or not (Q.dtype == K.dtype == V.dtype) or \
+            (K.shape[0], K.shape[1], K.shape[3], K.shape[4]) != (Q.shape[0], Q.shape[1], Q.shape[3], Q.shape[4]):
+        raise ValueError("Q [B][L][H][S][d] and K, V [B][L][Hkv][S][d] must share B, L, S, d and dtype")
+    O = torch.empty_like(Q) if O is None else O
     _dev(O, "O")
     B, Lq, H, S, d = Q.shape
-    _check(load_library().attncache_attend_full(ctx.handle, B, Lq, H, S, d, _DT[Q.dtype], _p(Q), _p(K), _p(V),
-                                                float(scale), _p(skip), _p(O), _stream(stream, Q.device)))
+    _check(load_library().attncache_attend_full_gqa(ctx.handle, B, Lq, H, K.shape[2], S, d, _DT[Q.dtype], _p(Q), _p(K),
+                                                    _p(V), float(scale), _p(skip), _p(O), _stream(stream, Q.device)))
     return O
+
+
+def attncache_attend_full_gqa(ctx: Context, Q, K, V, O=None, scale: float = 0.0, skip=None, stream=None):
+    """Grouped-query causal attention (the C call of the same name): K, V with Hkv heads."""
+    return attncache_attend_full(ctx, Q, K, V, O, scale, skip, stream)
 
 
 def attncache_route_plan(idx, hit, shard_begins: torch.Tensor, owner=None, counts=None, order=None, stream=None):
@@ -399,17 +421,24 @@ def attncache_capture_maps(ctx: Context, Q: torch.Tensor, K: torch.Tensor, map_d
     [B][L][H][map] (PACKED or DENSE [..][S][S]) in map_dtype."""
     for t, n in ((Q, "Q"), (K, "K")):
         _dev(t, n)
-    if Q.shape != K.shape or Q.dim() != 5 or Q.dtype != K.dtype:
-        raise ValueError("Q, K must share one [B][L][H][S][d] shape and dtype")
+    if Q.dim() != 5 or K.dim() != 5 or Q.dtype != K.dtype or \
+            (K.shape[0], K.shape[1], K.shape[3], K.shape[4]) != (Q.shape[0], Q.shape[1], Q.shape[3], Q.shape[4]):
+        raise ValueError("Q [B][L][H][S][d] and K [B][L][Hkv][S][d] must share B, L, S, d and dtype")
     B, Lq, H, S, d = Q.shape
     if out is None:
         tail = (attncache_packed_map_elems(S),) if packed else (S, S)
         out = torch.empty((B, Lq, H, *tail), dtype=map_dtype, device=Q.device)
     _dev(out, "out")
-    _check(load_library().attncache_capture_maps(ctx.handle, B, Lq, H, S, d, _DT[Q.dtype], _p(Q), _p(K), float(scale),
-                                                 _p(skip), _DT[out.dtype], 1 if packed else 0, _p(out),
-                                                 _stream(stream, Q.device)))
+    _check(load_library().attncache_capture_maps_gqa(ctx.handle, B, Lq, H, K.shape[2], S, d, _DT[Q.dtype], _p(Q), _p(K),
+                                                     float(scale), _p(skip), _DT[out.dtype], 1 if packed else 0, _p(out),
+                                                     _stream(stream, Q.device)))
     return out
+
+
+def attncache_capture_maps_gqa(ctx: Context, Q, K, map_dtype=torch.bfloat16, packed: bool = True, out=None,
+                               scale: float = 0.0, skip=None, stream=None):
+    """Grouped-query capture (the C call of the same name): K with Hkv heads, one map per query head."""
+    return attncache_capture_maps(ctx, Q, K, map_dtype, packed, out, scale, skip, stream)
 
 
 def attncache_rope(X: torch.Tensor, base: float = 10000.0, stream=None) -> torch.Tensor:

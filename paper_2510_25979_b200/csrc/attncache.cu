@@ -296,8 +296,19 @@ attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, co
                                         int32_t layer_begin, int32_t layer_end, int32_t head_dim, int32_t act_dtype,
                                         const void *V, void *O, void *stream) {
     if (!db) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: db is NULL");
+    return attncache_apply_cached_gqa(db, idx, hit, n_rows, layer_begin, layer_end, head_dim, db->d.n_heads, act_dtype,
+                                      V, O, stream);
+}
+
+attncache_status attncache_apply_cached_gqa(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                            int32_t layer_begin, int32_t layer_end, int32_t head_dim,
+                                            int32_t n_kv_heads, int32_t act_dtype, const void *V, void *O,
+                                            void *stream) {
+    if (!db) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: db is NULL");
     const attncache_db_desc &d = db->d;
     if (d.n_layers <= 0) return fail(ATTNCACHE_ERR_STATE, "apply_cached: this database holds no maps");
+    if (n_kv_heads <= 0 || d.n_heads % n_kv_heads)
+        return fail(ATTNCACHE_ERR_SHAPE, "apply_cached: n_kv_heads %d does not divide n_heads %d", n_kv_heads, d.n_heads);
     if (n_rows < 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: n_rows < 0");
     if (layer_begin < 0 || layer_end > d.n_layers || layer_begin >= layer_end)
         return fail(ATTNCACHE_ERR_SHAPE, "apply_cached: layers [%d, %d) outside [0, %d)", layer_begin, layer_end, d.n_layers);
@@ -328,6 +339,7 @@ attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, co
     a.map_layout = d.map_layout;
     a.map_stride = map_elems(d.seq_len, d.map_layout);
     a.causal = d.maps_noncausal ? 0 : 1;
+    a.Hkv = n_kv_heads;
     a.V = V;
     a.O = O;
     a.list = rowlist_view(db->ctx->apply_list.ptr, n_rows);
@@ -346,7 +358,15 @@ attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, co
 attncache_status attncache_attend_full(attncache_ctx *ctx, int64_t batch, int32_t L, int32_t H, int32_t S, int32_t dd,
                                        int32_t act_dtype, const void *Q, const void *K, const void *V, float scale,
                                        const uint8_t *skip, void *O, void *stream) {
+    return attncache_attend_full_gqa(ctx, batch, L, H, H, S, dd, act_dtype, Q, K, V, scale, skip, O, stream);
+}
+
+attncache_status attncache_attend_full_gqa(attncache_ctx *ctx, int64_t batch, int32_t L, int32_t H, int32_t n_kv_heads,
+                                           int32_t S, int32_t dd, int32_t act_dtype, const void *Q, const void *K,
+                                           const void *V, float scale, const uint8_t *skip, void *O, void *stream) {
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "attend_full: ctx is NULL");
+    if (H > 0 && (n_kv_heads <= 0 || H % n_kv_heads))
+        return fail(ATTNCACHE_ERR_SHAPE, "attend_full: n_kv_heads %d does not divide n_heads %d", n_kv_heads, H);
     if (batch < 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "attend_full: batch < 0");
     if (L <= 0 || H <= 0 || S <= 0 || dd <= 0) return fail(ATTNCACHE_ERR_SHAPE, "attend_full: L=%d H=%d S=%d d=%d", L, H, S, dd);
     if (S > 8192) return fail(ATTNCACHE_ERR_SHAPE, "attend_full: seq_len %d > 8192", S);
@@ -369,6 +389,7 @@ attncache_status attncache_attend_full(attncache_ctx *ctx, int64_t batch, int32_
     a.d = dd;
     a.dt = act_dtype;
     a.scale = scale > 0.f ? scale : 1.0f / sqrtf((float)dd);
+    a.Hkv = n_kv_heads;
     a.Q = Q;
     a.K = K;
     a.V = V;
@@ -451,7 +472,17 @@ attncache_status attncache_capture_maps(attncache_ctx *ctx, int64_t batch, int32
                                         int32_t act_dtype, const void *Q, const void *K, float scale,
                                         const uint8_t *skip, int32_t map_dtype, int32_t map_layout, void *maps_out,
                                         void *stream) {
+    return attncache_capture_maps_gqa(ctx, batch, L, H, H, S, dd, act_dtype, Q, K, scale, skip, map_dtype, map_layout,
+                                      maps_out, stream);
+}
+
+attncache_status attncache_capture_maps_gqa(attncache_ctx *ctx, int64_t batch, int32_t L, int32_t H, int32_t n_kv_heads,
+                                            int32_t S, int32_t dd, int32_t act_dtype, const void *Q, const void *K,
+                                            float scale, const uint8_t *skip, int32_t map_dtype, int32_t map_layout,
+                                            void *maps_out, void *stream) {
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "capture_maps: ctx is NULL");
+    if (H > 0 && (n_kv_heads <= 0 || H % n_kv_heads))
+        return fail(ATTNCACHE_ERR_SHAPE, "capture_maps: n_kv_heads %d does not divide n_heads %d", n_kv_heads, H);
     if (batch < 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "capture_maps: batch < 0");
     if (L <= 0 || H <= 0 || S <= 0 || dd <= 0) return fail(ATTNCACHE_ERR_SHAPE, "capture_maps: L=%d H=%d S=%d d=%d", L, H, S, dd);
     if (S % 8 || S > 8192) return fail(ATTNCACHE_ERR_SHAPE, "capture_maps: seq_len %d (needs S %% 8 == 0, <= 8192)", S);
@@ -481,6 +512,7 @@ attncache_status attncache_capture_maps(attncache_ctx *ctx, int64_t batch, int32
     a.map_layout = map_layout;
     a.map_stride = map_elems(S, map_layout);
     a.scale = scale > 0.f ? scale : 1.0f / sqrtf((float)dd);
+    a.Hkv = n_kv_heads;
     a.Q = Q;
     a.K = K;
     a.maps = maps_out;

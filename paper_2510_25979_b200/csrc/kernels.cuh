@@ -42,6 +42,7 @@ struct ApplyArgs {
     int32_t map_layout;  // ATTNCACHE_MAPS_DENSE / _PACKED
     int64_t map_stride;  // elements per S x S map
     int32_t causal;      // 1: lower-triangular maps (decoder); 0: full maps (encoder, f3)
+    int32_t Hkv;         // V heads (grouped-query attention: map head h reads V head h / (H / Hkv)); H for MHA
     const void *V;
     void *O;
     RowList list;
@@ -54,6 +55,7 @@ cudaError_t launch_apply_tc(const ApplyArgs &a, int sm_count, cudaStream_t st);
 // ---- attend (causal softmax attention) ----
 struct AttendArgs {
     int32_t L, H, S, d, dt;
+    int32_t Hkv;  // K/V heads (grouped-query attention: query head h reads K/V head h / (H / Hkv)); H for MHA
     float scale;
     const void *Q, *K, *V;
     void *O;
@@ -67,6 +69,7 @@ cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st)
 // ---- capture (DB building: the causal maps of a prefill) ----
 struct CaptureArgs {
     int32_t L, H, S, d, dt;  // dt: Q/K dtype
+    int32_t Hkv;             // K heads (grouped-query attention); H for MHA
     int32_t map_dt, map_layout;
     int64_t map_stride;      // elements per S x S map in map_layout
     float scale;

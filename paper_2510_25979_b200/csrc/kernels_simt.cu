@@ -222,14 +222,15 @@ __global__ void __launch_bounds__(256) apply_simt_kernel(ApplyArgs a) {
         const int l = (int)(lh / a.H), h = (int)(lh % a.H);
         const int64_t row = a.list.rows[slot], ent = a.list.ents[slot];
         const MT *A = maps + ((ent * a.L + a.layer_begin + l) * a.H + h) * a.map_stride + map_row_off(i, a.S, a.map_layout);
-        const int64_t vbase = ((row * a.n_lay + l) * a.H + h) * (int64_t)a.S * a.d;
+        const int64_t vbase = ((row * a.n_lay + l) * a.Hkv + h / (a.H / a.Hkv)) * (int64_t)a.S * a.d;
+        const int64_t obase = ((row * a.n_lay + l) * a.H + h) * (int64_t)a.S * a.d;
         for (int c0 = 0; c0 < a.d; c0 += 32) {
             const int c = c0 + lane;
             float acc = 0.f;
             if (c < a.d)
                 for (int j = 0, jn = a.causal ? i : a.S - 1; j <= jn; ++j)
                     acc = fmaf(Elem<MDT>::ld(A, j), Elem<VDT>::ld(V, vbase + (int64_t)j * a.d + c), acc);
-            if (c < a.d) Elem<VDT>::st(O, vbase + (int64_t)i * a.d + c, acc);
+            if (c < a.d) Elem<VDT>::st(O, obase + (int64_t)i * a.d + c, acc);
         }
     }
 }
@@ -271,12 +272,14 @@ __global__ void __launch_bounds__(256) attend_simt_kernel(AttendArgs a) {
         const int64_t u = w / a.S;
         const int64_t slot = u / units_per_row, lh = u % units_per_row;
         const int64_t row = a.list.rows[slot];
-        const int64_t base = (row * units_per_row + lh) * (int64_t)a.S * a.d;
+        const int64_t base = (row * units_per_row + lh) * (int64_t)a.S * a.d;  // Q and O
+        const int64_t kvbase =
+            ((row * a.L + lh / a.H) * a.Hkv + (lh % a.H) / (a.H / a.Hkv)) * (int64_t)a.S * a.d;  // K and V
         float m = -INFINITY;
         for (int j = lane; j <= i; j += 32) {
             float z = 0.f;
             for (int c = 0; c < a.d; ++c)
-                z = fmaf(Elem<DT>::ld(Q, base + (int64_t)i * a.d + c), Elem<DT>::ld(K, base + (int64_t)j * a.d + c), z);
+                z = fmaf(Elem<DT>::ld(Q, base + (int64_t)i * a.d + c), Elem<DT>::ld(K, kvbase + (int64_t)j * a.d + c), z);
             z *= a.scale;
             p[j] = z;
             m = fmaxf(m, z);
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(256) attend_simt_kernel(AttendArgs a) {
         const float inv = 1.f / sum;
         for (int c = lane; c < a.d; c += 32) {
             float acc = 0.f;
-            for (int j = 0; j <= i; ++j) acc = fmaf(p[j], Elem<DT>::ld(V, base + (int64_t)j * a.d + c), acc);
+            for (int j = 0; j <= i; ++j) acc = fmaf(p[j], Elem<DT>::ld(V, kvbase + (int64_t)j * a.d + c), acc);
             Elem<DT>::st(O, base + (int64_t)i * a.d + c, acc * inv);
         }
         __syncwarp();
@@ -342,14 +345,15 @@ __global__ void __launch_bounds__(256) capture_simt_kernel(CaptureArgs a) {
         const int64_t u = w / a.S;
         const int64_t slot = u / units_per_row, lh = u % units_per_row;
         const int64_t row = a.list.rows[slot];
-        const int64_t base = (row * units_per_row + lh) * (int64_t)a.S * a.d;
+        const int64_t base = (row * units_per_row + lh) * (int64_t)a.S * a.d;  // Q
+        const int64_t kbase = ((row * a.L + lh / a.H) * a.Hkv + (lh % a.H) / (a.H / a.Hkv)) * (int64_t)a.S * a.d;
         MT *mrow = maps + (row * units_per_row + lh) * a.map_stride + map_row_off(i, a.S, a.map_layout);
         const int stored = packed ? 8 * (i / 8 + 1) : a.S;
         float m = -INFINITY;
         for (int j = lane; j <= i; j += 32) {
             float z = 0.f;
             for (int c = 0; c < a.d; ++c)
-                z = fmaf(Elem<DT>::ld(Q, base + (int64_t)i * a.d + c), Elem<DT>::ld(K, base + (int64_t)j * a.d + c), z);
+                z = fmaf(Elem<DT>::ld(Q, base + (int64_t)i * a.d + c), Elem<DT>::ld(K, kbase + (int64_t)j * a.d + c), z);
             z *= a.scale;
             p[j] = z;
             m = fmaxf(m, z);

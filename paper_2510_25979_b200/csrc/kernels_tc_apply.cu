@@ -173,7 +173,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t lh;
             int64_t row, ent;
             while (iter.next(lh, row, ent)) {
-                const int32_t vrow0 = (int32_t)((row * per_row + lh) * S);
+                // V head of map head h under grouped-query attention: h / (H / Hkv) (Hkv = H for MHA)
+                const uint32_t l = lh / (uint32_t)a.H, h = lh % (uint32_t)a.H;
+                const int32_t vrow0 = (int32_t)(((row * a.n_lay + l) * a.Hkv + h / (uint32_t)(a.H / a.Hkv)) * S);
                 for (int rb = 0; rb < n_rb; ++rb) {
                     const int n_kc = a.causal ? 2 * (rb + 1) : S / kChunk;
                     for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
@@ -293,8 +295,9 @@ cudaError_t launch(const ApplyArgs &a, int sm_count, cudaStream_t st) {
     using C = Cfg<kD>;
     const bool bf16 = a.act_dt == ATTNCACHE_BF16;
     const uint64_t rows = (uint64_t)a.max_rows * a.n_lay * a.H * a.S;
+    const uint64_t vrows = (uint64_t)a.max_rows * a.n_lay * a.Hkv * a.S;
     CUtensorMap tmV, tmO;
-    cudaError_t e = make_tmap_2d_16(&tmV, a.V, bf16, kD, rows, (uint64_t)kD * 2, 64, kChunk, 128);
+    cudaError_t e = make_tmap_2d_16(&tmV, a.V, bf16, kD, vrows, (uint64_t)kD * 2, 64, kChunk, 128);
     if (e == cudaSuccess) e = make_tmap_2d_16(&tmO, a.O, bf16, kD, rows, (uint64_t)kD * 2, 64, 32, 128);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(apply_tc_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);

@@ -102,15 +102,16 @@ __device__ __forceinline__ Ring ring(uint32_t i) {
 // group is the batch's tail, still heaviest first, so the persistent CTAs finish together.
 // j walks the item's key blocks.
 struct Stream {
-    uint32_t t, stride, items, units, per_row, n_qb, S, group;
+    uint32_t t, stride, items, units, per_row, n_qb, S, group, H, Hkv, L;
     const int32_t *rows;
     bool active = false;
-    int64_t row0 = 0;
+    int64_t row0 = 0;     // first Q / O row of the unit
+    int64_t kv_row0 = 0;  // first K / V row of the unit (its K/V head under grouped-query attention)
     int qb = 0, j = 0;
     __device__ void init(uint32_t first, uint32_t stride_, uint32_t items_, uint32_t units_, uint32_t per_row_,
-                         uint32_t n_qb_, uint32_t S_, uint32_t group_, const int32_t *rows_) {
+                         uint32_t n_qb_, uint32_t S_, uint32_t group_, const int32_t *rows_, uint32_t H_, uint32_t Hkv_) {
         t = first, stride = stride_, items = items_, units = units_, per_row = per_row_, n_qb = n_qb_, S = S_;
-        group = group_;
+        group = group_, H = H_, Hkv = Hkv_, L = per_row_ / H_;
         rows = rows_;
         start_item();
     }
@@ -121,7 +122,10 @@ struct Stream {
         const uint32_t gbase = gi * group, gsize = min(group, units - gbase);
         const uint32_t u = gbase + w % gsize;
         qb = (int)(n_qb - 1 - w / gsize);
-        row0 = ((int64_t)rows[u / per_row] * per_row + u % per_row) * S;
+        const int64_t row = rows[u / per_row];
+        const uint32_t lh = u % per_row;
+        row0 = (row * per_row + lh) * S;
+        kv_row0 = ((row * L + lh / H) * Hkv + (lh % H) / (H / Hkv)) * (int64_t)S;
         j = 0;
     }
     // Moves past the current key block; returns true when that block ended the item.
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int g = warp >> 1;
         if (lane == 0) {
             Stream st;
-            st.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows);
+            st.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
             uint32_t b = 0, it = 0;  // key blocks and items of this stream
             if ((warp & 1) == 0) {
                 // ------------------------------ TMA loader of group g ----------------------------
@@ -219,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t v_s = smem_u32(sV + g * C::kTile);
                 while (st.active) {
 #if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
-                    const int32_t r_j = (int32_t)(st.row0 + st.j * kBlk);
+                    const int32_t r_j = (int32_t)(st.kv_row0 + st.j * kBlk);
                     if (st.j == 0) {
                         mbar_wait(&q_empty[g], (it & 1u) ^ 1u);
                         mbar_arrive_expect_tx(&q_full[g], C::kTile);
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t stage_o_u32 = smem_u32(stage_o);
         const float sl2 = a.scale * 1.4426950408889634f;  // scale * log2(e)
         Stream s;
-        s.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows);
+        s.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
         uint32_t b = 0;  // key blocks of this stream
         float m_ref = 0.f, l = 0.f;
         while (s.active) {
@@ -487,11 +491,12 @@ cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
     using C = Cfg<kD>;
     const bool bf16 = a.dt == ATTNCACHE_BF16;
     const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
+    const uint64_t kvrows = (uint64_t)a.max_rows * a.L * a.Hkv * a.S;
     CUtensorMap tq, tk, tv, to;
     cudaError_t e = make_tmap_2d_16(&tq, a.Q, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e == cudaSuccess) e = make_tmap_2d_16(&to, a.O, bf16, kD, rows, (uint64_t)kD * 2, 64, 32, 128);
-    if (e == cudaSuccess) e = make_tmap_2d_16(&tk, a.K, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
-    if (e == cudaSuccess) e = make_tmap_2d_16(&tv, a.V, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
+    if (e == cudaSuccess) e = make_tmap_2d_16(&tk, a.K, bf16, kD, kvrows, (uint64_t)kD * 2, 64, kBlk, 128);
+    if (e == cudaSuccess) e = make_tmap_2d_16(&tv, a.V, bf16, kD, kvrows, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(attend_tc_kernel<kD, kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;

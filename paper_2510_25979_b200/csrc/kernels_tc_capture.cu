@@ -123,7 +123,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t lh;
                 int qb;
                 decode(t, row, lh, qb);
-                const int64_t row0 = (row * per_row + lh) * (int64_t)S;  // first Q/K row of the unit
+                const int64_t row0 = (row * per_row + lh) * (int64_t)S;  // first Q row of the unit
+                // first K row: the unit's K head under grouped-query attention (Hkv = H for MHA)
+                const int64_t krow0 = ((row * a.L + lh / (uint32_t)a.H) * a.Hkv + (lh % (uint32_t)a.H) / (uint32_t)(a.H / a.Hkv)) * (int64_t)S;
                 const uint32_t qph = it & 1u;
                 if ((warp & 1) == 0) {
                     mbar_wait(&q_empty[g], qph ^ 1u);
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             mbar_arrive_expect_tx(&k_full[ks], C::kTile);
                             for (int h = 0; h < kD / 64; ++h)
                                 tma_load_2d(smem_u32(sK + ks * C::kTile + h * (kBlk * 128)), &tmK, &k_full[ks],
-                                            h * 64, (int32_t)(row0 + j * kBlk));
+                                            h * 64, (int32_t)(krow0 + j * kBlk));
                         } else {
                             const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
                             mbar_wait(&k_full[ks], kph);
@@ -277,7 +279,8 @@ cudaError_t launch(const CaptureArgs &a, int sm_count, cudaStream_t st) {
     const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
     CUtensorMap tq, tk;
     cudaError_t e = make_tmap_2d_16(&tq, a.Q, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
-    if (e == cudaSuccess) e = make_tmap_2d_16(&tk, a.K, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
+    if (e == cudaSuccess)
+        e = make_tmap_2d_16(&tk, a.K, bf16, kD, (uint64_t)a.max_rows * a.L * a.Hkv * a.S, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(capture_tc_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;

@@ -673,3 +673,64 @@ def test_project_errors(ac, ctx):
     assert L.attncache_project_features(ctx.handle, h.data_ptr(), 4, 196, 2, *args, f.data_ptr(), None) == 4  # pitch
     out = ac.attncache_project_features(ctx, h[:0], W1, b1, W2, b2)
     assert out.shape == (0, cfg.D)
+
+
+# ------------------------------------------------------------------------------------------------
+# grouped-query attention (SURVEY.md §8(f) f3 "optional GQA n_kv_heads"): a query head h reads K/V
+# head h // (H // Hkv).  The expected values repeat the K/V heads on the host (GQA is MHA with shared
+# K/V heads) and use the MHA oracle; the library reads the un-repeated tensors.
+# ------------------------------------------------------------------------------------------------
+
+def _repeat_heads(X, H):
+    """[B][L][Hkv][S][d] -> [B][L][H][S][d] (host-side reference construction)."""
+    return X.repeat_interleave(H // X.shape[2], dim=2).contiguous()
+
+
+@pytest.mark.parametrize("cfg_name,N,B,Hkv,n_sample", [("llama32_1b", 12, 3, 2, 48), ("llama32_1b", 12, 3, 1, 48),
+                                                       ("llama3_8b", 4, 2, 4, 24), ("tiny", 6, 3, 2, None)])
+def test_gqa_apply_attend_capture(ac, ctx, cfg_name, N, B, Hkv, n_sample):
+    base = synth.CONFIGS[cfg_name]
+    cfg = base.with_(N=N, B=B, L=2, H=8 if base.H > 4 else 4)
+    H = cfg.H
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    maps = synth.maps(cfg, 0, cfg.N, DEV)
+    db = ac.Database(ctx, x, maps)
+    g = torch.Generator(device=DEV).manual_seed(11)
+    adt = synth.torch_dtype(cfg.act_dtype)
+    Q = torch.randn(B, cfg.L, H, cfg.S, cfg.d, device=DEV, generator=g).to(adt)
+    K, V = (torch.randn(B, cfg.L, Hkv, cfg.S, cfg.d, device=DEV, generator=g).to(adt) for _ in range(2))
+    idx = torch.randperm(cfg.N, generator=torch.Generator().manual_seed(1))[:B].to(DEV)
+    O_apply = ac.attncache_apply_cached(db, idx, V)
+    O_att = ac.attncache_attend_full(ctx, Q, K, V)
+    torch.cuda.synchronize()
+    assert O_apply.shape == Q.shape and O_att.shape == Q.shape
+    Vr, Kr = _repeat_heads(V, H), _repeat_heads(K, H)
+    units = _units(list(range(B)), cfg.L, H)
+    if n_sample:
+        rng = np.random.default_rng(5)
+        units = [units[i] for i in sorted(rng.choice(len(units), n_sample, replace=False))]
+    ents = idx.cpu().numpy()
+    ref = _apply_ref(storage(maps), cfg.map_dtype, ents, storage(Vr), cfg.act_dtype, units, cfg.L, H, cfg.S, cfg.d)
+    check_close(_gather_units(O_apply, units), ref, adt, f"gqa apply {cfg_name} Hkv={Hkv}")
+    off = [(((b * cfg.L + l) * H + h) * cfg.S * cfg.d) for b, l, h in units]
+    ref = oracle.attend(storage(Q), storage(Kr), storage(Vr), cfg.act_dtype, off, cfg.S, cfg.d)
+    check_close(_gather_units(O_att, units), ref, adt, f"gqa attend {cfg_name} Hkv={Hkv}")
+    # the repeated-head MHA call gives the same bits (the kernels only index differently)
+    assert torch.equal(O_apply, ac.attncache_apply_cached(db, idx, Vr))
+    assert torch.equal(O_att, ac.attncache_attend_full(ctx, Q, Kr, Vr))
+    if cfg.S % 8 == 0 and cfg.map_dtype in ("f16", "bf16"):
+        m1 = ac.attncache_capture_maps(ctx, Q, K, map_dtype=synth.torch_dtype(cfg.map_dtype), packed=False)
+        m2 = ac.attncache_capture_maps(ctx, Q, Kr, map_dtype=synth.torch_dtype(cfg.map_dtype), packed=False)
+        assert torch.equal(m1, m2)
+
+
+def test_gqa_errors(ac, ctx):
+    cfg = synth.CONFIGS["llama32_1b"].with_(N=4, B=2, L=1, H=8)
+    db = ac.Database(ctx, synth.features(cfg, 0, cfg.N, DEV), synth.maps(cfg, 0, cfg.N, DEV))
+    V = torch.zeros(2, 1, 3, cfg.S, cfg.d, device=DEV, dtype=torch.bfloat16)  # 3 does not divide 8
+    with pytest.raises(ac.AttnCacheError) as e:
+        ac.attncache_apply_cached(db, torch.arange(2, device=DEV), V)
+    assert e.value.status == 2
+    Q = torch.zeros(2, 1, 8, cfg.S, cfg.d, device=DEV, dtype=torch.bfloat16)
+    with pytest.raises(ac.AttnCacheError):
+        ac.attncache_attend_full(ctx, Q, V, V)
