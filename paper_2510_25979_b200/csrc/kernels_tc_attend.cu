@@ -384,26 +384,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // use MUFU only.
                 auto exp_pass = [&](auto poly) {
 #pragma unroll
-                    for (int e = 0; e < kBlk / 2; ++e) {
-                        const uint64_t x2 = ffma2(((uint64_t)sv[2 * e + 1] << 32) | sv[2 * e], scale2, neg_m2);
-                        float p0, p1;
-#if defined(ATT_EXP) && ATT_EXP == 2  // experiment: no MUFU
-                        p0 = __uint_as_float((uint32_t)x2) * 0.001f, p1 = __uint_as_float((uint32_t)(x2 >> 32)) * 0.001f;
-#else
-                        if (decltype(poly)::value && (e & 7) < kPolyPairs) {
-                            exp2_poly2(x2, p0, p1);
-                        } else {
-                            p0 = ex2(__uint_as_float((uint32_t)x2));
-                            p1 = ex2(__uint_as_float((uint32_t)(x2 >> 32)));
+                    for (int c = 0; c < kBlk / 32; ++c) {
+                        // diagonal blocks: warp q's rows are < 32(q+1), so its key chunks c > q are all masked:
+                        // P = 0 there without spending MUFU work (a warp-uniform branch)
+                        if (!decltype(poly)::value && c > q) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) sv[c * 16 + i] = 0u;
+                            continue;
                         }
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int e = c * 16 + i;
+                            const uint64_t x2 = ffma2(((uint64_t)sv[2 * e + 1] << 32) | sv[2 * e], scale2, neg_m2);
+                            float p0, p1;
+#if defined(ATT_EXP) && ATT_EXP == 2  // experiment: no MUFU
+                            p0 = __uint_as_float((uint32_t)x2) * 0.001f, p1 = __uint_as_float((uint32_t)(x2 >> 32)) * 0.001f;
+#else
+                            if (decltype(poly)::value && (e & 7) < kPolyPairs) {
+                                exp2_poly2(x2, p0, p1);
+                            } else {
+                                p0 = ex2(__uint_as_float((uint32_t)x2));
+                                p1 = ex2(__uint_as_float((uint32_t)(x2 >> 32)));
+                            }
 #endif
-                        rs2[e & 3] = fadd2(rs2[e & 3], pack2(p0, p1));
-                        if constexpr (kBF16) {
-                            __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                            sv[e] = *reinterpret_cast<uint32_t *>(&h2);
-                        } else {
-                            __half2 h2 = __floats2half2_rn(p0, p1);
-                            sv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                            rs2[e & 3] = fadd2(rs2[e & 3], pack2(p0, p1));
+                            if constexpr (kBF16) {
+                                __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                                sv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                            } else {
+                                __half2 h2 = __floats2half2_rn(p0, p1);
+                                sv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                            }
                         }
                     }
                 };
