@@ -518,14 +518,17 @@ def test_capture_then_reuse_through_the_gpu_path(ac, ctx):
 
 def test_rope_kernel_matches_oracle(ac, ctx):
     """f4 support kernel: RoPE (rotate-half, reading R29) against the oracle.  fp32 angles p*theta
-    carry ~3 ulp relative error, i.e. up to S*3*2^-24 ~ 5e-5 rad at S = 256, times |x| <~ 5."""
-    for dtype, tol in ((torch.float32, 3e-4), (torch.bfloat16, 2e-2)):
-        X = torch.randn(3, 2, 256, 128, device=DEV).to(dtype)
-        ref = oracle.rope(storage(X), DT_NAME[dtype], 256, 128, base=500000.0)
+    carry ~3 ulp relative error, i.e. up to S*3*2^-24 ~ 2e-4 rad at S = 1024, times |x| <~ 5.  Covers the
+    16-byte 16-bit path (d % 16 == 0), the scalar path (fp32; d = 40) and long sequences."""
+    cases = ((torch.float32, 256, 128, 3e-4), (torch.bfloat16, 256, 128, 2e-2), (torch.float16, 1024, 64, 4e-3),
+             (torch.bfloat16, 1024, 128, 2e-2), (torch.bfloat16, 48, 40, 2e-2))
+    for dtype, S, d, tol in cases:
+        X = torch.randn(3, 2, S, d, device=DEV).to(dtype)
+        ref = oracle.rope(storage(X), DT_NAME[dtype], S, d, base=500000.0)
         Y = ac.attncache_rope(X.clone(), 500000.0)
         torch.cuda.synchronize()
         err = np.abs(Y.double().cpu().numpy().reshape(ref.shape) - ref).max()
-        assert err <= tol, (dtype, err)
+        assert err <= tol, (dtype, S, d, err)
 
 
 def test_eq5_block_cached_equals_full_with_captured_maps(ac, ctx):
