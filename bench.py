@@ -454,6 +454,7 @@ def search_sweep(ac, ctx, dev, stream, steps, peaks):
                               "planted_hits": len(pos),
                               "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                               "tensor_frac": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                              "tensor_frac_sustained": flops / (ms * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"],
                               "variant": ac.attncache_variant("search", q.dtype, 0, cfg.D)})
     del db, x
     return out
