@@ -296,6 +296,7 @@ def run_ours(args, cfg):
             "scaling": args.scaling, "vs_baseline": None, "dtype": cfg.act_dtype, "data": "synthetic (synth/, seed 0)",
             "config": {"workload": cfg.name, "bj_config_index": cfg.bj_index, "N": cfg.N, "D": cfg.D, "L": cfg.L,
                        "H": cfg.H, "S": cfg.S, "d": cfg.d, "B": cfg.B, "hits": n_hit, "tau": cfg.tau,
+                       "planted_hit_rate": cfg.hit_rate, "seed": cfg.seed,
                        "parallelism": "single GPU", "l2": "inputs exceed L2 (no flush)"},
             "speedup_vs_full_attention": {"batch": full_ms / ms, "per_hit_kernel": full_hits_ms / apply_ms,
                                           "full_attention_ms": full_ms, "paper_context": PAPER_CONTEXT},
@@ -637,11 +638,19 @@ def main(argv=None):
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="N > 1: the config's global batch split over the GPUs (strong, default) or the config's batch "
                          "on every GPU (weak)")
+    ap.add_argument("--tau", type=float, default=None, help="override the config's threshold (not for bench lines)")
+    ap.add_argument("--hit-rate", type=float, default=None, help="override the config's planted hit rate")
+    ap.add_argument("--batch", type=int, default=None, help="override the config's query batch")
+    ap.add_argument("--seed", type=int, default=None, help="override the config's seed")
     ap.add_argument("--force-dist", action="store_true", help="run the multi-GPU path even at world size 1 (testing)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("bench.py: note: --warmup < 3 does not meet the timing rules (profiling runs only)", file=sys.stderr)
     cfg = synth.CONFIGS[args.config]
+    over = {k: v for k, v in (("tau", args.tau), ("hit_rate", args.hit_rate), ("B", args.batch), ("seed", args.seed))
+            if v is not None}
+    if over:  # SURVEY.md §5 config overrides; the line's config then records them
+        cfg = cfg.with_(**over)
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)

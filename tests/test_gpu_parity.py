@@ -737,3 +737,81 @@ def test_gqa_errors(ac, ctx):
     Q = torch.zeros(2, 1, 8, cfg.S, cfg.d, device=DEV, dtype=torch.bfloat16)
     with pytest.raises(ac.AttnCacheError):
         ac.attncache_attend_full(ctx, Q, V, V)
+
+
+# ------------------------------------------------------------------------------------------------
+# multi-GPU path on one GPU: g virtual shards (one Database per contiguous entry range, SURVEY.md §4
+# "fake multi-shard"), the real per-rank kernels of the routed and the owner-affinity placements, with
+# local copies standing in for the NCCL exchanges; the result must equal the single-shard step bitwise
+# (reading R19).  Ownership is skewed on purpose: all hits on one shard, no hits, hits only off shard 0.
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("pattern", ["spread", "one_shard", "no_hits", "remote_only"])
+def test_virtual_shards_routed_and_affinity_equal_single_gpu(ac, ctx, pattern):
+    from paper_2510_25979_b200.dist import shard_range
+    from paper_2510_25979_b200.pipeline import PrefillStep
+    cfg = synth.CONFIGS["llama32_1b"].with_(N=40, B=12, L=2)
+    world = 3
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    maps = ac.attncache_pack_maps(synth.maps(cfg, 0, cfg.N, DEV))
+    g = torch.Generator(device=DEV).manual_seed(2)
+    tg = torch.Generator().manual_seed(4)
+    if pattern == "spread":
+        tgt = torch.randperm(cfg.N, generator=tg)[:9]
+    elif pattern == "one_shard":
+        tgt = torch.randperm(shard_range(cfg.N, world, 1)[1], generator=tg)[:9] + shard_range(cfg.N, world, 1)[0]
+    elif pattern == "remote_only":
+        tgt = torch.randperm(cfg.N - shard_range(cfg.N, world, 0)[1], generator=tg)[:9] + shard_range(cfg.N, world, 1)[0]
+    else:
+        tgt = torch.tensor([], dtype=torch.int64)
+    q = torch.randn(cfg.B, cfg.D, device=DEV, generator=g)
+    q[:len(tgt)] = x[tgt.to(DEV)].float() + 0.001 * torch.randn(len(tgt), cfg.D, device=DEV, generator=g)
+    q = (q / q.norm(dim=1, keepdim=True)).to(x.dtype)
+    Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qkv")
+    O_ref = torch.empty_like(V)
+    ref = PrefillStep(ctx, ac.Database(ctx, x, maps, packed=True, seq_len=cfg.S), cfg.tau)(q, Q, K, V, O_ref)
+    torch.cuda.synchronize()
+    dbs, begins = [], []
+    for r in range(world):
+        b0, c0 = shard_range(cfg.N, world, r)
+        begins.append(b0)
+        dbs.append(ac.Database(ctx, x[b0:b0 + c0], maps[b0:b0 + c0], n_global=cfg.N, shard_begin=b0, packed=True,
+                               seq_len=cfg.S))
+    # sharded search: every shard's keys over all queries ("all-gather"), decode
+    keys = torch.stack([ac.attncache_search_keys(db, q) for db in dbs])
+    idx, score, hit = ac.attncache_keys_decode(keys, cfg.tau)
+    for a, b in zip(ref, (idx, score, hit)):
+        assert torch.equal(a, b)
+    sb = torch.tensor(begins + [cfg.N], dtype=torch.int64, device=DEV)
+    # routed: bucket the hits by owner, ship V rows, A.V on the owner's shard, scatter O back
+    owner, counts, order = ac.attncache_route_plan(idx, hit, sb)
+    O_routed = torch.empty_like(V)
+    off = 0
+    for r, n in enumerate(counts.tolist()):
+        if n:
+            rows = order[off:off + n].contiguous()
+            V_r = ac.attncache_gather_rows(V, rows)
+            O_r = ac.attncache_apply_cached(dbs[r], ac.attncache_gather_rows(idx, rows), V_r)
+            ac.attncache_scatter_rows(O_r, rows, O_routed)
+        off += n
+    ac.attncache_attend_full(ctx, Q, K, V, O_routed, skip=hit)
+    # owner-affinity: the plan places every query once; each "rank" processes its queries locally
+    assign, load = ac.attncache_affinity_plan(idx, hit, sb, 1.0, 1.3)
+    O_aff = torch.empty_like(V)
+    for r in range(world):
+        loc = torch.nonzero(assign == r).flatten().to(DEV)
+        if not loc.numel():
+            continue
+        V_l, Q_l, K_l = (t.index_select(0, loc).contiguous() for t in (V, Q, K))
+        idx_l, hit_l = idx.index_select(0, loc).contiguous(), hit.index_select(0, loc).contiguous()
+        O_l = torch.empty_like(V_l)
+        ac.attncache_apply_cached(dbs[r], idx_l, V_l, O_l, hit=hit_l)
+        ac.attncache_attend_full(ctx, Q_l, K_l, V_l, O_l, skip=hit_l)
+        O_aff.index_copy_(0, loc, O_l)
+    ctx.sync()
+    assert torch.equal(O_routed, O_ref)
+    assert torch.equal(O_aff, O_ref)
+    if pattern == "no_hits":
+        assert int(hit.sum()) == 0
+    if pattern == "one_shard":
+        assert set(owner[hit.bool()].tolist()) == {1}
