@@ -8,7 +8,7 @@
 // Roles (320 threads):
 //   warps 0-3  map loader: cp.async 16-byte pieces of the lower triangle straight from the DB
 //              (no "attention cache" copy, reading R18); pieces entirely above the diagonal are
-//              zero-filled in shared memory without touching HBM.  Writes the 128B-swizzled
+//              zero-filled in shared memory without touching HBM (normal L2 policy).  Writes the 128B-swizzled
 //              K-major layout tcgen05 reads.
 //   warp 4     V loader: TMA 2-D loads of V rows [64kc, 64kc+64) (128B swizzle, MN-major B).
 //   warp 5     MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128, N=d, K=16, fp32 in TMEM;
@@ -120,7 +120,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tid = threadIdx.x;
         const int c = tid & 7, r0 = tid >> 3;
         const uint32_t soff = (uint32_t)((r0 >> 3) * 1024 + (r0 & 7) * 128 + ((c ^ (r0 & 7)) << 4));
-        const uint64_t policy = policy_evict_first();  // maps are read exactly once
+        // Maps are read once, but a 32-byte sector of a PACKED map can straddle two 16-byte pieces read
+        // in different pipeline stages (rows start at 16-byte multiples): the normal L2 policy keeps it
+        // for the second piece (evict_first measured the same within noise: scripts/apply_experiment.sh).
+#if defined(APPLY_EXP) && APPLY_EXP == 1  // experiment: evict_first for the maps (the previous policy)
+        const uint64_t policy = policy_evict_first();
+#else
+        uint64_t policy;
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(policy));
+#endif
         const __nv_bfloat16 *maps = (const __nv_bfloat16 *)a.maps;  // 16-bit payload (bf16 or f16)
         const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
         uint32_t cnt = 0, pending = 0;
@@ -169,7 +177,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
             // V is re-read by every row block of the unit (S > 128): keep it in L2 (evict_last) while
             // the maps stream through with evict_first.
+#if defined(APPLY_EXP) && APPLY_EXP == 2  // experiment: V with the normal policy
+            uint64_t v_policy;
+            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(v_policy));
+#else
             const uint64_t v_policy = policy_evict_last();
+#endif
             uint32_t lh;
             int64_t row, ent;
             while (iter.next(lh, row, ent)) {
