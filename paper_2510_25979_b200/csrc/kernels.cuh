@@ -65,6 +65,7 @@ struct AttendArgs {
 cudaError_t launch_attend_ffma(const AttendArgs &a, int sm_count, cudaStream_t st);
 bool attend_tc_supported(int32_t dt, int32_t S, int32_t d);
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st);
+cudaError_t launch_attend_split(const AttendArgs &a, int sm_count, cudaStream_t st);  // d = 128, double-buffered S
 
 // ---- capture (DB building: the causal maps of a prefill) ----
 struct CaptureArgs {

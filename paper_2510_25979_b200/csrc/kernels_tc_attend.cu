@@ -532,7 +532,14 @@ cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st)
     // d = 64 uses the same two-group kernel (the earlier two-CTA-per-SM d = 64 kernel with O in registers
     // reached 78 % of the HBM roofline at configs[1]; this one 94 %)
     if (a.d == 64) return a.dt == ATTNCACHE_BF16 ? launch<64, true>(a, sm_count, st) : launch<64, false>(a, sm_count, st);
+    // d = 128: the double-buffered-S, column-split kernel (kernels_tc_attend2.cu; configs[2] 0.63 -> 0.60 ms,
+    // configs[3] 1.51 -> 1.49 ms against this file's two-group kernel, kept for d = 64 and under
+    // ATT_TWO_GROUP128 for comparison)
+#if defined(ATT_TWO_GROUP128)
     return a.dt == ATTNCACHE_BF16 ? launch<128, true>(a, sm_count, st) : launch<128, false>(a, sm_count, st);
+#else
+    return launch_attend_split(a, sm_count, st);
+#endif
 }
 
 }  // namespace ac

@@ -1,0 +1,461 @@
+// kernels_tc_attend2.cu — causal softmax attention, d = 128, with a double-buffered S and a column-split
+// softmax (the miss branch of Alg. 2; Eq. 5):
+//   O = softmax(Q K^T * scale, keys j > i masked) . V.
+//
+// Work item = (unit, 128-query block qb) visiting key blocks j = 0..qb; one item stream per CTA; blocks are
+// numbered b across items.  TMEM (384 of 512 columns): two S/P buffers of 128 columns (S_b in buffer b % 2)
+// and O (128 columns).  P_b is written over the first 64 columns of its S buffer (two bf16 keys per column).
+// The MMA thread issues S_0, S_1, then for every b: PV_b (once the softmax wrote P_b) followed by S_{b+2}
+// into the buffer PV_b just read -- tcgen05.mma ops of one thread execute in issue order, so S_{b+2} is
+// queued behind PV_b -- and the softmax of block b+1 overlaps PV_b and S_{b+2} on the tensor pipe.
+// (kernels_tc_attend.cu keeps one S buffer per group, so a group's next S always waited for its PV.)
+// The softmax runs on 8 warps: warp w handles rows 32(w%4)..+31 (its TMEM lane quarter) and key half
+// w/4 - 1 (64 keys).  The two warps of a row quarter exchange their partial row maxima (and, at the
+// item's end, row sums) through spare TMEM columns behind a 64-thread named barrier, so both use the same
+// reference max; each owns half of P and half of O (rescale, epilogue).  Online softmax with lazy
+// rescaling (the reference max moves only when the block max exceeds it by > 8 in log2 units).
+// Roles (384 threads = 3 warpgroups): warp 0 TMA loader (Q per item into a 2-slot ring, K_b / V_b into
+// 2-slot rings), warp 1 MMA issuer + TMEM owner, warps 2-3 idle; warps 4-7 and 8-11 the softmax /
+// epilogue halves (setmaxnreg moves registers from the producers to the softmax warps).
+#include "kernels.cuh"
+#include "sm100.cuh"
+
+namespace ac {
+using namespace sm100;
+
+namespace {
+
+constexpr int kThreads = 384;
+constexpr int kBlk = 128;
+constexpr int kD = 128;
+constexpr float kRescaleThreshold = 8.f;
+constexpr int kTile = kBlk * kD * 2;    // one [128][128] 16-bit tile (two 64-column swizzle halves)
+constexpr int kOutWarp = 32 * 64 * 2;   // per softmax warp: O staging [32 rows][64 cols]
+constexpr int kSmem = 6 * kTile + 8 * kOutWarp + 1024 + 256;
+// TMEM columns (of 512): S/P buffers [0, 256), O [256, 384), and the pair exchange of partial row maxima
+// (parity-double-buffered, kXmax + 2 * parity + half) and row sums (kXsum + half) at [384, 390): both warps
+// of a row quarter address the same lanes, so TMEM carries the exchange without shared memory.
+constexpr uint32_t kXmax = 384, kXsum = 388;
+constexpr uint32_t kTmemCols = 512;
+// Key pairs (of every 8) whose exp2 runs as a polynomial on the FMA pipe on off-diagonal blocks: 0, the
+// sweep was slower at every ratio (configs[3]: 0 -> 1.49 ms, 1 -> 1.54, 2 -> 1.58, 4 -> 1.69).
+#ifndef SPLIT_POLY
+#define SPLIT_POLY 0
+#endif
+constexpr int kSplitPoly = SPLIT_POLY;
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+// Named barrier over the 64 threads of one row quarter's two softmax warps.
+__device__ __forceinline__ void pair_sync(int q) { asm volatile("bar.sync %0, 64;" ::"r"(q + 1) : "memory"); }
+
+// Item walker shared by all roles: items t = first, first + stride, ...; item -> (unit, qb) in L2-sized
+// unit groups, heaviest query blocks first inside a group (kernels_tc_attend.cu, Stream); j walks the
+// item's key blocks.  row0: first Q/O row of the unit; kv_row0: first K/V row (GQA: K/V head h/(H/Hkv)).
+struct Walker {
+    uint32_t t, stride, items, units, per_row, n_qb, S, group, H, Hkv, L;
+    const int32_t *rows;
+    bool active = false;
+    int64_t row0 = 0, kv_row0 = 0;
+    int qb = 0, j = 0;
+    __device__ void init(uint32_t first, uint32_t stride_, uint32_t items_, uint32_t units_, uint32_t per_row_,
+                         uint32_t n_qb_, uint32_t S_, uint32_t group_, const int32_t *rows_, uint32_t H_,
+                         uint32_t Hkv_) {
+        t = first, stride = stride_, items = items_, units = units_, per_row = per_row_, n_qb = n_qb_, S = S_;
+        group = group_, H = H_, Hkv = Hkv_, L = per_row_ / H_, rows = rows_;
+        start_item();
+    }
+    __device__ void start_item() {
+        active = t < items;
+        if (!active) return;
+        const uint32_t gi = t / (group * n_qb), w = t - gi * (group * n_qb);
+        const uint32_t gbase = gi * group, gsize = min(group, units - gbase);
+        const uint32_t u = gbase + w % gsize;
+        qb = (int)(n_qb - 1 - w / gsize);
+        const int64_t row = rows[u / per_row];
+        const uint32_t lh = u % per_row;
+        row0 = (row * per_row + lh) * S;
+        kv_row0 = ((row * L + lh / H) * Hkv + (lh % H) / (H / Hkv)) * (int64_t)S;
+        j = 0;
+    }
+    // Moves past the current key block; returns true when that block ended the item.
+    __device__ bool advance() {
+        if (++j > qb) {
+            t += stride;
+            start_item();
+            return true;
+        }
+        return false;
+    }
+};
+
+#if defined(ATT_TRACE)  // timeline experiment (scripts/attend_trace.py --split): clock64 stamps of CTA 0
+__device__ unsigned long long g_split_trace_sm[256][6];   // softmax warp 4, lane 0, first 256 blocks
+__device__ unsigned long long g_split_trace_mma[256][6];  // MMA thread, first 256 blocks
+#define SPLIT_TR_SM(slot)                                                                          \
+    do {                                                                                           \
+        if (blockIdx.x == 0 && warp == 4 && lane == 0 && b < 256) g_split_trace_sm[b][slot] = clock64(); \
+    } while (0)
+#define SPLIT_TR_MMA(bb, slot)                                                                     \
+    do {                                                                                           \
+        if (blockIdx.x == 0 && (bb) < 256) g_split_trace_mma[(bb)][slot] = clock64();              \
+    } while (0)
+#else
+#define SPLIT_TR_SM(slot) \
+    do {                  \
+    } while (0)
+#define SPLIT_TR_MMA(bb, slot) \
+    do {                       \
+    } while (0)
+#endif
+
+template <bool kBF16>
+__global__ void __launch_bounds__(kThreads, 1)
+    attend_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                        const AttendArgs a, const uint32_t idesc_s, const uint32_t idesc_pv) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sQ = smem;               // [2][tile]
+    uint8_t *sK = sQ + 2 * kTile;     // [2][tile]
+    uint8_t *sV = sK + 2 * kTile;     // [2][tile]
+    uint8_t *sOut = sV + 2 * kTile;   // [8 softmax warps][kOutWarp]
+    uint64_t *bars = (uint64_t *)(sOut + 8 * kOutWarp);
+    uint64_t *q_full = bars, *q_empty = q_full + 2;
+    uint64_t *k_full = q_empty + 2, *k_empty = k_full + 2;
+    uint64_t *v_full = k_empty + 2, *v_empty = v_full + 2;
+    uint64_t *s_full = v_empty + 2;   // [2] S_b computed in buffer b % 2
+    uint64_t *p_full = s_full + 2;    // [2] P_b written (256 arrivals)
+    uint64_t *pv_done = p_full + 2;   // PV_b retired (one phase per block)
+    uint32_t *tmem_slot = (uint32_t *)(pv_done + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], 1);
+            mbar_init(&k_full[s], 1);
+            mbar_init(&k_empty[s], 1);
+            mbar_init(&v_full[s], 1);
+            mbar_init(&v_empty[s], 1);
+            mbar_init(&s_full[s], 1);
+            mbar_init(&p_full[s], 256);
+        }
+        mbar_init(&pv_done[0], 1);
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmQ);
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+        tma_prefetch_desc(&tmO);
+    }
+    if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const uint32_t S = (uint32_t)a.S;
+    const uint32_t n_qb = S / kBlk;
+    const uint32_t per_row = (uint32_t)(a.L * a.H);
+    const uint32_t units = (uint32_t)(*a.list.count) * per_row;
+    const uint32_t items = units * n_qb;
+    const uint32_t l2_group = max(1u, (48u << 20) / (2u * S * kD * 2u));
+
+    if (warp < 4) {
+        setmaxnreg_dec<56>();
+        if (warp == 0 && lane == 0) {
+            // ------------------------------ TMA loader -------------------------------------------
+            Walker w;
+            w.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+            uint32_t b = 0, it = 0;
+            while (w.active) {
+                if (w.j == 0) {
+                    const uint32_t qs = it & 1u;
+                    mbar_wait(&q_empty[qs], ((it >> 1) & 1u) ^ 1u);
+                    mbar_arrive_expect_tx(&q_full[qs], kTile);
+                    for (int h = 0; h < 2; ++h)
+                        tma_load_2d(smem_u32(sQ + qs * kTile + h * (kBlk * 128)), &tmQ, &q_full[qs], h * 64,
+                                    (int32_t)(w.row0 + w.qb * kBlk));
+                }
+                const uint32_t ks = b & 1u, kph = ((b >> 1) & 1u) ^ 1u;
+                const int32_t r_j = (int32_t)(w.kv_row0 + w.j * kBlk);
+                mbar_wait(&k_empty[ks], kph);
+                mbar_arrive_expect_tx(&k_full[ks], kTile);
+                for (int h = 0; h < 2; ++h)
+                    tma_load_2d(smem_u32(sK + ks * kTile + h * (kBlk * 128)), &tmK, &k_full[ks], h * 64, r_j);
+                mbar_wait(&v_empty[ks], kph);
+                mbar_arrive_expect_tx(&v_full[ks], kTile);
+                for (int h = 0; h < 2; ++h)
+                    tma_load_2d(smem_u32(sV + ks * kTile + h * (kBlk * 128)), &tmV, &v_full[ks], h * 64, r_j);
+                ++b;
+                if (w.advance()) ++it;
+            }
+        } else if (warp == 1 && lane == 0) {
+            // ------------------------------ MMA issuer -------------------------------------------
+            // wS runs two blocks ahead of wP: S_0, S_1, then PV_b followed by S_{b+2}.
+            Walker wS, wP;
+            wS.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+            wP.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+            uint32_t bS = 0, itS = 0, bP = 0;
+            auto issue_s = [&]() {
+                const uint32_t buf = bS & 1u, qs = itS & 1u;
+                if (wS.j == 0) mbar_wait(&q_full[qs], (itS >> 1) & 1u);
+                mbar_wait(&k_full[buf], (bS >> 1) & 1u);
+                tc_fence_after();
+                umma_f16_ss_k8<kBlk * 128 / 16>(tmem + buf * kBlk,
+                                               smem_desc(smem_u32(sQ + qs * kTile), 16, 1024, kSwizzle128B),
+                                               smem_desc(smem_u32(sK + buf * kTile), 16, 1024, kSwizzle128B),
+                                               idesc_s, 0u);
+                umma_commit(&s_full[buf]);
+                umma_commit(&k_empty[buf]);
+                if (wS.j == wS.qb) umma_commit(&q_empty[qs]);
+                ++bS;
+                if (wS.advance()) ++itS;
+            };
+            if (wS.active) issue_s();
+            if (wS.active) issue_s();
+            while (wP.active) {
+                const uint32_t buf = bP & 1u, ph = (bP >> 1) & 1u;
+                SPLIT_TR_MMA(bP, 0);
+                mbar_wait(&p_full[buf], ph);
+                SPLIT_TR_MMA(bP, 1);
+                mbar_wait(&v_full[buf], ph);
+                SPLIT_TR_MMA(bP, 2);
+                tc_fence_after();
+                umma_f16_ts_k8(tmem + 256, tmem + buf * kBlk,
+                               smem_desc(smem_u32(sV + buf * kTile), kBlk * 128, 1024, kSwizzle128B), idesc_pv,
+                               wP.j == 0 ? 0u : 1u);
+                umma_commit(&v_empty[buf]);
+                umma_commit(&pv_done[0]);
+                SPLIT_TR_MMA(bP, 3);
+                ++bP;
+                wP.advance();
+                if (wS.active) issue_s();  // into the buffer PV_b reads: queued behind it
+                SPLIT_TR_MMA(bP - 1, 4);
+            }
+        }
+    } else {
+        // ------------------------------ softmax + epilogue (8 warps) --------------------------------
+        setmaxnreg_inc<224>();
+        const int half = (warp - 4) >> 2;   // key half (64 keys) and O half (64 columns) of this warp
+        const int q = warp & 3;             // TMEM lane quarter
+        const int r = q * 32 + lane;        // query row inside the block == TMEM lane
+        const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+        const uint32_t o_addr = tmem + lane_addr + 256 + half * 64;
+        uint8_t *stage_o = sOut + (warp - 4) * kOutWarp;
+        const uint32_t stage_o_u32 = smem_u32(stage_o);
+        const float sl2 = a.scale * 1.4426950408889634f;
+        Walker w;
+        w.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+        uint32_t b = 0;
+        float m_ref = 0.f, l = 0.f;
+        while (w.active) {
+            const int j = w.j;
+            const bool diag = j == w.qb;
+            const uint32_t buf = b & 1u;
+            const uint32_t s_addr = tmem + lane_addr + buf * kBlk;
+            SPLIT_TR_SM(0);
+            mbar_wait(&s_full[buf], (b >> 1) & 1u);
+            SPLIT_TR_SM(1);
+            tc_fence_after();
+            uint32_t sv[64];  // this warp's 64 keys of its row
+            tmem_ld_32x32b_x64(s_addr + half * 64, sv);
+            tmem_ld_wait();
+            if (diag) {  // keys 64*half + e > r are masked
+#pragma unroll
+                for (int e = 0; e < 64; ++e)
+                    if (half * 64 + e > r) sv[e] = 0xff800000u;  // -inf
+            }
+            float m8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m8[i] = fmaxf(__uint_as_float(sv[i]), __uint_as_float(sv[8 + i]));
+#pragma unroll
+            for (int e = 16; e < 64; e += 16)
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    m8[i] = fmaxf(m8[i], fmaxf(__uint_as_float(sv[e + i]), __uint_as_float(sv[e + 8 + i])));
+            float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+            // the row's max over both key halves, exchanged through TMEM (after the barrier both warps have
+            // read their S columns, so the P writes below cannot clobber S the partner still needs)
+            const uint32_t xcol = tmem + lane_addr + kXmax + 2 * (b & 1u);
+            tmem_st_32x32b_x1(xcol + half, __float_as_uint(mx));
+            tmem_st_wait();
+            tc_fence_before();
+            pair_sync(q);
+            tc_fence_after();
+            mx = fmaxf(mx, __uint_as_float(tmem_ld_32x32b_x1(xcol + (half ^ 1))));
+            tmem_ld_wait();
+            SPLIT_TR_SM(2);
+            const float m_blk = mx * sl2;
+            if (j == 0) {
+                m_ref = m_blk;
+                l = 0.f;
+            } else if (m_blk > m_ref + kRescaleThreshold) {
+                // lazy rescale of this warp's O half (complete once PV_{b-1} retired) and l
+                const float alpha = ex2(m_ref - m_blk);
+                mbar_wait(&pv_done[0], (b - 1) & 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(o_addr + c * 32, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        uint32_t wv[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) wv[e] = __float_as_uint(__uint_as_float(v[h2 * 16 + e]) * alpha);
+                        tmem_st_32x32b_x16(o_addr + c * 32 + h2 * 16, wv);
+                    }
+                }
+                l *= alpha;
+                m_ref = m_blk;
+            }
+            // p = exp2(s * scale * log2e - m_ref), rounded to the MMA dtype, keys 64*half.. -> P columns
+            // 32*half..; l sums the unrounded p (an unbiased estimate of the rounded sum)
+            {
+                const uint64_t scale2 = pack2(sl2, sl2), neg_m2 = pack2(-m_ref, -m_ref);
+                uint64_t rs2[4] = {0ull, 0ull, 0ull, 0ull};
+                // off-diagonal blocks may compute kSplitPoly of every 8 key pairs with the FMA-pipe
+                // polynomial (exp2_poly2; masked -inf keys only occur on diagonal blocks, which stay on MUFU)
+                const bool poly_ok = !diag;
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    const uint64_t x2 = ffma2(((uint64_t)sv[2 * e + 1] << 32) | sv[2 * e], scale2, neg_m2);
+                    float p0, p1;
+                    if ((e & 7) < kSplitPoly && poly_ok) {
+                        exp2_poly2(x2, p0, p1);
+                    } else {
+                        p0 = ex2(__uint_as_float((uint32_t)x2));
+                        p1 = ex2(__uint_as_float((uint32_t)(x2 >> 32)));
+                    }
+                    rs2[e & 3] = fadd2(rs2[e & 3], pack2(p0, p1));
+                    if constexpr (kBF16) {
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                        sv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                    } else {
+                        __half2 h2 = __floats2half2_rn(p0, p1);
+                        sv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t wv[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) wv[e] = sv[c * 16 + e];
+                    tmem_st_32x32b_x16(s_addr + half * 32 + c * 16, wv);
+                }
+                const uint64_t t2 = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
+                l += __uint_as_float((uint32_t)t2) + __uint_as_float((uint32_t)(t2 >> 32));
+            }
+            tmem_st_wait();
+            SPLIT_TR_SM(3);
+            tc_fence_before();
+            mbar_arrive(&p_full[buf]);
+            SPLIT_TR_SM(4);
+            if (diag) {
+                // epilogue: the item's last PV retired -> O / (l_0 + l_1) -> act dtype -> this warp's
+                // 128B-swizzled staging tile -> TMA store of its 32 rows x 64 columns
+                tmem_st_32x32b_x1(tmem + lane_addr + kXsum + half, __float_as_uint(l));
+                tmem_st_wait();
+                tc_fence_before();
+                // PV_b retired.  s_full(b) only implied PV_{b-2}: wait for PV_{b-1} first so the parity wait
+                // on PV_b cannot be satisfied by a phase two behind (a race the bitwise-repeat test caught)
+                if (b > 0) mbar_wait(&pv_done[0], (b - 1) & 1u);
+                mbar_wait(&pv_done[0], b & 1u);
+                pair_sync(q);
+                tc_fence_after();
+                const float inv = 1.f / (l + __uint_as_float(tmem_ld_32x32b_x1(tmem + lane_addr + kXsum + (half ^ 1))));
+                uint32_t v[64];
+                tmem_ld_32x32b_x32(o_addr, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                tmem_ld_32x32b_x32(o_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+                tmem_ld_wait();
+                if (lane == 0) bulk_wait_read<0>();  // the previous TMA store has read the staging tile
+                __syncwarp();
+#pragma unroll
+                for (int c8 = 0; c8 < 8; ++c8) {
+                    uint32_t wv[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float lo = __uint_as_float(v[c8 * 8 + 2 * e]) * inv;
+                        const float hi = __uint_as_float(v[c8 * 8 + 2 * e + 1]) * inv;
+                        if constexpr (kBF16) {
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
+                            wv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        } else {
+                            __half2 h2 = __floats2half2_rn(lo, hi);
+                            wv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        }
+                    }
+                    *reinterpret_cast<uint4 *>(stage_o + sw128_offset(lane, c8)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tmO, stage_o_u32, half * 64, (int32_t)(w.row0 + w.qb * kBlk + q * 32));
+                    bulk_commit();
+                }
+                // the partner reads this warp's row sum before the next item's epilogue rewrites it: the
+                // exchange barriers of the blocks in between order the two
+                tc_fence_before();
+            }
+            ++b;
+            w.advance();
+        }
+        if (lane == 0) bulk_wait<0>();  // O stores complete before the CTA (and its smem) retires
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<kTmemCols>(tmem);
+    }
+}
+
+template <bool kBF16>
+cudaError_t launch_t(const AttendArgs &a, int sm_count, cudaStream_t st) {
+    const bool bf16 = kBF16;
+    const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
+    const uint64_t kvrows = (uint64_t)a.max_rows * a.L * a.Hkv * a.S;
+    CUtensorMap tq, tk, tv, to;
+    cudaError_t e = make_tmap_2d_16(&tq, a.Q, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
+    if (e == cudaSuccess) e = make_tmap_2d_16(&to, a.O, bf16, kD, rows, (uint64_t)kD * 2, 64, 32, 128);
+    if (e == cudaSuccess) e = make_tmap_2d_16(&tk, a.K, bf16, kD, kvrows, (uint64_t)kD * 2, 64, kBlk, 128);
+    if (e == cudaSuccess) e = make_tmap_2d_16(&tv, a.V, bf16, kD, kvrows, (uint64_t)kD * 2, 64, kBlk, 128);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attend_split_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    const uint32_t fmt = bf16 ? 1u : 0u;
+    const uint32_t idesc_s = idesc_f16(kBlk, kBlk, fmt, 0u, 0u);  // Q K-major x K K-major
+    const uint32_t idesc_pv = idesc_f16(kBlk, kD, fmt, 0u, 1u);   // P (TMEM) x V MN-major
+    attend_split_kernel<kBF16><<<sm_count, kThreads, kSmem, st>>>(tq, tk, tv, to, a, idesc_s, idesc_pv);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_attend_split(const AttendArgs &a, int sm_count, cudaStream_t st) {
+    return a.dt == ATTNCACHE_BF16 ? launch_t<true>(a, sm_count, st) : launch_t<false>(a, sm_count, st);
+}
+
+}  // namespace ac
+#if defined(ATT_TRACE)
+extern "C" int attncache_debug_split_trace(void *sm, void *mma) {
+    cudaError_t e = cudaMemcpyFromSymbol(sm, ac::g_split_trace_sm, sizeof(ac::g_split_trace_sm));
+    if (e == cudaSuccess) e = cudaMemcpyFromSymbol(mma, ac::g_split_trace_mma, sizeof(ac::g_split_trace_mma));
+    return (int)e;
+}
+#endif

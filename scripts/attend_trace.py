@@ -1,4 +1,5 @@
-"""Timeline of the d=128 attention softmax (CTA 0, group 0 = warp 4 and group 1 = warp 8, lane 0): builds
+"""Timeline of the d=128 attention (--split: the default column-split kernel, softmax warp 4 and the MMA thread;
+otherwise the two-group kernel, CTA 0, group 0 = warp 4 and group 1 = warp 8, lane 0): builds
 the library with -DATT_TRACE out of tree, runs configs[3]'s misses once and prints per-block phase
 durations in cycles: wait for S, TMEM load of S, row max, exp + P store, arrive, and the gap to the next."""
 import ctypes
@@ -11,11 +12,15 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-env = dict(os.environ, ATTNCACHE_BUILD_ROOT="/tmp/atttrace", ATTNCACHE_EXTRA_FLAGS="-DATT_TRACE")
+SPLIT = "--split" in sys.argv
+if SPLIT:
+    sys.argv.remove("--split")
+env = dict(os.environ, ATTNCACHE_BUILD_ROOT="/tmp/atttrace" + ("s" if SPLIT else ""),
+           ATTNCACHE_EXTRA_FLAGS="-DATT_TRACE" + ("" if SPLIT else " -DATT_TWO_GROUP128"))
 subprocess.check_call([sys.executable, "-m", "paper_2510_25979_b200.build"], env=env, cwd=ROOT, stdout=subprocess.DEVNULL)
 import synth  # noqa: E402
 import paper_2510_25979_b200 as ac  # noqa: E402
-ac.lib_path = "/tmp/atttrace/lib/libattncache.so"
+ac.lib_path = "/tmp/atttrace" + ("s" if SPLIT else "") + "/lib/libattncache.so"
 name = sys.argv[1] if len(sys.argv) > 1 else "long_prefill"
 cfg = synth.CONFIGS[name]
 rows = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.B - cfg.n_hit
@@ -27,8 +32,23 @@ O = ac.attncache_attend_full(ctx, Q, K, V)
 torch.cuda.synchronize()
 ac.attncache_attend_full(ctx, Q, K, V, O)
 torch.cuda.synchronize()
-buf = np.zeros((2, 256, 6), dtype=np.uint64)
 lib = ac.load_library()
+if SPLIT:
+    sm = np.zeros((256, 6), dtype=np.uint64)
+    mm = np.zeros((256, 6), dtype=np.uint64)
+    assert lib.attncache_debug_split_trace(ctypes.c_void_p(sm.ctypes.data), ctypes.c_void_p(mm.ctypes.data)) == 0
+    t, m = sm.astype(np.int64), mm.astype(np.int64)
+    d = np.diff(t[:, :5], axis=1)
+    per = t[1:, 0] - t[:-1, 0]
+    sel = slice(20, 200)
+    print(f"softmax warp 4: median cycles wait_S {np.median(d[sel, 0]):.0f}  load+exchange {np.median(d[sel, 1]):.0f}  "
+          f"exp+store {np.median(d[sel, 2]):.0f}  arrive {np.median(d[sel, 3]):.0f}  period {np.median(per[sel]):.0f}")
+    dm = np.diff(m[:, :5], axis=1)
+    perm = m[1:, 0] - m[:-1, 0]
+    print(f"MMA: median cycles wait_P {np.median(dm[sel, 0]):.0f}  wait_V {np.median(dm[sel, 1]):.0f}  PV issue "
+          f"{np.median(dm[sel, 2]):.0f}  S issue {np.median(dm[sel, 3]):.0f}  period {np.median(perm[sel]):.0f}")
+    sys.exit(0)
+buf = np.zeros((2, 256, 6), dtype=np.uint64)
 assert lib.attncache_debug_att_trace(ctypes.c_void_p(buf.ctypes.data)) == 0
 t = buf.astype(np.int64)
 for grp in range(2):

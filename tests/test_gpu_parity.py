@@ -451,8 +451,9 @@ def test_host_prefill_pipeline_matches_device_step(ac, ctx):
 def test_repeat_runs_are_bitwise_identical(ac, ctx):
     """racecheck does not see the async proxy (TMA/tcgen05), so every tensor-core
     kernel is re-run on identical inputs and must reproduce its output bit for bit."""
-    for name in ("llama32_1b", "llama3_8b"):
-        cfg = synth.CONFIGS[name].with_(N=24, B=10, L=2)
+    for name, over in (("llama32_1b", dict(N=24, B=10, L=2)), ("llama3_8b", dict(N=24, B=10, L=2)),
+                       ("long_prefill", dict(N=4, B=3, L=1))):
+        cfg = synth.CONFIGS[name].with_(**over)
         x = synth.features(cfg, 0, cfg.N, DEV)
         maps = ac.attncache_pack_maps(synth.maps(cfg, 0, cfg.N, DEV))
         db = ac.Database(ctx, x, maps, packed=True, seq_len=cfg.S)
