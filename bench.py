@@ -304,6 +304,8 @@ def run_ours(args, cfg):
             "stages": secondary, "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
     # §8(f) f1, DB building: capture the misses' maps (Q, K -> packed bf16 DB entries)
     secondary["capture_misses"] = capture_stage(ac, ctx, cfg, Q, K, hit, stream, max(3, args.steps), peaks)
+    # small batches (a serving request at a time): per-step time eager vs one CUDA-graph replay
+    secondary["small_batch"] = small_batch_stage(ac, ctx, db, cfg, q, Q, K, V, stream)
     # §8(f) f2: the feature projector (Alg. 1 l.254) on this batch and at a tensor-bound batch
     secondary["project"] = project_stage(ac, ctx, cfg, dev, stream, max(3, args.steps), peaks)
     # paper-comparable baseline: eager torch attention (matmul -> masked softmax -> matmul, the
@@ -344,6 +346,37 @@ def capture_stage(ac, ctx, cfg, Q, K, hit, stream, steps, peaks):
     del out
     return {"ms": ms, "bytes": nbytes, "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
             "variant": ac.attncache_variant("capture", Q.dtype, cfg.S, cfg.d)}
+
+
+def small_batch_stage(ac, ctx, db, cfg, q, Q, K, V, stream, iters=50):
+    """Latency-bound batches of B = 1 and 8 prefills (the first rows of the batch): the whole step issued
+    eagerly (six library launches plus host-side checks per step) vs replayed as one CUDA graph
+    (pipeline.GraphedPrefillStep)."""
+    from paper_2510_25979_b200.pipeline import GraphedPrefillStep, PrefillStep
+    step = PrefillStep(ctx, db, cfg.tau)
+    out = []
+    for B in (1, 8):
+        qb, Qb, Kb, Vb = (t[:B].contiguous() for t in (q, Q, K, V))
+        Ob = torch.empty_like(Vb)
+        g = GraphedPrefillStep(step, qb, Qb, Kb, Vb)
+
+        def timed(fn):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(iters):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / iters
+
+        eager = timed(lambda: step(qb, Qb, Kb, Vb, Ob))
+        graph = timed(g.replay)
+        out.append({"B": B, "eager_ms": eager, "graph_ms": graph, "graph_tokens_per_s": B * cfg.S / (graph * 1e-3)})
+        del g
+    return out
 
 
 def project_stage(ac, ctx, cfg, dev, stream, steps, peaks):

@@ -816,3 +816,33 @@ def test_virtual_shards_routed_and_affinity_equal_single_gpu(ac, ctx, pattern):
         assert int(hit.sum()) == 0
     if pattern == "one_shard":
         assert set(owner[hit.bool()].tolist()) == {1}
+
+
+def test_graphed_prefill_step_equals_eager(ac, ctx):
+    """pipeline.GraphedPrefillStep: the captured step replays to the eager step's bits, and a replay after
+    new inputs are written into its static buffers gives the eager result for those inputs."""
+    from paper_2510_25979_b200.pipeline import GraphedPrefillStep, PrefillStep
+    cfg = synth.CONFIGS["llama32_1b"].with_(N=64, B=8, L=2)
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    db = ac.Database(ctx, x, ac.attncache_pack_maps(synth.maps(cfg, 0, cfg.N, DEV)), packed=True, seq_len=cfg.S)
+    step = PrefillStep(ctx, db, cfg.tau)
+    q, _, _ = synth.queries(cfg, DEV)
+    Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qkv")
+    gstep = GraphedPrefillStep(step, q, Q, K, V)
+    O_e = torch.empty_like(V)
+    ref = tuple(t.clone() for t in step(q, Q, K, V, O_e))
+    out = gstep.replay()
+    torch.cuda.synchronize()
+    for a, b in zip((*ref, O_e), out):
+        assert torch.equal(a, b)
+    # new inputs: a different query batch (other hit pattern) and other activations
+    q2, _, _ = synth.queries(cfg.with_(seed=5), DEV)
+    Q2, K2, V2 = (synth.activations(cfg.with_(seed=5), k, 0, cfg.B, device=DEV) for k in "qkv")
+    for dst, src in zip(gstep.inputs, (q2, Q2, K2, V2)):
+        dst.copy_(src)
+    out = tuple(t.clone() for t in gstep.replay())
+    O_e2 = torch.empty_like(V)
+    ref2 = step(q2, Q2, K2, V2, O_e2)
+    torch.cuda.synchronize()
+    for a, b in zip((*ref2, O_e2), out):
+        assert torch.equal(a, b)
