@@ -15,7 +15,8 @@
 // reference max; each owns half of P and half of O (rescale, epilogue).  Online softmax with lazy
 // rescaling (the reference max moves only when the block max exceeds it by > 8 in log2 units).
 // Roles (384 threads = 3 warpgroups): warp 0 TMA loader (Q per item into a 2-slot ring, K_b / V_b into
-// 2-slot rings), warp 1 MMA issuer + TMEM owner, warps 2-3 idle; warps 4-7 and 8-11 the softmax /
+// 2-slot rings), warp 1 MMA issuer (the whole warp runs the issue loop, one elected lane issues, so the
+// descriptor arithmetic stays in uniform registers) + TMEM owner, warps 2-3 idle; warps 4-7 and 8-11 the softmax /
 // epilogue halves (setmaxnreg moves registers from the producers to the softmax warps).
 #include "kernels.cuh"
 #include "sm100.cuh"
@@ -31,7 +32,14 @@ constexpr int kD = 128;
 constexpr float kRescaleThreshold = 8.f;
 constexpr int kTile = kBlk * kD * 2;    // one [128][128] 16-bit tile (two 64-column swizzle halves)
 constexpr int kOutWarp = 32 * 64 * 2;   // per softmax warp: O staging [32 rows][64 cols]
-constexpr int kSmem = 6 * kTile + 8 * kOutWarp + 1024 + 256;
+// Rings: Q 2 slots (one item ahead), K kNK slots, V kNV slots (shared memory holds 6 tiles next to the O staging;
+// K 3 / V 1 measured 45 % slower than 2 / 2: a one-slot V ring serializes PV with the next V load).
+#ifndef SPLIT_NK
+#define SPLIT_NK 2
+#endif
+constexpr int kNK = SPLIT_NK, kNV = 4 - SPLIT_NK;
+static_assert(kNK >= 1 && kNV >= 1 && kNK <= 4 && kNV <= 4, "ring sizes");
+constexpr int kSmem = (2 + kNK + kNV) * kTile + 8 * kOutWarp + 1024 + 256;
 // TMEM columns (of 512): S/P buffers [0, 256), O [256, 384), and the pair exchange of partial row maxima
 // (parity-double-buffered, kXmax + 2 * parity + half) and row sums (kXsum + half) at [384, 390): both warps
 // of a row quarter address the same lanes, so TMEM carries the exchange without shared memory.
@@ -128,29 +136,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sQ = smem;               // [2][tile]
-    uint8_t *sK = sQ + 2 * kTile;     // [2][tile]
-    uint8_t *sV = sK + 2 * kTile;     // [2][tile]
-    uint8_t *sOut = sV + 2 * kTile;   // [8 softmax warps][kOutWarp]
+    uint8_t *sK = sQ + 2 * kTile;     // [kNK][tile]
+    uint8_t *sV = sK + kNK * kTile;   // [kNV][tile]
+    uint8_t *sOut = sV + kNV * kTile; // [8 softmax warps][kOutWarp]
     uint64_t *bars = (uint64_t *)(sOut + 8 * kOutWarp);
     uint64_t *q_full = bars, *q_empty = q_full + 2;
-    uint64_t *k_full = q_empty + 2, *k_empty = k_full + 2;
-    uint64_t *v_full = k_empty + 2, *v_empty = v_full + 2;
-    uint64_t *s_full = v_empty + 2;   // [2] S_b computed in buffer b % 2
+    uint64_t *k_full = q_empty + 2, *k_empty = k_full + kNK;
+    uint64_t *v_full = k_empty + kNK, *v_empty = v_full + kNV;
+    uint64_t *s_full = v_empty + kNV;  // [2] S_b computed in buffer b % 2
     uint64_t *p_full = s_full + 2;    // [2] P_b written (256 arrivals)
     uint64_t *pv_done = p_full + 2;   // PV_b retired (one phase per block)
     uint32_t *tmem_slot = (uint32_t *)(pv_done + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&q_full[s], 1);
-            mbar_init(&q_empty[s], 1);
-            mbar_init(&k_full[s], 1);
-            mbar_init(&k_empty[s], 1);
-            mbar_init(&v_full[s], 1);
-            mbar_init(&v_empty[s], 1);
-            mbar_init(&s_full[s], 1);
-            mbar_init(&p_full[s], 256);
+        for (int s = 0; s < 4; ++s) {
+            if (s < 2) {
+                mbar_init(&q_full[s], 1);
+                mbar_init(&q_empty[s], 1);
+                mbar_init(&s_full[s], 1);
+                mbar_init(&p_full[s], 256);
+            }
+            if (s < kNK) {
+                mbar_init(&k_full[s], 1);
+                mbar_init(&k_empty[s], 1);
+            }
+            if (s < kNV) {
+                mbar_init(&v_full[s], 1);
+                mbar_init(&v_empty[s], 1);
+            }
         }
         mbar_init(&pv_done[0], 1);
         fence_barrier_init();
@@ -190,19 +204,68 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tma_load_2d(smem_u32(sQ + qs * kTile + h * (kBlk * 128)), &tmQ, &q_full[qs], h * 64,
                                     (int32_t)(w.row0 + w.qb * kBlk));
                 }
-                const uint32_t ks = b & 1u, kph = ((b >> 1) & 1u) ^ 1u;
                 const int32_t r_j = (int32_t)(w.kv_row0 + w.j * kBlk);
-                mbar_wait(&k_empty[ks], kph);
-                mbar_arrive_expect_tx(&k_full[ks], kTile);
+                const uint32_t kk = b % kNK, kkph = ((b / kNK) & 1u) ^ 1u;
+                const uint32_t vv = b % kNV, vvph = ((b / kNV) & 1u) ^ 1u;
+                mbar_wait(&k_empty[kk], kkph);
+                mbar_arrive_expect_tx(&k_full[kk], kTile);
                 for (int h = 0; h < 2; ++h)
-                    tma_load_2d(smem_u32(sK + ks * kTile + h * (kBlk * 128)), &tmK, &k_full[ks], h * 64, r_j);
-                mbar_wait(&v_empty[ks], kph);
-                mbar_arrive_expect_tx(&v_full[ks], kTile);
+                    tma_load_2d(smem_u32(sK + kk * kTile + h * (kBlk * 128)), &tmK, &k_full[kk], h * 64, r_j);
+                mbar_wait(&v_empty[vv], vvph);
+                mbar_arrive_expect_tx(&v_full[vv], kTile);
                 for (int h = 0; h < 2; ++h)
-                    tma_load_2d(smem_u32(sV + ks * kTile + h * (kBlk * 128)), &tmV, &v_full[ks], h * 64, r_j);
+                    tma_load_2d(smem_u32(sV + vv * kTile + h * (kBlk * 128)), &tmV, &v_full[vv], h * 64, r_j);
                 ++b;
                 if (w.advance()) ++it;
             }
+#if !defined(SPLIT_LANE_MMA)  // default: warp-converged MMA issuer (descriptors in uniform registers; -DSPLIT_LANE_MMA
+                              // selects the single-lane issuer, ~0.7 % slower at configs[3])
+        } else if (warp == 1) {
+            // ------------------------------ MMA issuer (whole warp; one elected lane issues) --------
+            // wS runs two blocks ahead of wP: S_0, S_1, then PV_b followed by S_{b+2}.
+            Walker wS, wP;
+            wS.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+            wP.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+            uint32_t bS = 0, itS = 0, bP = 0;
+            auto issue_s = [&]() {
+                const uint32_t buf = bS & 1u, qs = itS & 1u;
+                if (wS.j == 0) mbar_wait(&q_full[qs], (itS >> 1) & 1u);
+                mbar_wait(&k_full[bS % kNK], (bS / kNK) & 1u);
+                SPLIT_TR_MMA(bS, 5);  // K (and Q) of S_{bS} ready
+                tc_fence_after();
+                umma_f16_ss_k8_w<kBlk * 128 / 16>(tmem + buf * kBlk,
+                                               smem_desc(smem_u32(sQ + qs * kTile), 16, 1024, kSwizzle128B),
+                                               smem_desc(smem_u32(sK + (bS % kNK) * kTile), 16, 1024, kSwizzle128B),
+                                               idesc_s, 0u);
+                umma_commit_w(&s_full[buf]);
+                umma_commit_w(&k_empty[bS % kNK]);
+                if (wS.j == wS.qb) umma_commit_w(&q_empty[qs]);
+                ++bS;
+                if (wS.advance()) ++itS;
+            };
+            if (wS.active) issue_s();
+            if (wS.active) issue_s();
+            while (wP.active) {
+                const uint32_t buf = bP & 1u, ph = (bP >> 1) & 1u;
+                SPLIT_TR_MMA(bP, 0);
+                mbar_wait(&p_full[buf], ph);
+                SPLIT_TR_MMA(bP, 1);
+                mbar_wait(&v_full[bP % kNV], (bP / kNV) & 1u);
+                SPLIT_TR_MMA(bP, 2);
+                tc_fence_after();
+                umma_f16_ts_k8_w(tmem + 256, tmem + buf * kBlk,
+                               smem_desc(smem_u32(sV + (bP % kNV) * kTile), kBlk * 128, 1024, kSwizzle128B), idesc_pv,
+                               wP.j == 0 ? 0u : 1u);
+                umma_commit_w(&v_empty[bP % kNV]);
+                umma_commit_w(&pv_done[0]);
+                SPLIT_TR_MMA(bP, 3);
+                ++bP;
+                wP.advance();
+                if (wS.active) issue_s();  // into the buffer PV_b reads: queued behind it
+                SPLIT_TR_MMA(bP - 1, 4);
+            }
+        }
+#else
         } else if (warp == 1 && lane == 0) {
             // ------------------------------ MMA issuer -------------------------------------------
             // wS runs two blocks ahead of wP: S_0, S_1, then PV_b followed by S_{b+2}.
@@ -213,14 +276,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             auto issue_s = [&]() {
                 const uint32_t buf = bS & 1u, qs = itS & 1u;
                 if (wS.j == 0) mbar_wait(&q_full[qs], (itS >> 1) & 1u);
-                mbar_wait(&k_full[buf], (bS >> 1) & 1u);
+                mbar_wait(&k_full[bS % kNK], (bS / kNK) & 1u);
+                SPLIT_TR_MMA(bS, 5);  // K (and Q) of S_{bS} ready
                 tc_fence_after();
                 umma_f16_ss_k8<kBlk * 128 / 16>(tmem + buf * kBlk,
                                                smem_desc(smem_u32(sQ + qs * kTile), 16, 1024, kSwizzle128B),
-                                               smem_desc(smem_u32(sK + buf * kTile), 16, 1024, kSwizzle128B),
+                                               smem_desc(smem_u32(sK + (bS % kNK) * kTile), 16, 1024, kSwizzle128B),
                                                idesc_s, 0u);
                 umma_commit(&s_full[buf]);
-                umma_commit(&k_empty[buf]);
+                umma_commit(&k_empty[bS % kNK]);
                 if (wS.j == wS.qb) umma_commit(&q_empty[qs]);
                 ++bS;
                 if (wS.advance()) ++itS;
@@ -232,13 +296,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 SPLIT_TR_MMA(bP, 0);
                 mbar_wait(&p_full[buf], ph);
                 SPLIT_TR_MMA(bP, 1);
-                mbar_wait(&v_full[buf], ph);
+                mbar_wait(&v_full[bP % kNV], (bP / kNV) & 1u);
                 SPLIT_TR_MMA(bP, 2);
                 tc_fence_after();
                 umma_f16_ts_k8(tmem + 256, tmem + buf * kBlk,
-                               smem_desc(smem_u32(sV + buf * kTile), kBlk * 128, 1024, kSwizzle128B), idesc_pv,
+                               smem_desc(smem_u32(sV + (bP % kNV) * kTile), kBlk * 128, 1024, kSwizzle128B), idesc_pv,
                                wP.j == 0 ? 0u : 1u);
-                umma_commit(&v_empty[buf]);
+                umma_commit(&v_empty[bP % kNV]);
                 umma_commit(&pv_done[0]);
                 SPLIT_TR_MMA(bP, 3);
                 ++bP;
@@ -247,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 SPLIT_TR_MMA(bP - 1, 4);
             }
         }
+#endif
     } else {
         // ------------------------------ softmax + epilogue (8 warps) --------------------------------
         setmaxnreg_inc<224>();

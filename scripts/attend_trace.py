@@ -16,7 +16,7 @@ SPLIT = "--split" in sys.argv
 if SPLIT:
     sys.argv.remove("--split")
 env = dict(os.environ, ATTNCACHE_BUILD_ROOT="/tmp/atttrace" + ("s" if SPLIT else ""),
-           ATTNCACHE_EXTRA_FLAGS="-DATT_TRACE" + ("" if SPLIT else " -DATT_TWO_GROUP128"))
+           ATTNCACHE_EXTRA_FLAGS="-DATT_TRACE " + os.environ.get("TRACE_FLAGS", "") + ("" if SPLIT else " -DATT_TWO_GROUP128"))
 subprocess.check_call([sys.executable, "-m", "paper_2510_25979_b200.build"], env=env, cwd=ROOT, stdout=subprocess.DEVNULL)
 import synth  # noqa: E402
 import paper_2510_25979_b200 as ac  # noqa: E402
@@ -47,6 +47,10 @@ if SPLIT:
     perm = m[1:, 0] - m[:-1, 0]
     print(f"MMA: median cycles wait_P {np.median(dm[sel, 0]):.0f}  wait_V {np.median(dm[sel, 1]):.0f}  PV issue "
           f"{np.median(dm[sel, 2]):.0f}  S issue {np.median(dm[sel, 3]):.0f}  period {np.median(perm[sel]):.0f}")
+    # slot 5 of block b: K_b ready inside the issue of S_b (which follows PV_{b-2}, slot 3 of b-2)
+    kw = m[22:200, 5] - m[20:198, 3]
+    print(f"MMA: median cycles from PV_(b-2) issued to K_b ready {np.median(kw):.0f}; S_b issue after K ready "
+          f"{np.median(m[22:200, 4 - 4 + 4] * 0 + (m[20:198, 4] - m[22:200, 5])):.0f}")
     sys.exit(0)
 buf = np.zeros((2, 256, 6), dtype=np.uint64)
 assert lib.attncache_debug_att_trace(ctypes.c_void_p(buf.ctypes.data)) == 0
