@@ -222,7 +222,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t q_s = smem_u32(sQ + g * C::kTile), k_s = smem_u32(sK + g * C::kTile);
                 const uint32_t v_s = smem_u32(sV + g * C::kTile);
                 while (st.active) {
-#if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
                     const int32_t r_j = (int32_t)(st.kv_row0 + st.j * kBlk);
                     if (st.j == 0) {
                         mbar_wait(&q_empty[g], (it & 1u) ^ 1u);
@@ -236,7 +235,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&v_empty[g], (b & 1u) ^ 1u);
                     mbar_arrive_expect_tx(&v_full[g], C::kTile);
                     for (int h = 0; h < kD / 64; ++h) tma_load_2d(v_s + h * (kBlk * 128), &tmV, &v_full[g], h * 64, r_j);
-#endif
                     ++b;
                     if (st.advance()) ++it;
                 }
@@ -250,10 +248,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 while (st.active) {
                     const int j = st.j;
                     ATT_TRACE_MMA(b * 2 + g, 0);
-#if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
                     if (j == 0) mbar_wait(&q_full[g], it & 1u);
                     mbar_wait(&k_full[g], b & 1u);
-#endif
                     ATT_TRACE_MMA(b * 2 + g, 1);
                     tc_fence_after();
                     if constexpr (kD == 128) {  // 8 K-steps of 16 over two 64-column swizzle halves
@@ -271,9 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ATT_TRACE_MMA(b * 2 + g, 2);
                     mbar_wait(&p_full[g], b & 1u);
                     ATT_TRACE_MMA(b * 2 + g, 4);
-#if !(defined(ATT_EXP) && (ATT_EXP == 3 || ATT_EXP == 4 || ATT_EXP == 5))
                     mbar_wait(&v_full[g], b & 1u);
-#endif
                     ATT_TRACE_MMA(b * 2 + g, 5);
                     tc_fence_after();
                     // A = P (8 TMEM columns = 16 keys per step), B = V MN-major: 8 steps in one statement
@@ -313,19 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // The whole S row (128 keys) is loaded from TMEM once (two back-to-back loads, one wait) and
             // kept in registers for the max and the exponentials.  Diagonal blocks set keys k > r to -inf,
             // which the exponential turns into an exact 0.
-#if defined(ATT_EXP) && (ATT_EXP == 1 || ATT_EXP == 4 || ATT_EXP == 5)  // experiment: no softmax math
             {
-                uint32_t w[16];
-#pragma unroll
-                for (int e = 0; e < 16; ++e) w[e] = 0u;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_st_32x32b_x16(s_addr + c * 16, w);
-                l = 1.f;
-            }
-            if (false) {
-#else
-            {
-#endif
             uint32_t sv[kBlk];
             tmem_ld_32x32b_x64(s_addr, sv);
             tmem_ld_32x32b_x64(s_addr + 64, sv + 64);
@@ -397,16 +379,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int e = c * 16 + i;
                             const uint64_t x2 = ffma2(((uint64_t)sv[2 * e + 1] << 32) | sv[2 * e], scale2, neg_m2);
                             float p0, p1;
-#if defined(ATT_EXP) && ATT_EXP == 2  // experiment: no MUFU
-                            p0 = __uint_as_float((uint32_t)x2) * 0.001f, p1 = __uint_as_float((uint32_t)(x2 >> 32)) * 0.001f;
-#else
                             if (decltype(poly)::value && (e & 7) < kPolyPairs) {
                                 exp2_poly2(x2, p0, p1);
                             } else {
                                 p0 = ex2(__uint_as_float((uint32_t)x2));
                                 p1 = ex2(__uint_as_float((uint32_t)(x2 >> 32)));
                             }
-#endif
                             rs2[e & 3] = fadd2(rs2[e & 3], pack2(p0, p1));
                             if constexpr (kBF16) {
                                 __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
@@ -438,11 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             mbar_arrive(&p_full[g]);
             ATT_TRACE_REC(5);
-#if defined(ATT_EXP) && ATT_EXP == 5  // experiment: skeleton without the epilogue
-            if (false) {
-#else
             if (diag) {
-#endif
                 // epilogue: the item's last PV retired -> O / l -> act dtype -> 32-byte stores
                 mbar_wait(&pv_done[g], b & 1u);
                 tc_fence_after();

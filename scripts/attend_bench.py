@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 import paper_2510_25979_b200 as ac  # noqa: E402
 
-if os.environ.get("ATTNCACHE_LIB"):  # an out-of-tree experiment build (scripts/attend_experiment.sh)
+if os.environ.get("ATTNCACHE_LIB"):  # an out-of-tree experiment build (ATTNCACHE_BUILD_ROOT / ATTNCACHE_EXTRA_FLAGS)
     ac.lib_path = os.environ["ATTNCACHE_LIB"]
 
 name = sys.argv[1] if len(sys.argv) > 1 else "long_prefill"
