@@ -348,13 +348,17 @@ def test_capture_then_reuse_matches_full_attention(ac, ctx):
 # ------------------------------------------------------------------------------------------------
 
 @pytest.mark.slow
-def test_full_step_llama32(ac, ctx):
+@pytest.mark.parametrize("cfg_name", ["llama32_1b", "llama3_8b", "long_prefill"])
+def test_full_step(ac, ctx, cfg_name):
+    """BASELINE.json configs[1-3] at full size in the launch configuration bench.py times (the bench's PACKED
+    DB, the whole batch in one step): every search decision checked, sampled A.V and attention units vs the
+    oracle."""
     from paper_2510_25979_b200.pipeline import PrefillStep
-    cfg = synth.CONFIGS["llama32_1b"]
+    cfg = synth.CONFIGS[cfg_name]
     x = synth.features(cfg, 0, cfg.N, DEV)
     # the bench's DB: PACKED maps built by the library from the generator's dense maps
     maps = ac.pack_db_maps(lambda b, out: synth.fill_maps(cfg, out, b), cfg.N, cfg.L, cfg.H, cfg.S,
-                           torch.bfloat16, DEV, chunk=64)
+                           torch.bfloat16, DEV, chunk=max(1, (1 << 30) // cfg.map_bytes_per_entry))
     db = ac.Database(ctx, x, maps, packed=True, seq_len=cfg.S)
     q, pos, tgt = synth.queries(cfg, DEV)
     Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qkv")
@@ -380,6 +384,8 @@ def test_full_step_llama32(ac, ctx):
     off = [(((b * cfg.L + l) * cfg.H + h) * cfg.S * cfg.d) for b, l, h in mu]
     ref = oracle.attend(storage(Q), storage(K), Vs, "bf16", off, cfg.S, cfg.d)
     check_close(_gather_units(O, mu), ref, torch.bfloat16, "step attend")
+    del db, maps, Q, K, V, O
+    torch.cuda.empty_cache()
 
 
 def test_sharded_prefill_world1_matches_single_gpu_step(ac, ctx):
