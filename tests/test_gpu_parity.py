@@ -852,3 +852,51 @@ def test_graphed_prefill_step_equals_eager(ac, ctx):
     torch.cuda.synchronize()
     for a, b in zip((*ref2, O_e2), out):
         assert torch.equal(a, b)
+
+
+def test_edge_cases_empty_skipped_and_extreme_shapes(ac, ctx):
+    """Empty batches are no-ops; fully skipped rows leave O (and capture outputs) untouched; the longest
+    sequence the attention accepts (S = 8192) matches the oracle on sampled rows and S = 8193 is refused;
+    head dims the tensor-core kernels do not take (d = 32) run on the CUDA-core kernels."""
+    cfg = synth.CONFIGS["llama32_1b"].with_(N=8, B=4, L=1, H=2)
+    db = ac.Database(ctx, synth.features(cfg, 0, cfg.N, DEV), synth.maps(cfg, 0, cfg.N, DEV))
+    V = synth.activations(cfg, "v", 0, cfg.B, device=DEV)
+    Q, K = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qk")
+    idx = torch.arange(cfg.B, device=DEV)
+    # empty batches
+    assert ac.attncache_apply_cached(db, idx[:0], V[:0]).shape[0] == 0
+    assert ac.attncache_attend_full(ctx, Q[:0], K[:0], V[:0]).shape[0] == 0
+    # everything skipped: outputs untouched
+    O = torch.full_like(V, 7.0)
+    ac.attncache_apply_cached(db, idx, V, O, hit=torch.zeros(cfg.B, dtype=torch.uint8, device=DEV))
+    ac.attncache_attend_full(ctx, Q, K, V, O, skip=torch.ones(cfg.B, dtype=torch.uint8, device=DEV))
+    maps = torch.full((cfg.B, cfg.L, cfg.H, ac.attncache_packed_map_elems(cfg.S)), 5.0, dtype=torch.bfloat16, device=DEV)
+    ac.attncache_capture_maps(ctx, Q, K, out=maps, skip=torch.ones(cfg.B, dtype=torch.uint8, device=DEV))
+    torch.cuda.synchronize()
+    assert torch.all(O == 7.0) and torch.all(maps == 5.0)
+    # S = 8192 (the attention's limit): sampled rows of one unit vs the oracle
+    g = torch.Generator(device=DEV).manual_seed(9)
+    Ql, Kl, Vl = (torch.randn(1, 1, 1, 8192, 128, device=DEV, generator=g).to(torch.bfloat16) for _ in range(3))
+    Ol = ac.attncache_attend_full(ctx, Ql, Kl, Vl)
+    torch.cuda.synchronize()
+    ref = oracle.attend(storage(Ql), storage(Kl), storage(Vl), "bf16", [0], 8192, 128)[0]
+    rows = [0, 1, 127, 128, 4095, 8191]
+    check_close(Ol[0, 0, 0, rows].unsqueeze(0), ref[rows][None], torch.bfloat16, "attend S=8192")
+    with pytest.raises(ac.AttnCacheError) as e:
+        z = torch.zeros(1, 1, 1, 8193, 64, device=DEV, dtype=torch.bfloat16)
+        ac.attncache_attend_full(ctx, z, z, z)
+    assert e.value.name == "ATTNCACHE_ERR_SHAPE"
+    # d = 32: CUDA-core kernels for A.V and attention
+    c32 = cfg.with_(d=32)
+    V32, Q32, K32 = (synth.activations(c32, k, 0, cfg.B, device=DEV) for k in "vqk")
+    assert ac.attncache_variant("apply", V32.dtype, c32.S, 32) == "ffma"
+    O32 = ac.attncache_apply_cached(db, idx, V32)
+    A32 = ac.attncache_attend_full(ctx, Q32, K32, V32)
+    torch.cuda.synchronize()
+    units = _units(list(range(cfg.B)), cfg.L, cfg.H)
+    ref = _apply_ref(storage(db.maps), cfg.map_dtype, idx.cpu().numpy(), storage(V32), cfg.act_dtype, units, cfg.L,
+                     cfg.H, cfg.S, 32)
+    check_close(_gather_units(O32, units), ref, torch.bfloat16, "apply d=32")
+    off = [(((b * cfg.L + l) * cfg.H + h) * cfg.S * 32) for b, l, h in units]
+    ref = oracle.attend(storage(Q32), storage(K32), storage(V32), cfg.act_dtype, off, cfg.S, 32)
+    check_close(_gather_units(A32, units), ref, torch.bfloat16, "attend d=32")
