@@ -327,6 +327,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         w.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
         uint32_t b = 0;
         float m_ref = 0.f, l = 0.f;
+        bool pend = false;  // an item whose epilogue is deferred to the next block
+        int32_t pend_row = 0;
+        float pend_l = 0.f;
+        // epilogue of the item whose last block is lb: PV_lb retired -> O / (l_0 + l_1) -> act dtype ->
+        // this warp's 128B-swizzled staging tile -> TMA store of its 32 rows x 64 columns
+        auto epilogue = [&](uint32_t lb, int32_t orow, float l_own) {
+            tmem_st_32x32b_x1(tmem + lane_addr + kXsum + half, __float_as_uint(l_own));
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_wait(&pv_done[0], lb & 1u);
+            pair_sync(q);
+            tc_fence_after();
+            const float inv = 1.f / (l_own + __uint_as_float(tmem_ld_32x32b_x1(tmem + lane_addr + kXsum + (half ^ 1))));
+            uint32_t v[64];
+            tmem_ld_32x32b_x32(o_addr, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+            tmem_ld_32x32b_x32(o_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+            tmem_ld_wait();
+            if (lane == 0) bulk_wait_read<0>();  // the previous TMA store has read the staging tile
+            __syncwarp();
+#pragma unroll
+            for (int c8 = 0; c8 < 8; ++c8) {
+                uint32_t wv[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float lo = __uint_as_float(v[c8 * 8 + 2 * e]) * inv;
+                    const float hi = __uint_as_float(v[c8 * 8 + 2 * e + 1]) * inv;
+                    if constexpr (kBF16) {
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
+                        wv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                    } else {
+                        __half2 h2 = __floats2half2_rn(lo, hi);
+                        wv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                    }
+                }
+                *reinterpret_cast<uint4 *>(stage_o + sw128_offset(lane, c8)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(&tmO, stage_o_u32, half * 64, orow);
+                bulk_commit();
+            }
+            // the partner reads this warp's row sum before the next epilogue rewrites it: the exchange
+            // barriers of the blocks in between order the two
+            tc_fence_before();
+        };
         while (w.active) {
             const int j = w.j;
             const bool diag = j == w.qb;
@@ -428,57 +474,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tmem_st_wait();
             SPLIT_TR_SM(3);
+            if (pend) {
+                // the previous item's epilogue, deferred until this block's P is written: PV_{b-1} (its
+                // last block) has retired meanwhile (s_full(b) implied PV_{b-2}; the parity wait on
+                // PV_{b-1} is unambiguous), and PV_b -- which restarts O -- waits for this arrive
+                epilogue(b - 1, pend_row, pend_l);
+                pend = false;
+            }
             tc_fence_before();
             mbar_arrive(&p_full[buf]);
             SPLIT_TR_SM(4);
-            if (diag) {
-                // epilogue: the item's last PV retired -> O / (l_0 + l_1) -> act dtype -> this warp's
-                // 128B-swizzled staging tile -> TMA store of its 32 rows x 64 columns
-                tmem_st_32x32b_x1(tmem + lane_addr + kXsum + half, __float_as_uint(l));
-                tmem_st_wait();
-                tc_fence_before();
-                // PV_b retired.  s_full(b) only implied PV_{b-2}: wait for PV_{b-1} first so the parity wait
-                // on PV_b cannot be satisfied by a phase two behind (a race the bitwise-repeat test caught)
-                if (b > 0) mbar_wait(&pv_done[0], (b - 1) & 1u);
-                mbar_wait(&pv_done[0], b & 1u);
-                pair_sync(q);
-                tc_fence_after();
-                const float inv = 1.f / (l + __uint_as_float(tmem_ld_32x32b_x1(tmem + lane_addr + kXsum + (half ^ 1))));
-                uint32_t v[64];
-                tmem_ld_32x32b_x32(o_addr, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-                tmem_ld_32x32b_x32(o_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
-                tmem_ld_wait();
-                if (lane == 0) bulk_wait_read<0>();  // the previous TMA store has read the staging tile
-                __syncwarp();
-#pragma unroll
-                for (int c8 = 0; c8 < 8; ++c8) {
-                    uint32_t wv[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float lo = __uint_as_float(v[c8 * 8 + 2 * e]) * inv;
-                        const float hi = __uint_as_float(v[c8 * 8 + 2 * e + 1]) * inv;
-                        if constexpr (kBF16) {
-                            __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
-                            wv[e] = *reinterpret_cast<uint32_t *>(&h2);
-                        } else {
-                            __half2 h2 = __floats2half2_rn(lo, hi);
-                            wv[e] = *reinterpret_cast<uint32_t *>(&h2);
-                        }
-                    }
-                    *reinterpret_cast<uint4 *>(stage_o + sw128_offset(lane, c8)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-                }
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_2d(&tmO, stage_o_u32, half * 64, (int32_t)(w.row0 + w.qb * kBlk + q * 32));
-                    bulk_commit();
-                }
-                // the partner reads this warp's row sum before the next item's epilogue rewrites it: the
-                // exchange barriers of the blocks in between order the two
-                tc_fence_before();
+            if (diag) {  // this item ends here: its epilogue runs after the next block's softmax
+                pend = true;
+                pend_row = (int32_t)(w.row0 + w.qb * kBlk + q * 32);
+                pend_l = l;
             }
             ++b;
             w.advance();
+        }
+        if (pend) {  // the stream's last item: PV_{b-1} may still run (wait PV_{b-2} first: parity)
+            if (b >= 2) mbar_wait(&pv_done[0], (b - 2) & 1u);
+            epilogue(b - 1, pend_row, pend_l);
         }
         if (lane == 0) bulk_wait<0>();  // O stores complete before the CTA (and its smem) retires
     }
