@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *s_full = v_empty + kNV;  // [2] S_b computed in buffer b % 2
     uint64_t *p_full = s_full + 2;    // [2] P_b written (256 arrivals)
     uint64_t *pv_done = p_full + 2;   // PV_b retired (one phase per block)
-    uint32_t *tmem_slot = (uint32_t *)(pv_done + 1);
+    uint64_t *last_done = pv_done + 1;  // the stream's last PV retired (single phase)
+    uint32_t *tmem_slot = (uint32_t *)(last_done + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         mbar_init(&pv_done[0], 1);
+        mbar_init(last_done, 1);
         fence_barrier_init();
     }
     if (warp == 0 && lane == 0) {
@@ -264,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (wS.active) issue_s();  // into the buffer PV_b reads: queued behind it
                 SPLIT_TR_MMA(bP - 1, 4);
             }
+            if (bP > 0) umma_commit_w(last_done);
         }
 #else
         } else if (warp == 1 && lane == 0) {
@@ -310,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (wS.active) issue_s();  // into the buffer PV_b reads: queued behind it
                 SPLIT_TR_MMA(bP - 1, 4);
             }
+            if (bP > 0) umma_commit(last_done);
         }
 #endif
     } else {
@@ -492,8 +496,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++b;
             w.advance();
         }
-        if (pend) {  // the stream's last item: PV_{b-1} may still run (wait PV_{b-2} first: parity)
-            if (b >= 2) mbar_wait(&pv_done[0], (b - 2) & 1u);
+        if (pend) {
+            // the stream's last item: pv_done may be anywhere from PV_{b-3} to PV_{b-1} retired, which one
+            // parity bit cannot tell apart; last_done (committed after the last PV) can, and once it fired
+            // the epilogue's wait on PV_{b-1} passes at once
+            mbar_wait(last_done, 0u);
             epilogue(b - 1, pend_row, pend_l);
         }
         if (lane == 0) bulk_wait<0>();  // O stores complete before the CTA (and its smem) retires
