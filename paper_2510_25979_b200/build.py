@@ -52,6 +52,10 @@ def _compile(src, obj, ptxas_v):
 def build(force: bool = False, ptxas_v: bool = False, quiet: bool = True) -> str:
     os.makedirs(OBJ, exist_ok=True)
     os.makedirs(LIB_DIR, exist_ok=True)
+    stamp = os.path.join(OBJ, "flags.txt")  # objects built with other flags are stale
+    flags = " ".join(FLAGS)
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     deps = _deps()
     jobs = []
@@ -69,6 +73,8 @@ def build(force: bool = False, ptxas_v: bool = False, quiet: bool = True) -> str
         tmp = LIB + f".tmp{os.getpid()}"
         subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"])
         os.replace(tmp, LIB)
+    with open(stamp, "w") as f:
+        f.write(flags)
     return LIB
 
 

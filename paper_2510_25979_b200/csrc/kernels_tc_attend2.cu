@@ -33,7 +33,8 @@ constexpr float kRescaleThreshold = 8.f;
 constexpr int kTile = kBlk * kD * 2;    // one [128][128] 16-bit tile (two 64-column swizzle halves)
 constexpr int kOutWarp = 32 * 64 * 2;   // per softmax warp: O staging [32 rows][64 cols]
 // Rings: Q 2 slots (one item ahead), K kNK slots, V kNV slots (shared memory holds 6 tiles next to the O staging;
-// K 3 / V 1 measured 45 % slower than 2 / 2: a one-slot V ring serializes PV with the next V load).
+// K 3 / V 1 measured 45 % slower than 2 / 2: a one-slot V ring serializes PV with the next V load; moving the
+// V loads to a thread of their own, so K_{b+1} is not held behind V_b, measured 1 % / 9 % slower at configs[3] / [2]).
 #ifndef SPLIT_NK
 #define SPLIT_NK 2
 #endif
@@ -71,30 +72,46 @@ __device__ __forceinline__ void pair_sync(int q) { asm volatile("bar.sync %0, 64
 // Item walker shared by all roles: items t = first, first + stride, ...; item -> (unit, qb) in L2-sized
 // unit groups, heaviest query blocks first inside a group (kernels_tc_attend.cu, Stream); j walks the
 // item's key blocks.  row0: first Q/O row of the unit; kv_row0: first K/V row (GQA: K/V head h/(H/Hkv)).
+// Launch-time constants of the item order with their division magics (FastDiv).
+struct Sched {
+    uint32_t group, n_qb, per_row, S;
+    FastDiv gq, grp, per_row_d, h_d, hq_d;  // group * n_qb, group, L * H, H, H / Hkv
+    uint32_t L, Hkv;
+};
+
 struct Walker {
-    uint32_t t, stride, items, units, per_row, n_qb, S, group, H, Hkv, L;
+    uint32_t t, stride, items, units;
+    const Sched *sc;
     const int32_t *rows;
     bool active = false;
     int64_t row0 = 0, kv_row0 = 0;
     int qb = 0, j = 0;
-    __device__ void init(uint32_t first, uint32_t stride_, uint32_t items_, uint32_t units_, uint32_t per_row_,
-                         uint32_t n_qb_, uint32_t S_, uint32_t group_, const int32_t *rows_, uint32_t H_,
-                         uint32_t Hkv_) {
-        t = first, stride = stride_, items = items_, units = units_, per_row = per_row_, n_qb = n_qb_, S = S_;
-        group = group_, H = H_, Hkv = Hkv_, L = per_row_ / H_, rows = rows_;
+    __device__ void init(uint32_t first, uint32_t stride_, uint32_t items_, uint32_t units_, const Sched &sc_,
+                         const int32_t *rows_) {
+        t = first, stride = stride_, items = items_, units = units_, sc = &sc_, rows = rows_;
         start_item();
     }
     __device__ void start_item() {
         active = t < items;
         if (!active) return;
-        const uint32_t gi = t / (group * n_qb), w = t - gi * (group * n_qb);
-        const uint32_t gbase = gi * group, gsize = min(group, units - gbase);
-        const uint32_t u = gbase + w % gsize;
-        qb = (int)(n_qb - 1 - w / gsize);
-        const int64_t row = rows[u / per_row];
-        const uint32_t lh = u % per_row;
-        row0 = (row * per_row + lh) * S;
-        kv_row0 = ((row * L + lh / H) * Hkv + (lh % H) / (H / Hkv)) * (int64_t)S;
+        const Sched &c = *sc;
+        const uint32_t gi = c.gq.div(t), w = t - gi * c.gq.d;
+        const uint32_t gbase = gi * c.group;
+        uint32_t u;
+        if (gbase + c.group <= units) {
+            const uint32_t a = c.grp.div(w);
+            qb = (int)(c.n_qb - 1 - a);
+            u = gbase + (w - a * c.group);
+        } else {  // the last, partial group
+            const uint32_t gsize = units - gbase;
+            qb = (int)(c.n_qb - 1 - w / gsize);
+            u = gbase + w % gsize;
+        }
+        const uint32_t ri = c.per_row_d.div(u), lh = u - ri * c.per_row;
+        const int64_t row = rows[ri];
+        const uint32_t l = c.h_d.div(lh), h = lh - l * c.h_d.d;
+        row0 = (row * c.per_row + lh) * c.S;
+        kv_row0 = ((row * c.L + l) * c.Hkv + c.hq_d.div(h)) * (int64_t)c.S;
         j = 0;
     }
     // Moves past the current key block; returns true when that block ended the item.
@@ -132,7 +149,8 @@ template <bool kBF16>
 __global__ void __launch_bounds__(kThreads, 1)
     attend_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
-                        const AttendArgs a, const uint32_t idesc_s, const uint32_t idesc_pv) {
+                        const AttendArgs a, const __grid_constant__ Sched sc, const uint32_t idesc_s,
+                        const uint32_t idesc_pv) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sQ = smem;               // [2][tile]
@@ -183,19 +201,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    const uint32_t S = (uint32_t)a.S;
-    const uint32_t n_qb = S / kBlk;
-    const uint32_t per_row = (uint32_t)(a.L * a.H);
-    const uint32_t units = (uint32_t)(*a.list.count) * per_row;
-    const uint32_t items = units * n_qb;
-    const uint32_t l2_group = max(1u, (48u << 20) / (2u * S * kD * 2u));
+    const uint32_t units = (uint32_t)(*a.list.count) * sc.per_row;
+    const uint32_t items = units * sc.n_qb;
 
     if (warp < 4) {
         setmaxnreg_dec<56>();
         if (warp == 0 && lane == 0) {
             // ------------------------------ TMA loader -------------------------------------------
             Walker w;
-            w.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+            w.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
             uint32_t b = 0, it = 0;
             while (w.active) {
                 if (w.j == 0) {
@@ -226,8 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ------------------------------ MMA issuer (whole warp; one elected lane issues) --------
             // wS runs two blocks ahead of wP: S_0, S_1, then PV_b followed by S_{b+2}.
             Walker wS, wP;
-            wS.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
-            wP.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+            wS.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
+            wP.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
             uint32_t bS = 0, itS = 0, bP = 0;
             auto issue_s = [&]() {
                 const uint32_t buf = bS & 1u, qs = itS & 1u;
@@ -273,8 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ------------------------------ MMA issuer -------------------------------------------
             // wS runs two blocks ahead of wP: S_0, S_1, then PV_b followed by S_{b+2}.
             Walker wS, wP;
-            wS.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
-            wP.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+            wS.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
+            wP.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
             uint32_t bS = 0, itS = 0, bP = 0;
             auto issue_s = [&]() {
                 const uint32_t buf = bS & 1u, qs = itS & 1u;
@@ -328,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t stage_o_u32 = smem_u32(stage_o);
         const float sl2 = a.scale * 1.4426950408889634f;
         Walker w;
-        w.init(blockIdx.x, gridDim.x, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+        w.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
         uint32_t b = 0;
         float m_ref = 0.f, l = 0.f;
         bool pend = false;  // an item whose epilogue is deferred to the next block
@@ -528,7 +542,19 @@ cudaError_t launch_t(const AttendArgs &a, int sm_count, cudaStream_t st) {
     const uint32_t fmt = bf16 ? 1u : 0u;
     const uint32_t idesc_s = idesc_f16(kBlk, kBlk, fmt, 0u, 0u);  // Q K-major x K K-major
     const uint32_t idesc_pv = idesc_f16(kBlk, kD, fmt, 0u, 1u);   // P (TMEM) x V MN-major
-    attend_split_kernel<kBF16><<<sm_count, kThreads, kSmem, st>>>(tq, tk, tv, to, a, idesc_s, idesc_pv);
+    Sched sc;
+    sc.S = (uint32_t)a.S;
+    sc.n_qb = sc.S / kBlk;
+    sc.per_row = (uint32_t)(a.L * a.H);
+    sc.group = std::max(1u, (48u << 20) / (2u * sc.S * kD * 2u));  // units whose K and V fill ~48 MB of L2
+    sc.L = (uint32_t)a.L;
+    sc.Hkv = (uint32_t)a.Hkv;
+    sc.gq = FastDiv(sc.group * sc.n_qb);
+    sc.grp = FastDiv(sc.group);
+    sc.per_row_d = FastDiv(sc.per_row);
+    sc.h_d = FastDiv((uint32_t)a.H);
+    sc.hq_d = FastDiv((uint32_t)(a.H / a.Hkv));
+    attend_split_kernel<kBF16><<<sm_count, kThreads, kSmem, st>>>(tq, tk, tv, to, a, sc, idesc_s, idesc_pv);
     count_launches(1);
     return cudaGetLastError();
 }

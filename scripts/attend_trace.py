@@ -43,6 +43,12 @@ if SPLIT:
     sel = slice(20, 200)
     print(f"softmax warp 4: median cycles wait_S {np.median(d[sel, 0]):.0f}  load+exchange {np.median(d[sel, 1]):.0f}  "
           f"exp+store {np.median(d[sel, 2]):.0f}  arrive {np.median(d[sel, 3]):.0f}  period {np.median(per[sel]):.0f}")
+    gap = t[1:, 0] - t[:-1, 4]
+    print(f"softmax warp 4: mean cycles wait_S {d[sel, 0].mean():.0f}  load+exchange {d[sel, 1].mean():.0f}  "
+          f"exp+store {d[sel, 2].mean():.0f}  arrive(+epilogue) {d[sel, 3].mean():.0f}  gap {gap[sel].mean():.0f}  "
+          f"period {per[sel].mean():.0f}")
+    big = np.argsort(-gap[sel])[:6] + 20
+    print("largest gaps (block, gap, next wait_S):", [(int(i), int(gap[i]), int(d[i + 1, 0])) for i in big])
     dm = np.diff(m[:, :5], axis=1)
     perm = m[1:, 0] - m[:-1, 0]
     print(f"MMA: median cycles wait_P {np.median(dm[sel, 0]):.0f}  wait_V {np.median(dm[sel, 1]):.0f}  PV issue "
