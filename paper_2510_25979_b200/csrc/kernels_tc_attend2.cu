@@ -19,6 +19,7 @@
 // descriptor arithmetic stays in uniform registers) + TMEM owner, warps 2-3 idle; warps 4-7 and 8-11 the softmax /
 // epilogue halves (setmaxnreg moves registers from the producers to the softmax warps).
 #include "kernels.cuh"
+#include "item_sched.cuh"
 #include "sm100.cuh"
 
 namespace ac {
@@ -69,61 +70,8 @@ __device__ __forceinline__ void setmaxnreg_dec() {
 // Named barrier over the 64 threads of one row quarter's two softmax warps.
 __device__ __forceinline__ void pair_sync(int q) { asm volatile("bar.sync %0, 64;" ::"r"(q + 1) : "memory"); }
 
-// Item walker shared by all roles: items t = first, first + stride, ...; item -> (unit, qb) in L2-sized
-// unit groups, heaviest query blocks first inside a group (kernels_tc_attend.cu, Stream); j walks the
-// item's key blocks.  row0: first Q/O row of the unit; kv_row0: first K/V row (GQA: K/V head h/(H/Hkv)).
-// Launch-time constants of the item order with their division magics (FastDiv).
-struct Sched {
-    uint32_t group, n_qb, per_row, S;
-    FastDiv gq, grp, per_row_d, h_d, hq_d;  // group * n_qb, group, L * H, H, H / Hkv
-    uint32_t L, Hkv;
-};
-
-struct Walker {
-    uint32_t t, stride, items, units;
-    const Sched *sc;
-    const int32_t *rows;
-    bool active = false;
-    int64_t row0 = 0, kv_row0 = 0;
-    int qb = 0, j = 0;
-    __device__ void init(uint32_t first, uint32_t stride_, uint32_t items_, uint32_t units_, const Sched &sc_,
-                         const int32_t *rows_) {
-        t = first, stride = stride_, items = items_, units = units_, sc = &sc_, rows = rows_;
-        start_item();
-    }
-    __device__ void start_item() {
-        active = t < items;
-        if (!active) return;
-        const Sched &c = *sc;
-        const uint32_t gi = c.gq.div(t), w = t - gi * c.gq.d;
-        const uint32_t gbase = gi * c.group;
-        uint32_t u;
-        if (gbase + c.group <= units) {
-            const uint32_t a = c.grp.div(w);
-            qb = (int)(c.n_qb - 1 - a);
-            u = gbase + (w - a * c.group);
-        } else {  // the last, partial group
-            const uint32_t gsize = units - gbase;
-            qb = (int)(c.n_qb - 1 - w / gsize);
-            u = gbase + w % gsize;
-        }
-        const uint32_t ri = c.per_row_d.div(u), lh = u - ri * c.per_row;
-        const int64_t row = rows[ri];
-        const uint32_t l = c.h_d.div(lh), h = lh - l * c.h_d.d;
-        row0 = (row * c.per_row + lh) * c.S;
-        kv_row0 = ((row * c.L + l) * c.Hkv + c.hq_d.div(h)) * (int64_t)c.S;
-        j = 0;
-    }
-    // Moves past the current key block; returns true when that block ended the item.
-    __device__ bool advance() {
-        if (++j > qb) {
-            t += stride;
-            start_item();
-            return true;
-        }
-        return false;
-    }
-};
+// Item order and walker: item_sched.cuh (L2-sized unit groups, heaviest query blocks first).
+using Walker = ItemWalker;
 
 #if defined(ATT_TRACE)  // timeline experiment (scripts/attend_trace.py --split): clock64 stamps of CTA 0
 __device__ unsigned long long g_split_trace_sm[256][6];   // softmax warp 4, lane 0, first 256 blocks
@@ -149,7 +97,7 @@ template <bool kBF16>
 __global__ void __launch_bounds__(kThreads, 1)
     attend_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
-                        const AttendArgs a, const __grid_constant__ Sched sc, const uint32_t idesc_s,
+                        const AttendArgs a, const __grid_constant__ ItemSched sc, const uint32_t idesc_s,
                         const uint32_t idesc_pv) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -209,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (warp == 0 && lane == 0) {
             // ------------------------------ TMA loader -------------------------------------------
             Walker w;
-            w.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
+            w.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
             uint32_t b = 0, it = 0;
             while (w.active) {
                 if (w.j == 0) {
@@ -232,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int h = 0; h < 2; ++h)
                     tma_load_2d(smem_u32(sV + vv * kTile + h * (kBlk * 128)), &tmV, &v_full[vv], h * 64, r_j);
                 ++b;
-                if (w.advance()) ++it;
+                if (w.advance(sc)) ++it;
             }
 #if !defined(SPLIT_LANE_MMA)  // default: warp-converged MMA issuer (descriptors in uniform registers; -DSPLIT_LANE_MMA
                               // selects the single-lane issuer, ~0.7 % slower at configs[3])
@@ -240,8 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ------------------------------ MMA issuer (whole warp; one elected lane issues) --------
             // wS runs two blocks ahead of wP: S_0, S_1, then PV_b followed by S_{b+2}.
             Walker wS, wP;
-            wS.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
-            wP.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
+            wS.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
+            wP.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
             uint32_t bS = 0, itS = 0, bP = 0;
             auto issue_s = [&]() {
                 const uint32_t buf = bS & 1u, qs = itS & 1u;
@@ -257,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma_commit_w(&k_empty[bS % kNK]);
                 if (wS.j == wS.qb) umma_commit_w(&q_empty[qs]);
                 ++bS;
-                if (wS.advance()) ++itS;
+                if (wS.advance(sc)) ++itS;
             };
             if (wS.active) issue_s();
             if (wS.active) issue_s();
@@ -276,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma_commit_w(&pv_done[0]);
                 SPLIT_TR_MMA(bP, 3);
                 ++bP;
-                wP.advance();
+                wP.advance(sc);
                 if (wS.active) issue_s();  // into the buffer PV_b reads: queued behind it
                 SPLIT_TR_MMA(bP - 1, 4);
             }
@@ -287,8 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ------------------------------ MMA issuer -------------------------------------------
             // wS runs two blocks ahead of wP: S_0, S_1, then PV_b followed by S_{b+2}.
             Walker wS, wP;
-            wS.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
-            wP.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
+            wS.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
+            wP.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
             uint32_t bS = 0, itS = 0, bP = 0;
             auto issue_s = [&]() {
                 const uint32_t buf = bS & 1u, qs = itS & 1u;
@@ -304,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma_commit(&k_empty[bS % kNK]);
                 if (wS.j == wS.qb) umma_commit(&q_empty[qs]);
                 ++bS;
-                if (wS.advance()) ++itS;
+                if (wS.advance(sc)) ++itS;
             };
             if (wS.active) issue_s();
             if (wS.active) issue_s();
@@ -323,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma_commit(&pv_done[0]);
                 SPLIT_TR_MMA(bP, 3);
                 ++bP;
-                wP.advance();
+                wP.advance(sc);
                 if (wS.active) issue_s();  // into the buffer PV_b reads: queued behind it
                 SPLIT_TR_MMA(bP - 1, 4);
             }
@@ -342,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t stage_o_u32 = smem_u32(stage_o);
         const float sl2 = a.scale * 1.4426950408889634f;
         Walker w;
-        w.init(blockIdx.x, gridDim.x, items, units, sc, a.list.rows);
+        w.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
         uint32_t b = 0;
         float m_ref = 0.f, l = 0.f;
         bool pend = false;  // an item whose epilogue is deferred to the next block
@@ -508,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 pend_l = l;
             }
             ++b;
-            w.advance();
+            w.advance(sc);
         }
         if (pend) {
             // the stream's last item: pv_done may be anywhere from PV_{b-3} to PV_{b-1} retired, which one
@@ -542,18 +490,9 @@ cudaError_t launch_t(const AttendArgs &a, int sm_count, cudaStream_t st) {
     const uint32_t fmt = bf16 ? 1u : 0u;
     const uint32_t idesc_s = idesc_f16(kBlk, kBlk, fmt, 0u, 0u);  // Q K-major x K K-major
     const uint32_t idesc_pv = idesc_f16(kBlk, kD, fmt, 0u, 1u);   // P (TMEM) x V MN-major
-    Sched sc;
-    sc.S = (uint32_t)a.S;
-    sc.n_qb = sc.S / kBlk;
-    sc.per_row = (uint32_t)(a.L * a.H);
-    sc.group = std::max(1u, (48u << 20) / (2u * sc.S * kD * 2u));  // units whose K and V fill ~48 MB of L2
-    sc.L = (uint32_t)a.L;
-    sc.Hkv = (uint32_t)a.Hkv;
-    sc.gq = FastDiv(sc.group * sc.n_qb);
-    sc.grp = FastDiv(sc.group);
-    sc.per_row_d = FastDiv(sc.per_row);
-    sc.h_d = FastDiv((uint32_t)a.H);
-    sc.hq_d = FastDiv((uint32_t)(a.H / a.Hkv));
+    // units whose K and V fill ~48 MB of L2 form a group
+    const ItemSched sc = ItemSched::make((uint32_t)a.S, (uint32_t)a.L, (uint32_t)a.H, (uint32_t)a.Hkv, kBlk,
+                                         2u * (uint32_t)a.S * kD * 2u);
     attend_split_kernel<kBF16><<<sm_count, kThreads, kSmem, st>>>(tq, tk, tv, to, a, sc, idesc_s, idesc_pv);
     count_launches(1);
     return cudaGetLastError();

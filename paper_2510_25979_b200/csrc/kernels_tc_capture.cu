@@ -14,12 +14,26 @@
 // registers: one TMEM load per block).  A single epilogue group left the kernel at 0.29 of its HBM
 // roofline (bench stages.capture_misses, configs[1]).
 #include "kernels.cuh"
+#include "item_sched.cuh"
 #include "sm100.cuh"
 
 namespace ac {
 using namespace sm100;
 
 namespace {
+
+// Experiment switches (scripts/capture_ab.sh): pass-1 key-block order (descending when 1) and the L2
+// policy of the K loads (0 evict_first, 1 evict_normal, 2 evict_last).  Measured (packed bf16 maps,
+// configs 1 / 2 / 3): descending 0.272 / 0.582 / 2.40 ms vs ascending 0.250 / 0.551 / 2.44 (plain
+// stores); K evict_last vs normal neutral at S <= 256, 2.27 -> 2.18 ms at S = 1024 with streamed stores.
+#ifndef CAP_DESC
+#define CAP_DESC 0
+#endif
+#ifndef CAP_KPOL
+#define CAP_KPOL 2
+#endif
+constexpr bool kCapDesc = CAP_DESC;
+constexpr int kCapKPol = CAP_KPOL;
 
 constexpr int kThreads = 384;  // 3 warpgroups: producers (warps 0-3), epilogue group 0 (4-7), group 1 (8-11)
 constexpr int kBlk = 128;
@@ -51,10 +65,10 @@ __device__ __forceinline__ void setmaxnreg_dec() {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
 }
 
-template <int kD>
+template <int kD, bool kStreamOut>
 __global__ void __launch_bounds__(kThreads, 1)
     capture_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                      const CaptureArgs a, const uint32_t idesc) {
+                      const CaptureArgs a, const __grid_constant__ ItemSched sc, const uint32_t idesc) {
     using C = Cfg<kD>;
     constexpr int NK = C::kKSlots;
     extern __shared__ uint8_t smem_raw[];
@@ -93,22 +107,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     const uint32_t S = (uint32_t)a.S;
-    const uint32_t n_qb = S / kBlk;
-    const uint32_t per_row = (uint32_t)(a.L * a.H);
+    const uint32_t per_row = sc.per_row;
     const uint32_t units = (uint32_t)(*a.list.count) * per_row;
-    const uint32_t items = units * n_qb;
+    const uint32_t items = units * sc.n_qb;
     const uint32_t stride = 2 * gridDim.x;  // two item streams per CTA (one per group)
-    // item t -> (selected row, (layer, head), qb): units in L2-sized groups (K of a group fits in ~48 MB;
-    // both passes re-read it), heaviest query blocks first inside a group
-    const uint32_t l2_group = max(1u, (48u << 20) / (S * (uint32_t)a.d * 2u));
-    auto decode = [&](uint32_t t, int64_t &row, uint32_t &lh, int &qb) {
-        const uint32_t gi = t / (l2_group * n_qb), w = t - gi * (l2_group * n_qb);
-        const uint32_t gbase = gi * l2_group, gsize = min(l2_group, units - gbase);
-        qb = (int)(n_qb - 1 - w / gsize);
-        const uint32_t u = gbase + w % gsize;
-        row = a.list.rows[u / per_row];
-        lh = u % per_row;
-    };
+    // item t -> (selected row, (layer, head), qb): item_sched.cuh (units in L2-sized groups -- K of a group
+    // fits in ~48 MB; both passes re-read it -- heaviest query blocks first inside a group)
 
     if (warp < 4) {
         // Producers: per group g, warp 2g loads Q (per item) and K_j (per block and pass), warp 2g+1
@@ -117,50 +121,51 @@ __global__ void __launch_bounds__(kThreads, 1)
         setmaxnreg_dec<56>();
         const int g = warp >> 1;
         if (lane == 0) {
+            // Q is read once, K twice (both passes) within an item: Q evict_first, K per CAP_KPOL
+            const uint64_t pol_q = policy_evict_first();
+            const uint64_t pol_k = kCapKPol == 2 ? policy_evict_last() : kCapKPol == 1 ? policy_evict_normal() : policy_evict_first();
             uint32_t it = 0, blk = 0;
             for (uint32_t t = blockIdx.x + g * gridDim.x; t < items; t += stride, ++it) {
-                int64_t row;
-                uint32_t lh;
-                int qb;
-                decode(t, row, lh, qb);
-                const int64_t row0 = (row * per_row + lh) * (int64_t)S;  // first Q row of the unit
-                // first K row: the unit's K head under grouped-query attention (Hkv = H for MHA)
-                const int64_t krow0 = ((row * a.L + lh / (uint32_t)a.H) * a.Hkv + (lh % (uint32_t)a.H) / (uint32_t)(a.H / a.Hkv)) * (int64_t)S;
+                const ItemSched::Item item = sc.decode(t, units, a.list.rows);
+                const int qb = item.qb;
                 const uint32_t qph = it & 1u;
                 if ((warp & 1) == 0) {
                     mbar_wait(&q_empty[g], qph ^ 1u);
                     mbar_arrive_expect_tx(&q_full[g], C::kTile);
                     for (int h = 0; h < kD / 64; ++h)
-                        tma_load_2d(smem_u32(sQ + g * C::kTile + h * (kBlk * 128)), &tmQ, &q_full[g], h * 64,
-                                    (int32_t)(row0 + qb * kBlk));
+                        tma_load_2d_hint(smem_u32(sQ + g * C::kTile + h * (kBlk * 128)), &tmQ, &q_full[g], h * 64,
+                                    (int32_t)(item.row0 + qb * kBlk), pol_q);
                 } else {
                     mbar_wait(&q_full[g], qph);
                 }
-                for (int pass = 0; pass < 2; ++pass) {
-                    for (int j = 0; j <= qb; ++j, ++blk) {
-                        const uint32_t ks = g * NK + blk % NK, kph = (blk / NK) & 1u;
-                        if ((warp & 1) == 0) {
-                            mbar_wait(&k_empty[ks], kph ^ 1u);
-                            mbar_arrive_expect_tx(&k_full[ks], C::kTile);
-                            for (int h = 0; h < kD / 64; ++h)
-                                tma_load_2d(smem_u32(sK + ks * C::kTile + h * (kBlk * 128)), &tmK, &k_full[ks],
-                                            h * 64, (int32_t)(krow0 + j * kBlk));
-                        } else {
-                            const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
-                            mbar_wait(&k_full[ks], kph);
-                            mbar_wait(&s_free[g * 2 + buf], bph ^ 1u);
-                            tc_fence_after();
-                            const uint32_t q_base = smem_u32(sQ + g * C::kTile), k_base = smem_u32(sK + ks * C::kTile);
+                // pass 0 visits key blocks 0..qb (row max and sum), pass 1 blocks qb-1..0 (the diagonal
+                // block's P is written in pass 0 from registers; descending, so the 32-byte sectors a row
+                // shares between neighbouring blocks are completed back to back while still in L2 -- the
+                // ascending order measured 10 % slower at configs[3]'s S = 1024)
+                for (int i = 0; i <= 2 * qb; ++i, ++blk) {
+                    const int j = i <= qb ? i : kCapDesc ? 2 * qb - i : i - qb - 1;
+                    const uint32_t ks = g * NK + blk % NK, kph = (blk / NK) & 1u;
+                    if ((warp & 1) == 0) {
+                        mbar_wait(&k_empty[ks], kph ^ 1u);
+                        mbar_arrive_expect_tx(&k_full[ks], C::kTile);
+                        for (int h = 0; h < kD / 64; ++h)
+                            tma_load_2d_hint(smem_u32(sK + ks * C::kTile + h * (kBlk * 128)), &tmK, &k_full[ks], h * 64,
+                                             (int32_t)(item.kv_row0 + j * kBlk), pol_k);
+                    } else {
+                        const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
+                        mbar_wait(&k_full[ks], kph);
+                        mbar_wait(&s_free[g * 2 + buf], bph ^ 1u);
+                        tc_fence_after();
+                        const uint32_t q_base = smem_u32(sQ + g * C::kTile), k_base = smem_u32(sK + ks * C::kTile);
 #pragma unroll
-                            for (int k = 0; k < kD / 16; ++k) {
-                                const uint32_t off = (k >> 2) * (kBlk * 128) + (k & 3) * 32;
-                                umma_f16(tmem + g * 256 + buf * kBlk, smem_desc(q_base + off, 16, 1024, kSwizzle128B),
-                                         smem_desc(k_base + off, 16, 1024, kSwizzle128B), idesc, k != 0);
-                            }
-                            umma_commit(&s_full[g * 2 + buf]);
-                            umma_commit(&k_empty[ks]);
-                            if (pass == 1 && j == qb) umma_commit(&q_empty[g]);
+                        for (int k = 0; k < kD / 16; ++k) {
+                            const uint32_t off = (k >> 2) * (kBlk * 128) + (k & 3) * 32;
+                            umma_f16(tmem + g * 256 + buf * kBlk, smem_desc(q_base + off, 16, 1024, kSwizzle128B),
+                                     smem_desc(k_base + off, 16, 1024, kSwizzle128B), idesc, k != 0);
                         }
+                        umma_commit(&s_full[g * 2 + buf]);
+                        umma_commit(&k_empty[ks]);
+                        if (i == 2 * qb) umma_commit(&q_empty[g]);
                     }
                 }
             }
@@ -173,88 +178,118 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r = q * 32 + lane;
         const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
         const float sl2 = a.scale * 1.4426950408889634f;
+        const uint64_t pol_out = policy_evict_first();  // maps: written once (used when kStreamOut)
         uint16_t *maps = (uint16_t *)a.maps;
         const bool bf16 = a.map_dt == ATTNCACHE_BF16;
         const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
         uint32_t blk = 0;
+        // writes 32 P values (16 packed pairs) of this thread's row at column c0 + 32c, clipped to the stored length
+        auto store_chunk = [&](uint16_t *mrow, int c0, int c, int stored, const uint32_t (&w)[16]) {
+            const int ncols = min(kBlk, stored - c0);
+            uint4 *dst = (uint4 *)(mrow + c0 + c * 32);
+#if defined(CAP_EXP) && CAP_EXP == 1  // experiment: no map stores
+            if (w[0] == 0x12345678u && w[15] == 0x9abcdef0u) dst[0] = make_uint4(w[1], w[2], w[3], w[4]);
+#else
+#pragma unroll
+            for (int pc = 0; pc < 4; ++pc)
+                if (c * 32 + pc * 8 < ncols) {
+                    const uint4 v = make_uint4(w[4 * pc], w[4 * pc + 1], w[4 * pc + 2], w[4 * pc + 3]);
+                    if constexpr (kStreamOut)
+                        st_global_16_hint(dst + pc, v, pol_out);
+                    else
+                        dst[pc] = v;
+                }
+#endif
+        };
+        auto pack = [&](float p0, float p1) -> uint32_t {
+            if (bf16) {
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                return *reinterpret_cast<uint32_t *>(&h2);
+            }
+            __half2 h2 = __floats2half2_rn(p0, p1);
+            return *reinterpret_cast<uint32_t *>(&h2);
+        };
         for (uint32_t t = blockIdx.x + g * gridDim.x; t < items; t += stride) {
-            int64_t row;
-            uint32_t lh;
-            int qb;
-            decode(t, row, lh, qb);
+            const ItemSched::Item item = sc.decode(t, units, a.list.rows);
+            const int qb = item.qb;
             const int R = qb * kBlk + r;  // this thread's query row in the unit
-            uint16_t *mrow = maps + ((row * per_row + lh) * a.map_stride) + map_row_off(R, S, a.map_layout);
+            uint16_t *mrow = maps + ((item.row * per_row + item.lh) * a.map_stride) + map_row_off(R, S, a.map_layout);
             // packed rows hold 8*(R/8 + 1) elements; dense rows S (zeros above the diagonal)
             const int stored = packed ? 8 * (R / 8 + 1) : (int)S;
             float m = -INFINITY, l = 0.f, off = 0.f;
-            for (int pass = 0; pass < 2; ++pass) {
-                for (int j = 0; j <= qb; ++j, ++blk) {
-                    const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
-                    const bool diag = j == qb;
-                    const int lim = diag ? r : kBlk - 1;
-                    mbar_wait(&s_full[g * 2 + buf], bph);
-                    tc_fence_after();
-                    const uint32_t s_addr = tmem + lane_addr + g * 256 + buf * kBlk;
-                    // the whole S row of the block in registers (one TMEM round trip); masked keys -inf
-                    uint32_t sv[kBlk];
-                    tmem_ld_32x32b_x64(s_addr, sv);
-                    tmem_ld_32x32b_x64(s_addr + 64, sv + 64);
-                    tmem_ld_wait();
-                    tc_fence_before();
-                    mbar_arrive(&s_free[g * 2 + buf]);  // S is in registers: the buffer may be refilled
-                    if (diag) {
+            // pass 0: key blocks 0..qb (row max and sum; the diagonal block, visited last, keeps its
+            // exponentials in registers and writes its P at once); pass 1: blocks qb-1..0 write P
+            for (int i = 0; i <= 2 * qb; ++i, ++blk) {
+                const bool pass0 = i <= qb;
+                const int j = pass0 ? i : kCapDesc ? 2 * qb - i : i - qb - 1;
+                const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
+                const bool diag = j == qb;
+                const int lim = diag ? r : kBlk - 1;
+                mbar_wait(&s_full[g * 2 + buf], bph);
+                tc_fence_after();
+                const uint32_t s_addr = tmem + lane_addr + g * 256 + buf * kBlk;
+                // the whole S row of the block in registers (one TMEM round trip); masked keys -inf
+                uint32_t sv[kBlk];
+                tmem_ld_32x32b_x64(s_addr, sv);
+                tmem_ld_32x32b_x64(s_addr + 64, sv + 64);
+                tmem_ld_wait();
+                tc_fence_before();
+                mbar_arrive(&s_free[g * 2 + buf]);  // S is in registers: the buffer may be refilled
+                if (diag) {
 #pragma unroll
-                        for (int e = 0; e < kBlk; ++e)
-                            if (e > lim) sv[e] = 0xff800000u;
-                    }
-                    if (pass == 0) {
-                        float m8[8];
+                    for (int e = 0; e < kBlk; ++e)
+                        if (e > lim) sv[e] = 0xff800000u;
+                }
+                if (pass0) {
+                    float m8[8];
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) m8[i] = fmaxf(__uint_as_float(sv[i]), __uint_as_float(sv[8 + i]));
+                    for (int i8 = 0; i8 < 8; ++i8) m8[i8] = fmaxf(__uint_as_float(sv[i8]), __uint_as_float(sv[8 + i8]));
 #pragma unroll
-                        for (int e = 16; e < kBlk; e += 16)
+                    for (int e = 16; e < kBlk; e += 16)
 #pragma unroll
-                            for (int i = 0; i < 8; ++i)
-                                m8[i] = fmaxf(m8[i], fmaxf(__uint_as_float(sv[e + i]), __uint_as_float(sv[e + 8 + i])));
-                        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * sl2;
-                        const float m_new = fmaxf(m, mx);
-                        // row sum on MUFU.EX2 (an FMA-pipe polynomial for 2-8 of every 8 pairs was measured
-                        // slower: scripts/capture_poly.sh at configs 1/2)
-                        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+                        for (int i8 = 0; i8 < 8; ++i8)
+                            m8[i8] = fmaxf(m8[i8], fmaxf(__uint_as_float(sv[e + i8]), __uint_as_float(sv[e + 8 + i8])));
+                    const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                           fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) * sl2;
+                    const float m_new = fmaxf(m, mx);
+                    // row sum on MUFU.EX2 (an FMA-pipe polynomial for 2-8 of every 8 pairs was measured
+                    // slower: scripts/capture_poly.sh at configs 1/2)
+                    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+                    if (!diag) {
 #pragma unroll
                         for (int e = 0; e < kBlk; ++e) s4[e & 3] += ex2(fmaf(__uint_as_float(sv[e]), sl2, -m_new));
                         l = l * ex2(m - m_new) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
                         m = m_new;
-                        if (diag) off = m + lg2(l);  // P = exp2(s*sl2 - off)
                     } else {
-                        // this block's columns [128j, 128j + 128) that the row stores
-                        const int c0 = j * kBlk;
-                        const int ncols = min(kBlk, stored - c0);
+                        // p = exp2(s * sl2 - m_new) once, row sum, then P = p / l for this block
+#pragma unroll
+                        for (int e = 0; e < kBlk; ++e) {
+                            const float pe = ex2(fmaf(__uint_as_float(sv[e]), sl2, -m_new));
+                            sv[e] = __float_as_uint(pe);
+                            s4[e & 3] += pe;
+                        }
+                        l = l * ex2(m - m_new) + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
+                        m = m_new;
+                        off = m + lg2(l);  // pass 1: P = exp2(s * sl2 - off)
+                        const float inv = 1.f / l;
 #pragma unroll
                         for (int c = 0; c < kBlk / 32; ++c) {
                             uint32_t w[16];
 #pragma unroll
-                            for (int e = 0; e < 16; ++e) {
-                                const float p0 = ex2(fmaf(__uint_as_float(sv[c * 32 + 2 * e]), sl2, -off));
-                                const float p1 = ex2(fmaf(__uint_as_float(sv[c * 32 + 2 * e + 1]), sl2, -off));
-                                if (bf16) {
-                                    __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                                    w[e] = *reinterpret_cast<uint32_t *>(&h2);
-                                } else {
-                                    __half2 h2 = __floats2half2_rn(p0, p1);
-                                    w[e] = *reinterpret_cast<uint32_t *>(&h2);
-                                }
-                            }
-                            uint4 *dst = (uint4 *)(mrow + c0 + c * 32);
-#if defined(CAP_EXP) && CAP_EXP == 1  // experiment: no map stores
-                            if (w[0] == 0x12345678u && w[15] == 0x9abcdef0u) dst[0] = make_uint4(w[1], w[2], w[3], w[4]);
-#else
-#pragma unroll
-                            for (int pc = 0; pc < 4; ++pc)
-                                if (c * 32 + pc * 8 < ncols) dst[pc] = make_uint4(w[4 * pc], w[4 * pc + 1], w[4 * pc + 2], w[4 * pc + 3]);
-#endif
+                            for (int e = 0; e < 16; ++e)
+                                w[e] = pack(__uint_as_float(sv[c * 32 + 2 * e]) * inv, __uint_as_float(sv[c * 32 + 2 * e + 1]) * inv);
+                            store_chunk(mrow, qb * kBlk, c, stored, w);
                         }
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < kBlk / 32; ++c) {
+                        uint32_t w[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            w[e] = pack(ex2(fmaf(__uint_as_float(sv[c * 32 + 2 * e]), sl2, -off)),
+                                        ex2(fmaf(__uint_as_float(sv[c * 32 + 2 * e + 1]), sl2, -off)));
+                        store_chunk(mrow, j * kBlk, c, stored, w);
                     }
                 }
             }
@@ -282,10 +317,21 @@ cudaError_t launch(const CaptureArgs &a, int sm_count, cudaStream_t st) {
     if (e == cudaSuccess)
         e = make_tmap_2d_16(&tk, a.K, bf16, kD, (uint64_t)a.max_rows * a.L * a.Hkv * a.S, (uint64_t)kD * 2, 64, kBlk, 128);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(capture_tc_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    e = cudaFuncSetAttribute(capture_tc_kernel<kD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(capture_tc_kernel<kD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     const uint32_t idesc = idesc_f16(kBlk, kBlk, bf16 ? 1u : 0u, 0u, 0u);
-    capture_tc_kernel<kD><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, a, idesc);
+    // units whose K fills ~48 MB of L2 form a group (both passes re-read it)
+    const ItemSched sc = ItemSched::make((uint32_t)a.S, (uint32_t)a.L, (uint32_t)a.H, (uint32_t)a.Hkv, kBlk,
+                                         (uint32_t)a.S * kD * 2u);
+    // map stores with an L2 evict_first policy from S = 512 on: there a unit's K (re-read by all its query
+    // blocks, in both passes) stays in L2 for long, and the streamed maps would push it out (configs[3]:
+    // 2.44 -> 2.19 ms); at S <= 256 the plain store is faster (configs 1 / 2: 0.275 -> 0.250, 0.584 -> 0.551 ms)
+    if (a.S >= 512)
+        capture_tc_kernel<kD, true><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, a, sc, idesc);
+    else
+        capture_tc_kernel<kD, false><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, a, sc, idesc);
     count_launches(1);
     return cudaGetLastError();
 }
