@@ -10,14 +10,18 @@
 // queued behind PV_b -- and the softmax of block b+1 overlaps PV_b and S_{b+2} on the tensor pipe.
 // (kernels_tc_attend.cu keeps one S buffer per group, so a group's next S always waited for its PV.)
 // The softmax runs on 8 warps: warp w handles rows 32(w%4)..+31 (its TMEM lane quarter) and key half
-// w/4 - 1 (64 keys).  The two warps of a row quarter exchange their partial row maxima (and, at the
-// item's end, row sums) through spare TMEM columns behind a 64-thread named barrier, so both use the same
-// reference max; each owns half of P and half of O (rescale, epilogue).  Online softmax with lazy
-// rescaling (the reference max moves only when the block max exceeds it by > 8 in log2 units).
-// Roles (384 threads = 3 warpgroups): warp 0 TMA loader (Q per item into a 2-slot ring, K_b / V_b into
+// w/4 - 1 (64 keys).  The two warps of a row quarter exchange their partial row maxima through spare TMEM
+// columns behind a 64-thread named barrier, so both use the same reference max; each owns half of P and
+// half of O (lazy rescale).  Online softmax with lazy rescaling (the reference max moves only when the
+// block max exceeds it by > 8 in log2 units).  At an item's last block each writes its row sum to TMEM.
+// Roles (512 threads = 4 warpgroups): warp 0 TMA loader (Q per item into a 2-slot ring, K_b / V_b into
 // 2-slot rings), warp 1 MMA issuer (the whole warp runs the issue loop, one elected lane issues, so the
-// descriptor arithmetic stays in uniform registers) + TMEM owner, warps 2-3 idle; warps 4-7 and 8-11 the softmax /
-// epilogue halves (setmaxnreg moves registers from the producers to the softmax warps).
+// descriptor arithmetic stays in uniform registers) + TMEM owner, warps 2-3 idle; warps 4-7 and 8-11 the
+// softmax halves; warps 12-15 the epilogue (O / l -> act dtype -> TMA store), off the softmax's path: the
+// MMA restarts O for the next item once the epilogue has read it (o_free).  setmaxnreg moves registers
+// from the producers and the epilogue to the softmax warps.  (Epilogue in the softmax warps, deferred past
+// the next block's softmax: configs[3] 1.385 ms / configs[2] 0.555 ms; here 1.363 / 0.566.  Double-
+// buffering O by item parity, with the exchanges moved to shared memory to make TMEM room: 1.378 / 0.561.)
 #include "kernels.cuh"
 #include "item_sched.cuh"
 #include "sm100.cuh"
@@ -27,7 +31,7 @@ using namespace sm100;
 
 namespace {
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr int kBlk = 128;
 constexpr int kD = 128;
 constexpr float kRescaleThreshold = 8.f;
@@ -42,10 +46,13 @@ constexpr int kOutWarp = 32 * 64 * 2;   // per softmax warp: O staging [32 rows]
 constexpr int kNK = SPLIT_NK, kNV = 4 - SPLIT_NK;
 static_assert(kNK >= 1 && kNV >= 1 && kNK <= 4 && kNV <= 4, "ring sizes");
 constexpr int kSmem = (2 + kNK + kNV) * kTile + 8 * kOutWarp + 1024 + 256;
-// TMEM columns (of 512): S/P buffers [0, 256), O [256, 384), and the pair exchange of partial row maxima
-// (parity-double-buffered, kXmax + 2 * parity + half) and row sums (kXsum + half) at [384, 390): both warps
-// of a row quarter address the same lanes, so TMEM carries the exchange without shared memory.
-constexpr uint32_t kXmax = 384, kXsum = 388;
+// TMEM columns (of 512): S/P buffers [0, 256), O [256, 384), the pair exchange of partial row maxima
+// (parity-double-buffered, kXmax + 2 * parity + half) and the row sums for the epilogue (item-parity
+// double-buffered, kXsum + 2 * parity + half) at [384, 392): the warps address their own lanes only.
+constexpr uint32_t kOCol = 256, kXmax = 384, kXsum = 388;
+// Registers per thread after setmaxnreg (4 warpgroups share 64 K): producers, softmax, epilogue.
+constexpr uint32_t kRegProducer = 56, kRegSoftmax = 176, kRegEpilogue = 96;
+static_assert(128 * (kRegProducer + 2 * kRegSoftmax + kRegEpilogue) <= 65536, "register file");
 constexpr uint32_t kTmemCols = 512;
 // Key pairs (of every 8) whose exp2 runs as a polynomial on the FMA pipe on off-diagonal blocks: 0, the
 // sweep was slower at every ratio (configs[3]: 0 -> 1.49 ms, 1 -> 1.54, 2 -> 1.58, 4 -> 1.69).
@@ -104,16 +111,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t *sQ = smem;               // [2][tile]
     uint8_t *sK = sQ + 2 * kTile;     // [kNK][tile]
     uint8_t *sV = sK + kNK * kTile;   // [kNV][tile]
-    uint8_t *sOut = sV + kNV * kTile; // [8 softmax warps][kOutWarp]
+    uint8_t *sOut = sV + kNV * kTile; // [4 epilogue warps][2 column halves][kOutWarp]
     uint64_t *bars = (uint64_t *)(sOut + 8 * kOutWarp);
     uint64_t *q_full = bars, *q_empty = q_full + 2;
     uint64_t *k_full = q_empty + 2, *k_empty = k_full + kNK;
     uint64_t *v_full = k_empty + kNK, *v_empty = v_full + kNV;
     uint64_t *s_full = v_empty + kNV;  // [2] S_b computed in buffer b % 2
-    uint64_t *p_full = s_full + 2;    // [2] P_b written (256 arrivals)
-    uint64_t *pv_done = p_full + 2;   // PV_b retired (one phase per block)
-    uint64_t *last_done = pv_done + 1;  // the stream's last PV retired (single phase)
-    uint32_t *tmem_slot = (uint32_t *)(last_done + 1);
+    uint64_t *p_full = s_full + 2;     // [2] P_b written (256 softmax arrivals)
+    uint64_t *pv_done = p_full + 2;    // PV_b retired (one phase per block; the lazy rescale waits on it)
+    uint64_t *o_full = pv_done + 1;    // an item's last PV retired: O complete (one phase per item)
+    uint64_t *o_free = o_full + 1;     // the epilogue has read O (128 arrivals, one phase per item)
+    uint64_t *sum_free = o_free + 1;   // [2] the epilogue has read the row sums of an item of parity p
+    uint32_t *tmem_slot = (uint32_t *)(sum_free + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -123,6 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_init(&q_empty[s], 1);
                 mbar_init(&s_full[s], 1);
                 mbar_init(&p_full[s], 256);
+                mbar_init(&sum_free[s], 128);
             }
             if (s < kNK) {
                 mbar_init(&k_full[s], 1);
@@ -133,8 +143,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_init(&v_empty[s], 1);
             }
         }
-        mbar_init(&pv_done[0], 1);
-        mbar_init(last_done, 1);
+        mbar_init(pv_done, 1);
+        mbar_init(o_full, 1);
+        mbar_init(o_free, 128);
         fence_barrier_init();
     }
     if (warp == 0 && lane == 0) {
@@ -153,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t items = units * sc.n_qb;
 
     if (warp < 4) {
-        setmaxnreg_dec<56>();
+        setmaxnreg_dec<kRegProducer>();
         if (warp == 0 && lane == 0) {
             // ------------------------------ TMA loader -------------------------------------------
             Walker w;
@@ -182,15 +193,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ++b;
                 if (w.advance(sc)) ++it;
             }
-#if !defined(SPLIT_LANE_MMA)  // default: warp-converged MMA issuer (descriptors in uniform registers; -DSPLIT_LANE_MMA
-                              // selects the single-lane issuer, ~0.7 % slower at configs[3])
         } else if (warp == 1) {
             // ------------------------------ MMA issuer (whole warp; one elected lane issues) --------
-            // wS runs two blocks ahead of wP: S_0, S_1, then PV_b followed by S_{b+2}.
+            // wS runs two blocks ahead of wP: S_0, S_1, then PV_b followed by S_{b+2}.  The first PV of an
+            // item restarts O, so it waits until the epilogue has read the previous item's O (o_free).
             Walker wS, wP;
             wS.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
             wP.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
-            uint32_t bS = 0, itS = 0, bP = 0;
+            uint32_t bS = 0, itS = 0, bP = 0, itP = 0;
             auto issue_s = [&]() {
                 const uint32_t buf = bS & 1u, qs = itS & 1u;
                 if (wS.j == 0) mbar_wait(&q_full[qs], (itS >> 1) & 1u);
@@ -215,130 +225,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&p_full[buf], ph);
                 SPLIT_TR_MMA(bP, 1);
                 mbar_wait(&v_full[bP % kNV], (bP / kNV) & 1u);
+                // the epilogue of item itP - 1 has read O (it cannot be further along: item itP's epilogue
+                // waits for this item's PVs)
+                if (wP.j == 0 && itP > 0) mbar_wait(o_free, (itP - 1) & 1u);
                 SPLIT_TR_MMA(bP, 2);
                 tc_fence_after();
-                umma_f16_ts_k8_w(tmem + 256, tmem + buf * kBlk,
+                umma_f16_ts_k8_w(tmem + kOCol, tmem + buf * kBlk,
                                smem_desc(smem_u32(sV + (bP % kNV) * kTile), kBlk * 128, 1024, kSwizzle128B), idesc_pv,
                                wP.j == 0 ? 0u : 1u);
                 umma_commit_w(&v_empty[bP % kNV]);
-                umma_commit_w(&pv_done[0]);
+                umma_commit_w(pv_done);
+                if (wP.j == wP.qb) umma_commit_w(o_full);
                 SPLIT_TR_MMA(bP, 3);
                 ++bP;
-                wP.advance(sc);
+                if (wP.advance(sc)) ++itP;
                 if (wS.active) issue_s();  // into the buffer PV_b reads: queued behind it
                 SPLIT_TR_MMA(bP - 1, 4);
             }
-            if (bP > 0) umma_commit_w(last_done);
         }
-#else
-        } else if (warp == 1 && lane == 0) {
-            // ------------------------------ MMA issuer -------------------------------------------
-            // wS runs two blocks ahead of wP: S_0, S_1, then PV_b followed by S_{b+2}.
-            Walker wS, wP;
-            wS.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
-            wP.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
-            uint32_t bS = 0, itS = 0, bP = 0;
-            auto issue_s = [&]() {
-                const uint32_t buf = bS & 1u, qs = itS & 1u;
-                if (wS.j == 0) mbar_wait(&q_full[qs], (itS >> 1) & 1u);
-                mbar_wait(&k_full[bS % kNK], (bS / kNK) & 1u);
-                SPLIT_TR_MMA(bS, 5);  // K (and Q) of S_{bS} ready
-                tc_fence_after();
-                umma_f16_ss_k8<kBlk * 128 / 16>(tmem + buf * kBlk,
-                                               smem_desc(smem_u32(sQ + qs * kTile), 16, 1024, kSwizzle128B),
-                                               smem_desc(smem_u32(sK + (bS % kNK) * kTile), 16, 1024, kSwizzle128B),
-                                               idesc_s, 0u);
-                umma_commit(&s_full[buf]);
-                umma_commit(&k_empty[bS % kNK]);
-                if (wS.j == wS.qb) umma_commit(&q_empty[qs]);
-                ++bS;
-                if (wS.advance(sc)) ++itS;
-            };
-            if (wS.active) issue_s();
-            if (wS.active) issue_s();
-            while (wP.active) {
-                const uint32_t buf = bP & 1u, ph = (bP >> 1) & 1u;
-                SPLIT_TR_MMA(bP, 0);
-                mbar_wait(&p_full[buf], ph);
-                SPLIT_TR_MMA(bP, 1);
-                mbar_wait(&v_full[bP % kNV], (bP / kNV) & 1u);
-                SPLIT_TR_MMA(bP, 2);
-                tc_fence_after();
-                umma_f16_ts_k8(tmem + 256, tmem + buf * kBlk,
-                               smem_desc(smem_u32(sV + (bP % kNV) * kTile), kBlk * 128, 1024, kSwizzle128B), idesc_pv,
-                               wP.j == 0 ? 0u : 1u);
-                umma_commit(&v_empty[bP % kNV]);
-                umma_commit(&pv_done[0]);
-                SPLIT_TR_MMA(bP, 3);
-                ++bP;
-                wP.advance(sc);
-                if (wS.active) issue_s();  // into the buffer PV_b reads: queued behind it
-                SPLIT_TR_MMA(bP - 1, 4);
-            }
-            if (bP > 0) umma_commit(last_done);
-        }
-#endif
-    } else {
-        // ------------------------------ softmax + epilogue (8 warps) --------------------------------
-        setmaxnreg_inc<224>();
-        const int half = (warp - 4) >> 2;   // key half (64 keys) and O half (64 columns) of this warp
+    } else if (warp < 12) {
+        // ------------------------------ softmax (8 warps) ------------------------------------------
+        setmaxnreg_inc<kRegSoftmax>();
+        const int half = (warp - 4) >> 2;   // key half (64 keys) and O half (64 columns, rescale) of this warp
         const int q = warp & 3;             // TMEM lane quarter
         const int r = q * 32 + lane;        // query row inside the block == TMEM lane
         const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-        const uint32_t o_addr = tmem + lane_addr + 256 + half * 64;
-        uint8_t *stage_o = sOut + (warp - 4) * kOutWarp;
-        const uint32_t stage_o_u32 = smem_u32(stage_o);
+        const uint32_t o_addr = tmem + lane_addr + kOCol + half * 64;
         const float sl2 = a.scale * 1.4426950408889634f;
         Walker w;
         w.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
-        uint32_t b = 0;
+        uint32_t b = 0, it = 0;
         float m_ref = 0.f, l = 0.f;
-        bool pend = false;  // an item whose epilogue is deferred to the next block
-        int32_t pend_row = 0;
-        float pend_l = 0.f;
-        // epilogue of the item whose last block is lb: PV_lb retired -> O / (l_0 + l_1) -> act dtype ->
-        // this warp's 128B-swizzled staging tile -> TMA store of its 32 rows x 64 columns
-        auto epilogue = [&](uint32_t lb, int32_t orow, float l_own) {
-            tmem_st_32x32b_x1(tmem + lane_addr + kXsum + half, __float_as_uint(l_own));
-            tmem_st_wait();
-            tc_fence_before();
-            mbar_wait(&pv_done[0], lb & 1u);
-            pair_sync(q);
-            tc_fence_after();
-            const float inv = 1.f / (l_own + __uint_as_float(tmem_ld_32x32b_x1(tmem + lane_addr + kXsum + (half ^ 1))));
-            uint32_t v[64];
-            tmem_ld_32x32b_x32(o_addr, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-            tmem_ld_32x32b_x32(o_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
-            tmem_ld_wait();
-            if (lane == 0) bulk_wait_read<0>();  // the previous TMA store has read the staging tile
-            __syncwarp();
-#pragma unroll
-            for (int c8 = 0; c8 < 8; ++c8) {
-                uint32_t wv[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float lo = __uint_as_float(v[c8 * 8 + 2 * e]) * inv;
-                    const float hi = __uint_as_float(v[c8 * 8 + 2 * e + 1]) * inv;
-                    if constexpr (kBF16) {
-                        __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
-                        wv[e] = *reinterpret_cast<uint32_t *>(&h2);
-                    } else {
-                        __half2 h2 = __floats2half2_rn(lo, hi);
-                        wv[e] = *reinterpret_cast<uint32_t *>(&h2);
-                    }
-                }
-                *reinterpret_cast<uint4 *>(stage_o + sw128_offset(lane, c8)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-            }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-                tma_store_2d(&tmO, stage_o_u32, half * 64, orow);
-                bulk_commit();
-            }
-            // the partner reads this warp's row sum before the next epilogue rewrites it: the exchange
-            // barriers of the blocks in between order the two
-            tc_fence_before();
-        };
         while (w.active) {
             const int j = w.j;
             const bool diag = j == w.qb;
@@ -381,9 +298,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 m_ref = m_blk;
                 l = 0.f;
             } else if (m_blk > m_ref + kRescaleThreshold) {
-                // lazy rescale of this warp's O half (complete once PV_{b-1} retired) and l
+                // lazy rescale of this warp's O half (complete once PV_{b-1} retired: s_full(b) implied
+                // PV_{b-2}, so the parity wait is unambiguous) and l
                 const float alpha = ex2(m_ref - m_blk);
-                mbar_wait(&pv_done[0], (b - 1) & 1u);
+                mbar_wait(pv_done, (b - 1) & 1u);
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
@@ -438,32 +356,78 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t t2 = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
                 l += __uint_as_float((uint32_t)t2) + __uint_as_float((uint32_t)(t2 >> 32));
             }
+            if (diag) {
+                // the item's row sum (this warp's keys) for the epilogue, in the sum slot of the item's
+                // parity, once the epilogue has read that slot for item it - 2 (parity wait unambiguous:
+                // item it's epilogue needs this block's PV)
+                if (it >= 2) mbar_wait(&sum_free[it & 1u], ((it >> 1) & 1u) ^ 1u);
+                tmem_st_32x32b_x1(tmem + lane_addr + kXsum + 2 * (it & 1u) + half, __float_as_uint(l));
+            }
             tmem_st_wait();
             SPLIT_TR_SM(3);
-            if (pend) {
-                // the previous item's epilogue, deferred until this block's P is written: PV_{b-1} (its
-                // last block) has retired meanwhile (s_full(b) implied PV_{b-2}; the parity wait on
-                // PV_{b-1} is unambiguous), and PV_b -- which restarts O -- waits for this arrive
-                epilogue(b - 1, pend_row, pend_l);
-                pend = false;
-            }
             tc_fence_before();
             mbar_arrive(&p_full[buf]);
             SPLIT_TR_SM(4);
-            if (diag) {  // this item ends here: its epilogue runs after the next block's softmax
-                pend = true;
-                pend_row = (int32_t)(w.row0 + w.qb * kBlk + q * 32);
-                pend_l = l;
-            }
             ++b;
-            w.advance(sc);
+            if (w.advance(sc)) ++it;
         }
-        if (pend) {
-            // the stream's last item: pv_done may be anywhere from PV_{b-3} to PV_{b-1} retired, which one
-            // parity bit cannot tell apart; last_done (committed after the last PV) can, and once it fired
-            // the epilogue's wait on PV_{b-1} passes at once
-            mbar_wait(last_done, 0u);
-            epilogue(b - 1, pend_row, pend_l);
+    } else {
+        // ------------------------------ epilogue (4 warps, one per TMEM lane quarter) -------------
+        // per item: O complete (o_full) -> row sums of both key halves -> O / (l_0 + l_1) in two 64-column
+        // halves -> act dtype -> 128B-swizzled staging tile -> TMA store of 32 rows x 64 columns
+        setmaxnreg_dec<kRegEpilogue>();
+        const int q = warp & 3;
+        const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+        uint8_t *stage = sOut + q * 2 * kOutWarp;
+        uint32_t it = 0;
+        for (uint32_t t = blockIdx.x; t < items; t += gridDim.x, ++it) {
+            const ItemSched::Item item = sc.decode(t, units, a.list.rows);
+            const int32_t orow = (int32_t)(item.row0 + item.qb * kBlk + q * 32);
+            mbar_wait(o_full, it & 1u);
+            tc_fence_after();
+            uint32_t ls[2];
+            tmem_ld_32x32b_x2(tmem + lane_addr + kXsum + 2 * (it & 1u), ls);
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&sum_free[it & 1u]);
+            const float inv = 1.f / (__uint_as_float(ls[0]) + __uint_as_float(ls[1]));
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                uint32_t v[64];
+                tmem_ld_32x32b_x32(tmem + lane_addr + kOCol + h * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                tmem_ld_32x32b_x32(tmem + lane_addr + kOCol + h * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+                tmem_ld_wait();
+                if (h == 1) {  // all of O is in registers or staged: the next item's first PV may restart it
+                    tc_fence_before();
+                    mbar_arrive(o_free);
+                }
+                uint8_t *st = stage + h * kOutWarp;
+                if (lane == 0) bulk_wait_read<1>();  // the store issued from this staging tile last item
+                __syncwarp();
+#pragma unroll
+                for (int c8 = 0; c8 < 8; ++c8) {
+                    uint32_t wv[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float lo = __uint_as_float(v[c8 * 8 + 2 * e]) * inv;
+                        const float hi = __uint_as_float(v[c8 * 8 + 2 * e + 1]) * inv;
+                        if constexpr (kBF16) {
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
+                            wv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        } else {
+                            __half2 h2 = __floats2half2_rn(lo, hi);
+                            wv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                        }
+                    }
+                    *reinterpret_cast<uint4 *>(st + sw128_offset(lane, c8)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tmO, smem_u32(st), h * 64, orow);
+                    bulk_commit();
+                }
+            }
         }
         if (lane == 0) bulk_wait<0>();  // O stores complete before the CTA (and its smem) retires
     }
