@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t lh;
         int64_t row, ent;
         while (iter.next(lh, row, ent)) {
+            AC_STRESS_DELAY(809u);
             const int l = (int)(lh / a.H), h = (int)(lh % a.H);
             const __nv_bfloat16 *A = maps + ((ent * a.L + a.layer_begin + l) * a.H + h) * a.map_stride + c * 8;
             for (int rb = 0; rb < n_rb; ++rb) {
@@ -186,6 +187,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t lh;
             int64_t row, ent;
             while (iter.next(lh, row, ent)) {
+                AC_STRESS_DELAY(574u);
+                AC_STRESS_DELAY(66u);
                 // V head of map head h under grouped-query attention: h / (H / Hkv) (Hkv = H for MHA)
                 const uint32_t l = lh / (uint32_t)a.H, h = lh % (uint32_t)a.H;
                 const int32_t vrow0 = (int32_t)(((row * a.n_lay + l) * a.Hkv + h / (uint32_t)(a.H / a.Hkv)) * S);
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             uint32_t cnt = 0, item = 0;
             for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+                AC_STRESS_DELAY(426u);
                 for (int rb = 0; rb < n_rb; ++rb, ++item) {
                     const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;
                     mbar_wait(&tempty[acc], aph ^ 1u);

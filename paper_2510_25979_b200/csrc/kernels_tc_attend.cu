@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t q_s = smem_u32(sQ + g * C::kTile), k_s = smem_u32(sK + g * C::kTile);
                 const uint32_t v_s = smem_u32(sV + g * C::kTile);
                 while (st.active) {
+                    AC_STRESS_DELAY(137u);
                     const int32_t r_j = (int32_t)(st.kv_row0 + st.j * kBlk);
                     if (st.j == 0) {
                         mbar_wait(&q_empty[g], (it & 1u) ^ 1u);
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t v_b = smem_u32(sV + g * C::kTile);
                 const uint32_t s_t = tmem + g * kBlk, o_t = tmem + 256 + g * kD;
                 while (st.active) {
+                    AC_STRESS_DELAY(17u);
                     const int j = st.j;
                     ATT_TRACE_MMA(b * 2 + g, 0);
                     if (j == 0) mbar_wait(&q_full[g], it & 1u);
@@ -298,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t b = 0;  // key blocks of this stream
         float m_ref = 0.f, l = 0.f;
         while (s.active) {
+            AC_STRESS_DELAY(818u);
             const int j = s.j;
             const bool diag = j == s.qb;
             const int lim = diag ? r : kBlk - 1;            // keys k <= lim are visible (causal mask)

@@ -171,6 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             w.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
             uint32_t b = 0, it = 0;
             while (w.active) {
+                AC_STRESS_DELAY(716u);
+                AC_STRESS_DELAY(178u);
                 if (w.j == 0) {
                     const uint32_t qs = it & 1u;
                     mbar_wait(&q_empty[qs], ((it >> 1) & 1u) ^ 1u);
@@ -220,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (wS.active) issue_s();
             if (wS.active) issue_s();
             while (wP.active) {
+                AC_STRESS_DELAY(146u);
                 const uint32_t buf = bP & 1u, ph = (bP >> 1) & 1u;
                 SPLIT_TR_MMA(bP, 0);
                 mbar_wait(&p_full[buf], ph);
@@ -381,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t *stage = sOut + q * 2 * kOutWarp;
         uint32_t it = 0;
         for (uint32_t t = blockIdx.x; t < items; t += gridDim.x, ++it) {
+            AC_STRESS_DELAY(99u);
             const ItemSched::Item item = sc.decode(t, units, a.list.rows);
             const int32_t orow = (int32_t)(item.row0 + item.qb * kBlk + q * 32);
             mbar_wait(o_full, it & 1u);

@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol_k = kCapKPol == 2 ? policy_evict_last() : kCapKPol == 1 ? policy_evict_normal() : policy_evict_first();
             uint32_t it = 0, blk = 0;
             for (uint32_t t = blockIdx.x + g * gridDim.x; t < items; t += stride, ++it) {
+                AC_STRESS_DELAY(390u);
                 const ItemSched::Item item = sc.decode(t, units, a.list.rows);
                 const int qb = item.qb;
                 const uint32_t qph = it & 1u;
@@ -210,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             return *reinterpret_cast<uint32_t *>(&h2);
         };
         for (uint32_t t = blockIdx.x + g * gridDim.x; t < items; t += stride) {
+            AC_STRESS_DELAY(312u);
             const ItemSched::Item item = sc.decode(t, units, a.list.rows);
             const int qb = item.qb;
             const int R = qb * kBlk + r;  // this thread's query row in the unit

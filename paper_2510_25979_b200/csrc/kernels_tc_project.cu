@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             uint32_t cnt = 0;
             for (int64_t t = blockIdx.x; t < items; t += gridDim.x) {
+                AC_STRESS_DELAY(719u);
                 const int32_t mt = (int32_t)(t % n_mt), nt = (int32_t)(t / n_mt);
                 for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
                     const uint32_t s = cnt % kStages, ph = (cnt / kStages) & 1u;
@@ -97,6 +98,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             uint32_t cnt = 0, item = 0;
             for (int64_t t = blockIdx.x; t < items; t += gridDim.x, ++item) {
+                AC_STRESS_DELAY(446u);
+                AC_STRESS_DELAY(165u);
                 const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;
                 mbar_wait(&tempty[acc], aph ^ 1u);
                 tc_fence_after();

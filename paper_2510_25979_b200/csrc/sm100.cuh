@@ -384,6 +384,28 @@ __device__ __forceinline__ void exp2_poly2(uint64_t x2, float &p0, float &p1) {
     p1 = __uint_as_float((uint32_t)(q2 >> 32) + ((uint32_t)(t2 >> 32) << 23));
 }
 
+// ---- schedule stress (verification builds only) ---------------------------------------------------
+// With -DAC_STRESS every role loop of the persistent kernels starts with a pseudo-random, warp-uniform
+// __nanosleep of up to ~4 us on one iteration in four, so the roles drift against each other far more
+// than in a normal run.  Arithmetic is untouched: a stress build must give bitwise the same outputs as
+// the normal one, and finish (tests/test_gpu_stress.py).  Catches mbarrier parity waits that could see
+// a barrier two phases ahead, and missing waits that only a slow producer or consumer exposes.
+#if defined(AC_STRESS)
+__device__ __forceinline__ void stress_delay(uint32_t site) {
+    uint32_t x = (uint32_t)clock() * 2654435761u ^ (site * 0x9e3779b9u) ^ (blockIdx.x << 12) ^ (threadIdx.x >> 5);
+    x = __shfl_sync(__activemask(), x, __ffs(__activemask()) - 1);  // warp-uniform
+    x ^= x >> 13;
+    x *= 0x5bd1e995u;
+    x ^= x >> 15;
+    if ((x & 3u) == 0u) __nanosleep((x >> 18) & 4095u);
+}
+#define AC_STRESS_DELAY(site) ::ac::sm100::stress_delay(site)
+#else
+#define AC_STRESS_DELAY(site) \
+    do {                      \
+    } while (0)
+#endif
+
 // ---- division by a launch-time constant ------------------------------------------------------------
 // n / d for 32-bit n as (umulhi(n, m) + n) >> s with s = ceil(log2 d), m = 2^32 (2^s - d) / d + 1
 // (the sum taken in 64 bits); the magic is made on the host, so the per-item index arithmetic of the
