@@ -188,7 +188,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             int64_t row, ent;
             while (iter.next(lh, row, ent)) {
                 AC_STRESS_DELAY(574u);
-                AC_STRESS_DELAY(66u);
                 // V head of map head h under grouped-query attention: h / (H / Hkv) (Hkv = H for MHA)
                 const uint32_t l = lh / (uint32_t)a.H, h = lh % (uint32_t)a.H;
                 const int32_t vrow0 = (int32_t)(((row * a.n_lay + l) * a.Hkv + h / (uint32_t)(a.H / a.Hkv)) * S);
@@ -252,6 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t lh;
         int64_t row, ent;
         while (iter.next(lh, row, ent)) {
+            AC_STRESS_DELAY(66u);
             const int64_t orow_unit = (row * per_row + lh) * S;  // first O row of the unit
             for (int rb = 0; rb < n_rb; ++rb, ++item) {
                 const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;

@@ -172,7 +172,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t b = 0, it = 0;
             while (w.active) {
                 AC_STRESS_DELAY(716u);
-                AC_STRESS_DELAY(178u);
                 if (w.j == 0) {
                     const uint32_t qs = it & 1u;
                     mbar_wait(&q_empty[qs], ((it >> 1) & 1u) ^ 1u);
@@ -260,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t b = 0, it = 0;
         float m_ref = 0.f, l = 0.f;
         while (w.active) {
+            AC_STRESS_DELAY(178u);
             const int j = w.j;
             const bool diag = j == w.qb;
             const uint32_t buf = b & 1u;

@@ -99,7 +99,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t cnt = 0, item = 0;
             for (int64_t t = blockIdx.x; t < items; t += gridDim.x, ++item) {
                 AC_STRESS_DELAY(446u);
-                AC_STRESS_DELAY(165u);
                 const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;
                 mbar_wait(&tempty[acc], aph ^ 1u);
                 tc_fence_after();
@@ -123,6 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r = q * 32 + lane;
         uint32_t item = 0;
         for (int64_t t = blockIdx.x; t < items; t += gridDim.x, ++item) {
+            AC_STRESS_DELAY(165u);
             const int64_t mt = t % n_mt, nt = t / n_mt;
             const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;
             mbar_wait(&tfull[acc], aph);

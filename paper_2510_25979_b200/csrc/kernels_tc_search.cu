@@ -96,7 +96,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t cnt = 0, item = 0;
             for (int64_t t = blockIdx.x; t < items; t += gridDim.x, ++item) {
                 AC_STRESS_DELAY(781u);
-                AC_STRESS_DELAY(490u);
                 const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;
                 mbar_wait(&tempty[acc], aph ^ 1u);
                 tc_fence_after();
@@ -120,6 +119,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r = q * 32 + lane;
         uint32_t item = 0;
         for (int64_t t = blockIdx.x; t < items; t += gridDim.x, ++item) {
+            AC_STRESS_DELAY(490u);
             const int64_t qt = t % n_qt, et = t / n_qt;
             const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;
             mbar_wait(&tfull[acc], aph);
