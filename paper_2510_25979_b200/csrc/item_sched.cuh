@@ -43,7 +43,7 @@ struct ItemSched {
         int qb;           // query block
     };
 
-    __device__ __forceinline__ Item decode(uint32_t t, uint32_t units, const int32_t *rows) const {
+    __host__ __device__ __forceinline__ Item decode(uint32_t t, uint32_t units, const int32_t *rows) const {
         Item it;
         const uint32_t gi = gq.div(t), w = t - gi * gq.d;
         const uint32_t gbase = gi * group;

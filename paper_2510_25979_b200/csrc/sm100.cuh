@@ -417,10 +417,15 @@ struct FastDiv {
         while ((1ull << s) < d) ++s;
         m = (uint32_t)((((1ull << 32) * ((1ull << s) - d)) / d) + 1);
     }
-    __device__ __forceinline__ uint32_t div(uint32_t n) const {
-        return (uint32_t)(((uint64_t)__umulhi(n, m) + n) >> s);
+    __host__ __device__ __forceinline__ uint32_t div(uint32_t n) const {
+#if defined(__CUDA_ARCH__)
+        const uint32_t hi = __umulhi(n, m);
+#else
+        const uint32_t hi = (uint32_t)(((uint64_t)n * m) >> 32);
+#endif
+        return (uint32_t)(((uint64_t)hi + n) >> s);
     }
-    __device__ __forceinline__ uint32_t mod(uint32_t n) const { return n - div(n) * d; }
+    __host__ __device__ __forceinline__ uint32_t mod(uint32_t n) const { return n - div(n) * d; }
 };
 
 // ---- descriptors ----------------------------------------------------------------------------------
