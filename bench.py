@@ -504,8 +504,9 @@ def _rows_activations(cfg, kind, rows, dev):
 
 def run_dist(args, cfg):
     """N > 1 (torchrun, one process per GPU, NCCL): the DB is sharded by contiguous entry ranges,
-    each rank is home to a contiguous block of the query batch; same global data at every N (strong
-    scaling).  One step = sharded search (query all-gather, local top-1, key all-gather + max), then
+    each rank is home to a contiguous block of the query batch: the config's batch per GPU by default
+    (--scaling weak: per-GPU work fixed, global batch B * N against the same DB), or the config's batch
+    split over the GPUs (--scaling strong: same global data at every N).  One step = sharded search (query all-gather, local top-1, key all-gather + max), then
 
       --placement affinity (default; SURVEY.md §8(e) owner-affinity): every query is placed once on the
         rank that processes all its layers (hits on the owner of their entry, misses greedily on the
@@ -668,9 +669,9 @@ def main(argv=None):
     ap.add_argument("--no-search-sweep", action="store_true", help="skip the configs[4] search-QPS sweep")
     ap.add_argument("--placement", default="affinity", choices=["affinity", "routed"],
                     help="N > 1: owner-affinity placement (default) or the literal V->owner / O->home routing")
-    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
-                    help="N > 1: the config's global batch split over the GPUs (strong, default) or the config's batch "
-                         "on every GPU (weak)")
+    ap.add_argument("--scaling", default="weak", choices=["strong", "weak"],
+                    help="N > 1: the config's batch on every GPU against the same sharded DB (weak, default: a serving "
+                         "box answers N times the requests) or the config's global batch split over the GPUs (strong)")
     ap.add_argument("--tau", type=float, default=None, help="override the config's threshold (not for bench lines)")
     ap.add_argument("--hit-rate", type=float, default=None, help="override the config's planted hit rate")
     ap.add_argument("--batch", type=int, default=None, help="override the config's query batch")

@@ -274,6 +274,27 @@ attncache_status attncache_affinity_plan(const int64_t *idx, const uint8_t *hit,
                                          const int64_t *shard_begins, int32_t world, double hit_cost,
                                          double miss_cost, int32_t *assign, double *load);
 
+/* The same plan on the DEVICE, plus one rank's relocation lists, so the placement costs no host round
+ * trip beyond the counts NCCL's all_to_all needs (one kernel launch of one CTA on `stream`).  assign and
+ * load are bitwise those of attncache_affinity_plan (the per-rank loads are the same sequential sums).
+ * Inputs: idx, hit: device [n_rows] (the whole batch; every rank passes the same); shard_begins,
+ * home_begins: HOST [world + 1] (home_begins: the batch positions of each rank's home block, 0 .. n_rows);
+ * world in [1, 32]; rank: this rank.  Outputs (device, caller-allocated): assign int32 [n_rows];
+ * load double [world]; loc int64 [n_rows] (the positions placed on `rank`, ascending: the first n_loc
+ * entries); idx_loc int64 / hit_loc uint8 [n_rows] (their idx, 0 for misses, and hit flags); send_order
+ * int64 [home size] (this rank's home rows, home-relative, stably sorted by destination rank);
+ * counts int32 [2 world + 1] = send_n[world] | recv_n[world] | n_loc.  A hit idx outside
+ * [shard_begins[0], shard_begins[world]) is placed on rank 0 or world - 1 (the host function rejects it).
+ * Scratch: n_rows int64 from ctx.  Errors: INVALID_ARGUMENT (world outside [1, 32], rank outside
+ * [0, world), NULL arrays, begins not non-decreasing, home_begins not spanning [0, n_rows], NaN or
+ * negative costs), OUT_OF_MEMORY, CUDA. */
+attncache_status attncache_affinity_plan_device(attncache_ctx *ctx, const int64_t *idx, const uint8_t *hit,
+                                                int64_t n_rows, const int64_t *shard_begins, int32_t world,
+                                                double hit_cost, double miss_cost, int32_t rank,
+                                                const int64_t *home_begins, int32_t *assign, double *load,
+                                                int64_t *loc, int64_t *idx_loc, uint8_t *hit_loc,
+                                                int64_t *send_order, int32_t *counts, void *stream);
+
 /* ---- DB building: packed map layout (Fig. 4 step 3) -----------
  * Number of elements one PACKED S x S map occupies (0 if S % 8 != 0). */
 int64_t attncache_packed_map_elems(int32_t seq_len);

@@ -26,7 +26,7 @@ __all__ = [
     "attncache_scatter_rows", "attncache_fetch_maps", "attncache_variant", "attncache_version", "attncache_launch_count",
     "attncache_packed_map_elems", "attncache_pack_maps", "pack_db_maps", "attncache_capture_maps", "attncache_rope",
     "attncache_affinity_plan", "attncache_project_features", "attncache_apply_cached_gqa", "attncache_attend_full_gqa",
-    "attncache_capture_maps_gqa", "ABI_FUNCTIONS",
+    "attncache_capture_maps_gqa", "attncache_affinity_plan_device", "ABI_FUNCTIONS",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -41,6 +41,7 @@ ABI_FUNCTIONS = [
     "attncache_variant", "attncache_launch_count", "attncache_packed_map_elems", "attncache_pack_maps",
     "attncache_capture_maps", "attncache_rope", "attncache_affinity_plan", "attncache_project_features",
     "attncache_apply_cached_gqa", "attncache_attend_full_gqa", "attncache_capture_maps_gqa",
+    "attncache_affinity_plan_device",
 ]
 
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -103,6 +104,8 @@ def load_library():
         "attncache_apply_cached_gqa": ([P, P, P, I64, I32, I32, I32, I32, I32, P, P, P], I32),
         "attncache_attend_full_gqa": ([P, I64, I32, I32, I32, I32, I32, I32, P, P, P, F32, P, P, P], I32),
         "attncache_capture_maps_gqa": ([P, I64, I32, I32, I32, I32, I32, I32, P, P, F32, P, I32, I32, P, P], I32),
+        "attncache_affinity_plan_device": ([P, P, P, I64, P, I32, ctypes.c_double, ctypes.c_double, I32, P, P, P, P, P,
+                                            P, P, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -448,6 +451,42 @@ def attncache_rope(X: torch.Tensor, base: float = 10000.0, stream=None) -> torch
     _check(load_library().attncache_rope(_p(X), X.numel() // (S * d), S, d, _DT[X.dtype], float(base),
                                          _stream(stream, X.device)))
     return X
+
+
+def attncache_affinity_plan_device(ctx: "Context", idx: torch.Tensor, hit: torch.Tensor, shard_begins, home_begins,
+                                   rank: int, hit_cost: float = 1.0, miss_cost: float = 1.0, stream=None):
+    """Owner-affinity placement on the device (include/attncache.h attncache_affinity_plan_device): the plan of
+    attncache_affinity_plan, bitwise, plus this rank's relocation lists.  idx int64 / hit uint8 on the device
+    ([n], the whole batch); shard_begins, home_begins: host sequences [world + 1].  Returns a dict of device
+    tensors assign (int32 [n]), load (float64 [world]), loc / idx_loc (int64 [n]), hit_loc (uint8 [n]),
+    send_order (int64 [home size]) and counts (int32 [2 world + 1] = send_n | recv_n | n_loc)."""
+    import numpy as np
+    _dev(idx, "idx")
+    _dev(hit, "hit")
+    sb = np.ascontiguousarray(list(shard_begins), dtype=np.int64)
+    hb = np.ascontiguousarray(list(home_begins), dtype=np.int64)
+    world = sb.shape[0] - 1
+    n = idx.shape[0]
+    if idx.dtype != torch.int64 or hit.dtype != torch.uint8 or hit.shape[0] != n:
+        raise ValueError("affinity_plan_device: idx int64 [n], hit uint8 [n]")
+    if hb.shape[0] != world + 1:
+        raise ValueError("affinity_plan_device: home_begins must have world + 1 entries")
+    dev = idx.device
+    home = int(hb[rank + 1] - hb[rank]) if 0 <= rank < world else 0
+    out = {"assign": torch.empty(n, dtype=torch.int32, device=dev),
+           "load": torch.empty(max(world, 1), dtype=torch.float64, device=dev),
+           "loc": torch.empty(n, dtype=torch.int64, device=dev), "idx_loc": torch.empty(n, dtype=torch.int64, device=dev),
+           "hit_loc": torch.empty(n, dtype=torch.uint8, device=dev),
+           "send_order": torch.empty(max(home, 1), dtype=torch.int64, device=dev),
+           "counts": torch.zeros(2 * max(world, 1) + 1, dtype=torch.int32, device=dev)}
+    p = lambda t: ctypes.c_void_p(t.data_ptr()) if t.numel() else None  # noqa: E731
+    _check(load_library().attncache_affinity_plan_device(
+        ctx.handle, p(idx.contiguous()), p(hit.contiguous()), n, ctypes.c_void_p(sb.ctypes.data), world,
+        float(hit_cost), float(miss_cost), int(rank), ctypes.c_void_p(hb.ctypes.data), p(out["assign"]),
+        p(out["load"]), p(out["loc"]), p(out["idx_loc"]), p(out["hit_loc"]), p(out["send_order"]),
+        p(out["counts"]), _stream(stream, dev)))
+    out["send_order"] = out["send_order"][:home]
+    return out
 
 
 def attncache_affinity_plan(idx, hit, shard_begins, hit_cost: float = 1.0, miss_cost: float = 1.0):

@@ -156,6 +156,7 @@ attncache_status attncache_ctx_destroy(attncache_ctx *ctx) {
     cudaFree(ctx->attend_list.ptr);
     cudaFree(ctx->search_keys.ptr);
     cudaFree(ctx->project_buf.ptr);
+    cudaFree(ctx->plan_buf.ptr);
     delete ctx;
     return ATTNCACHE_OK;
 }
@@ -576,6 +577,41 @@ attncache_status attncache_affinity_plan(const int64_t *idx, const uint8_t *hit,
     }
     if (load)
         for (int r = 0; r < world; ++r) load[r] = acc[r];
+    return ATTNCACHE_OK;
+}
+
+attncache_status attncache_affinity_plan_device(attncache_ctx *ctx, const int64_t *idx, const uint8_t *hit, int64_t n,
+                                                const int64_t *sb, int32_t world, double hit_cost, double miss_cost,
+                                                int32_t rank, const int64_t *hb, int32_t *assign, double *load,
+                                                int64_t *loc, int64_t *idx_loc, uint8_t *hit_loc, int64_t *send_order,
+                                                int32_t *counts, void *stream) {
+    if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan_device: ctx is NULL");
+    if (n < 0 || world <= 0 || world > ac::kPlanMaxWorld || rank < 0 || rank >= world)
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan_device: n=%lld world=%d rank=%d (world <= %d)",
+                    (long long)n, world, rank, ac::kPlanMaxWorld);
+    if (!sb || !hb || !load || !counts || (n > 0 && (!idx || !hit || !assign || !loc || !idx_loc || !hit_loc || !send_order)))
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan_device: NULL argument");
+    if (!(hit_cost >= 0.0) || !(miss_cost >= 0.0))
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan_device: costs must be non-negative numbers");
+    if (hb[0] != 0 || hb[world] != n)
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan_device: home_begins must span [0, n_rows]");
+    for (int r = 0; r < world; ++r)
+        if (sb[r + 1] < sb[r] || hb[r + 1] < hb[r])
+            return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan_device: begins decreasing at %d", r);
+    DeviceGuard g(ctx->device);
+    attncache_status s = ensure_scratch(ctx->plan_buf, (size_t)std::max<int64_t>(n, 1) * sizeof(int64_t));
+    if (s) return s;
+    ac::PlanArgs a;
+    a.world = world;
+    a.rank = rank;
+    a.hit_cost = hit_cost;
+    a.miss_cost = miss_cost;
+    for (int r = 0; r <= world; ++r) {
+        a.shard_begins[r] = sb[r];
+        a.home_begins[r] = hb[r];
+    }
+    AC_CUDA(ac::launch_affinity_plan(idx, hit, n, a, assign, load, (int64_t *)ctx->plan_buf.ptr, loc, idx_loc, hit_loc,
+                                     send_order, counts, (cudaStream_t)stream));
     return ATTNCACHE_OK;
 }
 

@@ -98,6 +98,7 @@ struct attncache_ctx {
     ac::Scratch attend_list; // compacted row list for attend
     ac::Scratch search_keys; // per-query keys for single-rank search
     ac::Scratch project_buf; // feature projector intermediates (z, y)
+    ac::Scratch plan_buf;    // device affinity plan: the miss list
 };
 
 struct attncache_db {

@@ -95,6 +95,18 @@ struct ProjectArgs {
     void *f;              // [M][D] in feat_dt
 };
 bool linear_tc_supported(int32_t dt, int32_t K, int32_t Nout);
+
+// ---- owner-affinity placement on the device (kernels_plan.cu) ----
+constexpr int kPlanMaxWorld = 32;
+struct PlanArgs {
+    int32_t world, rank;
+    double hit_cost, miss_cost;
+    int64_t shard_begins[kPlanMaxWorld + 1];
+    int64_t home_begins[kPlanMaxWorld + 1];
+};
+cudaError_t launch_affinity_plan(const int64_t *idx, const uint8_t *hit, int64_t n, const PlanArgs &a, int32_t *assign,
+                                 double *load, int64_t *scratch, int64_t *loc, int64_t *idx_loc, uint8_t *hit_loc,
+                                 int64_t *send_order, int32_t *counts, cudaStream_t st);
 cudaError_t launch_project(const ProjectArgs &a, int sm_count, cudaStream_t st);
 
 // ---- RoPE (f4 block-level comparison) ----

@@ -31,7 +31,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import (Context, Database, attncache_affinity_plan, attncache_apply_cached, attncache_attend_full,
+from . import (Context, Database, attncache_affinity_plan, attncache_affinity_plan_device, attncache_apply_cached, attncache_attend_full,
                attncache_gather_rows, attncache_keys_decode, attncache_route_plan, attncache_scatter_rows,
                attncache_search_keys)
 
@@ -69,6 +69,9 @@ class CudaOps:
 
     def apply_cached_masked(self, idx, hit, V, O, layer_begin=0, layer_end=None):
         return attncache_apply_cached(self.db, idx, V, O, hit=hit, layer_begin=layer_begin, layer_end=layer_end)
+
+    def affinity_plan_device(self, idx, hit, shard_begins, home_begins, rank, hit_cost, miss_cost):
+        return attncache_affinity_plan_device(self.ctx, idx, hit, shard_begins, home_begins, rank, hit_cost, miss_cost)
 
     def attend_full(self, Q, K, V, O, skip):
         return attncache_attend_full(self.ctx, Q, K, V, O, skip=skip)
@@ -166,9 +169,10 @@ class AffinityPrefill(ShardedPrefill):
     hit_cost / miss_cost weight the greedy miss placement (attncache_affinity_plan); callers pass the
     algorithmic HBM bytes of one query's A.V and of one query's attention.
 
-    Host work per batch is one small D2H (the decoded top-1 of every query, misses as -1), the C
-    placement, and one small H2D (this rank's relocation order and its local idx/hit), so the GPU idles
-    only for the host's planning between the search and the local layer work."""
+    With the product's ops (CudaOps, world <= 32) the placement runs on the device
+    (attncache_affinity_plan_device, bitwise the host plan) and only the all_to_all counts come back
+    (one small D2H).  Otherwise (the gloo reference ops): one small D2H of the decoded top-1 of every
+    query, the C host placement, and one small H2D of this rank's relocation order and local idx/hit."""
 
     def __init__(self, ops, n_global: int, tau: float, hit_cost: float = 1.0, miss_cost: float = 1.0,
                  group=None, device="cuda"):
@@ -182,6 +186,18 @@ class AffinityPrefill(ShardedPrefill):
         (numpy int32[B], the processing rank of every query), the home sizes, the per-rank loads, and
         this rank's local queries with their idx/hit on the device."""
         idx, score, hit, sizes = self.search_all(q_home, sizes)
+        if hasattr(self.ops, "affinity_plan_device") and self.world <= 32:
+            # the plan on the device (bitwise the host plan); only the all_to_all counts come back
+            home_begins = np.cumsum([0] + list(sizes)).tolist()
+            out = self.ops.affinity_plan_device(idx, hit, self._sb_host.tolist(), home_begins, self.rank,
+                                                self.hit_cost, self.miss_cost)
+            counts = out["counts"].tolist()                                                      # one small D2H
+            w = self.world
+            n_loc = counts[2 * w]
+            return {"idx": idx, "score": score, "hit": hit, "assign": out["assign"], "sizes": sizes,
+                    "load": out["load"], "loc": out["loc"][:n_loc], "send_order": out["send_order"],
+                    "send_n": counts[:w], "recv_n": counts[w:2 * w], "idx_loc": out["idx_loc"][:n_loc],
+                    "hit_loc": out["hit_loc"][:n_loc]}
         code = torch.where(hit.bool(), idx, torch.full_like(idx, -1)).cpu().numpy()            # one D2H
         hit_h = (code >= 0).astype(np.uint8)
         assign, load = attncache_affinity_plan(np.maximum(code, 0), hit_h, self._sb_host, self.hit_cost,
@@ -204,7 +220,7 @@ class AffinityPrefill(ShardedPrefill):
 
     def local_queries(self, plan) -> torch.Tensor:
         """Global batch positions this rank processes, ascending (int64, CPU)."""
-        return plan["loc"]
+        return plan["loc"].cpu()
 
     def relocate(self, rows_home: torch.Tensor, plan) -> torch.Tensor:
         """Moves each home row (one query's request state, e.g. its hidden states [S][E]) to the rank

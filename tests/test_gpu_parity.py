@@ -900,3 +900,42 @@ def test_edge_cases_empty_skipped_and_extreme_shapes(ac, ctx):
     off = [(((b * cfg.L + l) * cfg.H + h) * cfg.S * 32) for b, l, h in units]
     ref = oracle.attend(storage(Q32), storage(K32), storage(V32), cfg.act_dtype, off, cfg.S, 32)
     check_close(_gather_units(A32, units), ref, torch.bfloat16, "attend d=32")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 3, 8, 32])
+def test_affinity_plan_device_matches_host(ac, ctx, world):
+    """attncache_affinity_plan_device: assign and load bitwise equal to the host plan (exact ties, zero costs,
+    empty shards and empty home blocks included), and every rank's lists equal to the ones derived from the
+    host plan the way dist.AffinityPrefill does on the host path."""
+    g = np.random.default_rng(100 + world)
+    costs = [(1.0, 1.0), (2.0, 1.5), (0.0, 1.0), (1.0, 0.0), (0.0, 0.0), (3.3e6, 1.7e7)]
+    for trial in range(12):
+        n = int(g.choice([0, 1, 7, 300, 2048, 5000]))
+        N = int(g.integers(world, 20000))
+        cuts = np.sort(g.integers(0, N, world - 1)).tolist() if world > 1 else []
+        sb = [0] + cuts + [N]
+        hcuts = np.sort(g.integers(0, n + 1, world - 1)).tolist() if world > 1 else []
+        hb = [0] + hcuts + [n]
+        idx = g.integers(0, N, n).astype(np.int64)
+        hit = (g.random(n) < float(g.choice([0.0, 0.5, 0.8, 1.0]))).astype(np.uint8)
+        hc, mc = costs[trial % len(costs)]
+        assign_h, load_h = ac.attncache_affinity_plan(idx, hit, sb, hc, mc)
+        idx_d, hit_d = torch.from_numpy(idx).to(DEV), torch.from_numpy(hit).to(DEV)
+        for rank in sorted({0, world - 1, int(g.integers(0, world))}):
+            out = ac.attncache_affinity_plan_device(ctx, idx_d, hit_d, sb, hb, rank, hc, mc)
+            torch.cuda.synchronize()
+            assert np.array_equal(out["assign"].cpu().numpy(), assign_h), (world, trial, rank)
+            assert np.array_equal(out["load"][:world].cpu().numpy(), load_h), (world, trial, rank)
+            counts = out["counts"].cpu().tolist()
+            loc = np.nonzero(assign_h == rank)[0]
+            mine = assign_h[hb[rank]:hb[rank + 1]].astype(np.int64)
+            assert counts[:world] == np.bincount(mine, minlength=world).tolist()
+            assert counts[world:2 * world] == [int((assign_h[hb[s]:hb[s + 1]] == rank).sum()) for s in range(world)]
+            assert counts[2 * world] == loc.shape[0]
+            assert np.array_equal(out["loc"][:loc.shape[0]].cpu().numpy(), loc)
+            assert np.array_equal(out["idx_loc"][:loc.shape[0]].cpu().numpy(), np.where(hit[loc] == 1, idx[loc], 0))
+            assert np.array_equal(out["hit_loc"][:loc.shape[0]].cpu().numpy(), hit[loc])
+            assert np.array_equal(out["send_order"].cpu().numpy(), np.argsort(mine, kind="stable"))
+    with pytest.raises(ac.AttnCacheError):
+        ac.attncache_affinity_plan_device(ctx, idx_d[:0], hit_d[:0], list(range(34)), [0] * 34, 0)  # world 33
