@@ -293,6 +293,15 @@ attncache_status attncache_search(attncache_db *db, const void *queries, int64_t
 
 // ---- apply ----------------------------------------------------------------------------------
 
+#if defined(SM_EXPERIMENT)  // experiment: per-call CTA counts from the environment
+static int sm_override(const char *name, int def) {
+    const char *v = getenv(name);
+    return v && atoi(v) > 0 ? atoi(v) : def;
+}
+#else
+static inline int sm_override(const char *, int def) { return def; }
+#endif
+
 attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
                                         int32_t layer_begin, int32_t layer_end, int32_t head_dim, int32_t act_dtype,
                                         const void *V, void *O, void *stream) {
@@ -347,7 +356,7 @@ attncache_status attncache_apply_cached_gqa(attncache_db *db, const int64_t *idx
     a.max_rows = n_rows;
     AC_CUDA(launch_select_apply(idx, hit, n_rows, d.shard_begin, d.shard_count, a.list, db->ctx->d_error, st));
     if (apply_tc_supported(d.map_dtype, act_dtype, d.seq_len, head_dim)) {
-        AC_CUDA(launch_apply_tc(a, db->ctx->sm_count, st));
+        AC_CUDA(launch_apply_tc(a, sm_override("AC_APPLY_SMS", db->ctx->sm_count), st));
     } else {
         AC_CUDA(launch_apply_ffma(a, db->ctx->sm_count, st));
     }
@@ -399,7 +408,7 @@ attncache_status attncache_attend_full_gqa(attncache_ctx *ctx, int64_t batch, in
     a.max_rows = batch;
     AC_CUDA(launch_select_attend(skip, batch, a.list, st));
     if (attend_tc_supported(act_dtype, S, dd)) {
-        AC_CUDA(launch_attend_tc(a, ctx->sm_count, st));
+        AC_CUDA(launch_attend_tc(a, sm_override("AC_ATTEND_SMS", ctx->sm_count), st));
     } else {
         AC_CUDA(launch_attend_ffma(a, ctx->sm_count, st));
     }
