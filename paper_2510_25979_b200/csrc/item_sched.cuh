@@ -16,7 +16,8 @@ namespace ac {
 
 struct ItemSched {
     uint32_t group, n_qb, per_row, S, L, Hkv;
-    sm100::FastDiv gq, grp, per_row_d, h_d, hq_d;  // group * n_qb, group, L * H, H, H / Hkv
+    uint32_t rotate = 0;  // wave order (make_wave): query-block levels rotate by group index
+    sm100::FastDiv gq, grp, per_row_d, h_d, hq_d, qb_d;  // group * n_qb, group, L * H, H, H / Hkv, n_qb
 
     // unit_bytes: L2 bytes one unit keeps live (its K and V, or K alone); blk: query block rows
     __host__ static ItemSched make(uint32_t S, uint32_t L, uint32_t H, uint32_t Hkv, uint32_t blk, uint32_t unit_bytes) {
@@ -32,6 +33,19 @@ struct ItemSched {
         c.per_row_d = sm100::FastDiv(c.per_row);
         c.h_d = sm100::FastDiv(H);
         c.hq_d = sm100::FastDiv(H / Hkv);
+        c.qb_d = sm100::FastDiv(c.n_qb);
+        return c;
+    }
+
+    // Wave order: a group holds as many items as there are item streams (one wave), so the streams work on
+    // few units at a time (their K/V stay in L2 across the query blocks); the query-block level of a
+    // stream's item rotates from group to group, so every stream gets every level in turn.
+    __host__ static ItemSched make_wave(uint32_t S, uint32_t L, uint32_t H, uint32_t Hkv, uint32_t blk, uint32_t streams) {
+        ItemSched c = make(S, L, H, Hkv, blk, 1u << 30);
+        c.group = std::max(1u, streams / c.n_qb);
+        c.gq = sm100::FastDiv(c.group * c.n_qb);
+        c.grp = sm100::FastDiv(c.group);
+        c.rotate = 1;
         return c;
     }
 
@@ -48,15 +62,17 @@ struct ItemSched {
         const uint32_t gi = gq.div(t), w = t - gi * gq.d;
         const uint32_t gbase = gi * group;
         uint32_t u;
+        uint32_t a;
         if (gbase + group <= units) {
-            const uint32_t a = grp.div(w);
-            it.qb = (int)(n_qb - 1 - a);
+            a = grp.div(w);
             u = gbase + (w - a * group);
         } else {  // the last, partial group
             const uint32_t gsize = units - gbase;
-            it.qb = (int)(n_qb - 1 - w / gsize);
+            a = w / gsize;
             u = gbase + w % gsize;
         }
+        if (rotate) a = qb_d.mod(a + qb_d.mod(gi));
+        it.qb = (int)(n_qb - 1 - a);
         const uint32_t ri = per_row_d.div(u);
         it.lh = u - ri * per_row;
         it.row = rows[ri];

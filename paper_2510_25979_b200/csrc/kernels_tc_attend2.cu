@@ -459,8 +459,12 @@ cudaError_t launch_t(const AttendArgs &a, int sm_count, cudaStream_t st) {
     const uint32_t idesc_s = idesc_f16(kBlk, kBlk, fmt, 0u, 0u);  // Q K-major x K K-major
     const uint32_t idesc_pv = idesc_f16(kBlk, kD, fmt, 0u, 1u);   // P (TMEM) x V MN-major
     // units whose K and V fill ~48 MB of L2 form a group
-    const ItemSched sc = ItemSched::make((uint32_t)a.S, (uint32_t)a.L, (uint32_t)a.H, (uint32_t)a.Hkv, kBlk,
-                                         2u * (uint32_t)a.S * kD * 2u);
+    // wave order (item_sched.cuh): the sm_count item streams work on few units at a time, so a unit's K/V
+    // blocks, re-read by each of its query blocks, stay in L2 (configs[2] 13 rows 0.566 -> 0.532 ms, all
+    // 128 rows 5.53-5.68 -> 5.18-5.41, configs[3] 1.364 -> 1.349 against L2-sized unit groups in
+    // heaviest-first order)
+    const ItemSched sc = ItemSched::make_wave((uint32_t)a.S, (uint32_t)a.L, (uint32_t)a.H, (uint32_t)a.Hkv, kBlk,
+                                              (uint32_t)sm_count);
     attend_split_kernel<kBF16><<<sm_count, kThreads, kSmem, st>>>(tq, tk, tv, to, a, sc, idesc_s, idesc_pv);
     count_launches(1);
     return cudaGetLastError();

@@ -48,9 +48,10 @@ static int check_fastdiv() {
     return 0;
 }
 
-// S, L, H, Hkv, n_rows, unit_bytes
-static int check_sched(uint32_t S, uint32_t L, uint32_t H, uint32_t Hkv, uint32_t n_rows, uint32_t unit_bytes) {
-    const ItemSched sc = ItemSched::make(S, L, H, Hkv, 128, unit_bytes);
+// S, L, H, Hkv, n_rows, unit_bytes (wave: streams, for ItemSched::make_wave)
+static int check_sched(uint32_t S, uint32_t L, uint32_t H, uint32_t Hkv, uint32_t n_rows, uint32_t unit_bytes,
+                       uint32_t wave = 0) {
+    const ItemSched sc = wave ? ItemSched::make_wave(S, L, H, Hkv, 128, wave) : ItemSched::make(S, L, H, Hkv, 128, unit_bytes);
     std::vector<int32_t> rows(n_rows);
     for (uint32_t i = 0; i < n_rows; ++i) rows[i] = (int32_t)(3 * i + 1);  // a selected-row list (distinct rows)
     const uint32_t units = n_rows * L * H, items = units * sc.n_qb;
@@ -72,7 +73,7 @@ static int check_sched(uint32_t S, uint32_t L, uint32_t H, uint32_t Hkv, uint32_
             last_group = g;
             last_qb = 1 << 30;
         }
-        if (it.qb > last_qb) return fail("heaviest first", t, it.qb, last_qb);
+        if (!sc.rotate && it.qb > last_qb) return fail("heaviest first", t, it.qb, last_qb);
         last_qb = it.qb;
     }
     for (size_t i = 0; i < seen.size(); ++i)
@@ -90,6 +91,9 @@ int main() {
     bad |= check_sched(384, 2, 8, 2, 7, 2 * 384 * 128 * 2);
     bad |= check_sched(8192, 1, 4, 1, 3, 2 * 8192 * 128 * 2);
     bad |= check_sched(256, 3, 6, 3, 5, 40u << 20);  // groups of one unit
+    bad |= check_sched(1024, 8, 32, 32, 16, 0, 296);  // wave order (capture: two streams per CTA)
+    bad |= check_sched(1024, 8, 32, 32, 16, 0, 148);
+    bad |= check_sched(384, 2, 8, 2, 7, 0, 148);
     std::printf(bad ? "item_sched_check FAILED\n" : "item_sched_check ok\n");
     return bad;
 }
