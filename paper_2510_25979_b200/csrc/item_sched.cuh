@@ -45,7 +45,7 @@ struct ItemSched {
         c.group = std::max(1u, streams / c.n_qb);
         c.gq = sm100::FastDiv(c.group * c.n_qb);
         c.grp = sm100::FastDiv(c.group);
-        c.rotate = 1;
+        c.rotate = c.n_qb > 1 ? 1u : 0u;  // one query block per unit: the plain unit order
         return c;
     }
 

@@ -328,8 +328,13 @@ cudaError_t launch(const CaptureArgs &a, int sm_count, cudaStream_t st) {
     // wave order (item_sched.cuh): the 2 x sm_count item streams work on few units at a time, so the K
     // blocks both passes re-read stay in L2 (configs 2 / 3: 0.556 -> 0.547, 2.194 -> 2.156 ms against
     // L2-sized unit groups in heaviest-first order)
+#if defined(CAP_GROUPS)  // experiment: L2-sized unit groups, heaviest first
+    const ItemSched sc = ItemSched::make((uint32_t)a.S, (uint32_t)a.L, (uint32_t)a.H, (uint32_t)a.Hkv, kBlk,
+                                         (uint32_t)a.S * kD * 2u);
+#else
     const ItemSched sc = ItemSched::make_wave((uint32_t)a.S, (uint32_t)a.L, (uint32_t)a.H, (uint32_t)a.Hkv, kBlk,
                                               2u * (uint32_t)sm_count);
+#endif
     // map stores with an L2 evict_first policy from S = 512 on: there a unit's K (re-read by all its query
     // blocks, in both passes) stays in L2 for long, and the streamed maps would push it out (configs[3]:
     // 2.44 -> 2.19 ms); at S <= 256 the plain store is faster (configs 1 / 2: 0.275 -> 0.250, 0.584 -> 0.551 ms)
