@@ -463,8 +463,12 @@ cudaError_t launch_t(const AttendArgs &a, int sm_count, cudaStream_t st) {
     // blocks, re-read by each of its query blocks, stay in L2 (configs[2] 13 rows 0.566 -> 0.532 ms, all
     // 128 rows 5.53-5.68 -> 5.18-5.41, configs[3] 1.364 -> 1.349 against L2-sized unit groups in
     // heaviest-first order)
+#ifndef ATT_WAVE_STREAMS_X4
+#define ATT_WAVE_STREAMS_X4 4  // wave size in quarters of the stream count (2 / 8 / 16 measured: configs[2]
+                                // 0.703 / 0.533 / 0.544 ms against 0.529, configs[3] within 1 %)
+#endif
     const ItemSched sc = ItemSched::make_wave((uint32_t)a.S, (uint32_t)a.L, (uint32_t)a.H, (uint32_t)a.Hkv, kBlk,
-                                              (uint32_t)sm_count);
+                                              (uint32_t)sm_count * ATT_WAVE_STREAMS_X4 / 4);
     attend_split_kernel<kBF16><<<sm_count, kThreads, kSmem, st>>>(tq, tk, tv, to, a, sc, idesc_s, idesc_pv);
     count_launches(1);
     return cudaGetLastError();
