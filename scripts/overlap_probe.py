@@ -1,7 +1,7 @@
 """Step time at a config with apply_cached and attend_full on one stream (sequential, the bench's step) vs
 forked onto two streams after the search (the miss attention's CTAs fill SMs as the A.V kernel's retire).
 
-    python scripts/overlap_test.py [config] [steps]
+    python scripts/overlap_probe.py [config] [steps]
 """
 import os
 import sys

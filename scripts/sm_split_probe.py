@@ -1,7 +1,7 @@
 """Experiment: A.V (hits, HBM-bound) and miss attention (compute-bound at S = 1024) run concurrently on two
 streams with the SMs split between the two persistent kernels (library built with -DSM_EXPERIMENT, CTA
 counts from AC_APPLY_SMS / AC_ATTEND_SMS), against the sequential step.
-    ATTNCACHE_LIB=ab/smx.so python scripts/sm_split_test.py [config]"""
+    ATTNCACHE_LIB=ab/smx.so python scripts/sm_split_probe.py [config]"""
 import os
 import sys
 

@@ -139,11 +139,19 @@ def fill_maps(cfg: Config, out: torch.Tensor, begin: int, causal: bool = True) -
     n, S = out.shape[0], cfg.S
     dev = out.device
     upper = torch.triu(torch.ones(S, S, dtype=torch.bool, device=dev), diagonal=1)
-    for e in range(n):
-        z = torch.randn(cfg.L * cfg.H, S, S, generator=_gen(dev, cfg.seed, "map", begin + e), device=dev)
+    # logits are drawn per entry (its own generator); mask, softmax and the cast run on groups of entries
+    # (row-wise operations: the bytes do not depend on the grouping), bounded to ~256 MB of fp32 logits
+    per = cfg.L * cfg.H * S * S
+    group = max(1, min(n, (64 << 20) // max(per, 1)))
+    for e0 in range(0, n, group):
+        g = min(group, n - e0)
+        z = torch.empty(g, cfg.L * cfg.H, S, S, device=dev)
+        for e in range(g):
+            torch.randn(cfg.L * cfg.H, S, S, generator=_gen(dev, cfg.seed, "map", begin + e0 + e), device=dev,
+                        out=z[e])
         if causal:
             z.masked_fill_(upper, float("-inf"))
-        out[e].view(cfg.L * cfg.H, S, S).copy_(torch.softmax(z, dim=-1))
+        out[e0:e0 + g].view(g, cfg.L * cfg.H, S, S).copy_(torch.softmax(z, dim=-1))
     return out
 
 

@@ -161,16 +161,49 @@ def test_search_sharded_keys_equal_single_rank(ac, ctx):
     assert got[0][5].item() == 17
 
 
-def test_search_sweep_1m_sampled(ac, ctx):
+@pytest.fixture(scope="module")
+def sweep_db(ac, ctx):
+    """BASELINE.json configs[4]: 1M x 1024 bf16 features (2.05 GB), built once for the module."""
     cfg = synth.CONFIGS["search_sweep"]
     x = synth.features(cfg, 0, cfg.N, DEV)
-    db = ac.Database(ctx, x)
-    q, pos, tgt = synth.queries(cfg, DEV, B=1024)
+    return cfg, x, ac.Database(ctx, x)
+
+
+@pytest.mark.parametrize("B", [1, 64, 1024, 8192])
+def test_search_sweep_1m_sampled(ac, ctx, sweep_db, B):
+    """configs[4] at every batch the bench times (the full batch is searched in the bench's launch
+    configuration); min(B, 128) sampled queries, half planted hits and half misses, are checked against the
+    brute-force oracle over all 1M entries (>= 128 queries)."""
+    cfg, x, db = sweep_db
+    q, pos, tgt = synth.queries(cfg, DEV, B=B)
     idx, score, hit = ac.attncache_search(db, q, cfg.tau)
+    assert ac.attncache_variant("search", q.dtype, 0, cfg.D) == "tc"
     assert idx[pos].cpu().tolist() == tgt.tolist()        # planted hits find their entry
     assert hit[pos].all() and hit.sum().item() == len(pos)
-    sample = torch.cat([pos[:12], torch.nonzero(hit == 0).flatten()[:12].cpu()])
-    check_search(q[sample.to(DEV)], x, idx[sample.to(DEV)], score[sample.to(DEV)], hit[sample.to(DEV)], cfg.tau)
+    n = min(B, 128)
+    misses = torch.nonzero(hit == 0).flatten().cpu()
+    sample = torch.cat([pos[:n - min(n // 2, len(misses))], misses[:n // 2]])
+    assert len(sample) == n
+    s = sample.to(DEV)
+    check_search(q[s], x, idx[s], score[s], hit[s], cfg.tau)
+
+
+def test_search_mid_tile_and_simt_bf16(ac, ctx):
+    """The 128-entry tile of search_tc_kernel (N = 50,000 with B = 128: fewer than 2 work items per SM with
+    256-entry tiles, enough with 128) and the bf16 CUDA-core search (D = 200 is not a multiple of the
+    64-element tensor-core chunk), each against the oracle with planted cross-tile duplicates."""
+    for N, B, D in ((50_000, 128, 1024), (777, 33, 200)):
+        x = _normed(N, D, torch.bfloat16, 31)
+        q = _normed(B, D, torch.bfloat16, 32)
+        x[N - 5] = x[130]
+        x[257] = x[130]
+        q[0] = x[N - 5]
+        db = ac.Database(ctx, x)
+        idx, score, hit = ac.attncache_search(db, q, 0.9)
+        check_search(q, x, idx, score, hit, 0.9)
+        assert idx[0].item() == 130 and hit[0].item() == 1
+        want = "tc" if D % 64 == 0 else "ffma"
+        assert ac.attncache_variant("search", torch.bfloat16, 0, D) == want
 
 
 # ------------------------------------------------------------------------------------------------
@@ -818,6 +851,22 @@ def test_virtual_shards_routed_and_affinity_equal_single_gpu(ac, ctx, pattern):
     ctx.sync()
     assert torch.equal(O_routed, O_ref)
     assert torch.equal(O_aff, O_ref)
+    # ... and against the oracle: the sharded decisions, every hit unit (A.V with the owner's maps) and every
+    # miss unit (causal attention) of the routed result
+    check_search(q, x, idx, score, hit, cfg.tau)
+    dense = storage(synth.maps(cfg, 0, cfg.N, DEV))
+    ents = idx.cpu().numpy()
+    hits = torch.nonzero(hit).flatten().tolist()
+    misses = torch.nonzero(hit == 0).flatten().tolist()
+    if hits:
+        u = _units(hits, cfg.L, cfg.H)
+        ref_a = _apply_ref(dense, DT_NAME[maps.dtype], ents, storage(V), DT_NAME[V.dtype], u, cfg.L, cfg.H, cfg.S, cfg.d)
+        check_close(_gather_units(O_routed, u), ref_a, V.dtype, f"virtual shards apply {pattern}")
+    if misses:
+        u = _units(misses, cfg.L, cfg.H)
+        off = [(((b * cfg.L + l) * cfg.H + h) * cfg.S * cfg.d) for b, l, h in u]
+        ref_m = oracle.attend(storage(Q), storage(K), storage(V), DT_NAME[V.dtype], off, cfg.S, cfg.d)
+        check_close(_gather_units(O_routed, u), ref_m, V.dtype, f"virtual shards attend {pattern}")
     if pattern == "no_hits":
         assert int(hit.sum()) == 0
     if pattern == "one_shard":

@@ -372,6 +372,56 @@ def test_rope_pins():
     assert abs(Q[10] @ K[7] - Q[30] @ K[27]) < 1e-9 and abs(Q[5] @ K[5] - q.astype(np.float64) @ k) < 1e-9
 
 
+def test_rope_frequency_schedule_golden():
+    """The frequencies theta_i = base^(-2i/d) for i >= 1 (a wrong exponent such as base^(-i/d) passes every
+    invariant above): hand-computed angles of tests/golden/rope_theta.json."""
+    g = _gold("rope_theta.json")
+    for c in g["cases"]:
+        d, p, i = c["d"], c["p"], c["i"]
+        X = np.zeros((1, p + 1, d), np.float32)
+        X[0, :, i] = 1.0                                                        # e_i at every position
+        Y = oracle.rope(X, "f32", p + 1, d, base=c["base"])[0, p]
+        want = np.zeros(d)
+        want[i], want[i + d // 2] = c["cos"], c["sin"]
+        assert np.allclose(Y, want, atol=1e-12), (c, Y)
+
+
+# ----------------------------------------------------------------------------------------------
+# oracle_scores — the checker behind every near-tie search decision (tests/_util.py check_search)
+# ----------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_scores_equal_exact_rational_pairs(dtype):
+    """s[p] = q[qb[p]] . x[xi[p]]: exact rational inner products on pairs whose q and x row counts differ
+    (B = 5, N = 23), so swapping the roles of qb and xi, or of q and x, changes the value or the range."""
+    rng = np.random.default_rng(21)
+    B, N, D = 5, 23, 9
+    xf = rng.standard_normal((N, D)).astype(np.float32)
+    qf = (3.0 * rng.standard_normal((B, D))).astype(np.float32)   # a different scale than x
+    x = xf if dtype == "f32" else _bf16_bits(xf)
+    q = qf if dtype == "f32" else _bf16_bits(qf)
+    X = np.array(_exact(x, dtype), dtype=object).reshape(N, D)
+    Q = np.array(_exact(q, dtype), dtype=object).reshape(B, D)
+    qb = np.array([0, 4, 2, 2, 1, 3, 4], np.int64)
+    xi = np.array([22, 0, 7, 8, 19, 3, 11], np.int64)
+    s = oracle.scores(q, x, dtype, qb, xi)
+    for p in range(len(qb)):
+        want = sum(Q[qb[p], k] * X[xi[p], k] for k in range(D))
+        assert abs(s[p] - float(want)) <= 1e-12 * max(1.0, abs(float(want))), (p, s[p], float(want))
+    # consistency with the search: the score at the oracle's own top-1 / runner-up is s1 / s2
+    idx, s1, s2, _ = oracle.search(q, x, dtype, tau=0.0)
+    assert np.array_equal(oracle.scores(q, x, dtype, np.arange(B), idx), s1)
+    second = []
+    for b in range(B):
+        row = oracle.scores(q, x, dtype, np.full(N, b), np.arange(N))
+        order = np.argsort(-row, kind="stable")
+        second.append(row[order[1]])
+        assert order[0] == idx[b]
+    assert np.array_equal(np.array(second), s2)
+    with pytest.raises(IndexError):
+        oracle.scores(q, x, dtype, np.array([B]), np.array([0]))             # qb indexes q, not x
+
+
 # ----------------------------------------------------------------------------------------------
 # feature projector — Alg. 1 l.254 (PAPER.md:254), PAPER.md:278 two-layer MLP; readings R30-R32
 # ----------------------------------------------------------------------------------------------
