@@ -167,23 +167,40 @@ def oracle_step_sample(cfg, budget=2.5e9, seed=0):
     return t_search + t_apply + t_attend, desc, oracle.get_threads()
 
 
+def _line_config(cfg, n_hit=None, **extra):
+    """The full workload description carried by every line (ours and the reference arm)."""
+    d = {"workload": cfg.name, "bj_config_index": cfg.bj_index, "N": cfg.N, "D": cfg.D, "L": cfg.L, "H": cfg.H,
+         "S": cfg.S, "d": cfg.d, "B": cfg.B, "tau": cfg.tau, "planted_hit_rate": cfg.hit_rate, "seed": cfg.seed,
+         "feat_dtype": cfg.feat_dtype, "map_dtype": cfg.map_dtype, "act_dtype": cfg.act_dtype}
+    if n_hit is not None:
+        d["hits"] = n_hit
+    d.update(extra)
+    return d
+
+
 def run_reference(args, cfg):
+    """The reference arm of this paper-only tier: the CPU oracle (oracle/) timed as it stands on the host
+    cores, each step a bounded sample of one step of the workload, extrapolated to the full step (so the
+    line's ms_per_step is an extrapolation, flagged, while the wall time of the run stays a few minutes)."""
     rank, world, _ = _env_rank()
     if rank != 0:
         return 0
     import oracle
     oracle.set_threads(os.cpu_count() or 1)
-    times = []
+    times, walls = [], []
     for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         t, desc, cores = oracle_step_sample(cfg, seed=i)
         if i >= args.warmup:
             times.append(t)
+            walls.append(time.perf_counter() - t0)
     t = statistics.median(times)
     value = cfg.B * cfg.S / t
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "bj_config_index": cfg.bj_index, "B": cfg.B, "S": cfg.S},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth/, seed 0)",
+            "extrapolated": True, "sample_wall_s_per_step": statistics.median(walls),
+            "config": _line_config(cfg, cfg.n_hit, parallelism="CPU oracle (OpenMP over independent units)"),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -294,10 +311,7 @@ def run_ours(args, cfg):
     line = {"metric": METRIC, "value": cfg.B * cfg.S / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": cfg.act_dtype, "data": "synthetic (synth/, seed 0)",
-            "config": {"workload": cfg.name, "bj_config_index": cfg.bj_index, "N": cfg.N, "D": cfg.D, "L": cfg.L,
-                       "H": cfg.H, "S": cfg.S, "d": cfg.d, "B": cfg.B, "hits": n_hit, "tau": cfg.tau,
-                       "planted_hit_rate": cfg.hit_rate, "seed": cfg.seed,
-                       "parallelism": "single GPU", "l2": "inputs exceed L2 (no flush)"},
+            "config": _line_config(cfg, n_hit, parallelism="single GPU", l2="inputs exceed L2 (no flush)"),
             "speedup_vs_full_attention": {"batch": full_ms / ms, "per_hit_kernel": full_hits_ms / apply_ms,
                                           "full_attention_ms": full_ms, "paper_context": PAPER_CONTEXT},
             "search_qps": cfg.B / (search_ms * 1e-3),
@@ -316,16 +330,97 @@ def run_ours(args, cfg):
     del O_full
     # §8(f) f4: Eq. 5 block level (Q/K/V projections + RoPE + attention vs V projection + A.V)
     line["eq5_block"] = eq5_block(ac, ctx, db, cfg, idx, hit, stream, max(3, args.steps // 2))
+    if not args.no_target and cfg.name != "llama3_8b":
+        # north_star's target shape (>= 3x at Llama-3-8B shape: BASELINE.json configs[2], Table 4)
+        del step, db, maps, x, q, Q, K, V, O, idx, score, hit, hit_rows_only
+        torch.cuda.empty_cache()
+        line["north_star_target"] = target_config_block(args, ac, ctx, dev, stream, peaks, "llama3_8b")
     if not args.no_search_sweep:
         line["search_sweep"] = search_sweep(ac, ctx, dev, stream, max(3, args.steps), peaks)
     if not args.no_cpu_baseline:
         import oracle
         oracle.set_threads(os.cpu_count() or 1)
         t, desc, cores = oracle_step_sample(cfg)
+        oracle.set_threads(1)  # BASELINE.md's CPU plan: also at one thread (a smaller sample)
+        t1, desc1, _ = oracle_step_sample(cfg, budget=6e8)
+        oracle.set_threads(os.cpu_count() or 1)
         line["cpu_baseline"] = {"value": cfg.B * cfg.S / t, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                                "sample": desc}
+                                "sample": desc, "extrapolated": True,
+                                "one_thread": {"value": cfg.B * cfg.S / t1, "unit": "tokens/s", "cores": 1,
+                                               "sample": desc1}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def target_config_block(args, ac, ctx, dev, stream, peaks, name):
+    """The whole step at another BASELINE.json config (default: configs[2], Llama-3-8B shape, where north_star
+    states its >= 3x target): step time and tokens/s, per-stage times, the A.V and attention rooflines, the
+    speedups over in-library full attention (batch and per hit), and the Eq. 5 block ratio."""
+    from paper_2510_25979_b200.pipeline import PrefillStep
+    cfg = synth.CONFIGS[name]
+    x = synth.features(cfg, 0, cfg.N, dev)
+    maps = ac.pack_db_maps(lambda b, out: synth.fill_maps(cfg, out, b), cfg.N, cfg.L, cfg.H, cfg.S,
+                           synth.torch_dtype(cfg.map_dtype), dev, chunk=max(1, (1 << 30) // cfg.map_bytes_per_entry))
+    db = ac.Database(ctx, x, maps, packed=True, seq_len=cfg.S)
+    q, _, _ = synth.queries(cfg, dev)
+    Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=dev) for k in "qkv")
+    O = torch.empty_like(V)
+    step = PrefillStep(ctx, db, cfg.tau)
+    steps = max(3, min(args.steps, 20))
+    for _ in range(max(3, args.warmup)):
+        step(q, Q, K, V, O)
+    ctx.sync()
+    idx, score, hit = step.search(q)
+    n_hit = int(hit.sum().item())
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    for k in range(steps):
+        e = ev[k]
+        e[0].record(stream)
+        step.search(q)
+        e[1].record(stream)
+        ac.attncache_apply_cached(db, idx, V, O, hit=hit)
+        e[2].record(stream)
+        ac.attncache_attend_full(ctx, Q, K, V, O, skip=hit)
+        e[3].record(stream)
+    torch.cuda.synchronize()
+    search_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    apply_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    attend_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in ev)
+    ms = statistics.mean(e[0].elapsed_time(e[3]) for e in ev)
+
+    def timed(fn):
+        fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    O_full = torch.empty_like(V)
+    full_ms = timed(lambda: ac.attncache_attend_full(ctx, Q, K, V, O_full))
+    miss_rows = (1 - hit).contiguous()
+    full_hits_ms = timed(lambda: ac.attncache_attend_full(ctx, Q, K, V, O_full, skip=miss_rows))
+    del O_full
+    bytes_alg = n_hit * apply_bytes_per_hit(cfg)
+    attend_alg = (cfg.B - n_hit) * attend_bytes_per_miss(cfg)
+    out = {"workload": cfg.name, "bj_config_index": cfg.bj_index, "config": _line_config(cfg, n_hit),
+           "ms_per_step": ms, "tokens_per_s": cfg.B * cfg.S / (ms * 1e-3), "steps": steps,
+           "stages_ms": {"search": search_ms, "apply_cached": apply_ms, "attend_full_misses": attend_ms},
+           "apply_roofline": {"bound": "hbm", "achieved": bytes_alg / (apply_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                              "unit": "GB/s", "frac": bytes_alg / (apply_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                              "algorithmic_bytes_per_launch": bytes_alg,
+                              "traffic": _ncu_traffic(cfg.name, "apply")},
+           "attend_misses_hbm_frac": attend_alg / (attend_ms * 1e-3) / 1e9 / peaks["hbm_gbs"] if attend_ms else None,
+           "speedup_vs_full_attention": {"batch": full_ms / ms, "per_hit_kernel": full_hits_ms / apply_ms,
+                                         "full_attention_ms": full_ms, "full_attention_hit_rows_ms": full_hits_ms,
+                                         "ceiling_vs_roofline_attention_per_hit": 8 * cfg.d / (cfg.S + 1 + 4 * cfg.d),
+                                         "paper_context": PAPER_CONTEXT},
+           "eq5_block": eq5_block(ac, ctx, db, cfg, idx, hit, stream, steps)}
+    del step, db, maps, x, q, Q, K, V, O
+    torch.cuda.empty_cache()
+    return out
 
 
 def capture_stage(ac, ctx, cfg, Q, K, hit, stream, steps, peaks):
@@ -502,161 +597,178 @@ def _rows_activations(cfg, kind, rows, dev):
     return out
 
 
-def run_dist(args, cfg):
-    """N > 1 (torchrun, one process per GPU, NCCL): the DB is sharded by contiguous entry ranges,
-    each rank is home to a contiguous block of the query batch: the config's batch per GPU by default
-    (--scaling weak: per-GPU work fixed, global batch B * N against the same DB), or the config's batch
-    split over the GPUs (--scaling strong: same global data at every N).  One step = sharded search (query all-gather, local top-1, key all-gather + max), then
-
-      --placement affinity (default; SURVEY.md §8(e) owner-affinity): every query is placed once on the
-        rank that processes all its layers (hits on the owner of their entry, misses greedily on the
-        least-loaded ranks), its request state (hidden states [S][E]) moves there by one all_to_all, and
-        A.V / attention run locally;
-      --placement routed (the north_star's literal routing): hits' V rows go to the owner and O rows
-        come back by all_to_all, misses stay home."""
+def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
+    """Builds one rank's inputs for the global batch cfg.B (home blocks: contiguous, shard_range) and times
+    K steps of the chosen placement; returns (ms max over ranks, extra dict, launches, hits)."""
     import torch.distributed as dist
 
-    import paper_2510_25979_b200 as ac
-    from paper_2510_25979_b200.dist import AffinityPrefill, CudaOps, ShardedPrefill, shard_range
-    rank, world, local = _env_rank()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
-    ctx = ac.Context(local)
-    peaks = _peaks()
-    if args.scaling == "weak":  # the config's batch on EVERY GPU: global batch B * world, same sharded DB
-        cfg = cfg.with_(B=cfg.B * world)
-    begin, count = shard_range(cfg.N, world, rank)
-    x = synth.features(cfg, begin, count, dev)
-    maps = ac.pack_db_maps(lambda b, out: synth.fill_maps(cfg, out, begin + b), count, cfg.L, cfg.H, cfg.S,
-                           synth.torch_dtype(cfg.map_dtype), dev, chunk=max(1, (1 << 30) // cfg.map_bytes_per_entry))
-    db = ac.Database(ctx, x, maps, n_global=cfg.N, shard_begin=begin, packed=True, seq_len=cfg.S)
+    from paper_2510_25979_b200.dist import AffinityPrefill, ShardedPrefill, shard_range
     q_all, _, _ = synth.queries(cfg, dev)
     hb, hc = shard_range(cfg.B, world, rank)
     q = q_all[hb:hb + hc].contiguous()
     sizes = [shard_range(cfg.B, world, r)[1] for r in range(world)]
-    if args.placement == "affinity":
-        step = AffinityPrefill(CudaOps(ctx, db), cfg.N, cfg.tau, hit_cost=apply_bytes_per_hit(cfg),
-                               miss_cost=attend_bytes_per_miss(cfg), device=dev)
-        plan0 = step.plan(q, sizes)
+    comp = torch.cuda.current_stream(dev)
+    if placement == "affinity":
+        step = AffinityPrefill(ctx, db, cfg.tau, sizes, hit_cost=apply_bytes_per_hit(cfg),
+                               miss_cost=attend_bytes_per_miss(cfg))
+        plan0 = step.plan(q)
         loc = step.local_queries(plan0)
         # the synthetic activations of the queries this rank processes, generated here from their seeds
         # (in a model they come from the relocated hidden states; SURVEY.md §8(e))
         Q, K, V = (_rows_activations(cfg, k, loc.tolist(), dev) for k in "qkv")
         O = torch.empty_like(V)
-        E = cfg.H * cfg.d
-        X_home = torch.randn(hc, cfg.S, E, device=dev).to(synth.torch_dtype(cfg.act_dtype))
-
-        comp = torch.cuda.current_stream(dev)
+        X_home = torch.randn(hc, cfg.S, cfg.H * cfg.d, device=dev).to(synth.torch_dtype(cfg.act_dtype))
         comm = torch.cuda.Stream(dev)
 
         def one_step():
             # steady state of a serving loop: the request state of the NEXT batch (same plan here: the bench
             # repeats one batch) moves on a communication stream while this batch's layers run locally
-            plan = step.plan(q, sizes)
+            plan = step.plan(q)
             comm.wait_stream(comp)
-            with torch.cuda.stream(comm):
-                step.relocate(X_home, plan)
+            step.relocate(X_home, plan, stream=comm)
             step.apply_local(plan, loc, V, O, Q, K)
             comp.wait_stream(comm)
             return plan
     else:
         Q, K, V = (synth.activations(cfg, k, hb, hc, device=dev) for k in "qkv")
         O = torch.empty_like(V)
-        step = ShardedPrefill(CudaOps(ctx, db), cfg.N, cfg.tau, device=dev)
+        step = ShardedPrefill(ctx, db, cfg.tau, sizes)
         one_step = lambda: step(q, Q, K, V, O)  # noqa: E731
     for _ in range(args.warmup):
         res = one_step()
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = ac.attncache_launch_count()
-    clocks = ClockSampler(local)
-    clocks.start()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record()
+    start.record(comp)
     for _ in range(args.steps):
         res = one_step()
-    end.record()
+    end.record(comp)
     torch.cuda.synchronize()
     dist.barrier()
-    clk = clocks.stop()
     ms = torch.tensor([start.elapsed_time(end) / args.steps], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)  # the step time is the slowest rank's
-    if args.placement == "affinity":
+    launches = torch.tensor([ac.attncache_launch_count() - launches0], device=dev)
+    dist.all_reduce(launches)
+    extra = {}
+    if placement == "affinity":
         assert torch.equal(step.local_queries(res), loc), "placement changed between steps"
-        n_hit = torch.tensor([int(res["hit"].sum().item()) if rank == 0 else 0], device=dev)
-        extra = {"local_queries": int(loc.numel()), "relocated_bytes_per_query": cfg.S * cfg.H * cfg.d * 2,
-                 "pipelining": "request-state relocation (NCCL all_to_all, communication stream) overlaps the "
-                               "local A.V / attention of the step; both complete inside the step"}
+        n_hit = int(res["hit"].sum().item())
         per_rank = torch.tensor([loc.numel()], device=dev)
         gathered = [torch.empty_like(per_rank) for _ in range(world)]
         dist.all_gather(gathered, per_rank)
-        extra["queries_per_rank"] = [int(t.item()) for t in gathered]
-        extra["plan_load_bytes_per_rank"] = [float(v) for v in res["load"].tolist()]
+        extra = {"queries_per_rank": [int(t.item()) for t in gathered],
+                 "plan_load_bytes_per_rank": [float(v) for v in res["load"].tolist()],
+                 "relocated_bytes_per_query": cfg.S * cfg.H * cfg.d * 2,
+                 "pipelining": "request-state relocation (attncache_relocate_rows on a communication stream) "
+                               "overlaps the local A.V / attention of the step; both complete inside the step"}
     else:
-        n_hit = torch.tensor([int(res[2].sum().item())], device=dev)
-        extra = {}
-    dist.all_reduce(n_hit)
-    launches = torch.tensor([ac.attncache_launch_count() - launches0], device=dev)
-    dist.all_reduce(launches)
+        t = torch.tensor([int(res[2].sum().item())], device=dev)
+        dist.all_reduce(t)
+        n_hit = int(t.item())
+    del Q, K, V, O
+    return float(ms.item()), extra, int(launches.item()), n_hit
+
+
+def run_dist(args, cfg):
+    """N > 1 (torchrun, one process per GPU): the DB is sharded by contiguous entry ranges over the GPUs and
+    every exchange runs inside libattncache over its own NCCL communicator (torch.distributed only
+    broadcasts the NCCL unique id and provides the barrier / max-over-ranks timing).  Each rank is home to a
+    contiguous block of the query batch.  Measured both ways:
+      weak   : the config's batch on EVERY GPU (global batch B * N against the same sharded DB);
+      strong : the config's batch split over the GPUs (the same global data at every N; SURVEY.md:737).
+    `--scaling` picks which one is the line's value; the other is reported beside it.
+      --placement affinity (default; SURVEY.md §8(e) owner-affinity): search_all, the device placement, one
+        relocation of the request state, then A.V / attention locally;
+      --placement routed (the north_star's literal routing): hits' V rows go to the owner and O rows come back
+        inside attncache_apply_cached, misses stay home."""
+    import torch.distributed as dist
+
+    import paper_2510_25979_b200 as ac
+    from paper_2510_25979_b200.dist import shard_range
+    if "MASTER_ADDR" not in os.environ:  # --force-dist without torchrun: a one-rank group
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]), RANK="0",
+                              WORLD_SIZE="1", LOCAL_RANK="0")
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    ctx = ac.Context.from_process_group(local)  # the library's own NCCL communicator
+    begin, count = shard_range(cfg.N, world, rank)
+    x = synth.features(cfg, begin, count, dev)
+    maps = ac.pack_db_maps(lambda b, out: synth.fill_maps(cfg, out, begin + b), count, cfg.L, cfg.H, cfg.S,
+                           synth.torch_dtype(cfg.map_dtype), dev, chunk=max(1, (1 << 30) // cfg.map_bytes_per_entry))
+    db = ac.Database(ctx, x, maps, n_global=cfg.N, shard_begin=begin, packed=True, seq_len=cfg.S)  # collective
+    clocks = ClockSampler(local)
+    clocks.start()
+    runs = {}
+    for mode in (args.scaling, "strong" if args.scaling == "weak" else "weak"):
+        c = cfg.with_(B=cfg.B * world) if mode == "weak" else cfg
+        runs[mode] = (c,) + _dist_timed(args, c, ac, ctx, db, dev, args.placement, world, rank, local)
+    clk = clocks.stop()
     ctx.sync()
-    ms = float(ms.item())
     if rank == 0:
-        par = (f"DB sharded by entry over {world} GPUs; " +
+        c, ms, extra, launches, n_hit = runs[args.scaling]
+        oc, oms, oextra, _, on_hit = runs["strong" if args.scaling == "weak" else "weak"]
+        par = (f"DB sharded by entry over {world} GPUs; collectives inside libattncache (NCCL); " +
                ("owner-affinity placement: hits on the owner, misses on the least-loaded GPUs, request state "
-                "moved once (NCCL all_to_all), all layers local" if args.placement == "affinity" else
-                "hits routed to the owner (V out, O back by NCCL all_to_all)"))
-        line = {"metric": METRIC, "value": cfg.B * cfg.S / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world,
+                "moved once, all layers local" if args.placement == "affinity" else
+                "hits routed to the owner (V out, O back by grouped NCCL send/recv inside apply_cached)"))
+        line = {"metric": METRIC, "value": c.B * c.S / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": args.scaling, "vs_baseline": None, "dtype": cfg.act_dtype,
                 "data": "synthetic (synth/, seed 0)",
-                "config": {"workload": cfg.name, "bj_config_index": cfg.bj_index, "N": cfg.N, "B": cfg.B, "S": cfg.S,
-                           "hits": int(n_hit.item()), "placement": args.placement, "parallelism": par,
-                           "l2": "inputs exceed L2 (no flush)", **extra},
-                "gpu_launches": int(launches.item()), "clocks": clk,
-                "roofline": {"bound": "hbm", "achieved": None, "peak": peaks["hbm_gbs"] * world, "unit": "GB/s",
+                "config": {"workload": cfg.name, "bj_config_index": cfg.bj_index, "N": cfg.N, "D": cfg.D, "L": cfg.L,
+                           "H": cfg.H, "S": cfg.S, "d": cfg.d, "B": c.B, "hits": n_hit, "tau": cfg.tau,
+                           "placement": args.placement, "parallelism": par, "l2": "inputs exceed L2 (no flush)",
+                           **extra},
+                "other_scaling": {"scaling": "strong" if args.scaling == "weak" else "weak", "B": oc.B,
+                                  "ms_per_step": oms, "value": oc.B * oc.S / (oms * 1e-3), "hits": on_hit},
+                "gpu_launches": launches, "clocks": clk,
+                "roofline": {"bound": "hbm", "achieved": None, "peak": _peaks()["hbm_gbs"] * world, "unit": "GB/s",
                              "frac": None, "traffic": None,
                              "note": "multi-GPU line: per-kernel roofline is reported by the N=1 run"},
                 "e2e": {"value": None, "unit": "tokens/s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                         "note": "end-to-end host-buffer timing is reported by the N=1 run"}}
         print(json.dumps(line), flush=True)
+    del db
+    ctx.close()
     dist.destroy_process_group()
     return 0
 
 
 def run_e2e(args, cfg, ctx, db, step, q, Q, K, V, dev, stream):
-    """The step through the public host-buffer API (pipeline.HostPrefill): per step H2D of the queries,
-    D2H of the hit mask, then chunk-pipelined H2D of V (all rows) and Q/K (miss rows only: Alg. 2
-    computes q/k only on a miss), the kernels, and D2H of O; plus D2H of idx/score/hit."""
-    from paper_2510_25979_b200.pipeline import HostPrefill
+    """The step through the public host-buffer C call (attncache_prefill_host): per step, inside the library,
+    H2D of the queries, D2H of the decisions, then chunk-pipelined H2D of V (all rows) and Q/K (miss rows
+    only: Alg. 2 computes q/k only on a miss), the kernels, and D2H of O.  The call is synchronous, so the
+    host wall clock of K calls is the end-to-end time (CUDA events would not see the library's streams)."""
+    import paper_2510_25979_b200 as ac
     qh = q.cpu().pin_memory()
     Vh = V.cpu().pin_memory()
     Qh = Q.cpu().pin_memory()
     Kh = K.cpu().pin_memory()
     Oh = torch.empty(V.shape, dtype=V.dtype).pin_memory()
-    hp = HostPrefill(step, chunk=16, depth=4)
     row = Vh[0].numel() * Vh.element_size()
-    res = hp(qh, Qh, Kh, Vh, Oh)
-    torch.cuda.synchronize()
-    n_miss = int((res[2] == 0).sum())
+    idx, score, hit, _ = ac.attncache_prefill_host(db, qh, Qh, Kh, Vh, cfg.tau, O=Oh)
+    n_miss = int((hit == 0).sum())
     for _ in range(max(0, args.warmup - 1)):
-        hp(qh, Qh, Kh, Vh, Oh)
+        ac.attncache_prefill_host(db, qh, Qh, Kh, Vh, cfg.tau, O=Oh, idx=idx, score=score, hit=hit)
     torch.cuda.synchronize()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
     n = max(1, min(args.steps, 5))
-    t0.record(stream)
+    t0 = time.perf_counter()
     for _ in range(n):
-        hp(qh, Qh, Kh, Vh, Oh)
-    t1.record(stream)
-    torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1) / n
+        ac.attncache_prefill_host(db, qh, Qh, Kh, Vh, cfg.tau, O=Oh, idx=idx, score=score, hit=hit)
+    ms = (time.perf_counter() - t0) * 1e3 / n
     h2d = qh.numel() * qh.element_size() + Vh.numel() * Vh.element_size() + 2 * n_miss * row
-    d2h = Oh.numel() * Oh.element_size() + cfg.B * (8 + 4 + 1) + cfg.B
+    d2h = Oh.numel() * Oh.element_size() + cfg.B * (8 + 4 + 1)
     return {"value": cfg.B * cfg.S / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms, "steps": n,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "note": "pinned host buffers, chunk-pipelined copies (16 rows, 4-deep ring) overlapping the kernels; "
-                    "one mid-step D2H of the hit mask"}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "attncache_prefill_host (C ABI)",
+            "note": "pinned host buffers; one synchronous C-ABI call per step: chunk-pipelined copies (16 rows, "
+                    "4-deep ring, three library streams) overlapping the kernels; one mid-call D2H of the "
+                    "decisions"}
 
 
 def _ncu_traffic(cfg_name, kernel):
@@ -677,6 +789,7 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-search-sweep", action="store_true", help="skip the configs[4] search-QPS sweep")
+    ap.add_argument("--no-target", action="store_true", help="skip the configs[2] (north_star target shape) block")
     ap.add_argument("--placement", default="affinity", choices=["affinity", "routed"],
                     help="N > 1: owner-affinity placement (default) or the literal V->owner / O->home routing")
     ap.add_argument("--scaling", default="weak", choices=["strong", "weak"],
@@ -695,6 +808,16 @@ def main(argv=None):
             if v is not None}
     if over:  # SURVEY.md §5 config overrides; the line's config then records them
         cfg = cfg.with_(**over)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: start N ranks (one process per GPU) under torch.distributed.run
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+               *(argv if argv is not None else sys.argv[1:])]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)

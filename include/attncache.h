@@ -26,6 +26,13 @@
  *  - All arrays are dense row-major with the innermost dimension contiguous.
  *  - A ctx is used by one host thread at a time.  A db is immutable after
  *    load and may be read concurrently.
+ *  - Scratch is per (ctx, stream) and stream-ordered (cudaMallocAsync/cudaFreeAsync on the call's
+ *    stream): growing it never synchronises the device, and calls on two streams never share a buffer.
+ *    A call captured into a CUDA graph gets scratch of its own that lives as long as the ctx.
+ *  - COLLECTIVE calls (marked below) run on a ctx created with a communicator (rank, world, uid):
+ *    every rank calls them in the same order with the same tau / layer range (NCCL semantics);
+ *    the NCCL operations are enqueued on the caller's stream.  Host round trips inside a collective
+ *    call are listed with the call.  On a ctx without a communicator they are the local calls.
  */
 #ifndef ATTNCACHE_H_
 #define ATTNCACHE_H_
@@ -47,7 +54,8 @@ typedef enum {
     ATTNCACHE_ERR_OUT_OF_MEMORY = 7,
     ATTNCACHE_ERR_CUDA = 8,             /* a CUDA runtime/driver error (sticky errors too)    */
     ATTNCACHE_ERR_STATE = 9,            /* wrong device / destroyed handle                    */
-    ATTNCACHE_ERR_UNSUPPORTED = 10      /* e.g. no sm_100 device                              */
+    ATTNCACHE_ERR_UNSUPPORTED = 10,     /* e.g. no sm_100 device                              */
+    ATTNCACHE_ERR_NCCL = 11             /* NCCL missing or an NCCL call failed (also async)   */
 } attncache_status;
 
 typedef enum { ATTNCACHE_F32 = 0, ATTNCACHE_F16 = 1, ATTNCACHE_BF16 = 2 } attncache_dtype;
@@ -77,13 +85,34 @@ uint64_t attncache_launch_count(void);
 
 /* ---- lifecycle --------------------------------------------------------- */
 
+/* A 128-byte NCCL unique id (ncclGetUniqueId) for attncache_ctx_create: rank 0 creates it and the caller
+ * broadcasts it to the other ranks by any means (torch.distributed, a file, MPI).  NCCL is loaded with
+ * dlopen (the copy already in the process, else $ATTNCACHE_NCCL_LIB, else libnccl.so.2).
+ * Errors: NCCL (library not found or call failed), INVALID_ARGUMENT (out NULL). */
+attncache_status attncache_get_unique_id(uint8_t out[128]);
+
 /* Creates a context bound to CUDA device `device` (the caller's current device is not changed
- * permanently).  Requires compute capability 10.0 (sm_100a); else ATTNCACHE_ERR_UNSUPPORTED. */
-attncache_status attncache_ctx_create(int32_t device, attncache_ctx **out);
+ * permanently).  Requires compute capability 10.0 (sm_100a); else ATTNCACHE_ERR_UNSUPPORTED.
+ * uid == NULL (world must be 1): a local ctx, no communicator.  uid != NULL: COLLECTIVE — every rank r of
+ * [0, world) calls it with the same uid and world, and the ctx owns an NCCL communicator (one process per
+ * GPU; north_star: the DB shards by entry across the GPUs of one box).  A world-1 ctx with a uid runs the
+ * collective code paths over a one-rank communicator.
+ * Errors: INVALID_ARGUMENT (rank outside [0, world), world > 1 without uid), UNSUPPORTED, NCCL, CUDA. */
+attncache_status attncache_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t *uid,
+                                      attncache_ctx **out);
+/* rank / world of the ctx (0 / 1 for a local ctx); either pointer may be NULL. */
+attncache_status attncache_ctx_info(const attncache_ctx *ctx, int32_t *rank, int32_t *world);
 attncache_status attncache_ctx_destroy(attncache_ctx *ctx);
 /* Synchronises the device and returns (then clears) any deferred error: ERR_NOT_FOUND when an
- * apply call met an index outside its shard, ERR_CUDA on an asynchronous CUDA fault. */
+ * apply call met an index outside its shard, ERR_CUDA on an asynchronous CUDA fault, ERR_NCCL on an
+ * asynchronous communicator error. */
 attncache_status attncache_ctx_sync(attncache_ctx *ctx);
+
+/* The home batch size of every rank for the following collective calls (home_counts: host int64 [world];
+ * NULL clears it).  With a layout, collective search needs no host round trip (CUDA-graph capturable);
+ * without one it all-gathers the counts and synchronises the stream once per call.  A collective call
+ * whose n_home differs from home_counts[rank] returns ERR_STATE. */
+attncache_status attncache_set_batch_layout(attncache_ctx *ctx, const int64_t *home_counts, int32_t world);
 
 /* ---- database (Fig. 4: "Both databases share the same index") ----
  *
@@ -98,8 +127,12 @@ attncache_status attncache_ctx_sync(attncache_ctx *ctx);
  *          above the diagonal, reading R11; PACKED: see attncache_map_layout) — layer-
  *          contiguous per entry and head-major inside a layer.  May be NULL
  *          for a search-only database (n_layers = n_heads = seq_len = 0).
+ * COLLECTIVE on a ctx with a communicator: the ranks' descriptors must agree on every global field
+ * (n_global, feat_dim/dtype, L, H, S, map dtype/layout) and their shards must tile [0, n_global) in rank
+ * order (rank r's shard_begin = the sum of the lower ranks' shard_count); one host round trip.
  * Errors: INVALID_ARGUMENT (ranges, null feats with shard_count > 0, n_global >= 2^32, PACKED
- * non-causal maps), DTYPE, ALIGNMENT (feats/maps base or row pitch not a multiple of 16 bytes). */
+ * non-causal maps, shards not tiling), SHAPE (ranks disagree), DTYPE, ALIGNMENT (feats/maps base or row
+ * pitch not a multiple of 16 bytes), NCCL. */
 typedef struct {
     int64_t n_global;
     int64_t shard_begin;
@@ -122,16 +155,28 @@ attncache_status attncache_db_free(attncache_db *db);
 
 /* ---- Alg. 1: VecDB.search + theta gate -----------
  *
- * attncache_search — single-rank search over this shard (which must cover the whole DB,
- * shard_count == n_global; otherwise use search_keys + keys_decode across ranks).
+ * attncache_search — the top-1 of this rank's n_queries HOME queries over the WHOLE database.
+ *   Local ctx: the shard must cover the whole DB (shard_count == n_global; for shards on one process use
+ *   search_keys + keys_decode).  COLLECTIVE ctx (north_star's sharded search):
+ *   C1 the query batch is gathered on every rank (an NCCL all-gather when every home block has the same
+ *   size, else grouped send/recv), K1 every rank takes its shard's top-1 key of every query, C2 one NCCL
+ *   u64 max-all-reduce of the keys (= the global top-1 with the lowest-index tie-break, reading R3), K2
+ *   decode + tau gate of the home block.  Host round trip: the home counts exchange when no batch layout
+ *   is set (attncache_set_batch_layout).  n_queries may be 0 on some ranks.
  *   queries: [n_queries][feat_dim] in the DB's feat_dtype (no silent casts; reading R10).
  *   idx[b]  : global index of the top-1 entry by inner product s = q . x (fp32 accumulation),
  *             the LOWEST index among equal scores (reading R3); always set, also on a miss.
  *   score[b]: that fp32 inner product.   hit[b]: 1 iff score[b] >= tau (inclusive).
  * tau may be any non-NaN float (tau > 1: every query misses).  n_queries may be 0.
- * Errors: EMPTY (n_global == 0), INVALID_ARGUMENT (NaN tau, null pointers with n > 0). */
+ * Errors: EMPTY (n_global == 0), INVALID_ARGUMENT (NaN tau, null pointers with n > 0), STATE (a partial
+ * shard on a local ctx; n_queries disagreeing with the batch layout), NCCL. */
 attncache_status attncache_search(attncache_db *db, const void *queries, int64_t n_queries, float tau,
                                   int64_t *idx, float *score, uint8_t *hit, void *stream);
+/* The same search, writing the decisions of the WHOLE batch (every rank's home block in rank order,
+ * sum of the home counts rows) on every rank — what the owner-affinity placement needs.
+ * COLLECTIVE on a ctx with a communicator; on a local ctx the same as attncache_search. */
+attncache_status attncache_search_all(attncache_db *db, const void *queries, int64_t n_queries, float tau,
+                                      int64_t *idx, float *score, uint8_t *hit, void *stream);
 
 /* Sharded halves of the same search (C1/C2 of SURVEY.md §2.4).  search_keys writes, per query,
  * the packed key of this shard's top-1:  key = ord(score) << 32 | (0xFFFFFFFF - global_index),
@@ -151,7 +196,7 @@ attncache_status attncache_keys_decode(const uint64_t *keys, int32_t n_shards, i
 /* ---- Alg. 2 hit branch: O = attn_map . V ---------------
  *
  * For every row b in [0, n_rows) that is selected — hit[b] != 0 when `hit` is non-NULL, else
- * idx[b] >= 0 — and for every layer l in [layer_begin, layer_end) and head h:
+ * idx[b] >= 0 — and for every layer l in [layer_begin, layer_end) and head h (idx: GLOBAL entry indices):
  *     O[b][l-layer_begin][h] (S x d) = maps[idx[b] - shard_begin][l][h] (S x S) . V[b][l-layer_begin][h] (S x d)
  * accumulated in fp32 and rounded once to act_dtype.  Unselected rows of O are left untouched.
  * V, O: [n_rows][layer_end-layer_begin][n_heads][seq_len][head_dim] in act_dtype.
@@ -159,11 +204,25 @@ attncache_status attncache_keys_decode(const uint64_t *keys, int32_t n_shards, i
  * the diagonal are never read.  A selected idx outside this shard is skipped and reported by the
  * next attncache_ctx_sync() as ERR_NOT_FOUND.  Supported: act_dtype == map_dtype (tensor cores),
  * or act_dtype F32 with any map dtype (CUDA cores).
+ * COLLECTIVE ctx (north_star: "Hit queries are then routed to the owning GPU, whose A.V output returns
+ * to the query's home GPU by NCCL send/recv"): K3 buckets the selected home rows by the rank owning their
+ * entry, C3 exchanges the per-peer counts (one host round trip sizes the transfers), C4 ships the V rows
+ * and entry indices to the owners (grouped ncclSend/ncclRecv), K4 runs A.V there on the local maps, C5
+ * returns the O rows, K3 scatters them into O.  Scratch for the transfers is stream-ordered.
  * Errors: SHAPE (layer range outside [0, n_layers), head_dim <= 0), DTYPE, ALIGNMENT, STATE
- * (db has no maps). */
+ * (db has no maps), NCCL. */
 attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
                                         int32_t layer_begin, int32_t layer_end, int32_t head_dim,
                                         int32_t act_dtype, const void *V, void *O, void *stream);
+
+/* The LOCAL A.V of the rows whose entry lies in this rank's shard (no communication, never routes; the
+ * owner-affinity placement runs every hit on its owner): the same as attncache_apply_cached
+ * on a local ctx, with GQA head counts as attncache_apply_cached_gqa.  A selected idx outside this shard is
+ * skipped and reported by the next ctx_sync as ERR_NOT_FOUND. */
+attncache_status attncache_apply_cached_local(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                              int32_t layer_begin, int32_t layer_end, int32_t head_dim,
+                                              int32_t n_kv_heads, int32_t act_dtype, const void *V, void *O,
+                                              void *stream);
 
 /* Grouped-query attention (GQA; SURVEY.md §8(f) f3 "optional GQA n_kv_heads"; Llama-3 models keep fewer
  * K/V heads than query heads): the same as attncache_apply_cached with V: [n_rows][layer_end-layer_begin]
@@ -194,6 +253,22 @@ attncache_status attncache_attend_full_gqa(attncache_ctx *ctx, int64_t batch, in
                                            int32_t n_kv_heads, int32_t seq_len, int32_t head_dim, int32_t act_dtype,
                                            const void *Q, const void *K, const void *V, float scale,
                                            const uint8_t *skip, void *O, void *stream);
+
+/* ---- the whole single-rank step from HOST buffers (the end-to-end call) ----------------------
+ * Alg. 1 then Alg. 2 for every layer of the DB, with the host<->device copies inside the call: H2D of the
+ * queries, search (idx/score/hit as attncache_search), D2H of the decisions (one host sync: Alg. 2 computes
+ * q and k only on a miss, so only the misses' Q and K cross PCIe), then chunks of `chunk`
+ * rows through a ring of `depth` device slots on three library streams (copy-in, compute, copy-out):
+ * H2D of V (every row) and Q, K (miss rows), attncache_apply_cached on the hits and attncache_attend_full on
+ * the misses, D2H of O.  Synchronous: returns when O and idx/score/hit are in host memory.
+ *   q: [n][feat_dim] feat dtype; Q, K, V, O: [n][n_layers][n_heads][seq_len][head_dim] act_dtype;
+ *   idx int64 / score fp32 / hit uint8: [n].  Every pointer must be PAGE-LOCKED HOST memory
+ *   (cudaHostAlloc / cudaHostRegister).  Device staging is ctx scratch.  A local db holding every entry.
+ * Errors: INVALID_ARGUMENT (pageable or device pointers, chunk <= 0, depth outside [2, 8], NaN tau), STATE
+ * (a shard / a collective ctx of world > 1 / no maps), EMPTY, DTYPE, ALIGNMENT, CUDA. */
+attncache_status attncache_prefill_host(attncache_db *db, const void *q, int64_t n, float tau, const void *Q,
+                                        const void *K, const void *V, int32_t head_dim, int32_t act_dtype, void *O,
+                                        int64_t *idx, float *score, uint8_t *hit, int32_t chunk, int32_t depth);
 
 /* ---- DB building, capture (Fig. 4 step 1; "collect
  * the input hidden states and their corresponding attention maps at each layer") --------------
@@ -246,7 +321,8 @@ attncache_status attncache_rope(void *X, int64_t n_units, int32_t seq_len, int32
  * owner[b] = -1 for misses.  counts[r] = number of rows owned by r; order = the selected rows
  * grouped by owner (ascending rank, ascending b inside a rank), n = sum(counts) entries used.
  * Deterministic.  gather_rows: dst[k] = src[rows[k]]; scatter_rows: dst[rows[k]] = src[k];
- * rows are int64 row numbers and rows are row_bytes long (a multiple of 8; 16 is faster). */
+ * rows are int64 row numbers and rows are row_bytes long (a multiple of 8; 16 is faster).
+ * route_plan with hit == NULL selects the rows with idx[b] >= 0. */
 attncache_status attncache_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n_rows,
                                       const int64_t *shard_begins, int32_t world, int32_t *owner, int32_t *counts,
                                       int64_t *order, void *stream);
@@ -294,6 +370,15 @@ attncache_status attncache_affinity_plan_device(attncache_ctx *ctx, const int64_
                                                 const int64_t *home_begins, int32_t *assign, double *load,
                                                 int64_t *loc, int64_t *idx_loc, uint8_t *hit_loc,
                                                 int64_t *send_order, int32_t *counts, void *stream);
+
+/* Moves request state to the ranks the placement chose (COLLECTIVE; SURVEY.md §8(e) owner-affinity: "the
+ * request's hidden state moves once").  Sends this rank's home rows src[send_order[k]] (k < n_home) to the
+ * ranks in the order of `counts` (host int32 [2 world + 1] as attncache_affinity_plan_device returns it:
+ * send_n[world] | recv_n[world] | n_loc; send_n sums to n_home) and writes the rows received from ranks
+ * 0..world-1, in rank order, to dst [sum recv_n rows].  Rows are row_bytes long (a multiple of 8).  One
+ * NCCL group of send/recv pairs; on a local ctx a device copy.  Errors: INVALID_ARGUMENT, NCCL, CUDA. */
+attncache_status attncache_relocate_rows(attncache_ctx *ctx, const void *src, int64_t n_home, int64_t row_bytes,
+                                         const int64_t *send_order, const int32_t *counts, void *dst, void *stream);
 
 /* ---- DB building: packed map layout (Fig. 4 step 3) -----------
  * Number of elements one PACKED S x S map occupies (0 if S % 8 != 0). */

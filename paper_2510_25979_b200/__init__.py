@@ -26,7 +26,9 @@ __all__ = [
     "attncache_scatter_rows", "attncache_fetch_maps", "attncache_variant", "attncache_version", "attncache_launch_count",
     "attncache_packed_map_elems", "attncache_pack_maps", "pack_db_maps", "attncache_capture_maps", "attncache_rope",
     "attncache_affinity_plan", "attncache_project_features", "attncache_apply_cached_gqa", "attncache_attend_full_gqa",
-    "attncache_capture_maps_gqa", "attncache_affinity_plan_device", "ABI_FUNCTIONS",
+    "attncache_capture_maps_gqa", "attncache_affinity_plan_device", "ABI_FUNCTIONS", "attncache_get_unique_id",
+    "attncache_ctx_info", "attncache_set_batch_layout", "attncache_search_all", "attncache_apply_cached_local",
+    "attncache_relocate_rows", "attncache_prefill_host",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -41,7 +43,8 @@ ABI_FUNCTIONS = [
     "attncache_variant", "attncache_launch_count", "attncache_packed_map_elems", "attncache_pack_maps",
     "attncache_capture_maps", "attncache_rope", "attncache_affinity_plan", "attncache_project_features",
     "attncache_apply_cached_gqa", "attncache_attend_full_gqa", "attncache_capture_maps_gqa",
-    "attncache_affinity_plan_device",
+    "attncache_affinity_plan_device", "attncache_get_unique_id", "attncache_ctx_info", "attncache_set_batch_layout",
+    "attncache_search_all", "attncache_apply_cached_local", "attncache_relocate_rows", "attncache_prefill_host",
 ]
 
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -73,6 +76,14 @@ def load_library():
     if not os.path.exists(lib_path):
         raise ImportError(f"libattncache.so not built at {lib_path}; run `python -m paper_2510_25979_b200.build` "
                           "(there is no CPU fallback)")
+    if "ATTNCACHE_NCCL_LIB" not in os.environ:  # the NCCL copy torch uses (the library dlopens it on demand)
+        try:
+            import nvidia.nccl as _nv
+            cand = os.path.join(list(_nv.__path__)[0], "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["ATTNCACHE_NCCL_LIB"] = cand
+        except Exception:  # pragma: no cover - the system libnccl.so.2 is the fallback
+            pass
     L = ctypes.CDLL(lib_path)
     P, I64, I32, F32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
     sig = {
@@ -81,7 +92,14 @@ def load_library():
         "attncache_version": ([], I32),
         "attncache_launch_count": ([], ctypes.c_uint64),
         "attncache_variant": ([I32, I32, I32, I32], ctypes.c_char_p),
-        "attncache_ctx_create": ([I32, ctypes.POINTER(P)], I32),
+        "attncache_ctx_create": ([I32, I32, I32, P, ctypes.POINTER(P)], I32),
+        "attncache_get_unique_id": ([P], I32),
+        "attncache_ctx_info": ([P, P, P], I32),
+        "attncache_set_batch_layout": ([P, P, I32], I32),
+        "attncache_search_all": ([P, P, I64, F32, P, P, P, P], I32),
+        "attncache_apply_cached_local": ([P, P, P, I64, I32, I32, I32, I32, I32, P, P, P], I32),
+        "attncache_relocate_rows": ([P, P, I64, I64, P, P, P, P], I32),
+        "attncache_prefill_host": ([P, P, I64, F32, P, P, P, I32, I32, P, P, P, P, I32, I32], I32),
         "attncache_ctx_destroy": ([P], I32),
         "attncache_ctx_sync": ([P], I32),
         "attncache_db_load": ([P, ctypes.POINTER(_DbDesc), ctypes.POINTER(P)], I32),
@@ -139,14 +157,38 @@ def _dev(t: torch.Tensor, what: str):
 
 
 class Context:
-    """attncache_ctx: one per process and device."""
+    """attncache_ctx: one per process and device.  rank/world/uid (a 128-byte attncache_get_unique_id from
+    rank 0) make it COLLECTIVE: the library owns an NCCL communicator over the world's GPUs; world=1 with no
+    uid is a local context.  ``Context.from_process_group`` creates one per rank of a torch.distributed
+    group, using torch only to broadcast the uid."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, uid: Optional[bytes] = None):
         L = load_library()
         h = ctypes.c_void_p()
-        _check(L.attncache_ctx_create(int(device), ctypes.byref(h)))
+        ub = None
+        if uid is not None:
+            if len(uid) != 128:
+                raise ValueError("uid must be the 128 bytes of attncache_get_unique_id")
+            ub = ctypes.create_string_buffer(bytes(uid), 128)
+        _check(L.attncache_ctx_create(int(device), int(rank), int(world), ub, ctypes.byref(h)))
         self.handle = h
         self.device = int(device)
+        self.rank, self.world = int(rank), int(world)
+        self.collective = uid is not None
+
+    @classmethod
+    def from_process_group(cls, device: int, group=None) -> "Context":
+        """Every rank of `group` calls this: rank 0 makes the NCCL unique id, torch.distributed broadcasts its
+        bytes (the only thing torch carries), and each rank creates its communicator-owning context."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [attncache_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        return cls(device, rank, world, obj[0])
+
+    def set_batch_layout(self, home_counts):
+        """Declares every rank's home batch size for the following collective calls (None clears it)."""
+        attncache_set_batch_layout(self, home_counts)
 
     def sync(self):
         _check(load_library().attncache_ctx_sync(self.handle))
@@ -237,8 +279,30 @@ def attncache_variant(kind: str, dtype: torch.dtype, seq_len: int, head_dim: int
     return load_library().attncache_variant(k, _DT[dtype], int(seq_len), int(head_dim)).decode()
 
 
-def attncache_ctx_create(device: int = 0) -> Context:
-    return Context(device)
+def attncache_ctx_create(device: int = 0, rank: int = 0, world: int = 1, uid: Optional[bytes] = None) -> Context:
+    return Context(device, rank, world, uid)
+
+
+def attncache_get_unique_id() -> bytes:
+    """128-byte NCCL unique id for a collective Context (rank 0 makes it; broadcast it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().attncache_get_unique_id(buf))
+    return buf.raw
+
+
+def attncache_ctx_info(ctx: Context):
+    r, w = ctypes.c_int32(), ctypes.c_int32()
+    _check(load_library().attncache_ctx_info(ctx.handle, ctypes.byref(r), ctypes.byref(w)))
+    return r.value, w.value
+
+
+def attncache_set_batch_layout(ctx: Context, home_counts) -> None:
+    if home_counts is None:
+        _check(load_library().attncache_set_batch_layout(ctx.handle, None, 0))
+        return
+    import numpy as np
+    hc = np.ascontiguousarray(list(home_counts), dtype=np.int64)
+    _check(load_library().attncache_set_batch_layout(ctx.handle, ctypes.c_void_p(hc.ctypes.data), hc.shape[0]))
 
 
 def attncache_ctx_destroy(ctx: Context) -> None:
@@ -257,62 +321,134 @@ def attncache_db_free(db: Database) -> None:
     db.close()
 
 
-def attncache_search(db: Database, queries: torch.Tensor, tau: float, idx=None, score=None, hit=None, stream=None):
-    """Alg. 1 l.255-257 on a single rank: returns (idx int64[B], score f32[B], hit u8[B])."""
+def _vec(t: Optional[torch.Tensor], n: int, dtype, dev, what: str) -> torch.Tensor:
+    """An output/input vector of n elements: allocated when None, else checked (dtype, length, device)."""
+    if t is None:
+        return torch.empty(n, dtype=dtype, device=dev)
+    _dev(t, what)
+    if t.dtype != dtype or t.dim() != 1 or t.shape[0] < n or t.device != dev:
+        raise ValueError(f"{what} must be a contiguous {dtype} vector of >= {n} elements on {dev}")
+    return t
+
+
+def _mask(t: Optional[torch.Tensor], n: int, dev, what: str):
+    """A uint8/bool row mask of n elements (None allowed)."""
+    if t is None:
+        return None
+    _dev(t, what)
+    if t.dtype not in (torch.uint8, torch.bool) or t.dim() != 1 or t.shape[0] != n or t.device != dev:
+        raise ValueError(f"{what} must be a contiguous uint8/bool vector of {n} elements on {dev}")
+    return t
+
+
+def _check_queries(db: Database, queries: torch.Tensor):
     _dev(queries, "queries")
+    if queries.dim() != 2 or queries.shape[1] != db.feats.shape[1] or queries.dtype != db.feats.dtype:
+        raise ValueError(f"queries must be [B][{db.feats.shape[1]}] {db.feats.dtype} (the DB's feature dim and dtype; "
+                         "no silent casts)")
+    if queries.device != db.device:
+        raise ValueError("queries must live on the database's device")
+
+
+def attncache_search(db: Database, queries: torch.Tensor, tau: float, idx=None, score=None, hit=None, stream=None):
+    """Alg. 1 l.255-257: returns (idx int64[B], score f32[B], hit u8[B]) of this rank's B home queries (on a
+    collective Context: the global top-1 over every rank's shard)."""
+    _check_queries(db, queries)
     B = queries.shape[0]
     dev = queries.device
-    idx = torch.empty(B, dtype=torch.int64, device=dev) if idx is None else idx
-    score = torch.empty(B, dtype=torch.float32, device=dev) if score is None else score
-    hit = torch.empty(B, dtype=torch.uint8, device=dev) if hit is None else hit
+    idx = _vec(idx, B, torch.int64, dev, "idx")
+    score = _vec(score, B, torch.float32, dev, "score")
+    hit = _vec(hit, B, torch.uint8, dev, "hit")
     _check(load_library().attncache_search(db.handle, _p(queries), B, float(tau), _p(idx), _p(score), _p(hit),
                                            _stream(stream, dev)))
     return idx, score, hit
 
 
+def attncache_search_all(db: Database, queries: torch.Tensor, tau: float, total: Optional[int] = None, idx=None,
+                         score=None, hit=None, stream=None):
+    """The decisions of the WHOLE batch (every rank's home block in rank order) on every rank; `total` = the
+    sum of the home batch sizes (the Context's batch layout, or this rank's B on a local Context)."""
+    _check_queries(db, queries)
+    B = queries.shape[0]
+    dev = queries.device
+    total = B if total is None else int(total)
+    idx = _vec(idx, total, torch.int64, dev, "idx")
+    score = _vec(score, total, torch.float32, dev, "score")
+    hit = _vec(hit, total, torch.uint8, dev, "hit")
+    _check(load_library().attncache_search_all(db.handle, _p(queries), B, float(tau), _p(idx), _p(score), _p(hit),
+                                               _stream(stream, dev)))
+    return idx, score, hit
+
+
 def attncache_search_keys(db: Database, queries: torch.Tensor, keys=None, stream=None) -> torch.Tensor:
     """This shard's packed top-1 keys (int64 view of the u64 keys)."""
-    _dev(queries, "queries")
+    _check_queries(db, queries)
     B = queries.shape[0]
-    keys = torch.empty(B, dtype=torch.int64, device=queries.device) if keys is None else keys
+    keys = _vec(keys, B, torch.int64, queries.device, "keys")
     _check(load_library().attncache_search_keys(db.handle, _p(queries), B, _p(keys), _stream(stream, queries.device)))
     return keys
 
 
 def attncache_keys_decode(keys: torch.Tensor, tau: float, idx=None, score=None, hit=None, stream=None):
     """keys: [n_shards][B] (or [B]) packed keys -> cross-shard top-1 idx/score/hit."""
+    _dev(keys, "keys")
+    if keys.dtype != torch.int64:
+        raise ValueError("keys must be int64 (the u64 bit patterns)")
     keys = keys.reshape(-1, keys.shape[-1])
     n_shards, B = keys.shape
     dev = keys.device
-    idx = torch.empty(B, dtype=torch.int64, device=dev) if idx is None else idx
-    score = torch.empty(B, dtype=torch.float32, device=dev) if score is None else score
-    hit = torch.empty(B, dtype=torch.uint8, device=dev) if hit is None else hit
+    idx = _vec(idx, B, torch.int64, dev, "idx")
+    score = _vec(score, B, torch.float32, dev, "score")
+    hit = _vec(hit, B, torch.uint8, dev, "hit")
     _check(load_library().attncache_keys_decode(_p(keys), n_shards, B, float(tau), _p(idx), _p(score), _p(hit),
                                                 _stream(stream, dev)))
     return idx, score, hit
+
+
+def _apply_args(db: Database, idx, V, O, hit, layer_begin, layer_end):
+    _dev(V, "V")
+    _dev(idx, "idx")
+    layer_end = db.n_layers if layer_end is None else layer_end
+    if idx.dtype != torch.int64 or idx.dim() != 1:
+        raise ValueError("idx must be an int64 vector")
+    if V.dim() != 5 or V.shape[0] != idx.shape[0]:
+        raise ValueError("V must be [B][L'][Hkv][S][d] matching idx")
+    H = db.n_heads if db.maps is not None else V.shape[2]
+    want = (V.shape[0], V.shape[1], H, V.shape[3], V.shape[4])
+    if O is None:
+        O = torch.empty(want, dtype=V.dtype, device=V.device)
+    _dev(O, "O")
+    if tuple(O.shape) != want or O.dtype != V.dtype or O.device != V.device:
+        raise ValueError("O must be [B][L'][H][S][d] with V's B, L', S, d, dtype and device")
+    if idx.device != V.device:
+        raise ValueError("idx must live on V's device")
+    hit = _mask(hit, idx.shape[0], V.device, "hit")
+    if db.maps is not None and (V.shape[1] != layer_end - layer_begin or V.shape[3] != db.seq_len):
+        raise AttnCacheError(2, "ATTNCACHE_ERR_SHAPE", "V shape disagrees with the database (L', S)")
+    return O, hit, layer_end
 
 
 def attncache_apply_cached(db: Database, idx: torch.Tensor, V: torch.Tensor, O: Optional[torch.Tensor] = None,
                            hit: Optional[torch.Tensor] = None, layer_begin: int = 0, layer_end: Optional[int] = None,
                            stream=None) -> torch.Tensor:
     """Alg. 2 l.373-375: O[b] = maps[idx[b]] . V[b] for selected rows; V [B][L'][Hkv][S][d], O [B][L'][H][S][d]
-    (Hkv = H: multi-head; Hkv < H dividing H: grouped-query attention, map head h reads V head h // (H // Hkv))."""
-    _dev(V, "V")
-    _dev(idx, "idx")
-    layer_end = db.n_layers if layer_end is None else layer_end
-    if V.dim() != 5 or V.shape[0] != idx.shape[0]:
-        raise ValueError("V must be [B][L'][Hkv][S][d] matching idx")
-    H = db.n_heads if db.maps is not None else V.shape[2]
-    if O is None:
-        O = torch.empty((V.shape[0], V.shape[1], H, V.shape[3], V.shape[4]), dtype=V.dtype, device=V.device)
-    _dev(O, "O")
-    if O.shape != (V.shape[0], V.shape[1], H, V.shape[3], V.shape[4]):
-        raise ValueError("O must be [B][L'][H][S][d] with V's B, L', S, d")
-    if db.maps is not None and (V.shape[1] != layer_end - layer_begin or V.shape[3] != db.seq_len):
-        raise AttnCacheError(2, "ATTNCACHE_ERR_SHAPE", "V shape disagrees with the database (L', S)")
+    (Hkv = H: multi-head; Hkv < H dividing H: grouped-query attention, map head h reads V head h // (H // Hkv)).
+    On a collective Context the hits are routed to the rank owning their entry and O comes back (COLLECTIVE)."""
+    O, hit, layer_end = _apply_args(db, idx, V, O, hit, layer_begin, layer_end)
     _check(load_library().attncache_apply_cached_gqa(db.handle, _p(idx), _p(hit), V.shape[0], int(layer_begin),
                                                      int(layer_end), V.shape[4], V.shape[2], _DT[V.dtype], _p(V), _p(O),
                                                      _stream(stream, V.device)))
+    return O
+
+
+def attncache_apply_cached_local(db: Database, idx: torch.Tensor, V: torch.Tensor, O: Optional[torch.Tensor] = None,
+                                 hit: Optional[torch.Tensor] = None, layer_begin: int = 0,
+                                 layer_end: Optional[int] = None, stream=None) -> torch.Tensor:
+    """The local A.V (rows whose entry lies in this shard; never communicates): the owner-affinity placement."""
+    O, hit, layer_end = _apply_args(db, idx, V, O, hit, layer_begin, layer_end)
+    _check(load_library().attncache_apply_cached_local(db.handle, _p(idx), _p(hit), V.shape[0], int(layer_begin),
+                                                       int(layer_end), V.shape[4], V.shape[2], _DT[V.dtype], _p(V),
+                                                       _p(O), _stream(stream, V.device)))
     return O
 
 
@@ -332,8 +468,13 @@ def attncache_attend_full(ctx: Context, Q: torch.Tensor, K: torch.Tensor, V: tor
     if Q.dim() != 5 or K.shape != V.shape or not (Q.dtype == K.dtype == V.dtype) or \
             (K.shape[0], K.shape[1], K.shape[3], K.shape[4]) != (Q.shape[0], Q.shape[1], Q.shape[3], Q.shape[4]):
         raise ValueError("Q [B][L][H][S][d] and K, V [B][L][Hkv][S][d] must share B, L, S, d and dtype")
+    if not (Q.device == K.device == V.device):
+        raise ValueError("Q, K, V must live on one device")
     O = torch.empty_like(Q) if O is None else O
     _dev(O, "O")
+    if O.shape != Q.shape or O.dtype != Q.dtype or O.device != Q.device:
+        raise ValueError("O must have Q's shape, dtype and device")
+    skip = _mask(skip, Q.shape[0], Q.device, "skip")
     B, Lq, H, S, d = Q.shape
     _check(load_library().attncache_attend_full_gqa(ctx.handle, B, Lq, H, K.shape[2], S, d, _DT[Q.dtype], _p(Q), _p(K),
                                                     _p(V), float(scale), _p(skip), _p(O), _stream(stream, Q.device)))
@@ -343,6 +484,58 @@ def attncache_attend_full(ctx: Context, Q: torch.Tensor, K: torch.Tensor, V: tor
 def attncache_attend_full_gqa(ctx: Context, Q, K, V, O=None, scale: float = 0.0, skip=None, stream=None):
     """Grouped-query causal attention (the C call of the same name): K, V with Hkv heads."""
     return attncache_attend_full(ctx, Q, K, V, O, scale, skip, stream)
+
+
+def attncache_prefill_host(db: Database, q: torch.Tensor, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor,
+                           tau: float, O: Optional[torch.Tensor] = None, idx=None, score=None, hit=None,
+                           chunk: int = 16, depth: int = 4):
+    """The whole single-rank step end to end from PINNED host tensors (include/attncache.h
+    attncache_prefill_host): every copy happens inside the library call, which returns when O and
+    idx/score/hit are in host memory.  q [B][D]; Q, K, V, O [B][L][H][S][d] (all layers of the DB)."""
+    ts = [(q, "q"), (Q, "Q"), (K, "K"), (V, "V")]
+    for t, nme in ts:
+        if t.is_cuda or not t.is_pinned() or not t.is_contiguous():
+            raise ValueError(f"{nme} must be a contiguous pinned host tensor")
+    B = q.shape[0]
+    if q.dim() != 2 or q.shape[1] != db.feats.shape[1] or q.dtype != db.feats.dtype:
+        raise ValueError("q must be [B][D] in the DB's feature dim and dtype")
+    if V.dim() != 5 or V.shape[0] != B or V.shape[1] != db.n_layers or V.shape[2] != db.n_heads or \
+            V.shape[3] != db.seq_len or Q.shape != V.shape or K.shape != V.shape or not (Q.dtype == K.dtype == V.dtype):
+        raise ValueError("Q, K, V must be [B][L][H][S][d] with the DB's L, H, S and one dtype")
+    mk = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory()  # noqa: E731
+    O = mk(V.shape, V.dtype) if O is None else O
+    idx = mk((B,), torch.int64) if idx is None else idx
+    score = mk((B,), torch.float32) if score is None else score
+    hit = mk((B,), torch.uint8) if hit is None else hit
+    for t, nme, dt, shape in ((O, "O", V.dtype, V.shape), (idx, "idx", torch.int64, (B,)),
+                              (score, "score", torch.float32, (B,)), (hit, "hit", torch.uint8, (B,))):
+        if t.is_cuda or not t.is_pinned() or not t.is_contiguous() or t.dtype != dt or tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{nme} must be a contiguous pinned host {dt} tensor of shape {tuple(shape)}")
+    _check(load_library().attncache_prefill_host(db.handle, _p(q), B, float(tau), _p(Q), _p(K), _p(V), V.shape[4],
+                                                 _DT[V.dtype], _p(O), _p(idx), _p(score), _p(hit), int(chunk),
+                                                 int(depth)))
+    return idx, score, hit, O
+
+
+def attncache_relocate_rows(ctx: Context, src: torch.Tensor, send_order: torch.Tensor, counts, dst=None, stream=None):
+    """COLLECTIVE: moves this rank's home rows src[send_order] to the ranks the placement chose and returns
+    the rows received from every rank, in rank order (include/attncache.h attncache_relocate_rows).  counts:
+    the 2 world + 1 ints of attncache_affinity_plan_device (send_n | recv_n | n_loc; host sequence)."""
+    import numpy as np
+    _dev(src, "src")
+    c = np.ascontiguousarray(list(counts), dtype=np.int32)
+    w = (c.shape[0] - 1) // 2
+    n_recv = int(c[w:2 * w].sum())
+    row_shape = src.shape[1:]
+    dst = torch.empty((n_recv, *row_shape), dtype=src.dtype, device=src.device) if dst is None else dst
+    _dev(dst, "dst")
+    n_home = src.shape[0]
+    row_bytes = (src[0].numel() if n_home else int(np.prod(row_shape))) * src.element_size()
+    so = send_order[:n_home].contiguous() if n_home else None
+    _check(load_library().attncache_relocate_rows(ctx.handle, _p(src) if n_home else None, n_home, row_bytes, _p(so),
+                                                  ctypes.c_void_p(c.ctypes.data), _p(dst) if n_recv else None,
+                                                  _stream(stream, src.device)))
+    return dst
 
 
 def attncache_route_plan(idx, hit, shard_begins: torch.Tensor, owner=None, counts=None, order=None, stream=None):

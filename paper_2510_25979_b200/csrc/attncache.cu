@@ -7,7 +7,7 @@
 #include <atomic>
 #include <cmath>
 
-#include "kernels.cuh"
+#include "abi_internal.cuh"
 
 namespace ac {
 
@@ -37,44 +37,38 @@ attncache_status cuda_status(cudaError_t e, const char *what) {
     return fail(ATTNCACHE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-attncache_status ensure_scratch(Scratch &s, size_t bytes) {
-    if (s.bytes >= bytes) return ATTNCACHE_OK;
-    if (s.ptr) {
-        AC_CUDA(cudaDeviceSynchronize());  // the old buffer may still be in use by queued work
-        AC_CUDA(cudaFree(s.ptr));
+attncache_status scratch(attncache_ctx *ctx, cudaStream_t st, int kind, size_t bytes, void **out) {
+    *out = nullptr;
+    if (bytes == 0) bytes = 16;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    AC_CUDA(cudaStreamIsCapturing(st, &cs));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (cs == cudaStreamCaptureStatusActive) {
+        // a graph keeps its scratch for its whole life: a buffer of its own, allocated outside the capture
+        // (relaxed mode: cudaMalloc does not touch the captured stream) and freed with the ctx
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        AC_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
+        void *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        if (e != cudaSuccess) return cuda_status(e, "scratch (graph capture)");
+        ctx->graph_owned.push_back(p);
+        *out = p;
+        return ATTNCACHE_OK;
+    }
+    Scratch &s = ctx->scratch[st].s[kind];
+    if (s.bytes < bytes) {
+        // stream-ordered: the old buffer is released after the work already queued on this stream
+        if (s.ptr) AC_CUDA(cudaFreeAsync(s.ptr, st));
         s.ptr = nullptr;
         s.bytes = 0;
+        const size_t cap = bytes < 4096 ? 4096 : bytes + bytes / 4;
+        AC_CUDA(cudaMallocAsync(&s.ptr, cap, st));
+        s.bytes = cap;
     }
-    size_t cap = bytes < 4096 ? 4096 : bytes + bytes / 2;
-    AC_CUDA(cudaMalloc(&s.ptr, cap));
-    s.bytes = cap;
+    *out = s.ptr;
     return ATTNCACHE_OK;
 }
-
-// A device pointer check: rejects host (unregistered or pinned) memory when the runtime can tell.
-static bool is_device_ptr(const void *p) {
-    cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
-}
-
-static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
-
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        int cur;
-        cudaGetDevice(&cur);
-        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-    }
-};
 
 }  // namespace ac
 
@@ -95,13 +89,14 @@ const char *attncache_status_string(attncache_status s) {
     case ATTNCACHE_ERR_CUDA: return "ATTNCACHE_ERR_CUDA";
     case ATTNCACHE_ERR_STATE: return "ATTNCACHE_ERR_STATE";
     case ATTNCACHE_ERR_UNSUPPORTED: return "ATTNCACHE_ERR_UNSUPPORTED";
+    case ATTNCACHE_ERR_NCCL: return "ATTNCACHE_ERR_NCCL";
     }
     return "ATTNCACHE_ERR_UNKNOWN";
 }
 
 const char *attncache_last_error(void) { return g_err; }
 
-int32_t attncache_version(void) { return 100; }
+int32_t attncache_version(void) { return 200; }
 
 uint64_t attncache_launch_count(void) { return ac::launch_count(); }
 
@@ -118,9 +113,13 @@ const char *attncache_variant(int32_t kind, int32_t dtype, int32_t seq_len, int3
 
 // ---- lifecycle ------------------------------------------------------------------------------
 
-attncache_status attncache_ctx_create(int32_t device, attncache_ctx **out) {
+attncache_status attncache_ctx_create(int32_t device, int32_t rank, int32_t world, const uint8_t *uid,
+                                      attncache_ctx **out) {
     if (!out) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_create: out is NULL");
     *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world)
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_create: rank %d of world %d", rank, world);
+    if (world > 1 && !uid) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_create: world %d needs a unique id", world);
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
     if (e != cudaSuccess || n == 0) {
@@ -137,13 +136,31 @@ attncache_status attncache_ctx_create(int32_t device, attncache_ctx **out) {
     attncache_ctx *c = new attncache_ctx();
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
+    const char *fr = getenv("ATTNCACHE_FORCE_ROUTE");
+    c->force_route = fr && *fr == '1';
     e = cudaMalloc(&c->d_error, sizeof(int));
     if (e == cudaSuccess) e = cudaMemset(c->d_error, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_small, sizeof(int64_t) * kPinnedInts);
+    if (e == cudaSuccess) e = cudaMallocHost(&c->h_pinned, sizeof(int64_t) * kPinnedInts);
     if (e != cudaSuccess) {
-        delete c;
+        attncache_ctx_destroy(c);
         return cuda_status(e, "ctx_create: scratch");
     }
+    if (uid) {  // COLLECTIVE: every rank of the world calls ctx_create with the same uid
+        attncache_status s = comm_init(c, rank, world, uid);
+        if (s) {
+            attncache_ctx_destroy(c);
+            return s;
+        }
+    }
     *out = c;
+    return ATTNCACHE_OK;
+}
+
+attncache_status attncache_ctx_info(const attncache_ctx *ctx, int32_t *rank, int32_t *world) {
+    if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_info: ctx is NULL");
+    if (rank) *rank = ctx->rank;
+    if (world) *world = ctx->world;
     return ATTNCACHE_OK;
 }
 
@@ -151,12 +168,16 @@ attncache_status attncache_ctx_destroy(attncache_ctx *ctx) {
     if (!ctx) return ATTNCACHE_OK;
     DeviceGuard g(ctx->device);
     cudaDeviceSynchronize();
+    comm_destroy(ctx);
     cudaFree(ctx->d_error);
-    cudaFree(ctx->apply_list.ptr);
-    cudaFree(ctx->attend_list.ptr);
-    cudaFree(ctx->search_keys.ptr);
-    cudaFree(ctx->project_buf.ptr);
-    cudaFree(ctx->plan_buf.ptr);
+    cudaFree(ctx->d_small);
+    if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+    for (auto &kv : ctx->scratch)
+        for (auto &sc : kv.second.s)
+            if (sc.ptr) cudaFree(sc.ptr);
+    for (void *p : ctx->graph_owned) cudaFree(p);
+    for (int i = 0; i < 3; ++i)
+        if (ctx->io_stream[i]) cudaStreamDestroy(ctx->io_stream[i]);
     delete ctx;
     return ATTNCACHE_OK;
 }
@@ -165,6 +186,8 @@ attncache_status attncache_ctx_sync(attncache_ctx *ctx) {
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_sync: ctx is NULL");
     DeviceGuard g(ctx->device);
     AC_CUDA(cudaDeviceSynchronize());
+    attncache_status s = comm_check(ctx);
+    if (s) return s;
     int flags = 0;
     AC_CUDA(cudaMemcpy(&flags, ctx->d_error, sizeof(int), cudaMemcpyDeviceToHost));
     if (flags) {
@@ -217,19 +240,31 @@ attncache_status attncache_db_load(attncache_ctx *ctx, const attncache_db_desc *
     db->ctx = ctx;
     db->d = *d;
     if (!has_maps) db->d.maps = nullptr;
+    attncache_status s = db_load_collective(db);  // COLLECTIVE with a communicator: checks the shard tiling
+    if (s) {
+        attncache_db_free(db);
+        return s;
+    }
     *out = db;
     return ATTNCACHE_OK;
 }
 
 attncache_status attncache_db_free(attncache_db *db) {
+    if (!db) return ATTNCACHE_OK;
+    if (db->d_shard_begins) {
+        DeviceGuard g(db->ctx->device);
+        cudaFree(db->d_shard_begins);
+    }
     delete db;
     return ATTNCACHE_OK;
 }
 
 // ---- search ---------------------------------------------------------------------------------
 
-static attncache_status search_keys_impl(attncache_db *db, const void *queries, int64_t n, uint64_t *keys,
-                                         cudaStream_t st) {
+}  // extern "C"
+
+attncache_status ac::search_keys_impl(attncache_db *db, const void *queries, int64_t n, uint64_t *keys,
+                                      cudaStream_t st) {
     const attncache_db_desc &d = db->d;
     AC_CUDA(cudaMemsetAsync(keys, 0, sizeof(uint64_t) * (size_t)n, st));
     if (d.shard_count == 0 || n == 0) return ATTNCACHE_OK;
@@ -237,10 +272,15 @@ static attncache_status search_keys_impl(attncache_db *db, const void *queries, 
         AC_CUDA(launch_search_tc(queries, d.feats, n, d.shard_count, d.feat_dim, d.shard_begin, keys,
                                  db->ctx->sm_count, st));
     } else {
+        if (d.feat_dim > kSimtMaxLen)
+            return fail(ATTNCACHE_ERR_SHAPE, "search: feat_dim %d of dtype %d takes the CUDA-core kernel, which holds "
+                        "at most %d elements per query", d.feat_dim, d.feat_dtype, kSimtMaxLen);
         AC_CUDA(launch_search_ffma(d.feat_dtype, queries, d.feats, n, d.shard_count, d.feat_dim, d.shard_begin, keys, st));
     }
     return ATTNCACHE_OK;
 }
+
+extern "C" {
 
 static attncache_status check_queries(attncache_db *db, const void *queries, int64_t n) {
     if (!db) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: db is NULL");
@@ -270,25 +310,39 @@ attncache_status attncache_keys_decode(const uint64_t *keys, int32_t n_shards, i
     return ATTNCACHE_OK;
 }
 
-attncache_status attncache_search(attncache_db *db, const void *queries, int64_t n, float tau, int64_t *idx,
-                                  float *score, uint8_t *hit, void *stream) {
+static attncache_status search_common(attncache_db *db, const void *queries, int64_t n, float tau, int64_t *idx,
+                                      float *score, uint8_t *hit, bool all, void *stream) {
     attncache_status s = check_queries(db, queries, n);
     if (s) return s;
     if (std::isnan(tau)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: tau is NaN");
     if (db->d.n_global == 0) return fail(ATTNCACHE_ERR_EMPTY, "search: the database has no entries");
+    DeviceGuard g(db->ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (db->ctx->comm) {  // COLLECTIVE: C1 query all-gather, K1, C2 key max-all-reduce, K2
+        if (n > 0 && !all && (!idx || !score || !hit)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: NULL output");
+        return search_collective(db, queries, n, tau, all, idx, score, hit, st);
+    }
     if (db->d.shard_count != db->d.n_global)
-        return fail(ATTNCACHE_ERR_STATE, "search: this db is one shard of %lld; use search_keys + keys_decode",
-                    (long long)db->d.n_global);
+        return fail(ATTNCACHE_ERR_STATE, "search: this db is one shard of %lld and the ctx has no communicator; use "
+                    "search_keys + keys_decode, or a ctx created with rank/world/uid", (long long)db->d.n_global);
     if (n == 0) return ATTNCACHE_OK;
     if (!idx || !score || !hit) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: NULL output");
-    DeviceGuard g(db->ctx->device);
-    s = ensure_scratch(db->ctx->search_keys, sizeof(uint64_t) * (size_t)n);
-    if (s) return s;
-    uint64_t *keys = (uint64_t *)db->ctx->search_keys.ptr;
-    s = search_keys_impl(db, queries, n, keys, (cudaStream_t)stream);
-    if (s) return s;
-    AC_CUDA(launch_keys_decode(keys, 1, n, tau, idx, score, hit, (cudaStream_t)stream));
+    void *keys = nullptr;
+    if ((s = scratch(db->ctx, st, kScSearchKeys, sizeof(uint64_t) * (size_t)n, &keys))) return s;
+    if ((s = search_keys_impl(db, queries, n, (uint64_t *)keys, st))) return s;
+    AC_CUDA(launch_keys_decode((const uint64_t *)keys, 1, n, tau, idx, score, hit, st));
     return ATTNCACHE_OK;
+}
+
+attncache_status attncache_search(attncache_db *db, const void *queries, int64_t n, float tau, int64_t *idx,
+                                  float *score, uint8_t *hit, void *stream) {
+    return search_common(db, queries, n, tau, idx, score, hit, false, stream);
+}
+
+attncache_status attncache_search_all(attncache_db *db, const void *queries, int64_t n, float tau, int64_t *idx,
+                                      float *score, uint8_t *hit, void *stream) {
+    if (n > 0 && (!idx || !score || !hit)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search_all: NULL output");
+    return search_common(db, queries, n, tau, idx, score, hit, true, stream);
 }
 
 // ---- apply ----------------------------------------------------------------------------------
@@ -302,18 +356,9 @@ static int sm_override(const char *name, int def) {
 static inline int sm_override(const char *, int def) { return def; }
 #endif
 
-attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
-                                        int32_t layer_begin, int32_t layer_end, int32_t head_dim, int32_t act_dtype,
-                                        const void *V, void *O, void *stream) {
-    if (!db) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: db is NULL");
-    return attncache_apply_cached_gqa(db, idx, hit, n_rows, layer_begin, layer_end, head_dim, db->d.n_heads, act_dtype,
-                                      V, O, stream);
-}
-
-attncache_status attncache_apply_cached_gqa(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
-                                            int32_t layer_begin, int32_t layer_end, int32_t head_dim,
-                                            int32_t n_kv_heads, int32_t act_dtype, const void *V, void *O,
-                                            void *stream) {
+static attncache_status apply_check(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                    int32_t layer_begin, int32_t layer_end, int32_t head_dim, int32_t n_kv_heads,
+                                    int32_t act_dtype, const void *V, void *O) {
     if (!db) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: db is NULL");
     const attncache_db_desc &d = db->d;
     if (d.n_layers <= 0) return fail(ATTNCACHE_ERR_STATE, "apply_cached: this database holds no maps");
@@ -332,10 +377,20 @@ attncache_status attncache_apply_cached_gqa(attncache_db *db, const int64_t *idx
         return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: idx/hit/V/O must be device memory");
     if (!aligned16(V) || !aligned16(O) || ((int64_t)head_dim * dtype_size(act_dtype)) % 16)
         return fail(ATTNCACHE_ERR_ALIGNMENT, "apply_cached: V/O base or row pitch (head_dim*elem) not 16-byte aligned");
+    return ATTNCACHE_OK;
+}
+
+}  // extern "C"
+
+attncache_status ac::apply_local_impl(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                      int32_t layer_begin, int32_t layer_end, int32_t head_dim, int32_t n_kv_heads,
+                                      int32_t act_dtype, const void *V, void *O, cudaStream_t st) {
+    attncache_status s = apply_check(db, idx, hit, n_rows, layer_begin, layer_end, head_dim, n_kv_heads, act_dtype, V, O);
+    if (s || n_rows == 0) return s;
+    const attncache_db_desc &d = db->d;
     DeviceGuard g(db->ctx->device);
-    cudaStream_t st = (cudaStream_t)stream;
-    attncache_status s = ensure_scratch(db->ctx->apply_list, rowlist_bytes(n_rows));
-    if (s) return s;
+    void *list = nullptr;
+    if ((s = scratch(db->ctx, st, kScApplyList, rowlist_bytes(n_rows), &list))) return s;
     ApplyArgs a;
     a.maps = d.maps;
     a.L = d.n_layers;
@@ -352,7 +407,7 @@ attncache_status attncache_apply_cached_gqa(attncache_db *db, const int64_t *idx
     a.Hkv = n_kv_heads;
     a.V = V;
     a.O = O;
-    a.list = rowlist_view(db->ctx->apply_list.ptr, n_rows);
+    a.list = rowlist_view(list, n_rows);
     a.max_rows = n_rows;
     AC_CUDA(launch_select_apply(idx, hit, n_rows, d.shard_begin, d.shard_count, a.list, db->ctx->d_error, st));
     if (apply_tc_supported(d.map_dtype, act_dtype, d.seq_len, head_dim)) {
@@ -361,6 +416,42 @@ attncache_status attncache_apply_cached_gqa(attncache_db *db, const int64_t *idx
         AC_CUDA(launch_apply_ffma(a, db->ctx->sm_count, st));
     }
     return ATTNCACHE_OK;
+}
+
+extern "C" {
+
+attncache_status attncache_apply_cached_local(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                              int32_t layer_begin, int32_t layer_end, int32_t head_dim,
+                                              int32_t n_kv_heads, int32_t act_dtype, const void *V, void *O,
+                                              void *stream) {
+    return apply_local_impl(db, idx, hit, n_rows, layer_begin, layer_end, head_dim, n_kv_heads, act_dtype, V, O,
+                            (cudaStream_t)stream);
+}
+
+attncache_status attncache_apply_cached_gqa(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                            int32_t layer_begin, int32_t layer_end, int32_t head_dim,
+                                            int32_t n_kv_heads, int32_t act_dtype, const void *V, void *O,
+                                            void *stream) {
+    attncache_status s = apply_check(db, idx, hit, n_rows, layer_begin, layer_end, head_dim, n_kv_heads, act_dtype, V, O);
+    if (s) return s;
+    attncache_ctx *ctx = db->ctx;
+    if (ctx->comm && (ctx->world > 1 || ctx->force_route)) {  // COLLECTIVE: route hits to the owner and O back
+        if (n_rows && hit && !is_device_ptr(hit))
+            return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: hit must be device memory");
+        DeviceGuard g(ctx->device);
+        return apply_routed(db, idx, hit, n_rows, layer_begin, layer_end, head_dim, n_kv_heads, act_dtype, V, O,
+                            (cudaStream_t)stream);
+    }
+    return apply_local_impl(db, idx, hit, n_rows, layer_begin, layer_end, head_dim, n_kv_heads, act_dtype, V, O,
+                            (cudaStream_t)stream);
+}
+
+attncache_status attncache_apply_cached(attncache_db *db, const int64_t *idx, const uint8_t *hit, int64_t n_rows,
+                                        int32_t layer_begin, int32_t layer_end, int32_t head_dim, int32_t act_dtype,
+                                        const void *V, void *O, void *stream) {
+    if (!db) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: db is NULL");
+    return attncache_apply_cached_gqa(db, idx, hit, n_rows, layer_begin, layer_end, head_dim, db->d.n_heads, act_dtype,
+                                      V, O, stream);
 }
 
 // ---- attend ---------------------------------------------------------------------------------
@@ -388,9 +479,13 @@ attncache_status attncache_attend_full_gqa(attncache_ctx *ctx, int64_t batch, in
         return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "attend_full: Q/K/V/O/skip must be device memory");
     if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || ((int64_t)dd * dtype_size(act_dtype)) % 16)
         return fail(ATTNCACHE_ERR_ALIGNMENT, "attend_full: base or row pitch (head_dim*elem) not 16-byte aligned");
+    if (!attend_tc_supported(act_dtype, S, dd) && S > kSimtMaxLen)
+        return fail(ATTNCACHE_ERR_SHAPE, "attend_full: seq_len %d takes the CUDA-core kernel (dtype %d, head_dim %d), "
+                    "which holds at most %d keys per row", S, act_dtype, dd, kSimtMaxLen);
     DeviceGuard g(ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
-    attncache_status s = ensure_scratch(ctx->attend_list, rowlist_bytes(batch));
+    void *list = nullptr;
+    attncache_status s = scratch(ctx, st, kScAttendList, rowlist_bytes(batch), &list);
     if (s) return s;
     AttendArgs a;
     a.L = L;
@@ -404,7 +499,7 @@ attncache_status attncache_attend_full_gqa(attncache_ctx *ctx, int64_t batch, in
     a.K = K;
     a.V = V;
     a.O = O;
-    a.list = rowlist_view(ctx->attend_list.ptr, batch);
+    a.list = rowlist_view(list, batch);
     a.max_rows = batch;
     AC_CUDA(launch_select_attend(skip, batch, a.list, st));
     if (attend_tc_supported(act_dtype, S, dd)) {
@@ -442,7 +537,8 @@ attncache_status attncache_project_features(attncache_ctx *ctx, const void *h, i
     // scratch: z [n][Hd] (act dtype) then y [n][D] fp32, 256-byte aligned
     const size_t zb = ((size_t)n * hidden_dim * es + 255) & ~(size_t)255;
     const size_t yb = (size_t)n * feat_dim * 4;
-    attncache_status s = ensure_scratch(ctx->project_buf, zb + yb);
+    void *buf = nullptr;
+    attncache_status s = scratch(ctx, (cudaStream_t)stream, kScProject, zb + yb, &buf);
     if (s) return s;
     ProjectArgs a;
     a.M = n;
@@ -456,8 +552,8 @@ attncache_status attncache_project_features(attncache_ctx *ctx, const void *h, i
     a.W2 = W2;
     a.b1 = b1;
     a.b2 = b2;
-    a.z = ctx->project_buf.ptr;
-    a.y = (float *)((uint8_t *)ctx->project_buf.ptr + zb);
+    a.z = buf;
+    a.y = (float *)((uint8_t *)buf + zb);
     a.f = features;
     AC_CUDA(launch_project(a, ctx->sm_count, (cudaStream_t)stream));
     return ATTNCACHE_OK;
@@ -508,9 +604,13 @@ attncache_status attncache_capture_maps_gqa(attncache_ctx *ctx, int64_t batch, i
         return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "capture_maps: Q/K/maps_out/skip must be device memory");
     if (!aligned16(Q) || !aligned16(K) || !aligned16(maps_out) || ((int64_t)dd * dtype_size(act_dtype)) % 16)
         return fail(ATTNCACHE_ERR_ALIGNMENT, "capture_maps: base or row pitch not 16-byte aligned");
+    if (!capture_tc_supported(act_dtype, S, dd) && S > kSimtMaxLen)
+        return fail(ATTNCACHE_ERR_SHAPE, "capture_maps: seq_len %d takes the CUDA-core kernel (dtype %d, head_dim %d), "
+                    "which holds at most %d keys per row", S, act_dtype, dd, kSimtMaxLen);
     DeviceGuard g(ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
-    attncache_status s = ensure_scratch(ctx->attend_list, rowlist_bytes(batch));
+    void *list = nullptr;
+    attncache_status s = scratch(ctx, st, kScAttendList, rowlist_bytes(batch), &list);
     if (s) return s;
     CaptureArgs a;
     a.L = L;
@@ -526,7 +626,7 @@ attncache_status attncache_capture_maps_gqa(attncache_ctx *ctx, int64_t batch, i
     a.Q = Q;
     a.K = K;
     a.maps = maps_out;
-    a.list = rowlist_view(ctx->attend_list.ptr, batch);
+    a.list = rowlist_view(list, batch);
     a.max_rows = batch;
     AC_CUDA(launch_select_attend(skip, batch, a.list, st));
     if (capture_tc_supported(act_dtype, S, dd)) {
@@ -608,7 +708,8 @@ attncache_status attncache_affinity_plan_device(attncache_ctx *ctx, const int64_
         if (sb[r + 1] < sb[r] || hb[r + 1] < hb[r])
             return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan_device: begins decreasing at %d", r);
     DeviceGuard g(ctx->device);
-    attncache_status s = ensure_scratch(ctx->plan_buf, (size_t)std::max<int64_t>(n, 1) * sizeof(int64_t));
+    void *buf = nullptr;
+    attncache_status s = scratch(ctx, (cudaStream_t)stream, kScPlan, (size_t)std::max<int64_t>(n, 1) * sizeof(int64_t), &buf);
     if (s) return s;
     ac::PlanArgs a;
     a.world = world;
@@ -619,7 +720,7 @@ attncache_status attncache_affinity_plan_device(attncache_ctx *ctx, const int64_
         a.shard_begins[r] = sb[r];
         a.home_begins[r] = hb[r];
     }
-    AC_CUDA(ac::launch_affinity_plan(idx, hit, n, a, assign, load, (int64_t *)ctx->plan_buf.ptr, loc, idx_loc, hit_loc,
+    AC_CUDA(ac::launch_affinity_plan(idx, hit, n, a, assign, load, (int64_t *)buf, loc, idx_loc, hit_loc,
                                      send_order, counts, (cudaStream_t)stream));
     return ATTNCACHE_OK;
 }
@@ -632,7 +733,7 @@ static attncache_status copy_rows(const void *src, const int64_t *rows, int64_t 
     const bool ok16 = row_bytes % 16 == 0 && aligned16(src) && aligned16(dst);
     const bool ok8 = row_bytes % 8 == 0 && ((uintptr_t)src & 7) == 0 && ((uintptr_t)dst & 7) == 0;
     if (!ok16 && !ok8) return fail(ATTNCACHE_ERR_ALIGNMENT, "copy_rows: rows and bases must be 8-byte multiples/aligned");
-    AC_CUDA(launch_copy_rows(src, rows, n, row_bytes, dst, gather, (cudaStream_t)stream));
+    AC_CUDA(launch_copy_rows(src, rows, n, row_bytes, dst, gather, ok16, (cudaStream_t)stream));
     return ATTNCACHE_OK;
 }
 

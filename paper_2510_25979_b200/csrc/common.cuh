@@ -88,24 +88,100 @@ struct Scratch {
     size_t bytes = 0;
 };
 
+// Scratch kinds.  Scratch is PER STREAM (work on two streams never shares a buffer) and stream-ordered
+// (cudaMallocAsync / cudaFreeAsync on the call's stream: growing a buffer never stalls the device, and the
+// old buffer is released only after the work queued before it on that stream).  A call issued while its
+// stream is being captured into a CUDA graph gets buffers of its own that live as long as the ctx, so a
+// graph's scratch is never freed or reused by later eager calls.
+enum ScratchKind : int {
+    kScApplyList = 0,  // compacted (row, entry) list for apply
+    kScAttendList,     // compacted row list for attend / capture
+    kScSearchKeys,     // per-query packed keys
+    kScProject,        // feature projector intermediates (z, y)
+    kScPlan,           // device affinity plan: the miss list
+    kScQueries,        // collective search: the gathered query batch
+    kScRoute,          // collective apply: owners, counts, order, idx rows
+    kScSend,           // collective apply / relocate: rows sent
+    kScRecv,           // collective apply / relocate: rows received
+    kScOut,            // collective apply: O of the received rows
+    kScBack,           // collective apply: O rows returned home
+    kScHost,           // host prefill: device staging
+    kNumScratch
+};
+struct StreamScratch {
+    Scratch s[kNumScratch];
+};
+
 }  // namespace ac
+
+#include <mutex>
+#include <unordered_map>
+#include <vector>
 
 struct attncache_ctx {
     int device = 0;
     int sm_count = 148;
     int *d_error = nullptr;  // deferred device-side error flags (bit 0: NOT_FOUND)
-    ac::Scratch apply_list;  // compacted (row, entry) list for apply
-    ac::Scratch attend_list; // compacted row list for attend
-    ac::Scratch search_keys; // per-query keys for single-rank search
-    ac::Scratch project_buf; // feature projector intermediates (z, y)
-    ac::Scratch plan_buf;    // device affinity plan: the miss list
+    // collectives (one NCCL communicator per ctx; world == 1 and comm == nullptr for a local ctx)
+    int rank = 0, world = 1;
+    void *comm = nullptr;            // ncclComm_t
+    int64_t *h_pinned = nullptr;     // pinned host staging for counts (kPinnedInts int64)
+    int64_t *d_small = nullptr;      // device staging for small exchanges (kPinnedInts int64)
+    std::vector<int64_t> layout;     // the per-rank home batch sizes set by attncache_set_batch_layout (or empty)
+    bool force_route = false;        // ATTNCACHE_FORCE_ROUTE=1: run the routed apply even at world 1 (tests)
+    cudaStream_t io_stream[3] = {};  // host prefill: copy-in, compute, copy-out (created on first use)
+    // scratch
+    std::mutex mu;
+    std::unordered_map<cudaStream_t, ac::StreamScratch> scratch;
+    std::vector<void *> graph_owned;  // buffers of calls captured into CUDA graphs (freed at destroy)
 };
 
 struct attncache_db {
     attncache_ctx *ctx = nullptr;
     attncache_db_desc d{};
+    std::vector<int64_t> shard_begins;  // [world + 1] global entry ranges of every rank (collective load)
+    int64_t *d_shard_begins = nullptr;  // device copy
 };
 
 namespace ac {
-attncache_status ensure_scratch(Scratch &s, size_t bytes);
+constexpr int kPinnedInts = 4 * 1024 + 16;
+// Device scratch of at least `bytes` for (stream, kind); see ScratchKind.
+attncache_status scratch(attncache_ctx *ctx, cudaStream_t st, int kind, size_t bytes, void **out);
+
+// A device pointer check: rejects host (unregistered or pinned) memory when the runtime can tell.
+inline bool is_device_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
+// Page-locked (pinned or registered) host memory: the only host memory the async copies accept.
+inline bool is_pinned_host_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+inline bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// ---- collectives (collective.cu) ----
+attncache_status comm_init(attncache_ctx *ctx, int rank, int world, const uint8_t uid[128]);
+void comm_destroy(attncache_ctx *ctx);
+}  // namespace ac

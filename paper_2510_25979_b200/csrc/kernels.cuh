@@ -63,6 +63,9 @@ struct AttendArgs {
     int64_t max_rows;
 };
 cudaError_t launch_attend_ffma(const AttendArgs &a, int sm_count, cudaStream_t st);
+// The CUDA-core attention / capture / search fallbacks keep one fp32 row of S (or D) values per warp in shared
+// memory (8 warps): 32 * S bytes <= 227 KB.
+constexpr int32_t kSimtMaxLen = 7264;
 bool attend_tc_supported(int32_t dt, int32_t S, int32_t d);
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st);
 cudaError_t launch_attend_split(const AttendArgs &a, int sm_count, cudaStream_t st);  // d = 128, double-buffered S
@@ -122,7 +125,8 @@ cudaError_t launch_pack_maps(const void *dense, int64_t n_maps, int32_t S, void 
 // ---- routing ----
 cudaError_t launch_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n, const int64_t *shard_begins,
                               int32_t world, int32_t *owner, int32_t *counts, int64_t *order, cudaStream_t st);
+// ok16: row_bytes % 16 == 0 and both bases 16-byte aligned (int4 accesses); else 8-byte accesses.
 cudaError_t launch_copy_rows(const void *src, const int64_t *rows, int64_t n_rows, int64_t row_bytes, void *dst,
-                             bool gather, cudaStream_t st);
+                             bool gather, bool ok16, cudaStream_t st);
 
 }  // namespace ac

@@ -152,12 +152,14 @@ cudaError_t launch_search_ffma(int32_t dt, const void *q, const void *x, int64_t
     size_t smem = sizeof(float) * kSearchQPB * D;
     switch (dt) {
     case ATTNCACHE_F32:
-        cudaFuncSetAttribute(search_simt_kernel<ATTNCACHE_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaError_t e = cudaFuncSetAttribute(search_simt_kernel<ATTNCACHE_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem)) return e;
         search_simt_kernel<ATTNCACHE_F32><<<grid, kSearchThreads, smem, st>>>(
             (const float *)q, (const float *)x, B, n, D, gbase, per_block, keys);
         break;
     case ATTNCACHE_BF16:
-        cudaFuncSetAttribute(search_simt_kernel<ATTNCACHE_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaError_t e = cudaFuncSetAttribute(search_simt_kernel<ATTNCACHE_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem)) return e;
         search_simt_kernel<ATTNCACHE_BF16><<<grid, kSearchThreads, smem, st>>>(
             (const __nv_bfloat16 *)q, (const __nv_bfloat16 *)x, B, n, D, gbase, per_block, keys);
         break;
@@ -310,7 +312,8 @@ cudaError_t launch_attend_ffma(const AttendArgs &a, int sm_count, cudaStream_t s
     size_t smem = sizeof(float) * 8 * a.S;
 #define AC_ATTEND(DT)                                                                                   \
     if (a.dt == DT) {                                                                                  \
-        cudaFuncSetAttribute(attend_simt_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        cudaError_t e_ = cudaFuncSetAttribute(attend_simt_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e_ != cudaSuccess) return e_;                                                              \
         attend_simt_kernel<DT><<<blocks, 256, smem, st>>>(a);                                         \
         return count_launches(1), cudaGetLastError();                                                                     \
     }
@@ -380,7 +383,8 @@ cudaError_t launch_capture_simt(const CaptureArgs &a, int sm_count, cudaStream_t
     size_t smem = sizeof(float) * 8 * a.S;
 #define AC_CAPTURE(DT, MDT)                                                                                  \
     if (a.dt == DT && a.map_dt == MDT) {                                                                    \
-        cudaFuncSetAttribute(capture_simt_kernel<DT, MDT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        cudaError_t e_ = cudaFuncSetAttribute(capture_simt_kernel<DT, MDT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e_ != cudaSuccess) return e_;                                                                   \
         capture_simt_kernel<DT, MDT><<<blocks, 256, smem, st>>>(a);                                         \
         return count_launches(1), cudaGetLastError();                                                       \
     }
@@ -510,7 +514,7 @@ __global__ void route_plan_kernel(const int64_t *idx, const uint8_t *hit, int64_
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int64_t b = tid; b < n; b += blockDim.x) {
         int o = -1;
-        if (hit[b]) {
+        if (hit ? hit[b] != 0 : idx[b] >= 0) {
             int64_t e = idx[b];
             for (int r = 0; r < world; ++r)
                 if (e >= sb[r] && e < sb[r + 1]) o = r;
@@ -554,29 +558,28 @@ cudaError_t launch_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n,
 template <typename W>
 __global__ void copy_rows_kernel(const W *src, const int64_t *rows, int64_t n_rows, int64_t row_words, W *dst,
                                  bool gather) {
-    const int64_t total = n_rows * row_words;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        int64_t k = t / row_words, w = t % row_words;
-        int64_t r = rows[k];
-        if (gather)
-            dst[k * row_words + w] = src[r * row_words + w];
-        else
-            dst[r * row_words + w] = src[k * row_words + w];
+    // rows over blockIdx.y (grid-stride), words of a row over blockIdx.x: no per-element 64-bit division
+    for (int64_t k = blockIdx.y; k < n_rows; k += gridDim.y) {
+        const int64_t r = rows[k];
+        const W *s = src + (gather ? r : k) * row_words;
+        W *d = dst + (gather ? k : r) * row_words;
+        for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < row_words; w += (int64_t)gridDim.x * blockDim.x)
+            d[w] = s[w];
     }
 }
 
 cudaError_t launch_copy_rows(const void *src, const int64_t *rows, int64_t n_rows, int64_t row_bytes, void *dst,
-                             bool gather, cudaStream_t st) {
+                             bool gather, bool ok16, cudaStream_t st) {
     if (n_rows == 0) return cudaSuccess;
-    if (row_bytes % 16 == 0) {
-        const int64_t words = row_bytes / 16;
-        int blocks = (int)min64((n_rows * words + 255) / 256, 148 * 16);
-        copy_rows_kernel<int4><<<blocks, 256, 0, st>>>((const int4 *)src, rows, n_rows, words, (int4 *)dst, gather);
-    } else {
-        const int64_t words = row_bytes / 8;
-        int blocks = (int)min64((n_rows * words + 255) / 256, 148 * 16);
-        copy_rows_kernel<int2><<<blocks, 256, 0, st>>>((const int2 *)src, rows, n_rows, words, (int2 *)dst, gather);
-    }
+    const int64_t words = ok16 ? row_bytes / 16 : row_bytes / 8;
+    // about 16 resident CTAs per SM in total: split between the rows and the words of a row
+    const int64_t gy = min64(n_rows, 65535);
+    const int64_t gx = max64(1, min64((words + 255) / 256, (148 * 16 + gy - 1) / gy));
+    const dim3 grid((unsigned)gx, (unsigned)gy);
+    if (ok16)  // 16-byte rows AND 16-byte aligned bases (an 8-byte aligned base takes the int2 path)
+        copy_rows_kernel<int4><<<grid, 256, 0, st>>>((const int4 *)src, rows, n_rows, words, (int4 *)dst, gather);
+    else
+        copy_rows_kernel<int2><<<grid, 256, 0, st>>>((const int2 *)src, rows, n_rows, words, (int2 *)dst, gather);
     return count_launches(1), cudaGetLastError();
 }
 

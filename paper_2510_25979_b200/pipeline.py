@@ -12,8 +12,8 @@ from typing import Optional
 
 import torch
 
-from . import (Context, Database, attncache_apply_cached, attncache_attend_full, attncache_project_features,
-               attncache_search)
+from . import (Context, Database, attncache_apply_cached, attncache_attend_full, attncache_prefill_host,
+               attncache_project_features, attncache_search)
 
 
 class PrefillStep:
@@ -114,66 +114,22 @@ class PerLayerPrefill:
 
 
 class HostPrefill:
-    """The same step end to end from (pinned) host buffers, pipelined over chunks of the batch.
+    """The same step end to end from pinned host buffers: one C-ABI call (attncache_prefill_host) that does
+    every copy inside the library - H2D of the queries, search, D2H of the decisions, then chunk-pipelined
+    H2D of V (every row) and Q, K (miss rows only: Alg. 2 computes q, k only on a miss), the kernels, and D2H
+    of O over a ring of `depth` device slots on three library streams.  Synchronous: when the call returns,
+    O_h and the returned idx/score/hit (pinned host tensors) hold the results."""
 
-    search on all queries (H2D of the queries, D2H of the hit mask: the host must know the misses,
-    whose Q and K exist only on a miss — Alg. 2 l.376-378), then per chunk of `chunk` rows: H2D of
-    V (every row) and of Q, K (miss rows only) on a copy-in stream, apply_cached + attend_full on the
-    compute stream, D2H of O on a copy-out stream.  A ring of `depth` device chunk buffers lets the
-    copies of chunk k+1 and k-1 overlap the kernels of chunk k (PCIe is full duplex).
-    """
-
-    def __init__(self, step: PrefillStep, chunk: int = 32, depth: int = 3):
+    def __init__(self, step: PrefillStep, chunk: int = 16, depth: int = 4):
         self.step, self.chunk, self.depth = step, int(chunk), int(depth)
-        self._dev = None
+        self._out = {}
 
-    def _buffers(self, row_shape, dtype, device):
-        key = (tuple(row_shape), dtype, device)
-        if self._dev is None or self._dev[0] != key:
-            c, R = self.chunk, self.depth
-            mk = lambda: [torch.empty((c, *row_shape), dtype=dtype, device=device) for _ in range(R)]
-            self._dev = (key, mk(), mk(), mk(), mk())  # V, Q, K, O rings
-        return self._dev[1:]
-
-    def __call__(self, q_h, Q_h, K_h, V_h, O_h, device=None):
-        device = device or self.step.db.device
-        comp = torch.cuda.current_stream(device)
-        cin, cout = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    def __call__(self, q_h, Q_h, K_h, V_h, O_h):
         B = q_h.shape[0]
-        qd = q_h.to(device, non_blocking=True)
-        idx, score, hit = self.step.search(qd)
-        hit_h = hit.cpu()  # one host sync: which rows need Q and K
-        Vr, Qr, Kr, Or = self._buffers(V_h.shape[1:], V_h.dtype, device)
-        R, c = self.depth, self.chunk
-        ev_in = [torch.cuda.Event() for _ in range(R)]
-        ev_comp = [torch.cuda.Event() for _ in range(R)]
-        ev_out = [torch.cuda.Event() for _ in range(R)]
-        used = [False] * R
-        n_chunks = (B + c - 1) // c
-        miss = (hit_h == 0).tolist()
-        for k in range(n_chunks):
-            r = k % R
-            b0, b1 = k * c, min(B, (k + 1) * c)
-            n = b1 - b0
-            with torch.cuda.stream(cin):
-                if used[r]:
-                    cin.wait_event(ev_comp[r])
-                Vr[r][:n].copy_(V_h[b0:b1], non_blocking=True)
-                for b in range(b0, b1):
-                    if miss[b]:
-                        Qr[r][b - b0].copy_(Q_h[b], non_blocking=True)
-                        Kr[r][b - b0].copy_(K_h[b], non_blocking=True)
-                ev_in[r].record(cin)
-            comp.wait_event(ev_in[r])
-            if used[r]:
-                comp.wait_event(ev_out[r])  # O slot drained to the host
-            self.step.attend(idx[b0:b1], hit[b0:b1], Qr[r][:n], Kr[r][:n], Vr[r][:n], Or[r][:n], stream=comp)
-            ev_comp[r].record(comp)
-            with torch.cuda.stream(cout):
-                cout.wait_event(ev_comp[r])
-                O_h[b0:b1].copy_(Or[r][:n], non_blocking=True)
-                ev_out[r].record(cout)
-            used[r] = True
-        comp.wait_stream(cout)
-        res = tuple(t.to("cpu", non_blocking=True) for t in (idx, score, hit))
-        return res
+        if B not in self._out:
+            self._out[B] = tuple(torch.empty(B, dtype=dt).pin_memory() for dt in (torch.int64, torch.float32,
+                                                                                  torch.uint8))
+        idx, score, hit = self._out[B]
+        attncache_prefill_host(self.step.db, q_h, Q_h, K_h, V_h, self.step.tau, O=O_h, idx=idx, score=score, hit=hit,
+                               chunk=self.chunk, depth=self.depth)
+        return idx, score, hit

@@ -12,13 +12,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import synth  # noqa: E402
 import paper_2510_25979_b200 as ac  # noqa: E402
-from paper_2510_25979_b200.dist import AffinityPrefill, CudaOps  # noqa: E402
+from paper_2510_25979_b200.dist import AffinityPrefill  # noqa: E402
 
 cfg = synth.CONFIGS[os.environ.get("CFG", "llama32_1b")]
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(dev)
 dist.init_process_group("nccl", device_id=dev)
-ctx = ac.Context(0)
+ctx = ac.Context.from_process_group(0)
 x = synth.features(cfg, 0, cfg.N, dev)
 maps = ac.pack_db_maps(lambda b, out: synth.fill_maps(cfg, out, b), cfg.N, cfg.L, cfg.H, cfg.S,
                        synth.torch_dtype(cfg.map_dtype), dev, chunk=max(1, (1 << 30) // cfg.map_bytes_per_entry))
@@ -27,11 +27,10 @@ q, _, _ = synth.queries(cfg, dev)
 Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=dev) for k in "qkv")
 O = torch.empty_like(V)
 X = torch.randn(cfg.B, cfg.S, cfg.H * cfg.d, device=dev).to(torch.bfloat16)
-step = AffinityPrefill(CudaOps(ctx, db), cfg.N, cfg.tau, bench.apply_bytes_per_hit(cfg), bench.attend_bytes_per_miss(cfg),
-                       device=dev)
 sizes = [cfg.B]
+step = AffinityPrefill(ctx, db, cfg.tau, sizes, bench.apply_bytes_per_hit(cfg), bench.attend_bytes_per_miss(cfg))
 for _ in range(3):
-    p = step.plan(q, sizes)
+    p = step.plan(q)
     step.relocate(X, p)
     step.apply_local(p, p["loc"], V, O, Q, K)
 torch.cuda.synchronize()
@@ -40,11 +39,11 @@ host = []
 res = []
 for it in range(10):
     ev[0].record()
-    idx, score, hit, _ = step.search_all(q, sizes)
+    ac.attncache_search_all(db, q, cfg.tau, total=cfg.B)
     ev[1].record()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    p = step.plan(q, sizes)  # includes a second search (host planning measured separately below)
+    p = step.plan(q)  # includes a second search (host planning measured separately below)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     ev[2].record()
@@ -67,7 +66,7 @@ print({n: round(st.median(r[i] for r in res), 4) for i, n in enumerate(names)})
 s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s0.record()
 for _ in range(10):
-    p = step.plan(q, sizes)
+    p = step.plan(q)
     step.relocate(X, p)
     step.apply_local(p, p["loc"], V, O, Q, K)
 s1.record()

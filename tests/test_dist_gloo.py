@@ -1,5 +1,5 @@
-"""N>1 host logic on CPU: paper_2510_25979_b200.dist.ShardedPrefill under torch.distributed/gloo with
-world size 2 and 3, with the per-rank kernels replaced by reference ops built on the oracle.
+"""N>1 host logic on CPU: the collective protocol (tests/dist_model.py, the model of the library's COLLECTIVE calls) under
+torch.distributed/gloo with world size 2 and 3, with the per-rank kernels replaced by reference ops built on the oracle.
 
 Checks (north_star): the sharded search (query all-gather, local top-1 as packed
 keys, key all-gather + max) equals the single-process oracle search bit-for-bit (idx, hit), routed
@@ -105,7 +105,7 @@ def _worker(rank, world, port, homes):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2510_25979_b200.dist import ShardedPrefill, shard_range
+        from tests.dist_model import ShardedPrefill, shard_range
         cfg = synth.CONFIGS["tiny"]
         x = synth.features(cfg, 0, cfg.N)
         x[200] = x[3]                                     # duplicate across shards: global top-1 is 3
@@ -151,7 +151,7 @@ def _affinity_worker(rank, world, port, homes):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2510_25979_b200.dist import AffinityPrefill, shard_range
+        from tests.dist_model import AffinityPrefill, shard_range
         cfg = synth.CONFIGS["tiny"]
         x = synth.features(cfg, 0, cfg.N)
         x[200] = x[3]

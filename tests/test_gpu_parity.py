@@ -421,48 +421,53 @@ def test_full_step(ac, ctx, cfg_name):
     torch.cuda.empty_cache()
 
 
-def test_sharded_prefill_world1_matches_single_gpu_step(ac, ctx):
-    """The multi-GPU orchestration (dist.ShardedPrefill over NCCL) at world size 1 reproduces the
-    single-GPU step bitwise (the multi-rank host logic is covered by tests/test_dist_gloo.py)."""
-    import socket
-
-    import torch.distributed as dist
-
-    from paper_2510_25979_b200.dist import CudaOps, ShardedPrefill
+@pytest.mark.parametrize("layout", [False, True])
+def test_collective_ctx_world1_matches_single_gpu_step(ac, ctx, monkeypatch, layout):
+    """The library's collective calls over its own NCCL communicator (a world-1 ctx made from a unique id;
+    ATTNCACHE_FORCE_ROUTE makes apply_cached take the routed path - route plan, count exchange, V and idx
+    sent to the owner, A.V, O returned and scattered - even at world 1) reproduce the local single-GPU step
+    bitwise, with and without a declared batch layout (the counts all-gather + host sync vs none); the
+    owner-affinity calls (search_all, device plan, relocate_rows, local apply) likewise.  The multi-rank
+    protocol is covered by tests/test_dist_gloo.py and test_torchrun_world (>= 2 GPUs)."""
+    from paper_2510_25979_b200.dist import AffinityPrefill, ShardedPrefill
     from paper_2510_25979_b200.pipeline import PrefillStep
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
-                            device_id=torch.device("cuda", 0))
-    try:
-        cfg = synth.CONFIGS["llama32_1b"].with_(N=64, B=16, L=2)
-        x = synth.features(cfg, 0, cfg.N, DEV)
-        maps = ac.attncache_pack_maps(synth.maps(cfg, 0, cfg.N, DEV))
-        db = ac.Database(ctx, x, maps, packed=True, seq_len=cfg.S)
-        q, pos, tgt = synth.queries(cfg, DEV)
-        Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qkv")
-        O1, O2 = torch.empty_like(V), torch.empty_like(V)
-        r1 = PrefillStep(ctx, db, cfg.tau)(q, Q, K, V, O1)
-        r2 = ShardedPrefill(CudaOps(ctx, db), cfg.N, cfg.tau, device=DEV)(q, Q, K, V, O2)
-        torch.cuda.synchronize()
-        for a, b in zip(r1, r2):
-            assert torch.equal(a, b)
-        assert torch.equal(O1, O2)
-        # owner-affinity placement: at world size 1 every query is local and the result is the same
-        from paper_2510_25979_b200.dist import AffinityPrefill
-        aff = AffinityPrefill(CudaOps(ctx, db), cfg.N, cfg.tau, hit_cost=1.0, miss_cost=1.3, device=DEV)
-        plan = aff.plan(q)
-        loc = aff.local_queries(plan)
-        assert loc.tolist() == list(range(cfg.B))
-        X = torch.randn(cfg.B, cfg.S, 64, device=DEV, dtype=torch.bfloat16)
-        assert torch.equal(aff.relocate(X, plan), X)
-        O3 = torch.empty_like(V)
-        aff.apply_local(plan, loc, V, O3, Q, K)
-        torch.cuda.synchronize()
-        assert torch.equal(O1, O3)
-    finally:
-        dist.destroy_process_group()
+    monkeypatch.setenv("ATTNCACHE_FORCE_ROUTE", "1")
+    cctx = ac.Context(0, rank=0, world=1, uid=ac.attncache_get_unique_id())
+    assert ac.attncache_ctx_info(cctx) == (0, 1)
+    cfg = synth.CONFIGS["llama32_1b"].with_(N=64, B=16, L=2)
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    maps = ac.attncache_pack_maps(synth.maps(cfg, 0, cfg.N, DEV))
+    db = ac.Database(ctx, x, maps, packed=True, seq_len=cfg.S)
+    cdb = ac.Database(cctx, x, maps, packed=True, seq_len=cfg.S)          # collective load (world 1)
+    q, pos, tgt = synth.queries(cfg, DEV)
+    Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qkv")
+    O1, O2 = torch.empty_like(V), torch.empty_like(V)
+    r1 = PrefillStep(ctx, db, cfg.tau)(q, Q, K, V, O1)
+    r2 = ShardedPrefill(cctx, cdb, cfg.tau, sizes=[cfg.B] if layout else None)(q, Q, K, V, O2)
+    cctx.sync()
+    for a, b in zip(r1, r2):
+        assert torch.equal(a, b)
+    assert torch.equal(O1, O2)
+    # owner-affinity placement: at world size 1 every query is local and the result is the same
+    aff = AffinityPrefill(cctx, cdb, cfg.tau, sizes=[cfg.B], hit_cost=1.0, miss_cost=1.3)
+    plan = aff.plan(q)
+    loc = aff.local_queries(plan)
+    assert loc.tolist() == list(range(cfg.B))
+    assert torch.equal(plan["idx"], r1[0]) and torch.equal(plan["hit"], r1[2])
+    X = torch.randn(cfg.B, cfg.S, 64, device=DEV, dtype=torch.bfloat16)
+    assert torch.equal(aff.relocate(X, plan), X)
+    O3 = torch.empty_like(V)
+    aff.apply_local(plan, loc, V, O3, Q, K)
+    cctx.sync()
+    assert torch.equal(O1, O3)
+    # a layout that disagrees with the call is an error, not a hang
+    cctx.set_batch_layout([cfg.B + 1])
+    with pytest.raises(ac.AttnCacheError) as e:
+        ac.attncache_search(cdb, q, cfg.tau)
+    assert e.value.name == "ATTNCACHE_ERR_STATE"
+    cctx.set_batch_layout(None)
+    del cdb
+    cctx.close()
 
 
 def test_host_prefill_pipeline_matches_device_step(ac, ctx):
