@@ -151,6 +151,8 @@ typedef struct {
 } attncache_db_desc;
 
 attncache_status attncache_db_load(attncache_ctx *ctx, const attncache_db_desc *desc, attncache_db **out);
+/* Frees the db handle (never the borrowed tensors).  May run after its ctx is destroyed; every other call
+ * on a db needs its ctx alive. */
 attncache_status attncache_db_free(attncache_db *db);
 
 /* ---- Alg. 1: VecDB.search + theta gate -----------
@@ -306,6 +308,18 @@ attncache_status attncache_capture_maps_gqa(attncache_ctx *ctx, int64_t batch, i
                                             int32_t n_kv_heads, int32_t seq_len, int32_t head_dim, int32_t act_dtype,
                                             const void *Q, const void *K, float scale, const uint8_t *skip,
                                             int32_t map_dtype, int32_t map_layout, void *maps_out, void *stream);
+
+/* ---- projection GEMM for the Eq. 5 block-level comparison (Alg. 2 l.372 "v = V(h)",
+ * l.377-378 "q = Q(h)", "k = K(h)"; Eq. 5) ----------------------------------------
+ * Y = X W^T (+ bias): X [M][K] with M = B * seq_len rows (row m = sequence b, position s), W [N][K] (the
+ * nn.Linear layout), N = n_heads * head_dim; the result is stored HEAD-MAJOR, Y [B][n_heads][seq_len][head_dim]
+ * (the layout attncache_attend_full / attncache_apply_cached read, so no permute pass follows).  dtype for X, W
+ * and Y; fp32 accumulation, one rounding; bias: NULL or device fp32 [N].  BF16/F16 with K % 64 == 0,
+ * N % 64 == 0 and head_dim % 32 == 0: tcgen05 GEMM; other shapes / F32: CUDA cores.
+ * Errors: SHAPE (M not whole sequences, N not whole heads), DTYPE, ALIGNMENT, INVALID_ARGUMENT. */
+attncache_status attncache_linear(attncache_ctx *ctx, const void *X, int64_t M, int32_t K, const void *W, int32_t N,
+                                  int32_t dtype, const float *bias, int32_t seq_len, int32_t head_dim, void *Y,
+                                  void *stream);
 
 /* ---- RoPE for the Eq. 5 block-level comparison (Alg. 2 l.379) ----------
  * In place on X [n_units][S][d] (act_dtype): for i < d/2 the pair (x_i, x_{i+d/2}) at position p

@@ -54,6 +54,7 @@ def _load():
             lib.oracle_attention_map.argtypes = [P, P, I32, P, I64, I32, I32, D, P]
             lib.oracle_rope.argtypes = [P, I32, I64, I32, I32, D, P]
             lib.oracle_project.argtypes = [P, I64, I32, I32, P, P, I32, P, P, I32, P]
+            lib.oracle_linear.argtypes = [P, I64, I32, P, I32, I32, P]
             lib.oracle_decode.argtypes = [P, I64, I32]
             lib.oracle_decode.restype = D
             lib.oracle_set_threads.argtypes = [I32]
@@ -195,3 +196,16 @@ def project(h: np.ndarray, dtype: str, W1: np.ndarray, b1: np.ndarray, W2: np.nd
     f = np.empty((B, D), np.float64)
     _load().oracle_project(_ptr(h), B, E, _DT[dtype], _ptr(W1), _ptr(b1), Hd, _ptr(W2), _ptr(b2), D, _ptr(f))
     return f
+
+
+def linear(X: np.ndarray, W: np.ndarray, dtype: str) -> np.ndarray:
+    """Alg. 2 l.372 / l.377-378 projections (f4): Y = X W^T, X [M][K], W [N][K] (nn.Linear layout) -> f64 [M][N]."""
+    X = _raw(X, dtype)
+    W = _raw(W, dtype)
+    M, K = X.shape
+    N = W.shape[0]
+    if W.shape[1] != K:
+        raise ValueError("oracle.linear: X [M][K] and W [N][K] disagree on K")
+    Y = np.empty((M, N), np.float64)
+    _load().oracle_linear(_ptr(X), M, K, _ptr(W), N, _DT[dtype], _ptr(Y))
+    return Y

@@ -30,6 +30,9 @@
  *             projector of PAPER.md:278 ("two layers of Multi-Layer Perceptron
  *             ... maps the input embedding to a feature vector"): z = relu(W1 h
  *             + b1), y = W2 z + b2, f = y / ||y||_2 (readings R30-R32).
+ *   linear  — Alg. 2 l.372, l.377-378 "v = V(h)", "q = Q(h)", "k = K(h)": the
+ *             projections of the Eq. 5 block-level comparison (f4), Y = X W^T with W in the nn.Linear
+ *             layout [N][K] (reading R34).
  *
  * Parity pins for each function live in tests/test_oracle_pins.py.
  */
@@ -280,4 +283,16 @@ void oracle_project(const void *h, int64_t B, int32_t E, int32_t dtype, const vo
         for (int32_t c = 0; c < D; ++c) y[c] = norm > 0.0 ? y[c] / norm : 0.0;
         free(z);
     }
+}
+
+/* ---- projections: Alg. 2 l.372, l.377-378 -------------
+ * Y[m][n] = sum_k X[m][k] * W[n][k]: X [M][K], W [N][K] (the nn.Linear layout) in `dtype`; Y [M][N] fp64. */
+void oracle_linear(const void *X, int64_t M, int32_t K, const void *W, int32_t N, int32_t dtype, double *Y) {
+#pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m)
+        for (int32_t n = 0; n < N; ++n) {
+            double s = 0.0;
+            for (int32_t k = 0; k < K; ++k) s += load(X, m * K + k, dtype) * load(W, (int64_t)n * K + k, dtype);
+            Y[m * N + n] = s;
+        }
 }

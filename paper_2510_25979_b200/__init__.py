@@ -28,7 +28,7 @@ __all__ = [
     "attncache_affinity_plan", "attncache_project_features", "attncache_apply_cached_gqa", "attncache_attend_full_gqa",
     "attncache_capture_maps_gqa", "attncache_affinity_plan_device", "ABI_FUNCTIONS", "attncache_get_unique_id",
     "attncache_ctx_info", "attncache_set_batch_layout", "attncache_search_all", "attncache_apply_cached_local",
-    "attncache_relocate_rows", "attncache_prefill_host",
+    "attncache_relocate_rows", "attncache_prefill_host", "attncache_linear",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -45,6 +45,7 @@ ABI_FUNCTIONS = [
     "attncache_apply_cached_gqa", "attncache_attend_full_gqa", "attncache_capture_maps_gqa",
     "attncache_affinity_plan_device", "attncache_get_unique_id", "attncache_ctx_info", "attncache_set_batch_layout",
     "attncache_search_all", "attncache_apply_cached_local", "attncache_relocate_rows", "attncache_prefill_host",
+    "attncache_linear",
 ]
 
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -99,6 +100,7 @@ def load_library():
         "attncache_search_all": ([P, P, I64, F32, P, P, P, P], I32),
         "attncache_apply_cached_local": ([P, P, P, I64, I32, I32, I32, I32, I32, P, P, P], I32),
         "attncache_relocate_rows": ([P, P, I64, I64, P, P, P, P], I32),
+        "attncache_linear": ([P, P, I64, I32, P, I32, I32, P, I32, I32, P, P], I32),
         "attncache_prefill_host": ([P, P, I64, F32, P, P, P, I32, I32, P, P, P, P, I32, I32], I32),
         "attncache_ctx_destroy": ([P], I32),
         "attncache_ctx_sync": ([P], I32),
@@ -635,6 +637,30 @@ def attncache_capture_maps_gqa(ctx: Context, Q, K, map_dtype=torch.bfloat16, pac
                                scale: float = 0.0, skip=None, stream=None):
     """Grouped-query capture (the C call of the same name): K with Hkv heads, one map per query head."""
     return attncache_capture_maps(ctx, Q, K, map_dtype, packed, out, scale, skip, stream)
+
+
+def attncache_linear(ctx: Context, X: torch.Tensor, W: torch.Tensor, n_heads: int, bias=None, out=None,
+                     stream=None) -> torch.Tensor:
+    """f4 projection (Alg. 2 l.372, l.377-378): X [B][S][K] times W [N][K] (nn.Linear layout, N = n_heads * d),
+    stored head-major as [B][1][n_heads][S][d] (one layer; the layout attend_full / apply_cached read)."""
+    _dev(X, "X")
+    _dev(W, "W")
+    if X.dim() != 3 or W.dim() != 2 or W.shape[1] != X.shape[2] or X.dtype != W.dtype or W.shape[0] % n_heads:
+        raise ValueError("linear: X [B][S][K], W [N][K] (one dtype), N a multiple of n_heads")
+    B, S, K = X.shape
+    N = W.shape[0]
+    d = N // n_heads
+    out = torch.empty(B, 1, n_heads, S, d, dtype=X.dtype, device=X.device) if out is None else out
+    _dev(out, "out")
+    if out.numel() != B * N * S or out.dtype != X.dtype:
+        raise ValueError("linear: out must hold [B][n_heads][S][d] elements of X's dtype")
+    if bias is not None:
+        _dev(bias, "bias")
+        if bias.dtype != torch.float32 or bias.shape != (N,):
+            raise ValueError("linear: bias must be float32 [N]")
+    _check(load_library().attncache_linear(ctx.handle, _p(X), B * S, K, _p(W), N, _DT[X.dtype], _p(bias), S, d,
+                                           _p(out), _stream(stream, X.device)))
+    return out
 
 
 def attncache_rope(X: torch.Tensor, base: float = 10000.0, stream=None) -> torch.Tensor:

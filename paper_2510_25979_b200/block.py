@@ -6,20 +6,21 @@ One attention block of one layer over a query batch, the two ways Alg. 2 runs it
   cached (hit,  Alg. 2 l.373-375):  V = X W_V, O = A_cached . V        ("Q and K are neither computed
                                                                         nor stored")
 
-The projections are plain library GEMMs (torch.matmul -> cuBLAS, [B*S][E] x [E][H*d]) followed by a
-copy into the head-major [B][H][S][d] layout the kernels read (the same cost on both paths); RoPE,
-A.V and attention are this library's kernels.  Weights are synthetic (no trained model is available); timing does not depend on
+Every step runs in this library: the projections are attncache_linear (a tcgen05 GEMM X W^T, W in the
+nn.Linear layout [H*d][E], whose epilogue stores the head-major [B][H][S][d] layout the attention and A.V
+kernels read, so no permute pass follows), then attncache_rope, attncache_attend_full /
+attncache_apply_cached.  Weights are synthetic (no trained model is available); timing does not depend on
 their values.
 """
 from __future__ import annotations
 
 import torch
 
-from . import Context, Database, attncache_apply_cached, attncache_attend_full, attncache_rope
+from . import Context, Database, attncache_apply_cached, attncache_attend_full, attncache_linear, attncache_rope
 
 
 class AttentionBlock:
-    """One layer's attention block; projection weights [E][H*d]."""
+    """One layer's attention block; projection weights in the nn.Linear layout [H*d][E]."""
 
     def __init__(self, ctx: Context, db: Database, W_Q: torch.Tensor, W_K: torch.Tensor, W_V: torch.Tensor,
                  n_heads: int, head_dim: int, layer: int = 0, rope_base: float = 500000.0):
@@ -28,10 +29,8 @@ class AttentionBlock:
         self.ctx, self.db, self.layer, self.rope_base = ctx, db, layer, rope_base
 
     def _proj(self, X, W):
-        # [B*S][E] x [E][H*d] -> [B][S][H][d] -> head-major [B][1][H][S][d] slice
-        B, S, E = X.shape
-        Y = torch.matmul(X.view(B * S, E), W).view(B, S, self.H, self.d)
-        return Y.permute(0, 2, 1, 3).contiguous().unsqueeze(1)
+        # [B][S][E] x [H*d][E]^T -> head-major [B][1][H][S][d] (one layer), in the GEMM's epilogue
+        return attncache_linear(self.ctx, X, W, self.H)
 
     def full(self, X: torch.Tensor) -> torch.Tensor:
         Q, K, V = self._proj(X, self.Wq), self._proj(X, self.Wk), self._proj(X, self.Wv)

@@ -238,6 +238,7 @@ attncache_status attncache_db_load(attncache_ctx *ctx, const attncache_db_desc *
     }
     attncache_db *db = new attncache_db();
     db->ctx = ctx;
+    db->device = ctx->device;
     db->d = *d;
     if (!has_maps) db->d.maps = nullptr;
     attncache_status s = db_load_collective(db);  // COLLECTIVE with a communicator: checks the shard tiling
@@ -251,8 +252,8 @@ attncache_status attncache_db_load(attncache_ctx *ctx, const attncache_db_desc *
 
 attncache_status attncache_db_free(attncache_db *db) {
     if (!db) return ATTNCACHE_OK;
-    if (db->d_shard_begins) {
-        DeviceGuard g(db->ctx->device);
+    if (db->d_shard_begins) {  // db-local state only: the ctx may already be destroyed
+        DeviceGuard g(db->device);
         cudaFree(db->d_shard_begins);
     }
     delete db;
@@ -556,6 +557,31 @@ attncache_status attncache_project_features(attncache_ctx *ctx, const void *h, i
     a.y = (float *)((uint8_t *)buf + zb);
     a.f = features;
     AC_CUDA(launch_project(a, ctx->sm_count, (cudaStream_t)stream));
+    return ATTNCACHE_OK;
+}
+
+// ---- projection GEMM (f4) ------------------------------------------------------------------------
+
+attncache_status attncache_linear(attncache_ctx *ctx, const void *X, int64_t M, int32_t K, const void *W, int32_t N,
+                                  int32_t dtype, const float *bias, int32_t seq_len, int32_t head_dim, void *Y,
+                                  void *stream) {
+    if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "linear: ctx is NULL");
+    if (M < 0 || K <= 0 || N <= 0 || seq_len <= 0 || head_dim <= 0)
+        return fail(ATTNCACHE_ERR_SHAPE, "linear: M=%lld K=%d N=%d S=%d d=%d", (long long)M, K, N, seq_len, head_dim);
+    if (M % seq_len || N % head_dim)
+        return fail(ATTNCACHE_ERR_SHAPE, "linear: M=%lld must be whole sequences of %d rows and N=%d whole heads of %d",
+                    (long long)M, seq_len, N, head_dim);
+    if (!dtype_valid(dtype)) return fail(ATTNCACHE_ERR_DTYPE, "linear: dtype %d", dtype);
+    if (M == 0) return ATTNCACHE_OK;
+    if (!X || !W || !Y) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "linear: NULL X/W/Y");
+    if (!is_device_ptr(X) || !is_device_ptr(W) || !is_device_ptr(Y) || (bias && !is_device_ptr(bias)))
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "linear: X/W/Y/bias must be device memory");
+    const int es = dtype_size(dtype);
+    if (!aligned16(X) || !aligned16(W) || !aligned16(Y) || (bias && !aligned16(bias)) || ((int64_t)K * es) % 16 ||
+        ((int64_t)head_dim * es) % 16)
+        return fail(ATTNCACHE_ERR_ALIGNMENT, "linear: bases or rows (K, head_dim elements) not 16-byte aligned");
+    DeviceGuard g(ctx->device);
+    AC_CUDA(launch_linear_heads(dtype, X, M, K, W, N, bias, seq_len, head_dim, Y, ctx->sm_count, (cudaStream_t)stream));
     return ATTNCACHE_OK;
 }
 

@@ -138,6 +138,7 @@ struct attncache_ctx {
 
 struct attncache_db {
     attncache_ctx *ctx = nullptr;
+    int device = 0;
     attncache_db_desc d{};
     std::vector<int64_t> shard_begins;  // [world + 1] global entry ranges of every rank (collective load)
     int64_t *d_shard_begins = nullptr;  // device copy

@@ -98,6 +98,9 @@ struct ProjectArgs {
     void *f;              // [M][D] in feat_dt
 };
 bool linear_tc_supported(int32_t dt, int32_t K, int32_t Nout);
+// Y = X W^T stored head-major [M / S][N / d][S][d] (+ bias when non-NULL), rounded once to dt (f4 projections).
+cudaError_t launch_linear_heads(int32_t dt, const void *X, int64_t M, int32_t K, const void *W, int32_t N,
+                                const float *bias, int32_t S, int32_t d, void *Y, int sm_count, cudaStream_t st);
 
 // ---- owner-affinity placement on the device (kernels_plan.cu) ----
 constexpr int kPlanMaxWorld = 32;

@@ -32,12 +32,24 @@ struct Cfg {
     static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
 };
 
-// Y[m][n] = act(sum_k A[m][k] W[n][k] + bias[n]); kF32Out: Y fp32 (no activation), else Y in the input
-// 16-bit type with ReLU.
-template <int kTileN, bool kF32Out, bool kBf16>
+// Output modes of the GEMM epilogue.
+//   kOutF32  : Y [M][Nout] fp32, + bias (projector layer 2)
+//   kOutRelu : Y [M][Nout] in the input 16-bit type, relu(. + bias) (projector layer 1)
+//   kOutHeads: head-major Y [M / S][Nout / d][S][d] in the input type (+ bias when non-NULL): row m = (b, s),
+//              column n = (h, c) -> Y[b][h][s][c], the layout the attention and A.V kernels read (the Eq. 5
+//              block's Q/K/V projections, f4), so no permute pass follows the GEMM
+enum { kOutF32 = 0, kOutRelu = 1, kOutHeads = 2 };
+struct OutShape {
+    int32_t S, d;  // kOutHeads: sequence length and head dim (d % 32 == 0)
+};
+
+// Y[m][n] = epilogue(sum_k A[m][k] W[n][k]) per kMode.
+template <int kTileN, int kMode, bool kBf16>
 __global__ void __launch_bounds__(kThreads, 1)
     linear_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW, int64_t M,
-                     int Nout, int K, const float *__restrict__ bias, void *Y, uint32_t idesc, uint32_t a_rows) {
+                     int Nout, int K, const float *__restrict__ bias, void *Y, uint32_t idesc, uint32_t a_rows,
+                     OutShape osh) {
+    constexpr bool kF32Out = kMode == kOutF32;
     using C = Cfg<kTileN>;
     constexpr int kStages = C::kStages, kStageBytes = C::kStageBytes;
     constexpr uint32_t kTmemCols = C::kTmemCols;
@@ -137,14 +149,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld_wait();
                 if (m < M) {
                     float o[32];
-                    const float4 *b4 = reinterpret_cast<const float4 *>(bias + col0);
+                    if (bias) {
+                        const float4 *b4 = reinterpret_cast<const float4 *>(bias + col0);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const float4 bb = __ldg(b4 + i);
-                        o[4 * i + 0] = __uint_as_float(v[4 * i + 0]) + bb.x;
-                        o[4 * i + 1] = __uint_as_float(v[4 * i + 1]) + bb.y;
-                        o[4 * i + 2] = __uint_as_float(v[4 * i + 2]) + bb.z;
-                        o[4 * i + 3] = __uint_as_float(v[4 * i + 3]) + bb.w;
+                        for (int i = 0; i < 8; ++i) {
+                            const float4 bb = __ldg(b4 + i);
+                            o[4 * i + 0] = __uint_as_float(v[4 * i + 0]) + bb.x;
+                            o[4 * i + 1] = __uint_as_float(v[4 * i + 1]) + bb.y;
+                            o[4 * i + 2] = __uint_as_float(v[4 * i + 2]) + bb.z;
+                            o[4 * i + 3] = __uint_as_float(v[4 * i + 3]) + bb.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(v[i]);
                     }
                     if constexpr (kF32Out) {
                         float4 *dst = reinterpret_cast<float4 *>((float *)Y + m * (int64_t)Nout + col0);
@@ -154,7 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint32_t w[16];
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
-                            const float x0 = fmaxf(o[2 * i], 0.f), x1 = fmaxf(o[2 * i + 1], 0.f);
+                            const float x0 = kMode == kOutRelu ? fmaxf(o[2 * i], 0.f) : o[2 * i];
+                            const float x1 = kMode == kOutRelu ? fmaxf(o[2 * i + 1], 0.f) : o[2 * i + 1];
                             if constexpr (kBf16) {
                                 __nv_bfloat162 p = __floats2bfloat162_rn(x0, x1);
                                 w[i] = *reinterpret_cast<uint32_t *>(&p);
@@ -163,7 +181,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 w[i] = *reinterpret_cast<uint32_t *>(&p);
                             }
                         }
-                        uint4 *dst = reinterpret_cast<uint4 *>((uint16_t *)Y + m * (int64_t)Nout + col0);
+                        int64_t off = m * (int64_t)Nout + col0;
+                        if constexpr (kMode == kOutHeads) {  // [b][h][s][c]: 64 contiguous bytes of one head row
+                            const int64_t b = m / osh.S, sq = m - b * osh.S;
+                            const int h = col0 / osh.d, c0 = col0 - h * osh.d;
+                            off = ((b * (Nout / osh.d) + h) * osh.S + sq) * osh.d + c0;
+                        }
+                        uint4 *dst = reinterpret_cast<uint4 *>((uint16_t *)Y + off);
 #pragma unroll
                         for (int i = 0; i < 4; ++i) dst[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
                     }
@@ -183,9 +207,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ---- FFMA fallback: shared-memory tiled GEMM, 32 x 32 outputs per 256-thread block ---------------------
 constexpr int kST = 32, kSK = 16;
 
-template <int DT, bool kF32Out>
+template <int DT, int kMode>
 __global__ void __launch_bounds__(256) linear_simt_kernel(const void *A_, const void *W_, int64_t M, int Nout, int K,
-                                                         const float *__restrict__ bias, void *Y) {
+                                                         const float *__restrict__ bias, void *Y, OutShape osh) {
     using E = Elem<DT>;
     using T = typename E::T;
     const T *A = (const T *)A_, *W = (const T *)W_;
@@ -218,11 +242,16 @@ __global__ void __launch_bounds__(256) linear_simt_kernel(const void *A_, const 
             const int64_t m = m0 + ty + 16 * i;
             const int n = n0 + tx + 16 * j;
             if (m >= M || n >= Nout) continue;
-            const float v = acc[i][j] + bias[n];
-            if constexpr (kF32Out)
+            const float v = acc[i][j] + (bias ? bias[n] : 0.f);
+            if constexpr (kMode == kOutF32) {
                 ((float *)Y)[m * Nout + n] = v;
-            else
+            } else if constexpr (kMode == kOutRelu) {
                 E::st((T *)Y, m * Nout + n, fmaxf(v, 0.f));
+            } else {
+                const int64_t b = m / osh.S, sq = m - b * osh.S;
+                const int h = n / osh.d, c = n - h * osh.d;
+                E::st((T *)Y, ((b * (Nout / osh.d) + h) * osh.S + sq) * osh.d + c, v);
+            }
         }
 }
 
@@ -244,9 +273,9 @@ __global__ void normalize_rows_kernel(const float *__restrict__ Yf, int64_t M, i
     for (int c = lane; c < D; c += 32) E::st(F, row * D + c, y[c] * inv);
 }
 
-template <int kTileN, bool kF32Out>
+template <int kTileN, int kMode>
 cudaError_t launch_linear_tc_t(const void *A, const void *W, int64_t M, int Nout, int K, const float *bias, void *Y,
-                               bool bf16, int sm_count, cudaStream_t st) {
+                               bool bf16, int sm_count, cudaStream_t st, OutShape osh) {
     using C = Cfg<kTileN>;
     CUtensorMap ta, tw;
     const uint32_t a_rows = M >= kTileM ? kTileM : (uint32_t)((M + 7) / 8 * 8);
@@ -257,40 +286,40 @@ cudaError_t launch_linear_tc_t(const void *A, const void *W, int64_t M, int Nout
     const int grid = (int)min64(items, sm_count);
     const uint32_t idesc = idesc_f16(kTileM, kTileN, bf16 ? 1u : 0u, 0u, 0u);
     if (bf16) {
-        auto k = linear_tc_kernel<kTileN, kF32Out, true>;
+        auto k = linear_tc_kernel<kTileN, kMode, true>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         if (e != cudaSuccess) return e;
-        k<<<grid, kThreads, C::kSmem, st>>>(ta, tw, M, Nout, K, bias, Y, idesc, a_rows);
+        k<<<grid, kThreads, C::kSmem, st>>>(ta, tw, M, Nout, K, bias, Y, idesc, a_rows, osh);
     } else {
-        auto k = linear_tc_kernel<kTileN, kF32Out, false>;
+        auto k = linear_tc_kernel<kTileN, kMode, false>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         if (e != cudaSuccess) return e;
-        k<<<grid, kThreads, C::kSmem, st>>>(ta, tw, M, Nout, K, bias, Y, idesc, a_rows);
+        k<<<grid, kThreads, C::kSmem, st>>>(ta, tw, M, Nout, K, bias, Y, idesc, a_rows, osh);
     }
     count_launches(1);
     return cudaGetLastError();
 }
 
-template <bool kF32Out>
+template <int kMode>
 cudaError_t launch_linear_tc(const void *A, const void *W, int64_t M, int Nout, int K, const float *bias, void *Y,
-                             bool bf16, int sm_count, cudaStream_t st) {
+                             bool bf16, int sm_count, cudaStream_t st, OutShape osh = {1, 32}) {
     // the widest column tile that still gives every SM at least one work item
     const int64_t n_mt = (M + kTileM - 1) / kTileM;
     if (n_mt * ((Nout + 255) / 256) >= sm_count)
-        return launch_linear_tc_t<256, kF32Out>(A, W, M, Nout, K, bias, Y, bf16, sm_count, st);
+        return launch_linear_tc_t<256, kMode>(A, W, M, Nout, K, bias, Y, bf16, sm_count, st, osh);
     if (n_mt * ((Nout + 127) / 128) >= sm_count)
-        return launch_linear_tc_t<128, kF32Out>(A, W, M, Nout, K, bias, Y, bf16, sm_count, st);
-    return launch_linear_tc_t<64, kF32Out>(A, W, M, Nout, K, bias, Y, bf16, sm_count, st);
+        return launch_linear_tc_t<128, kMode>(A, W, M, Nout, K, bias, Y, bf16, sm_count, st, osh);
+    return launch_linear_tc_t<64, kMode>(A, W, M, Nout, K, bias, Y, bf16, sm_count, st, osh);
 }
 
-template <bool kF32Out>
+template <int kMode>
 cudaError_t launch_linear_simt(int32_t dt, const void *A, const void *W, int64_t M, int Nout, int K, const float *bias,
-                               void *Y, cudaStream_t st) {
+                               void *Y, cudaStream_t st, OutShape osh = {1, 32}) {
     dim3 grid((Nout + kST - 1) / kST, (unsigned)((M + kST - 1) / kST));
     switch (dt) {
-    case ATTNCACHE_F32: linear_simt_kernel<ATTNCACHE_F32, kF32Out><<<grid, 256, 0, st>>>(A, W, M, Nout, K, bias, Y); break;
-    case ATTNCACHE_F16: linear_simt_kernel<ATTNCACHE_F16, kF32Out><<<grid, 256, 0, st>>>(A, W, M, Nout, K, bias, Y); break;
-    default: linear_simt_kernel<ATTNCACHE_BF16, kF32Out><<<grid, 256, 0, st>>>(A, W, M, Nout, K, bias, Y); break;
+    case ATTNCACHE_F32: linear_simt_kernel<ATTNCACHE_F32, kMode><<<grid, 256, 0, st>>>(A, W, M, Nout, K, bias, Y, osh); break;
+    case ATTNCACHE_F16: linear_simt_kernel<ATTNCACHE_F16, kMode><<<grid, 256, 0, st>>>(A, W, M, Nout, K, bias, Y, osh); break;
+    default: linear_simt_kernel<ATTNCACHE_BF16, kMode><<<grid, 256, 0, st>>>(A, W, M, Nout, K, bias, Y, osh); break;
     }
     count_launches(1);
     return cudaGetLastError();
@@ -308,15 +337,15 @@ cudaError_t launch_project(const ProjectArgs &a, int sm_count, cudaStream_t st) 
     cudaError_t e;
     // layer 1: z = relu(W1 h + b1) in the activation dtype
     if (linear_tc_supported(a.dt, a.E, a.Hd))
-        e = launch_linear_tc<false>(a.h, a.W1, a.M, a.Hd, a.E, a.b1, a.z, a.dt == ATTNCACHE_BF16, sm_count, st);
+        e = launch_linear_tc<kOutRelu>(a.h, a.W1, a.M, a.Hd, a.E, a.b1, a.z, a.dt == ATTNCACHE_BF16, sm_count, st);
     else
-        e = launch_linear_simt<false>(a.dt, a.h, a.W1, a.M, a.Hd, a.E, a.b1, a.z, st);
+        e = launch_linear_simt<kOutRelu>(a.dt, a.h, a.W1, a.M, a.Hd, a.E, a.b1, a.z, st);
     if (e != cudaSuccess) return e;
     // layer 2: y = W2 z + b2 in fp32
     if (linear_tc_supported(a.dt, a.Hd, a.D))
-        e = launch_linear_tc<true>(a.z, a.W2, a.M, a.D, a.Hd, a.b2, a.y, a.dt == ATTNCACHE_BF16, sm_count, st);
+        e = launch_linear_tc<kOutF32>(a.z, a.W2, a.M, a.D, a.Hd, a.b2, a.y, a.dt == ATTNCACHE_BF16, sm_count, st);
     else
-        e = launch_linear_simt<true>(a.dt, a.z, a.W2, a.M, a.D, a.Hd, a.b2, a.y, st);
+        e = launch_linear_simt<kOutF32>(a.dt, a.z, a.W2, a.M, a.D, a.Hd, a.b2, a.y, st);
     if (e != cudaSuccess) return e;
     // f = y / ||y|| in the feature dtype
     const int rows_per_block = 8;
@@ -328,6 +357,15 @@ cudaError_t launch_project(const ProjectArgs &a, int sm_count, cudaStream_t st) 
     }
     count_launches(1);
     return cudaGetLastError();
+}
+
+cudaError_t launch_linear_heads(int32_t dt, const void *X, int64_t M, int32_t K, const void *W, int32_t N,
+                                const float *bias, int32_t S, int32_t d, void *Y, int sm_count, cudaStream_t st) {
+    if (M == 0) return cudaSuccess;
+    const OutShape osh{S, d};
+    if (linear_tc_supported(dt, K, N) && d % 32 == 0)
+        return launch_linear_tc<kOutHeads>(X, W, M, N, K, bias, Y, dt == ATTNCACHE_BF16, sm_count, st, osh);
+    return launch_linear_simt<kOutHeads>(dt, X, W, M, N, K, bias, Y, st, osh);
 }
 
 }  // namespace ac

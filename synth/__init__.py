@@ -212,7 +212,7 @@ def activations(cfg: Config, kind: str, b_begin: int, count: int, layer_begin: i
 
 def block_inputs(cfg: Config, device="cpu", B: int | None = None):
     """Eq. 5 block-level comparison inputs (f4): hidden states X [B][S][E] ~ N(0,1) and projection
-    weights W_Q, W_K, W_V [E][E] ~ N(0, 1/E), E = H * d, in the activation dtype (synthetic: no
+    weights W_Q, W_K, W_V [E][E] ~ N(0, 1/E) (nn.Linear layout), E = H * d, in the activation dtype (synthetic: no
     trained weights are available)."""
     B = cfg.B if B is None else B
     E = cfg.H * cfg.d

@@ -601,6 +601,58 @@ def test_eq5_block_cached_equals_full_with_captured_maps(ac, ctx):
     assert torch.equal(O_mixed[1], O_full[1])
 
 
+def _round_bf16(a: np.ndarray) -> torch.Tensor:
+    """fp64 oracle values rounded once (RN-even) to bf16: the storage dtype of the block's activations."""
+    return torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("M,K,N,S,d", [(256, 256, 256, 128, 64), (3 * 96, 192, 128, 96, 32), (2 * 40, 200, 96, 40, 48)])
+def test_linear_head_major_matches_oracle(ac, ctx, M, K, N, S, d):
+    """f4 projections (attncache_linear): Y = X W^T stored head-major [B][H][S][d], against oracle.linear; the
+    tcgen05 path (K, N multiples of 64, d % 32 == 0, ragged M) and the CUDA-core path (K = 200)."""
+    g = torch.Generator(device=DEV).manual_seed(41)
+    X = torch.randn(M // S, S, K, device=DEV, generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, K, device=DEV, generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    Y = ac.attncache_linear(ctx, X, W, N // d)
+    ref = oracle.linear(storage(X.view(M, K)), storage(W), "bf16")            # [M][N] = [(b, s)][(h, c)]
+    ref = ref.reshape(M // S, S, N // d, d).transpose(0, 2, 1, 3)              # -> [b][h][s][c]
+    check_close(Y.view(M // S, N // d, S, d).reshape(-1, S, d), ref.reshape(-1, S, d), torch.bfloat16, "linear")
+
+
+def test_eq5_block_matches_oracle(ac, ctx):
+    """f4 (Eq. 5; Alg. 2 l.372-381) against the oracle composed step by step: q, k, v =
+    oracle.linear (rounded to the bf16 activation dtype), RoPE (oracle.rope, rounded), causal softmax attention
+    (oracle.attend) for the full block; v then A.V with the DB's maps (oracle.apply) for the cached block."""
+    from paper_2510_25979_b200.block import AttentionBlock
+    cfg = synth.CONFIGS["llama32_1b"].with_(B=3, N=3, L=1, H=4)
+    X, (Wq, Wk, Wv) = synth.block_inputs(cfg, DEV)
+    E, S, H, d = X.shape[2], cfg.S, cfg.H, cfg.d
+    maps = ac.attncache_pack_maps(synth.maps(cfg, 0, 3, DEV))
+    db = ac.Database(ctx, synth.features(cfg, 0, 3, DEV), maps, packed=True, seq_len=S)
+    blk = AttentionBlock(ctx, db, Wq, Wk, Wv, H, d)
+    O_full = blk.full(X)
+    idx = torch.tensor([2, 0, 1], device=DEV)
+    O_cached = blk.cached(X, idx, torch.ones(3, dtype=torch.uint8, device=DEV), idx[:0])
+    torch.cuda.synchronize()
+    Xs = storage(X.view(-1, E))
+
+    def heads(W):  # oracle projection -> bf16 [B][H][S][d]
+        y = oracle.linear(Xs, storage(W), "bf16").reshape(cfg.B, S, H, d).transpose(0, 2, 1, 3)
+        return _round_bf16(y.copy())
+
+    Qo, Ko, Vo = heads(Wq), heads(Wk), heads(Wv)
+    Qr = _round_bf16(oracle.rope(storage(Qo), "bf16", S, d, base=blk.rope_base))
+    Kr = _round_bf16(oracle.rope(storage(Ko), "bf16", S, d, base=blk.rope_base))
+    units = [(b, h) for b in range(cfg.B) for h in range(H)]
+    off = [((b * H + h) * S * d) for b, h in units]
+    ref = oracle.attend(storage(Qr), storage(Kr), storage(Vo), "bf16", off, S, d)
+    check_close(torch.stack([O_full[b, 0, h] for b, h in units]), ref, torch.bfloat16, "eq5 full block")
+    dense = storage(synth.maps(cfg, 0, 3, DEV))
+    a_off = [((int(idx[b]) * H + h) * S * S) for b, h in units]
+    ref = oracle.apply(dense, "bf16", a_off, storage(Vo), "bf16", off, S, d)
+    check_close(torch.stack([O_cached[b, 0, h] for b, h in units]), ref, torch.bfloat16, "eq5 cached block")
+
+
 @pytest.mark.parametrize("cfg_name,N,B", [("tiny", 5, 3), ("llama32_1b", 4, 3), ("llama3_8b", 2, 2)])
 def test_apply_noncausal_encoder_maps(ac, ctx, cfg_name, N, B):
     """f3: bidirectional (encoder) maps — A.V over every column."""

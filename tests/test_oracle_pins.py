@@ -509,3 +509,33 @@ def test_project_matches_library_mlp():
     y = torch.nn.functional.linear(z, t(W2), torch.from_numpy(b2).double())
     ref = torch.nn.functional.normalize(y, dim=1).numpy()
     assert np.allclose(f, ref, rtol=0, atol=1e-13)
+
+
+# ----------------------------------------------------------------------------------------------
+# projections — Alg. 2 l.372, l.377-378 (f4 block comparison; reading R34: W in the nn.Linear layout)
+# ----------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_linear_exact_rational_and_layout(dtype):
+    """Y = X W^T against exact rationals on a non-square W (N = 5 != K = 7, so W [K][N] would not even fit),
+    identity weights give X back exactly, and a golden 2 x 2 case computed by hand."""
+    rng = np.random.default_rng(31)
+    M, K, N = 4, 7, 5
+    Xf = rng.standard_normal((M, K)).astype(np.float32)
+    Wf = rng.standard_normal((N, K)).astype(np.float32)
+    X = Xf if dtype == "f32" else _bf16_bits(Xf)
+    W = Wf if dtype == "f32" else _bf16_bits(Wf)
+    XE = np.array(_exact(X, dtype), dtype=object).reshape(M, K)
+    WE = np.array(_exact(W, dtype), dtype=object).reshape(N, K)
+    Y = oracle.linear(X, W, dtype)
+    for m in range(M):
+        for n in range(N):
+            want = float(sum(XE[m, k] * WE[n, k] for k in range(K)))
+            assert abs(Y[m, n] - want) <= 1e-12 * max(1.0, abs(want))
+    I = np.eye(K, dtype=np.float32)
+    assert np.array_equal(oracle.linear(X, I if dtype == "f32" else _bf16_bits(I), dtype),
+                          np.asarray(_exact(X, dtype), dtype=np.float64).reshape(M, K))
+    # [[1, 2], [3, 4]] . [[5, 6], [7, 8]]^T = [[17, 23], [39, 53]]
+    A = np.array([[1, 2], [3, 4]], np.float32)
+    B = np.array([[5, 6], [7, 8]], np.float32)
+    assert np.array_equal(oracle.linear(A, B, "f32"), np.array([[17.0, 23.0], [39.0, 53.0]]))
