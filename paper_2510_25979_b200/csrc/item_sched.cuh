@@ -23,7 +23,7 @@ struct ItemSched {
     __host__ static ItemSched make(uint32_t S, uint32_t L, uint32_t H, uint32_t Hkv, uint32_t blk, uint32_t unit_bytes) {
         ItemSched c;
         c.S = S;
-        c.n_qb = S / blk;
+        c.n_qb = (S + blk - 1) / blk;  // a last, partial query block when S % blk != 0
         c.per_row = L * H;
         c.L = L;
         c.Hkv = Hkv;
@@ -50,8 +50,10 @@ struct ItemSched {
     }
 
     struct Item {
-        int64_t row0;     // first Q / O row of the unit ([rows][L][H][S] flattened)
-        int64_t kv_row0;  // first K / V row (grouped-query attention: K/V head h / (H / Hkv))
+        int64_t row0;     // first Q / O row of the unit ([rows][L][H][S] flattened) = unit * S
+        int64_t kv_row0;  // first K / V row (grouped-query attention: K/V head h / (H / Hkv)) = kv_unit * S
+        int32_t unit;     // the Q / O unit index ([rows][L][H]): the outer coordinate of the 3-D tensor maps
+        int32_t kv_unit;  // the K / V unit index ([rows][L][Hkv])
         int64_t row;      // the selected batch row
         uint32_t lh;      // layer * H + head
         int qb;           // query block
@@ -77,8 +79,10 @@ struct ItemSched {
         it.lh = u - ri * per_row;
         it.row = rows[ri];
         const uint32_t l = h_d.div(it.lh), h = it.lh - l * h_d.d;
-        it.row0 = (it.row * per_row + it.lh) * S;
-        it.kv_row0 = ((it.row * L + l) * Hkv + hq_d.div(h)) * (int64_t)S;
+        it.unit = (int32_t)(it.row * per_row + it.lh);
+        it.kv_unit = (int32_t)((it.row * L + l) * Hkv + hq_d.div(h));
+        it.row0 = (int64_t)it.unit * S;
+        it.kv_row0 = (int64_t)it.kv_unit * S;
         return it;
     }
 };
@@ -91,6 +95,7 @@ struct ItemWalker {
     const int32_t *rows;
     bool active = false;
     int64_t row0 = 0, kv_row0 = 0;
+    int32_t unit = 0, kv_unit = 0;
     int qb = 0, j = 0;
     __device__ __forceinline__ void init(const ItemSched &sc, uint32_t first, uint32_t stride_, uint32_t items_,
                                          uint32_t units_, const int32_t *rows_) {
@@ -103,6 +108,8 @@ struct ItemWalker {
         const ItemSched::Item it = sc.decode(t, units, rows);
         row0 = it.row0;
         kv_row0 = it.kv_row0;
+        unit = it.unit;
+        kv_unit = it.kv_unit;
         qb = it.qb;
         j = 0;
     }

@@ -69,6 +69,9 @@ constexpr int32_t kSimtMaxLen = 7264;
 bool attend_tc_supported(int32_t dt, int32_t S, int32_t d);
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st);
 cudaError_t launch_attend_split(const AttendArgs &a, int sm_count, cudaStream_t st);  // d = 128, double-buffered S
+// The four 3-D tensor maps of an attention launch: Q, K, V boxes [128 rows][64 cols], O box [32][64].
+cudaError_t make_attend_tmaps(const AttendArgs &a, int d, CUtensorMap *tq, CUtensorMap *tk, CUtensorMap *tv,
+                              CUtensorMap *to);
 
 // ---- capture (DB building: the causal maps of a prefill) ----
 struct CaptureArgs {
@@ -121,6 +124,13 @@ cudaError_t launch_rope(void *X, int64_t n_units, int32_t S, int32_t d, int32_t 
 // ---- TMA descriptors (tma_host.cu) ----
 cudaError_t make_tmap_2d_16(CUtensorMap *out, const void *base, bool bf16, uint64_t inner, uint64_t outer,
                             uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
+
+// [outer][mid][inner] 16-bit tensor (e.g. [units][S][d]) with box [1][box_mid][box_inner]: rows past `mid`
+// read as zeros and are clipped on store, so a unit's last partial 128-row block needs no masking in the
+// kernels, and the unit index is its own coordinate (no 2^31 limit on units * S rows).
+cudaError_t make_tmap_3d_16(CUtensorMap *out, const void *base, bool bf16, uint64_t inner, uint64_t mid, uint64_t outer,
+                            uint64_t row_bytes, uint64_t plane_bytes, uint32_t box_inner, uint32_t box_mid,
+                            int swizzle_bytes);
 
 // ---- packed map layout ----
 cudaError_t launch_pack_maps(const void *dense, int64_t n_maps, int32_t S, void *packed, bool unpack, cudaStream_t st);

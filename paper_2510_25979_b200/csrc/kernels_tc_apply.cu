@@ -10,7 +10,11 @@
 //              (no "attention cache" copy, reading R18); pieces entirely above the diagonal are
 //              zero-filled in shared memory without touching HBM (normal L2 policy).  Writes the 128B-swizzled
 //              K-major layout tcgen05 reads.
-//   warp 4     V loader: TMA 2-D loads of V rows [64kc, 64kc+64) (128B swizzle, MN-major B).
+//   warp 4     V loader: TMA 3-D loads ([units][S][d]) of V rows [64kc, 64kc+64) (128B swizzle, MN-major B).
+//
+// Any S % 8 == 0 (the paper's contexts are 94-1019 tokens, Table 3): a unit has ceil(S / 128) row blocks and
+// ceil(S / 64) column chunks; map pieces of rows >= S or columns >= S are zero-filled in shared memory, V rows
+// past S read as zeros (3-D tensor map bounds) and O rows past S are clipped by the TMA store.
 //   warp 5     MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128, N=d, K=16, fp32 in TMEM;
 //              owns TMEM allocation (2 accumulators: the epilogue of one row block overlaps the
 //              MMAs of the next).
@@ -108,7 +112,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     const int S = a.S;
-    const int n_rb = S / kRows;
+    const int n_rb = (S + kRows - 1) / kRows;
+    const int n_cc = (S + kChunk - 1) / kChunk;  // column chunks holding at least one stored column
     const uint32_t per_row = (uint32_t)(a.n_lay * a.H);
     const uint32_t units = (uint32_t)(*a.list.count) * per_row;
 
@@ -143,10 +148,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const __nv_bfloat16 *rowp[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const int R = rb * kRows + r0 + 16 * j;
+                    const int R = min(rb * kRows + r0 + 16 * j, S - 1);  // rows >= S: zero-filled below
                     rowp[j] = A + (packed ? packed_row_off(R) : (int64_t)R * S);
                 }
-                const int n_kc = a.causal ? 2 * (rb + 1) : S / kChunk;
+                const int n_kc = a.causal ? min(2 * (rb + 1), n_cc) : n_cc;
                 for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
                     const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
@@ -154,8 +159,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int col = kc * kChunk + c * 8;  // first column of this thread's piece
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        // the piece holds at least one entry on/below the diagonal, else zero-fill
-                        const bool need = !a.causal || col <= rb * kRows + r0 + 16 * j;
+                        // the piece holds at least one stored entry (on/below the diagonal, inside the
+                        // S x S map), else zero-fill
+                        const int R = rb * kRows + r0 + 16 * j;
+                        const bool need = R < S && col < S && (!a.causal || col <= R);
                         cp_async_16_hint(dst + 2048 * j, rowp[j] + (need ? kc * kChunk : 0), need ? 16u : 0u, policy);
                     }
                     cp_async_commit();
@@ -190,9 +197,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 AC_STRESS_DELAY(574u);
                 // V head of map head h under grouped-query attention: h / (H / Hkv) (Hkv = H for MHA)
                 const uint32_t l = lh / (uint32_t)a.H, h = lh % (uint32_t)a.H;
-                const int32_t vrow0 = (int32_t)(((row * a.n_lay + l) * a.Hkv + h / (uint32_t)(a.H / a.Hkv)) * S);
+                const int32_t vunit = (int32_t)((row * a.n_lay + l) * a.Hkv + h / (uint32_t)(a.H / a.Hkv));
                 for (int rb = 0; rb < n_rb; ++rb) {
-                    const int n_kc = a.causal ? 2 * (rb + 1) : S / kChunk;
+                    const int n_kc = a.causal ? min(2 * (rb + 1), n_cc) : n_cc;
                     for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
                         const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
                         mbar_wait(&empty[s], ph ^ 1u);
@@ -200,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t dst = smem_u32(smem + s * C::kStageBytes + kABytes);
 #pragma unroll
                         for (int half = 0; half < kD / 64; ++half)
-                            tma_load_2d_hint(dst + half * (kChunk * 128), &tmV, &full[s], half * 64, vrow0 + kc * kChunk,
+                            tma_load_3d_hint(dst + half * (kChunk * 128), &tmV, &full[s], half * 64, kc * kChunk, vunit,
                                              v_policy);
                     }
                 }
@@ -217,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&tempty[acc], aph ^ 1u);
                     tc_fence_after();
                     const uint32_t d_tmem = tmem + acc * kD;
-                    const int n_kc = a.causal ? 2 * (rb + 1) : S / kChunk;
+                    const int n_kc = a.causal ? min(2 * (rb + 1), n_cc) : n_cc;
                     for (int kc = 0; kc < n_kc; ++kc, ++cnt) {
                         const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
                         mbar_wait(&full[s], ph);
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int64_t row, ent;
         while (iter.next(lh, row, ent)) {
             AC_STRESS_DELAY(66u);
-            const int64_t orow_unit = (row * per_row + lh) * S;  // first O row of the unit
+            const int32_t ounit = (int32_t)(row * per_row + lh);  // the O unit (3-D tensor map coordinate)
             for (int rb = 0; rb < n_rb; ++rb, ++item) {
                 const uint32_t acc = item & 1u, aph = (item >> 1) & 1u;
                 mbar_wait(&tfull[acc], aph);
@@ -291,9 +298,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    const int32_t orow = (int32_t)(orow_unit + rb * kRows + q * 32);
+                    const int32_t orow = rb * kRows + q * 32;  // rows >= S are clipped by the tensor map
 #pragma unroll
-                    for (int half = 0; half < kD / 64; ++half) tma_store_2d(&tmO, stage_o_u32 + half * 4096, half * 64, orow);
+                    for (int half = 0; half < kD / 64; ++half)
+                        tma_store_3d(&tmO, stage_o_u32 + half * 4096, half * 64, orow, ounit);
                     bulk_commit();
                 }
             }
@@ -311,11 +319,11 @@ template <int kD>
 cudaError_t launch(const ApplyArgs &a, int sm_count, cudaStream_t st) {
     using C = Cfg<kD>;
     const bool bf16 = a.act_dt == ATTNCACHE_BF16;
-    const uint64_t rows = (uint64_t)a.max_rows * a.n_lay * a.H * a.S;
-    const uint64_t vrows = (uint64_t)a.max_rows * a.n_lay * a.Hkv * a.S;
+    const uint64_t units = (uint64_t)a.max_rows * a.n_lay * a.H, vunits = (uint64_t)a.max_rows * a.n_lay * a.Hkv;
+    const uint64_t plane = (uint64_t)a.S * kD * 2;
     CUtensorMap tmV, tmO;
-    cudaError_t e = make_tmap_2d_16(&tmV, a.V, bf16, kD, vrows, (uint64_t)kD * 2, 64, kChunk, 128);
-    if (e == cudaSuccess) e = make_tmap_2d_16(&tmO, a.O, bf16, kD, rows, (uint64_t)kD * 2, 64, 32, 128);
+    cudaError_t e = make_tmap_3d_16(&tmV, a.V, bf16, kD, a.S, vunits, (uint64_t)kD * 2, plane, 64, kChunk, 128);
+    if (e == cudaSuccess) e = make_tmap_3d_16(&tmO, a.O, bf16, kD, a.S, units, (uint64_t)kD * 2, plane, 64, 32, 128);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(apply_tc_kernel<kD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
@@ -328,12 +336,13 @@ cudaError_t launch(const ApplyArgs &a, int sm_count, cudaStream_t st) {
 }  // namespace
 
 bool apply_tc_supported(int32_t map_dt, int32_t act_dt, int32_t S, int32_t d) {
-    return map_dt == act_dt && (map_dt == ATTNCACHE_BF16 || map_dt == ATTNCACHE_F16) && S >= kRows && S % kRows == 0 &&
+    return map_dt == act_dt && (map_dt == ATTNCACHE_BF16 || map_dt == ATTNCACHE_F16) && S >= 8 && S % 8 == 0 &&
            (d == 64 || d == 128);
 }
 
 cudaError_t launch_apply_tc(const ApplyArgs &a, int sm_count, cudaStream_t st) {
-    if ((uint64_t)a.max_rows * a.n_lay * a.H * a.S >= (1ull << 31)) return cudaErrorInvalidValue;  // TMA coordinate range
+    // unit indices are int32 TMA coordinates and units * per_row is a uint32 loop bound
+    if ((uint64_t)a.max_rows * a.n_lay * a.H >= (1ull << 31)) return cudaErrorInvalidValue;
     return a.d == 64 ? launch<64>(a, sm_count, st) : launch<128>(a, sm_count, st);
 }
 

@@ -94,8 +94,7 @@ __device__ __forceinline__ Ring ring(uint32_t i) {
     return {i % N, (i / N) & 1u};
 }
 
-// One CTA-local item stream: items t = first, first + stride, ...; item -> (unit's first row,
-// query block qb).  Units are taken in L2-sized groups of `group` units (K/V of a group fit in about
+// One CTA-local item stream: items t = first, first + stride, ...; item -> (unit, query block qb).  Units are taken in L2-sized groups of `group` units (K/V of a group fit in about
 // 48 MB of L2) and inside a group the heaviest query blocks come first: every query block of a unit
 // re-reads the unit's K/V blocks, and ordering all units' qb = n_qb-1 blocks first (the previous
 // order) made those re-reads come from HBM (3.3x the algorithmic bytes at configs[3]).  The last
@@ -106,8 +105,8 @@ struct Stream {
     uint32_t t, stride, items, units, per_row, n_qb, S, group, H, Hkv, L;
     const int32_t *rows;
     bool active = false;
-    int64_t row0 = 0;     // first Q / O row of the unit
-    int64_t kv_row0 = 0;  // first K / V row of the unit (its K/V head under grouped-query attention)
+    int32_t unit = 0;     // the Q / O unit (outer coordinate of the 3-D tensor maps)
+    int32_t kv_unit = 0;  // the K / V unit (its K/V head under grouped-query attention)
     int qb = 0, j = 0;
     __device__ void init(uint32_t first, uint32_t stride_, uint32_t items_, uint32_t units_, uint32_t per_row_,
                          uint32_t n_qb_, uint32_t S_, uint32_t group_, const int32_t *rows_, uint32_t H_, uint32_t Hkv_) {
@@ -125,8 +124,8 @@ struct Stream {
         qb = (int)(n_qb - 1 - w / gsize);
         const int64_t row = rows[u / per_row];
         const uint32_t lh = u % per_row;
-        row0 = (row * per_row + lh) * S;
-        kv_row0 = ((row * L + lh / H) * Hkv + (lh % H) / (H / Hkv)) * (int64_t)S;
+        unit = (int32_t)(row * per_row + lh);
+        kv_unit = (int32_t)((row * L + lh / H) * Hkv + (lh % H) / (H / Hkv));
         j = 0;
     }
     // Moves past the current key block; returns true when that block ended the item.
@@ -196,7 +195,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     const uint32_t S = (uint32_t)a.S;
-    const uint32_t n_qb = S / kBlk;
+    // a last, partial block when S % 128 != 0: Q / K / V rows past S read as zeros (3-D tensor maps) and only
+    // padded query rows (never stored: the O store clips at S) see padded keys through the causal mask
+    const uint32_t n_qb = (S + kBlk - 1) / kBlk;
     const uint32_t per_row = (uint32_t)(a.L * a.H);
     const uint32_t units = (uint32_t)(*a.list.count) * per_row;
     const uint32_t items = units * n_qb;
@@ -224,19 +225,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t v_s = smem_u32(sV + g * C::kTile);
                 while (st.active) {
                     AC_STRESS_DELAY(137u);
-                    const int32_t r_j = (int32_t)(st.kv_row0 + st.j * kBlk);
+                    const int32_t r_j = st.j * kBlk;
                     if (st.j == 0) {
                         mbar_wait(&q_empty[g], (it & 1u) ^ 1u);
                         mbar_arrive_expect_tx(&q_full[g], C::kTile);
                         for (int h = 0; h < kD / 64; ++h)
-                            tma_load_2d(q_s + h * (kBlk * 128), &tmQ, &q_full[g], h * 64, (int32_t)(st.row0 + st.qb * kBlk));
+                            tma_load_3d(q_s + h * (kBlk * 128), &tmQ, &q_full[g], h * 64, st.qb * kBlk, st.unit);
                     }
                     mbar_wait(&k_empty[g], (b & 1u) ^ 1u);
                     mbar_arrive_expect_tx(&k_full[g], C::kTile);
-                    for (int h = 0; h < kD / 64; ++h) tma_load_2d(k_s + h * (kBlk * 128), &tmK, &k_full[g], h * 64, r_j);
+                    for (int h = 0; h < kD / 64; ++h)
+                        tma_load_3d(k_s + h * (kBlk * 128), &tmK, &k_full[g], h * 64, r_j, st.kv_unit);
                     mbar_wait(&v_empty[g], (b & 1u) ^ 1u);
                     mbar_arrive_expect_tx(&v_full[g], C::kTile);
-                    for (int h = 0; h < kD / 64; ++h) tma_load_2d(v_s + h * (kBlk * 128), &tmV, &v_full[g], h * 64, r_j);
+                    for (int h = 0; h < kD / 64; ++h)
+                        tma_load_3d(v_s + h * (kBlk * 128), &tmV, &v_full[g], h * 64, r_j, st.kv_unit);
                     ++b;
                     if (st.advance()) ++it;
                 }
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // TMEM -> registers -> act dtype -> this warp's 128B-swizzled staging tile -> TMA store of the
                 // warp's 32 rows, 64 columns at a time (full-line writes; per-thread row stores stalled the
                 // group on the LSU and delayed its next P)
-                const int32_t orow = (int32_t)(s.row0 + s.qb * kBlk + q * 32);
+                const int32_t orow = s.qb * kBlk + q * 32;  // rows >= S are clipped by the tensor map
 #pragma unroll
                 for (int half = 0; half < kD / 64; ++half) {
                     uint32_t v[64];
@@ -457,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_2d(&tmO, stage_o_u32, half * 64, orow);
+                        tma_store_3d(&tmO, stage_o_u32, half * 64, orow, s.unit);
                         bulk_commit();
                     }
                 }
@@ -479,13 +482,8 @@ template <int kD, bool kBF16>
 cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
     using C = Cfg<kD>;
     const bool bf16 = a.dt == ATTNCACHE_BF16;
-    const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
-    const uint64_t kvrows = (uint64_t)a.max_rows * a.L * a.Hkv * a.S;
     CUtensorMap tq, tk, tv, to;
-    cudaError_t e = make_tmap_2d_16(&tq, a.Q, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
-    if (e == cudaSuccess) e = make_tmap_2d_16(&to, a.O, bf16, kD, rows, (uint64_t)kD * 2, 64, 32, 128);
-    if (e == cudaSuccess) e = make_tmap_2d_16(&tk, a.K, bf16, kD, kvrows, (uint64_t)kD * 2, 64, kBlk, 128);
-    if (e == cudaSuccess) e = make_tmap_2d_16(&tv, a.V, bf16, kD, kvrows, (uint64_t)kD * 2, 64, kBlk, 128);
+    cudaError_t e = make_attend_tmaps(a, kD, &tq, &tk, &tv, &to);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(attend_tc_kernel<kD, kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
@@ -499,14 +497,26 @@ cudaError_t launch(const AttendArgs &a, int sm_count, cudaStream_t st) {
 
 }  // namespace
 
+cudaError_t make_attend_tmaps(const AttendArgs &a, int d, CUtensorMap *tq, CUtensorMap *tk, CUtensorMap *tv,
+                              CUtensorMap *to) {
+    const bool bf16 = a.dt == ATTNCACHE_BF16;
+    const uint64_t units = (uint64_t)a.max_rows * a.L * a.H, kvunits = (uint64_t)a.max_rows * a.L * a.Hkv;
+    const uint64_t row = (uint64_t)d * 2, plane = (uint64_t)a.S * d * 2;
+    cudaError_t e = make_tmap_3d_16(tq, a.Q, bf16, d, a.S, units, row, plane, 64, kBlk, 128);
+    if (e == cudaSuccess) e = make_tmap_3d_16(to, a.O, bf16, d, a.S, units, row, plane, 64, 32, 128);
+    if (e == cudaSuccess) e = make_tmap_3d_16(tk, a.K, bf16, d, a.S, kvunits, row, plane, 64, kBlk, 128);
+    if (e == cudaSuccess) e = make_tmap_3d_16(tv, a.V, bf16, d, a.S, kvunits, row, plane, 64, kBlk, 128);
+    return e;
+}
+
 bool attend_tc_supported(int32_t dt, int32_t S, int32_t d) {
-    return (dt == ATTNCACHE_BF16 || dt == ATTNCACHE_F16) && S >= kBlk && S % kBlk == 0 && (d == 64 || d == 128);
+    return (dt == ATTNCACHE_BF16 || dt == ATTNCACHE_F16) && S >= 1 && (d == 64 || d == 128);
 }
 
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st) {
-    const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
-    if (rows >= (1ull << 31) || (uint64_t)a.max_rows * a.L * a.H * (a.S / kBlk) >= (1ull << 31))
-        return cudaErrorInvalidValue;
+    // unit indices are int32 TMA coordinates; items = units * ceil(S / 128) is a uint32 loop bound
+    const uint64_t units = (uint64_t)a.max_rows * a.L * a.H;
+    if (units >= (1ull << 31) || units * ((a.S + kBlk - 1) / kBlk) >= (1ull << 31)) return cudaErrorInvalidValue;
     // d = 64 uses the same two-group kernel (the earlier two-CTA-per-SM d = 64 kernel with O in registers
     // reached 78 % of the HBM roofline at configs[1]; this one 94 %)
     if (a.d == 64) return a.dt == ATTNCACHE_BF16 ? launch<64, true>(a, sm_count, st) : launch<64, false>(a, sm_count, st);

@@ -177,20 +177,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&q_empty[qs], ((it >> 1) & 1u) ^ 1u);
                     mbar_arrive_expect_tx(&q_full[qs], kTile);
                     for (int h = 0; h < 2; ++h)
-                        tma_load_2d(smem_u32(sQ + qs * kTile + h * (kBlk * 128)), &tmQ, &q_full[qs], h * 64,
-                                    (int32_t)(w.row0 + w.qb * kBlk));
+                        tma_load_3d(smem_u32(sQ + qs * kTile + h * (kBlk * 128)), &tmQ, &q_full[qs], h * 64,
+                                    w.qb * kBlk, w.unit);
                 }
-                const int32_t r_j = (int32_t)(w.kv_row0 + w.j * kBlk);
+                const int32_t r_j = w.j * kBlk;
                 const uint32_t kk = b % kNK, kkph = ((b / kNK) & 1u) ^ 1u;
                 const uint32_t vv = b % kNV, vvph = ((b / kNV) & 1u) ^ 1u;
                 mbar_wait(&k_empty[kk], kkph);
                 mbar_arrive_expect_tx(&k_full[kk], kTile);
                 for (int h = 0; h < 2; ++h)
-                    tma_load_2d(smem_u32(sK + kk * kTile + h * (kBlk * 128)), &tmK, &k_full[kk], h * 64, r_j);
+                    tma_load_3d(smem_u32(sK + kk * kTile + h * (kBlk * 128)), &tmK, &k_full[kk], h * 64, r_j, w.kv_unit);
                 mbar_wait(&v_empty[vv], vvph);
                 mbar_arrive_expect_tx(&v_full[vv], kTile);
                 for (int h = 0; h < 2; ++h)
-                    tma_load_2d(smem_u32(sV + vv * kTile + h * (kBlk * 128)), &tmV, &v_full[vv], h * 64, r_j);
+                    tma_load_3d(smem_u32(sV + vv * kTile + h * (kBlk * 128)), &tmV, &v_full[vv], h * 64, r_j, w.kv_unit);
                 ++b;
                 if (w.advance(sc)) ++it;
             }
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t t = blockIdx.x; t < items; t += gridDim.x, ++it) {
             AC_STRESS_DELAY(99u);
             const ItemSched::Item item = sc.decode(t, units, a.list.rows);
-            const int32_t orow = (int32_t)(item.row0 + item.qb * kBlk + q * 32);
+            const int32_t orow = item.qb * kBlk + q * 32;  // rows >= S are clipped by the tensor map
             mbar_wait(o_full, it & 1u);
             tc_fence_after();
             uint32_t ls[2];
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_2d(&tmO, smem_u32(st), h * 64, orow);
+                    tma_store_3d(&tmO, smem_u32(st), h * 64, orow, item.unit);
                     bulk_commit();
                 }
             }
@@ -445,13 +445,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <bool kBF16>
 cudaError_t launch_t(const AttendArgs &a, int sm_count, cudaStream_t st) {
     const bool bf16 = kBF16;
-    const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
-    const uint64_t kvrows = (uint64_t)a.max_rows * a.L * a.Hkv * a.S;
     CUtensorMap tq, tk, tv, to;
-    cudaError_t e = make_tmap_2d_16(&tq, a.Q, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
-    if (e == cudaSuccess) e = make_tmap_2d_16(&to, a.O, bf16, kD, rows, (uint64_t)kD * 2, 64, 32, 128);
-    if (e == cudaSuccess) e = make_tmap_2d_16(&tk, a.K, bf16, kD, kvrows, (uint64_t)kD * 2, 64, kBlk, 128);
-    if (e == cudaSuccess) e = make_tmap_2d_16(&tv, a.V, bf16, kD, kvrows, (uint64_t)kD * 2, 64, kBlk, 128);
+    cudaError_t e = make_attend_tmaps(a, kD, &tq, &tk, &tv, &to);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(attend_split_kernel<kBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;

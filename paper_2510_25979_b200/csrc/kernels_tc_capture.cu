@@ -134,8 +134,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&q_empty[g], qph ^ 1u);
                     mbar_arrive_expect_tx(&q_full[g], C::kTile);
                     for (int h = 0; h < kD / 64; ++h)
-                        tma_load_2d_hint(smem_u32(sQ + g * C::kTile + h * (kBlk * 128)), &tmQ, &q_full[g], h * 64,
-                                    (int32_t)(item.row0 + qb * kBlk), pol_q);
+                        tma_load_3d_hint(smem_u32(sQ + g * C::kTile + h * (kBlk * 128)), &tmQ, &q_full[g], h * 64,
+                                         qb * kBlk, item.unit, pol_q);
                 } else {
                     mbar_wait(&q_full[g], qph);
                 }
@@ -150,8 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_wait(&k_empty[ks], kph ^ 1u);
                         mbar_arrive_expect_tx(&k_full[ks], C::kTile);
                         for (int h = 0; h < kD / 64; ++h)
-                            tma_load_2d_hint(smem_u32(sK + ks * C::kTile + h * (kBlk * 128)), &tmK, &k_full[ks], h * 64,
-                                             (int32_t)(item.kv_row0 + j * kBlk), pol_k);
+                            tma_load_3d_hint(smem_u32(sK + ks * C::kTile + h * (kBlk * 128)), &tmK, &k_full[ks], h * 64,
+                                             j * kBlk, item.kv_unit, pol_k);
                     } else {
                         const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
                         mbar_wait(&k_full[ks], kph);
@@ -215,9 +215,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const ItemSched::Item item = sc.decode(t, units, a.list.rows);
             const int qb = item.qb;
             const int R = qb * kBlk + r;  // this thread's query row in the unit
-            uint16_t *mrow = maps + ((item.row * per_row + item.lh) * a.map_stride) + map_row_off(R, S, a.map_layout);
+            const bool valid = R < (int)S;  // rows of a last, partial block past S are computed, never stored
+            uint16_t *mrow = maps + ((item.row * per_row + item.lh) * a.map_stride) +
+                             map_row_off(valid ? R : 0, S, a.map_layout);
             // packed rows hold 8*(R/8 + 1) elements; dense rows S (zeros above the diagonal)
-            const int stored = packed ? 8 * (R / 8 + 1) : (int)S;
+            const int stored = !valid ? 0 : packed ? 8 * (R / 8 + 1) : (int)S;
             float m = -INFINITY, l = 0.f, off = 0.f;
             // pass 0: key blocks 0..qb (row max and sum; the diagonal block, visited last, keeps its
             // exponentials in registers and writes its P at once); pass 1: blocks qb-1..0 write P
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             // dense maps: the columns right of this block's diagonal are exact zeros (reading R11)
-            if (!packed) {
+            if (!packed && valid) {
                 for (int c0 = (qb + 1) * kBlk; c0 < (int)S; c0 += 8)
                     *(uint4 *)(mrow + c0) = make_uint4(0, 0, 0, 0);
             }
@@ -313,11 +315,13 @@ template <int kD>
 cudaError_t launch(const CaptureArgs &a, int sm_count, cudaStream_t st) {
     using C = Cfg<kD>;
     const bool bf16 = a.dt == ATTNCACHE_BF16;
-    const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
+    const uint64_t plane = (uint64_t)a.S * kD * 2;
     CUtensorMap tq, tk;
-    cudaError_t e = make_tmap_2d_16(&tq, a.Q, bf16, kD, rows, (uint64_t)kD * 2, 64, kBlk, 128);
+    cudaError_t e = make_tmap_3d_16(&tq, a.Q, bf16, kD, a.S, (uint64_t)a.max_rows * a.L * a.H, (uint64_t)kD * 2, plane,
+                                    64, kBlk, 128);
     if (e == cudaSuccess)
-        e = make_tmap_2d_16(&tk, a.K, bf16, kD, (uint64_t)a.max_rows * a.L * a.Hkv * a.S, (uint64_t)kD * 2, 64, kBlk, 128);
+        e = make_tmap_3d_16(&tk, a.K, bf16, kD, a.S, (uint64_t)a.max_rows * a.L * a.Hkv, (uint64_t)kD * 2, plane, 64,
+                            kBlk, 128);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(capture_tc_kernel<kD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e == cudaSuccess)
@@ -349,13 +353,13 @@ cudaError_t launch(const CaptureArgs &a, int sm_count, cudaStream_t st) {
 }  // namespace
 
 bool capture_tc_supported(int32_t dt, int32_t S, int32_t d) {
-    return (dt == ATTNCACHE_BF16 || dt == ATTNCACHE_F16) && S >= kBlk && S % kBlk == 0 && (d == 64 || d == 128);
+    return (dt == ATTNCACHE_BF16 || dt == ATTNCACHE_F16) && S >= 8 && S % 8 == 0 && (d == 64 || d == 128);
 }
 
 cudaError_t launch_capture_tc(const CaptureArgs &a, int sm_count, cudaStream_t st) {
-    const uint64_t rows = (uint64_t)a.max_rows * a.L * a.H * a.S;
-    if (rows >= (1ull << 31) || (uint64_t)a.max_rows * a.L * a.H * (a.S / kBlk) >= (1ull << 31))
-        return cudaErrorInvalidValue;
+    // unit indices are int32 TMA coordinates; items = units * ceil(S / 128) is a uint32 loop bound
+    const uint64_t units = (uint64_t)a.max_rows * a.L * a.H;
+    if (units >= (1ull << 31) || units * ((a.S + kBlk - 1) / kBlk) >= (1ull << 31)) return cudaErrorInvalidValue;
     return a.d == 64 ? launch<64>(a, sm_count, st) : launch<128>(a, sm_count, st);
 }
 

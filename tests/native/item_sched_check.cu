@@ -63,9 +63,12 @@ static int check_sched(uint32_t S, uint32_t L, uint32_t H, uint32_t Hkv, uint32_
         const uint32_t ri = (uint32_t)(std::find(rows.begin(), rows.end(), (int32_t)it.row) - rows.begin());
         const uint32_t u = ri * L * H + it.lh;
         if (ri >= n_rows || u >= units || it.qb < 0 || it.qb >= (int)sc.n_qb) return fail("decode range", t, u, it.qb);
+        if (sc.n_qb != (S + 127) / 128) return fail("n_qb", S, sc.n_qb, 0);
         if (it.row0 != ((int64_t)it.row * L * H + it.lh) * S) return fail("row0", t, it.row0, 0);
+        if (it.unit != (int32_t)((int64_t)it.row * L * H + it.lh)) return fail("unit", t, it.unit, 0);
         const uint32_t l = it.lh / H, h = it.lh % H;
         if (it.kv_row0 != (((int64_t)it.row * L + l) * Hkv + h / (H / Hkv)) * (int64_t)S) return fail("kv_row0", t, it.kv_row0, 0);
+        if ((int64_t)it.kv_unit * S != it.kv_row0) return fail("kv_unit", t, it.kv_unit, 0);
         if (seen[(size_t)u * sc.n_qb + it.qb]++) return fail("item twice", t, u, it.qb);
         const int g = (int)(u / sc.group);
         if (g != (int)(t / (sc.group * sc.n_qb))) return fail("group order", t, g, 0);
@@ -94,6 +97,11 @@ int main() {
     bad |= check_sched(1024, 8, 32, 32, 16, 0, 296);  // wave order (capture: two streams per CTA)
     bad |= check_sched(1024, 8, 32, 32, 16, 0, 148);
     bad |= check_sched(384, 2, 8, 2, 7, 0, 148);
+    // S % 128 != 0: a last, partial query block (the paper's context lengths, Table 3: 373 / 1019 tokens)
+    bad |= check_sched(200, 4, 8, 8, 5, 2 * 200 * 128 * 2);
+    bad |= check_sched(373, 2, 8, 2, 3, 2 * 373 * 128 * 2);
+    bad |= check_sched(1019, 2, 4, 4, 3, 0, 148);
+    bad |= check_sched(40, 2, 4, 4, 3, 2 * 40 * 64 * 2);
     std::printf(bad ? "item_sched_check FAILED\n" : "item_sched_check ok\n");
     return bad;
 }

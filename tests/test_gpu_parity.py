@@ -345,8 +345,11 @@ def test_attend_config_shapes(ac, ctx, cfg_name, B, n_sample):
     check_close(_gather_units(O, units), ref, V.dtype, f"attend {cfg_name}")
 
 
-@pytest.mark.parametrize("S,d", [(1, 64), (5, 64), (128, 64), (200, 128)])
+@pytest.mark.parametrize("S,d", [(1, 64), (5, 64), (128, 64), (200, 128), (373, 64), (373, 128), (1019, 128)])
 def test_attend_odd_lengths(ac, ctx, S, d):
+    """Any S on the tensor-core kernels (a last, partial 128-row block): the paper's context lengths (Table 3,
+    PAPER.md:617-622: 373 and 1019 tokens) and tiny ones."""
+    assert ac.attncache_variant("attend", torch.bfloat16, S, d) == "tc"
     Q, K, V = (torch.randn(2, 2, 2, S, d, device=DEV).to(torch.bfloat16) for _ in range(3))
     O = ac.attncache_attend_full(ctx, Q, K, V)
     torch.cuda.synchronize()
@@ -356,6 +359,46 @@ def test_attend_odd_lengths(ac, ctx, S, d):
     check_close(_gather_units(O, units), ref, torch.bfloat16, "attend odd")
     if S == 1:
         assert torch.equal(O, V)
+
+
+@pytest.mark.parametrize("S,d", [(200, 64), (376, 128), (1016, 128), (40, 64)])
+def test_partial_blocks_apply_capture_attend(ac, ctx, S, d):
+    """S % 128 != 0 on the tensor-core A.V and capture kernels (maps need S % 8 == 0: 16-byte map rows):
+    A.V against the oracle with PACKED and DENSE maps, the captured maps against the oracle's causal softmax
+    (DENSE zeros above the diagonal, PACKED row lengths), and capture -> reuse equal to attention."""
+    assert ac.attncache_variant("apply", torch.bfloat16, S, d) == "tc"
+    assert ac.attncache_variant("capture", torch.bfloat16, S, d) == "tc"
+    g = torch.Generator(device=DEV).manual_seed(S + d)
+    B, L, H, N = 3, 2, 2, 4
+    Qm, Km = (torch.randn(N, L, H, S, d, device=DEV, generator=g).to(torch.bfloat16) for _ in range(2))
+    dense = ac.attncache_capture_maps(ctx, Qm, Km, packed=False)
+    packed = ac.attncache_capture_maps(ctx, Qm, Km, packed=True)
+    units = _units(list(range(N)), L, H)
+    off = [(((b * L + l) * H + h) * S * d) for b, l, h in units]
+    P = oracle.attention_map(storage(Qm), storage(Km), "bf16", off, S, d)
+    got = torch.stack([dense[b, l, h] for b, l, h in units]).double().cpu().numpy()
+    iu = np.triu_indices(S, 1)
+    assert np.all(got[:, iu[0], iu[1]] == 0.0)
+    assert np.max(np.abs(got - P)) <= 3e-3
+    x = _normed(N, 1024, torch.bfloat16, 5)
+    db_p = ac.Database(ctx, x, packed, packed=True, seq_len=S)
+    db_d = ac.Database(ctx, x, dense)
+    assert torch.equal(torch.stack([ac.attncache_fetch_maps(db_p, e) for e in range(N)]), dense)
+    V = torch.randn(B, L, H, S, d, device=DEV, generator=g).to(torch.bfloat16)
+    idx = torch.tensor([2, 0, 3], device=DEV)
+    O_p = ac.attncache_apply_cached(db_p, idx, V)
+    O_d = ac.attncache_apply_cached(db_d, idx, V)
+    torch.cuda.synchronize()
+    assert torch.equal(O_p, O_d)
+    u = _units(list(range(B)), L, H)
+    ref = _apply_ref(storage(dense), "bf16", idx.cpu().numpy(), storage(V), "bf16", u, L, H, S, d)
+    check_close(_gather_units(O_p, u), ref, torch.bfloat16, f"apply S={S}")
+    # capture -> reuse: A.V with the captured maps of (Q, K) is attention on (Q, K, V) up to map rounding
+    Qa, Ka = Qm[[2, 0, 3]].contiguous(), Km[[2, 0, 3]].contiguous()
+    O_att = ac.attncache_attend_full(ctx, Qa, Ka, V)
+    torch.cuda.synchronize()
+    d_max = (O_att.double() - O_p.double()).abs().max().item()
+    assert d_max < 3e-2, d_max
 
 
 def test_capture_then_reuse_matches_full_attention(ac, ctx):
