@@ -618,17 +618,24 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
         Q, K, V = (_rows_activations(cfg, k, loc.tolist(), dev) for k in "qkv")
         O = torch.empty_like(V)
         X_home = torch.randn(hc, cfg.S, cfg.H * cfg.d, device=dev).to(synth.torch_dtype(cfg.act_dtype))
-        comm = torch.cuda.Stream(dev)
+        comm, plan_st = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        state = {"plan": plan0}
 
         def one_step():
-            # steady state of a serving loop: the request state of the NEXT batch (same plan here: the bench
-            # repeats one batch) moves on a communication stream while this batch's layers run locally
-            plan = step.plan(q)
-            comm.wait_stream(comp)
-            step.relocate(X_home, plan, stream=comm)
-            step.apply_local(plan, loc, V, O, Q, K)
+            # steady state of a serving loop: this batch's layers run locally on the compute stream (planned and
+            # relocated during the previous step), while the NEXT batch's sharded search and placement (plan
+            # stream; its one host round trip for the send/recv counts stalls only that stream) and the
+            # relocation of its request state (communication stream) run beside them.  The bench repeats one
+            # batch, so every step does one batch's search, placement, relocation and layers; the step ends when
+            # all three streams are done.
+            cur = state["plan"]
+            step.apply_local(cur, loc, V, O, Q, K)
+            nxt = step.plan(q, stream=plan_st)
+            comm.wait_stream(plan_st)
+            step.relocate(X_home, nxt, stream=comm)
             comp.wait_stream(comm)
-            return plan
+            state["plan"] = nxt
+            return nxt
     else:
         Q, K, V = (synth.activations(cfg, k, hb, hc, device=dev) for k in "qkv")
         O = torch.empty_like(V)
@@ -660,8 +667,9 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
         extra = {"queries_per_rank": [int(t.item()) for t in gathered],
                  "plan_load_bytes_per_rank": [float(v) for v in res["load"].tolist()],
                  "relocated_bytes_per_query": cfg.S * cfg.H * cfg.d * 2,
-                 "pipelining": "request-state relocation (attncache_relocate_rows on a communication stream) "
-                               "overlaps the local A.V / attention of the step; both complete inside the step"}
+                 "pipelining": "the next batch's search + placement (plan stream) and request-state relocation "
+                               "(attncache_relocate_rows, communication stream) overlap this batch's local A.V / "
+                               "attention; all complete inside the step"}
     else:
         t = torch.tensor([int(res[2].sum().item())], device=dev)
         dist.all_reduce(t)

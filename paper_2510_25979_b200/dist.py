@@ -83,7 +83,8 @@ class AffinityPrefill(ShardedPrefill):
         idx, score, hit = attncache_search_all(self.db, q_home, self.tau, total=self.total, stream=stream)
         out = attncache_affinity_plan_device(self.ctx, idx, hit, self._sb, self._hb, self.rank, self.hit_cost,
                                              self.miss_cost, stream=stream)
-        counts = out["counts"].tolist()                                                          # one small D2H
+        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream(q_home.device)):
+            counts = out["counts"].tolist()                     # one small D2H: waits for this stream only
         w = self.world
         n_loc = counts[2 * w]
         return {"idx": idx, "score": score, "hit": hit, "assign": out["assign"], "sizes": self.sizes,
