@@ -630,9 +630,12 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
             # all three streams are done.
             cur = state["plan"]
             step.apply_local(cur, loc, V, O, Q, K)
+            for t in (cur["idx_loc"], cur["hit_loc"]):  # made on the plan stream, read here (caching allocator)
+                t.record_stream(comp)
             nxt = step.plan(q, stream=plan_st)
             comm.wait_stream(plan_st)
             step.relocate(X_home, nxt, stream=comm)
+            nxt["send_order"].record_stream(comm)
             comp.wait_stream(comm)
             state["plan"] = nxt
             return nxt

@@ -692,20 +692,26 @@ def attncache_affinity_plan_device(ctx: "Context", idx: torch.Tensor, hit: torch
         raise ValueError("affinity_plan_device: home_begins must have world + 1 entries")
     dev = idx.device
     home = int(hb[rank + 1] - hb[rank]) if 0 <= rank < world else 0
-    out = {"assign": torch.empty(n, dtype=torch.int32, device=dev),
+    p = lambda t: ctypes.c_void_p(t.data_ptr()) if t.numel() else None  # noqa: E731
+    st = torch.cuda.current_stream(dev) if stream is None else stream
+    with torch.cuda.stream(st):  # the outputs (and the counts' zero fill) are ordered on the launch stream
+        out = _plan_outputs(n, world, home, dev)
+    _check(load_library().attncache_affinity_plan_device(
+        ctx.handle, p(idx.contiguous()), p(hit.contiguous()), n, ctypes.c_void_p(sb.ctypes.data), world,
+        float(hit_cost), float(miss_cost), int(rank), ctypes.c_void_p(hb.ctypes.data), p(out["assign"]),
+        p(out["load"]), p(out["loc"]), p(out["idx_loc"]), p(out["hit_loc"]), p(out["send_order"]),
+        p(out["counts"]), _stream(st, dev)))
+    out["send_order"] = out["send_order"][:home]
+    return out
+
+
+def _plan_outputs(n, world, home, dev):
+    return {"assign": torch.empty(n, dtype=torch.int32, device=dev),
            "load": torch.empty(max(world, 1), dtype=torch.float64, device=dev),
            "loc": torch.empty(n, dtype=torch.int64, device=dev), "idx_loc": torch.empty(n, dtype=torch.int64, device=dev),
            "hit_loc": torch.empty(n, dtype=torch.uint8, device=dev),
            "send_order": torch.empty(max(home, 1), dtype=torch.int64, device=dev),
            "counts": torch.zeros(2 * max(world, 1) + 1, dtype=torch.int32, device=dev)}
-    p = lambda t: ctypes.c_void_p(t.data_ptr()) if t.numel() else None  # noqa: E731
-    _check(load_library().attncache_affinity_plan_device(
-        ctx.handle, p(idx.contiguous()), p(hit.contiguous()), n, ctypes.c_void_p(sb.ctypes.data), world,
-        float(hit_cost), float(miss_cost), int(rank), ctypes.c_void_p(hb.ctypes.data), p(out["assign"]),
-        p(out["load"]), p(out["loc"]), p(out["idx_loc"]), p(out["hit_loc"]), p(out["send_order"]),
-        p(out["counts"]), _stream(stream, dev)))
-    out["send_order"] = out["send_order"][:home]
-    return out
 
 
 def attncache_affinity_plan(idx, hit, shard_begins, hit_cost: float = 1.0, miss_cost: float = 1.0):

@@ -80,10 +80,11 @@ class AffinityPrefill(ShardedPrefill):
     def plan(self, q_home: torch.Tensor, stream=None):
         """Search + placement.  Returns a dict with the whole batch's idx/score/hit and plan arrays (device),
         the host counts (send_n | recv_n | n_loc: one small D2H) and this rank's local queries."""
-        idx, score, hit = attncache_search_all(self.db, q_home, self.tau, total=self.total, stream=stream)
-        out = attncache_affinity_plan_device(self.ctx, idx, hit, self._sb, self._hb, self.rank, self.hit_cost,
-                                             self.miss_cost, stream=stream)
-        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream(q_home.device)):
+        st = stream if stream is not None else torch.cuda.current_stream(q_home.device)
+        with torch.cuda.stream(st):  # every output is allocated (caching allocator) and written on `st`
+            idx, score, hit = attncache_search_all(self.db, q_home, self.tau, total=self.total, stream=st)
+            out = attncache_affinity_plan_device(self.ctx, idx, hit, self._sb, self._hb, self.rank, self.hit_cost,
+                                                 self.miss_cost, stream=st)
             counts = out["counts"].tolist()                     # one small D2H: waits for this stream only
         w = self.world
         n_loc = counts[2 * w]
