@@ -43,9 +43,19 @@ constexpr int kOutWarp = 32 * 64 * 2;   // per softmax warp: O staging [32 rows]
 #ifndef SPLIT_NK
 #define SPLIT_NK 2
 #endif
-constexpr int kNK = SPLIT_NK, kNV = 4 - SPLIT_NK;
-static_assert(kNK >= 1 && kNV >= 1 && kNK <= 4 && kNV <= 4, "ring sizes");
-constexpr int kSmem = (2 + kNK + kNV) * kTile + 8 * kOutWarp + 1024 + 256;
+#ifndef SPLIT_NV
+#define SPLIT_NV (4 - SPLIT_NK)
+#endif
+#ifndef SPLIT_NQ
+#define SPLIT_NQ 2
+#endif
+#ifndef SPLIT_STAGE
+#define SPLIT_STAGE 2  // O staging tiles per epilogue warp (2: the two 64-column halves in flight)
+#endif
+constexpr int kNK = SPLIT_NK, kNV = SPLIT_NV, kNQ = SPLIT_NQ, kStage = SPLIT_STAGE;
+static_assert(kNK >= 1 && kNV >= 1 && kNQ >= 1 && kNK <= 4 && kNV <= 4 && kNQ <= 2, "ring sizes");
+constexpr int kSmem = (kNQ + kNK + kNV) * kTile + 4 * kStage * kOutWarp + 1024 + 256;
+static_assert(kSmem <= 232448, "shared memory");
 // TMEM columns (of 512): S/P buffers [0, 256), O [256, 384), the pair exchange of partial row maxima
 // (parity-double-buffered, kXmax + 2 * parity + half) and the row sums for the epilogue (item-parity
 // double-buffered, kXsum + 2 * parity + half) at [384, 392): the warps address their own lanes only.
@@ -109,10 +119,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sQ = smem;               // [2][tile]
-    uint8_t *sK = sQ + 2 * kTile;     // [kNK][tile]
+    uint8_t *sK = sQ + kNQ * kTile;   // [kNK][tile]
     uint8_t *sV = sK + kNK * kTile;   // [kNV][tile]
-    uint8_t *sOut = sV + kNV * kTile; // [4 epilogue warps][2 column halves][kOutWarp]
-    uint64_t *bars = (uint64_t *)(sOut + 8 * kOutWarp);
+    uint8_t *sOut = sV + kNV * kTile; // [4 epilogue warps][kStage][kOutWarp]
+    uint64_t *bars = (uint64_t *)(sOut + 4 * kStage * kOutWarp);
     uint64_t *q_full = bars, *q_empty = q_full + 2;
     uint64_t *k_full = q_empty + 2, *k_empty = k_full + kNK;
     uint64_t *v_full = k_empty + kNK, *v_empty = v_full + kNV;
@@ -173,8 +183,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             while (w.active) {
                 AC_STRESS_DELAY(716u);
                 if (w.j == 0) {
-                    const uint32_t qs = it & 1u;
-                    mbar_wait(&q_empty[qs], ((it >> 1) & 1u) ^ 1u);
+                    const uint32_t qs = it % kNQ;
+                    mbar_wait(&q_empty[qs], ((it / kNQ) & 1u) ^ 1u);
                     mbar_arrive_expect_tx(&q_full[qs], kTile);
                     for (int h = 0; h < 2; ++h)
                         tma_load_3d(smem_u32(sQ + qs * kTile + h * (kBlk * 128)), &tmQ, &q_full[qs], h * 64,
@@ -203,8 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             wP.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
             uint32_t bS = 0, itS = 0, bP = 0, itP = 0;
             auto issue_s = [&]() {
-                const uint32_t buf = bS & 1u, qs = itS & 1u;
-                if (wS.j == 0) mbar_wait(&q_full[qs], (itS >> 1) & 1u);
+                const uint32_t buf = bS & 1u, qs = itS % kNQ;
+                if (wS.j == 0) mbar_wait(&q_full[qs], (itS / kNQ) & 1u);
                 mbar_wait(&k_full[bS % kNK], (bS / kNK) & 1u);
                 SPLIT_TR_MMA(bS, 5);  // K (and Q) of S_{bS} ready
                 tc_fence_after();
@@ -381,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         setmaxnreg_dec<kRegEpilogue>();
         const int q = warp & 3;
         const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-        uint8_t *stage = sOut + q * 2 * kOutWarp;
+        uint8_t *stage = sOut + q * kStage * kOutWarp;
         uint32_t it = 0;
         for (uint32_t t = blockIdx.x; t < items; t += gridDim.x, ++it) {
             AC_STRESS_DELAY(99u);
@@ -405,8 +415,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_before();
                     mbar_arrive(o_free);
                 }
-                uint8_t *st = stage + h * kOutWarp;
-                if (lane == 0) bulk_wait_read<1>();  // the store issued from this staging tile last item
+                uint8_t *st = stage + (h % kStage) * kOutWarp;
+                if (lane == 0) bulk_wait_read<kStage - 1>();  // the store that last read this staging tile
                 __syncwarp();
 #pragma unroll
                 for (int c8 = 0; c8 < 8; ++c8) {
