@@ -1001,6 +1001,44 @@ def test_graphed_prefill_step_equals_eager(ac, ctx):
     torch.cuda.synchronize()
     for a, b in zip((*ref2, O_e2), out):
         assert torch.equal(a, b)
+    # an eager call with a LARGER batch on the same ctx and stream grows (stream-ordered: frees and
+    # reallocates) that stream's scratch; the graph captured its own scratch, so later replays are unaffected
+    big = cfg.with_(B=96)
+    qb, _, _ = synth.queries(big, DEV)
+    Qb, Kb, Vb = (synth.activations(big, k, 0, big.B, device=DEV) for k in "qkv")
+    step(qb, Qb, Kb, Vb, torch.empty_like(Vb))
+    junk = torch.full((1 << 22,), 7, dtype=torch.int64, device=DEV)  # reuse freed memory with other bytes
+    out3 = tuple(t.clone() for t in gstep.replay())
+    torch.cuda.synchronize()
+    for a, b in zip(out, out3):
+        assert torch.equal(a, b)
+    del junk
+
+
+def test_binding_rejects_mismatched_buffers(ac, ctx):
+    """the binding checks what the C ABI cannot see (shapes, dtypes, lengths, devices) before any
+    pointer reaches the library: a wrong-width or wrong-dtype query matrix, an O of another dtype or shape, a
+    hit mask of the wrong length or dtype, an int32 idx, pageable host buffers for the host-buffer call."""
+    cfg = synth.CONFIGS["llama32_1b"].with_(N=8, B=3, L=2)
+    x = synth.features(cfg, 0, cfg.N, DEV)
+    db = ac.Database(ctx, x, ac.attncache_pack_maps(synth.maps(cfg, 0, cfg.N, DEV)), packed=True, seq_len=cfg.S)
+    q, _, _ = synth.queries(cfg, DEV)
+    V = synth.activations(cfg, "v", 0, cfg.B, device=DEV)
+    idx = torch.zeros(cfg.B, dtype=torch.int64, device=DEV)
+    bad = [lambda: ac.attncache_search(db, q[:, :512].contiguous(), 0.9),
+           lambda: ac.attncache_search(db, q.float(), 0.9),
+           lambda: ac.attncache_search(db, q, 0.9, idx=torch.empty(2, dtype=torch.int64, device=DEV)),
+           lambda: ac.attncache_apply_cached(db, idx, V, torch.empty_like(V, dtype=torch.float32)),
+           lambda: ac.attncache_apply_cached(db, idx, V, V[:2].clone()),
+           lambda: ac.attncache_apply_cached(db, idx, V, hit=torch.ones(2, dtype=torch.uint8, device=DEV)),
+           lambda: ac.attncache_apply_cached(db, idx, V, hit=torch.ones(cfg.B, dtype=torch.int32, device=DEV)),
+           lambda: ac.attncache_apply_cached(db, idx.int(), V),
+           lambda: ac.attncache_attend_full(ctx, V, V, V, torch.empty(1, device=DEV)),
+           lambda: ac.attncache_attend_full(ctx, V, V, V, skip=torch.zeros(cfg.B + 1, dtype=torch.uint8, device=DEV)),
+           lambda: ac.attncache_prefill_host(db, q.cpu(), V.cpu(), V.cpu(), V.cpu(), 0.9)]
+    for f in bad:
+        with pytest.raises(ValueError):
+            f()
 
 
 def test_edge_cases_empty_skipped_and_extreme_shapes(ac, ctx):
