@@ -1003,7 +1003,7 @@ def test_graphed_prefill_step_equals_eager(ac, ctx):
         assert torch.equal(a, b)
     # an eager call with a LARGER batch on the same ctx and stream grows (stream-ordered: frees and
     # reallocates) that stream's scratch; the graph captured its own scratch, so later replays are unaffected
-    big = cfg.with_(B=96)
+    big = cfg.with_(B=48)
     qb, _, _ = synth.queries(big, DEV)
     Qb, Kb, Vb = (synth.activations(big, k, 0, big.B, device=DEV) for k in "qkv")
     step(qb, Qb, Kb, Vb, torch.empty_like(Vb))
