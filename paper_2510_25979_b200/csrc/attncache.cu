@@ -117,7 +117,7 @@ attncache_status attncache_ctx_create(int32_t device, int32_t rank, int32_t worl
                                       attncache_ctx **out) {
     if (!out) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_create: out is NULL");
     *out = nullptr;
-    if (world < 1 || rank < 0 || rank >= world)
+    if (world < 1 || world > 1024 || rank < 0 || rank >= world)
         return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_create: rank %d of world %d", rank, world);
     if (world > 1 && !uid) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_create: world %d needs a unique id", world);
     int n = 0;

@@ -263,7 +263,9 @@ attncache_status apply_routed(attncache_db *db, const int64_t *idx, const uint8_
     int32_t *owner = (int32_t *)route;
     int64_t *order = (int64_t *)((uint8_t *)route + ((nh * 4 + 15) & ~(size_t)15));
     int64_t *idx_send = order + nh;
-    int32_t *counts = (int32_t *)(ctx->d_small + 8);  // int32 [world]
+    // int32 [world] send counts | [world] receive counts, in a region of the small staging buffers that the
+    // count exchange of home_counts (elements [0, 8 + world)) never touches
+    int32_t *counts = (int32_t *)(ctx->d_small + kPinnedInts / 2);
     if (n_home) {
         AC_CUDA(launch_route_plan(idx, hit, n_home, db->d_shard_begins, w, owner, counts, order, st));
     } else {
@@ -277,7 +279,7 @@ attncache_status apply_routed(attncache_db *db, const int64_t *idx, const uint8_
         AC_NCCL(N->Recv(recv_counts + p, 1, ncclInt32, p, comm_of(ctx), st));
     }
     AC_NCCL(N->GroupEnd());
-    int32_t *hc = (int32_t *)ctx->h_pinned;
+    int32_t *hc = (int32_t *)(ctx->h_pinned + kPinnedInts / 2);
     AC_CUDA(cudaMemcpyAsync(hc, counts, sizeof(int32_t) * 2 * w, cudaMemcpyDeviceToHost, st));
     AC_CUDA(cudaStreamSynchronize(st));
     std::vector<int64_t> sn(w), rn(w), so(w + 1, 0), ro(w + 1, 0);

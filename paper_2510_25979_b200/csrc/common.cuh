@@ -145,7 +145,7 @@ struct attncache_db {
 };
 
 namespace ac {
-constexpr int kPinnedInts = 4 * 1024 + 16;
+constexpr int kPinnedInts = 4 * 1024 + 16;  // small int64 staging (host pinned and device): world <= 1024
 // Device scratch of at least `bytes` for (stream, kind); see ScratchKind.
 attncache_status scratch(attncache_ctx *ctx, cudaStream_t st, int kind, size_t bytes, void **out);
 
