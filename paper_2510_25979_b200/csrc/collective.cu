@@ -373,18 +373,35 @@ attncache_status attncache_relocate_rows(attncache_ctx *ctx, const void *src, in
         return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "relocate_rows: buffers must be device memory");
     DeviceGuard g(ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
+    // rows that stay on this rank are gathered straight into their place in dst (one copy, no NCCL); the rows
+    // for the other ranks are gathered into a send buffer and exchanged in one NCCL group
+    const int me = (w == 1 || !ctx->comm) ? 0 : ctx->rank;
+    const bool ok8 = row_bytes % 8 == 0;
+    if (sn[me] && rn[me] != sn[me])
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "relocate_rows: %lld rows to self but %lld from self",
+                    (long long)sn[me], (long long)rn[me]);
+    if (sn[me]) {
+        uint8_t *d = (uint8_t *)dst + (size_t)row_bytes * ro[me];
+        const bool ok16 = row_bytes % 16 == 0 && aligned16(src) && aligned16(d);
+        AC_CUDA(launch_copy_rows(src, send_order + so[me], sn[me], row_bytes, d, true, ok16 && ok8, st));
+    }
+    if (w == 1 || !ctx->comm) return ATTNCACHE_OK;
+    const int64_t n_out = n_home - sn[me];
     void *send = nullptr;
-    attncache_status s = scratch(ctx, st, kScSend, (size_t)row_bytes * (size_t)n_home, &send);
+    attncache_status s = scratch(ctx, st, kScSend, (size_t)row_bytes * (size_t)std::max<int64_t>(n_out, 1), &send);
     if (s) return s;
-    if (n_home) {
-        const bool ok16 = row_bytes % 16 == 0 && aligned16(src) && aligned16(send);
-        AC_CUDA(launch_copy_rows(src, send_order, n_home, row_bytes, send, true, ok16, st));
-    }
-    if (w == 1 || !ctx->comm) {
-        if (ro[w]) AC_CUDA(cudaMemcpyAsync(dst, send, (size_t)row_bytes * ro[w], cudaMemcpyDeviceToDevice, st));
-        return ATTNCACHE_OK;
-    }
-    return exchange_rows(ctx, send, sn.data(), so.data(), dst, rn.data(), ro.data(), (size_t)row_bytes, st);
+    // send buffer: the rows of ranks below me at [0, so[me]), above me at [so[me], n_out)
+    const bool ok16 = row_bytes % 16 == 0 && aligned16(src) && aligned16(send);
+    if (so[me]) AC_CUDA(launch_copy_rows(src, send_order, so[me], row_bytes, send, true, ok16, st));
+    if (so[w] > so[me + 1])
+        AC_CUDA(launch_copy_rows(src, send_order + so[me + 1], so[w] - so[me + 1], row_bytes,
+                                 (uint8_t *)send + (size_t)row_bytes * so[me], true,
+                                 ok16 && ((size_t)row_bytes * so[me]) % 16 == 0, st));
+    std::vector<int64_t> sn2 = sn, so2(w, 0), rn2 = rn;
+    for (int p = 0; p < w; ++p) so2[p] = p < me ? so[p] : so[p] - sn[me];
+    sn2[me] = 0;
+    rn2[me] = 0;
+    return exchange_rows(ctx, send, sn2.data(), so2.data(), dst, rn2.data(), ro.data(), (size_t)row_bytes, st);
 }
 
 }  // extern "C"
