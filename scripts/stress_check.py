@@ -43,7 +43,8 @@ cases = []
 # attention: d = 128 (column-split kernel; S = 1024 and a GQA S = 384 case with a skipped row) and
 # d = 64 (two-group kernel)
 for name, (rows, L, H, Hkv, S, d) in {"att128": (8, 4, 8, 8, 1024, 128), "att128gqa": (16, 2, 8, 2, 384, 128),
-                                      "att64": (16, 4, 8, 8, 256, 64)}.items():
+                                      "att64": (16, 4, 8, 8, 256, 64), "att64tail": (8, 2, 8, 8, 200, 64),
+                                      "att128tail": (8, 2, 8, 8, 1019, 128)}.items():
     Q = rnd((rows, L, H, S, d), 1)
     K = rnd((rows, L, Hkv, S, d), 2)
     V = rnd((rows, L, Hkv, S, d), 3)
@@ -53,7 +54,9 @@ for name, (rows, L, H, Hkv, S, d) in {"att128": (8, 4, 8, 8, 1024, 128), "att128
                                                                                  skip=skip)))
 
 # A.V over packed causal maps: d = 64 / S = 128 and d = 128 / S = 256
-for name, (N, B, L, H, S, d) in {"apply64": (16, 64, 4, 8, 128, 64), "apply128": (8, 16, 4, 8, 256, 128)}.items():
+# (S > 128: the paired-row-block kernel, an odd row-block count and a partial last block included)
+for name, (N, B, L, H, S, d) in {"apply64": (16, 64, 4, 8, 128, 64), "apply128": (8, 16, 4, 8, 256, 128),
+                                 "apply128pairs": (6, 12, 2, 8, 640, 128), "apply64tail": (6, 12, 2, 8, 584, 64)}.items():
     maps = torch.empty((N, L, H, ac.attncache_packed_map_elems(S)), dtype=torch.bfloat16, device=dev)
     ac.attncache_pack_maps(softmax_maps(N, L, H, S, 4), maps)
     db = ac.Database(ctx, normed(N, 256, 5), maps, packed=True, seq_len=S)
