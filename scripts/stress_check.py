@@ -80,6 +80,11 @@ db_s = ac.Database(ctx, x)
 for B in (64, 1024):
     q = normed(B, 1024, 11 + B)
     cases.append((f"search{B}", lambda q=q: torch.stack([t.to(torch.float64) for t in ac.attncache_search(db_s, q, 0.5)])))
+# the two-query-tile search kernel (B > 128 and enough (pair, entry tile) items): 150,001 entries, B = 300
+x2 = normed(150_001, 1024, 12)
+db_s2 = ac.Database(ctx, x2)
+q2 = normed(300, 1024, 13)
+cases.append(("search_pairs", lambda: torch.stack([t.to(torch.float64) for t in ac.attncache_search(db_s2, q2, 0.5)])))
 
 # feature projector (two tcgen05 GEMMs + normalisation)
 h = rnd((2048, 2048), 12)

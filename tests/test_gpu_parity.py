@@ -190,9 +190,10 @@ def test_search_sweep_1m_sampled(ac, ctx, sweep_db, B):
 
 def test_search_mid_tile_and_simt_bf16(ac, ctx):
     """The 128-entry tile of search_tc_kernel (N = 50,000 with B = 128: fewer than 2 work items per SM with
-    256-entry tiles, enough with 128) and the bf16 CUDA-core search (D = 200 is not a multiple of the
-    64-element tensor-core chunk), each against the oracle with planted cross-tile duplicates."""
-    for N, B, D in ((50_000, 128, 1024), (777, 33, 200)):
+    256-entry tiles, enough with 128), the bf16 CUDA-core search (D = 200 is not a multiple of the 64-element
+    tensor-core chunk) and the two-query-tile kernel with a ragged batch (B = 300: a pair and a lone tile; a
+    partial entry tile), each against the oracle with planted cross-tile duplicates."""
+    for N, B, D in ((50_000, 128, 1024), (777, 33, 200), (100_003, 300, 1024)):
         x = _normed(N, D, torch.bfloat16, 31)
         q = _normed(B, D, torch.bfloat16, 32)
         x[N - 5] = x[130]
