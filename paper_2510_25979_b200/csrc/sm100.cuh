@@ -396,6 +396,116 @@ __device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         : "memory");
 }
 
+// ---- CTA pairs (cta_group::2): two SMs of a cluster share one MMA of M = 256 ---------------------------
+// Each CTA provides half of A (its 128 rows) and half of B (N / 2 of the columns) from its own shared memory
+// at the same offsets; each CTA's TMEM receives its 128 rows of D.  Only the leader (cluster rank 0) issues
+// the MMAs; commits multicast to both CTAs' barriers; operand loads of both CTAs signal the leader's barriers.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// The shared::cluster address of `local` (a shared::cta address) in the CTA of cluster rank `rank`.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+// Arrive (release at cluster scope) on an mbarrier given by a shared::cluster address (possibly remote).
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc2(uint32_t *dst_smem) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
+}
+// TMA 3-D load into this CTA's shared memory whose completion is signalled on the mbarrier at the
+// shared::cluster address `bar` (the leader's).
+__device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const CUtensorMap *m, uint32_t bar, int32_t c0, int32_t c1,
+                                                int32_t c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+        "%5}], [%2];" ::"r"(dst),
+        "l"((uint64_t)m), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+// Arrives on the barrier at this offset in both CTAs of the pair once the leader's prior MMAs complete.
+__device__ __forceinline__ void umma2_commit_w(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+// Eight K = 16 SS steps of a pair MMA (K = 128), whole warp, one elected lane: A and B are K-major 128B-swizzled
+// tiles of two 64-column halves with their own half strides (descriptor units of 16 bytes).
+template <uint32_t kHalfA, uint32_t kHalfB>
+__device__ __forceinline__ void umma2_f16_ss_k8_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, t, e;\n\t.reg .b64 a, b;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.b32 t, 0, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "add.s64 a, %1, 2;\n\tadd.s64 b, %2, 2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, 4;\n\tadd.s64 b, %2, 4;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, 6;\n\tadd.s64 b, %2, 6;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, %5;\n\tadd.s64 b, %2, %9;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, %6;\n\tadd.s64 b, %2, %10;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %11;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, %8;\n\tadd.s64 b, %2, %12;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "n"(kHalfA), "n"(kHalfA + 2), "n"(kHalfA + 4),
+        "n"(kHalfA + 6), "n"(kHalfB), "n"(kHalfB + 2), "n"(kHalfB + 4), "n"(kHalfB + 6)
+        : "memory");
+}
+// Eight K = 16 TS steps of a pair MMA: A = 8 TMEM columns per step (each CTA's own rows), B MN-major (2048 B
+// per step).
+__device__ __forceinline__ void umma2_f16_ts_k8_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, t, e;\n\t.reg .b64 b;\n\t.reg .b32 a;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.b32 t, 0, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+        "add.s32 a, %1, 8;\n\tadd.s64 b, %2, 128;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.s32 a, %1, 16;\n\tadd.s64 b, %2, 256;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.s32 a, %1, 24;\n\tadd.s64 b, %2, 384;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.s32 a, %1, 32;\n\tadd.s64 b, %2, 512;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.s32 a, %1, 40;\n\tadd.s64 b, %2, 640;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.s32 a, %1, 48;\n\tadd.s64 b, %2, 768;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.s32 a, %1, 56;\n\tadd.s64 b, %2, 896;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // ---- packed fp32 pairs and an FMA-pipe exp2 ----------------------------------------------------------
 // Packed fp32 pairs (sm_100 FFMA2 / FADD2): low word = first element.
 __device__ __forceinline__ uint64_t pack2(float lo, float hi) {
