@@ -402,6 +402,34 @@ def test_partial_blocks_apply_capture_attend(ac, ctx, S, d):
     assert d_max < 3e-2, d_max
 
 
+@pytest.mark.parametrize("S,d", [(128, 64), (256, 128), (200, 64)])
+def test_fp16_tensor_core_paths(ac, ctx, S, d):
+    """The fp16 variants of the tensor-core kernels (the configs are bf16): capture of fp16 maps from fp16
+    Q, K, A.V with those maps (single-row-block and paired kernels), attention, each against the oracle."""
+    assert ac.attncache_variant("apply", torch.float16, S, d) == "tc"
+    g = torch.Generator(device=DEV).manual_seed(S * 7 + d)
+    N, B, L, H = 3, 2, 2, 2
+    Qm, Km = (torch.randn(N, L, H, S, d, device=DEV, generator=g).to(torch.float16) for _ in range(2))
+    maps = ac.attncache_capture_maps(ctx, Qm, Km, map_dtype=torch.float16, packed=True)
+    db = ac.Database(ctx, _normed(N, 1024, torch.bfloat16, 9), maps, packed=True, seq_len=S)
+    dense = torch.stack([ac.attncache_fetch_maps(db, e) for e in range(N)])
+    units_m = _units(list(range(N)), L, H)
+    off_m = [(((b * L + l) * H + h) * S * d) for b, l, h in units_m]
+    P = oracle.attention_map(storage(Qm), storage(Km), "f16", off_m, S, d)
+    assert np.max(np.abs(torch.stack([dense[b, l, h] for b, l, h in units_m]).double().cpu().numpy() - P)) <= 2e-3
+    Q, K, V = (torch.randn(B, L, H, S, d, device=DEV, generator=g).to(torch.float16) for _ in range(3))
+    idx = torch.tensor([2, 0], device=DEV)
+    O = ac.attncache_apply_cached(db, idx, V)
+    A = ac.attncache_attend_full(ctx, Q, K, V)
+    torch.cuda.synchronize()
+    u = _units(list(range(B)), L, H)
+    ref = _apply_ref(storage(dense), "f16", idx.cpu().numpy(), storage(V), "f16", u, L, H, S, d)
+    check_close(_gather_units(O, u), ref, torch.float16, f"fp16 apply S={S}")
+    off = [(((b * L + l) * H + h) * S * d) for b, l, h in u]
+    ref = oracle.attend(storage(Q), storage(K), storage(V), "f16", off, S, d)
+    check_close(_gather_units(A, u), ref, torch.float16, f"fp16 attend S={S}")
+
+
 def test_capture_then_reuse_matches_full_attention(ac, ctx):
     """maps captured from an input, stored as a DB entry, reproduce full attention."""
     cfg = synth.CONFIGS["llama32_1b"].with_(N=2, L=2, H=4)
