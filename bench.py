@@ -527,8 +527,8 @@ def eq5_block(ac, ctx, db, cfg, idx, hit, stream, steps):
     del X, Wq, Wk, Wv, blk
     return {"layer_full_ms": full_ms, "layer_cached_ms": cached_ms, "layer_all_hits_ms": hits_ms,
             "speedup_batch": full_ms / cached_ms, "speedup_per_hit": full_ms / hits_ms,
-            "note": "one layer, whole batch; projections via cuBLAS (torch.matmul), RoPE/A.V/attention via "
-                    "this library; synthetic weights; paper: 3x attention on A100 (PAPER.md:446)"}
+            "note": "one layer, whole batch; Q/K/V projections (attncache_linear), RoPE, A.V and attention all "
+                    "in this library; synthetic weights; paper: 3x attention on A100 (PAPER.md:446)"}
 
 
 def eager_attention_ms(Q, K, V, stream, steps):
