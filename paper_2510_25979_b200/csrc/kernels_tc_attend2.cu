@@ -93,6 +93,12 @@ using Walker = ItemWalker;
 #if defined(ATT_TRACE)  // timeline experiment (scripts/attend_trace.py --split): clock64 stamps of CTA 0
 __device__ unsigned long long g_split_trace_sm[256][6];   // softmax warp 4, lane 0, first 256 blocks
 __device__ unsigned long long g_split_trace_mma[256][6];  // MMA thread, first 256 blocks
+__device__ unsigned long long g_split_trace_arr[256][8][5];  // every softmax warp (lane 0), first 256 blocks:
+                                                               // start, S ok, exchanged, P stored, arrived
+#define SPLIT_TR_ARR(slot)                                                                              \
+    do {                                                                                                \
+        if (blockIdx.x == 0 && lane == 0 && b < 256) g_split_trace_arr[b][warp - 4][slot] = clock64();  \
+    } while (0)
 #define SPLIT_TR_SM(slot)                                                                          \
     do {                                                                                           \
         if (blockIdx.x == 0 && warp == 4 && lane == 0 && b < 256) g_split_trace_sm[b][slot] = clock64(); \
@@ -107,6 +113,9 @@ __device__ unsigned long long g_split_trace_mma[256][6];  // MMA thread, first 2
     } while (0)
 #define SPLIT_TR_MMA(bb, slot) \
     do {                       \
+    } while (0)
+#define SPLIT_TR_ARR(slot) \
+    do {                   \
     } while (0)
 #endif
 
@@ -275,8 +284,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t buf = b & 1u;
             const uint32_t s_addr = tmem + lane_addr + buf * kBlk;
             SPLIT_TR_SM(0);
+            SPLIT_TR_ARR(0);
             mbar_wait(&s_full[buf], (b >> 1) & 1u);
             SPLIT_TR_SM(1);
+            SPLIT_TR_ARR(1);
             tc_fence_after();
             uint32_t sv[64];  // this warp's 64 keys of its row
             tmem_ld_32x32b_x64(s_addr + half * 64, sv);
@@ -306,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mx = fmaxf(mx, __uint_as_float(tmem_ld_32x32b_x1(xcol + (half ^ 1))));
             tmem_ld_wait();
             SPLIT_TR_SM(2);
+            SPLIT_TR_ARR(2);
             const float m_blk = mx * sl2;
             if (j == 0) {
                 m_ref = m_blk;
@@ -378,9 +390,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tmem_st_wait();
             SPLIT_TR_SM(3);
+            SPLIT_TR_ARR(3);
             tc_fence_before();
             mbar_arrive(&p_full[buf]);
             SPLIT_TR_SM(4);
+            SPLIT_TR_ARR(4);
             ++b;
             if (w.advance(sc)) ++it;
         }
@@ -491,5 +505,8 @@ extern "C" int attncache_debug_split_trace(void *sm, void *mma) {
     cudaError_t e = cudaMemcpyFromSymbol(sm, ac::g_split_trace_sm, sizeof(ac::g_split_trace_sm));
     if (e == cudaSuccess) e = cudaMemcpyFromSymbol(mma, ac::g_split_trace_mma, sizeof(ac::g_split_trace_mma));
     return (int)e;
+}
+extern "C" int attncache_debug_split_trace_arr(void *arr) {
+    return (int)cudaMemcpyFromSymbol(arr, ac::g_split_trace_arr, sizeof(ac::g_split_trace_arr));
 }
 #endif

@@ -332,6 +332,73 @@ __device__ __forceinline__ void umma_commit_w(uint64_t *bar) {
         : "memory");
 }
 
+// Lean forms of the two eight-step issues above: the descriptors are passed as 32-bit words (the low word holds
+// the start address and LBO fields, the high word SBO / version / swizzle and never changes for a k step), the
+// k-step offsets are 32-bit adds on the low word and the instruction descriptor is an immediate.  With warp-
+// uniform inputs (e.g. from __shfl_sync) ptxas keeps all of it in uniform registers: no R2UR per MMA.
+template <uint32_t kIdesc, uint32_t kHalfUnits>
+__device__ __forceinline__ void umma_ss8_lo(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t a_hi, uint32_t b_hi,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, t, e;\n\t.reg .b64 a, b;\n\t.reg .b32 x, y;\n\t"
+        "setp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "mov.b64 a, {%1, %3};\n\tmov.b64 b, {%2, %4};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, p;\n\t"
+        "add.u32 x, %1, 2;\n\tadd.u32 y, %2, 2;\n\tmov.b64 a, {x, %3};\n\tmov.b64 b, {y, %4};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, t;\n\t"
+        "add.u32 x, %1, 4;\n\tadd.u32 y, %2, 4;\n\tmov.b64 a, {x, %3};\n\tmov.b64 b, {y, %4};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, t;\n\t"
+        "add.u32 x, %1, 6;\n\tadd.u32 y, %2, 6;\n\tmov.b64 a, {x, %3};\n\tmov.b64 b, {y, %4};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, t;\n\t"
+        "add.u32 x, %1, %7;\n\tadd.u32 y, %2, %7;\n\tmov.b64 a, {x, %3};\n\tmov.b64 b, {y, %4};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, t;\n\t"
+        "add.u32 x, %1, %8;\n\tadd.u32 y, %2, %8;\n\tmov.b64 a, {x, %3};\n\tmov.b64 b, {y, %4};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, t;\n\t"
+        "add.u32 x, %1, %9;\n\tadd.u32 y, %2, %9;\n\tmov.b64 a, {x, %3};\n\tmov.b64 b, {y, %4};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, t;\n\t"
+        "add.u32 x, %1, %10;\n\tadd.u32 y, %2, %10;\n\tmov.b64 a, {x, %3};\n\tmov.b64 b, {y, %4};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %6, t;\n\t}" ::"r"(d_tmem),
+        "r"(a_lo), "r"(b_lo), "r"(a_hi), "r"(b_hi), "r"(accumulate), "n"(kIdesc), "n"(kHalfUnits), "n"(kHalfUnits + 2),
+        "n"(kHalfUnits + 4), "n"(kHalfUnits + 6)
+        : "memory");
+}
+// A from TMEM (8 columns per k step), B an MN-major smem operand advancing kBStep descriptor units per k step.
+template <uint32_t kIdesc, uint32_t kBStep>
+__device__ __forceinline__ void umma_ts8_lo(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t b_hi,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, t, e;\n\t.reg .b64 b;\n\t.reg .b32 x, y;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "mov.b64 b, {%2, %3};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], b, %5, p;\n\t"
+        "add.u32 x, %1, 8;\n\tadd.u32 y, %2, %6;\n\tmov.b64 b, {y, %3};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %5, t;\n\t"
+        "add.u32 x, %1, 16;\n\tadd.u32 y, %2, %7;\n\tmov.b64 b, {y, %3};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %5, t;\n\t"
+        "add.u32 x, %1, 24;\n\tadd.u32 y, %2, %8;\n\tmov.b64 b, {y, %3};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %5, t;\n\t"
+        "add.u32 x, %1, 32;\n\tadd.u32 y, %2, %9;\n\tmov.b64 b, {y, %3};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %5, t;\n\t"
+        "add.u32 x, %1, 40;\n\tadd.u32 y, %2, %10;\n\tmov.b64 b, {y, %3};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %5, t;\n\t"
+        "add.u32 x, %1, 48;\n\tadd.u32 y, %2, %11;\n\tmov.b64 b, {y, %3};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %5, t;\n\t"
+        "add.u32 x, %1, 56;\n\tadd.u32 y, %2, %12;\n\tmov.b64 b, {y, %3};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %5, t;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(accumulate), "n"(kIdesc), "n"(kBStep), "n"(2 * kBStep),
+        "n"(3 * kBStep), "n"(4 * kBStep), "n"(5 * kBStep), "n"(6 * kBStep), "n"(7 * kBStep)
+        : "memory");
+}
+// Low / high 32-bit words of smem_desc(saddr, lbo, sbo, layout).
+__host__ __device__ constexpr uint32_t smem_desc_lo(uint32_t saddr, uint32_t lbo_bytes) {
+    return ((saddr & 0x3FFFFu) >> 4) | (((lbo_bytes >> 4) & 0x3FFFu) << 16);
+}
+__host__ __device__ constexpr uint32_t smem_desc_hi(uint32_t sbo_bytes, uint32_t layout) {
+    return ((sbo_bytes >> 4) & 0x3FFFu) | (1u << 14) | (layout << 29);
+}
+// Warp-uniform copy of a value every lane holds (ptxas keeps SHFL-with-lane-0 results in uniform registers).
+__device__ __forceinline__ uint32_t warp_uniform(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+
 // ---- tcgen05.ld: 32 lanes x 32 bit, 32 consecutive columns per thread ------------------------------
 __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
