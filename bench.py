@@ -620,6 +620,11 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
         X_home = torch.randn(hc, cfg.S, cfg.H * cfg.d, device=dev).to(synth.torch_dtype(cfg.act_dtype))
         comm, plan_st = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         state = {"plan": plan0}
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        budget = (sms - args.aux_sms, args.aux_sms) if 0 < args.aux_sms < sms else (sms, sms)
+        # the layers' persistent kernels leave aux_sms SMs to the next batch's search, placement, relocation
+        # copies and NCCL kernels on the side streams (attncache_ctx_set_sm_budget)
+        ctx.set_sm_budget(*budget)
 
         def one_step():
             # steady state of a serving loop: this batch's layers run locally on the compute stream (planned and
@@ -667,7 +672,8 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
         per_rank = torch.tensor([loc.numel()], device=dev)
         gathered = [torch.empty_like(per_rank) for _ in range(world)]
         dist.all_gather(gathered, per_rank)
-        extra = {"queries_per_rank": [int(t.item()) for t in gathered],
+        extra = {"sm_budget": {"compute_sms": budget[0], "aux_sms": budget[1]},
+                 "queries_per_rank": [int(t.item()) for t in gathered],
                  "plan_load_bytes_per_rank": [float(v) for v in res["load"].tolist()],
                  "relocated_bytes_per_query": cfg.S * cfg.H * cfg.d * 2,
                  "pipelining": "the next batch's search + placement (plan stream) and request-state relocation "
@@ -811,6 +817,10 @@ def main(argv=None):
     ap.add_argument("--batch", type=int, default=None, help="override the config's query batch")
     ap.add_argument("--seed", type=int, default=None, help="override the config's seed")
     ap.add_argument("--force-dist", action="store_true", help="run the multi-GPU path even at world size 1 (testing)")
+    ap.add_argument("--aux-sms", type=int, default=0,
+                    help="N > 1 pipelined step: SMs left to the side streams' search / placement / relocation kernels "
+                         "(attncache_ctx_set_sm_budget; 0 = no budget, the default: at world 1 every reserve measured "
+                         "slower, scripts/sm_budget_sweep.sh)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("bench.py: note: --warmup < 3 does not meet the timing rules (profiling runs only)", file=sys.stderr)

@@ -102,6 +102,15 @@ attncache_status attncache_ctx_create(int32_t device, int32_t rank, int32_t worl
                                       attncache_ctx **out);
 /* rank / world of the ctx (0 / 1 for a local ctx); either pointer may be NULL. */
 attncache_status attncache_ctx_info(const attncache_ctx *ctx, int32_t *rank, int32_t *world);
+/* SM budget of the ctx's kernels (no paper passage: a B200 scheduling control for the pipelined multi-GPU
+ * step).  compute_sms caps the CTAs of the persistent layer kernels (apply_cached / _local,
+ * attend_full, capture_maps, linear), aux_sms the CTAs of the search, projector, placement and row-copy
+ * kernels.  Both default to the device's SM count.  A caller that runs the next batch's search, placement
+ * and relocation on other streams beside this batch's layers sets compute_sms + aux_sms <= the SM count,
+ * so those kernels (and NCCL's) find free SMs instead of queueing behind the persistent kernels.  Results
+ * do not depend on the budget (the kernels' outputs are independent of their CTA counts).
+ * Errors: INVALID_ARGUMENT (NULL ctx, a value < 1 or above the SM count). */
+attncache_status attncache_ctx_set_sm_budget(attncache_ctx *ctx, int32_t compute_sms, int32_t aux_sms);
 attncache_status attncache_ctx_destroy(attncache_ctx *ctx);
 /* Synchronises the device and returns (then clears) any deferred error: ERR_NOT_FOUND when an
  * apply call met an index outside its shard, ERR_CUDA on an asynchronous CUDA fault, ERR_NCCL on an

@@ -28,7 +28,7 @@ __all__ = [
     "attncache_affinity_plan", "attncache_project_features", "attncache_apply_cached_gqa", "attncache_attend_full_gqa",
     "attncache_capture_maps_gqa", "attncache_affinity_plan_device", "ABI_FUNCTIONS", "attncache_get_unique_id",
     "attncache_ctx_info", "attncache_set_batch_layout", "attncache_search_all", "attncache_apply_cached_local",
-    "attncache_relocate_rows", "attncache_prefill_host", "attncache_linear",
+    "attncache_relocate_rows", "attncache_prefill_host", "attncache_linear", "attncache_ctx_set_sm_budget",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -45,7 +45,7 @@ ABI_FUNCTIONS = [
     "attncache_apply_cached_gqa", "attncache_attend_full_gqa", "attncache_capture_maps_gqa",
     "attncache_affinity_plan_device", "attncache_get_unique_id", "attncache_ctx_info", "attncache_set_batch_layout",
     "attncache_search_all", "attncache_apply_cached_local", "attncache_relocate_rows", "attncache_prefill_host",
-    "attncache_linear",
+    "attncache_linear", "attncache_ctx_set_sm_budget",
 ]
 
 _DT = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -96,6 +96,7 @@ def load_library():
         "attncache_ctx_create": ([I32, I32, I32, P, ctypes.POINTER(P)], I32),
         "attncache_get_unique_id": ([P], I32),
         "attncache_ctx_info": ([P, P, P], I32),
+        "attncache_ctx_set_sm_budget": ([P, I32, I32], I32),
         "attncache_set_batch_layout": ([P, P, I32], I32),
         "attncache_search_all": ([P, P, I64, F32, P, P, P, P], I32),
         "attncache_apply_cached_local": ([P, P, P, I64, I32, I32, I32, I32, I32, P, P, P], I32),
@@ -187,6 +188,11 @@ class Context:
         obj = [attncache_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
         return cls(device, rank, world, obj[0])
+
+    def set_sm_budget(self, compute_sms: int, aux_sms: int):
+        """CTA caps of the persistent layer kernels and of the search / placement / copy kernels (both default
+        to the SM count); see attncache_ctx_set_sm_budget."""
+        attncache_ctx_set_sm_budget(self, compute_sms, aux_sms)
 
     def set_batch_layout(self, home_counts):
         """Declares every rank's home batch size for the following collective calls (None clears it)."""
@@ -290,6 +296,10 @@ def attncache_get_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(load_library().attncache_get_unique_id(buf))
     return buf.raw
+
+
+def attncache_ctx_set_sm_budget(ctx: Context, compute_sms: int, aux_sms: int):
+    _check(load_library().attncache_ctx_set_sm_budget(ctx.handle, int(compute_sms), int(aux_sms)))
 
 
 def attncache_ctx_info(ctx: Context):

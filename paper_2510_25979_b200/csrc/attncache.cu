@@ -136,6 +136,7 @@ attncache_status attncache_ctx_create(int32_t device, int32_t rank, int32_t worl
     attncache_ctx *c = new attncache_ctx();
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
+    c->compute_sms = c->aux_sms = c->sm_count;
     const char *fr = getenv("ATTNCACHE_FORCE_ROUTE");
     c->force_route = fr && *fr == '1';
     e = cudaMalloc(&c->d_error, sizeof(int));
@@ -161,6 +162,17 @@ attncache_status attncache_ctx_info(const attncache_ctx *ctx, int32_t *rank, int
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_info: ctx is NULL");
     if (rank) *rank = ctx->rank;
     if (world) *world = ctx->world;
+    return ATTNCACHE_OK;
+}
+
+attncache_status attncache_ctx_set_sm_budget(attncache_ctx *ctx, int32_t compute_sms, int32_t aux_sms) {
+    if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_set_sm_budget: ctx is NULL");
+    if (compute_sms < 1 || compute_sms > ctx->sm_count || aux_sms < 1 || aux_sms > ctx->sm_count)
+        return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_set_sm_budget: compute_sms %d / aux_sms %d outside [1, %d]",
+                    compute_sms, aux_sms, ctx->sm_count);
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->compute_sms = compute_sms;
+    ctx->aux_sms = aux_sms;
     return ATTNCACHE_OK;
 }
 
@@ -271,7 +283,7 @@ attncache_status ac::search_keys_impl(attncache_db *db, const void *queries, int
     if (d.shard_count == 0 || n == 0) return ATTNCACHE_OK;
     if (search_tc_supported(d.feat_dtype, d.feat_dim)) {
         AC_CUDA(launch_search_tc(queries, d.feats, n, d.shard_count, d.feat_dim, d.shard_begin, keys,
-                                 db->ctx->sm_count, st));
+                                 db->ctx->aux_sms, st));
     } else {
         if (d.feat_dim > kSimtMaxLen)
             return fail(ATTNCACHE_ERR_SHAPE, "search: feat_dim %d of dtype %d takes the CUDA-core kernel, which holds "
@@ -412,9 +424,9 @@ attncache_status ac::apply_local_impl(attncache_db *db, const int64_t *idx, cons
     a.max_rows = n_rows;
     AC_CUDA(launch_select_apply(idx, hit, n_rows, d.shard_begin, d.shard_count, a.list, db->ctx->d_error, st));
     if (apply_tc_supported(d.map_dtype, act_dtype, d.seq_len, head_dim)) {
-        AC_CUDA(launch_apply_tc(a, sm_override("AC_APPLY_SMS", db->ctx->sm_count), st));
+        AC_CUDA(launch_apply_tc(a, sm_override("AC_APPLY_SMS", db->ctx->compute_sms), st));
     } else {
-        AC_CUDA(launch_apply_ffma(a, db->ctx->sm_count, st));
+        AC_CUDA(launch_apply_ffma(a, db->ctx->compute_sms, st));
     }
     return ATTNCACHE_OK;
 }
@@ -504,9 +516,9 @@ attncache_status attncache_attend_full_gqa(attncache_ctx *ctx, int64_t batch, in
     a.max_rows = batch;
     AC_CUDA(launch_select_attend(skip, batch, a.list, st));
     if (attend_tc_supported(act_dtype, S, dd)) {
-        AC_CUDA(launch_attend_tc(a, sm_override("AC_ATTEND_SMS", ctx->sm_count), st));
+        AC_CUDA(launch_attend_tc(a, sm_override("AC_ATTEND_SMS", ctx->compute_sms), st));
     } else {
-        AC_CUDA(launch_attend_ffma(a, ctx->sm_count, st));
+        AC_CUDA(launch_attend_ffma(a, ctx->compute_sms, st));
     }
     return ATTNCACHE_OK;
 }
@@ -556,7 +568,7 @@ attncache_status attncache_project_features(attncache_ctx *ctx, const void *h, i
     a.z = buf;
     a.y = (float *)((uint8_t *)buf + zb);
     a.f = features;
-    AC_CUDA(launch_project(a, ctx->sm_count, (cudaStream_t)stream));
+    AC_CUDA(launch_project(a, ctx->aux_sms, (cudaStream_t)stream));
     return ATTNCACHE_OK;
 }
 
@@ -581,7 +593,7 @@ attncache_status attncache_linear(attncache_ctx *ctx, const void *X, int64_t M, 
         ((int64_t)head_dim * es) % 16)
         return fail(ATTNCACHE_ERR_ALIGNMENT, "linear: bases or rows (K, head_dim elements) not 16-byte aligned");
     DeviceGuard g(ctx->device);
-    AC_CUDA(launch_linear_heads(dtype, X, M, K, W, N, bias, seq_len, head_dim, Y, ctx->sm_count, (cudaStream_t)stream));
+    AC_CUDA(launch_linear_heads(dtype, X, M, K, W, N, bias, seq_len, head_dim, Y, ctx->compute_sms, (cudaStream_t)stream));
     return ATTNCACHE_OK;
 }
 
@@ -656,9 +668,9 @@ attncache_status attncache_capture_maps_gqa(attncache_ctx *ctx, int64_t batch, i
     a.max_rows = batch;
     AC_CUDA(launch_select_attend(skip, batch, a.list, st));
     if (capture_tc_supported(act_dtype, S, dd)) {
-        AC_CUDA(launch_capture_tc(a, ctx->sm_count, st));
+        AC_CUDA(launch_capture_tc(a, ctx->compute_sms, st));
     } else {
-        AC_CUDA(launch_capture_simt(a, ctx->sm_count, st));
+        AC_CUDA(launch_capture_simt(a, ctx->compute_sms, st));
     }
     return ATTNCACHE_OK;
 }
@@ -759,7 +771,7 @@ static attncache_status copy_rows(const void *src, const int64_t *rows, int64_t 
     const bool ok16 = row_bytes % 16 == 0 && aligned16(src) && aligned16(dst);
     const bool ok8 = row_bytes % 8 == 0 && ((uintptr_t)src & 7) == 0 && ((uintptr_t)dst & 7) == 0;
     if (!ok16 && !ok8) return fail(ATTNCACHE_ERR_ALIGNMENT, "copy_rows: rows and bases must be 8-byte multiples/aligned");
-    AC_CUDA(launch_copy_rows(src, rows, n, row_bytes, dst, gather, ok16, (cudaStream_t)stream));
+    AC_CUDA(launch_copy_rows(src, rows, n, row_bytes, dst, gather, ok16, 148, (cudaStream_t)stream));  // no ctx: B200
     return ATTNCACHE_OK;
 }
 

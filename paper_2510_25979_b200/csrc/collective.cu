@@ -299,8 +299,8 @@ attncache_status apply_routed(attncache_db *db, const int64_t *idx, const uint8_
     // C4: V rows and their entry indices to the owners
     if (n_send) {
         const bool ok16 = row_v % 16 == 0 && aligned16(V) && aligned16(v_send);
-        AC_CUDA(launch_copy_rows(V, order, n_send, (int64_t)row_v, v_send, true, ok16, st));
-        AC_CUDA(launch_copy_rows(idx, order, n_send, 8, idx_send, true, false, st));
+        AC_CUDA(launch_copy_rows(V, order, n_send, (int64_t)row_v, v_send, true, ok16, ctx->aux_sms, st));
+        AC_CUDA(launch_copy_rows(idx, order, n_send, 8, idx_send, true, false, ctx->aux_sms, st));
     }
     if ((s = exchange_rows(ctx, v_send, sn.data(), so.data(), v_recv, rn.data(), ro.data(), row_v, st))) return s;
     if ((s = exchange_rows(ctx, idx_send, sn.data(), so.data(), idx_recv, rn.data(), ro.data(), 8, st))) return s;
@@ -314,7 +314,7 @@ attncache_status apply_routed(attncache_db *db, const int64_t *idx, const uint8_
     if ((s = exchange_rows(ctx, o_recv, rn.data(), ro.data(), o_back, sn.data(), so.data(), row_o, st))) return s;
     if (n_send) {
         const bool ok16 = row_o % 16 == 0 && aligned16(O) && aligned16(o_back);
-        AC_CUDA(launch_copy_rows(o_back, order, n_send, (int64_t)row_o, O, false, ok16, st));
+        AC_CUDA(launch_copy_rows(o_back, order, n_send, (int64_t)row_o, O, false, ok16, ctx->aux_sms, st));
     }
     return ATTNCACHE_OK;
 }
@@ -383,7 +383,7 @@ attncache_status attncache_relocate_rows(attncache_ctx *ctx, const void *src, in
     if (sn[me]) {
         uint8_t *d = (uint8_t *)dst + (size_t)row_bytes * ro[me];
         const bool ok16 = row_bytes % 16 == 0 && aligned16(src) && aligned16(d);
-        AC_CUDA(launch_copy_rows(src, send_order + so[me], sn[me], row_bytes, d, true, ok16 && ok8, st));
+        AC_CUDA(launch_copy_rows(src, send_order + so[me], sn[me], row_bytes, d, true, ok16 && ok8, ctx->aux_sms, st));
     }
     if (w == 1 || !ctx->comm) return ATTNCACHE_OK;
     const int64_t n_out = n_home - sn[me];
@@ -392,11 +392,11 @@ attncache_status attncache_relocate_rows(attncache_ctx *ctx, const void *src, in
     if (s) return s;
     // send buffer: the rows of ranks below me at [0, so[me]), above me at [so[me], n_out)
     const bool ok16 = row_bytes % 16 == 0 && aligned16(src) && aligned16(send);
-    if (so[me]) AC_CUDA(launch_copy_rows(src, send_order, so[me], row_bytes, send, true, ok16, st));
+    if (so[me]) AC_CUDA(launch_copy_rows(src, send_order, so[me], row_bytes, send, true, ok16, ctx->aux_sms, st));
     if (so[w] > so[me + 1])
         AC_CUDA(launch_copy_rows(src, send_order + so[me + 1], so[w] - so[me + 1], row_bytes,
                                  (uint8_t *)send + (size_t)row_bytes * so[me], true,
-                                 ok16 && ((size_t)row_bytes * so[me]) % 16 == 0, st));
+                                 ok16 && ((size_t)row_bytes * so[me]) % 16 == 0, ctx->aux_sms, st));
     std::vector<int64_t> sn2 = sn, so2(w, 0), rn2 = rn;
     for (int p = 0; p < w; ++p) so2[p] = p < me ? so[p] : so[p] - sn[me];
     sn2[me] = 0;

@@ -121,6 +121,7 @@ struct StreamScratch {
 struct attncache_ctx {
     int device = 0;
     int sm_count = 148;
+    int compute_sms = 148, aux_sms = 148;  // CTA caps (attncache_ctx_set_sm_budget); default sm_count
     int *d_error = nullptr;  // deferred device-side error flags (bit 0: NOT_FOUND)
     // collectives (one NCCL communicator per ctx; world == 1 and comm == nullptr for a local ctx)
     int rank = 0, world = 1;

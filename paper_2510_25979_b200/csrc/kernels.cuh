@@ -140,6 +140,6 @@ cudaError_t launch_route_plan(const int64_t *idx, const uint8_t *hit, int64_t n,
                               int32_t world, int32_t *owner, int32_t *counts, int64_t *order, cudaStream_t st);
 // ok16: row_bytes % 16 == 0 and both bases 16-byte aligned (int4 accesses); else 8-byte accesses.
 cudaError_t launch_copy_rows(const void *src, const int64_t *rows, int64_t n_rows, int64_t row_bytes, void *dst,
-                             bool gather, bool ok16, cudaStream_t st);
+                             bool gather, bool ok16, int sms, cudaStream_t st);  // sms: CTA budget (~16 per SM)
 
 }  // namespace ac

@@ -569,12 +569,12 @@ __global__ void copy_rows_kernel(const W *src, const int64_t *rows, int64_t n_ro
 }
 
 cudaError_t launch_copy_rows(const void *src, const int64_t *rows, int64_t n_rows, int64_t row_bytes, void *dst,
-                             bool gather, bool ok16, cudaStream_t st) {
+                             bool gather, bool ok16, int sms, cudaStream_t st) {
     if (n_rows == 0) return cudaSuccess;
     const int64_t words = ok16 ? row_bytes / 16 : row_bytes / 8;
-    // about 16 resident CTAs per SM in total: split between the rows and the words of a row
+    // about 16 resident CTAs per SM of the budget in total: split between the rows and the words of a row
     const int64_t gy = min64(n_rows, 65535);
-    const int64_t gx = max64(1, min64((words + 255) / 256, (148 * 16 + gy - 1) / gy));
+    const int64_t gx = max64(1, min64((words + 255) / 256, ((int64_t)sms * 16 + gy - 1) / gy));
     const dim3 grid((unsigned)gx, (unsigned)gy);
     if (ok16)  // 16-byte rows AND 16-byte aligned bases (an 8-byte aligned base takes the int2 path)
         copy_rows_kernel<int4><<<grid, 256, 0, st>>>((const int4 *)src, rows, n_rows, words, (int4 *)dst, gather);

@@ -588,6 +588,39 @@ def test_repeat_runs_are_bitwise_identical(ac, ctx):
                 assert all(torch.equal(a, b) for a, b in zip(ref, cur)), name
 
 
+def test_sm_budget_does_not_change_results(ac):
+    """attncache_ctx_set_sm_budget: every kernel's output is independent of its CTA count, so a
+    small budget (odd CTA counts, fewer CTAs than work items) must reproduce the default run bit for bit; the
+    setter rejects values outside [1, SM count]."""
+    c = ac.Context(0)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    for name, over in (("llama32_1b", dict(N=24, B=10, L=2)), ("llama3_8b", dict(N=24, B=10, L=2)),
+                       ("long_prefill", dict(N=4, B=3, L=1))):
+        cfg = synth.CONFIGS[name].with_(**over)
+        x = synth.features(cfg, 0, cfg.N, DEV)
+        maps = ac.attncache_pack_maps(synth.maps(cfg, 0, cfg.N, DEV))
+        db = ac.Database(c, x, maps, packed=True, seq_len=cfg.S)
+        q, _, _ = synth.queries(cfg, DEV)
+        Q, K, V = (synth.activations(cfg, k, 0, cfg.B, device=DEV) for k in "qkv")
+        idx0 = torch.arange(cfg.B, device=DEV) % cfg.N
+        out = []
+        for budget in (None, (7, 3), (1, 1)):
+            if budget is not None:
+                c.set_sm_budget(*budget)
+            s = ac.attncache_search(db, q, cfg.tau)
+            Oa = ac.attncache_apply_cached(db, idx0, V)
+            Of = ac.attncache_attend_full(c, Q, K, V)
+            cap = ac.attncache_capture_maps(c, Q[:1], K[:1])
+            out.append(tuple(t.clone() for t in (*s, Oa, Of, cap)))
+        c.set_sm_budget(sms, sms)
+        for o in out[1:]:
+            assert all(torch.equal(a, b) for a, b in zip(out[0], o)), name
+        del db
+    for bad in ((0, 10), (10, 0), (sms + 1, 10), (10, sms + 1)):
+        with pytest.raises(ac.AttnCacheError):
+            c.set_sm_budget(*bad)
+
+
 @pytest.mark.parametrize("cfg_name,B,n_sample", [("tiny", 2, None), ("llama32_1b", 2, 24), ("llama3_8b", 1, 12),
                                                  ("long_prefill", 1, 4)])
 @pytest.mark.parametrize("packed", [False, True])
