@@ -506,6 +506,32 @@ __device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const CUtensorMap 
         "l"((uint64_t)m), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+// TMA 2-D load into this CTA's shared memory whose completion is signalled on the mbarrier at the
+// shared::cluster address `bar` (the leader's).
+__device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap *m, uint32_t bar, int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];" ::"r"(dst),
+        "l"((uint64_t)m), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+// One K = 16 SS step of a pair MMA, issued by the calling thread (the caller elects it).
+__device__ __forceinline__ void umma2_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Single-thread form of umma2_commit_w.
+__device__ __forceinline__ void umma2_commit(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
 // Arrives on the barrier at this offset in both CTAs of the pair once the leader's prior MMAs complete.
 __device__ __forceinline__ void umma2_commit_w(uint64_t *bar) {
     asm volatile(
