@@ -33,6 +33,19 @@ namespace {
 #define CAP_KPOL 2
 #endif
 constexpr bool kCapDesc = CAP_DESC;
+
+#if defined(CAP_TRACE)  // timeline experiment (scripts/capture_trace.py): clock64 stamps of CTA 0, lane 0 of
+                        // warps 4-11, first 512 block-passes of each: top, S ok, S loaded, body done
+__device__ unsigned long long g_cap_trace[8][512][4];
+#define CAP_TR(slot)                                                                                  \
+    do {                                                                                              \
+        if (blockIdx.x == 0 && lane == 0 && blk < 512) g_cap_trace[warp - 4][blk][slot] = clock64();  \
+    } while (0)
+#else
+#define CAP_TR(slot) \
+    do {             \
+    } while (0)
+#endif
 constexpr int kCapKPol = CAP_KPOL;
 
 constexpr int kThreads = 384;  // 3 warpgroups: producers (warps 0-3), epilogue group 0 (4-7), group 1 (8-11)
@@ -229,7 +242,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t buf = blk & 1u, bph = (blk >> 1) & 1u;
                 const bool diag = j == qb;
                 const int lim = diag ? r : kBlk - 1;
+                CAP_TR(0);
                 mbar_wait(&s_full[g * 2 + buf], bph);
+                CAP_TR(1);
                 tc_fence_after();
                 const uint32_t s_addr = tmem + lane_addr + g * 256 + buf * kBlk;
                 // the whole S row of the block in registers (one TMEM round trip); masked keys -inf
@@ -237,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld_32x32b_x64(s_addr, sv);
                 tmem_ld_32x32b_x64(s_addr + 64, sv + 64);
                 tmem_ld_wait();
+                CAP_TR(2);
                 tc_fence_before();
                 mbar_arrive(&s_free[g * 2 + buf]);  // S is in registers: the buffer may be refilled
                 if (diag) {
@@ -296,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         store_chunk(mrow, j * kBlk, c, stored, w);
                     }
                 }
+                CAP_TR(3);
             }
             // dense maps: the columns right of this block's diagonal are exact zeros (reading R11)
             if (!packed && valid) {
@@ -364,3 +381,8 @@ cudaError_t launch_capture_tc(const CaptureArgs &a, int sm_count, cudaStream_t s
 }
 
 }  // namespace ac
+#if defined(CAP_TRACE)
+extern "C" int attncache_debug_cap_trace(void *out) {
+    return (int)cudaMemcpyFromSymbol(out, ac::g_cap_trace, sizeof(ac::g_cap_trace));
+}
+#endif
