@@ -49,6 +49,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
 }
+// try_wait with a suspend-time hint: the waiting warp is suspended (no issue slots spent spinning) until the
+// phase completes or `ns` nanoseconds pass.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, uint32_t parity, uint32_t ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_hint(uint64_t *bar, uint32_t parity, uint32_t ns = 1000000u) {
+    while (!mbar_try_wait_hint(bar, parity, ns)) {
+    }
+}
 
 // ---- cp.async (Ampere-style, 16 bytes, L1 bypass) -----------------------------------------------
 // src_bytes = 16 copies, 0 writes 16 zero bytes without reading global memory.

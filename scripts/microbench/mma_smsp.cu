@@ -19,7 +19,8 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 // mode 0: no MMAs; 1: whole warp, elected lane issues (umma_*_w); 2: lane 0 only issues; 3: whole warp but
-// each group waits for the previous group's commit before issuing (the queue never backs up)
+// each group waits for the previous group's commit before issuing (the queue never backs up); 4: as 3 with a
+// suspend-time hint on the wait (mbar_wait_hint)
 template <int mode>
 __global__ void bench(int iters, int exp_iters, int mma_warp, unsigned long long *out, float *sink) {
     extern __shared__ uint8_t smem_raw[];
@@ -44,6 +45,7 @@ __global__ void bench(int iters, int exp_iters, int mma_warp, unsigned long long
         long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
             if (mode == 3 && it > 0) mbar_wait(&bar, (it - 1) & 1);
+            if (mode == 4 && it > 0) mbar_wait_hint(&bar, (it - 1) & 1);
             for (int h = 0; h < 2; ++h) {
                 if (mode == 2)
 #pragma unroll
@@ -107,6 +109,7 @@ int main() {
     run<1>("whole warp, elected issue (blocking)", 1, iters * 4, exp_iters, d, sink);
     run<2>("lane 0 only issues (blocking)", 1, iters * 4, exp_iters, d, sink);
     run<3>("whole warp, waits for previous group", 1, iters * 4, exp_iters, d, sink);
+    run<4>("whole warp, hinted wait for previous group", 1, iters * 4, exp_iters, d, sink);
     run<1>("whole warp, elected issue, on warp 2", 2, iters * 4, exp_iters, d, sink);
     return 0;
 }
