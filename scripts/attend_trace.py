@@ -78,6 +78,9 @@ if SPLIT:
     print(f"softmax warp 4: mean cycles wait_S {d[sel, 0].mean():.0f}  load+exchange {d[sel, 1].mean():.0f}  "
           f"exp+store {d[sel, 2].mean():.0f}  arrive(+epilogue) {d[sel, 3].mean():.0f}  gap {gap[sel].mean():.0f}  "
           f"period {per[sel].mean():.0f}")
+    g_sel = gap[sel]
+    print("gap histogram (cycles):", np.histogram(g_sel, bins=[0, 50, 100, 150, 200, 300, 400, 600, 1000, 10**6])[0].tolist(),
+          "bins 0/50/100/150/200/300/400/600/1000/inf")
     big = np.argsort(-gap[sel])[:6] + 20
     print("largest gaps (block, gap, next wait_S):", [(int(i), int(gap[i]), int(d[i + 1, 0])) for i in big])
     dm = np.diff(m[:, :5], axis=1)
