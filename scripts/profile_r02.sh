@@ -16,10 +16,10 @@ for b in 1024 8192; do
   ncu --set full --clock-control none --import-source on -k "regex:search_tc" -s 2 -c 1 -o gpurun_out/${P}_search_$b \
       python scripts/search_bench.py $b 1 > gpurun_out/ncu_search_$b.log 2>&1; echo search_$b=$?
 done
-ncu --set full --clock-control none --import-source on -k "regex:apply_tc|attend_tc|attend_split|search_tc" -s 8 -c 6 \
+ncu --set full --clock-control none --import-source on -k "regex:apply_tc|apply_pair|attend_tc|attend_split|search_tc" -s 8 -c 6 \
     -o gpurun_out/${P}_full_c1 $B > gpurun_out/ncu_full_c1.log 2>&1; echo full_c1=$?
 python scripts/apply_bench.py llama3_8b 115 128 1 > /dev/null 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:apply_tc" -s 3 -c 1 -o gpurun_out/${P}_apply_llama3_8b \
+ncu --set full --clock-control none --import-source on -k "regex:apply_tc|apply_pair" -s 3 -c 1 -o gpurun_out/${P}_apply_llama3_8b \
     python scripts/apply_bench.py llama3_8b 115 128 1 > gpurun_out/ncu_apply_c2.log 2>&1; echo apply_c2=$?
 for c in "long_prefill 16" "llama3_8b 13"; do
   set -- $c
