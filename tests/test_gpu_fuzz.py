@@ -1,0 +1,85 @@
+"""Seeded randomized parity: random shapes across the ranges the C ABI accepts -- sequence lengths
+with and without a partial last 128-row block, head dims on the tensor-core (64, 128) and CUDA-core paths, bf16
+and fp16, grouped-query heads, PACKED and DENSE maps -- for the miss attention (Alg. 2 l.376-381), the capture
+(Fig. 4 step 1) and A.V with the captured maps as the database (Alg. 2 l.373-375), each against the fp64 oracle on
+sampled units within the stated tolerances."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from tests._util import DT_NAME, check_close, storage
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def ac():
+    import paper_2510_25979_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(ac):
+    return ac.Context(0)
+
+
+def _expand(t, H):
+    """[B][L][Hkv][S][d] -> [B][L][H][S][d] (query head h reads K/V head h // (H // Hkv))."""
+    return t.repeat_interleave(H // t.shape[2], dim=2).contiguous()
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_random_shapes_attend_capture_apply(ac, ctx, seed):
+    rng = np.random.default_rng(7000 + seed)
+    S = int(rng.choice([1, 5, 8, 40, 64, 96, 127, 128, 136, 200, 256, 264, 384, 520]))
+    d = int(rng.choice([64, 128, 64, 128, 32, 80]))
+    dt = torch.bfloat16 if rng.random() < 0.7 else torch.float16
+    name = DT_NAME[dt]
+    L, H = int(rng.integers(1, 3)), int(rng.choice([1, 2, 4]))
+    Hkv = int(rng.choice([h for h in (1, 2, 4) if H % h == 0]))
+    B, N = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+    packed = bool(rng.random() < 0.5)
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    rnd = lambda *shape: torch.randn(*shape, device=DEV, generator=g).to(dt)  # noqa: E731
+    what = f"S={S} d={d} {name} L={L} H={H} Hkv={Hkv} B={B} packed={packed}"
+    units = [(b, l, h) for b in range(B) for l in range(L) for h in range(H)]
+    pick = [units[i] for i in sorted(rng.choice(len(units), min(len(units), 6), replace=False))]
+    off = [(((b * L + l) * H + h) * S * d) for b, l, h in pick]
+
+    # miss attention (GQA through the expanded K/V on the oracle side)
+    Q, K, V = rnd(B, L, H, S, d), rnd(B, L, Hkv, S, d), rnd(B, L, Hkv, S, d)
+    O = ac.attncache_attend_full(ctx, Q, K, V)
+    torch.cuda.synchronize()
+    ref = oracle.attend(storage(Q), storage(_expand(K, H)), storage(_expand(V, H)), name, off, S, d)
+    check_close(torch.stack([O[b, l, h] for b, l, h in pick]), ref, dt, "attend " + what)
+
+    if S % 8:  # capture / 16-byte map rows need S % 8 == 0 (include/attncache.h: ERR_SHAPE)
+        with pytest.raises(ac.AttnCacheError):
+            ac.attncache_capture_maps(ctx, Q, K, map_dtype=dt, packed=packed)
+        return
+    # capture N entries, then A.V with them as the database
+    Qm, Km = rnd(N, L, H, S, d), rnd(N, L, Hkv, S, d)
+    maps = ac.attncache_capture_maps(ctx, Qm, Km, map_dtype=dt, packed=packed)
+    x = torch.randn(N, 1024, device=DEV, generator=g)
+    x = (x / x.norm(dim=1, keepdim=True)).to(torch.bfloat16)
+    db = ac.Database(ctx, x, maps, packed=packed, seq_len=S)
+    dense = torch.stack([ac.attncache_fetch_maps(db, e) for e in range(N)])  # [N][L][H][S][S]
+    m_units = [(e, l, h) for e in range(N) for l in range(L) for h in range(H)]
+    m_pick = [m_units[i] for i in sorted(rng.choice(len(m_units), min(len(m_units), 6), replace=False))]
+    m_off = [(((e * L + l) * H + h) * S * d) for e, l, h in m_pick]
+    P = oracle.attention_map(storage(Qm), storage(_expand(Km, H)), name, m_off, S, d)
+    got = torch.stack([dense[e, l, h] for e, l, h in m_pick]).double().cpu().numpy()
+    iu = np.triu_indices(S, 1)
+    assert np.all(got[:, iu[0], iu[1]] == 0.0), "capture: non-zero above the diagonal " + what
+    assert np.max(np.abs(got - P)) <= 4e-3, f"capture {what}: max-abs {np.max(np.abs(got - P))}"
+    idx = torch.as_tensor(rng.integers(0, N, B), device=DEV)
+    Vh = rnd(B, L, Hkv, S, d)
+    Oa = ac.attncache_apply_cached(db, idx, Vh)
+    torch.cuda.synchronize()
+    ents = idx.cpu().numpy()
+    a_off = [(((int(ents[b]) * L + l) * H + h) * S * S) for b, l, h in pick]
+    v_off = [(((b * L + l) * Hkv + h // (H // Hkv)) * S * d) for b, l, h in pick]
+    ref = oracle.apply(storage(dense), name, a_off, storage(Vh), name, v_off, S, d)
+    check_close(torch.stack([Oa[b, l, h] for b, l, h in pick]), ref, dt, "apply " + what)
