@@ -83,3 +83,34 @@ def test_random_shapes_attend_capture_apply(ac, ctx, seed):
     v_off = [(((b * L + l) * Hkv + h // (H // Hkv)) * S * d) for b, l, h in pick]
     ref = oracle.apply(storage(dense), name, a_off, storage(Vh), name, v_off, S, d)
     check_close(torch.stack([Oa[b, l, h] for b, l, h in pick]), ref, dt, "apply " + what)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_shapes_search(ac, ctx, seed):
+    """Alg. 1 l.255-257 over random DB sizes, batch sizes, feature dims (multiples of 64: tcgen05; others and fp32:
+    CUDA cores) and thresholds, with planted exact matches and near-duplicates: the A5 exactness rule against the
+    brute-force oracle (tests/_util.check_search)."""
+    from tests._util import check_search
+    rng = np.random.default_rng(9000 + seed)
+    N = int(rng.choice([1, 2, 63, 64, 65, 200, 257, 1000, 3000]))
+    B = int(rng.choice([1, 3, 64, 127, 128, 129, 300]))
+    D = int(rng.choice([64, 128, 192, 1024, 96, 104, 40, 100, 30]))
+    dt = torch.bfloat16 if rng.random() < 0.7 else torch.float32
+    tau = float(rng.choice([0.0, 0.5, 0.9, 0.99, 1.0]))
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    x = torch.randn(N, D, device=DEV, generator=g)
+    x = (x / x.norm(dim=1, keepdim=True)).to(dt)
+    q = torch.randn(B, D, device=DEV, generator=g)
+    q = (q / q.norm(dim=1, keepdim=True)).to(dt)
+    planted = rng.choice(B, min(B, max(1, B // 3)), replace=False)
+    q[torch.as_tensor(planted, device=DEV)] = x[torch.as_tensor(rng.integers(0, N, len(planted)), device=DEV)]
+    if N > 1:  # an exact duplicate entry: the tie must go to the lower index
+        x[N - 1] = x[0]
+    if (D * x.element_size()) % 16:  # feature rows must be 16-byte multiples (include/attncache.h: ERR_ALIGNMENT)
+        with pytest.raises(ac.AttnCacheError):
+            ac.Database(ctx, x)
+        return
+    db = ac.Database(ctx, x)
+    idx, score, hit = ac.attncache_search(db, q, tau)
+    torch.cuda.synchronize()
+    check_search(q, x, idx, score, hit, tau)
