@@ -2,7 +2,8 @@
 with and without a partial last 128-row block, head dims on the tensor-core (64, 128) and CUDA-core paths, bf16
 and fp16, grouped-query heads, PACKED and DENSE maps -- for the miss attention (Alg. 2 l.376-381), the capture
 (Fig. 4 step 1) and A.V with the captured maps as the database (Alg. 2 l.373-375), each against the fp64 oracle on
-sampled units within the stated tolerances."""
+sampled units within the stated tolerances; the search (Alg. 1 l.255-257) under the A5 exactness
+rule; the f4 projections, RoPE and the f2 feature projector."""
 import numpy as np
 import pytest
 import torch
@@ -114,3 +115,46 @@ def test_random_shapes_search(ac, ctx, seed):
     idx, score, hit = ac.attncache_search(db, q, tau)
     torch.cuda.synchronize()
     check_search(q, x, idx, score, hit, tau)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_shapes_linear_rope_project(ac, ctx, seed):
+    """f4 projections (attncache_linear, head-major output), RoPE and the f2 feature projector over random
+    shapes on both the tcgen05 and the CUDA-core paths, against oracle.linear / oracle.rope / oracle.project."""
+    import math
+    rng = np.random.default_rng(11000 + seed)
+    dt = torch.bfloat16 if rng.random() < 0.7 else torch.float16
+    name = DT_NAME[dt]
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    # linear: X [B][S][K] x W [N][K] -> [B][1][H][S][d]
+    S = int(rng.choice([8, 40, 96, 128, 200, 256]))
+    B = int(rng.integers(1, 4))
+    K = int(rng.choice([64, 128, 256, 200, 72]))
+    d = int(rng.choice([32, 64, 128, 48]))
+    H = int(rng.choice([1, 2, 3]))
+    X = torch.randn(B, S, K, device=DEV, generator=g).to(dt)
+    W = (torch.randn(H * d, K, device=DEV, generator=g) / math.sqrt(K)).to(dt)
+    Y = ac.attncache_linear(ctx, X, W, H)
+    torch.cuda.synchronize()
+    ref = oracle.linear(storage(X.view(B * S, K)), storage(W), name).reshape(B, S, H, d).transpose(0, 2, 1, 3)
+    check_close(Y.view(B, H, S, d).reshape(-1, S, d), ref.reshape(-1, S, d), dt, f"linear B={B} S={S} K={K} H={H} d={d}")
+    # RoPE on the projected heads (in place), in the 16-bit dtype: angles p * theta in fp32 (reading R29)
+    de = d - d % 2
+    R = torch.randn(B, H, S, de, device=DEV, generator=g).to(dt)
+    ref_r = oracle.rope(storage(R), name, S, de, base=10000.0)
+    got = ac.attncache_rope(R.clone(), 10000.0)
+    torch.cuda.synchronize()
+    assert np.abs(got.double().cpu().numpy().reshape(ref_r.shape) - ref_r).max() <= (2e-2 if dt == torch.bfloat16 else 4e-3)
+    # feature projector: f = normalize(W2 relu(W1 h + b1) + b2)
+    n, E, Hd, D = int(rng.choice([1, 5, 128, 130])), int(rng.choice([64, 256, 96])), int(rng.choice([64, 128, 192])), \
+        int(rng.choice([64, 128, 1024]))
+    h = torch.randn(n, E, device=DEV, generator=g).to(torch.bfloat16)
+    W1 = (torch.randn(Hd, E, device=DEV, generator=g) / math.sqrt(E)).to(torch.bfloat16)
+    W2 = (torch.randn(D, Hd, device=DEV, generator=g) / math.sqrt(Hd)).to(torch.bfloat16)
+    b1 = torch.randn(Hd, device=DEV, generator=g) * 0.1
+    b2 = torch.randn(D, device=DEV, generator=g) * 0.1
+    f = ac.attncache_project_features(ctx, h, W1, b1, W2, b2)
+    torch.cuda.synchronize()
+    ref_f = oracle.project(storage(h), "bf16", storage(W1), b1.cpu().numpy(), storage(W2), b2.cpu().numpy())
+    # one "unit" per row: max-abs over all elements and rel-L2 per row (the north_star bf16 bounds)
+    check_close(f.unsqueeze(1), ref_f[:, None, :], f.dtype, f"project n={n} E={E} Hd={Hd} D={D}")
