@@ -33,6 +33,9 @@ namespace {
 #define CAP_KPOL 2
 #endif
 constexpr bool kCapDesc = CAP_DESC;
+#ifndef CAP_STG256
+#define CAP_STG256 1
+#endif
 
 #if defined(CAP_TRACE)  // timeline experiment (scripts/capture_trace.py): clock64 stamps of CTA 0, lane 0 of
                         // warps 4-11, first 512 block-passes of each: top, S ok, S loaded, body done
@@ -302,6 +305,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 } else {
+#if CAP_STG256
+                    // pass-1 blocks are whole (j < qb: all 128 columns lie inside row R's stored length): P of the
+                    // block packed in place, then 32-byte stores, so each store request carries a full sector --
+                    // the 16-byte stores made the L1 -> L2 request rate the bound (configs[3] capture 1.21 ms
+                    // with no map stores at all against 2.19 ms with them).  Packed rows start on 16-byte
+                    // boundaries: a row whose block segment is not 32-byte aligned writes 16 + 7 x 32 + 16 bytes.
+#pragma unroll
+                    for (int e = 0; e < kBlk / 2; ++e)
+                        sv[e] = pack(ex2(fmaf(__uint_as_float(sv[2 * e]), sl2, -off)),
+                                     ex2(fmaf(__uint_as_float(sv[2 * e + 1]), sl2, -off)));
+                    if (valid) {
+                        uint16_t *seg = mrow + j * kBlk;
+                        if ((reinterpret_cast<uintptr_t>(seg) & 31u) == 0) {
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                if constexpr (kStreamOut) st_global_v8_hint(seg + 16 * k, &sv[8 * k], pol_out);
+                                else st_global_v8(seg + 16 * k, *reinterpret_cast<const uint32_t(*)[8]>(&sv[8 * k]));
+                            }
+                        } else {
+                            const uint4 head = make_uint4(sv[0], sv[1], sv[2], sv[3]);
+                            const uint4 tail = make_uint4(sv[60], sv[61], sv[62], sv[63]);
+                            if constexpr (kStreamOut) st_global_16_hint(seg, head, pol_out);
+                            else *reinterpret_cast<uint4 *>(seg) = head;
+#pragma unroll
+                            for (int k = 0; k < 7; ++k) {
+                                if constexpr (kStreamOut) st_global_v8_hint(seg + 8 + 16 * k, &sv[4 + 8 * k], pol_out);
+                                else st_global_v8(seg + 8 + 16 * k, *reinterpret_cast<const uint32_t(*)[8]>(&sv[4 + 8 * k]));
+                            }
+                            if constexpr (kStreamOut) st_global_16_hint(seg + 120, tail, pol_out);
+                            else *reinterpret_cast<uint4 *>(seg + 120) = tail;
+                        }
+                    }
+#else
 #pragma unroll
                     for (int c = 0; c < kBlk / 32; ++c) {
                         uint32_t w[16];
@@ -311,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         ex2(fmaf(__uint_as_float(sv[c * 32 + 2 * e + 1]), sl2, -off)));
                         store_chunk(mrow, j * kBlk, c, stored, w);
                     }
+#endif
                 }
                 CAP_TR(3);
             }

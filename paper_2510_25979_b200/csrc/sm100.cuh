@@ -104,6 +104,13 @@ __device__ __forceinline__ void st_global_v8(void *p, const uint32_t (&w)[8]) {
                  : "memory");
 }
 
+// 32-byte global store with an L2 cache policy.
+__device__ __forceinline__ void st_global_v8_hint(void *p, const uint32_t *w, uint64_t policy) {
+    asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "r"(w[0]),
+                 "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "l"(policy)
+                 : "memory");
+}
+
 // Bulk prefetch of a contiguous global range into L2 (no shared memory; bytes % 16 == 0).
 __device__ __forceinline__ void prefetch_l2_bulk(const void *src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
