@@ -33,9 +33,6 @@ namespace {
 #define CAP_KPOL 2
 #endif
 constexpr bool kCapDesc = CAP_DESC;
-#ifndef CAP_STG256
-#define CAP_STG256 1
-#endif
 
 #if defined(CAP_TRACE)  // timeline experiment (scripts/capture_trace.py): clock64 stamps of CTA 0, lane 0 of
                         // warps 4-11, first 512 block-passes of each: top, S ok, S loaded, body done
@@ -200,24 +197,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool bf16 = a.map_dt == ATTNCACHE_BF16;
         const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
         uint32_t blk = 0;
-        // writes 32 P values (16 packed pairs) of this thread's row at column c0 + 32c, clipped to the stored length
-        auto store_chunk = [&](uint16_t *mrow, int c0, int c, int stored, const uint32_t (&w)[16]) {
-            const int ncols = min(kBlk, stored - c0);
-            uint4 *dst = (uint4 *)(mrow + c0 + c * 32);
-#if defined(CAP_EXP) && CAP_EXP == 1  // experiment: no map stores
-            if (w[0] == 0x12345678u && w[15] == 0x9abcdef0u) dst[0] = make_uint4(w[1], w[2], w[3], w[4]);
-#else
-#pragma unroll
-            for (int pc = 0; pc < 4; ++pc)
-                if (c * 32 + pc * 8 < ncols) {
-                    const uint4 v = make_uint4(w[4 * pc], w[4 * pc + 1], w[4 * pc + 2], w[4 * pc + 3]);
-                    if constexpr (kStreamOut)
-                        st_global_16_hint(dst + pc, v, pol_out);
-                    else
-                        dst[pc] = v;
-                }
-#endif
-        };
         auto pack = [&](float p0, float p1) -> uint32_t {
             if (bf16) {
                 __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
@@ -225,6 +204,41 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __half2 h2 = __floats2half2_rn(p0, p1);
             return *reinterpret_cast<uint32_t *>(&h2);
+        };
+        // Stores the first n (a multiple of 8) of the 128 packed P values w[0..63] (two per word) of one row's block
+        // segment `seg` (16-byte aligned) with 32-byte stores: each store request then carries a whole sector (the
+        // 16-byte form made the L1 -> L2 request rate the bound of the store-heavy blocks).  A segment that is not
+        // 32-byte aligned starts with one 16-byte store.  All indices into w are compile-time.
+        auto st16 = [&](uint16_t *p, const uint32_t *w4) {
+            const uint4 v = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            if constexpr (kStreamOut) st_global_16_hint(p, v, pol_out);
+            else *reinterpret_cast<uint4 *>(p) = v;
+        };
+        auto st32 = [&](uint16_t *p, const uint32_t *w8) {
+            if constexpr (kStreamOut) st_global_v8_hint(p, w8, pol_out);
+            else st_global_v8(p, *reinterpret_cast<const uint32_t(*)[8]>(w8));
+        };
+        auto store_seg = [&](uint16_t *seg, const uint32_t (&w)[kBlk], int n) {
+#if defined(CAP_EXP) && CAP_EXP == 1  // experiment: no map stores (the values stay live through this test)
+            if (w[0] == 0x12345678u && w[kBlk / 2 - 1] == 0x9abcdef0u) st16(seg, &w[0]);
+            return;
+#endif
+            if ((reinterpret_cast<uintptr_t>(seg) & 31u) == 0) {
+#pragma unroll
+                for (int k = 0; k < kBlk / 16; ++k) {
+                    if (16 * k + 16 <= n) st32(seg + 16 * k, &w[8 * k]);
+                    else if (16 * k + 8 <= n) st16(seg + 16 * k, &w[8 * k]);
+                }
+            } else {
+                if (n >= 8) st16(seg, &w[0]);
+#pragma unroll
+                for (int k = 0; k < kBlk / 16 - 1; ++k) {
+                    const int e0 = 8 + 16 * k;
+                    if (e0 + 16 <= n) st32(seg + e0, &w[4 + 8 * k]);
+                    else if (e0 + 8 <= n) st16(seg + e0, &w[4 + 8 * k]);
+                }
+                if (n >= kBlk) st16(seg + kBlk - 8, &w[kBlk / 2 - 4]);
+            }
         };
         for (uint32_t t = blockIdx.x + g * gridDim.x; t < items; t += stride) {
             AC_STRESS_DELAY(312u);
@@ -296,58 +310,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         off = m + lg2(l);  // pass 1: P = exp2(s * sl2 - off)
                         const float inv = 1.f / l;
 #pragma unroll
-                        for (int c = 0; c < kBlk / 32; ++c) {
-                            uint32_t w[16];
-#pragma unroll
-                            for (int e = 0; e < 16; ++e)
-                                w[e] = pack(__uint_as_float(sv[c * 32 + 2 * e]) * inv, __uint_as_float(sv[c * 32 + 2 * e + 1]) * inv);
-                            store_chunk(mrow, qb * kBlk, c, stored, w);
-                        }
+                        for (int e = 0; e < kBlk / 2; ++e)
+                            sv[e] = pack(__uint_as_float(sv[2 * e]) * inv, __uint_as_float(sv[2 * e + 1]) * inv);
+                        store_seg(mrow + qb * kBlk, sv, min(kBlk, stored - qb * kBlk));  // stored = 0: no stores
                     }
                 } else {
-#if CAP_STG256
-                    // pass-1 blocks are whole (j < qb: all 128 columns lie inside row R's stored length): P of the
-                    // block packed in place, then 32-byte stores, so each store request carries a full sector --
-                    // the 16-byte stores made the L1 -> L2 request rate the bound (configs[3] capture 1.21 ms
-                    // with no map stores at all against 2.19 ms with them).  Packed rows start on 16-byte
-                    // boundaries: a row whose block segment is not 32-byte aligned writes 16 + 7 x 32 + 16 bytes.
+                    // pass-1 blocks are whole (j < qb: all 128 columns lie inside row R's stored length)
 #pragma unroll
                     for (int e = 0; e < kBlk / 2; ++e)
                         sv[e] = pack(ex2(fmaf(__uint_as_float(sv[2 * e]), sl2, -off)),
                                      ex2(fmaf(__uint_as_float(sv[2 * e + 1]), sl2, -off)));
-                    if (valid) {
-                        uint16_t *seg = mrow + j * kBlk;
-                        if ((reinterpret_cast<uintptr_t>(seg) & 31u) == 0) {
-#pragma unroll
-                            for (int k = 0; k < 8; ++k) {
-                                if constexpr (kStreamOut) st_global_v8_hint(seg + 16 * k, &sv[8 * k], pol_out);
-                                else st_global_v8(seg + 16 * k, *reinterpret_cast<const uint32_t(*)[8]>(&sv[8 * k]));
-                            }
-                        } else {
-                            const uint4 head = make_uint4(sv[0], sv[1], sv[2], sv[3]);
-                            const uint4 tail = make_uint4(sv[60], sv[61], sv[62], sv[63]);
-                            if constexpr (kStreamOut) st_global_16_hint(seg, head, pol_out);
-                            else *reinterpret_cast<uint4 *>(seg) = head;
-#pragma unroll
-                            for (int k = 0; k < 7; ++k) {
-                                if constexpr (kStreamOut) st_global_v8_hint(seg + 8 + 16 * k, &sv[4 + 8 * k], pol_out);
-                                else st_global_v8(seg + 8 + 16 * k, *reinterpret_cast<const uint32_t(*)[8]>(&sv[4 + 8 * k]));
-                            }
-                            if constexpr (kStreamOut) st_global_16_hint(seg + 120, tail, pol_out);
-                            else *reinterpret_cast<uint4 *>(seg + 120) = tail;
-                        }
-                    }
-#else
-#pragma unroll
-                    for (int c = 0; c < kBlk / 32; ++c) {
-                        uint32_t w[16];
-#pragma unroll
-                        for (int e = 0; e < 16; ++e)
-                            w[e] = pack(ex2(fmaf(__uint_as_float(sv[c * 32 + 2 * e]), sl2, -off)),
-                                        ex2(fmaf(__uint_as_float(sv[c * 32 + 2 * e + 1]), sl2, -off)));
-                        store_chunk(mrow, j * kBlk, c, stored, w);
-                    }
-#endif
+                    if (valid) store_seg(mrow + j * kBlk, sv, kBlk);
                 }
                 CAP_TR(3);
             }
