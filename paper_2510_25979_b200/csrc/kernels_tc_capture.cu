@@ -366,10 +366,14 @@ cudaError_t launch(const CaptureArgs &a, int sm_count, cudaStream_t st) {
     const ItemSched sc = ItemSched::make_wave((uint32_t)a.S, (uint32_t)a.L, (uint32_t)a.H, (uint32_t)a.Hkv, kBlk,
                                               2u * (uint32_t)sm_count);
 #endif
-    // map stores with an L2 evict_first policy from S = 512 on: there a unit's K (re-read by all its query
-    // blocks, in both passes) stays in L2 for long, and the streamed maps would push it out (configs[3]:
-    // 2.44 -> 2.19 ms); at S <= 256 the plain store is faster (configs 1 / 2: 0.275 -> 0.250, 0.584 -> 0.551 ms)
-    if (a.S >= 512)
+    // map stores with an L2 evict_first policy from S = CAP_STREAM_MIN_S on.  With 16-byte stores the hint paid
+    // at S = 1024 (configs[3]: 2.44 -> 2.19 ms: the streamed maps no longer pushed a unit's K out of L2); with the
+    // 32-byte stores the plain store is as fast or faster at every config (configs 1 / 2 / 3: 0.277 / 0.523 /
+    // 1.922 ms plain against 0.292 / 0.539 / 1.941 hinted), so the hint is off by default.
+#ifndef CAP_STREAM_MIN_S
+#define CAP_STREAM_MIN_S (1 << 30)
+#endif
+    if (a.S >= CAP_STREAM_MIN_S)
         capture_tc_kernel<kD, true><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, a, sc, idesc);
     else
         capture_tc_kernel<kD, false><<<sm_count, kThreads, C::kSmem, st>>>(tq, tk, a, sc, idesc);
