@@ -38,6 +38,9 @@ PAPER_CONTEXT = ("paper (PAPER.md:51, :446, :568; Table 3): 3x attention / 1.6x 
                  "A100 80GB, Llama-3-3B fp32, MMLU-STEM; 2x / 1.2x on 2x Xeon Silver 4410Y")
 
 
+_RDEV = None  # device of the torch.distributed reduction tensors (the GPU on NCCL, the CPU on gloo)
+
+
 def _env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -661,15 +664,15 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
     end.record(comp)
     torch.cuda.synchronize()
     dist.barrier()
-    ms = torch.tensor([start.elapsed_time(end) / args.steps], device=dev)
+    ms = torch.tensor([start.elapsed_time(end) / args.steps], device=_RDEV)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)  # the step time is the slowest rank's
-    launches = torch.tensor([ac.attncache_launch_count() - launches0], device=dev)
+    launches = torch.tensor([ac.attncache_launch_count() - launches0], device=_RDEV)
     dist.all_reduce(launches)
     extra = {}
     if placement == "affinity":
         assert torch.equal(step.local_queries(res), loc), "placement changed between steps"
         n_hit = int(res["hit"].sum().item())
-        per_rank = torch.tensor([loc.numel()], device=dev)
+        per_rank = torch.tensor([loc.numel()], device=_RDEV)
         gathered = [torch.empty_like(per_rank) for _ in range(world)]
         dist.all_gather(gathered, per_rank)
         extra = {"sm_budget": {"compute_sms": budget[0], "aux_sms": budget[1]},
@@ -680,7 +683,7 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
                                "(attncache_relocate_rows, communication stream) overlap this batch's local A.V / "
                                "attention; all complete inside the step"}
     else:
-        t = torch.tensor([int(res[2].sum().item())], device=dev)
+        t = torch.tensor([int(res[2].sum().item())], device=_RDEV)
         dist.all_reduce(t)
         n_hit = int(t.item())
     del Q, K, V, O
@@ -710,9 +713,20 @@ def run_dist(args, cfg):
             os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]), RANK="0",
                               WORLD_SIZE="1", LOCAL_RANK="0")
     rank, world, local = _env_rank()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    global _RDEV
+    if os.environ.get("ATTNCACHE_TEST_SINGLE_DEVICE") == "1":
+        # functional test of the N > 1 path on one GPU (tests/test_gpu_fake_nccl.py): every rank on GPU 0, the
+        # library's NCCL calls in tests/native/fake_nccl.cpp, torch.distributed on gloo; its times mean nothing
+        local = 0
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+        dist.init_process_group("gloo")
+        _RDEV = torch.device("cpu")
+    else:
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+        dist.init_process_group("nccl", device_id=dev)
+        _RDEV = dev
     ctx = ac.Context.from_process_group(local)  # the library's own NCCL communicator
     begin, count = shard_range(cfg.N, world, rank)
     x = synth.features(cfg, begin, count, dev)

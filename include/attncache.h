@@ -87,7 +87,7 @@ uint64_t attncache_launch_count(void);
 
 /* A 128-byte NCCL unique id (ncclGetUniqueId) for attncache_ctx_create: rank 0 creates it and the caller
  * broadcasts it to the other ranks by any means (torch.distributed, a file, MPI).  NCCL is loaded with
- * dlopen (the copy already in the process, else $ATTNCACHE_NCCL_LIB, else libnccl.so.2).
+ * dlopen ($ATTNCACHE_NCCL_LIB when set, else the copy already in the process, else libnccl.so.2).
  * Errors: NCCL (library not found or call failed), INVALID_ARGUMENT (out NULL). */
 attncache_status attncache_get_unique_id(uint8_t out[128]);
 

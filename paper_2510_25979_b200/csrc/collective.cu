@@ -4,8 +4,8 @@
 // query's home GPU by NCCL send/recv").
 //
 // NCCL is reached through dlopen (the library keeps no link-time dependency on libnccl or libcuda, so it
-// loads on a GPU-less host): the copy already in the process (e.g. the one torch loaded) is reused when
-// there is one, else ATTNCACHE_NCCL_LIB, else libnccl.so.2 from the loader path.  Every collective is
+// loads on a GPU-less host): ATTNCACHE_NCCL_LIB when set, else the copy already in the process (e.g. the one
+// torch loaded), else libnccl.so.2 from the loader path.  Every collective is
 // enqueued on the caller's stream; the only host round trips are the documented ones (count exchanges).
 #include <dlfcn.h>
 #include <stdio.h>
@@ -42,11 +42,10 @@ NcclApi g_nccl;
 std::once_flag g_nccl_once;
 
 void load_nccl() {
-    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the copy torch (or another user) loaded
-    if (!h) {
-        const char *env = getenv("ATTNCACHE_NCCL_LIB");
-        if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
-    }
+    void *h = nullptr;
+    const char *env = getenv("ATTNCACHE_NCCL_LIB");  // an explicit choice wins (e.g. the tests' fake_nccl)
+    if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the copy torch (or another user) loaded
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!h) {
         snprintf(g_nccl.why, sizeof g_nccl.why, "dlopen(libnccl.so.2) failed: %s", dlerror());

@@ -1,0 +1,215 @@
+// fake_nccl.cpp — TEST INFRASTRUCTURE: a functional stand-in for the NCCL calls libattncache uses, so that the
+// library's collective code (csrc/collective.cu: count exchanges, query all-gather, key max-all-reduce, grouped
+// send/recv of routed rows and relocated request state) runs at world 2-4 with every rank on ONE GPU
+// (tests/test_gpu_fake_nccl.py; real NCCL refuses two ranks on one device).  It is not a performance stand-in:
+// every call synchronises the caller's stream and moves the bytes through a host file mapping shared by the
+// ranks, between host barriers, so no rank's kernels ever wait on another rank's kernels.
+// Loaded by the library through ATTNCACHE_NCCL_LIB.  Build: g++ -shared -fPIC -O2 fake_nccl.cpp -lcudart.
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <ctime>
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <unistd.h>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+namespace {
+
+struct Header {
+    std::atomic<int> arrive;
+    std::atomic<int> gen;
+    uint64_t max_bytes[16];  // per rank: its largest message of the current group (P2P chunking rounds)
+};
+
+struct FakeComm {
+    int rank = 0, world = 1;
+    size_t slot = 0;  // bytes per rank slot (all-gather / all-reduce) and per (src, dst) mailbox
+    uint8_t *base = nullptr;
+    size_t bytes = 0;
+    char path[160] = "";
+    Header *hdr() const { return reinterpret_cast<Header *>(base); }
+    uint8_t *slot_of(int r) const { return base + 256 + (size_t)r * slot; }
+    uint8_t *box(int src, int dst) const { return base + 256 + (size_t)world * slot + ((size_t)src * world + dst) * slot; }
+};
+
+void barrier(FakeComm *c) {
+    Header *h = c->hdr();
+    const int g = h->gen.load(std::memory_order_acquire);
+    if (h->arrive.fetch_add(1, std::memory_order_acq_rel) == c->world - 1) {
+        h->arrive.store(0, std::memory_order_relaxed);
+        h->gen.fetch_add(1, std::memory_order_release);
+    } else {
+        while (h->gen.load(std::memory_order_acquire) == g) sched_yield();
+    }
+}
+
+size_t type_size(ncclDataType_t t) {
+    switch (t) {
+        case ncclInt8: case ncclUint8: return 1;
+        case ncclFloat16: case ncclBfloat16: return 2;
+        case ncclInt32: case ncclUint32: case ncclFloat32: return 4;
+        case ncclInt64: case ncclUint64: case ncclFloat64: return 8;
+        default: return 0;
+    }
+}
+
+struct P2p {
+    bool send;
+    void *buf;
+    size_t bytes;
+    int peer;
+    FakeComm *comm;
+    cudaStream_t st;
+};
+int g_group = 0;
+std::vector<P2p> g_ops;
+
+ncclResult_t run_p2p(std::vector<P2p> &ops) {
+    if (ops.empty()) return ncclSuccess;
+    FakeComm *c = ops[0].comm;
+    for (auto &o : ops)
+        if (cudaStreamSynchronize(o.st) != cudaSuccess) return ncclUnhandledCudaError;
+    // messages larger than a mailbox go in rounds of `slot` bytes; every rank runs the same number of rounds
+    uint64_t mine = 0;
+    for (auto &o : ops) mine = o.bytes > mine ? o.bytes : mine;
+    c->hdr()->max_bytes[c->rank] = mine;
+    barrier(c);
+    uint64_t most = 0;
+    for (int r = 0; r < c->world; ++r) most = c->hdr()->max_bytes[r] > most ? c->hdr()->max_bytes[r] : most;
+    const size_t rounds = (size_t)((most + c->slot - 1) / c->slot);
+    barrier(c);
+    for (size_t k = 0; k < rounds; ++k) {
+        const size_t off = k * c->slot;
+        for (auto &o : ops)
+            if (o.send && off < o.bytes) {
+                const size_t n = o.bytes - off < c->slot ? o.bytes - off : c->slot;
+                if (cudaMemcpy(c->box(c->rank, o.peer), (const uint8_t *)o.buf + off, n, cudaMemcpyDeviceToHost) != cudaSuccess)
+                    return ncclUnhandledCudaError;
+            }
+        barrier(c);
+        for (auto &o : ops)
+            if (!o.send && off < o.bytes) {
+                const size_t n = o.bytes - off < c->slot ? o.bytes - off : c->slot;
+                if (cudaMemcpy((uint8_t *)o.buf + off, c->box(o.peer, c->rank), n, cudaMemcpyHostToDevice) != cudaSuccess)
+                    return ncclUnhandledCudaError;
+            }
+        barrier(c);
+    }
+    ops.clear();
+    return ncclSuccess;
+}
+
+}  // namespace
+
+extern "C" {
+
+ncclResult_t ncclGetVersion(int *v) {
+    *v = 22809;
+    return ncclSuccess;
+}
+const char *ncclGetErrorString(ncclResult_t r) { return r == ncclSuccess ? "no error" : "fake_nccl error"; }
+ncclResult_t ncclCommGetAsyncError(ncclComm_t, ncclResult_t *e) {
+    *e = ncclSuccess;
+    return ncclSuccess;
+}
+
+ncclResult_t ncclGetUniqueId(ncclUniqueId *id) {
+    memset(id, 0, sizeof *id);
+    snprintf(id->internal, sizeof id->internal, "/tmp/fake_nccl_%d_%ld", (int)getpid(), (long)clock());
+    return ncclSuccess;
+}
+
+ncclResult_t ncclCommInitRank(ncclComm_t *out, int nranks, ncclUniqueId id, int rank) {
+    if (nranks > 16) return ncclInvalidArgument;
+    FakeComm *c = new FakeComm();
+    c->rank = rank;
+    c->world = nranks;
+    const char *mb = getenv("FAKE_NCCL_SLOT_MB");
+    c->slot = (size_t)(mb ? atoi(mb) : 16) << 20;
+    c->bytes = 256 + (size_t)nranks * c->slot + (size_t)nranks * nranks * c->slot;
+    static_assert(sizeof(Header) <= 256, "header");
+    snprintf(c->path, sizeof c->path, "%s", id.internal);
+    const int fd = open(c->path, O_RDWR | O_CREAT, 0600);
+    if (fd < 0 || ftruncate(fd, (off_t)c->bytes) != 0) return ncclSystemError;  // zero-filled: the barrier starts at 0
+    c->base = (uint8_t *)mmap(nullptr, c->bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (c->base == MAP_FAILED) return ncclSystemError;
+    barrier(c);
+    *out = reinterpret_cast<ncclComm_t>(c);
+    return ncclSuccess;
+}
+
+ncclResult_t ncclCommDestroy(ncclComm_t comm) {
+    FakeComm *c = reinterpret_cast<FakeComm *>(comm);
+    barrier(c);
+    munmap(c->base, c->bytes);
+    if (c->rank == 0) unlink(c->path);
+    delete c;
+    return ncclSuccess;
+}
+
+ncclResult_t ncclGroupStart() {
+    ++g_group;
+    return ncclSuccess;
+}
+ncclResult_t ncclGroupEnd() {
+    if (--g_group > 0) return ncclSuccess;
+    return run_p2p(g_ops);
+}
+
+ncclResult_t ncclSend(const void *buf, size_t count, ncclDataType_t t, int peer, ncclComm_t comm, cudaStream_t st) {
+    g_ops.push_back({true, const_cast<void *>(buf), count * type_size(t), peer, reinterpret_cast<FakeComm *>(comm), st});
+    return g_group ? ncclSuccess : run_p2p(g_ops);
+}
+ncclResult_t ncclRecv(void *buf, size_t count, ncclDataType_t t, int peer, ncclComm_t comm, cudaStream_t st) {
+    g_ops.push_back({false, buf, count * type_size(t), peer, reinterpret_cast<FakeComm *>(comm), st});
+    return g_group ? ncclSuccess : run_p2p(g_ops);
+}
+
+ncclResult_t ncclAllGather(const void *send, void *recv, size_t count, ncclDataType_t t, ncclComm_t comm,
+                           cudaStream_t st) {
+    FakeComm *c = reinterpret_cast<FakeComm *>(comm);
+    const size_t b = count * type_size(t);
+    if (b > c->slot) return ncclInvalidUsage;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return ncclUnhandledCudaError;
+    if (b && cudaMemcpy(c->slot_of(c->rank), send, b, cudaMemcpyDeviceToHost) != cudaSuccess) return ncclUnhandledCudaError;
+    barrier(c);
+    for (int r = 0; r < c->world; ++r)
+        if (b && cudaMemcpy((uint8_t *)recv + (size_t)r * b, c->slot_of(r), b, cudaMemcpyHostToDevice) != cudaSuccess)
+            return ncclUnhandledCudaError;
+    barrier(c);
+    return ncclSuccess;
+}
+
+ncclResult_t ncclAllReduce(const void *send, void *recv, size_t count, ncclDataType_t t, ncclRedOp_t op,
+                           ncclComm_t comm, cudaStream_t st) {
+    FakeComm *c = reinterpret_cast<FakeComm *>(comm);
+    if ((t != ncclUint64 && t != ncclInt64) || (op != ncclMax && op != ncclSum)) return ncclInvalidUsage;
+    const size_t b = count * 8;
+    if (b > c->slot) return ncclInvalidUsage;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return ncclUnhandledCudaError;
+    if (b && cudaMemcpy(c->slot_of(c->rank), send, b, cudaMemcpyDeviceToHost) != cudaSuccess) return ncclUnhandledCudaError;
+    barrier(c);
+    std::vector<uint64_t> acc(count);
+    for (int r = 0; r < c->world; ++r) {
+        const uint64_t *v = reinterpret_cast<const uint64_t *>(c->slot_of(r));
+        for (size_t i = 0; i < count; ++i) {
+            if (r == 0) acc[i] = v[i];
+            else if (op == ncclSum) acc[i] += v[i];
+            else if (t == ncclUint64) acc[i] = v[i] > acc[i] ? v[i] : acc[i];
+            else acc[i] = (int64_t)v[i] > (int64_t)acc[i] ? v[i] : acc[i];
+        }
+    }
+    barrier(c);
+    if (b && cudaMemcpy(recv, acc.data(), b, cudaMemcpyHostToDevice) != cudaSuccess) return ncclUnhandledCudaError;
+    return ncclSuccess;
+}
+
+}  // extern "C"

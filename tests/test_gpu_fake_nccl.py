@@ -1,0 +1,57 @@
+"""The library's collective code at world 2 and 3 on ONE GPU (this pool grants one): every rank is a process on
+GPU 0 and the library's NCCL calls go to tests/native/fake_nccl.cpp (ATTNCACHE_NCCL_LIB), a functional stand-in
+that moves the bytes through host memory between host barriers.  tests/workers/multi_gpu_step.py then checks
+the collective step (routed and owner-affinity placements, skewed ownership; search, search_all, count
+exchanges, routed V / O, relocation) bitwise against the single-GPU step.  A correctness
+check of collective.cu's logic only: no timing is taken here."""
+import os
+import socket
+import subprocess
+import sys
+import tempfile
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def fake_nccl():
+    out = os.path.join(tempfile.mkdtemp(), "libfake_nccl.so")
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    subprocess.run(["g++", "-shared", "-fPIC", "-O2", "-I", os.path.join(cuda, "include"), "-o", out,
+                    os.path.join(ROOT, "tests", "native", "fake_nccl.cpp"), "-L", os.path.join(cuda, "lib64"),
+                    "-lcudart"], check=True)
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g", [2, 3, 4])
+def test_collective_step_fake_nccl_one_gpu(fake_nccl, g):
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, ATTNCACHE_NCCL_LIB=fake_nccl, ATTNCACHE_TEST_SINGLE_DEVICE="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={g}",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(ROOT, "tests", "workers", "multi_gpu_step.py")],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+    assert f"world {g} ok" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("placement", ["affinity", "routed"])
+def test_bench_n2_line_fake_nccl_one_gpu(fake_nccl, placement):
+    """`bench.py --gpus 2` (self-launched ranks) runs its N > 1 path end to end and prints one well-formed JSON line
+    (the driver's SCALE run uses this path on a multi-GPU box); the numbers of this one-GPU run mean nothing."""
+    import json
+    env = dict(os.environ, ATTNCACHE_NCCL_LIB=fake_nccl, ATTNCACHE_TEST_SINGLE_DEVICE="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+                        "--placement", placement, "--no-cpu-baseline"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+    line = json.loads([s for s in r.stdout.splitlines() if s.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["scaling"] in ("weak", "strong")
+    assert line["other_scaling"]["ms_per_step"] > 0 and line["gpu_launches"] > 0
+    assert line["config"]["placement"] == placement

@@ -17,9 +17,17 @@ from paper_2510_25979_b200.pipeline import PrefillStep  # noqa: E402
 
 def main():
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    # ATTNCACHE_TEST_SINGLE_DEVICE=1 (tests/test_gpu_fake_nccl.py): every rank on GPU 0, the library's collectives
+    # over tests/native/fake_nccl.cpp (ATTNCACHE_NCCL_LIB), torch.distributed over gloo (uid broadcast only)
+    single = os.environ.get("ATTNCACHE_TEST_SINGLE_DEVICE") == "1"
+    if single:
+        local = 0
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    dist.init_process_group("nccl", device_id=dev)
+    if single:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     cctx = ac.Context.from_process_group(local)
     lctx = ac.Context(local)
     cfg = synth.CONFIGS["llama32_1b"].with_(N=8 * world + 3, B=4 * world + 1, L=2)
@@ -69,7 +77,7 @@ def main():
         aff.apply_local(plan, loc, moved, O_loc, Q[loc.to(dev)].contiguous(), K[loc.to(dev)].contiguous())
         cctx.sync()
         assert torch.equal(O_loc, O_ref[loc.to(dev)]), (rank, pattern, "affinity O")
-        n = torch.tensor([loc.numel()], device=dev)
+        n = torch.tensor([loc.numel()], device="cpu" if single else dev)
         dist.all_reduce(n)
         assert n.item() == cfg.B, "every query placed exactly once"
     del db, full_db
