@@ -3,7 +3,8 @@
 // send/recv of routed rows and relocated request state) runs at world 2-4 with every rank on ONE GPU
 // (tests/test_gpu_fake_nccl.py; real NCCL refuses two ranks on one device).  It is not a performance stand-in:
 // every call synchronises the caller's stream and moves the bytes through a host file mapping shared by the
-// ranks, between host barriers, so no rank's kernels ever wait on another rank's kernels.
+// ranks (collectives between host barriers; send / recv through per-pair mailboxes), so no rank's kernels ever
+// wait on another rank's kernels.
 // Loaded by the library through ATTNCACHE_NCCL_LIB.  Build: g++ -shared -fPIC -O2 fake_nccl.cpp -lcudart.
 #include <atomic>
 #include <cstdint>
@@ -22,10 +23,16 @@
 
 namespace {
 
+constexpr int kMaxRanks = 16;
+constexpr size_t kHeader = 8192;
+
 struct Header {
-    std::atomic<int> arrive;
+    std::atomic<int> arrive;  // barrier (collectives: every rank takes part)
     std::atomic<int> gen;
-    uint64_t max_bytes[16];  // per rank: its largest message of the current group (P2P chunking rounds)
+    // point-to-point mailbox (src, dst): chunks posted by src and consumed by dst.  P2P needs no global step:
+    // like NCCL, a rank with nothing to send or receive in a group does not take part.
+    std::atomic<uint64_t> posted[kMaxRanks][kMaxRanks];
+    std::atomic<uint64_t> consumed[kMaxRanks][kMaxRanks];
 };
 
 struct FakeComm {
@@ -35,8 +42,8 @@ struct FakeComm {
     size_t bytes = 0;
     char path[160] = "";
     Header *hdr() const { return reinterpret_cast<Header *>(base); }
-    uint8_t *slot_of(int r) const { return base + 256 + (size_t)r * slot; }
-    uint8_t *box(int src, int dst) const { return base + 256 + (size_t)world * slot + ((size_t)src * world + dst) * slot; }
+    uint8_t *slot_of(int r) const { return base + kHeader + (size_t)r * slot; }
+    uint8_t *box(int src, int dst) const { return base + kHeader + (size_t)world * slot + ((size_t)src * world + dst) * slot; }
 };
 
 void barrier(FakeComm *c) {
@@ -73,35 +80,44 @@ std::vector<P2p> g_ops;
 
 ncclResult_t run_p2p(std::vector<P2p> &ops) {
     if (ops.empty()) return ncclSuccess;
-    FakeComm *c = ops[0].comm;
     for (auto &o : ops)
         if (cudaStreamSynchronize(o.st) != cudaSuccess) return ncclUnhandledCudaError;
-    // messages larger than a mailbox go in rounds of `slot` bytes; every rank runs the same number of rounds
-    uint64_t mine = 0;
-    for (auto &o : ops) mine = o.bytes > mine ? o.bytes : mine;
-    c->hdr()->max_bytes[c->rank] = mine;
-    barrier(c);
-    uint64_t most = 0;
-    for (int r = 0; r < c->world; ++r) most = c->hdr()->max_bytes[r] > most ? c->hdr()->max_bytes[r] : most;
-    const size_t rounds = (size_t)((most + c->slot - 1) / c->slot);
-    barrier(c);
-    for (size_t k = 0; k < rounds; ++k) {
-        const size_t off = k * c->slot;
-        for (auto &o : ops)
-            if (o.send && off < o.bytes) {
-                const size_t n = o.bytes - off < c->slot ? o.bytes - off : c->slot;
-                if (cudaMemcpy(c->box(c->rank, o.peer), (const uint8_t *)o.buf + off, n, cudaMemcpyDeviceToHost) != cudaSuccess)
+    // progress every send and receive of the group chunk by chunk (`slot` bytes per chunk) through its pair's
+    // mailbox until all are done: a send posts a chunk once the receiver consumed the previous one
+    std::vector<size_t> done(ops.size(), 0);
+    bool left = true;
+    while (left) {
+        left = false;
+        bool moved = false;
+        for (size_t i = 0; i < ops.size(); ++i) {
+            P2p &o = ops[i];
+            if (done[i] >= o.bytes) continue;
+            left = true;
+            FakeComm *c = o.comm;
+            Header *h = c->hdr();
+            const int src = o.send ? c->rank : o.peer, dst = o.send ? o.peer : c->rank;
+            const uint64_t posted = h->posted[src][dst].load(std::memory_order_acquire);
+            const uint64_t consumed = h->consumed[src][dst].load(std::memory_order_acquire);
+            const size_t n = o.bytes - done[i] < c->slot ? o.bytes - done[i] : c->slot;
+            if (o.send && posted == consumed) {
+                if (cudaMemcpy(c->box(src, dst), (const uint8_t *)o.buf + done[i], n, cudaMemcpyDeviceToHost) != cudaSuccess)
                     return ncclUnhandledCudaError;
-            }
-        barrier(c);
-        for (auto &o : ops)
-            if (!o.send && off < o.bytes) {
-                const size_t n = o.bytes - off < c->slot ? o.bytes - off : c->slot;
-                if (cudaMemcpy((uint8_t *)o.buf + off, c->box(o.peer, c->rank), n, cudaMemcpyHostToDevice) != cudaSuccess)
+                h->posted[src][dst].store(posted + 1, std::memory_order_release);
+                done[i] += n;
+                moved = true;
+            } else if (!o.send && posted > consumed) {
+                if (cudaMemcpy((uint8_t *)o.buf + done[i], c->box(src, dst), n, cudaMemcpyHostToDevice) != cudaSuccess)
                     return ncclUnhandledCudaError;
+                h->consumed[src][dst].store(consumed + 1, std::memory_order_release);
+                done[i] += n;
+                moved = true;
             }
-        barrier(c);
+        }
+        if (left && !moved) sched_yield();
     }
+    // a receive is complete when its last chunk is consumed; a send when the receiver took its last chunk (the
+    // caller may reuse the buffer, but the mailbox must be free before this rank's next send to the same peer:
+    // the next post waits for that anyway)
     ops.clear();
     return ncclSuccess;
 }
@@ -127,14 +143,14 @@ ncclResult_t ncclGetUniqueId(ncclUniqueId *id) {
 }
 
 ncclResult_t ncclCommInitRank(ncclComm_t *out, int nranks, ncclUniqueId id, int rank) {
-    if (nranks > 16) return ncclInvalidArgument;
+    if (nranks > kMaxRanks) return ncclInvalidArgument;
     FakeComm *c = new FakeComm();
     c->rank = rank;
     c->world = nranks;
     const char *mb = getenv("FAKE_NCCL_SLOT_MB");
     c->slot = (size_t)(mb ? atoi(mb) : 16) << 20;
-    c->bytes = 256 + (size_t)nranks * c->slot + (size_t)nranks * nranks * c->slot;
-    static_assert(sizeof(Header) <= 256, "header");
+    c->bytes = kHeader + (size_t)nranks * c->slot + (size_t)nranks * nranks * c->slot;
+    static_assert(sizeof(Header) <= kHeader, "header");
     snprintf(c->path, sizeof c->path, "%s", id.internal);
     const int fd = open(c->path, O_RDWR | O_CREAT, 0600);
     if (fd < 0 || ftruncate(fd, (off_t)c->bytes) != 0) return ncclSystemError;  // zero-filled: the barrier starts at 0
