@@ -41,17 +41,31 @@ def test_collective_step_fake_nccl_one_gpu(fake_nccl, g):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("placement", ["affinity", "routed"])
-def test_bench_n2_line_fake_nccl_one_gpu(fake_nccl, placement):
+@pytest.mark.parametrize("placement,gpus,scaling", [("affinity", 2, "weak"), ("routed", 2, "weak"),
+                                                    ("affinity", 4, "strong")])
+def test_bench_n2_line_fake_nccl_one_gpu(fake_nccl, placement, gpus, scaling):
     """`bench.py --gpus 2` (self-launched ranks) runs its N > 1 path end to end and prints one well-formed JSON line
     (the driver's SCALE run uses this path on a multi-GPU box); the numbers of this one-GPU run mean nothing."""
     import json
     env = dict(os.environ, ATTNCACHE_NCCL_LIB=fake_nccl, ATTNCACHE_TEST_SINGLE_DEVICE="1")
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
-                        "--placement", placement, "--no-cpu-baseline"],
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(gpus), "--steps", "2", "--warmup",
+                        "3", "--placement", placement, "--scaling", scaling, "--no-cpu-baseline"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
     line = json.loads([s for s in r.stdout.splitlines() if s.startswith("{")][-1])
-    assert line["n_gpus"] == 2 and line["value"] > 0 and line["scaling"] in ("weak", "strong")
+    assert line["n_gpus"] == gpus and line["value"] > 0 and line["scaling"] == scaling
     assert line["other_scaling"]["ms_per_step"] > 0 and line["gpu_launches"] > 0
     assert line["config"]["placement"] == placement
+
+
+@pytest.mark.gpu
+def test_bench_reference_arm_n2(fake_nccl):
+    """`bench.py --impl reference --gpus 2`: rank 0 alone times the oracle and prints the line, the other rank exits
+    0 without work (the driver launches the reference arm the same way as ours)."""
+    import json
+    env = dict(os.environ, ATTNCACHE_NCCL_LIB=fake_nccl, ATTNCACHE_TEST_SINGLE_DEVICE="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps",
+                        "1", "--warmup", "3"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+    lines = [json.loads(s) for s in r.stdout.splitlines() if s.startswith("{")]
+    assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["value"] > 0
