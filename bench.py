@@ -72,6 +72,11 @@ def attend_bytes_per_miss(cfg):
     return 4 * cfg.L * cfg.H * cfg.S * cfg.d * e_v
 
 
+def attend_flops_per_miss(cfg):
+    """Causal attention flops: 4 d tri(S) per (layer, head)."""
+    return 4.0 * cfg.L * cfg.H * cfg.d * cfg.S * (cfg.S + 1) / 2
+
+
 # ------------------------------------------------------------------------------------------------
 # clocks sampled during the timed region (B200_PROFILING.md clocks line)
 # ------------------------------------------------------------------------------------------------
@@ -308,6 +313,8 @@ def run_ours(args, cfg):
         "search": {"ms": search_ms, "qps": cfg.B / (search_ms * 1e-3),
                    "variant": ac.attncache_variant("search", q.dtype, 0, cfg.D)},
         "attend_full_misses": {"ms": attend_ms, "hbm_frac": attend_alg / (attend_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                               "tensor_frac": (cfg.B - n_hit) * attend_flops_per_miss(cfg) / (attend_ms * 1e-3) / 1e12
+                               / peaks["bf16_tflops"],
                                "variant": ac.attncache_variant("attend", V.dtype, cfg.S, cfg.d)},
     }
 
