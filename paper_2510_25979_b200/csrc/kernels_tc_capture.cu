@@ -7,7 +7,8 @@
 //           its row's running max m and sum l of exp2(s*scale*log2e - m)           (row statistics)
 //   pass 1: S again; P = exp2(s*scale*log2e - m - log2 l), masked, rounded, stored.
 // Recomputing S (2x the Q K^T flops) keeps the kernel one launch with no score round trip through
-// HBM; the kernel is bound by writing the maps.
+// HBM.  The maps are written with 32-byte stores straight from the registers (store_seg): the store path's
+// request rate, not HBM, is what the map writes cost (configs[3]: 1.21 ms with the stores compiled out).
 // Roles (384 threads): two independent groups (two item streams per CTA), each with a TMA loader thread
 // (warp 2g), an MMA thread (warp 2g+1; two 128-column S buffers per group) and a 4-warp epilogue group
 // (warps 4-7 / 8-11; TMEM lane quarter = warp % 4, one query row per thread, the S row held in
