@@ -107,8 +107,9 @@ attncache_status attncache_ctx_info(const attncache_ctx *ctx, int32_t *rank, int
  * attend_full, capture_maps, linear), aux_sms the CTAs of the search, projector, placement and row-copy
  * kernels.  Both default to the device's SM count.  A caller that runs the next batch's search, placement
  * and relocation on other streams beside this batch's layers sets compute_sms + aux_sms <= the SM count,
- * so those kernels (and NCCL's) find free SMs instead of queueing behind the persistent kernels.  Results
- * do not depend on the budget (the kernels' outputs are independent of their CTA counts).
+ * so those kernels (and NCCL's) find free SMs instead of queueing behind the persistent kernels (at world 1
+ * every reserve measured slower: the HBM-bound A.V needs every SM).  Results do not depend on
+ * the budget (the kernels' outputs are independent of their CTA counts).
  * Errors: INVALID_ARGUMENT (NULL ctx, a value < 1 or above the SM count). */
 attncache_status attncache_ctx_set_sm_budget(attncache_ctx *ctx, int32_t compute_sms, int32_t aux_sms);
 attncache_status attncache_ctx_destroy(attncache_ctx *ctx);
