@@ -628,7 +628,10 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
         Q, K, V = (_rows_activations(cfg, k, loc.tolist(), dev) for k in "qkv")
         O = torch.empty_like(V)
         X_home = torch.randn(hc, cfg.S, cfg.H * cfg.d, device=dev).to(synth.torch_dtype(cfg.act_dtype))
-        comm, plan_st = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        # side streams at high priority: when a persistent layer kernel's CTAs retire, the block scheduler
+        # dispatches the next batch's search / placement / copy CTAs before the next layer kernel's
+        side_prio = int(os.environ.get("ATTNCACHE_BENCH_SIDE_PRIORITY", "-1"))
+        comm, plan_st = torch.cuda.Stream(dev, priority=side_prio), torch.cuda.Stream(dev, priority=side_prio)
         state = {"plan": plan0}
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         budget = (sms - args.aux_sms, args.aux_sms) if 0 < args.aux_sms < sms else (sms, sms)
