@@ -340,6 +340,8 @@ def run_ours(args, cfg):
     del O_full
     # §8(f) f4: Eq. 5 block level (Q/K/V projections + RoPE + attention vs V projection + A.V)
     line["eq5_block"] = eq5_block(ac, ctx, db, cfg, idx, hit, stream, max(3, args.steps // 2))
+    if cfg.H % 8 == 0:
+        line["eq5_block_gqa"] = eq5_block(ac, ctx, db, cfg, idx, hit, stream, max(3, args.steps // 2), n_kv_heads=8)
     if not args.no_target and cfg.name != "llama3_8b":
         # north_star's target shape (>= 3x at Llama-3-8B shape: BASELINE.json configs[2], Table 4)
         del step, db, maps, x, q, Q, K, V, O, idx, score, hit, hit_rows_only
@@ -427,7 +429,8 @@ def target_config_block(args, ac, ctx, dev, stream, peaks, name):
                                          "full_attention_ms": full_ms, "full_attention_hit_rows_ms": full_hits_ms,
                                          "ceiling_vs_roofline_attention_per_hit": 8 * cfg.d / (cfg.S + 1 + 4 * cfg.d),
                                          "paper_context": PAPER_CONTEXT},
-           "eq5_block": eq5_block(ac, ctx, db, cfg, idx, hit, stream, steps)}
+           "eq5_block": eq5_block(ac, ctx, db, cfg, idx, hit, stream, steps),
+           "eq5_block_gqa": eq5_block(ac, ctx, db, cfg, idx, hit, stream, steps, n_kv_heads=8)}
     del step, db, maps, x, q, Q, K, V, O
     torch.cuda.empty_cache()
     return out
@@ -510,12 +513,13 @@ def project_stage(ac, ctx, cfg, dev, stream, steps, peaks):
     return out
 
 
-def eq5_block(ac, ctx, db, cfg, idx, hit, stream, steps):
+def eq5_block(ac, ctx, db, cfg, idx, hit, stream, steps, n_kv_heads=None):
     """One layer's attention block for the whole batch: the full path on every row vs the cached
     path (hits: V projection + A.V; misses: the full path), and the all-hit per-row ratio.  The paper's
-    3x attention speedup is this block-level quantity (Table 4)."""
+    3x attention speedup is this block-level quantity (Table 4).  n_kv_heads: grouped-query
+    K / V projections (a supplementary variant; the configs are multi-head, reading A14)."""
     from paper_2510_25979_b200.block import AttentionBlock
-    X, (Wq, Wk, Wv) = synth.block_inputs(cfg, idx.device)
+    X, (Wq, Wk, Wv) = synth.block_inputs(cfg, idx.device, n_kv_heads=n_kv_heads)
     blk = AttentionBlock(ctx, db, Wq, Wk, Wv, cfg.H, cfg.d, layer=0)
     miss_rows = torch.nonzero(hit == 0).flatten()
     none = miss_rows[:0]
@@ -535,10 +539,15 @@ def eq5_block(ac, ctx, db, cfg, idx, hit, stream, steps):
     cached_ms = timed(lambda: blk.cached(X, idx, hit, miss_rows))
     hits_ms = timed(lambda: blk.cached(X, idx, all_hit, none))
     del X, Wq, Wk, Wv, blk
-    return {"layer_full_ms": full_ms, "layer_cached_ms": cached_ms, "layer_all_hits_ms": hits_ms,
-            "speedup_batch": full_ms / cached_ms, "speedup_per_hit": full_ms / hits_ms,
-            "note": "one layer, whole batch; Q/K/V projections (attncache_linear), RoPE, A.V and attention all "
-                    "in this library; synthetic weights; paper: 3x attention on A100 (PAPER.md:446)"}
+    out = {"layer_full_ms": full_ms, "layer_cached_ms": cached_ms, "layer_all_hits_ms": hits_ms,
+           "speedup_batch": full_ms / cached_ms, "speedup_per_hit": full_ms / hits_ms,
+           "note": "one layer, whole batch; Q/K/V projections (attncache_linear), RoPE, A.V and attention all "
+                   "in this library; synthetic weights; paper: 3x attention on A100 (PAPER.md:446)"}
+    if n_kv_heads is not None:
+        out["n_kv_heads"] = n_kv_heads
+        out["note"] += (f"; grouped-query variant: W_K, W_V with {n_kv_heads} KV heads (the Llama-3 count), "
+                        "maps and A.V per query head")
+    return out
 
 
 def eager_attention_ms(Q, K, V, stream, steps):

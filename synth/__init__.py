@@ -210,16 +210,17 @@ def activations(cfg: Config, kind: str, b_begin: int, count: int, layer_begin: i
     return out
 
 
-def block_inputs(cfg: Config, device="cpu", B: int | None = None):
+def block_inputs(cfg: Config, device="cpu", B: int | None = None, n_kv_heads: int | None = None):
     """Eq. 5 block-level comparison inputs (f4): hidden states X [B][S][E] ~ N(0,1) and projection
-    weights W_Q, W_K, W_V [E][E] ~ N(0, 1/E) (nn.Linear layout), E = H * d, in the activation dtype (synthetic: no
-    trained weights are available)."""
+    weights W_Q [E][E], W_K, W_V [Hkv*d][E] ~ N(0, 1/E) (nn.Linear layout), E = H * d, Hkv = n_kv_heads (default
+    H: multi-head), in the activation dtype (synthetic: no trained weights are available)."""
     B = cfg.B if B is None else B
     E = cfg.H * cfg.d
+    Ekv = (cfg.H if n_kv_heads is None else n_kv_heads) * cfg.d
     dt = _TD[cfg.act_dtype]
     X = torch.randn(B, cfg.S, E, generator=_gen(device, cfg.seed, "x", 0), device=device).to(dt)
-    W = [(torch.randn(E, E, generator=_gen(device, cfg.seed, k, 0), device=device) / math.sqrt(E)).to(dt)
-         for k in ("wq", "wk", "wv")]
+    W = [(torch.randn(n, E, generator=_gen(device, cfg.seed, k, 0), device=device) / math.sqrt(E)).to(dt)
+         for k, n in (("wq", E), ("wk", Ekv), ("wv", Ekv))]
     return X, W
 
 

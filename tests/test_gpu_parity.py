@@ -724,38 +724,48 @@ def test_linear_head_major_matches_oracle(ac, ctx, M, K, N, S, d):
     check_close(Y.view(M // S, N // d, S, d).reshape(-1, S, d), ref.reshape(-1, S, d), torch.bfloat16, "linear")
 
 
-def test_eq5_block_matches_oracle(ac, ctx):
+@pytest.mark.parametrize("n_kv", [None, 2, 1])
+def test_eq5_block_matches_oracle(ac, ctx, n_kv):
     """f4 (Eq. 5; Alg. 2 l.372-381) against the oracle composed step by step: q, k, v =
     oracle.linear (rounded to the bf16 activation dtype), RoPE (oracle.rope, rounded), causal softmax attention
-    (oracle.attend) for the full block; v then A.V with the DB's maps (oracle.apply) for the cached block."""
+    (oracle.attend) for the full block; v then A.V with the DB's maps (oracle.apply) for the cached block.
+    n_kv: grouped-query K / V projections (query head h reads K / V head h // (H / n_kv)); the oracle gets the
+    K / V heads repeated, the multi-head definition of the same block."""
     from paper_2510_25979_b200.block import AttentionBlock
     cfg = synth.CONFIGS["llama32_1b"].with_(B=3, N=3, L=1, H=4)
-    X, (Wq, Wk, Wv) = synth.block_inputs(cfg, DEV)
+    X, (Wq, Wk, Wv) = synth.block_inputs(cfg, DEV, n_kv_heads=n_kv)
     E, S, H, d = X.shape[2], cfg.S, cfg.H, cfg.d
+    Hkv = H if n_kv is None else n_kv
     maps = ac.attncache_pack_maps(synth.maps(cfg, 0, 3, DEV))
     db = ac.Database(ctx, synth.features(cfg, 0, 3, DEV), maps, packed=True, seq_len=S)
     blk = AttentionBlock(ctx, db, Wq, Wk, Wv, H, d)
+    assert blk.Hkv == Hkv
     O_full = blk.full(X)
     idx = torch.tensor([2, 0, 1], device=DEV)
     O_cached = blk.cached(X, idx, torch.ones(3, dtype=torch.uint8, device=DEV), idx[:0])
+    O_mixed = blk.cached(X, idx, torch.tensor([0, 1, 0], dtype=torch.uint8, device=DEV), torch.tensor([0, 2], device=DEV))
     torch.cuda.synchronize()
     Xs = storage(X.view(-1, E))
 
-    def heads(W):  # oracle projection -> bf16 [B][H][S][d]
-        y = oracle.linear(Xs, storage(W), "bf16").reshape(cfg.B, S, H, d).transpose(0, 2, 1, 3)
-        return _round_bf16(y.copy())
+    def heads(W, nh):  # oracle projection -> bf16 [B][nh][S][d], then K / V heads repeated up to H
+        y = oracle.linear(Xs, storage(W), "bf16").reshape(cfg.B, S, nh, d).transpose(0, 2, 1, 3)
+        return _round_bf16(y.copy()).repeat_interleave(H // nh, dim=1).contiguous()
 
-    Qo, Ko, Vo = heads(Wq), heads(Wk), heads(Wv)
+    Qo, Ko, Vo = heads(Wq, H), heads(Wk, Hkv), heads(Wv, Hkv)
     Qr = _round_bf16(oracle.rope(storage(Qo), "bf16", S, d, base=blk.rope_base))
     Kr = _round_bf16(oracle.rope(storage(Ko), "bf16", S, d, base=blk.rope_base))
     units = [(b, h) for b in range(cfg.B) for h in range(H)]
     off = [((b * H + h) * S * d) for b, h in units]
     ref = oracle.attend(storage(Qr), storage(Kr), storage(Vo), "bf16", off, S, d)
     check_close(torch.stack([O_full[b, 0, h] for b, h in units]), ref, torch.bfloat16, "eq5 full block")
+    check_close(torch.stack([O_mixed[b, 0, h] for b, h in units if b != 1]),
+                ref[[i for i, (b, h) in enumerate(units) if b != 1]], torch.bfloat16, "eq5 mixed block (misses)")
     dense = storage(synth.maps(cfg, 0, 3, DEV))
     a_off = [((int(idx[b]) * H + h) * S * S) for b, h in units]
     ref = oracle.apply(dense, "bf16", a_off, storage(Vo), "bf16", off, S, d)
     check_close(torch.stack([O_cached[b, 0, h] for b, h in units]), ref, torch.bfloat16, "eq5 cached block")
+    check_close(torch.stack([O_mixed[1, 0, h] for h in range(H)]), ref[H:2 * H], torch.bfloat16,
+                "eq5 mixed block (hit)")
 
 
 @pytest.mark.parametrize("cfg_name,N,B", [("tiny", 5, 3), ("llama32_1b", 4, 3), ("llama3_8b", 2, 2)])
