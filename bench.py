@@ -816,9 +816,41 @@ def run_e2e(args, cfg, ctx, db, step, q, Q, K, V, dev, stream):
     d2h = Oh.numel() * Oh.element_size() + cfg.B * (8 + 4 + 1)
     return {"value": cfg.B * cfg.S / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms, "steps": n,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "attncache_prefill_host (C ABI)",
+            "copy_bound": _copy_bound(Vh, V, Qh[:n_miss], Q[:n_miss], Kh[:n_miss], K[:n_miss], Oh, ms),
             "note": "pinned host buffers; one synchronous C-ABI call per step: chunk-pipelined copies (16 rows, "
                     "4-deep ring, three library streams) overlapping the kernels; one mid-call D2H of the "
                     "decisions"}
+
+
+def _copy_bound(Vh, V, Qh, Q, Kh, K, Oh, e2e_ms, reps=3):
+    """The PCIe floor of the e2e step, measured after it on the same buffers: the step's H2D bytes (V of every
+    row, Q / K of the misses; the host copies hold the device tensors' own values) and its D2H bytes (O, the
+    size of V) copied concurrently on two streams with no kernel, best of `reps`.  frac = floor / e2e step."""
+    dev = V.device
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def once(h2d=True, d2h=True):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if h2d:
+            with torch.cuda.stream(s_in):
+                for d, h in ((V, Vh), (Q, Qh), (K, Kh)):
+                    d.copy_(h, non_blocking=True)
+        if d2h:
+            with torch.cuda.stream(s_out):
+                Oh.copy_(V, non_blocking=True)
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) * 1e3
+
+    both = min(once() for _ in range(reps))
+    h2d_ms = min(once(d2h=False) for _ in range(reps))
+    d2h_ms = min(once(h2d=False) for _ in range(reps))
+    nin = sum(t.numel() * t.element_size() for t in (Vh, Qh, Kh))
+    nout = Oh.numel() * Oh.element_size()
+    return {"copies_only_ms": both, "frac": both / e2e_ms, "h2d_gbs_alone": nin / h2d_ms / 1e6,
+            "d2h_gbs_alone": nout / d2h_ms / 1e6, "h2d_plus_d2h_gbs_concurrent": (nin + nout) / both / 1e6,
+            "note": "the step's H2D and D2H bytes copied concurrently with no kernel (the e2e floor on this "
+                    "host link); frac = copies_only_ms / e2e ms_per_step"}
 
 
 def _ncu_traffic(cfg_name, kernel):
