@@ -307,6 +307,7 @@ static attncache_status check_queries(attncache_db *db, const void *queries, int
 }
 
 attncache_status attncache_search_keys(attncache_db *db, const void *queries, int64_t n, uint64_t *keys, void *stream) {
+    AC_NVTX("attncache_search_keys");
     attncache_status s = check_queries(db, queries, n);
     if (s) return s;
     if (n > 0 && !keys) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search_keys: keys is NULL");
@@ -325,6 +326,7 @@ attncache_status attncache_keys_decode(const uint64_t *keys, int32_t n_shards, i
 
 static attncache_status search_common(attncache_db *db, const void *queries, int64_t n, float tau, int64_t *idx,
                                       float *score, uint8_t *hit, bool all, void *stream) {
+    AC_NVTX("attncache_search");
     attncache_status s = check_queries(db, queries, n);
     if (s) return s;
     if (std::isnan(tau)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: tau is NaN");
@@ -437,6 +439,7 @@ attncache_status attncache_apply_cached_local(attncache_db *db, const int64_t *i
                                               int32_t layer_begin, int32_t layer_end, int32_t head_dim,
                                               int32_t n_kv_heads, int32_t act_dtype, const void *V, void *O,
                                               void *stream) {
+    AC_NVTX("attncache_apply_cached_local");
     return apply_local_impl(db, idx, hit, n_rows, layer_begin, layer_end, head_dim, n_kv_heads, act_dtype, V, O,
                             (cudaStream_t)stream);
 }
@@ -445,6 +448,7 @@ attncache_status attncache_apply_cached_gqa(attncache_db *db, const int64_t *idx
                                             int32_t layer_begin, int32_t layer_end, int32_t head_dim,
                                             int32_t n_kv_heads, int32_t act_dtype, const void *V, void *O,
                                             void *stream) {
+    AC_NVTX("attncache_apply_cached");
     attncache_status s = apply_check(db, idx, hit, n_rows, layer_begin, layer_end, head_dim, n_kv_heads, act_dtype, V, O);
     if (s) return s;
     attncache_ctx *ctx = db->ctx;
@@ -478,6 +482,7 @@ attncache_status attncache_attend_full(attncache_ctx *ctx, int64_t batch, int32_
 attncache_status attncache_attend_full_gqa(attncache_ctx *ctx, int64_t batch, int32_t L, int32_t H, int32_t n_kv_heads,
                                            int32_t S, int32_t dd, int32_t act_dtype, const void *Q, const void *K,
                                            const void *V, float scale, const uint8_t *skip, void *O, void *stream) {
+    AC_NVTX("attncache_attend_full");
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "attend_full: ctx is NULL");
     if (H > 0 && (n_kv_heads <= 0 || H % n_kv_heads))
         return fail(ATTNCACHE_ERR_SHAPE, "attend_full: n_kv_heads %d does not divide n_heads %d", n_kv_heads, H);
@@ -529,6 +534,7 @@ attncache_status attncache_project_features(attncache_ctx *ctx, const void *h, i
                                             int32_t act_dtype, const void *W1, const float *b1, int32_t hidden_dim,
                                             const void *W2, const float *b2, int32_t feat_dim, int32_t feat_dtype,
                                             void *features, void *stream) {
+    AC_NVTX("attncache_project_features");
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "project_features: ctx is NULL");
     if (n < 0) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "project_features: n < 0");
     if (in_dim <= 0 || hidden_dim <= 0 || feat_dim <= 0)
@@ -577,6 +583,7 @@ attncache_status attncache_project_features(attncache_ctx *ctx, const void *h, i
 attncache_status attncache_linear(attncache_ctx *ctx, const void *X, int64_t M, int32_t K, const void *W, int32_t N,
                                   int32_t dtype, const float *bias, int32_t seq_len, int32_t head_dim, void *Y,
                                   void *stream) {
+    AC_NVTX("attncache_linear");
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "linear: ctx is NULL");
     if (M < 0 || K <= 0 || N <= 0 || seq_len <= 0 || head_dim <= 0)
         return fail(ATTNCACHE_ERR_SHAPE, "linear: M=%lld K=%d N=%d S=%d d=%d", (long long)M, K, N, seq_len, head_dim);
@@ -600,6 +607,7 @@ attncache_status attncache_linear(attncache_ctx *ctx, const void *X, int64_t M, 
 // ---- RoPE (f4) ----------------------------------------------------------------------------------
 
 attncache_status attncache_rope(void *X, int64_t n_units, int32_t S, int32_t d, int32_t dt, float base, void *stream) {
+    AC_NVTX("attncache_rope");
     if (n_units < 0 || S <= 0 || d <= 0) return fail(ATTNCACHE_ERR_SHAPE, "rope: n_units=%lld S=%d d=%d", (long long)n_units, S, d);
     if (d % 2) return fail(ATTNCACHE_ERR_SHAPE, "rope: head_dim %d is odd", d);
     if (!dtype_valid(dt)) return fail(ATTNCACHE_ERR_DTYPE, "rope: dtype %d", dt);
@@ -624,6 +632,7 @@ attncache_status attncache_capture_maps_gqa(attncache_ctx *ctx, int64_t batch, i
                                             int32_t S, int32_t dd, int32_t act_dtype, const void *Q, const void *K,
                                             float scale, const uint8_t *skip, int32_t map_dtype, int32_t map_layout,
                                             void *maps_out, void *stream) {
+    AC_NVTX("attncache_capture_maps");
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "capture_maps: ctx is NULL");
     if (H > 0 && (n_kv_heads <= 0 || H % n_kv_heads))
         return fail(ATTNCACHE_ERR_SHAPE, "capture_maps: n_kv_heads %d does not divide n_heads %d", n_kv_heads, H);
@@ -732,6 +741,7 @@ attncache_status attncache_affinity_plan_device(attncache_ctx *ctx, const int64_
                                                 int32_t rank, const int64_t *hb, int32_t *assign, double *load,
                                                 int64_t *loc, int64_t *idx_loc, uint8_t *hit_loc, int64_t *send_order,
                                                 int32_t *counts, void *stream) {
+    AC_NVTX("attncache_affinity_plan_device");
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan_device: ctx is NULL");
     if (n < 0 || world <= 0 || world > ac::kPlanMaxWorld || rank < 0 || rank >= world)
         return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "affinity_plan_device: n=%lld world=%d rank=%d (world <= %d)",

@@ -350,6 +350,7 @@ attncache_status attncache_set_batch_layout(attncache_ctx *ctx, const int64_t *h
 
 attncache_status attncache_relocate_rows(attncache_ctx *ctx, const void *src, int64_t n_home, int64_t row_bytes,
                                          const int64_t *send_order, const int32_t *counts, void *dst, void *stream) {
+    AC_NVTX("attncache_relocate_rows");
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "relocate_rows: ctx is NULL");
     if (n_home < 0 || row_bytes <= 0 || row_bytes % 8)
         return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "relocate_rows: n_home=%lld row_bytes=%lld (a multiple of 8)",

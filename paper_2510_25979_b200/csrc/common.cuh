@@ -6,6 +6,18 @@
 #include <stdint.h>
 
 #include "../../include/attncache.h"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: a no-op unless a tool (ncu --nvtx, nsys) is attached
+
+namespace ac {
+// One NVTX range per C-ABI compute call (SURVEY.md §5 tracing): the calls show up by name in a tool's timeline.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+}  // namespace ac
+#define AC_NVTX(name) ::ac::NvtxRange ac_nvtx_range_(name)
 
 namespace ac {
 

@@ -33,6 +33,7 @@ extern "C" attncache_status attncache_prefill_host(attncache_db *db, const void 
                                                    const void *Q, const void *K, const void *V, int32_t head_dim,
                                                    int32_t act_dtype, void *O, int64_t *idx, float *score,
                                                    uint8_t *hit, int32_t chunk, int32_t depth) {
+    AC_NVTX("attncache_prefill_host");
     if (!db) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "prefill_host: db is NULL");
     attncache_ctx *ctx = db->ctx;
     const attncache_db_desc &d = db->d;
