@@ -115,7 +115,10 @@ attncache_status attncache_ctx_set_sm_budget(attncache_ctx *ctx, int32_t compute
 attncache_status attncache_ctx_destroy(attncache_ctx *ctx);
 /* Synchronises the device and returns (then clears) any deferred error: ERR_NOT_FOUND when an
  * apply call met an index outside its shard, ERR_CUDA on an asynchronous CUDA fault, ERR_NCCL on an
- * asynchronous communicator error. */
+ * asynchronous communicator error (ncclCommGetAsyncError).  On such an error the library aborts its
+ * communicator (ncclCommAbort: no barrier with peers that may be gone) and the ctx stays failed: every
+ * later collective call (search, apply_cached, relocate_rows, db_load) and ctx_sync return ERR_NCCL; the
+ * caller destroys the ctx (and its dbs) and creates a new one.  SURVEY.md §5 failure detection. */
 attncache_status attncache_ctx_sync(attncache_ctx *ctx);
 
 /* The home batch size of every rank for the following collective calls (home_counts: host int64 [world];

@@ -13,7 +13,8 @@ attncache_status apply_local_impl(attncache_db *db, const int64_t *idx, const ui
                                   int32_t act_dtype, const void *V, void *O, cudaStream_t st);
 
 // collective.cu
-attncache_status comm_check(attncache_ctx *ctx);
+attncache_status comm_check(attncache_ctx *ctx);          // polls the async error; aborts the comm on one
+attncache_status comm_failed_status();                    // ERR_NCCL: the comm was aborted (see comm_check)
 attncache_status db_load_collective(attncache_db *db);
 attncache_status search_collective(attncache_db *db, const void *q, int64_t n_home, float tau, bool all, int64_t *idx,
                                    float *score, uint8_t *hit, cudaStream_t st);

@@ -331,6 +331,7 @@ static attncache_status search_common(attncache_db *db, const void *queries, int
     if (s) return s;
     if (std::isnan(tau)) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: tau is NaN");
     if (db->d.n_global == 0) return fail(ATTNCACHE_ERR_EMPTY, "search: the database has no entries");
+    if (db->ctx->comm_failed) return comm_failed_status();
     DeviceGuard g(db->ctx->device);
     cudaStream_t st = (cudaStream_t)stream;
     if (db->ctx->comm) {  // COLLECTIVE: C1 query all-gather, K1, C2 key max-all-reduce, K2
@@ -452,6 +453,7 @@ attncache_status attncache_apply_cached_gqa(attncache_db *db, const int64_t *idx
     attncache_status s = apply_check(db, idx, hit, n_rows, layer_begin, layer_end, head_dim, n_kv_heads, act_dtype, V, O);
     if (s) return s;
     attncache_ctx *ctx = db->ctx;
+    if (ctx->comm_failed) return comm_failed_status();
     if (ctx->comm && (ctx->world > 1 || ctx->force_route)) {  // COLLECTIVE: route hits to the owner and O back
         if (n_rows && hit && !is_device_ptr(hit))
             return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "apply_cached: hit must be device memory");

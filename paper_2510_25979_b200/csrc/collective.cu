@@ -34,6 +34,7 @@ struct NcclApi {
     const char *(*GetErrorString)(ncclResult_t);
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *);
     ncclResult_t (*GetVersion)(int *);
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;  // optional: CommDestroy stands in when absent
     bool ok = false;
     char why[256] = "";
 };
@@ -70,6 +71,7 @@ void load_nccl() {
     AC_SYM(CommGetAsyncError, "ncclCommGetAsyncError")
     AC_SYM(GetVersion, "ncclGetVersion")
 #undef AC_SYM
+    g_nccl.CommAbort = reinterpret_cast<decltype(g_nccl.CommAbort)>(dlsym(h, "ncclCommAbort"));
     g_nccl.ok = true;
 }
 
@@ -151,18 +153,34 @@ void comm_destroy(attncache_ctx *ctx) {
     ctx->comm = nullptr;
 }
 
+// Polls the communicator's asynchronous error (SURVEY.md §5 failure detection).  On an error the communicator is
+// aborted (ncclCommAbort: no barrier with peers that may be gone) and the ctx is marked so that every later
+// collective call fails with ATTNCACHE_ERR_NCCL instead of waiting on a dead communicator.
 attncache_status comm_check(attncache_ctx *ctx) {
+    if (ctx->comm_failed) return comm_failed_status();
     if (!ctx->comm) return ATTNCACHE_OK;
     ncclResult_t r = ncclSuccess;
     AC_NCCL(nccl()->CommGetAsyncError(comm_of(ctx), &r));
-    if (r != ncclSuccess && r != ncclInProgress) return nccl_status(r, "asynchronous NCCL error");
+    if (r != ncclSuccess && r != ncclInProgress) {
+        const NcclApi *N = nccl();
+        (N->CommAbort ? N->CommAbort : N->CommDestroy)(comm_of(ctx));
+        ctx->comm = nullptr;
+        ctx->comm_failed = true;
+        return nccl_status(r, "asynchronous NCCL error (the communicator was aborted)");
+    }
     return ATTNCACHE_OK;
+}
+
+attncache_status comm_failed_status() {
+    return fail(ATTNCACHE_ERR_NCCL, "the ctx's NCCL communicator was aborted after an asynchronous error; destroy "
+                "the ctx and create a new one");
 }
 
 // Collective db_load check: every rank's descriptor agrees on the global fields and the shards tile
 // [0, n_global) contiguously in rank order ("partitioned by contiguous entry ranges").
 attncache_status db_load_collective(attncache_db *db) {
     attncache_ctx *ctx = db->ctx;
+    if (ctx->comm_failed) return comm_failed_status();
     const int w = ctx->world;
     const attncache_db_desc &d = db->d;
     db->shard_begins.assign(w + 1, 0);
@@ -352,6 +370,7 @@ attncache_status attncache_relocate_rows(attncache_ctx *ctx, const void *src, in
                                          const int64_t *send_order, const int32_t *counts, void *dst, void *stream) {
     AC_NVTX("attncache_relocate_rows");
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "relocate_rows: ctx is NULL");
+    if (ctx->comm_failed) return comm_failed_status();
     if (n_home < 0 || row_bytes <= 0 || row_bytes % 8)
         return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "relocate_rows: n_home=%lld row_bytes=%lld (a multiple of 8)",
                     (long long)n_home, (long long)row_bytes);

@@ -131,10 +131,14 @@ ncclResult_t ncclGetVersion(int *v) {
     return ncclSuccess;
 }
 const char *ncclGetErrorString(ncclResult_t r) { return r == ncclSuccess ? "no error" : "fake_nccl error"; }
+// FAKE_NCCL_ASYNC_ERROR=1 makes every communicator report an asynchronous error (the library's abort path)
 ncclResult_t ncclCommGetAsyncError(ncclComm_t, ncclResult_t *e) {
-    *e = ncclSuccess;
+    const char *f = getenv("FAKE_NCCL_ASYNC_ERROR");
+    *e = (f && *f == '1') ? ncclRemoteError : ncclSuccess;
     return ncclSuccess;
 }
+int g_aborts = 0;  // read by the tests through fake_nccl_abort_count()
+int fake_nccl_abort_count() { return g_aborts; }
 
 ncclResult_t ncclGetUniqueId(ncclUniqueId *id) {
     memset(id, 0, sizeof *id);
@@ -168,6 +172,15 @@ ncclResult_t ncclCommDestroy(ncclComm_t comm) {
     munmap(c->base, c->bytes);
     if (c->rank == 0) unlink(c->path);
     delete c;
+    return ncclSuccess;
+}
+
+// No barrier: the peers of an aborted communicator may be gone.
+ncclResult_t ncclCommAbort(ncclComm_t comm) {
+    FakeComm *c = reinterpret_cast<FakeComm *>(comm);
+    munmap(c->base, c->bytes);
+    delete c;
+    ++g_aborts;
     return ncclSuccess;
 }
 

@@ -69,3 +69,42 @@ def test_bench_reference_arm_n2(fake_nccl):
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
     lines = [json.loads(s) for s in r.stdout.splitlines() if s.startswith("{")]
     assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["value"] > 0
+
+
+_ABORT_SCRIPT = r"""
+import ctypes, os, torch
+import paper_2510_25979_b200 as ac
+ctx = ac.Context(0, 0, 1, ac.attncache_get_unique_id())            # collective ctx at world 1 (fake NCCL)
+x = torch.randn(4, 128, device="cuda")
+x = (x / x.norm(dim=1, keepdim=True)).to(torch.bfloat16)
+db = ac.Database(ctx, x)
+idx, score, hit = ac.attncache_search(db, x[:2], 0.5)
+ctx.sync()
+assert idx.tolist() == [0, 1], idx
+os.environ["FAKE_NCCL_ASYNC_ERROR"] = "1"                          # the communicator reports an async error
+codes = []
+for call in (ctx.sync, lambda: ac.attncache_search(db, x[:2], 0.5), ctx.sync):
+    try:
+        call()
+        codes.append(0)
+    except ac.AttnCacheError as e:
+        codes.append(e.status)
+    os.environ["FAKE_NCCL_ASYNC_ERROR"] = "0"                      # sticky: later calls fail without a new error
+fake = ctypes.CDLL(os.environ["ATTNCACHE_NCCL_LIB"])
+print("codes", codes, "aborts", fake.fake_nccl_abort_count())
+db.close()
+ctx.close()
+print("abort ok")
+"""
+
+
+@pytest.mark.gpu
+def test_async_nccl_error_aborts_the_communicator(fake_nccl):
+    """SURVEY.md §5 failure detection: an asynchronous NCCL error seen by attncache_ctx_sync aborts the
+    communicator (ncclCommAbort, once) and every later collective call returns ATTNCACHE_ERR_NCCL (11) instead of
+    waiting on it; the ctx and db can still be destroyed."""
+    env = dict(os.environ, ATTNCACHE_NCCL_LIB=fake_nccl)
+    r = subprocess.run([sys.executable, "-c", _ABORT_SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+    assert "codes [11, 11, 11] aborts 1" in r.stdout and "abort ok" in r.stdout, r.stdout
