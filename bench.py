@@ -817,9 +817,10 @@ def run_e2e(args, cfg, ctx, db, step, q, Q, K, V, dev, stream):
     return {"value": cfg.B * cfg.S / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms, "steps": n,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": "attncache_prefill_host (C ABI)",
             "copy_bound": _copy_bound(Vh, V, Qh[:n_miss], Q[:n_miss], Kh[:n_miss], K[:n_miss], Oh, ms),
-            "note": "pinned host buffers; one synchronous C-ABI call per step: chunk-pipelined copies (16 rows, "
-                    "4-deep ring, three library streams) overlapping the kernels; one mid-call D2H of the "
-                    "decisions"}
+            "chunk_rows": max(1, min(16, (192 << 20) // row)),
+            "note": "pinned host buffers; one synchronous C-ABI call per step: chunk-pipelined copies (chunk_rows "
+                    "rows, ~192 MB of V, 4-deep ring, three library streams) overlapping the kernels; one mid-call "
+                    "D2H of the decisions"}
 
 
 def _copy_bound(Vh, V, Qh, Q, Kh, K, Oh, e2e_ms, reps=3):

@@ -279,6 +279,8 @@ attncache_status attncache_attend_full_gqa(attncache_ctx *ctx, int64_t batch, in
  *   q: [n][feat_dim] feat dtype; Q, K, V, O: [n][n_layers][n_heads][seq_len][head_dim] act_dtype;
  *   idx int64 / score fp32 / hit uint8: [n].  Every pointer must be PAGE-LOCKED HOST memory
  *   (cudaHostAlloc / cudaHostRegister).  Device staging is ctx scratch.  A local db holding every entry.
+ *   chunk: rows per pipeline step; ~100-300 MB of V per chunk keeps the copy engines busy with a short ring
+ *   fill / drain (the Python binding's default: ~192 MB, at most 16 rows).
  * Errors: INVALID_ARGUMENT (pageable or device pointers, chunk <= 0, depth outside [2, 8], NaN tau), STATE
  * (a shard / a collective ctx of world > 1 / no maps), EMPTY, DTYPE, ALIGNMENT, CUDA. */
 attncache_status attncache_prefill_host(attncache_db *db, const void *q, int64_t n, float tau, const void *Q,

@@ -500,10 +500,13 @@ def attncache_attend_full_gqa(ctx: Context, Q, K, V, O=None, scale: float = 0.0,
 
 def attncache_prefill_host(db: Database, q: torch.Tensor, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor,
                            tau: float, O: Optional[torch.Tensor] = None, idx=None, score=None, hit=None,
-                           chunk: int = 16, depth: int = 4):
+                           chunk: Optional[int] = None, depth: int = 4):
     """The whole single-rank step end to end from PINNED host tensors (include/attncache.h
     attncache_prefill_host): every copy happens inside the library call, which returns when O and
-    idx/score/hit are in host memory.  q [B][D]; Q, K, V, O [B][L][H][S][d] (all layers of the DB)."""
+    idx/score/hit are in host memory.  q [B][D]; Q, K, V, O [B][L][H][S][d] (all layers of the DB).
+    chunk None: rows per pipeline chunk chosen for ~192 MB of V per chunk, at most 16 (a smaller chunk shortens
+    the ring's fill and drain: configs[2], 67 MB rows, 222 -> 209 ms per step from 16 to 2 rows;
+    scripts/e2e_chunk_sweep.py)."""
     ts = [(q, "q"), (Q, "Q"), (K, "K"), (V, "V")]
     for t, nme in ts:
         if t.is_cuda or not t.is_pinned() or not t.is_contiguous():
@@ -523,6 +526,8 @@ def attncache_prefill_host(db: Database, q: torch.Tensor, Q: torch.Tensor, K: to
                               (score, "score", torch.float32, (B,)), (hit, "hit", torch.uint8, (B,))):
         if t.is_cuda or not t.is_pinned() or not t.is_contiguous() or t.dtype != dt or tuple(t.shape) != tuple(shape):
             raise ValueError(f"{nme} must be a contiguous pinned host {dt} tensor of shape {tuple(shape)}")
+    if chunk is None:
+        chunk = max(1, min(16, (192 << 20) // max(1, V[0].numel() * V.element_size())))
     _check(load_library().attncache_prefill_host(db.handle, _p(q), B, float(tau), _p(Q), _p(K), _p(V), V.shape[4],
                                                  _DT[V.dtype], _p(O), _p(idx), _p(score), _p(hit), int(chunk),
                                                  int(depth)))
