@@ -118,7 +118,9 @@ attncache_status attncache_ctx_destroy(attncache_ctx *ctx);
  * asynchronous communicator error (ncclCommGetAsyncError).  On such an error the library aborts its
  * communicator (ncclCommAbort: no barrier with peers that may be gone) and the ctx stays failed: every
  * later collective call (search, apply_cached, relocate_rows, db_load) and ctx_sync return ERR_NCCL; the
- * caller destroys the ctx (and its dbs) and creates a new one.  SURVEY.md §5 failure detection. */
+ * caller destroys the ctx (and its dbs) and creates a new one.  Every host wait on collective work (this
+ * call, and the count exchanges inside search / apply_cached / db_load) polls that error while it waits, so a
+ * peer that died turns into ERR_NCCL instead of a wait that never ends.  SURVEY.md §5 failure detection. */
 attncache_status attncache_ctx_sync(attncache_ctx *ctx);
 
 /* The home batch size of every rank for the following collective calls (home_counts: host int64 [world];

@@ -15,6 +15,8 @@ attncache_status apply_local_impl(attncache_db *db, const int64_t *idx, const ui
 // collective.cu
 attncache_status comm_check(attncache_ctx *ctx);          // polls the async error; aborts the comm on one
 attncache_status comm_failed_status();                    // ERR_NCCL: the comm was aborted (see comm_check)
+// Host wait for `st` (marked_only: for the last collective work recorded, if any) polling the async NCCL error.
+attncache_status comm_wait(attncache_ctx *ctx, cudaStream_t st, bool marked_only);
 attncache_status db_load_collective(attncache_db *db);
 attncache_status search_collective(attncache_db *db, const void *q, int64_t n_home, float tau, bool all, int64_t *idx,
                                    float *score, uint8_t *hit, cudaStream_t st);

@@ -190,6 +190,7 @@ attncache_status attncache_ctx_destroy(attncache_ctx *ctx) {
     for (void *p : ctx->graph_owned) cudaFree(p);
     for (int i = 0; i < 3; ++i)
         if (ctx->io_stream[i]) cudaStreamDestroy(ctx->io_stream[i]);
+    if (ctx->comm_ev) cudaEventDestroy(ctx->comm_ev);
     delete ctx;
     return ATTNCACHE_OK;
 }
@@ -197,9 +198,12 @@ attncache_status attncache_ctx_destroy(attncache_ctx *ctx) {
 attncache_status attncache_ctx_sync(attncache_ctx *ctx) {
     if (!ctx) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "ctx_sync: ctx is NULL");
     DeviceGuard g(ctx->device);
-    AC_CUDA(cudaDeviceSynchronize());
-    attncache_status s = comm_check(ctx);
+    // the last collective work first, polling the communicator's async error (a dead peer would otherwise
+    // leave cudaDeviceSynchronize waiting forever)
+    attncache_status s = comm_wait(ctx, nullptr, true);
     if (s) return s;
+    AC_CUDA(cudaDeviceSynchronize());
+    if ((s = comm_check(ctx))) return s;
     int flags = 0;
     AC_CUDA(cudaMemcpy(&flags, ctx->d_error, sizeof(int), cudaMemcpyDeviceToHost));
     if (flags) {

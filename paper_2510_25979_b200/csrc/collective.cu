@@ -14,6 +14,7 @@
 #include <string.h>
 
 #include <numeric>
+#include <thread>
 
 #include "abi_internal.cuh"
 
@@ -92,6 +93,45 @@ attncache_status nccl_status(ncclResult_t r, const char *what) {
 
 inline ncclComm_t comm_of(const attncache_ctx *ctx) { return (ncclComm_t)ctx->comm; }
 
+// Records the completion of the NCCL work just enqueued on `st` (attncache_ctx_sync polls it; see comm_wait).
+attncache_status comm_mark(attncache_ctx *ctx, cudaStream_t st) {
+    if (!ctx->comm_ev) AC_CUDA(cudaEventCreateWithFlags(&ctx->comm_ev, cudaEventDisableTiming));
+    AC_CUDA(cudaEventRecord(ctx->comm_ev, st));
+    ctx->comm_ev_pending = true;
+    return ATTNCACHE_OK;
+}
+
+}  // namespace
+
+// Host wait for the collective work on `st` (or, st == nullptr, for the last marked one) that polls the
+// communicator's asynchronous error while it waits: a peer that died leaves NCCL's kernels waiting forever, and
+// NCCL reports it only through ncclCommGetAsyncError.  On such an error comm_check aborts the
+// communicator, which also releases the waiting kernels, and the wait returns ATTNCACHE_ERR_NCCL.
+attncache_status comm_wait(attncache_ctx *ctx, cudaStream_t st, bool marked_only) {
+    if (!ctx->comm) {
+        if (!marked_only) AC_CUDA(cudaStreamSynchronize(st));
+        return ATTNCACHE_OK;
+    }
+    if (marked_only) {
+        if (!ctx->comm_ev_pending) return ATTNCACHE_OK;
+    } else {
+        attncache_status s = comm_mark(ctx, st);
+        if (s) return s;
+    }
+    for (;;) {
+        const cudaError_t q = cudaEventQuery(ctx->comm_ev);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) AC_CUDA(q);
+        attncache_status s = comm_check(ctx);
+        if (s) return s;
+        std::this_thread::yield();
+    }
+    ctx->comm_ev_pending = false;
+    return ATTNCACHE_OK;
+}
+
+namespace {
+
 // Rows of `row_bytes` bytes from every rank to every rank: rank r sends send_n[p] rows starting at row
 // send_off[p] of `send` to peer p, and receives recv_n[p] rows from p at row recv_off[p] of `recv` (one NCCL
 // group of send/recv pairs; moved as bytes, so any dtype).
@@ -109,7 +149,7 @@ attncache_status exchange_rows(attncache_ctx *ctx, const void *send, const int64
                             comm_of(ctx), st));
     }
     AC_NCCL(N->GroupEnd());
-    return ATTNCACHE_OK;
+    return comm_mark(ctx, st);
 }
 
 // The home batch size of every rank: the declared layout, or one all-gather of the int64 counts and a host
@@ -126,9 +166,10 @@ attncache_status home_counts(attncache_ctx *ctx, int64_t n_home, cudaStream_t st
     ctx->h_pinned[0] = n_home;
     AC_CUDA(cudaMemcpyAsync(ctx->d_small, ctx->h_pinned, sizeof(int64_t), cudaMemcpyHostToDevice, st));
     AC_NCCL(N->AllGather(ctx->d_small, ctx->d_small + 8, 1, ncclInt64, comm_of(ctx), st));
+    if (attncache_status s = comm_mark(ctx, st)) return s;
     AC_CUDA(cudaMemcpyAsync(ctx->h_pinned + 8, ctx->d_small + 8, sizeof(int64_t) * ctx->world, cudaMemcpyDeviceToHost,
                             st));
-    AC_CUDA(cudaStreamSynchronize(st));
+    if (attncache_status s = comm_wait(ctx, st, false)) return s;
     out.assign(ctx->h_pinned + 8, ctx->h_pinned + 8 + ctx->world);
     return ATTNCACHE_OK;
 }
@@ -193,8 +234,9 @@ attncache_status db_load_collective(attncache_db *db) {
         cudaStream_t st = 0;
         AC_CUDA(cudaMemcpyAsync(ctx->d_small, ctx->h_pinned, sizeof mine, cudaMemcpyHostToDevice, st));
         AC_NCCL(nccl()->AllGather(ctx->d_small, ctx->d_small + kF, kF, ncclInt64, comm_of(ctx), st));
+        if (attncache_status s = comm_mark(ctx, st)) return s;
         AC_CUDA(cudaMemcpyAsync(ctx->h_pinned + kF, ctx->d_small + kF, sizeof(int64_t) * kF * w, cudaMemcpyDeviceToHost, st));
-        AC_CUDA(cudaStreamSynchronize(st));
+        if (attncache_status s = comm_wait(ctx, st, false)) return s;
         int64_t next = 0;
         for (int r = 0; r < w; ++r) {
             const int64_t *f = ctx->h_pinned + kF * (r + 1);
@@ -245,6 +287,7 @@ attncache_status search_collective(attncache_db *db, const void *q, int64_t n_ho
     for (int r = 1; r < w; ++r) equal = equal && cnt[r] == cnt[0];
     if (equal) {
         AC_NCCL(N->AllGather(q, q_all, row * (size_t)n_home, ncclUint8, comm_of(ctx), st));
+        if (attncache_status s = comm_mark(ctx, st)) return s;
     } else {
         std::vector<int64_t> sn(w, n_home), so(w, 0);
         if ((s = exchange_rows(ctx, q, sn.data(), so.data(), q_all, cnt.data(), off.data(), row, st))) return s;
@@ -253,6 +296,7 @@ attncache_status search_collective(attncache_db *db, const void *q, int64_t n_ho
     if ((s = search_keys_impl(db, q_all, total, (uint64_t *)keys, st))) return s;
     // C2: max over shards of the packed keys = the global top-1 with the lowest-index tie-break (reading R3)
     AC_NCCL(N->AllReduce(keys, keys, (size_t)total, ncclUint64, ncclMax, comm_of(ctx), st));
+    if (attncache_status s = comm_mark(ctx, st)) return s;
     // K2: decode + tau gate (the home block, or the whole batch)
     const int64_t b0 = all ? 0 : off[ctx->rank], n = all ? total : n_home;
     if (n) AC_CUDA(launch_keys_decode((const uint64_t *)keys + b0, 1, n, tau, idx, score, hit, st));
@@ -296,9 +340,10 @@ attncache_status apply_routed(attncache_db *db, const int64_t *idx, const uint8_
         AC_NCCL(N->Recv(recv_counts + p, 1, ncclInt32, p, comm_of(ctx), st));
     }
     AC_NCCL(N->GroupEnd());
+    if (attncache_status s = comm_mark(ctx, st)) return s;
     int32_t *hc = (int32_t *)(ctx->h_pinned + kPinnedInts / 2);
     AC_CUDA(cudaMemcpyAsync(hc, counts, sizeof(int32_t) * 2 * w, cudaMemcpyDeviceToHost, st));
-    AC_CUDA(cudaStreamSynchronize(st));
+    if (attncache_status s = comm_wait(ctx, st, false)) return s;
     std::vector<int64_t> sn(w), rn(w), so(w + 1, 0), ro(w + 1, 0);
     for (int p = 0; p < w; ++p) {
         sn[p] = hc[p];

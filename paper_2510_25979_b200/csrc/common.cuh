@@ -139,6 +139,8 @@ struct attncache_ctx {
     int rank = 0, world = 1;
     void *comm = nullptr;            // ncclComm_t
     bool comm_failed = false;        // the comm was aborted after an asynchronous NCCL error (comm_check)
+    cudaEvent_t comm_ev = nullptr;   // completion of the last collective work enqueued (comm_wait polls it)
+    bool comm_ev_pending = false;
     int64_t *h_pinned = nullptr;     // pinned host staging for counts (kPinnedInts int64)
     int64_t *d_small = nullptr;      // device staging for small exchanges (kPinnedInts int64)
     std::vector<int64_t> layout;     // the per-rank home batch sizes set by attncache_set_batch_layout (or empty)
