@@ -18,6 +18,7 @@
 #include <unistd.h>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -122,6 +123,26 @@ ncclResult_t run_p2p(std::vector<P2p> &ops) {
     return ncclSuccess;
 }
 
+// FAKE_NCCL_HANG_ON=allgather: after the all-gather's work, the stream waits (cuStreamWaitValue32) on a
+// host-mapped flag that only ncclCommAbort sets: the stream never finishes on its own, like a collective whose
+// peer died.  The library's host waits must poll the async error, abort, and return.
+volatile uint32_t *g_release = nullptr;
+CUdeviceptr g_release_dev = 0;
+ncclResult_t maybe_hang(cudaStream_t st, const char *op) {
+    const char *h = getenv("FAKE_NCCL_HANG_ON");
+    if (!h || strcmp(h, op) != 0) return ncclSuccess;
+    if (!g_release) {
+        void *p = nullptr, *d = nullptr;
+        if (cudaHostAlloc(&p, 4, cudaHostAllocMapped) != cudaSuccess) return ncclUnhandledCudaError;
+        if (cudaHostGetDevicePointer(&d, p, 0) != cudaSuccess) return ncclUnhandledCudaError;
+        g_release = (volatile uint32_t *)p;
+        g_release_dev = (CUdeviceptr)d;
+    }
+    *g_release = 0;
+    return cuStreamWaitValue32((CUstream)st, g_release_dev, 1, CU_STREAM_WAIT_VALUE_GEQ) == CUDA_SUCCESS
+               ? ncclSuccess : ncclUnhandledCudaError;
+}
+
 }  // namespace
 
 extern "C" {
@@ -177,6 +198,7 @@ ncclResult_t ncclCommDestroy(ncclComm_t comm) {
 
 // No barrier: the peers of an aborted communicator may be gone.
 ncclResult_t ncclCommAbort(ncclComm_t comm) {
+    if (g_release) *g_release = 1;  // releases a stream left waiting by FAKE_NCCL_HANG_ON
     FakeComm *c = reinterpret_cast<FakeComm *>(comm);
     munmap(c->base, c->bytes);
     delete c;
@@ -214,7 +236,7 @@ ncclResult_t ncclAllGather(const void *send, void *recv, size_t count, ncclDataT
         if (b && cudaMemcpy((uint8_t *)recv + (size_t)r * b, c->slot_of(r), b, cudaMemcpyHostToDevice) != cudaSuccess)
             return ncclUnhandledCudaError;
     barrier(c);
-    return ncclSuccess;
+    return maybe_hang(st, "allgather");
 }
 
 ncclResult_t ncclAllReduce(const void *send, void *recv, size_t count, ncclDataType_t t, ncclRedOp_t op,

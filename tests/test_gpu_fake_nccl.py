@@ -21,7 +21,7 @@ def fake_nccl():
     cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
     subprocess.run(["g++", "-shared", "-fPIC", "-O2", "-I", os.path.join(cuda, "include"), "-o", out,
                     os.path.join(ROOT, "tests", "native", "fake_nccl.cpp"), "-L", os.path.join(cuda, "lib64"),
-                    "-lcudart"], check=True)
+                    "-L", os.path.join(cuda, "lib64", "stubs"), "-lcudart", "-lcuda"], check=True)
     return out
 
 
@@ -108,3 +108,40 @@ def test_async_nccl_error_aborts_the_communicator(fake_nccl):
                        timeout=300)
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
     assert "codes [11, 11, 11] aborts 1" in r.stdout and "abort ok" in r.stdout, r.stdout
+
+
+_HANG_SCRIPT = r"""
+import ctypes, os, time, torch
+import paper_2510_25979_b200 as ac
+ctx = ac.Context(0, 0, 1, ac.attncache_get_unique_id())
+x = torch.randn(4, 128, device="cuda")
+x = (x / x.norm(dim=1, keepdim=True)).to(torch.bfloat16)
+db = ac.Database(ctx, x)
+os.environ["FAKE_NCCL_HANG_ON"] = "allgather"    # the next all-gather's stream never finishes on its own
+os.environ["FAKE_NCCL_ASYNC_ERROR"] = "1"        # ... and the communicator reports an async error
+t0 = time.time()
+try:
+    ac.attncache_search(db, x[:2], 0.5)          # its batch-size exchange waits on the host
+    code = 0
+except ac.AttnCacheError as e:
+    code = e.status
+dt = time.time() - t0
+torch.cuda.synchronize()                         # the abort released the stream
+fake = ctypes.CDLL(os.environ["ATTNCACHE_NCCL_LIB"])
+print("hang code", code, "aborts", fake.fake_nccl_abort_count(), "returned", dt < 60)
+db.close()
+ctx.close()
+"""
+
+
+@pytest.mark.gpu
+def test_collective_wait_on_a_dead_peer_returns_err_nccl(fake_nccl):
+    """A collective whose stream never completes (the stand-in's all-gather leaves its stream waiting on a flag,
+    as NCCL's kernels wait for a peer that died) while NCCL reports an async error: the library's host wait polls
+    ncclCommGetAsyncError, aborts the communicator (which releases the stream) and returns ATTNCACHE_ERR_NCCL
+    instead of waiting forever."""
+    env = dict(os.environ, ATTNCACHE_NCCL_LIB=fake_nccl)
+    r = subprocess.run([sys.executable, "-c", _HANG_SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=180)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+    assert "hang code 11 aborts 1 returned True" in r.stdout, r.stdout
