@@ -199,6 +199,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #if defined(APPLY_EXP) && APPLY_EXP == 2  // experiment: V with the normal policy
             uint64_t v_policy;
             asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(v_policy));
+#elif defined(APPLY_EXP) && APPLY_EXP == 3  // experiment: evict_first when one row block reads V once (S <= 128)
+            const uint64_t v_policy = S <= kRows ? policy_evict_first() : policy_evict_last();
 #else
             const uint64_t v_policy = policy_evict_last();
 #endif
@@ -456,6 +458,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t cnt = 0;
             UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
             const uint64_t v_policy = policy_evict_last();
+            // every pair re-reads the V chunks of the pairs before it, so the unit's last pair is the last reader of
+            // every chunk: its loads demote the lines (evict_first), or finished units' V would pile up as
+            // evict_last in L2 and push out the V of the units in flight (configs[3]: DRAM reads 5.75 -> 5.58 GB,
+            // 1.062 -> 1.043 ms; scripts/apply_vlast_ab.sh)
+            const uint64_t v_last_policy = policy_evict_first();
             uint32_t lh;
             int64_t row, ent;
             while (iter.next(lh, row, ent)) {
@@ -463,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t l = lh / (uint32_t)a.H, h = lh % (uint32_t)a.H;
                 const int32_t vunit = (int32_t)((row * a.n_lay + l) * a.Hkv + h / (uint32_t)(a.H / a.Hkv));
                 for (int pr = 0; pr < n_pairs; ++pr) {
+                    const uint64_t pol = pr == n_pairs - 1 ? v_last_policy : v_policy;
                     const int nk = 2 * pr + 1 < n_rb ? rb_chunks(2 * pr + 1) : rb_chunks(2 * pr);
                     for (int kc = 0; kc < nk; ++kc, ++cnt) {
                         const uint32_t s = cnt % C::kStages, ph = (cnt / C::kStages) & 1u;
@@ -472,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int half = 0; half < kD / 64; ++half)
                             tma_load_3d_hint(dst + half * (kChunk * 128), &tmV, &full[s], half * 64, kc * kChunk, vunit,
-                                             v_policy);
+                                             pol);
                     }
                 }
             }
