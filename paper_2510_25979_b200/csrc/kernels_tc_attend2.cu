@@ -189,6 +189,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             Walker w;
             w.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
             uint32_t b = 0, it = 0;
+#if defined(ATT2_POL)  // experiment (scripts/attend_policy_ab.sh): Q read once -> evict_first; 2: K/V evict_last
+            const uint64_t pol_q = policy_evict_first();
+#if ATT2_POL == 2
+            const uint64_t pol_kv = policy_evict_last();
+#else
+            uint64_t pol_kv;
+            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_kv));
+#endif
+#define ATT2_LOAD_Q(dst, map, bar, c0, c1, c2) tma_load_3d_hint(dst, map, bar, c0, c1, c2, pol_q)
+#define ATT2_LOAD_KV(dst, map, bar, c0, c1, c2) tma_load_3d_hint(dst, map, bar, c0, c1, c2, pol_kv)
+#else
+#define ATT2_LOAD_Q(dst, map, bar, c0, c1, c2) tma_load_3d(dst, map, bar, c0, c1, c2)
+#define ATT2_LOAD_KV(dst, map, bar, c0, c1, c2) tma_load_3d(dst, map, bar, c0, c1, c2)
+#endif
             while (w.active) {
                 AC_STRESS_DELAY(716u);
                 if (w.j == 0) {
@@ -196,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&q_empty[qs], ((it / kNQ) & 1u) ^ 1u);
                     mbar_arrive_expect_tx(&q_full[qs], kTile);
                     for (int h = 0; h < 2; ++h)
-                        tma_load_3d(smem_u32(sQ + qs * kTile + h * (kBlk * 128)), &tmQ, &q_full[qs], h * 64,
+                        ATT2_LOAD_Q(smem_u32(sQ + qs * kTile + h * (kBlk * 128)), &tmQ, &q_full[qs], h * 64,
                                     w.qb * kBlk, w.unit);
                 }
                 const int32_t r_j = w.j * kBlk;
@@ -205,11 +219,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&k_empty[kk], kkph);
                 mbar_arrive_expect_tx(&k_full[kk], kTile);
                 for (int h = 0; h < 2; ++h)
-                    tma_load_3d(smem_u32(sK + kk * kTile + h * (kBlk * 128)), &tmK, &k_full[kk], h * 64, r_j, w.kv_unit);
+                    ATT2_LOAD_KV(smem_u32(sK + kk * kTile + h * (kBlk * 128)), &tmK, &k_full[kk], h * 64, r_j, w.kv_unit);
                 mbar_wait(&v_empty[vv], vvph);
                 mbar_arrive_expect_tx(&v_full[vv], kTile);
                 for (int h = 0; h < 2; ++h)
-                    tma_load_3d(smem_u32(sV + vv * kTile + h * (kBlk * 128)), &tmV, &v_full[vv], h * 64, r_j, w.kv_unit);
+                    ATT2_LOAD_KV(smem_u32(sV + vv * kTile + h * (kBlk * 128)), &tmV, &v_full[vv], h * 64, r_j, w.kv_unit);
                 ++b;
                 if (w.advance(sc)) ++it;
             }
