@@ -709,6 +709,75 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
     return float(ms.item()), extra, int(launches.item()), n_hit
 
 
+def _dist_e2e(args, cfg, ctx, db, dev, world, rank):
+    """The N > 1 end-to-end leg: each rank's home block of the batch from PINNED host memory through the
+    library's collective calls (dist.ShardedPrefill's search, then the routed A.V and the local attention), with
+    every host <-> device copy inside the timed region: H2D of the home queries and V, the decisions to the host
+    (one sync: only the misses' Q and K cross the host link, Alg. 2 l.376-378), H2D of those Q / K rows, then
+    D2H of O.  Routed placement (the request state never moves).  Wall clock of K steps, max over ranks."""
+    import torch.distributed as dist
+
+    from paper_2510_25979_b200.dist import ShardedPrefill, shard_range
+    import paper_2510_25979_b200 as ac
+    q_all, _, _ = synth.queries(cfg, dev)
+    hb, hc = shard_range(cfg.B, world, rank)
+    sizes = [shard_range(cfg.B, world, r)[1] for r in range(world)]
+    step = ShardedPrefill(ctx, db, cfg.tau, sizes)
+    qh = q_all[hb:hb + hc].contiguous().cpu().pin_memory()
+    Qh, Kh, Vh = (synth.activations(cfg, k, hb, hc, device=dev).cpu().pin_memory() for k in "qkv")
+    # O double-buffered: step i's D2H of O runs on a copy stream beside step i + 1's H2D and kernels
+    Ohs = [torch.empty(Vh.shape, dtype=Vh.dtype).pin_memory() for _ in range(2)]
+    dq, dQ, dK, dV = (torch.empty(t.shape, dtype=t.dtype, device=dev) for t in (qh, Qh, Kh, Vh))
+    dOs = [torch.empty_like(dV) for _ in range(2)]
+    comp, cs = torch.cuda.current_stream(dev), torch.cuda.Stream(dev)
+    out_done = [torch.cuda.Event(), torch.cuda.Event()]
+    row = Vh[0].numel() * Vh.element_size() if hc else 0
+    n_miss = [0]
+
+    def one(i):
+        dO, Oh = dOs[i % 2], Ohs[i % 2]
+        dq.copy_(qh, non_blocking=True)
+        dV.copy_(Vh, non_blocking=True)
+        idx, score, hit = step.search(dq)
+        miss = torch.nonzero(hit == 0).flatten().cpu()  # the decisions to the host (one sync of this stream)
+        n_miss[0] = miss.numel()
+        for m in miss.tolist():  # only the misses' Q and K cross the host link
+            dQ[m].copy_(Qh[m], non_blocking=True)
+            dK[m].copy_(Kh[m], non_blocking=True)
+        comp.wait_event(out_done[i % 2])  # the D2H of step i - 2 has read this O buffer
+        step.apply_routed(idx, hit, dV, dO)
+        if miss.numel():
+            ac.attncache_attend_full(ctx, dQ, dK, dV, dO, skip=hit)
+        cs.wait_stream(comp)
+        with torch.cuda.stream(cs):
+            Oh.copy_(dO, non_blocking=True)
+            out_done[i % 2].record(cs)
+
+    for i in range(max(1, args.warmup)):
+        one(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    n = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for i in range(n):
+        one(i)
+    torch.cuda.synchronize()  # the last step's O is in host memory
+    ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / n], device=_RDEV)
+    dist.barrier()
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    h2d = torch.tensor([qh.numel() * qh.element_size() + Vh.numel() * Vh.element_size() + 2 * n_miss[0] * row],
+                       device=_RDEV, dtype=torch.float64)
+    d2h = torch.tensor([Ohs[0].numel() * Ohs[0].element_size() + hc * 13], device=_RDEV, dtype=torch.float64)
+    dist.all_reduce(h2d)
+    dist.all_reduce(d2h)
+    return {"value": cfg.B * cfg.S / (float(ms.item()) * 1e-3), "unit": "tokens/s", "ms_per_step": float(ms.item()),
+            "steps": n, "h2d_bytes_per_step": int(h2d.item()), "d2h_bytes_per_step": int(d2h.item()),
+            "api": "dist.ShardedPrefill (attncache_search / attncache_apply_cached COLLECTIVE, attncache_attend_full)",
+            "note": "pinned host buffers per rank, routed placement, global batch of the line's B (bytes summed "
+                    "over ranks); O double-buffered so a step's D2H overlaps the next step's H2D; wall clock of K "
+                    "steps ending when the last O is in host memory, max over ranks"}
+
+
 def run_dist(args, cfg):
     """N > 1 (torchrun, one process per GPU): the DB is sharded by contiguous entry ranges over the GPUs and
     every exchange runs inside libattncache over its own NCCL communicator (torch.distributed only
@@ -759,6 +828,8 @@ def run_dist(args, cfg):
         c = cfg.with_(B=cfg.B * world) if mode == "weak" else cfg
         runs[mode] = (c,) + _dist_timed(args, c, ac, ctx, db, dev, args.placement, world, rank, local)
     clk = clocks.stop()
+    e2e_cfg = runs[args.scaling][0]
+    e2e = _dist_e2e(args, e2e_cfg, ctx, db, dev, world, rank)
     ctx.sync()
     if rank == 0:
         c, ms, extra, launches, n_hit = runs[args.scaling]
@@ -781,8 +852,7 @@ def run_dist(args, cfg):
                 "roofline": {"bound": "hbm", "achieved": None, "peak": _peaks()["hbm_gbs"] * world, "unit": "GB/s",
                              "frac": None, "traffic": None,
                              "note": "multi-GPU line: per-kernel roofline is reported by the N=1 run"},
-                "e2e": {"value": None, "unit": "tokens/s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
-                        "note": "end-to-end host-buffer timing is reported by the N=1 run"}}
+                "e2e": e2e}
         print(json.dumps(line), flush=True)
     del db
     ctx.close()

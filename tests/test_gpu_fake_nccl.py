@@ -56,6 +56,7 @@ def test_bench_n2_line_fake_nccl_one_gpu(fake_nccl, placement, gpus, scaling):
     assert line["n_gpus"] == gpus and line["value"] > 0 and line["scaling"] == scaling
     assert line["other_scaling"]["ms_per_step"] > 0 and line["gpu_launches"] > 0
     assert line["config"]["placement"] == placement
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
 
 
 @pytest.mark.gpu
