@@ -656,7 +656,16 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
             # batch, so every step does one batch's search, placement, relocation and layers; the step ends when
             # all three streams are done.
             cur = state["plan"]
-            step.apply_local(cur, loc, V, O, Q, K)
+            if state.get("timing") is not None:  # events around the local A.V (the line's roofline kernel)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(comp)
+                step.apply_local(cur, loc, V, O)
+                e1.record(comp)
+                state["timing"].append((e0, e1))
+                if loc.numel():
+                    ac.attncache_attend_full(ctx, Q, K, V, O, skip=cur["hit_loc"])
+            else:
+                step.apply_local(cur, loc, V, O, Q, K)
             for t in (cur["idx_loc"], cur["hit_loc"]):  # made on the plan stream, read here (caching allocator)
                 t.record_stream(comp)
             nxt = step.plan(q, stream=plan_st)
@@ -676,6 +685,8 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = ac.attncache_launch_count()
+    if placement == "affinity":
+        state["timing"] = []
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(comp)
     for _ in range(args.steps):
@@ -694,7 +705,10 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
         per_rank = torch.tensor([loc.numel()], device=_RDEV)
         gathered = [torch.empty_like(per_rank) for _ in range(world)]
         dist.all_gather(gathered, per_rank)
-        extra = {"sm_budget": {"compute_sms": budget[0], "aux_sms": budget[1]},
+        av_ms = sum(a.elapsed_time(b) for a, b in state["timing"]) / max(1, len(state["timing"]))
+        n_hit_loc = int(res["hit_loc"].sum().item()) if loc.numel() else 0
+        extra = {"_av": (av_ms, n_hit_loc * apply_bytes_per_hit(cfg)),
+                 "sm_budget": {"compute_sms": budget[0], "aux_sms": budget[1]},
                  "queries_per_rank": [int(t.item()) for t in gathered],
                  "plan_load_bytes_per_rank": [float(v) for v in res["load"].tolist()],
                  "relocated_bytes_per_query": cfg.S * cfg.H * cfg.d * 2,
@@ -838,6 +852,19 @@ def run_dist(args, cfg):
                ("owner-affinity placement: hits on the owner, misses on the least-loaded GPUs, request state "
                 "moved once, all layers local" if args.placement == "affinity" else
                 "hits routed to the owner (V out, O back by grouped NCCL send/recv inside apply_cached)"))
+        av = extra.pop("_av", None)
+        oextra.pop("_av", None)
+        if av and av[0] > 0 and av[1] > 0:
+            ach = av[1] / (av[0] * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": _peaks()["hbm_gbs"], "unit": "GB/s",
+                    "frac": ach / _peaks()["hbm_gbs"], "traffic": None,
+                    "note": "rank 0's local A.V (attncache_apply_cached_local): its hits' algorithmic bytes / the "
+                            "launch's average CUDA-event duration on the compute stream, inside the timed steps; "
+                            "peak per GPU"}
+        else:
+            roof = {"bound": "hbm", "achieved": None, "peak": _peaks()["hbm_gbs"], "unit": "GB/s", "frac": None,
+                    "traffic": None, "note": "routed placement (the A.V call includes the exchanges) or no local "
+                                             "hit on rank 0: the per-kernel roofline is the N = 1 run's"}
         line = {"metric": METRIC, "value": c.B * c.S / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": args.scaling, "vs_baseline": None, "dtype": cfg.act_dtype,
@@ -849,9 +876,7 @@ def run_dist(args, cfg):
                 "other_scaling": {"scaling": "strong" if args.scaling == "weak" else "weak", "B": oc.B,
                                   "ms_per_step": oms, "value": oc.B * oc.S / (oms * 1e-3), "hits": on_hit},
                 "gpu_launches": launches, "clocks": clk,
-                "roofline": {"bound": "hbm", "achieved": None, "peak": _peaks()["hbm_gbs"] * world, "unit": "GB/s",
-                             "frac": None, "traffic": None,
-                             "note": "multi-GPU line: per-kernel roofline is reported by the N=1 run"},
+                "roofline": roof,
                 "e2e": e2e}
         print(json.dumps(line), flush=True)
     del db
