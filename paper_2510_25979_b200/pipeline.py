@@ -120,8 +120,9 @@ class HostPrefill:
     of O over a ring of `depth` device slots on three library streams.  Synchronous: when the call returns,
     O_h and the returned idx/score/hit (pinned host tensors) hold the results."""
 
-    def __init__(self, step: PrefillStep, chunk: int = 16, depth: int = 4):
-        self.step, self.chunk, self.depth = step, int(chunk), int(depth)
+    def __init__(self, step: PrefillStep, chunk: Optional[int] = None, depth: int = 4):
+        # chunk None: ~192 MB of V per pipeline chunk (attncache_prefill_host's default)
+        self.step, self.chunk, self.depth = step, None if chunk is None else int(chunk), int(depth)
         self._out = {}
 
     def __call__(self, q_h, Q_h, K_h, V_h, O_h):
