@@ -31,12 +31,16 @@ constexpr int kThreads = 384;  // 3 warpgroups: producers (warps 0-3), softmax g
 constexpr int kBlk = 128;                 // queries per item = keys per block
 constexpr float kRescaleThreshold = 8.f;  // log2 units: P <= 2^8 between rescales
 
+#ifndef ATT_DEPTH
+#define ATT_DEPTH 1
+#endif
 template <int kD>
 struct Cfg {
     static constexpr int kTile = kBlk * kD * 2;       // one [128][d] 16-bit tile
-    static constexpr int kQSlots = 1;                 // per stream
-    static constexpr int kK = 2;                      // K: one slot per group
-    static constexpr int kV = 2;                      // V: one slot per group
+    static constexpr int kDepth = kD == 64 ? ATT_DEPTH : 1;  // Q / K / V slots per group
+    static constexpr int kQSlots = kDepth;            // per stream
+    static constexpr int kK = 2 * kDepth;             // K: kDepth slots per group
+    static constexpr int kV = 2 * kDepth;             // V: kDepth slots per group
     static constexpr int kOutWarp = 32 * 64 * 2;     // per softmax warp: O staging [32 rows][64 cols] (128B swizzle)
     static constexpr int kSmem = (2 * kQSlots + kK + kV) * kTile + 8 * kOutWarp + 1024 + 512;
     static constexpr uint32_t kTmemCols = 512;        // S/P: 2 x 128 at 0; O: 2 x d at 256
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                      const AttendArgs a, const uint32_t idesc_s, const uint32_t idesc_pv) {
     using C = Cfg<kD>;
-    constexpr int NQ = C::kQSlots, NK = C::kK, NV = C::kV;
+    constexpr int NQ = C::kQSlots, NK = C::kK, NV = C::kV, DP = C::kDepth;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t *sQ = smem;                    // [2 streams][NQ][tile]
@@ -224,36 +228,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t b = 0, it = 0;  // key blocks and items of this stream
             if ((warp & 1) == 0) {
                 // ------------------------------ TMA loader of group g ----------------------------
-                const uint32_t q_s = smem_u32(sQ + g * C::kTile), k_s = smem_u32(sK + g * C::kTile);
-                const uint32_t v_s = smem_u32(sV + g * C::kTile);
                 while (st.active) {
                     AC_STRESS_DELAY(137u);
                     const int32_t r_j = st.j * kBlk;
                     if (st.j == 0) {
-                        mbar_wait(&q_empty[g], (it & 1u) ^ 1u);
-                        mbar_arrive_expect_tx(&q_full[g], C::kTile);
+                        const uint32_t qs = g * DP + it % DP, q_s = smem_u32(sQ + qs * C::kTile);
+                        mbar_wait(&q_empty[qs], ((it / DP) & 1u) ^ 1u);
+                        mbar_arrive_expect_tx(&q_full[qs], C::kTile);
                         for (int h = 0; h < kD / 64; ++h) {
                             if constexpr (k3D)
-                                tma_load_3d(q_s + h * (kBlk * 128), &tmQ, &q_full[g], h * 64, st.qb * kBlk, st.unit);
+                                tma_load_3d(q_s + h * (kBlk * 128), &tmQ, &q_full[qs], h * 64, st.qb * kBlk, st.unit);
                             else
-                                tma_load_2d(q_s + h * (kBlk * 128), &tmQ, &q_full[g], h * 64, st.unit * S + st.qb * kBlk);
+                                tma_load_2d(q_s + h * (kBlk * 128), &tmQ, &q_full[qs], h * 64, st.unit * S + st.qb * kBlk);
                         }
                     }
-                    mbar_wait(&k_empty[g], (b & 1u) ^ 1u);
-                    mbar_arrive_expect_tx(&k_full[g], C::kTile);
+                    const uint32_t ks = g * DP + b % DP, k_s = smem_u32(sK + ks * C::kTile);
+                    const uint32_t v_s = smem_u32(sV + ks * C::kTile);
+                    mbar_wait(&k_empty[ks], ((b / DP) & 1u) ^ 1u);
+                    mbar_arrive_expect_tx(&k_full[ks], C::kTile);
                     for (int h = 0; h < kD / 64; ++h) {
                         if constexpr (k3D)
-                            tma_load_3d(k_s + h * (kBlk * 128), &tmK, &k_full[g], h * 64, r_j, st.kv_unit);
+                            tma_load_3d(k_s + h * (kBlk * 128), &tmK, &k_full[ks], h * 64, r_j, st.kv_unit);
                         else
-                            tma_load_2d(k_s + h * (kBlk * 128), &tmK, &k_full[g], h * 64, st.kv_unit * S + r_j);
+                            tma_load_2d(k_s + h * (kBlk * 128), &tmK, &k_full[ks], h * 64, st.kv_unit * S + r_j);
                     }
-                    mbar_wait(&v_empty[g], (b & 1u) ^ 1u);
-                    mbar_arrive_expect_tx(&v_full[g], C::kTile);
+                    mbar_wait(&v_empty[ks], ((b / DP) & 1u) ^ 1u);
+                    mbar_arrive_expect_tx(&v_full[ks], C::kTile);
                     for (int h = 0; h < kD / 64; ++h) {
                         if constexpr (k3D)
-                            tma_load_3d(v_s + h * (kBlk * 128), &tmV, &v_full[g], h * 64, r_j, st.kv_unit);
+                            tma_load_3d(v_s + h * (kBlk * 128), &tmV, &v_full[ks], h * 64, r_j, st.kv_unit);
                         else
-                            tma_load_2d(v_s + h * (kBlk * 128), &tmV, &v_full[g], h * 64, st.kv_unit * S + r_j);
+                            tma_load_2d(v_s + h * (kBlk * 128), &tmV, &v_full[ks], h * 64, st.kv_unit * S + r_j);
                     }
                     ++b;
                     if (st.advance()) ++it;
@@ -262,15 +267,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // ------------------------------ MMA issuer of group g ----------------------------
                 // S_j overwrites the S/P columns PV_{j-1} reads: tcgen05.mma ops of one thread execute in
                 // issue order (the tcgen05 pipeline), so S_j is issued right behind PV_{j-1}.
-                const uint32_t q_b = smem_u32(sQ + g * C::kTile), k_b = smem_u32(sK + g * C::kTile);
-                const uint32_t v_b = smem_u32(sV + g * C::kTile);
                 const uint32_t s_t = tmem + g * kBlk, o_t = tmem + 256 + g * kD;
                 while (st.active) {
                     AC_STRESS_DELAY(17u);
                     const int j = st.j;
+                    const uint32_t qs = g * DP + it % DP, ks = g * DP + b % DP;
+                    const uint32_t q_b = smem_u32(sQ + qs * C::kTile), k_b = smem_u32(sK + ks * C::kTile);
+                    const uint32_t v_b = smem_u32(sV + ks * C::kTile);
                     ATT_TRACE_MMA(b * 2 + g, 0);
-                    if (j == 0) mbar_wait(&q_full[g], it & 1u);
-                    mbar_wait(&k_full[g], b & 1u);
+                    if (j == 0) mbar_wait(&q_full[qs], (it / DP) & 1u);
+                    mbar_wait(&k_full[ks], (b / DP) & 1u);
                     ATT_TRACE_MMA(b * 2 + g, 1);
                     tc_fence_after();
                     if constexpr (kD == 128) {  // 8 K-steps of 16 over two 64-column swizzle halves
@@ -283,17 +289,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      smem_desc(k_b + k * 32, 16, 1024, kSwizzle128B), idesc_s, k != 0);
                     }
                     umma_commit(&s_full[g]);
-                    umma_commit(&k_empty[g]);
-                    if (j == st.qb) umma_commit(&q_empty[g]);
+                    umma_commit(&k_empty[ks]);
+                    if (j == st.qb) umma_commit(&q_empty[qs]);
                     ATT_TRACE_MMA(b * 2 + g, 2);
                     mbar_wait(&p_full[g], b & 1u);
                     ATT_TRACE_MMA(b * 2 + g, 4);
-                    mbar_wait(&v_full[g], b & 1u);
+                    mbar_wait(&v_full[ks], (b / DP) & 1u);
                     ATT_TRACE_MMA(b * 2 + g, 5);
                     tc_fence_after();
                     // A = P (8 TMEM columns = 16 keys per step), B = V MN-major: 8 steps in one statement
                     umma_f16_ts_k8(o_t, s_t, smem_desc(v_b, kBlk * 128, 1024, kSwizzle128B), idesc_pv, j == 0 ? 0u : 1u);
-                    umma_commit(&v_empty[g]);
+                    umma_commit(&v_empty[ks]);
                     umma_commit(&pv_done[g]);
                     ATT_TRACE_MMA(b * 2 + g, 6);
                     ++b;
