@@ -37,8 +37,9 @@ attncache_status cuda_status(cudaError_t e, const char *what) {
     return fail(ATTNCACHE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-attncache_status scratch(attncache_ctx *ctx, cudaStream_t st, int kind, size_t bytes, void **out) {
+attncache_status scratch(attncache_ctx *ctx, cudaStream_t st, int kind, size_t bytes, void **out, bool *fresh) {
     *out = nullptr;
+    if (fresh) *fresh = false;
     if (bytes == 0) bytes = 16;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     AC_CUDA(cudaStreamIsCapturing(st, &cs));
@@ -54,6 +55,7 @@ attncache_status scratch(attncache_ctx *ctx, cudaStream_t st, int kind, size_t b
         if (e != cudaSuccess) return cuda_status(e, "scratch (graph capture)");
         ctx->graph_owned.push_back(p);
         *out = p;
+        if (fresh) *fresh = true;
         return ATTNCACHE_OK;
     }
     Scratch &s = ctx->scratch[st].s[kind];
@@ -65,6 +67,7 @@ attncache_status scratch(attncache_ctx *ctx, cudaStream_t st, int kind, size_t b
         const size_t cap = bytes < 4096 ? 4096 : bytes + bytes / 4;
         AC_CUDA(cudaMallocAsync(&s.ptr, cap, st));
         s.bytes = cap;
+        if (fresh) *fresh = true;
     }
     *out = s.ptr;
     return ATTNCACHE_OK;
@@ -347,6 +350,18 @@ static attncache_status search_common(attncache_db *db, const void *queries, int
                     "search_keys + keys_decode, or a ctx created with rank/world/uid", (long long)db->d.n_global);
     if (n == 0) return ATTNCACHE_OK;
     if (!idx || !score || !hit) return fail(ATTNCACHE_ERR_INVALID_ARGUMENT, "search: NULL output");
+    if (search_tc_supported(db->d.feat_dtype, db->d.feat_dim)) {
+        // K1 with K2 fused: the search kernel's last CTA to finish applies the gate and re-zeroes the keys for the
+        // next call (no memset and no decode launch per call; a fresh buffer is zeroed once)
+        void *buf = nullptr;
+        bool fresh = false;
+        if ((s = scratch(db->ctx, st, kScSearchFused, 16 + sizeof(uint64_t) * (size_t)n, &buf, &fresh))) return s;
+        if (fresh) AC_CUDA(cudaMemsetAsync(buf, 0, 16 + sizeof(uint64_t) * (size_t)n, st));
+        const SearchDecode dec{idx, score, hit, tau, (unsigned int *)buf};
+        AC_CUDA(launch_search_tc(queries, db->d.feats, n, db->d.shard_count, db->d.feat_dim, db->d.shard_begin,
+                                 (uint64_t *)((char *)buf + 16), db->ctx->aux_sms, st, &dec));
+        return ATTNCACHE_OK;
+    }
     void *keys = nullptr;
     if ((s = scratch(db->ctx, st, kScSearchKeys, sizeof(uint64_t) * (size_t)n, &keys))) return s;
     if ((s = search_keys_impl(db, queries, n, (uint64_t *)keys, st))) return s;

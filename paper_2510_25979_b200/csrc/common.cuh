@@ -93,6 +93,19 @@ __device__ __forceinline__ float ord_score(uint32_t o) {
 __device__ __forceinline__ uint64_t pack_key(float s, uint32_t gidx) {
     return ((uint64_t)score_ord(s) << 32) | (uint64_t)(0xFFFFFFFFu - gidx);
 }
+// K2: the tau gate on a (cross-shard maximum) key; key 0 = no entry anywhere (empty shards)
+__device__ __forceinline__ void decode_key(uint64_t k, float tau, int64_t *idx, float *score, uint8_t *hit) {
+    if (k == 0) {
+        *idx = -1;
+        *score = -INFINITY;
+        *hit = 0;
+    } else {
+        const float s = ord_score((uint32_t)(k >> 32));
+        *idx = (int64_t)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFu));
+        *score = s;
+        *hit = s >= tau ? 1 : 0;  // inclusive gate
+    }
+}
 
 // ---- scratch owned by a ctx -------------------------------------------------
 struct Scratch {
@@ -109,6 +122,7 @@ enum ScratchKind : int {
     kScApplyList = 0,  // compacted (row, entry) list for apply
     kScAttendList,     // compacted row list for attend / capture
     kScSearchKeys,     // per-query packed keys
+    kScSearchFused,    // single-GPU search with the decode fused in: arrival counter + keys, kept zero between calls
     kScProject,        // feature projector intermediates (z, y)
     kScPlan,           // device affinity plan: the miss list
     kScQueries,        // collective search: the gathered query batch
@@ -163,7 +177,8 @@ struct attncache_db {
 namespace ac {
 constexpr int kPinnedInts = 4 * 1024 + 16;  // small int64 staging (host pinned and device): world <= 1024
 // Device scratch of at least `bytes` for (stream, kind); see ScratchKind.
-attncache_status scratch(attncache_ctx *ctx, cudaStream_t st, int kind, size_t bytes, void **out);
+// fresh (optional): set when the returned buffer is newly allocated (its contents are undefined)
+attncache_status scratch(attncache_ctx *ctx, cudaStream_t st, int kind, size_t bytes, void **out, bool *fresh = nullptr);
 
 // A device pointer check: rejects host (unregistered or pinned) memory when the runtime can tell.
 inline bool is_device_ptr(const void *p) {

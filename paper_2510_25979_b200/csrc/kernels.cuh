@@ -28,8 +28,17 @@ cudaError_t launch_select_attend(const uint8_t *skip, int64_t n, RowList out, cu
 cudaError_t launch_search_ffma(int32_t dt, const void *q, const void *x, int64_t B, int64_t n, int32_t D,
                                int64_t gbase, uint64_t *keys, cudaStream_t st);
 bool search_tc_supported(int32_t dt, int32_t D);
+// K2 fused into the search kernel (single GPU): the last CTA to finish gates the keys into idx/score/hit and
+// re-zeroes them and the arrival counter `done` (both zero before the launch).
+struct SearchDecode {
+    int64_t *idx;
+    float *score;
+    uint8_t *hit;
+    float tau;
+    unsigned int *done;
+};
 cudaError_t launch_search_tc(const void *q, const void *x, int64_t B, int64_t n, int32_t D, int64_t gbase,
-                             uint64_t *keys, int sm_count, cudaStream_t st);
+                             uint64_t *keys, int sm_count, cudaStream_t st, const SearchDecode *dec = nullptr);
 cudaError_t launch_keys_decode(const uint64_t *keys, int32_t n_shards, int64_t n, float tau, int64_t *idx, float *score, uint8_t *hit,
                                cudaStream_t st);
 

@@ -177,16 +177,7 @@ __global__ void keys_decode_kernel(const uint64_t *keys, int n_shards, int64_t n
             uint64_t kr = keys[(int64_t)r * n + b];
             k = kr > k ? kr : k;
         }
-        if (k == 0) {  // no entry anywhere (empty shards)
-            idx[b] = -1;
-            score[b] = -INFINITY;
-            hit[b] = 0;
-        } else {
-            float s = ord_score((uint32_t)(k >> 32));
-            idx[b] = (int64_t)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFu));
-            score[b] = s;
-            hit[b] = s >= tau ? 1 : 0;  // inclusive gate
-        }
+        decode_key(k, tau, &idx[b], &score[b], &hit[b]);
     }
 }
 

@@ -34,7 +34,8 @@ struct Cfg {
 template <int kTileE>
 __global__ void __launch_bounds__(kThreads, 1)
     search_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX, int64_t B,
-                     int64_t n, int D, int64_t gbase, unsigned long long *keys, uint32_t idesc, uint32_t q_rows) {
+                     int64_t n, int D, int64_t gbase, unsigned long long *keys, uint32_t idesc, uint32_t q_rows,
+                     const SearchDecode dec) {
     using C = Cfg<kTileE>;
     constexpr int kStages = C::kStages, kStageBytes = C::kStageBytes;
     constexpr uint32_t kTmemCols = C::kTmemCols;
@@ -148,10 +149,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (b < B && bi >= 0) atomicMax(&keys[b], (unsigned long long)pack_key(best, (uint32_t)(gbase + e0 + bi)));
         }
     }
+    __threadfence();  // this thread's atomicMax results are visible device-wide before the CTA arrives
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
+    }
+    if (dec.done) {
+        // K2 fused (single GPU): the last CTA to arrive sees every CTA's keys, gates them and re-zeroes them (and
+        // the counter) for the next launch, which then needs neither a memset nor a decode launch
+        __shared__ unsigned int s_last;
+        if (threadIdx.x == 0) s_last = atomicAdd(dec.done, 1u) == gridDim.x - 1 ? 1u : 0u;
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
+                const unsigned long long k = atomicExch(&keys[b], 0ull);
+                decode_key(k, dec.tau, &dec.idx[b], &dec.score[b], &dec.hit[b]);
+            }
+            if (threadIdx.x == 0) *dec.done = 0u;
+        }
     }
 }
 
@@ -161,7 +178,7 @@ bool search_tc_supported(int32_t dt, int32_t D) { return dt == ATTNCACHE_BF16 &&
 
 template <int kTileE>
 static cudaError_t launch_t(const void *q, const void *x, int64_t B, int64_t n, int32_t D, int64_t gbase,
-                           uint64_t *keys, int sm_count, cudaStream_t st) {
+                           uint64_t *keys, int sm_count, cudaStream_t st, const SearchDecode *dec) {
     using C = Cfg<kTileE>;
     CUtensorMap tq, tx;
     const uint32_t q_rows = B >= kTileQ ? kTileQ : (uint32_t)((B + 7) / 8 * 8);
@@ -173,20 +190,21 @@ static cudaError_t launch_t(const void *q, const void *x, int64_t B, int64_t n, 
     const int64_t items = ((B + kTileQ - 1) / kTileQ) * ((n + kTileE - 1) / kTileE);
     const int grid = (int)min64(items, sm_count);
     const uint32_t idesc = idesc_f16(kTileQ, kTileE, 1u, 0u, 0u);
+    const SearchDecode d = dec ? *dec : SearchDecode{nullptr, nullptr, nullptr, 0.f, nullptr};
     search_tc_kernel<kTileE><<<grid, kThreads, C::kSmem, st>>>(tq, tx, B, n, D, gbase, (unsigned long long *)keys, idesc,
-                                                             q_rows);
+                                                             q_rows, d);
     count_launches(1);
     return cudaGetLastError();
 }
 
 cudaError_t launch_search_tc(const void *q, const void *x, int64_t B, int64_t n, int32_t D, int64_t gbase,
-                             uint64_t *keys, int sm_count, cudaStream_t st) {
+                             uint64_t *keys, int sm_count, cudaStream_t st, const SearchDecode *dec) {
     if (B == 0 || n == 0) return cudaSuccess;
     // the widest entry tile that still gives every SM at least two work items
     const int64_t n_qt = (B + kTileQ - 1) / kTileQ;
-    if (n_qt * ((n + 255) / 256) >= 2 * sm_count) return launch_t<256>(q, x, B, n, D, gbase, keys, sm_count, st);
-    if (n_qt * ((n + 127) / 128) >= 2 * sm_count) return launch_t<128>(q, x, B, n, D, gbase, keys, sm_count, st);
-    return launch_t<64>(q, x, B, n, D, gbase, keys, sm_count, st);
+    if (n_qt * ((n + 255) / 256) >= 2 * sm_count) return launch_t<256>(q, x, B, n, D, gbase, keys, sm_count, st, dec);
+    if (n_qt * ((n + 127) / 128) >= 2 * sm_count) return launch_t<128>(q, x, B, n, D, gbase, keys, sm_count, st, dec);
+    return launch_t<64>(q, x, B, n, D, gbase, keys, sm_count, st, dec);
 }
 
 }  // namespace ac
