@@ -444,6 +444,17 @@ attncache_status ac::apply_local_impl(attncache_db *db, const int64_t *idx, cons
     a.O = O;
     a.list = rowlist_view(list, n_rows);
     a.max_rows = n_rows;
+    if (apply_tc_fused_select(a, n_rows) && !getenv("AC_NO_FUSED_SELECT")) {
+        // the A.V kernel selects the rows in its prologue (one launch fewer; the same order-preserving list)
+        a.sel.idx = idx;
+        a.sel.mask = hit;
+        a.sel.n = n_rows;
+        a.sel.shard_begin = d.shard_begin;
+        a.sel.shard_count = d.shard_count;
+        a.sel.err = db->ctx->d_error;
+        AC_CUDA(launch_apply_tc(a, sm_override("AC_APPLY_SMS", db->ctx->compute_sms), st));
+        return ATTNCACHE_OK;
+    }
     AC_CUDA(launch_select_apply(idx, hit, n_rows, d.shard_begin, d.shard_count, a.list, db->ctx->d_error, st));
     if (apply_tc_supported(d.map_dtype, act_dtype, d.seq_len, head_dim)) {
         AC_CUDA(launch_apply_tc(a, sm_override("AC_APPLY_SMS", db->ctx->compute_sms), st));
@@ -540,6 +551,13 @@ attncache_status attncache_attend_full_gqa(attncache_ctx *ctx, int64_t batch, in
     a.O = O;
     a.list = rowlist_view(list, batch);
     a.max_rows = batch;
+    if (attend_tc_fused_select(a, batch) && !getenv("AC_NO_FUSED_SELECT")) {
+        // the attention kernel selects the rows in its prologue (one launch fewer; the same order-preserving list)
+        a.sel.mask = skip;
+        a.sel.n = batch;
+        AC_CUDA(launch_attend_tc(a, sm_override("AC_ATTEND_SMS", ctx->compute_sms), st));
+        return ATTNCACHE_OK;
+    }
     AC_CUDA(launch_select_attend(skip, batch, a.list, st));
     if (attend_tc_supported(act_dtype, S, dd)) {
         AC_CUDA(launch_attend_tc(a, sm_override("AC_ATTEND_SMS", ctx->compute_sms), st));

@@ -17,6 +17,70 @@ struct RowList {
 RowList rowlist_view(void *base, int64_t cap);
 size_t rowlist_bytes(int64_t cap);
 
+// Order-preserving block compaction by every thread of one CTA (blockDim.x a multiple of 32, <= 1024): the select
+// kernels (one CTA of 1024 threads; n up to a few 10^5 rows) and the fused prologues of the A.V / attention kernels
+// (out in shared memory).
+template <typename Pred>
+__device__ void compact_rows(int64_t n, Pred pred, RowList out) {
+    __shared__ int warp_tot[32];
+    __shared__ int base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) base = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < n; b0 += blockDim.x) {
+        int64_t b = b0 + tid;
+        int64_t ent = -1;
+        bool sel = (b < n) && pred(b, ent);
+        unsigned m = __ballot_sync(0xffffffffu, sel);
+        if (lane == 0) warp_tot[warp] = __popc(m);
+        __syncthreads();
+        if (tid == 0) {
+            int run = base;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                int t = warp_tot[w];
+                warp_tot[w] = run;
+                run += t;
+            }
+            base = run;
+        }
+        __syncthreads();
+        if (sel) {
+            int pos = warp_tot[warp] + __popc(m & ((1u << lane) - 1u));
+            out.rows[pos] = (int32_t)b;
+            out.ents[pos] = ent;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *out.count = base;
+}
+
+
+// Row selection done inside a persistent kernel's prologue instead of a select launch (n <= the kernel's shared-memory
+// list capacity): apply: rows with (hit ? hit[b] : idx[b] >= 0) and entry idx[b] - shard_begin in the shard (else
+// *err |= 1, dropped); attend: rows with skip == NULL || skip[b] == 0.  n == 0: the kernel reads its global list.
+struct SelectArgs {
+    const int64_t *idx = nullptr;
+    const uint8_t *mask = nullptr;  // hit (apply) or skip (attend)
+    int64_t n = 0;
+    int64_t shard_begin = 0, shard_count = 0;
+    int *err = nullptr;
+};
+__device__ __forceinline__ bool select_apply_pred(const SelectArgs &s, int64_t b, int64_t &ent) {
+    const bool want = s.mask ? (s.mask[b] != 0) : (s.idx[b] >= 0);
+    if (!want) return false;
+    const int64_t e = s.idx[b] - s.shard_begin;
+    if (e < 0 || e >= s.shard_count) {
+        if (blockIdx.x == 0) atomicOr(s.err, 1);
+        return false;
+    }
+    ent = e;
+    return true;
+}
+__device__ __forceinline__ bool select_attend_pred(const SelectArgs &s, int64_t b, int64_t &ent) {
+    ent = b;
+    return s.mask == nullptr || s.mask[b] == 0;
+}
+
 // Rows with (hit ? hit[b] : idx[b] >= 0); entry = idx[b] - shard_begin must lie in
 // [0, shard_count) else *err |= 1 and the row is dropped.
 cudaError_t launch_select_apply(const int64_t *idx, const uint8_t *hit, int64_t n, int64_t shard_begin,
@@ -56,9 +120,12 @@ struct ApplyArgs {
     void *O;
     RowList list;
     int64_t max_rows;  // host upper bound on list count (n_rows)
+    SelectArgs sel;    // sel.n > 0: the kernel selects the rows itself (apply_tc_fused_select)
 };
 cudaError_t launch_apply_ffma(const ApplyArgs &a, int sm_count, cudaStream_t st);
 bool apply_tc_supported(int32_t map_dt, int32_t act_dt, int32_t S, int32_t d);
+// true when launch_apply_tc can select the rows in its prologue (then no launch_select_apply is needed)
+bool apply_tc_fused_select(const ApplyArgs &a, int64_t n_rows);
 cudaError_t launch_apply_tc(const ApplyArgs &a, int sm_count, cudaStream_t st);
 
 // ---- attend (causal softmax attention) ----
@@ -70,12 +137,14 @@ struct AttendArgs {
     void *O;
     RowList list;
     int64_t max_rows;
+    SelectArgs sel;  // sel.n > 0: the kernel selects the rows itself (attend_tc_fused_select)
 };
 cudaError_t launch_attend_ffma(const AttendArgs &a, int sm_count, cudaStream_t st);
 // The CUDA-core attention / capture / search fallbacks keep one fp32 row of S (or D) values per warp in shared
 // memory (8 warps): 32 * S bytes <= 227 KB.
 constexpr int32_t kSimtMaxLen = 7264;
 bool attend_tc_supported(int32_t dt, int32_t S, int32_t d);
+bool attend_tc_fused_select(const AttendArgs &a, int64_t n_rows);
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st);
 cudaError_t launch_attend_split(const AttendArgs &a, int sm_count, cudaStream_t st);  // d = 128, double-buffered S
 // The four 3-D tensor maps of an attention launch: Q, K, V boxes [128 rows][64 cols], O box [32][64].

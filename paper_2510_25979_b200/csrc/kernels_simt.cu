@@ -25,41 +25,6 @@ RowList rowlist_view(void *base, int64_t cap) {
     return r;
 }
 
-// Order-preserving block compaction (one CTA of 1024 threads; n is at most a few 10^5 rows).
-template <typename Pred>
-__device__ void compact_rows(int64_t n, Pred pred, RowList out) {
-    __shared__ int warp_tot[32];
-    __shared__ int base;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) base = 0;
-    __syncthreads();
-    for (int64_t b0 = 0; b0 < n; b0 += blockDim.x) {
-        int64_t b = b0 + tid;
-        int64_t ent = -1;
-        bool sel = (b < n) && pred(b, ent);
-        unsigned m = __ballot_sync(0xffffffffu, sel);
-        if (lane == 0) warp_tot[warp] = __popc(m);
-        __syncthreads();
-        if (tid == 0) {
-            int run = base;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-                int t = warp_tot[w];
-                warp_tot[w] = run;
-                run += t;
-            }
-            base = run;
-        }
-        __syncthreads();
-        if (sel) {
-            int pos = warp_tot[warp] + __popc(m & ((1u << lane) - 1u));
-            out.rows[pos] = (int32_t)b;
-            out.ents[pos] = ent;
-        }
-        __syncthreads();
-    }
-    if (tid == 0) *out.count = base;
-}
-
 __global__ void select_apply_kernel(const int64_t *idx, const uint8_t *hit, int64_t n, int64_t shard_begin,
                                     int64_t shard_count, RowList out, int *err) {
     compact_rows(n,

@@ -40,7 +40,10 @@ struct Cfg {
     static constexpr int kLag = kStages - 2;  // cp.async groups a loader thread keeps in flight
     static constexpr uint32_t kTmemCols = 2 * kD;
     static constexpr int kOutWarpBytes = 32 * kD * 2;  // epilogue staging: one warp's 32 rows of O
-    static constexpr int kSmem = kStages * kStageBytes + 4 * kOutWarpBytes + 1024 /*align*/ + 256 /*barriers*/;
+    // rows the prologue can select into shared memory (12 B each; 0: the separate select kernel always runs)
+    static constexpr int kSelCap = kD == 64 ? 1024 : 0;
+    static constexpr int kSmem = kStages * kStageBytes + 4 * kOutWarpBytes + 1024 /*align*/ + 256 /*barriers*/ +
+                                 (kSelCap ? 16 + 12 * kSelCap : 0);
 };
 
 // Walks this CTA's units u = blockIdx.x, +gridDim.x, ... of the compacted hit list.  The hit-list
@@ -88,6 +91,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *tfull = empty + C::kStages;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+    // the prologue's row list (sel.n > 0): count | rows[kSelCap] | ents[kSelCap], after the 256 barrier bytes
+    uint8_t *sel_base = (uint8_t *)full + 256;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -106,6 +111,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmO);
     }
     if (warp == 5) tmem_alloc<C::kTmemCols>(tmem_slot);
+    RowList list = a.list;
+    if constexpr (C::kSelCap > 0) {
+        if (a.sel.n > 0) {  // row selection in the prologue (no select launch): every CTA builds the same list
+            list.count = (int32_t *)sel_base;
+            list.rows = (int32_t *)(sel_base + 16);
+            list.ents = (int64_t *)(sel_base + 16 + 4 * C::kSelCap);
+            list.cap = C::kSelCap;
+            compact_rows(a.sel.n, [&](int64_t b, int64_t &ent) { return select_apply_pred(a.sel, b, ent); }, list);
+        }
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -115,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int n_rb = (S + kRows - 1) / kRows;
     const int n_cc = (S + kChunk - 1) / kChunk;  // column chunks holding at least one stored column
     const uint32_t per_row = (uint32_t)(a.n_lay * a.H);
-    const uint32_t units = (uint32_t)(*a.list.count) * per_row;
+    const uint32_t units = (uint32_t)(*list.count) * per_row;
 
     if (warp < 4) {
         // ------------------------------ map loader ------------------------------------------
@@ -137,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const __nv_bfloat16 *maps = (const __nv_bfloat16 *)a.maps;  // 16-bit payload (bf16 or f16)
         const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
         uint32_t cnt = 0, pending = 0;
-        UnitIter<false, true> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
+        UnitIter<false, true> iter(blockIdx.x, gridDim.x, units, per_row, list);
         uint32_t lh;
         int64_t row, ent;
         while (iter.next(lh, row, ent)) {
@@ -193,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------ V loader (TMA) ---------------------------------------
         if (lane == 0) {
             uint32_t cnt = 0;
-            UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
+            UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, list);
             // V is re-read by every row block of the unit (S > 128): keep it in L2 (evict_last) while
             // the maps stream through with evict_first.
 #if defined(APPLY_EXP) && APPLY_EXP == 2  // experiment: V with the normal policy
@@ -267,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool bf16 = a.act_dt == ATTNCACHE_BF16;
         uint8_t *stage_o = sOut + (warp - 6) * C::kOutWarpBytes;
         const uint32_t stage_o_u32 = smem_u32(stage_o);
-        UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
+        UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, list);
         uint32_t lh;
         int64_t row, ent;
         while (iter.next(lh, row, ent)) {
@@ -622,6 +637,17 @@ cudaError_t launch(const ApplyArgs &a, int sm_count, cudaStream_t st) {
 bool apply_tc_supported(int32_t map_dt, int32_t act_dt, int32_t S, int32_t d) {
     return map_dt == act_dt && (map_dt == ATTNCACHE_BF16 || map_dt == ATTNCACHE_F16) && S >= 8 && S % 8 == 0 &&
            (d == 64 || d == 128);
+}
+
+bool apply_tc_fused_select(const ApplyArgs &a, int64_t n_rows) {
+    // the single-row-block kernel (S <= 128) at d = 64 selects up to Cfg<64>::kSelCap rows in its prologue
+#if defined(APPLY_NO_PAIR)
+    const bool single = true;
+#else
+    const bool single = a.S <= kRows;
+#endif
+    return apply_tc_supported(a.map_dt, a.act_dt, a.S, a.d) && a.d == 64 && single && n_rows > 0 &&
+           n_rows <= Cfg<64>::kSelCap;
 }
 
 cudaError_t launch_apply_tc(const ApplyArgs &a, int sm_count, cudaStream_t st) {

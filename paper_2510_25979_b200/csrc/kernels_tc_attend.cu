@@ -42,7 +42,10 @@ struct Cfg {
     static constexpr int kK = 2 * kDepth;             // K: kDepth slots per group
     static constexpr int kV = 2 * kDepth;             // V: kDepth slots per group
     static constexpr int kOutWarp = 32 * 64 * 2;     // per softmax warp: O staging [32 rows][64 cols] (128B swizzle)
-    static constexpr int kSmem = (2 * kQSlots + kK + kV) * kTile + 8 * kOutWarp + 1024 + 512;
+    // rows the prologue can select into shared memory (12 B each; 0: the separate select kernel always runs)
+    static constexpr int kSelCap = kD == 64 ? 1024 : 0;
+    static constexpr int kSmem = (2 * kQSlots + kK + kV) * kTile + 8 * kOutWarp + 1024 + 512 +
+                                 (kSelCap ? 16 + 12 * kSelCap : 0);
     static constexpr uint32_t kTmemCols = 512;        // S/P: 2 x 128 at 0; O: 2 x d at 256
 };
 
@@ -196,6 +199,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmO);
     }
     if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+    RowList list = a.list;
+    if constexpr (C::kSelCap > 0) {
+        if (a.sel.n > 0) {  // row selection in the prologue (no select launch): every CTA builds the same list
+            uint8_t *sel_base = (uint8_t *)bars + 512;  // after the 512 barrier bytes
+            list.count = (int32_t *)sel_base;
+            list.rows = (int32_t *)(sel_base + 16);
+            list.ents = (int64_t *)(sel_base + 16 + 4 * C::kSelCap);
+            list.cap = C::kSelCap;
+            compact_rows(a.sel.n, [&](int64_t b, int64_t &ent) { return select_attend_pred(a.sel, b, ent); }, list);
+        }
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -206,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // padded query rows (never stored: the O store clips at S) see padded keys through the causal mask
     const uint32_t n_qb = (S + kBlk - 1) / kBlk;
     const uint32_t per_row = (uint32_t)(a.L * a.H);
-    const uint32_t units = (uint32_t)(*a.list.count) * per_row;
+    const uint32_t units = (uint32_t)(*list.count) * per_row;
     const uint32_t items = units * n_qb;
     const uint32_t stride = 2 * gridDim.x;
     const uint32_t l2_group = max(1u, (48u << 20) / (2u * S * kD * 2u));  // units whose K and V fit in ~48 MB
@@ -224,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int g = warp >> 1;
         if (lane == 0) {
             Stream st;
-            st.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+            st.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, list.rows, a.H, a.Hkv);
             uint32_t b = 0, it = 0;  // key blocks and items of this stream
             if ((warp & 1) == 0) {
                 // ------------------------------ TMA loader of group g ----------------------------
@@ -320,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t stage_o_u32 = smem_u32(stage_o);
         const float sl2 = a.scale * 1.4426950408889634f;  // scale * log2(e)
         Stream s;
-        s.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, a.list.rows, a.H, a.Hkv);
+        s.init(blockIdx.x + g * gridDim.x, stride, items, units, per_row, n_qb, S, l2_group, list.rows, a.H, a.Hkv);
         uint32_t b = 0;  // key blocks of this stream
         float m_ref = 0.f, l = 0.f;
         while (s.active) {
@@ -550,6 +564,11 @@ cudaError_t make_attend_tmaps(const AttendArgs &a, int d, CUtensorMap *tq, CUten
 
 bool attend_tc_supported(int32_t dt, int32_t S, int32_t d) {
     return (dt == ATTNCACHE_BF16 || dt == ATTNCACHE_F16) && S >= 1 && (d == 64 || d == 128);
+}
+
+bool attend_tc_fused_select(const AttendArgs &a, int64_t n_rows) {
+    // the two-group kernel at d = 64 selects up to Cfg<64>::kSelCap rows in its prologue
+    return attend_tc_supported(a.dt, a.S, a.d) && a.d == 64 && n_rows > 0 && n_rows <= Cfg<64>::kSelCap;
 }
 
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st) {
