@@ -37,6 +37,12 @@ attncache_status cuda_status(cudaError_t e, const char *what) {
     return fail(ATTNCACHE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+// Row selection fused into the layer kernels (one launch fewer) on a local ctx only: a collective ctx runs the
+// next batch's search / placement / relocation on side streams beside its layer kernels, and the select launch
+// between A.V and attention is the window in which those kernels get SMs (world-1 pipelined step: 1.17 ms fused
+// against 1.10-1.15 with the select launches; DESIGN.md §7 K3).  AC_NO_FUSED_SELECT=1 turns it off everywhere.
+bool fused_select_ok(const attncache_ctx *ctx) { return ctx->comm == nullptr && !getenv("AC_NO_FUSED_SELECT"); }
+
 attncache_status scratch(attncache_ctx *ctx, cudaStream_t st, int kind, size_t bytes, void **out, bool *fresh) {
     *out = nullptr;
     if (fresh) *fresh = false;
@@ -444,7 +450,7 @@ attncache_status ac::apply_local_impl(attncache_db *db, const int64_t *idx, cons
     a.O = O;
     a.list = rowlist_view(list, n_rows);
     a.max_rows = n_rows;
-    if (apply_tc_fused_select(a, n_rows) && !getenv("AC_NO_FUSED_SELECT")) {
+    if (apply_tc_fused_select(a, n_rows) && fused_select_ok(db->ctx)) {
         // the A.V kernel selects the rows in its prologue (one launch fewer; the same order-preserving list)
         a.sel.idx = idx;
         a.sel.mask = hit;
@@ -551,7 +557,7 @@ attncache_status attncache_attend_full_gqa(attncache_ctx *ctx, int64_t batch, in
     a.O = O;
     a.list = rowlist_view(list, batch);
     a.max_rows = batch;
-    if (attend_tc_fused_select(a, batch) && !getenv("AC_NO_FUSED_SELECT")) {
+    if (attend_tc_fused_select(a, batch) && fused_select_ok(ctx)) {
         // the attention kernel selects the rows in its prologue (one launch fewer; the same order-preserving list)
         a.sel.mask = skip;
         a.sel.n = batch;

@@ -177,6 +177,7 @@ struct attncache_db {
 namespace ac {
 constexpr int kPinnedInts = 4 * 1024 + 16;  // small int64 staging (host pinned and device): world <= 1024
 // Device scratch of at least `bytes` for (stream, kind); see ScratchKind.
+bool fused_select_ok(const attncache_ctx *ctx);  // row selection inside the layer kernels (local ctx only)
 // fresh (optional): set when the returned buffer is newly allocated (its contents are undefined)
 attncache_status scratch(attncache_ctx *ctx, cudaStream_t st, int kind, size_t bytes, void **out, bool *fresh = nullptr);
 
