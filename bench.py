@@ -306,8 +306,9 @@ def run_ours(args, cfg):
                 "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                 "peak_source": f"{peaks['source']} MEASURED_PEAKS.json hbm_gbs",
                 "algorithmic_bytes_per_launch": bytes_alg, "avg_launch_ms": apply_ms,
-                "note": "launch time measured with CUDA events around the apply_cached call (row-select + A.V "
-                        "kernels) on the launch stream inside the timed region"}
+                "note": "launch time measured with CUDA events around the apply_cached call on the launch stream "
+                        "inside the timed region (one A.V kernel that selects its rows in its prologue; larger "
+                        "batches add a select launch)"}
     attend_alg = (cfg.B - n_hit) * attend_bytes_per_miss(cfg)
     secondary = {
         "search": {"ms": search_ms, "qps": cfg.B / (search_ms * 1e-3),
