@@ -145,6 +145,7 @@ cudaError_t launch_attend_ffma(const AttendArgs &a, int sm_count, cudaStream_t s
 constexpr int32_t kSimtMaxLen = 7264;
 bool attend_tc_supported(int32_t dt, int32_t S, int32_t d);
 bool attend_tc_fused_select(const AttendArgs &a, int64_t n_rows);
+int64_t attend_split_sel_cap();  // rows the d = 128 split kernel selects in its prologue
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st);
 cudaError_t launch_attend_split(const AttendArgs &a, int sm_count, cudaStream_t st);  // d = 128, double-buffered S
 // The four 3-D tensor maps of an attention launch: Q, K, V boxes [128 rows][64 cols], O box [32][64].

@@ -359,7 +359,8 @@ struct PairCfg {
     static constexpr int kLag = kStages - 2;
     static constexpr uint32_t kTmemCols = 4 * kD;                // [pair parity][row block of the pair]
     static constexpr int kOutWarpBytes = 32 * kD * 2;
-    static constexpr int kSmem = kStages * kStageBytes + 4 * kOutWarpBytes + 1024 + 256;
+    static constexpr int kSelCap = kD == 64 ? 512 : 128;  // prologue row list (12 B per row; the ring leaves ~1.7 KB)
+    static constexpr int kSmem = kStages * kStageBytes + 4 * kOutWarpBytes + 1024 + 256 + 16 + 12 * kSelCap;
 };
 
 template <int kD>
@@ -393,6 +394,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmO);
     }
     if (warp == 5) tmem_alloc<C::kTmemCols>(tmem_slot);
+    RowList list = a.list;
+    if (a.sel.n > 0) {  // row selection in the prologue (no select launch): every CTA builds the same list
+        uint8_t *sel_base = (uint8_t *)full + 256;
+        list.count = (int32_t *)sel_base;
+        list.rows = (int32_t *)(sel_base + 16);
+        list.ents = (int64_t *)(sel_base + 16 + 4 * C::kSelCap);
+        list.cap = C::kSelCap;
+        compact_rows(a.sel.n, [&](int64_t b, int64_t &ent) { return select_apply_pred(a.sel, b, ent); }, list);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -403,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int n_pairs = (n_rb + 1) / 2;
     const int n_cc = (S + kChunk - 1) / kChunk;
     const uint32_t per_row = (uint32_t)(a.n_lay * a.H);
-    const uint32_t units = (uint32_t)(*a.list.count) * per_row;
+    const uint32_t units = (uint32_t)(*list.count) * per_row;
     // chunks row block rb needs; a pair's chunk loop runs to its second (larger) row block's count
     auto rb_chunks = [&](int rb) { return a.causal ? min(2 * (rb + 1), n_cc) : n_cc; };
 
@@ -417,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const __nv_bfloat16 *maps = (const __nv_bfloat16 *)a.maps;
         const bool packed = a.map_layout == ATTNCACHE_MAPS_PACKED;
         uint32_t cnt = 0, pending = 0;
-        UnitIter<false, true> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
+        UnitIter<false, true> iter(blockIdx.x, gridDim.x, units, per_row, list);
         uint32_t lh;
         int64_t row, ent;
         while (iter.next(lh, row, ent)) {
@@ -471,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------ V loader (TMA): one V chunk per pair and chunk --------------
         if (lane == 0) {
             uint32_t cnt = 0;
-            UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
+            UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, list);
             const uint64_t v_policy = policy_evict_last();
             // every pair re-reads the V chunks of the pairs before it, so the unit's last pair is the last reader of
             // every chunk: its loads demote the lines (evict_first), or finished units' V would pile up as
@@ -541,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool bf16 = a.act_dt == ATTNCACHE_BF16;
         uint8_t *stage_o = sOut + (warp - 6) * C::kOutWarpBytes;
         const uint32_t stage_o_u32 = smem_u32(stage_o);
-        UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, a.list);
+        UnitIter<true, false> iter(blockIdx.x, gridDim.x, units, per_row, list);
         uint32_t lh;
         int64_t row, ent;
         while (iter.next(lh, row, ent)) {
@@ -640,14 +650,16 @@ bool apply_tc_supported(int32_t map_dt, int32_t act_dt, int32_t S, int32_t d) {
 }
 
 bool apply_tc_fused_select(const ApplyArgs &a, int64_t n_rows) {
-    // the single-row-block kernel (S <= 128) at d = 64 selects up to Cfg<64>::kSelCap rows in its prologue
+    // the single-row-block kernel (S <= 128) at d = 64 and the paired kernel (S > 128) select up to their kSelCap
+    // rows in the prologue
 #if defined(APPLY_NO_PAIR)
     const bool single = true;
 #else
     const bool single = a.S <= kRows;
 #endif
-    return apply_tc_supported(a.map_dt, a.act_dt, a.S, a.d) && a.d == 64 && single && n_rows > 0 &&
-           n_rows <= Cfg<64>::kSelCap;
+    if (!apply_tc_supported(a.map_dt, a.act_dt, a.S, a.d) || n_rows <= 0) return false;
+    if (single) return a.d == 64 && n_rows <= Cfg<64>::kSelCap;
+    return n_rows <= (a.d == 64 ? PairCfg<64>::kSelCap : PairCfg<128>::kSelCap);
 }
 
 cudaError_t launch_apply_tc(const ApplyArgs &a, int sm_count, cudaStream_t st) {

@@ -567,8 +567,12 @@ bool attend_tc_supported(int32_t dt, int32_t S, int32_t d) {
 }
 
 bool attend_tc_fused_select(const AttendArgs &a, int64_t n_rows) {
-    // the two-group kernel at d = 64 selects up to Cfg<64>::kSelCap rows in its prologue
-    return attend_tc_supported(a.dt, a.S, a.d) && a.d == 64 && n_rows > 0 && n_rows <= Cfg<64>::kSelCap;
+    // the two-group kernel (d = 64) and the split kernel (d = 128) select up to their kSelCap rows in the prologue
+    if (!attend_tc_supported(a.dt, a.S, a.d) || n_rows <= 0) return false;
+#if defined(ATT_TWO_GROUP128)
+    if (a.d == 128) return false;
+#endif
+    return n_rows <= (a.d == 64 ? Cfg<64>::kSelCap : attend_split_sel_cap());
 }
 
 cudaError_t launch_attend_tc(const AttendArgs &a, int sm_count, cudaStream_t st) {

@@ -54,8 +54,9 @@ constexpr int kOutWarp = 32 * 64 * 2;   // per softmax warp: O staging [32 rows]
 #endif
 constexpr int kNK = SPLIT_NK, kNV = SPLIT_NV, kNQ = SPLIT_NQ, kStage = SPLIT_STAGE;
 static_assert(kNK >= 1 && kNV >= 1 && kNQ >= 1 && kNK <= 4 && kNV <= 4 && kNQ <= 2, "ring sizes");
-constexpr int kSmem = (kNQ + kNK + kNV) * kTile + 4 * kStage * kOutWarp + 1024 + 256;
-static_assert(kSmem <= 232448, "shared memory");
+constexpr int kSelCap = 128;  // rows the prologue can select into shared memory (12 B each; the rings leave ~1.7 KB)
+constexpr int kSmem = (kNQ + kNK + kNV) * kTile + 4 * kStage * kOutWarp + 1024 + 256 + 16 + 12 * kSelCap;
+static_assert(kSmem + 160 <= 232448, "shared memory (dynamic + compact_rows static words, 132 B)");
 // TMEM columns (of 512): S/P buffers [0, 256), O [256, 384), the pair exchange of partial row maxima
 // (parity-double-buffered, kXmax + 2 * parity + half) and the row sums for the epilogue (item-parity
 // double-buffered, kXsum + 2 * parity + half) at [384, 392): the warps address their own lanes only.
@@ -174,12 +175,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmO);
     }
     if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+    RowList list = a.list;
+    if (a.sel.n > 0) {  // row selection in the prologue (no select launch): every CTA builds the same list
+        uint8_t *sel_base = (uint8_t *)bars + 256;
+        list.count = (int32_t *)sel_base;
+        list.rows = (int32_t *)(sel_base + 16);
+        list.ents = (int64_t *)(sel_base + 16 + 4 * kSelCap);
+        list.cap = kSelCap;
+        compact_rows(a.sel.n, [&](int64_t b, int64_t &ent) { return select_attend_pred(a.sel, b, ent); }, list);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    const uint32_t units = (uint32_t)(*a.list.count) * sc.per_row;
+    const uint32_t units = (uint32_t)(*list.count) * sc.per_row;
     const uint32_t items = units * sc.n_qb;
 
     if (warp < 4) {
@@ -187,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (warp == 0 && lane == 0) {
             // ------------------------------ TMA loader -------------------------------------------
             Walker w;
-            w.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
+            w.init(sc, blockIdx.x, gridDim.x, items, units, list.rows);
             uint32_t b = 0, it = 0;
 #if defined(ATT2_POL)  // experiment (scripts/attend_policy_ab.sh): Q read once -> evict_first; 2: K/V evict_last
             const uint64_t pol_q = policy_evict_first();
@@ -232,8 +242,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // wS runs two blocks ahead of wP: S_0, S_1, then PV_b followed by S_{b+2}.  The first PV of an
             // item restarts O, so it waits until the epilogue has read the previous item's O (o_free).
             Walker wS, wP;
-            wS.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
-            wP.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
+            wS.init(sc, blockIdx.x, gridDim.x, items, units, list.rows);
+            wP.init(sc, blockIdx.x, gridDim.x, items, units, list.rows);
             uint32_t bS = 0, itS = 0, bP = 0, itP = 0;
             auto issue_s = [&]() {
                 const uint32_t buf = bS & 1u, qs = itS % kNQ;
@@ -288,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t o_addr = tmem + lane_addr + kOCol + half * 64;
         const float sl2 = a.scale * 1.4426950408889634f;
         Walker w;
-        w.init(sc, blockIdx.x, gridDim.x, items, units, a.list.rows);
+        w.init(sc, blockIdx.x, gridDim.x, items, units, list.rows);
         uint32_t b = 0, it = 0;
         float m_ref = 0.f, l = 0.f;
         while (w.active) {
@@ -423,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t it = 0;
         for (uint32_t t = blockIdx.x; t < items; t += gridDim.x, ++it) {
             AC_STRESS_DELAY(99u);
-            const ItemSched::Item item = sc.decode(t, units, a.list.rows);
+            const ItemSched::Item item = sc.decode(t, units, list.rows);
             const int32_t orow = item.qb * kBlk + q * 32;  // rows >= S are clipped by the tensor map
             mbar_wait(o_full, it & 1u);
             tc_fence_after();
@@ -508,6 +518,8 @@ cudaError_t launch_t(const AttendArgs &a, int sm_count, cudaStream_t st) {
 }
 
 }  // namespace
+
+int64_t attend_split_sel_cap() { return kSelCap; }
 
 cudaError_t launch_attend_split(const AttendArgs &a, int sm_count, cudaStream_t st) {
     return a.dt == ATTNCACHE_BF16 ? launch_t<true>(a, sm_count, st) : launch_t<false>(a, sm_count, st);
