@@ -698,7 +698,9 @@ def _dist_timed(args, cfg, ac, ctx, db, dev, placement, world, rank, local):
         O = torch.empty_like(V)
         step = ShardedPrefill(ctx, db, cfg.tau, sizes)
         one_step = lambda: step(q, Q, K, V, O)  # noqa: E731
-    for _ in range(args.warmup):
+    # at least 10 untimed steps: with 3 the first timed run of the pipelined step was 5-8 % slower in about half the
+    # runs (its side streams' first allocations and NCCL's lazy setup still settling), with 10 within 1.5 %
+    for _ in range(max(args.warmup, 10)):
         res = one_step()
     torch.cuda.synchronize()
     dist.barrier()
