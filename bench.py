@@ -895,6 +895,7 @@ def run_dist(args, cfg):
                 "config": {"workload": cfg.name, "bj_config_index": cfg.bj_index, "N": cfg.N, "D": cfg.D, "L": cfg.L,
                            "H": cfg.H, "S": cfg.S, "d": cfg.d, "B": c.B, "hits": n_hit, "tau": cfg.tau,
                            "placement": args.placement, "parallelism": par, "l2": "inputs exceed L2 (no flush)",
+                           "warmup_steps_run": max(args.warmup, 10),
                            **extra},
                 "other_scaling": {"scaling": "strong" if args.scaling == "weak" else "weak", "B": oc.B,
                                   "ms_per_step": oms, "value": oc.B * oc.S / (oms * 1e-3), "hits": on_hit},
