@@ -339,7 +339,8 @@ def run_ours(args, cfg):
     line = {"metric": METRIC, "value": cfg.B * cfg.S / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": cfg.act_dtype, "data": "synthetic (synth/, seed 0)",
-            "config": _line_config(cfg, n_hit, parallelism="single GPU", l2="inputs exceed L2 (no flush)"),
+            "config": {**_line_config(cfg, n_hit, parallelism="single GPU", l2="inputs exceed L2 (no flush)"),
+                       "warmup_steps_run": args.warmup + 2},
             "speedup_vs_full_attention": {"batch": full_ms / ms, "per_hit_kernel": full_hits_ms / apply_ms,
                                           "full_attention_ms": full_ms, "paper_context": PAPER_CONTEXT},
             "search_qps": cfg.B / (search_ms * 1e-3),
