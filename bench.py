@@ -339,8 +339,8 @@ def run_ours(args, cfg):
     line = {"metric": METRIC, "value": cfg.B * cfg.S / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": cfg.act_dtype, "data": "synthetic (synth/, seed 0)",
-            "config": {**_line_config(cfg, n_hit, parallelism="single GPU", l2="inputs exceed L2 (no flush)"),
-                       "warmup_steps_run": args.warmup + 2},
+            "config": _line_config(cfg, n_hit, parallelism="single GPU", l2="inputs exceed L2 (no flush)"),
+            "warmup_steps_run": args.warmup + 2,
             "speedup_vs_full_attention": {"batch": full_ms / ms, "per_hit_kernel": full_hits_ms / apply_ms,
                                           "full_attention_ms": full_ms, "paper_context": PAPER_CONTEXT},
             "search_qps": cfg.B / (search_ms * 1e-3),
@@ -896,11 +896,10 @@ def run_dist(args, cfg):
                 "config": {"workload": cfg.name, "bj_config_index": cfg.bj_index, "N": cfg.N, "D": cfg.D, "L": cfg.L,
                            "H": cfg.H, "S": cfg.S, "d": cfg.d, "B": c.B, "hits": n_hit, "tau": cfg.tau,
                            "placement": args.placement, "parallelism": par, "l2": "inputs exceed L2 (no flush)",
-                           "warmup_steps_run": max(args.warmup, 10),
                            **extra},
                 "other_scaling": {"scaling": "strong" if args.scaling == "weak" else "weak", "B": oc.B,
                                   "ms_per_step": oms, "value": oc.B * oc.S / (oms * 1e-3), "hits": on_hit},
-                "gpu_launches": launches, "clocks": clk,
+                "gpu_launches": launches, "clocks": clk, "warmup_steps_run": max(args.warmup, 10),
                 "roofline": roof,
                 "e2e": e2e}
         print(json.dumps(line), flush=True)
